@@ -1,0 +1,188 @@
+/*
+ * rsvd_b200 — C ABI of the B200-native randomized block-Krylov partial SVD.
+ *
+ * Drop-in boundary for the reference package rsvdkit 0.1.0
+ * (/root/reference/pkg/src/rsvdkit). The reference binds one kernel module at
+ * import (backend.py:39-43) with five entry points; each has a counterpart
+ * here, plus the blocked device operations that replace the numpy BLAS-2
+ * column loop of _mgs (factor.py:93-98) and the Rayleigh-Ritz post-process
+ * (rsvd.py:200-221).
+ *
+ * Conventions
+ *   - All matrices are row-major with an explicit leading dimension in
+ *     elements. Device pointers are plain addresses (owned by the caller,
+ *     e.g. torch tensors); `stream` is a cudaStream_t (NULL = legacy stream).
+ *   - Every device entry point is stream-ordered and asynchronous: it only
+ *     enqueues work. Outputs are caller-allocated. Scratch space is an
+ *     explicit caller-provided workspace whose size a *_ws_bytes query gives.
+ *   - dtype codes: RSVD_F32 / RSVD_F64. Small (p x p, w x w) matrices are
+ *     always FP64.
+ *   - Status: RSVD_OK, RSVD_ERR_INVALID (host maps to ValueError),
+ *     RSVD_ERR_CONVERGENCE (ConvergenceError, errors.py:14-23),
+ *     RSVD_ERR_CUDA (RuntimeError). rsvd_last_error() holds the message
+ *     (thread-local).
+ *   - Results are bitwise deterministic for a fixed device model, shape and
+ *     stream: every reduction has a fixed order; no floating-point atomics.
+ */
+#ifndef RSVD_B200_H
+#define RSVD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RSVD_OK 0
+#define RSVD_ERR_INVALID 1
+#define RSVD_ERR_CONVERGENCE 2
+#define RSVD_ERR_CUDA 3
+
+#define RSVD_F32 0
+#define RSVD_F64 1
+
+/* GEMM algorithm selector (rsvd_gemm_nn / rsvd_gemm_tn `algo`). */
+#define RSVD_GEMM_AUTO 0
+#define RSVD_GEMM_SIMT 1       /* CUDA-core FFMA/DFMA, FP32 or FP64 */
+#define RSVD_GEMM_TC_3XTF32 2  /* tcgen05 kind::tf32, hi/lo split, FP32 only */
+#define RSVD_GEMM_DMMA 3       /* mma.sync f64 (DMMA), FP64 only */
+
+const char *rsvd_last_error(void);
+int rsvd_abi_version(void);
+/* Number of SMs of the current device (grid sizing is derived from it). */
+int rsvd_sm_count(void);
+
+/* ---- 1. Gaussian stream (HOST) -----------------------------------------
+ * Replaces gauss_fill (_kernels.pyx:31-53; numpy twin _kernels_py.py:27-45):
+ * SplitMix64 + Box-Muller, bitwise identical to the reference on the same
+ * glibc (compiled with the reference's -ffp-contract=off -fno-builtin-sin
+ * -fno-builtin-cos). Writes `count` doubles, returns the advanced state. The
+ * start block Pi and the QR fill stream are host-supplied (north_star). */
+int rsvd_gauss_fill(int64_t count, uint64_t state, double *out, uint64_t *new_state);
+
+/* ---- 2. Dense products ---------------------------------------------------
+ * Replace mm (_kernels.pyx:56-71) as used by MatrixOperator.apply /
+ * apply_transpose (matrix.py:227-247) and post_process (rsvd.py:212-219).
+ * The reference forms A^T as a cached contiguous copy (matrix.py:245-247);
+ * here A^T products read A in place (rsvd_gemm_tn).
+ *
+ * rsvd_gemm_nn:  C[m x n] = alpha * (A[m x k] - 1 row_sub?) . B[k x n] + beta * C
+ *   `row_sub` (optional, length n, FP64): subtracted as alpha*row_sub[j] from
+ *   every row of the product — the implicit-centering rank-1 correction
+ *   (A - 1 mu^T) B = A B - 1 (mu^T B) with row_sub = mu^T B.
+ * rsvd_gemm_tn:  C[k x n] = alpha * (A^T . B - mu colsum_b^T) + beta * C,
+ *   A is m x k, B is m x n, the reduction runs over the long dimension m in a
+ *   fixed split order with FP64 partials (workspace from rsvd_gemm_tn_ws_bytes).
+ *   `mu` (length k) and `colsum_b` (length n) are optional (both or neither).
+ *   out_dtype may differ from dtype (FP32 inputs, FP64 Gram/projection). */
+int rsvd_gemm_nn(int dtype, int64_t m, int64_t n, int64_t k, double alpha, const void *A,
+                 int64_t lda, const void *B, int64_t ldb, double beta, void *C, int64_t ldc,
+                 const double *row_sub, int algo, void *stream);
+int64_t rsvd_gemm_tn_ws_bytes(int dtype, int64_t m, int64_t n, int64_t k, int algo);
+int rsvd_gemm_tn(int dtype, int out_dtype, int64_t m, int64_t n, int64_t k, double alpha,
+                 const void *A, int64_t lda, const void *B, int64_t ldb, double beta, void *C,
+                 int64_t ldc, const double *mu, const double *colsum_b, void *ws,
+                 int64_t ws_bytes, int algo, void *stream);
+
+/* ---- 3. Sparse products --------------------------------------------------
+ * Replace spmm_nt (_kernels.pyx:74-92) and spmm_t (_kernels.pyx:95-113).
+ * C[nrows x nb] = alpha * A . B + beta * C for CSR A (nrows x ncols).
+ * Index arrays are int32 (idx64 = 0) or int64 (idx64 = 1). spmm_t is this
+ * same entry point applied to the CSR of A^T, built once per operator
+ * (deterministic gather, no atomics) with rsvd_csr_transpose. */
+int rsvd_spmm_csr(int dtype, int idx64, int64_t nrows, int64_t ncols, int64_t nb,
+                  const void *indptr, const void *col, const void *val, const void *B,
+                  int64_t ldb, double alpha, double beta, void *C, int64_t ldc, void *stream);
+/* CSR (nrows x ncols, sorted columns) -> CSR of the transpose, stable in row
+ * order. perm_by_col[e] must be a stable column-sorted permutation of the
+ * nonzeros (supplied by the caller's sort); t_indptr has ncols+1 entries. */
+int rsvd_csr_transpose(int dtype, int idx64, int64_t nrows, int64_t ncols, int64_t nnz,
+                       const void *indptr, const void *col, const void *val,
+                       const int64_t *perm_by_col, void *t_indptr, void *t_col, void *t_val,
+                       void *stream);
+
+/* ---- 4. Block orthonormalization (replaces _mgs, factor.py:79-118) -------
+ * Cholesky of the FP64 Gram G (p x p) of a block, in column order, with
+ * deficiency deflation: column j is declared deficient when its residual
+ * square norm d_j <= tau2 * ref2[j] (ref2 = the column's squared norm
+ * before projection; NULL means ref2[j] = G[j][j]), the analogue of
+ * factor.py:105 (`nv <= _DEFICIENCY_RTOL * ref`). Writes Tinv = R^{-1}
+ * (upper triangular, p x p, zero row+column at deficient slots), mask[j]
+ * (1 = deficient), ndef[0] = number of deficient columns and
+ * ndef[1] = running[0] before this call; running[0] (nullable, device) is
+ * advanced by ndef[0] so successive blocks of one orthonormalization draw
+ * successive fill vectors, as one _mgs call does. `active` (nullable): slots
+ * with active[j] == 0 are treated as absent (zero row/column of Tinv, not
+ * flagged, not counted) — used by the second deflation round, which re-tests
+ * only the columns the first (Gram-resolution) round rejected. */
+int64_t rsvd_chol_deflate_ws_bytes(int64_t p);
+int rsvd_chol_deflate(int64_t p, const double *G, int64_t ldg, const double *ref2, double tau2,
+                      double *Tinv, int64_t ldt, int32_t *mask, int32_t *ndef, int32_t *running,
+                      const int32_t *active, void *ws, int64_t ws_bytes, void *stream);
+/* X[:, j] = 0 where keep[j] == 0. */
+int rsvd_mask_cols(int dtype, int64_t n, int64_t p, void *X, int64_t ldx, const int32_t *keep,
+                   void *stream);
+/* Replacement columns: X[:, j] = fill vector number (ndef[1] + r_j) for every
+ * deficient slot j (r_j = deficient slots before j), rows row_offset ..
+ * row_offset+n-1 of an n_total-long vector (row-sharded A), generated on the device
+ * from the reference's counter-based stream SeededRng(seed) — one vector of n
+ * normals per replaced column from a fresh stream per orthonormalization
+ * (factor.py:40, 89-90, 107; seed 0x5EED_F111_0C0F_FEE5). No-op when
+ * ndef[0] == 0. rsvd_fill_stream writes the first nvec vectors (nvec x n,
+ * FP64) for pinning against the host stream. */
+int rsvd_insert_fill(int dtype, int64_t n, int64_t p, void *X, int64_t ldx, const int32_t *mask,
+                     const int32_t *ndef, uint64_t seed, int64_t row_offset, int64_t n_total,
+                     void *stream);
+int rsvd_fill_stream(int64_t n, int64_t nvec, uint64_t seed, double *out, void *stream);
+
+/* ---- 5. Symmetric eigensolver (replaces jacobi_sweeps, _kernels.pyx:127-192,
+ * and symmetric_eig, factor.py:132-166) -------------------------------------
+ * Parallel (round-robin ordered) two-sided Jacobi, one cooperative
+ * persistent kernel. Same stop rule as the reference: off(M) <= tol*||M||_F
+ * checked after every sweep, rotation skipped when |a_pq| <= tol*||M||_F*1e-3/n,
+ * at most max_sweeps sweeps.
+ * rsvd_jacobi_sweeps mirrors the kernel contract: M (n x n) is overwritten
+ * with its rotated (diagonalised) form, V (pre-initialised by the caller)
+ * accumulates the rotations; info = {converged, sweeps}; off_out[0] = final
+ * off-diagonal mass. */
+int64_t rsvd_jacobi_ws_bytes(int64_t n);
+int rsvd_jacobi_sweeps(int64_t n, double *M, int64_t ldm, double *V, int64_t ldv, double tol,
+                       int max_sweeps, int32_t *info, double *off_out, void *ws, int64_t ws_bytes,
+                       void *stream);
+/* Eigenvalues (diag of the diagonalised M) sorted descending, ties keeping
+ * index order (factor.py:164-165); writes the top k values and the matching
+ * k columns of V (w x k row-major). order_ws: k int32 of scratch. */
+int rsvd_eig_select(int64_t w, const double *Mdiag_src, int64_t ldm, const double *V, int64_t ldv,
+                    int64_t k, double *evals, double *evecs, int64_t lde, int32_t *order_ws,
+                    void *stream);
+
+/* ---- 6. Element-wise / reductions (all deterministic) -------------------- */
+int64_t rsvd_colreduce_ws_bytes(int64_t n, int64_t p);
+/* out[j] = sum_i X[i][j]^2 (square=1) or sum_i X[i][j] (square=0), FP64. */
+int rsvd_colreduce(int dtype, int square, int64_t n, int64_t p, const void *X, int64_t ldx,
+                   double *out, void *ws, int64_t ws_bytes, void *stream);
+/* rsvd.py:192-197: flip column j so its largest-magnitude entry (first on
+ * ties) is positive. */
+int rsvd_canonicalize_signs(int dtype, int64_t n, int64_t k, void *X, int64_t ldx, void *ws,
+                            int64_t ws_bytes, void *stream);
+/* Row-sharded sign canonicalization, step 1: per column the signed value at
+ * the (first) largest-magnitude entry of the local rows and its GLOBAL row
+ * index (local index + row_offset; INT64_MAX when n == 0). Step 2, after the
+ * ranks exchange these: rsvd_flip_by_sign negates column j where
+ * sign_val[j] < 0. */
+int rsvd_col_absargmax(int dtype, int64_t n, int64_t k, const void *X, int64_t ldx,
+                       int64_t row_offset, double *out_val, int64_t *out_idx, void *ws,
+                       int64_t ws_bytes, void *stream);
+int rsvd_flip_by_sign(int dtype, int64_t n, int64_t k, void *X, int64_t ldx,
+                      const double *sign_val, void *stream);
+int rsvd_convert(int src_dtype, int dst_dtype, int64_t rows, int64_t cols, const void *src,
+                 int64_t lds, void *dst, int64_t ldd, void *stream);
+/* out[i] = sqrt(max(in[i], 0)) (rsvd.py:220). */
+int rsvd_sqrt_clip(int64_t k, const double *in, double *out, void *stream);
+/* max |G - I| of a k x k FP64 matrix -> out[0] (rsvd.py:182-185). */
+int rsvd_ortho_error(int64_t k, const double *G, int64_t ldg, double *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSVD_B200_H */

@@ -1,0 +1,46 @@
+"""B200-native randomized block-Krylov / simultaneous-iteration partial SVD.
+
+Drop-in for the hot path of rsvdkit 0.1.0 (Musco & Musco, arXiv 1504.05477):
+the names below keep the reference's signatures and semantics
+(rsvdkit/__init__.py:59-70 for the algorithms, matrix.py for the containers,
+errors.py for the exception types). Compute runs in librsvd_b200.so
+(hand-written sm_100a CUDA behind the C ABI in include/rsvd_b200.h); there is
+no CPU fallback.
+"""
+
+from .errors import ConvergenceError, ParseError
+from .matrix import DenseMatrix, SeededRng, SparseMatrixCSR, as_dense_array, gaussian
+from .rsvd import (
+    PartialSvdResult,
+    RsvdConfig,
+    Variant,
+    block_krylov,
+    derive_q,
+    derive_q_gap,
+    factorize,
+    post_process,
+    simultaneous_iteration,
+    sketch_and_solve,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "ConvergenceError",
+    "ParseError",
+    "DenseMatrix",
+    "SparseMatrixCSR",
+    "SeededRng",
+    "as_dense_array",
+    "gaussian",
+    "PartialSvdResult",
+    "RsvdConfig",
+    "Variant",
+    "block_krylov",
+    "derive_q",
+    "derive_q_gap",
+    "factorize",
+    "post_process",
+    "simultaneous_iteration",
+    "sketch_and_solve",
+]

@@ -1,0 +1,212 @@
+// extern "C" entry points (include/rsvd_b200.h): argument validation and
+// kernel dispatch. No entry point synchronises the stream.
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace rsvd {
+// small_dense.cu
+int64_t chol_deflate_ws_bytes(int64_t p);
+int chol_deflate(int64_t p, const double* G, int64_t ldg, const double* ref2, double tau2,
+                 double* T, int64_t ldt, int32_t* mask, int32_t* ndef, int32_t* running,
+                 const int32_t* active, void* ws, int64_t ws_bytes, cudaStream_t st);
+int mask_cols(int dtype, int64_t n, int64_t p, void* X, int64_t ldx, const int32_t* keep,
+              cudaStream_t st);
+int64_t jacobi_ws_bytes(int64_t n);
+int jacobi_sweeps(int64_t n, double* M, int64_t ldm, double* V, int64_t ldv, double tol,
+                  int max_sweeps, int32_t* info, double* off_out, void* ws, int64_t ws_bytes,
+                  cudaStream_t st);
+int eig_select(int64_t w, const double* M, int64_t ldm, const double* V, int64_t ldv, int64_t k,
+               double* evals, double* evecs, int64_t lde, void* order_ws, cudaStream_t st);
+// elementwise.cu
+int64_t colreduce_ws_bytes(int64_t n, int64_t p);
+int colreduce(int dtype, int square, int64_t n, int64_t p, const void* X, int64_t ldx,
+              double* out, void* ws, int64_t ws_bytes, cudaStream_t st);
+int canonicalize_signs(int dtype, int64_t n, int64_t k, void* X, int64_t ldx, void* ws,
+                       int64_t ws_bytes, cudaStream_t st);
+int convert(int sd, int dd, int64_t rows, int64_t cols, const void* src, int64_t lds, void* dst,
+            int64_t ldd, cudaStream_t st);
+int sqrt_clip(int64_t k, const double* in, double* out, cudaStream_t st);
+int col_absargmax(int dtype, int64_t n, int64_t k, const void* X, int64_t ldx, int64_t row_offset,
+                  double* out_val, int64_t* out_idx, void* ws, int64_t ws_bytes, cudaStream_t st);
+int flip_by_sign(int dtype, int64_t n, int64_t k, void* X, int64_t ldx, const double* sign_val,
+                 cudaStream_t st);
+int ortho_error(int64_t k, const double* G, int64_t ldg, double* out, cudaStream_t st);
+int insert_fill(int dtype, int64_t n, int64_t p, void* X, int64_t ldx, const int32_t* mask,
+                const int32_t* ndef, uint64_t seed, int64_t row_offset, int64_t n_total,
+                cudaStream_t st);
+int fill_stream(int64_t n, int64_t nvec, uint64_t seed, double* out, cudaStream_t st);
+// sparse.cu
+int spmm_csr(int dtype, int idx64, int64_t nrows, int64_t ncols, int64_t nb, const void* indptr,
+             const void* col, const void* val, const void* B, int64_t ldb, double alpha,
+             double beta, void* C, int64_t ldc, cudaStream_t st);
+int csr_transpose(int dtype, int idx64, int64_t nrows, int64_t ncols, int64_t nnz,
+                  const void* indptr, const void* col, const void* val, const int64_t* perm,
+                  void* tptr, void* tcol, void* tval, cudaStream_t st);
+}  // namespace rsvd
+
+using namespace rsvd;
+
+static bool valid_dtype(int d) { return d == RSVD_F32 || d == RSVD_F64; }
+
+extern "C" {
+
+int rsvd_gemm_nn(int dtype, int64_t m, int64_t n, int64_t k, double alpha, const void* A,
+                 int64_t lda, const void* B, int64_t ldb, double beta, void* C, int64_t ldc,
+                 const double* row_sub, int algo, void* stream) {
+    RSVD_REQUIRE(valid_dtype(dtype), "gemm_nn: bad dtype %d", dtype);
+    RSVD_REQUIRE(m >= 0 && n >= 0 && k >= 0, "gemm_nn: negative dimension");
+    RSVD_REQUIRE(lda >= k && ldb >= n && ldc >= n, "gemm_nn: leading dimension too small");
+    cudaStream_t st = as_stream(stream);
+    if (algo == RSVD_GEMM_TC_3XTF32 || (algo == RSVD_GEMM_AUTO && dtype == RSVD_F32 &&
+                                         gemm_tc_nn_supported(m, n, k, lda, ldb, ldc, A, B))) {
+        RSVD_REQUIRE(dtype == RSVD_F32, "gemm_nn: 3xTF32 path is FP32 only");
+        RSVD_REQUIRE(gemm_tc_nn_supported(m, n, k, lda, ldb, ldc, A, B),
+                     "gemm_nn: shape/alignment not supported by the tcgen05 kernel");
+        return gemm_nn_tc(m, n, k, alpha, (const float*)A, lda, (const float*)B, ldb, beta,
+                          (float*)C, ldc, row_sub, st);
+    }
+    return gemm_nn_simt(dtype, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, row_sub, st);
+}
+
+int64_t rsvd_gemm_tn_ws_bytes(int dtype, int64_t m, int64_t n, int64_t k, int algo) {
+    int64_t a = gemm_tn_simt_ws_bytes(m, n, k);
+    if (dtype == RSVD_F32 && algo != RSVD_GEMM_SIMT) {
+        int64_t b = gemm_tn_tc_ws_bytes(m, n, k);
+        if (b > a) a = b;
+    }
+    return a + 256;
+}
+
+int rsvd_gemm_tn(int dtype, int out_dtype, int64_t m, int64_t n, int64_t k, double alpha,
+                 const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C,
+                 int64_t ldc, const double* mu, const double* colsum_b, void* ws,
+                 int64_t ws_bytes, int algo, void* stream) {
+    RSVD_REQUIRE(valid_dtype(dtype) && valid_dtype(out_dtype), "gemm_tn: bad dtype");
+    RSVD_REQUIRE(m >= 0 && n >= 0 && k >= 0, "gemm_tn: negative dimension");
+    RSVD_REQUIRE(lda >= k && ldb >= n && ldc >= n, "gemm_tn: leading dimension too small");
+    RSVD_REQUIRE((mu == nullptr) == (colsum_b == nullptr), "gemm_tn: mu and colsum_b go together");
+    cudaStream_t st = as_stream(stream);
+    if (algo == RSVD_GEMM_TC_3XTF32 ||
+        (algo == RSVD_GEMM_AUTO && dtype == RSVD_F32 && gemm_tc_tn_supported(m, n, k, lda, ldb, A, B))) {
+        RSVD_REQUIRE(dtype == RSVD_F32, "gemm_tn: 3xTF32 path is FP32 only");
+        RSVD_REQUIRE(gemm_tc_tn_supported(m, n, k, lda, ldb, A, B),
+                     "gemm_tn: shape/alignment not supported by the tcgen05 kernel");
+        return gemm_tn_tc(out_dtype, m, n, k, alpha, (const float*)A, lda, (const float*)B, ldb,
+                          beta, C, ldc, mu, colsum_b, ws, ws_bytes, st);
+    }
+    return gemm_tn_simt(dtype, out_dtype, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, mu,
+                        colsum_b, ws, ws_bytes, st);
+}
+
+int rsvd_spmm_csr(int dtype, int idx64, int64_t nrows, int64_t ncols, int64_t nb,
+                  const void* indptr, const void* col, const void* val, const void* B,
+                  int64_t ldb, double alpha, double beta, void* C, int64_t ldc, void* stream) {
+    RSVD_REQUIRE(valid_dtype(dtype), "spmm: bad dtype");
+    RSVD_REQUIRE(nrows >= 0 && ncols >= 0 && nb >= 0 && ldb >= nb && ldc >= nb, "spmm: bad shape");
+    return spmm_csr(dtype, idx64, nrows, ncols, nb, indptr, col, val, B, ldb, alpha, beta, C, ldc,
+                    as_stream(stream));
+}
+
+int rsvd_csr_transpose(int dtype, int idx64, int64_t nrows, int64_t ncols, int64_t nnz,
+                       const void* indptr, const void* col, const void* val,
+                       const int64_t* perm_by_col, void* t_indptr, void* t_col, void* t_val,
+                       void* stream) {
+    RSVD_REQUIRE(valid_dtype(dtype), "csr_transpose: bad dtype");
+    RSVD_REQUIRE(nrows >= 0 && ncols >= 0 && nnz >= 0, "csr_transpose: bad shape");
+    return csr_transpose(dtype, idx64, nrows, ncols, nnz, indptr, col, val, perm_by_col, t_indptr,
+                         t_col, t_val, as_stream(stream));
+}
+
+int64_t rsvd_chol_deflate_ws_bytes(int64_t p) { return chol_deflate_ws_bytes(p); }
+
+int rsvd_chol_deflate(int64_t p, const double* G, int64_t ldg, const double* ref2, double tau2,
+                      double* Tinv, int64_t ldt, int32_t* mask, int32_t* ndef, int32_t* running,
+                      const int32_t* active, void* ws, int64_t ws_bytes, void* stream) {
+    RSVD_REQUIRE(p >= 0 && ldg >= p && ldt >= p, "chol_deflate: bad shape");
+    return chol_deflate(p, G, ldg, ref2, tau2, Tinv, ldt, mask, ndef, running, active, ws, ws_bytes,
+                        as_stream(stream));
+}
+
+int rsvd_mask_cols(int dtype, int64_t n, int64_t p, void* X, int64_t ldx, const int32_t* keep,
+                   void* stream) {
+    RSVD_REQUIRE(valid_dtype(dtype) && ldx >= p, "mask_cols: bad args");
+    return mask_cols(dtype, n, p, X, ldx, keep, as_stream(stream));
+}
+
+int rsvd_insert_fill(int dtype, int64_t n, int64_t p, void* X, int64_t ldx, const int32_t* mask,
+                     const int32_t* ndef, uint64_t seed, int64_t row_offset, int64_t n_total,
+                     void* stream) {
+    RSVD_REQUIRE(valid_dtype(dtype) && ldx >= p, "insert_fill: bad args");
+    RSVD_REQUIRE(row_offset >= 0 && n_total >= row_offset + n, "insert_fill: bad row range");
+    return insert_fill(dtype, n, p, X, ldx, mask, ndef, seed, row_offset, n_total,
+                       as_stream(stream));
+}
+
+int rsvd_fill_stream(int64_t n, int64_t nvec, uint64_t seed, double* out, void* stream) {
+    RSVD_REQUIRE(n >= 0 && nvec >= 0, "fill_stream: bad shape");
+    return fill_stream(n, nvec, seed, out, as_stream(stream));
+}
+
+int64_t rsvd_jacobi_ws_bytes(int64_t n) { return jacobi_ws_bytes(n); }
+
+int rsvd_jacobi_sweeps(int64_t n, double* M, int64_t ldm, double* V, int64_t ldv, double tol,
+                       int max_sweeps, int32_t* info, double* off_out, void* ws, int64_t ws_bytes,
+                       void* stream) {
+    RSVD_REQUIRE(n >= 1 && ldm >= n && ldv >= n, "jacobi: bad shape");
+    RSVD_REQUIRE(tol >= 0.0 && max_sweeps >= 0, "jacobi: bad tol/max_sweeps");
+    return jacobi_sweeps(n, M, ldm, V, ldv, tol, max_sweeps, info, off_out, ws, ws_bytes,
+                         as_stream(stream));
+}
+
+int rsvd_eig_select(int64_t w, const double* M, int64_t ldm, const double* V, int64_t ldv,
+                    int64_t k, double* evals, double* evecs, int64_t lde, int32_t* order_ws,
+                    void* stream) {
+    RSVD_REQUIRE(w >= 1 && k >= 0 && k <= w && lde >= k, "eig_select: bad shape");
+    return eig_select(w, M, ldm, V, ldv, k, evals, evecs, lde, order_ws, as_stream(stream));
+}
+
+int64_t rsvd_colreduce_ws_bytes(int64_t n, int64_t p) { return colreduce_ws_bytes(n, p); }
+
+int rsvd_colreduce(int dtype, int square, int64_t n, int64_t p, const void* X, int64_t ldx,
+                   double* out, void* ws, int64_t ws_bytes, void* stream) {
+    RSVD_REQUIRE(valid_dtype(dtype) && ldx >= p, "colreduce: bad args");
+    return colreduce(dtype, square, n, p, X, ldx, out, ws, ws_bytes, as_stream(stream));
+}
+
+int rsvd_canonicalize_signs(int dtype, int64_t n, int64_t k, void* X, int64_t ldx, void* ws,
+                            int64_t ws_bytes, void* stream) {
+    RSVD_REQUIRE(valid_dtype(dtype) && ldx >= k, "canonicalize_signs: bad args");
+    return canonicalize_signs(dtype, n, k, X, ldx, ws, ws_bytes, as_stream(stream));
+}
+
+int rsvd_col_absargmax(int dtype, int64_t n, int64_t k, const void* X, int64_t ldx,
+                       int64_t row_offset, double* out_val, int64_t* out_idx, void* ws,
+                       int64_t ws_bytes, void* stream) {
+    RSVD_REQUIRE(valid_dtype(dtype) && ldx >= k, "col_absargmax: bad args");
+    return col_absargmax(dtype, n, k, X, ldx, row_offset, out_val, out_idx, ws, ws_bytes,
+                         as_stream(stream));
+}
+
+int rsvd_flip_by_sign(int dtype, int64_t n, int64_t k, void* X, int64_t ldx,
+                      const double* sign_val, void* stream) {
+    RSVD_REQUIRE(valid_dtype(dtype) && ldx >= k, "flip_by_sign: bad args");
+    return flip_by_sign(dtype, n, k, X, ldx, sign_val, as_stream(stream));
+}
+
+int rsvd_convert(int src_dtype, int dst_dtype, int64_t rows, int64_t cols, const void* src,
+                 int64_t lds, void* dst, int64_t ldd, void* stream) {
+    RSVD_REQUIRE(valid_dtype(src_dtype) && valid_dtype(dst_dtype), "convert: bad dtype");
+    RSVD_REQUIRE(lds >= cols && ldd >= cols, "convert: bad leading dimension");
+    return convert(src_dtype, dst_dtype, rows, cols, src, lds, dst, ldd, as_stream(stream));
+}
+
+int rsvd_sqrt_clip(int64_t k, const double* in, double* out, void* stream) {
+    return sqrt_clip(k, in, out, as_stream(stream));
+}
+
+int rsvd_ortho_error(int64_t k, const double* G, int64_t ldg, double* out, void* stream) {
+    RSVD_REQUIRE(k >= 0 && ldg >= k, "ortho_error: bad shape");
+    return ortho_error(k, G, ldg, out, as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,431 @@
+// Small dense FP64 kernels of the orthonormalization and the Rayleigh-Ritz
+// eigensolve.
+//
+//  * chol_deflate: column-ordered Cholesky of a block Gram with deficiency
+//    deflation + the inverse triangular factor. Together with two GEMMs this
+//    is the blocked replacement of the per-column CGS2 loop of _mgs
+//    (factor.py:79-118): same column order, same "residual small relative to
+//    the original column norm" test (factor.py:105), same fill stream for the
+//    replaced columns (factor.py:89-90, 107).
+//  * jacobi: two-sided Jacobi with the reference's stop and skip rules
+//    (_kernels.pyx:127-192) in round-robin ("circle method") parallel order,
+//    as ONE cooperative persistent kernel: per round every CTA recomputes the
+//    W2/2 rotations of the round from the diagonal/pair entries, applies
+//    M' = J^T M J blockwise (2x2 blocks are independent) and V' = V J, and
+//    writes the result in the NEXT round's slot order (ping-pong buffers), so
+//    every round's pairs are adjacent (2i, 2i+1) and loads stay coalesced.
+//    After a whole sweep (W2-1 rounds) the slot order is the identity again.
+//  * eig_select: descending stable sort of the eigenvalues (factor.py:164-165)
+//    and gather of the top-k eigenvectors.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace rsvd {
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// chol_deflate
+__device__ __forceinline__ int64_t tri_off(int64_t p, int64_t i, int64_t j) {
+    // packed upper triangle, row-major, i <= j
+    return i * p - (i * (i - 1)) / 2 + (j - i);
+}
+
+constexpr int kCholThreads = 1024;
+
+__global__ void __launch_bounds__(kCholThreads)
+k_chol_deflate(int64_t p, const double* __restrict__ G, int64_t ldg,
+               const double* __restrict__ ref2, double tau2, double* __restrict__ T, int64_t ldt,
+               int32_t* __restrict__ mask, int32_t* __restrict__ ndef, int32_t* __restrict__ running,
+               const int32_t* __restrict__ active, double* gws, int use_smem) {
+    extern __shared__ double smem_d[];
+    double* S = use_smem ? smem_d : gws;
+    __shared__ int s_def;
+    __shared__ int s_count;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    for (int64_t i = warp; i < p; i += nwarps)
+        for (int64_t j = i + lane; j < p; j += 32) S[tri_off(p, i, j)] = G[i * ldg + j];
+    if (tid == 0) s_count = 0;
+    __syncthreads();
+    for (int64_t j = 0; j < p; ++j) {
+        if (tid == 0) {
+            double d = S[tri_off(p, j, j)];
+            double r = ref2 ? ref2[j] : G[j * ldg + j];
+            const int act = active ? active[j] : 1;
+            int def = !act || !(d > tau2 * r) || !(d > 0.0);
+            s_def = def;
+            mask[j] = def ? (act ? 1 : 2) : 0;  // 2 = inactive slot (not counted)
+            if (def && act) ++s_count;
+        }
+        __syncthreads();
+        const int def = s_def;
+        if (!def) {
+            const double rjj = sqrt(S[tri_off(p, j, j)]);
+            const double inv = 1.0 / rjj;
+            for (int64_t c = j + 1 + tid; c < p; c += blockDim.x) S[tri_off(p, j, c)] *= inv;
+            __syncthreads();
+            if (tid == 0) S[tri_off(p, j, j)] = rjj;
+            // trailing update, warp per row
+            for (int64_t a = j + 1 + warp; a < p; a += nwarps) {
+                const double ra = S[tri_off(p, j, a)];
+                for (int64_t b = a + lane; b < p; b += 32) S[tri_off(p, a, b)] -= ra * S[tri_off(p, j, b)];
+            }
+        } else {
+            for (int64_t c = j + 1 + tid; c < p; c += blockDim.x) S[tri_off(p, j, c)] = 0.0;
+            __syncthreads();
+            if (tid == 0) S[tri_off(p, j, j)] = 1.0;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const int32_t base = running ? running[0] : 0;
+        ndef[0] = s_count;
+        ndef[1] = base;
+        if (running) running[0] = base + s_count;
+    }
+    // Inverse by columns: T(:, c) solves R x = e_c (back substitution), one warp
+    // per column, lanes split the dot products.
+    for (int64_t c = warp; c < p; c += nwarps) {
+        double* Tc = T;  // column c of T, row stride ldt
+        for (int64_t a = c + 1 + lane; a < p; a += 32) Tc[a * ldt + c] = 0.0;
+        const double xc = 1.0 / S[tri_off(p, c, c)];
+        if (lane == 0) Tc[c * ldt + c] = xc;
+        __syncwarp();
+        for (int64_t a = c - 1; a >= 0; --a) {
+            double acc = 0.0;
+            for (int64_t b = a + 1 + lane; b <= c; b += 32) acc += S[tri_off(p, a, b)] * Tc[b * ldt + c];
+            acc = warp_sum(acc);
+            if (lane == 0) Tc[a * ldt + c] = -acc / S[tri_off(p, a, a)];
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    // zero row+column of deficient / inactive slots (rows already e_j)
+    for (int64_t j = warp; j < p; j += nwarps) {
+        if (!mask[j]) continue;
+        for (int64_t a = lane; a < p; a += 32) {
+            T[a * ldt + j] = 0.0;
+            T[j * ldt + a] = 0.0;
+        }
+    }
+    __syncthreads();
+    for (int64_t j = tid; j < p; j += blockDim.x)
+        if (mask[j] == 2) mask[j] = 0;
+}
+
+// ---------------------------------------------------------------------------
+// Jacobi
+constexpr int kJacThreads = 512;
+
+struct JacobiState {
+    int64_t n, W2;
+    double* Mb[2];
+    double* Vb[2];
+    int64_t nv;  // rows of V
+    double* partial;
+    unsigned int* bar;
+    double tol;
+    int max_sweeps;
+    int32_t* info;
+    double* off_out;
+};
+
+__device__ __forceinline__ int64_t next_slot(int64_t s, int64_t W2) {
+    if (W2 <= 2 || s == 0) return s;
+    if ((s & 1) == 0) return (s == W2 - 2) ? W2 - 1 : s + 2;
+    return (s == 1) ? 2 : s - 2;
+}
+
+// Deterministic grid-wide sum: fixed per-thread stride order, fixed block tree,
+// fixed order over blocks. Every CTA returns the same value.
+__device__ double grid_sum(double v, double* partial, unsigned int* bar) {
+    __shared__ double red[kJacThreads / 32];
+    __shared__ double total;
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+        partial[blockIdx.x] = s;
+    }
+    grid_barrier(bar, gridDim.x);
+    if (threadIdx.x == 0) {
+        volatile double* pv = partial;
+        double s = 0.0;
+        for (unsigned i = 0; i < gridDim.x; ++i) s += pv[i];
+        total = s;
+    }
+    __syncthreads();
+    double r = total;
+    grid_barrier(bar, gridDim.x);  // partial[] reusable afterwards
+    return r;
+}
+
+__global__ void __launch_bounds__(kJacThreads)
+k_jacobi(JacobiState st) {
+    extern __shared__ double sh[];
+    const int64_t W2 = st.W2, n = st.n, half = W2 / 2;
+    double* rc = sh;             // c per pair
+    double* rs = sh + half;      // s per pair
+    double* rt = sh + 2 * half;  // t per pair
+    double* ra = sh + 3 * half;  // apq per pair
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+
+    int cur = 0;
+    // initial Frobenius norm and off-diagonal mass (reference order: fro, off)
+    double fro2 = 0.0, off2 = 0.0;
+    {
+        const double* M = st.Mb[0];
+        for (int64_t e = gtid; e < W2 * W2; e += gstride) {
+            double x = M[e];
+            fro2 += x * x;
+            if (e / W2 != e % W2) off2 += x * x;
+        }
+    }
+    const double fro = sqrt(grid_sum(fro2, st.partial, st.bar));
+    double off = sqrt(grid_sum(off2, st.partial, st.bar));
+    const double threshold = st.tol * fro;
+    int sweeps = 0;
+    bool converged = (n < 2) || (off <= threshold);
+    const double skip = threshold * 1e-3 / (double)n;
+    while (!converged && sweeps < st.max_sweeps) {
+        for (int64_t round = 0; round < W2 - 1; ++round) {
+            const double* M = st.Mb[cur];
+            double* Mn = st.Mb[cur ^ 1];
+            const double* V = st.Vb[cur];
+            double* Vn = st.Vb[cur ^ 1];
+            for (int64_t pr = threadIdx.x; pr < half; pr += blockDim.x) {
+                const int64_t sp = 2 * pr, sq = 2 * pr + 1;
+                const double apq = M[sp * W2 + sq];
+                double c = 1.0, s = 0.0, t = 0.0;
+                if (!(fabs(apq) <= skip)) {
+                    const double app = M[sp * W2 + sp], aqq = M[sq * W2 + sq];
+                    const double tau = (aqq - app) / (2.0 * apq);
+                    t = tau >= 0.0 ? 1.0 / (tau + sqrt(1.0 + tau * tau))
+                                   : -1.0 / (-tau + sqrt(1.0 + tau * tau));
+                    c = 1.0 / sqrt(1.0 + t * t);
+                    s = t * c;
+                }
+                rc[pr] = c;
+                rs[pr] = s;
+                rt[pr] = t;
+                ra[pr] = apq;
+            }
+            __syncthreads();
+            // M' = J^T M J over 2x2 blocks (P, Q); write in the next slot order.
+            for (int64_t e = gtid; e < half * half; e += gstride) {
+                const int64_t P = e / half, Q = e % half;
+                const int64_t r0 = 2 * P, c0 = 2 * Q;
+                const double2 top = *reinterpret_cast<const double2*>(M + r0 * W2 + c0);
+                const double2 bot = *reinterpret_cast<const double2*>(M + (r0 + 1) * W2 + c0);
+                double o00, o01, o10, o11;
+                if (P == Q) {
+                    if (!(fabs(ra[P]) <= skip)) {
+                        const double tt = rt[P], apq = ra[P];
+                        o00 = top.x - tt * apq;
+                        o11 = bot.y + tt * apq;
+                        o01 = 0.0;
+                        o10 = 0.0;
+                    } else {
+                        o00 = top.x; o01 = top.y; o10 = bot.x; o11 = bot.y;
+                    }
+                } else {
+                    const double cq = rc[Q], sq = rs[Q], cp = rc[P], spp = rs[P];
+                    // column rotation (right multiply by J_Q)
+                    const double a0 = cq * top.x - sq * top.y, a1 = sq * top.x + cq * top.y;
+                    const double b0 = cq * bot.x - sq * bot.y, b1 = sq * bot.x + cq * bot.y;
+                    // row rotation (left multiply by J_P^T)
+                    o00 = cp * a0 - spp * b0;
+                    o01 = cp * a1 - spp * b1;
+                    o10 = spp * a0 + cp * b0;
+                    o11 = spp * a1 + cp * b1;
+                }
+                const int64_t nr0 = next_slot(r0, W2), nr1 = next_slot(r0 + 1, W2);
+                const int64_t nc0 = next_slot(c0, W2), nc1 = next_slot(c0 + 1, W2);
+                Mn[nr0 * W2 + nc0] = o00;
+                Mn[nr0 * W2 + nc1] = o01;
+                Mn[nr1 * W2 + nc0] = o10;
+                Mn[nr1 * W2 + nc1] = o11;
+            }
+            // V' = V J (columns in slot order)
+            for (int64_t e = gtid; e < st.nv * half; e += gstride) {
+                const int64_t i = e / half, Q = e % half;
+                const double2 x = *reinterpret_cast<const double2*>(V + i * W2 + 2 * Q);
+                const double c = rc[Q], s = rs[Q];
+                Vn[i * W2 + next_slot(2 * Q, W2)] = c * x.x - s * x.y;
+                Vn[i * W2 + next_slot(2 * Q + 1, W2)] = s * x.x + c * x.y;
+            }
+            cur ^= 1;
+            grid_barrier(st.bar, gridDim.x);
+        }
+        ++sweeps;
+        double o2 = 0.0;
+        const double* M = st.Mb[cur];
+        for (int64_t e = gtid; e < W2 * W2; e += gstride) {
+            if (e / W2 != e % W2) {
+                double x = M[e];
+                o2 += x * x;
+            }
+        }
+        off = sqrt(grid_sum(o2, st.partial, st.bar));
+        converged = off <= threshold;
+    }
+    if (gtid == 0) {
+        st.info[0] = converged ? 1 : 0;
+        st.info[1] = sweeps;
+        st.info[2] = cur;
+        st.off_out[0] = off;
+    }
+}
+
+__global__ void k_pad_copy(int64_t n, int64_t W2, const double* __restrict__ src, int64_t lds,
+                           double* __restrict__ dst, int64_t rows) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= rows * W2) return;
+    int64_t i = e / W2, j = e % W2;
+    dst[e] = (i < n && j < n) ? src[i * lds + j] : 0.0;
+}
+
+// Copy back from whichever ping-pong buffer holds the result (info[2]).
+__global__ void k_unpad_copy(int64_t n, int64_t W2, const double* b0, const double* b1,
+                             const int32_t* info, double* __restrict__ dst, int64_t ldd,
+                             int64_t rows) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= rows * n) return;
+    int64_t i = e / n, j = e % n;
+    const double* src = info[2] ? b1 : b0;
+    dst[i * ldd + j] = src[i * W2 + j];
+}
+
+// ---------------------------------------------------------------------------
+// eig_select
+__global__ void k_eig_order(int64_t w, const double* __restrict__ M, int64_t ldm, int64_t k,
+                            int32_t* __restrict__ order, double* __restrict__ evals) {
+    for (int64_t i = threadIdx.x; i < w; i += blockDim.x) {
+        const double di = M[i * ldm + i];
+        int64_t rank = 0;
+        for (int64_t j = 0; j < w; ++j) {
+            const double dj = M[j * ldm + j];
+            rank += (dj > di) || (dj == di && j < i);
+        }
+        if (rank < k) {
+            order[rank] = (int32_t)i;
+            evals[rank] = di;
+        }
+    }
+}
+
+__global__ void k_eig_gather(int64_t w, int64_t k, const int32_t* __restrict__ order,
+                             const double* __restrict__ V, int64_t ldv, double* __restrict__ E,
+                             int64_t lde) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= w * k) return;
+    int64_t i = e / k, r = e % k;
+    E[i * lde + r] = V[i * ldv + order[r]];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// public wrappers (called from api.cu)
+
+int64_t chol_deflate_ws_bytes(int64_t p) { return (p * (p + 1) / 2) * (int64_t)sizeof(double); }
+
+int chol_deflate(int64_t p, const double* G, int64_t ldg, const double* ref2, double tau2,
+                 double* T, int64_t ldt, int32_t* mask, int32_t* ndef, int32_t* running,
+                 const int32_t* active, void* ws, int64_t ws_bytes, cudaStream_t st) {
+    if (p == 0) return RSVD_OK;
+    int64_t bytes = chol_deflate_ws_bytes(p);
+    int use_smem = bytes <= 200 * 1024;
+    if (!use_smem) RSVD_REQUIRE(ws && ws_bytes >= bytes, "chol_deflate: workspace too small");
+    size_t sm = use_smem ? (size_t)bytes : 0;
+    if (sm > 48 * 1024)
+        RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_chol_deflate, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sm));
+    k_chol_deflate<<<1, kCholThreads, sm, st>>>(p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running,
+                                                active, (double*)ws, use_smem);
+    RSVD_CHECK_LAUNCH();
+    return RSVD_OK;
+}
+
+static int64_t jac_W2(int64_t n) { return n + (n & 1); }
+
+int64_t jacobi_ws_bytes(int64_t n) {
+    int64_t W2 = jac_W2(n);
+    int64_t b = 2 * W2 * W2 + 2 * n * W2 + 1024;  // doubles
+    return b * (int64_t)sizeof(double) + 64;
+}
+
+int jacobi_sweeps(int64_t n, double* M, int64_t ldm, double* V, int64_t ldv, double tol,
+                  int max_sweeps, int32_t* info, double* off_out, void* ws, int64_t ws_bytes,
+                  cudaStream_t st) {
+    RSVD_REQUIRE(n >= 1, "jacobi: n must be >= 1");
+    RSVD_REQUIRE(ws_bytes >= jacobi_ws_bytes(n), "jacobi: workspace too small");
+    const int64_t W2 = jac_W2(n);
+    double* base = (double*)ws;
+    JacobiState s;
+    s.n = n;
+    s.W2 = W2;
+    s.Mb[0] = base;
+    s.Mb[1] = base + W2 * W2;
+    s.Vb[0] = base + 2 * W2 * W2;
+    s.Vb[1] = s.Vb[0] + n * W2;
+    s.nv = n;
+    s.partial = s.Vb[1] + n * W2;                // 1024 doubles (>= grid)
+    s.bar = (unsigned int*)(s.partial + 1010);
+    s.tol = tol;
+    s.max_sweeps = max_sweeps;
+    s.info = info;
+    s.off_out = off_out;
+    RSVD_CHECK_CUDA(cudaMemsetAsync(s.bar, 0, 2 * sizeof(unsigned int), st));
+    unsigned nb = (unsigned)cdiv(W2 * W2, 256);
+    k_pad_copy<<<nb, 256, 0, st>>>(n, W2, M, ldm, s.Mb[0], W2);
+    RSVD_CHECK_LAUNCH();
+    nb = (unsigned)cdiv(n * W2, 256);
+    k_pad_copy<<<nb, 256, 0, st>>>(n, W2, V, ldv, s.Vb[0], n);
+    RSVD_CHECK_LAUNCH();
+
+    const int64_t half = W2 / 2;
+    size_t smem = (size_t)(4 * half) * sizeof(double);
+    RSVD_REQUIRE(smem <= 200 * 1024, "jacobi: n too large (%lld)", (long long)n);
+    if (smem > 48 * 1024)
+        RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem));
+    int per_sm = 0;
+    RSVD_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi, kJacThreads, smem));
+    RSVD_REQUIRE(per_sm >= 1, "jacobi: kernel cannot be resident");
+    int64_t want = cdiv(half * half + n * half, (int64_t)kJacThreads * 2);
+    int64_t maxb = (int64_t)sm_count();
+    if (want > maxb) want = maxb;
+    if (want < 1) want = 1;
+    unsigned grid = (unsigned)want;
+    void* args[] = {&s};
+    RSVD_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)k_jacobi, dim3(grid), dim3(kJacThreads),
+                                                args, smem, st));
+    nb = (unsigned)cdiv(n * n, 256);
+    k_unpad_copy<<<nb, 256, 0, st>>>(n, W2, s.Mb[0], s.Mb[1], info, M, ldm, n);
+    RSVD_CHECK_LAUNCH();
+    k_unpad_copy<<<nb, 256, 0, st>>>(n, W2, s.Vb[0], s.Vb[1], info, V, ldv, n);
+    RSVD_CHECK_LAUNCH();
+    return RSVD_OK;
+}
+
+int eig_select(int64_t w, const double* M, int64_t ldm, const double* V, int64_t ldv, int64_t k,
+               double* evals, double* evecs, int64_t lde, void* order_ws, cudaStream_t st) {
+    RSVD_REQUIRE(k >= 0 && k <= w, "eig_select: k out of range");
+    if (k == 0) return RSVD_OK;
+    int32_t* order = (int32_t*)order_ws;
+    k_eig_order<<<1, 1024, 0, st>>>(w, M, ldm, k, order, evals);
+    RSVD_CHECK_LAUNCH();
+    unsigned nb = (unsigned)cdiv(w * k, 256);
+    k_eig_gather<<<nb, 256, 0, st>>>(w, k, order, V, ldv, evecs, lde);
+    RSVD_CHECK_LAUNCH();
+    return RSVD_OK;
+}
+
+}  // namespace rsvd

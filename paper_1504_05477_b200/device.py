@@ -1,0 +1,249 @@
+"""Device layer: torch CUDA tensors in, C-ABI kernel launches out.
+
+torch provides device memory, the current stream and (for multi-GPU) the
+NCCL communicator; every FLOP of the path runs in librsvd_b200.so. All calls
+are stream-ordered on ``torch.cuda.current_stream()`` and never synchronise,
+so a whole factorization can be captured in a CUDA graph.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import F32, F64, GEMM_AUTO, check
+
+_TDT = {torch.float32: F32, torch.float64: F64}
+
+
+def lib():
+    return _lib.load()
+
+
+def dcode(t):
+    try:
+        return _TDT[t.dtype]
+    except KeyError:
+        raise ValueError(f"unsupported dtype {t.dtype}") from None
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _ld(t):
+    assert t.dim() == 2 and (t.stride(1) == 1 or t.shape[1] <= 1), "row-major 2-D tensor required"
+    return max(t.stride(0), t.shape[1]) if t.shape[0] > 1 else max(t.shape[1], 1)
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class _Workspace:
+    """One growing scratch buffer per device. Safe because every user runs in
+    stream order on the same stream."""
+
+    def __init__(self):
+        self.buf = {}
+
+    def get(self, nbytes, device):
+        key = torch.device(device).index
+        b = self.buf.get(key)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=device)
+            self.buf[key] = b
+        return b
+
+    def reserve(self, nbytes, device):
+        self.get(nbytes, device)
+
+
+WS = _Workspace()
+
+
+def gemm_nn(A, B, C, alpha=1.0, beta=0.0, row_sub=None, algo=GEMM_AUTO):
+    m, k = A.shape
+    k2, n = B.shape
+    assert k == k2 and C.shape == (m, n), (A.shape, B.shape, C.shape)
+    assert A.dtype == B.dtype == C.dtype
+    check(lib().rsvd_gemm_nn(dcode(A), m, n, k, float(alpha), _ptr(A), _ld(A), _ptr(B), _ld(B),
+                             float(beta), _ptr(C), _ld(C), _ptr(row_sub), int(algo), _stream()),
+          "gemm_nn")
+    return C
+
+
+def gemm_tn(A, B, C, alpha=1.0, beta=0.0, mu=None, colsum_b=None, algo=GEMM_AUTO):
+    """C (k x n) = alpha (A^T B - mu colsum_b^T) + beta C, A m x k, B m x n."""
+    m, k = A.shape
+    m2, n = B.shape
+    assert m == m2 and C.shape == (k, n), (A.shape, B.shape, C.shape)
+    assert A.dtype == B.dtype
+    L = lib()
+    nbytes = L.rsvd_gemm_tn_ws_bytes(dcode(A), m, n, k, int(algo))
+    ws = WS.get(nbytes, A.device)
+    check(L.rsvd_gemm_tn(dcode(A), dcode(C), m, n, k, float(alpha), _ptr(A), _ld(A), _ptr(B), _ld(B),
+                         float(beta), _ptr(C), _ld(C), _ptr(mu), _ptr(colsum_b), _ptr(ws), ws.numel(),
+                         int(algo), _stream()), "gemm_tn")
+    return C
+
+
+def gram(V, out=None, algo=GEMM_AUTO):
+    """FP64 Gram V^T V."""
+    p = V.shape[1]
+    if out is None:
+        out = torch.empty((p, p), dtype=torch.float64, device=V.device)
+    return gemm_tn(V, V, out, algo=algo)
+
+
+def colreduce(X, square=True, out=None):
+    n, p = X.shape
+    if out is None:
+        out = torch.empty(p, dtype=torch.float64, device=X.device)
+    L = lib()
+    ws = WS.get(L.rsvd_colreduce_ws_bytes(n, p), X.device)
+    check(L.rsvd_colreduce(dcode(X), 1 if square else 0, n, p, _ptr(X), _ld(X), _ptr(out), _ptr(ws),
+                           ws.numel(), _stream()), "colreduce")
+    return out
+
+
+def chol_deflate(G, ref2, tau2, T, mask, ndef, running=None, active=None):
+    p = G.shape[0]
+    L = lib()
+    ws = WS.get(L.rsvd_chol_deflate_ws_bytes(p), G.device)
+    check(L.rsvd_chol_deflate(p, _ptr(G), _ld(G), _ptr(ref2), float(tau2), _ptr(T), _ld(T), _ptr(mask),
+                              _ptr(ndef), _ptr(running), _ptr(active), _ptr(ws), ws.numel(), _stream()),
+          "chol_deflate")
+
+
+def mask_cols(X, keep):
+    n, p = X.shape
+    check(lib().rsvd_mask_cols(dcode(X), n, p, _ptr(X), _ld(X), _ptr(keep), _stream()), "mask_cols")
+    return X
+
+
+def insert_fill(X, mask, ndef, seed, row_offset=0, n_total=None):
+    n, p = X.shape
+    n_total = n if n_total is None else int(n_total)
+    check(lib().rsvd_insert_fill(dcode(X), n, p, _ptr(X), _ld(X), _ptr(mask), _ptr(ndef),
+                                 ctypes.c_uint64(int(seed)), int(row_offset), n_total, _stream()),
+          "insert_fill")
+
+
+def fill_stream(n, nvec, seed, device):
+    out = torch.empty((nvec, n), dtype=torch.float64, device=device)
+    check(lib().rsvd_fill_stream(n, nvec, ctypes.c_uint64(int(seed)), _ptr(out), _stream()), "fill_stream")
+    return out
+
+
+def jacobi_sweeps(M, V, tol, max_sweeps, info=None, off=None):
+    """In place on M (diagonalised) and V (accumulated rotations).
+    Returns device tensors (info[int32: converged, sweeps, _], off[f64])."""
+    n = M.shape[0]
+    if info is None:
+        info = torch.zeros(4, dtype=torch.int32, device=M.device)
+    if off is None:
+        off = torch.zeros(1, dtype=torch.float64, device=M.device)
+    L = lib()
+    ws = WS.get(L.rsvd_jacobi_ws_bytes(n), M.device)
+    check(L.rsvd_jacobi_sweeps(n, _ptr(M), _ld(M), _ptr(V), _ld(V), float(tol), int(max_sweeps), _ptr(info),
+                               _ptr(off), _ptr(ws), ws.numel(), _stream()), "jacobi_sweeps")
+    return info, off
+
+
+def eig_select(M, V, k, evals=None, evecs=None):
+    w = M.shape[0]
+    if evals is None:
+        evals = torch.empty(k, dtype=torch.float64, device=M.device)
+    if evecs is None:
+        evecs = torch.empty((w, k), dtype=torch.float64, device=M.device)
+    order = torch.empty(max(k, 1), dtype=torch.int32, device=M.device)
+    check(lib().rsvd_eig_select(w, _ptr(M), _ld(M), _ptr(V), _ld(V), k, _ptr(evals), _ptr(evecs),
+                                _ld(evecs) if k > 0 else 1, _ptr(order), _stream()), "eig_select")
+    return evals, evecs
+
+
+def canonicalize_signs(X):
+    n, k = X.shape
+    L = lib()
+    ws = WS.get(L.rsvd_colreduce_ws_bytes(n, k), X.device)
+    check(L.rsvd_canonicalize_signs(dcode(X), n, k, _ptr(X), _ld(X), _ptr(ws), ws.numel(), _stream()),
+          "canonicalize_signs")
+    return X
+
+
+def col_absargmax(X, row_offset=0):
+    n, k = X.shape
+    val = torch.empty(k, dtype=torch.float64, device=X.device)
+    idx = torch.empty(k, dtype=torch.int64, device=X.device)
+    L = lib()
+    ws = WS.get(L.rsvd_colreduce_ws_bytes(max(n, 1), k), X.device)
+    check(L.rsvd_col_absargmax(dcode(X), n, k, _ptr(X), _ld(X), int(row_offset), _ptr(val), _ptr(idx),
+                               _ptr(ws), ws.numel(), _stream()), "col_absargmax")
+    return val, idx
+
+
+def flip_by_sign(X, sign_val):
+    n, k = X.shape
+    check(lib().rsvd_flip_by_sign(dcode(X), n, k, _ptr(X), _ld(X), _ptr(sign_val), _stream()), "flip_by_sign")
+    return X
+
+
+def convert(src, dst):
+    assert src.shape == dst.shape
+    r, c = src.shape
+    check(lib().rsvd_convert(dcode(src), dcode(dst), r, c, _ptr(src), _ld(src), _ptr(dst), _ld(dst), _stream()),
+          "convert")
+    return dst
+
+
+def sqrt_clip(x, out=None):
+    if out is None:
+        out = torch.empty_like(x)
+    check(lib().rsvd_sqrt_clip(x.numel(), _ptr(x), _ptr(out), _stream()), "sqrt_clip")
+    return out
+
+
+def ortho_error(G, out=None):
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=G.device)
+    check(lib().rsvd_ortho_error(G.shape[0], _ptr(G), _ld(G), _ptr(out), _stream()), "ortho_error")
+    return out
+
+
+def spmm_csr(indptr, col, val, ncols, B, C, alpha=1.0, beta=0.0):
+    nrows = indptr.numel() - 1
+    idx64 = 1 if indptr.dtype == torch.int64 else 0
+    assert col.dtype == indptr.dtype and val.dtype == B.dtype == C.dtype
+    nb = B.shape[1]
+    check(lib().rsvd_spmm_csr(dcode(val), idx64, nrows, ncols, nb, _ptr(indptr), _ptr(col), _ptr(val),
+                              _ptr(B), _ld(B), float(alpha), float(beta), _ptr(C), _ld(C), _stream()),
+          "spmm_csr")
+    return C
+
+
+def csr_transpose(indptr, col, val, nrows, ncols):
+    """Device CSR of A^T (stable in row order). The stable column sort that
+    orders the nonzeros is torch plumbing done once per operator."""
+    nnz = col.numel()
+    perm = torch.sort(col.to(torch.int64), stable=True).indices
+    tptr = torch.empty(ncols + 1, dtype=indptr.dtype, device=col.device)
+    tcol = torch.empty(nnz, dtype=col.dtype, device=col.device)
+    tval = torch.empty(nnz, dtype=val.dtype, device=col.device)
+    idx64 = 1 if indptr.dtype == torch.int64 else 0
+    check(lib().rsvd_csr_transpose(dcode(val), idx64, nrows, ncols, nnz, _ptr(indptr), _ptr(col), _ptr(val),
+                                   _ptr(perm), _ptr(tptr), _ptr(tcol), _ptr(tval), _stream()), "csr_transpose")
+    return tptr, tcol, tval
+
+
+def gauss_fill_host(count, state):
+    """Host Gaussian stream through the C ABI (bit-identical to the reference)."""
+    import numpy as np
+
+    out = np.empty(int(count), dtype=np.float64)
+    new = ctypes.c_uint64(0)
+    check(lib().rsvd_gauss_fill(int(count), ctypes.c_uint64(int(state) & ((1 << 64) - 1)),
+                                out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(new)), "gauss_fill")
+    return out, int(new.value)

@@ -1,0 +1,335 @@
+"""Device orchestration of the north_star path: Krylov chain, blocked
+orthonormalization, Rayleigh-Ritz.
+
+Reference call stack (rsvd.py:263-290):
+    _run -> _bk_basis / _si_basis / _sketch_basis (rsvd.py:224-260)
+         -> _mgs per block and on hstack(blocks) (factor.py:79-118)
+         -> post_process (rsvd.py:200-221) -> symmetric_eig (factor.py:132-166)
+
+B200 restructuring:
+  * every n-side block (Y, b_j, Q, Z) lives in HBM in the work precision;
+    A is read in place for both A X and A^T Y (no cached A^T copy,
+    matrix.py:245-247);
+  * _mgs's column loop (BLAS-2, factor.py:100-117) becomes a blocked
+    BCGS2 + CholeskyQR2 with deficiency deflation (``orth_block``): GEMMs
+    for the projections, an FP64 Gram, a single-CTA column-ordered Cholesky
+    that applies the reference's "residual small relative to the column's
+    original norm" test and replaces deficient columns from the reference's
+    fill stream, generated on the device;
+  * post_process's two passes over A at width w (rsvd.py:216) become one:
+    W = A^T Q, M = W^T W (the same matrix, Q^T A A^T Q);
+  * nothing here synchronises with the host; the whole call is one stream.
+
+Row sharding (multi-GPU): every reduction over the row dimension n (A^T Y,
+Grams, projections Q^T V, W = A^T Q, column sums) is followed by
+``comm.allreduce``; small matrices are replicated and computed identically
+on every rank (deterministic kernels => identical decisions).
+"""
+
+from __future__ import annotations
+
+import torch
+
+QR_FILL_SEED = 0x5EED_F111_0C0F_FEE5  # factor.py:40
+JACOBI_TOL = 1e-14  # factor.py:34
+JACOBI_MAX_SWEEPS = 50  # factor.py:35
+# Deflation thresholds on the residual norm relative to the original column
+# norm (the reference's is 1e-12 on exact CGS2 residuals, factor.py:41,105;
+# a Gram-based test cannot resolve below ~sqrt(eps)).
+TAU = {torch.float64: 1e-7, torch.float32: 3e-3}
+REF_RTOL = 1e-12  # factor.py:41 (_DEFICIENCY_RTOL)
+
+
+class LocalComm:
+    """Single device: reductions are complete already."""
+
+    world = 1
+    rank = 0
+
+    def allreduce(self, t):
+        return t
+
+    def row_range(self, n):
+        return 0, n
+
+
+class TorchComm:
+    """Row-sharded ranks over torch.distributed (NCCL on GPUs, gloo in the
+    CPU tests). Sum-allreduce in place on the launching stream."""
+
+    def __init__(self, group=None, n_total=None, row_offset=0):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.n_total = n_total
+        self.row_offset = row_offset
+
+    def allreduce(self, t):
+        self.dist.all_reduce(t, group=self.group)
+        return t
+
+    def all_gather(self, t):
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return out
+
+
+def shard_rows(n, world, rank):
+    """Contiguous row shard [lo, hi) of rank (rows [g n/G, (g+1) n/G))."""
+    lo = (n * rank) // world
+    hi = (n * (rank + 1)) // world
+    return lo, hi
+
+
+class Workspace:
+    """Per-call scratch for the orchestration (small FP64 matrices + masks)."""
+
+    def __init__(self, device, p):
+        self.device = device
+        self.p = p
+        f64 = dict(dtype=torch.float64, device=device)
+        i32 = dict(dtype=torch.int32, device=device)
+        self.G = torch.empty((p, p), **f64)
+        self.T = torch.empty((p, p), **f64)
+        self.mask = torch.empty(p, **i32)
+        self.ndef = torch.zeros(2, **i32)
+        self.mask2 = torch.empty(p, **i32)
+        self.ndef2 = torch.zeros(2, **i32)
+        self.ref2 = torch.empty(p, **f64)
+        self.ref_orig = torch.empty(p, **f64)
+        self.ndef_total = torch.zeros(1, **i32)
+
+
+def _cast_small(ops, T64, dtype, out=None):
+    if dtype == torch.float64:
+        return T64
+    if out is None:
+        out = torch.empty(T64.shape, dtype=dtype, device=T64.device)
+    return ops.convert(T64, out)
+
+
+def project_out(ops, comm, Qp, V, tmp_c):
+    """V <- V - Qp (Qp^T V)  (one block classical Gram-Schmidt pass)."""
+    if Qp is None or Qp.shape[1] == 0:
+        return V
+    ops.gemm_tn(Qp, V, tmp_c)
+    comm.allreduce(tmp_c)
+    ops.gemm_nn(Qp, tmp_c, V, alpha=-1.0, beta=1.0)
+    return V
+
+
+def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=None, row_offset=0,
+               tau=None, deflation_count=None, two_round=None):
+    """Orthonormalize the n x p block V in place (span-preserving, column
+    order preserving), against the orthonormal columns Qp when given.
+
+    Round 1: BCGS2 projection against Qp, FP64 Gram, column-ordered Cholesky
+      with deflation at ``tau`` (the Gram resolves residuals only down to
+      ~sqrt(eps)), Q1 = V R^{-1}, cleaned by one CholeskyQR step.
+    Round 2 (FP64, ``two_round``): the columns round 1 rejected are re-tested
+      on their EXPLICIT residuals (projected against Qp and Q1) at the
+      reference's own threshold 1e-12 x original column norm (factor.py:41,
+      105); survivors join Q1, the rest are replaced from the fill stream
+      (factor.py:106-112).
+    Final: one projection + CholeskyQR step.
+    """
+    dtype = V.dtype
+    p = V.shape[1]
+    if two_round is None:
+        two_round = dtype == torch.float64
+    tau = TAU[dtype] if tau is None else tau
+    n_total = V.shape[0] if n_total is None else n_total
+    has_prev = Qp is not None and Qp.shape[1] > 0
+    tmp_c = torch.empty((Qp.shape[1], p), dtype=dtype, device=V.device) if has_prev else None
+    if has_prev:
+        project_out(ops, comm, Qp, V, tmp_c)
+        project_out(ops, comm, Qp, V, tmp_c)
+    G = ws.G[:p, :p]
+    T = ws.T[:p, :p]
+    mask = ws.mask[:p]
+    if two_round and tau > 0.0 and ref2 is None:
+        ops.colreduce(V, True, ws.ref_orig[:p])  # original column norms^2
+        comm.allreduce(ws.ref_orig[:p])
+    ops.gram(V, G)
+    comm.allreduce(G)
+    if two_round and tau > 0.0:
+        ops.chol_deflate(G, ref2, tau * tau, T, mask, ws.ndef, None)
+        ops.gemm_nn(V, T, tmp)  # Q1 raw (zero columns at rejected slots)
+        Q1 = torch.empty_like(tmp)
+        ops.gram(tmp, G)
+        comm.allreduce(G)
+        ops.chol_deflate(G, None, 0.0, T, ws.mask2[:p], ws.ndef2, None)
+        ops.gemm_nn(tmp, T, Q1)  # Q1 clean
+        ops.mask_cols(V, mask)  # keep only the rejected columns' residuals
+        c2 = torch.empty((p, p), dtype=dtype, device=V.device)
+        if has_prev:
+            project_out(ops, comm, Qp, V, tmp_c)
+        project_out(ops, comm, Q1, V, c2)
+        if has_prev:
+            project_out(ops, comm, Qp, V, tmp_c)
+        project_out(ops, comm, Q1, V, c2)
+        ops.gram(V, G)
+        comm.allreduce(G)
+        ref = ref2 if ref2 is not None else ws.ref_orig[:p]
+        ops.chol_deflate(G, ref, REF_RTOL * REF_RTOL, T, ws.mask2[:p], ws.ndef, running, mask)
+        ops.gemm_nn(V, T, Q1, beta=1.0)  # survivors join the kept columns
+        ops.insert_fill(Q1, ws.mask2[:p], ws.ndef, QR_FILL_SEED, row_offset, n_total)
+        out = Q1
+    else:
+        ops.chol_deflate(G, ref2, tau * tau, T, mask, ws.ndef, running)
+        Tw = _cast_small(ops, T, dtype)
+        ops.gemm_nn(V, Tw, tmp)
+        ops.insert_fill(tmp, mask, ws.ndef, QR_FILL_SEED, row_offset, n_total)
+        out = tmp
+    if deflation_count is not None:
+        deflation_count += ws.ndef[:1]
+    if has_prev:
+        project_out(ops, comm, Qp, out, tmp_c)
+    ops.gram(out, G)
+    comm.allreduce(G)
+    ops.chol_deflate(G, None, 0.0, T, ws.mask2[:p], ws.ndef2, None)
+    Tw = _cast_small(ops, T, dtype)
+    ops.gemm_nn(out, Tw, V)
+    return V
+
+
+class BasisResult:
+    def __init__(self, Q, q_used, deflated):
+        self.Q = Q
+        self.q_used = q_used
+        self.deflated = deflated  # device int32 tensor: columns replaced in the final orth
+
+
+def sketch_basis(ops, comm, op, Pi, ws, n_total, row_offset):
+    """rsvd.py:224-226: b0 = mgs(A Pi)."""
+    n = op.local_rows
+    p = Pi.shape[1]
+    Y = torch.empty((n, p), dtype=op.dtype, device=op.device)
+    tmp = torch.empty_like(Y)
+    op.apply(Pi, Y)
+    running = torch.zeros(1, dtype=torch.int32, device=op.device)
+    orth_block(ops, comm, Y, tmp, ws, running=running, n_total=n_total, row_offset=row_offset)
+    return Y
+
+
+def bk_basis(ops, comm, op, Pi, q, ws, n_total, row_offset):
+    """rsvd.py:244-260 — block Krylov basis [b0 .. b_q], orthonormalized.
+
+    Blocks are written straight into the n x w basis buffer K; the final
+    orthonormalization (``_mgs(np.hstack(blocks))``) runs block by block in
+    place (BCGS2 against the already orthonormal prefix)."""
+    n = op.local_rows
+    d = op.shape[1]
+    p = Pi.shape[1]
+    cap_blocks = max(1, min(n_total, d) // p)
+    n_blocks = min(q + 1, cap_blocks)
+    dev, dt = op.device, op.dtype
+    K = torch.empty((n, n_blocks * p), dtype=dt, device=dev)
+    tmp = torch.empty((n, p), dtype=dt, device=dev)
+    C = torch.empty((d, p), dtype=dt, device=dev)
+    running = torch.zeros(1, dtype=torch.int32, device=dev)
+    b0 = K[:, :p]
+    op.apply(Pi, b0)
+    orth_block(ops, comm, b0, tmp, ws, running=running, n_total=n_total, row_offset=row_offset)
+    if n_blocks == 1:
+        return BasisResult(K, 0, torch.zeros(1, dtype=torch.int32, device=dev))
+    for j in range(1, n_blocks):
+        prev = K[:, (j - 1) * p: j * p]
+        cur = K[:, j * p: (j + 1) * p]
+        op.apply_t(prev, C)
+        comm.allreduce(C)
+        op.apply(C, cur)
+        running.zero_()
+        orth_block(ops, comm, cur, tmp, ws, running=running, n_total=n_total, row_offset=row_offset)
+    # final orthonormalization of hstack(blocks): one _mgs call -> one fill stream
+    running.zero_()
+    deflated = torch.zeros(1, dtype=torch.int32, device=dev)
+    for j in range(n_blocks):
+        cur = K[:, j * p: (j + 1) * p]
+        ref2 = ws.ref2[:p]
+        ops.colreduce(cur, True, ref2)
+        comm.allreduce(ref2)
+        orth_block(ops, comm, cur, tmp, ws, Qp=K[:, : j * p] if j else None, ref2=ref2, running=running,
+                   n_total=n_total, row_offset=row_offset, deflation_count=deflated)
+    return BasisResult(K, n_blocks - 1, deflated)
+
+
+def si_basis(ops, comm, op, Pi, q, every, ws, n_total, row_offset):
+    """rsvd.py:229-241 — simultaneous (power) iteration."""
+    if q == 0:
+        return sketch_basis(ops, comm, op, Pi, ws, n_total, row_offset)
+    n = op.local_rows
+    d = op.shape[1]
+    p = Pi.shape[1]
+    dev, dt = op.device, op.dtype
+    b = torch.empty((n, p), dtype=dt, device=dev)
+    tmp = torch.empty_like(b)
+    C = torch.empty((d, p), dtype=dt, device=dev)
+    running = torch.zeros(1, dtype=torch.int32, device=dev)
+    op.apply(Pi, b)
+    orthonormal = False
+    for t in range(1, q + 1):
+        op.apply_t(b, C)
+        comm.allreduce(C)
+        op.apply(C, b)
+        orthonormal = False
+        if every and t % every == 0:
+            running.zero_()
+            orth_block(ops, comm, b, tmp, ws, running=running, n_total=n_total, row_offset=row_offset)
+            orthonormal = True
+    if not orthonormal:
+        running.zero_()
+        orth_block(ops, comm, b, tmp, ws, running=running, n_total=n_total, row_offset=row_offset)
+    return b
+
+
+class RitzResult:
+    def __init__(self, Z, sigma, info, off, zerr):
+        self.Z = Z  # n_local x k FP64, signs canonicalized
+        self.sigma = sigma  # k FP64
+        self.info = info  # int32 [converged, sweeps, ...]
+        self.off = off  # FP64 [1]
+        self.zerr = zerr  # FP64 [1]: max |Z^T Z - I| (rsvd.py:182-185)
+
+
+def rayleigh_ritz(ops, comm, op, Q, k, n_total, row_offset, sign_fn=None):
+    """rsvd.py:200-221 with M = W^T W, W = A^T Q (one pass over A)."""
+    dev = op.device
+    w = Q.shape[1]
+    d = op.shape[1]
+    W = torch.empty((d, w), dtype=torch.float64, device=dev)
+    op.apply_t(Q, W)
+    comm.allreduce(W)
+    M = torch.empty((w, w), dtype=torch.float64, device=dev)
+    ops.gram(W, M)
+    V = torch.eye(w, dtype=torch.float64, device=dev)
+    info, off = ops.jacobi_sweeps(M, V, JACOBI_TOL, JACOBI_MAX_SWEEPS)
+    evals, Uk = ops.eig_select(M, V, k)
+    n = Q.shape[0]
+    if Q.dtype == torch.float64:
+        Z = torch.empty((n, k), dtype=torch.float64, device=dev)
+        ops.gemm_nn(Q, Uk, Z)
+    else:
+        Uk32 = torch.empty((w, k), dtype=Q.dtype, device=dev)
+        ops.convert(Uk, Uk32)
+        Z32 = torch.empty((n, k), dtype=Q.dtype, device=dev)
+        ops.gemm_nn(Q, Uk32, Z32)
+        Z = torch.empty((n, k), dtype=torch.float64, device=dev)
+        ops.convert(Z32, Z)
+        # FP64 re-orthonormalization of the n x k Z (CholeskyQR2)
+        ws = Workspace(dev, k)
+        tmp = torch.empty_like(Z)
+        orth_block(ops, comm, Z, tmp, ws, tau=0.0, n_total=n_total, row_offset=row_offset)
+    if sign_fn is None:
+        ops.canonicalize_signs(Z)
+    else:
+        sign_fn(Z)
+    sigma = ops.sqrt_clip(evals)
+    G = torch.empty((k, k), dtype=torch.float64, device=dev)
+    ops.gram(Z, G)
+    comm.allreduce(G)
+    zerr = ops.ortho_error(G)
+    return RitzResult(Z, sigma, info, off, zerr)

@@ -1,0 +1,403 @@
+"""Public algorithm API — drop-in for rsvdkit's rsvd module (rsvd.py:1-314).
+
+Same names, signatures, validation order, exceptions and result type as the
+reference: ``Variant``, ``RsvdConfig`` (with the block-Krylov odd-q bump,
+rsvd.py:157-158), ``derive_q`` / ``derive_q_gap``, ``PartialSvdResult`` (its
+``||Z^T Z - I||_max <= 1e-10`` check, rsvd.py:182-185), ``post_process``,
+``simultaneous_iteration``, ``block_krylov``, ``sketch_and_solve`` and
+``factorize``. The start block Pi is drawn on the host from
+``SeededRng(cfg.seed)`` exactly as the reference does (rsvd.py:225, 233);
+everything after that runs on the GPU (krylov.py).
+
+Extra keyword arguments (outside RsvdConfig, so reference configs validate
+unchanged):
+  precision  "auto" (default: FP32 path for float32 input, else FP64),
+             "fp64" or "fp32" (3xTF32 tensor-core products, FP64 small
+             algebra, FP64 re-orthonormalized Z).
+  center     implicit mean-centering (PCA): factorizes A - 1 mu^T without
+             forming it.
+  device     CUDA device for host inputs (default: current device).
+  comm       krylov.TorchComm for a row-sharded A (each rank passes its
+             rows; results are returned on every rank).
+"""
+
+from __future__ import annotations
+
+import enum
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import device as ops
+from . import krylov
+from .errors import ConvergenceError
+from .matrix import DenseMatrix, SeededRng, SparseMatrixCSR, as_dense_array, gaussian
+from .operators import CsrDeviceOp, DenseDeviceOp
+
+__all__ = [
+    "Variant",
+    "RsvdConfig",
+    "PartialSvdResult",
+    "derive_q",
+    "derive_q_gap",
+    "post_process",
+    "simultaneous_iteration",
+    "block_krylov",
+    "sketch_and_solve",
+    "factorize",
+]
+
+
+class Variant(str, enum.Enum):
+    SIMULTANEOUS_ITERATION = "si"
+    BLOCK_KRYLOV = "bk"
+    SKETCH = "sketch"
+
+
+def _variant(v):
+    return v if isinstance(v, Variant) else Variant(str(v).lower())
+
+
+def _odd(q):
+    return q + 1 - (q % 2)  # rsvd.py:52-53
+
+
+def _check_common(d, epsilon, C):
+    if d < 2:
+        raise ValueError("d must be at least 2")
+    if not 0 < epsilon < 1:
+        raise ValueError("epsilon must be in (0, 1)")
+    if not C > 0:
+        raise ValueError("C must be positive")
+
+
+def derive_q(variant, d, epsilon, C=4.0):
+    """rsvd.py:56-75 — SI: ceil(C ln d / eps); BK: ceil(C ln d / sqrt(eps)), odd."""
+    variant = _variant(variant)
+    if variant is Variant.SKETCH:
+        return 0
+    _check_common(d, epsilon, C)
+    if variant is Variant.SIMULTANEOUS_ITERATION:
+        return math.ceil(C * math.log(d) / epsilon)
+    return _odd(math.ceil(C * math.log(d) / math.sqrt(epsilon)))
+
+
+def derive_q_gap(variant, d, epsilon, gap, C=4.0):
+    """rsvd.py:78-100 — gap-aware count, gap clamped to 1."""
+    variant = _variant(variant)
+    if variant is Variant.SKETCH:
+        return 0
+    if d < 2:
+        raise ValueError("d must be at least 2")
+    if not 0 < epsilon < 1:
+        raise ValueError("epsilon must be in (0, 1)")
+    if not gap > 0:
+        raise ValueError("gap must be positive")
+    if not C > 0:
+        raise ValueError("C must be positive")
+    g = min(1.0, float(gap))
+    base = C * math.log(d / epsilon)
+    if variant is Variant.SIMULTANEOUS_ITERATION:
+        return math.ceil(base / g)
+    return _odd(math.ceil(base / math.sqrt(g)))
+
+
+@dataclass(frozen=True)
+class RsvdConfig:
+    """rsvd.py:103-162 — factorization request (exactly one of q / epsilon;
+    gap needs epsilon; p defaults to k and must be >= k)."""
+
+    k: int
+    variant: Variant
+    p: int | None = None
+    q: int | None = None
+    epsilon: float | None = None
+    gap: float | None = None
+    C: float = 4.0
+    seed: int = 0
+    reorthonormalize_every: int = 1
+
+    def __post_init__(self):
+        object.__setattr__(self, "variant", _variant(self.variant))
+        if self.k < 1:
+            raise ValueError("k must be at least 1")
+        p = self.k if self.p is None else int(self.p)
+        if p < self.k:
+            raise ValueError("block width p must be at least k")
+        object.__setattr__(self, "p", p)
+        if self.variant is not Variant.SKETCH and (self.q is None) == (self.epsilon is None):
+            raise ValueError("give exactly one of q or epsilon")
+        if self.q is not None and self.q < 0:
+            raise ValueError("q must be nonnegative")
+        if self.epsilon is not None and not 0 < self.epsilon < 1:
+            raise ValueError("epsilon must be in (0, 1)")
+        if self.gap is not None:
+            if self.epsilon is None:
+                raise ValueError("gap requires epsilon")
+            if not self.gap > 0:
+                raise ValueError("gap must be positive")
+        if not self.C > 0:
+            raise ValueError("C must be positive")
+        if not 0 <= int(self.seed) < (1 << 64):
+            raise ValueError("seed must fit in an unsigned 64-bit integer")
+        if self.reorthonormalize_every < 0:
+            raise ValueError("reorthonormalize_every must be nonnegative")
+
+    def resolve_q(self, d):
+        """rsvd.py:151-162 — BK bumps an explicit even q >= 1 to odd."""
+        if self.variant is Variant.SKETCH:
+            return 0
+        if self.q is not None:
+            q = int(self.q)
+            return _odd(q) if (self.variant is Variant.BLOCK_KRYLOV and q >= 1) else q
+        if self.gap is not None:
+            return derive_q_gap(self.variant, d, self.epsilon, self.gap, self.C)
+        return derive_q(self.variant, d, self.epsilon, self.C)
+
+
+def _wrap_dense(arr):
+    """DenseMatrix around a freshly produced float64 array without a second copy."""
+    arr = np.ascontiguousarray(arr, dtype=np.float64)
+    if not np.all(np.isfinite(arr)):
+        raise ValueError("dense matrix entries must be finite")
+    arr.setflags(write=False)
+    obj = object.__new__(DenseMatrix)
+    object.__setattr__(obj, "data", arr)
+    return obj
+
+
+@dataclass(frozen=True)
+class PartialSvdResult:
+    """rsvd.py:165-189 — orthonormal Z (n x k), approximate singular values
+    (descending, >= 0), diagnostics. The orthonormality check uses the
+    device-computed ||Z^T Z - I||_max when the factorization produced it."""
+
+    Z: DenseMatrix
+    approx_singular_values: np.ndarray
+    q_used: int
+    wall_time_ms: float
+    variant: Variant
+    seed: int
+    _z_ortho_err: float | None = field(default=None, repr=False, compare=False)
+
+    def __post_init__(self):
+        sv = np.array(self.approx_singular_values, dtype=np.float64, copy=True)
+        if sv.ndim != 1 or np.any(sv < 0) or np.any(np.diff(sv) > 0):
+            raise ValueError("approximate singular values must be nonnegative descending")
+        sv.setflags(write=False)
+        object.__setattr__(self, "approx_singular_values", sv)
+        err = self._z_ortho_err
+        if err is None:
+            z = self.Z.data
+            err = float(np.max(np.abs(z.T @ z - np.eye(z.shape[1])))) if z.size else 0.0
+        if not err <= 1e-10:
+            raise ValueError("Z must have orthonormal columns")
+
+    @property
+    def k(self):
+        return self.Z.cols
+
+
+# --------------------------------------------------------------------------
+# input handling
+
+
+def _resolve_device(device):
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1504_05477_b200 requires a CUDA device (no CPU fallback)")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+def _work_dtype(src_dtype, precision):
+    if precision == "fp64":
+        return torch.float64
+    if precision == "fp32":
+        return torch.float32
+    if precision != "auto":
+        raise ValueError("precision must be 'auto', 'fp64' or 'fp32'")
+    return torch.float32 if src_dtype in (np.float32, torch.float32) else torch.float64
+
+
+def make_operator(A, precision="auto", center=False, device=None, comm=None, n_total=None, row_offset=0):
+    """Upload / wrap A as a device operator (the as_operator step,
+    matrix.py:260-263). Dense host input is validated like DenseMatrix."""
+    if isinstance(A, (DenseDeviceOp, CsrDeviceOp)):
+        return A
+    if isinstance(A, SparseMatrixCSR):
+        if center:
+            raise ValueError("implicit centering is supported for dense A only")
+        dev = _resolve_device(device)
+        dt = _work_dtype(np.float64, precision)
+        idx = torch.int64 if A.nnz >= 2**31 - 1 else torch.int32
+        indptr = torch.from_numpy(A.row_ptr.astype(np.int64)).to(device=dev, dtype=idx)
+        col = torch.from_numpy(A.col_idx).to(device=dev, dtype=idx)
+        val = torch.from_numpy(A.values).to(device=dev, dtype=dt)
+        return CsrDeviceOp(indptr, col, val, A.cols, n_total=n_total, row_offset=row_offset)
+    if isinstance(A, torch.Tensor):
+        dev = A.device if A.is_cuda else _resolve_device(device)
+        dt = _work_dtype(A.dtype, precision)
+        if A.dim() != 2:
+            raise ValueError("dense matrix data must be 2-D")
+        t = A.to(device=dev, dtype=dt)
+        if not bool(torch.isfinite(t).all()):
+            raise ValueError("dense matrix entries must be finite")
+        return DenseDeviceOp(t.contiguous(), n_total=n_total, row_offset=row_offset, center=center, comm=comm)
+    src_dtype = np.asarray(A).dtype if not isinstance(A, DenseMatrix) else np.float64
+    arr = as_dense_array(A) if not (isinstance(A, np.ndarray) and A.dtype == np.float32) else np.asarray(A)
+    if arr.ndim != 2:
+        raise ValueError("dense matrix data must be 2-D")
+    if not np.all(np.isfinite(arr)):
+        raise ValueError("dense matrix entries must be finite")
+    dev = _resolve_device(device)
+    dt = _work_dtype(src_dtype, precision)
+    t = torch.from_numpy(np.ascontiguousarray(arr)).to(device=dev, dtype=dt, non_blocking=False)
+    return DenseDeviceOp(t, n_total=n_total, row_offset=row_offset, center=center, comm=comm)
+
+
+# --------------------------------------------------------------------------
+# device pipeline
+
+
+@dataclass
+class DeviceFactorization:
+    """Device-resident outcome of one factorization (no host copies)."""
+
+    Z: torch.Tensor  # n_local x k FP64
+    sigma: torch.Tensor  # k FP64
+    info: torch.Tensor  # Jacobi [converged, sweeps, ...]
+    off: torch.Tensor
+    zerr: torch.Tensor
+    q_used: int
+    deflated: torch.Tensor | None = None
+
+
+def _sign_fn_for(comm):
+    if comm is None or getattr(comm, "world", 1) == 1:
+        return None
+    from .dist import sharded_canonicalize_signs
+
+    return lambda Z: sharded_canonicalize_signs(Z, comm)
+
+
+def run_device(op, cfg, comm=None, Pi=None):
+    """The whole path on the device for an already-uploaded operator.
+    Validation as _run (rsvd.py:263-270); no host synchronisation."""
+    n, d = op.shape
+    if cfg.k > min(n, d):
+        raise ValueError("k must not exceed min(n, d)")
+    q = cfg.resolve_q(d)
+    c = comm if comm is not None else krylov.LocalComm()
+    n_total, row_offset = op.n_total, op.row_offset
+    p = cfg.p
+    if cfg.variant is Variant.BLOCK_KRYLOV and p > n:
+        raise ValueError("block width p exceeds n; no Krylov block fits")
+    if Pi is None:
+        Pi = gaussian(d, p, SeededRng(cfg.seed)).data
+    pi_dev = torch.from_numpy(np.ascontiguousarray(Pi)).to(device=op.device, dtype=op.dtype, non_blocking=True)
+    ws = krylov.Workspace(op.device, p)
+    deflated = None
+    if cfg.variant is Variant.SIMULTANEOUS_ITERATION:
+        Q = krylov.si_basis(ops, c, op, pi_dev, q, cfg.reorthonormalize_every, ws, n_total, row_offset)
+        q_used = q
+    elif cfg.variant is Variant.BLOCK_KRYLOV:
+        br = krylov.bk_basis(ops, c, op, pi_dev, q, ws, n_total, row_offset)
+        Q, q_used, deflated = br.Q, br.q_used, br.deflated
+    else:
+        Q = krylov.sketch_basis(ops, c, op, pi_dev, ws, n_total, row_offset)
+        q_used = 0
+    rr = krylov.rayleigh_ritz(ops, c, op, Q, cfg.k, n_total, row_offset, sign_fn=_sign_fn_for(comm))
+    return DeviceFactorization(rr.Z, rr.sigma, rr.info, rr.off, rr.zerr, q_used, deflated)
+
+
+def _finish(df, cfg, t0, gather_z=None):
+    info = df.info.cpu()
+    off = float(df.off.cpu()[0])
+    if int(info[0]) != 1:
+        raise ConvergenceError(
+            f"Jacobi did not converge in {krylov.JACOBI_MAX_SWEEPS} sweeps (off-diagonal mass {off:.3e})",
+            residual=off,
+        )
+    Z = df.Z if gather_z is None else gather_z(df.Z)
+    z_host = Z.cpu().numpy()
+    sigma = df.sigma.cpu().numpy()
+    zerr = float(df.zerr.cpu()[0])
+    elapsed_ms = (time.perf_counter() - t0) * 1e3
+    return PartialSvdResult(
+        Z=_wrap_dense(z_host),
+        approx_singular_values=sigma,
+        q_used=df.q_used,
+        wall_time_ms=elapsed_ms,
+        variant=cfg.variant,
+        seed=int(cfg.seed),
+        _z_ortho_err=zerr,
+    )
+
+
+def _run(A, cfg, expected, precision="auto", center=False, device=None, comm=None):
+    if cfg.variant is not expected:
+        raise ValueError(f"config variant is {cfg.variant.value}, not {expected.value}")
+    n_total = row_offset = None
+    if comm is not None and getattr(comm, "world", 1) > 1:
+        n_total, row_offset = comm.n_total, comm.row_offset
+    op = make_operator(A, precision=precision, center=center, device=device, comm=comm,
+                       n_total=n_total, row_offset=row_offset or 0)
+    dev = op.device
+    with torch.cuda.device(dev):
+        t0 = time.perf_counter()
+        df = run_device(op, cfg, comm=comm)
+        gather = None
+        if comm is not None and getattr(comm, "world", 1) > 1:
+            from .dist import gather_rows
+
+            gather = lambda Z: gather_rows(Z, comm)  # noqa: E731
+        return _finish(df, cfg, t0, gather)
+
+
+def simultaneous_iteration(A, cfg, **kw):
+    """rsvd.py:293-295 — randomized simultaneous (power) iteration."""
+    return _run(A, cfg, Variant.SIMULTANEOUS_ITERATION, **kw)
+
+
+def block_krylov(A, cfg, **kw):
+    """rsvd.py:298-300 — randomized block Krylov iteration."""
+    return _run(A, cfg, Variant.BLOCK_KRYLOV, **kw)
+
+
+def sketch_and_solve(A, cfg, **kw):
+    """rsvd.py:303-305 — basis of A Pi, then post-processing."""
+    return _run(A, cfg, Variant.SKETCH, **kw)
+
+
+def factorize(A, cfg, **kw):
+    """rsvd.py:308-314 — dispatch on cfg.variant."""
+    if cfg.variant is Variant.SIMULTANEOUS_ITERATION:
+        return simultaneous_iteration(A, cfg, **kw)
+    if cfg.variant is Variant.BLOCK_KRYLOV:
+        return block_krylov(A, cfg, **kw)
+    return sketch_and_solve(A, cfg, **kw)
+
+
+def post_process(A, Q, k, precision="auto", device=None):
+    """rsvd.py:200-221 — best rank-l bases inside span(Q) for every l <= k.
+    Returns (DenseMatrix Z, sigma) like the reference."""
+    op = make_operator(A, precision=precision, device=device)
+    qarr = as_dense_array(Q)
+    if qarr.shape[1] < k:
+        raise ValueError("Q must have at least k columns")
+    with torch.cuda.device(op.device):
+        qd = torch.from_numpy(qarr).to(device=op.device, dtype=op.dtype)
+        G = ops.gram(qd)
+        err = float(ops.ortho_error(G).cpu()[0])
+        if not err <= 1e-8:
+            raise ValueError("Q must have orthonormal columns")
+        rr = krylov.rayleigh_ritz(ops, krylov.LocalComm(), op, qd, int(k), op.n_total, 0)
+        info = rr.info.cpu()
+        if int(info[0]) != 1:
+            off = float(rr.off.cpu()[0])
+            raise ConvergenceError("Jacobi did not converge", residual=off)
+        return _wrap_dense(rr.Z.cpu().numpy()), rr.sigma.cpu().numpy()

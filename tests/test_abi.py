@@ -1,0 +1,68 @@
+"""C ABI checks that need no GPU: the library loads, exports every symbol
+the header declares, and the host Gaussian stream is bit-identical to the
+reference's (gauss_fill, _kernels.pyx:31-53)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+
+from conftest import GOLDEN, ROOT
+
+
+def _declared():
+    h = open(os.path.join(ROOT, "include", "rsvd_b200.h")).read()
+    return sorted(set(re.findall(r"\b(rsvd_[a-z0-9_]+)\s*\(", h)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1504_05477_b200 import _lib
+
+    L = _lib.load()
+    names = _declared()
+    assert len(names) >= 20
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(names) == set(_lib.exported_symbols())
+    assert L.rsvd_abi_version() == 1
+
+
+def test_host_gauss_fill_bitwise():
+    from paper_1504_05477_b200 import SeededRng, gaussian
+    from paper_1504_05477_b200.device import gauss_fill_host
+
+    g = np.load(os.path.join(GOLDEN, "gauss_fill.npz"))
+    for count in (1, 2, 7, 100, 1001):
+        out, st = gauss_fill_host(count, 987654321)
+        assert np.array_equal(out, g[f"fill_{count}"])
+        assert st == int(g[f"state_{count}"][0])
+    pi = gaussian(1000, 20, SeededRng(0)).data
+    assert np.array_equal(pi.ravel()[:64], g["pi_c1_head"])
+    # interleaved fills reproduce the one-shot stream (matrix.py:44-47)
+    r = SeededRng(0x5EED_F111_0C0F_FEE5)
+    parts = np.concatenate([r.normal_fill(1001), r.normal_fill(3095)])
+    assert parts[:1001].shape == (1001,)
+    one = SeededRng(0x5EED_F111_0C0F_FEE5).normal_fill(4096)
+    # 1001 is odd: the trailing pair's second half is discarded, so the
+    # streams re-align only by pair count — compare the first fill exactly
+    assert np.array_equal(parts[:1000], one[:1000])
+    assert np.array_equal(one, g["qr_fill_head"])
+
+
+def test_invalid_args_map_to_status():
+    from paper_1504_05477_b200 import _lib
+
+    L = _lib.load()
+    st = L.rsvd_gauss_fill(-1, 0, None, None)
+    assert st == _lib.RSVD_ERR_INVALID
+    assert "gauss_fill" in _lib.last_error()
+    # a bad dtype is rejected before any device work
+    st = L.rsvd_gemm_nn(7, 1, 1, 1, 1.0, None, 1, None, 1, 0.0, None, 1, None, 0, None)
+    assert st == _lib.RSVD_ERR_INVALID
+    try:
+        _lib.check(st, "gemm_nn")
+    except ValueError as e:
+        assert "dtype" in str(e)
+    else:
+        raise AssertionError("expected ValueError")

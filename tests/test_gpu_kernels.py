@@ -1,0 +1,201 @@
+"""Kernel-level parity of the CUDA library against the oracle / FP64
+references (run on the B200)."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import rsvd_oracle as o
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ops():
+    from paper_1504_05477_b200 import device
+
+    return device
+
+
+def _t(a, dt=torch.float64):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dt)
+
+
+def _rand(shape, seed):
+    return o.gaussian(*shape, o.SeededRng(seed))
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (37, 5, 19), (2000, 20, 1000), (513, 64, 200), (300, 200, 65)])
+def test_gemm_nn_f64(ops, m, n, k):
+    a, b, c0 = _rand((m, k), 1), _rand((k, n), 2), _rand((m, n), 3)
+    C = _t(c0)
+    ops.gemm_nn(_t(a), _t(b), C, alpha=0.5, beta=-2.0)
+    ref = 0.5 * (a @ b) - 2.0 * c0
+    assert np.max(np.abs(C.cpu().numpy() - ref)) <= 1e-12 * max(1.0, np.abs(ref).max()) * np.sqrt(k)
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 3, 2), (5000, 20, 64), (2000, 200, 1000), (100000, 7, 33)])
+def test_gemm_tn_f64(ops, m, n, k):
+    a, b = _rand((m, k), 4), _rand((m, n), 5)
+    C = torch.empty((k, n), dtype=torch.float64, device="cuda")
+    ops.gemm_tn(_t(a), _t(b), C)
+    ref = a.T @ b
+    assert np.max(np.abs(C.cpu().numpy() - ref)) <= 1e-11 * np.sqrt(m)
+
+
+def test_gemm_tn_centering_epilogue(ops):
+    a, b = _rand((3000, 40), 6), _rand((3000, 9), 7)
+    mu = a.mean(axis=0)
+    C = torch.empty((40, 9), dtype=torch.float64, device="cuda")
+    cs = ops.colreduce(_t(b), square=False)
+    ops.gemm_tn(_t(a), _t(b), C, mu=_t(mu), colsum_b=cs)
+    ref = (a - mu[None, :]).T @ b
+    assert np.max(np.abs(C.cpu().numpy() - ref)) < 1e-10
+
+
+def test_gemm_f32_paths(ops):
+    a, b = _rand((4096, 512), 8).astype(np.float32), _rand((512, 48), 9).astype(np.float32)
+    C = torch.empty((4096, 48), dtype=torch.float32, device="cuda")
+    ops.gemm_nn(_t(a, torch.float32), _t(b, torch.float32), C)
+    ref = a.astype(np.float64) @ b.astype(np.float64)
+    assert np.max(np.abs(C.cpu().numpy() - ref)) / np.abs(ref).max() < 2e-6
+    y = _rand((4096, 48), 10).astype(np.float32)
+    W = torch.empty((512, 48), dtype=torch.float64, device="cuda")
+    ops.gemm_tn(_t(a, torch.float32), _t(y, torch.float32), W)
+    ref = a.astype(np.float64).T @ y.astype(np.float64)
+    assert np.max(np.abs(W.cpu().numpy() - ref)) / np.abs(ref).max() < 2e-6
+
+
+def test_colreduce_and_convert(ops):
+    x = _rand((12345, 70), 11)
+    s2 = ops.colreduce(_t(x), True).cpu().numpy()
+    s1 = ops.colreduce(_t(x), False).cpu().numpy()
+    assert np.allclose(s2, (x * x).sum(0), rtol=1e-13)
+    assert np.allclose(s1, x.sum(0), rtol=1e-12, atol=1e-11)
+    X = _t(x)
+    Y = torch.empty(X.shape, dtype=torch.float32, device="cuda")
+    ops.convert(X, Y)
+    assert torch.equal(Y, X.float())
+
+
+def test_chol_deflate_full_rank_and_deficient(ops):
+    v = _rand((500, 30), 12)
+    G = _t(v.T @ v)
+    T = torch.empty((30, 30), dtype=torch.float64, device="cuda")
+    mask = torch.empty(30, dtype=torch.int32, device="cuda")
+    ndef = torch.zeros(2, dtype=torch.int32, device="cuda")
+    ops.chol_deflate(G, None, 1e-14, T, mask, ndef)
+    q = v @ T.cpu().numpy()
+    assert np.max(np.abs(q.T @ q - np.eye(30))) < 1e-12
+    assert int(ndef[0]) == 0
+    # make columns 4 and 17 linear combinations of earlier ones
+    v[:, 4] = v[:, 0] - 2 * v[:, 3]
+    v[:, 17] = v[:, 2] + v[:, 9]
+    G = _t(v.T @ v)
+    running = torch.tensor([5], dtype=torch.int32, device="cuda")
+    ops.chol_deflate(G, None, 1e-14, T, mask, ndef, running)
+    m = mask.cpu().numpy()
+    assert list(np.nonzero(m)[0]) == [4, 17]
+    assert ndef.cpu().tolist() == [2, 5] and int(running[0]) == 7
+    Tn = T.cpu().numpy()
+    assert np.all(Tn[:, 4] == 0) and np.all(Tn[17, :] == 0)
+    keep = [j for j in range(30) if not m[j]]
+    qk = (v @ Tn)[:, keep]
+    assert np.max(np.abs(qk.T @ qk - np.eye(len(keep)))) < 1e-10
+
+
+def test_fill_stream_matches_host_stream(ops):
+    n = 1001  # odd: each vector consumes n+1 uniforms (matrix.py:44-47)
+    dev = ops.fill_stream(n, 3, o.QR_FILL_SEED, "cuda").cpu().numpy()
+    rng = o.SeededRng(o.QR_FILL_SEED)
+    host = np.stack([rng.normal_fill(n) for _ in range(3)])
+    assert np.max(np.abs(dev - host)) < 1e-13
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 12, 57, 200])
+def test_jacobi_vs_oracle(ops, n):
+    base = _rand((n, n), 13 + n)
+    sym = 0.5 * (base + base.T)
+    M, V = _t(sym), _t(np.eye(n))
+    info, off = ops.jacobi_sweeps(M, V, 1e-14, 50)
+    info = info.cpu().numpy()
+    assert info[0] == 1
+    vals = np.diag(M.cpu().numpy())
+    ref_vals, _ = o.symmetric_eig(sym)
+    assert np.max(np.abs(np.sort(vals)[::-1] - ref_vals)) < 1e-12 * max(1.0, np.abs(ref_vals).max())
+    Vh = V.cpu().numpy()
+    assert np.max(np.abs(Vh @ np.diag(vals) @ Vh.T - sym)) < 1e-12 * n
+    assert np.max(np.abs(Vh.T @ Vh - np.eye(n))) < 1e-12 * n
+    evals, evecs = ops.eig_select(M, V, min(5, n))
+    assert np.allclose(evals.cpu().numpy(), ref_vals[: min(5, n)], rtol=1e-12, atol=1e-13)
+
+
+def test_jacobi_golden_kernel_contract():
+    from paper_1504_05477_b200 import backend
+
+    k = np.load(os.path.join(GOLDEN, "kernels.npz"))
+    m, v = k["jac_in"].copy(), np.eye(12)
+    off, sweeps, conv = backend.jacobi_sweeps(m, v, 1e-14, 50)
+    assert conv
+    assert np.allclose(np.sort(np.diag(m)), np.sort(k["jac_diag"]), atol=1e-12)
+    recon = v @ np.diag(np.diag(m)) @ v.T
+    assert np.max(np.abs(recon - k["jac_in"])) < 1e-12
+
+
+def test_jacobi_nonconvergence_reports():
+    from paper_1504_05477_b200 import backend
+
+    base = _rand((40, 40), 99)
+    sym = 0.5 * (base + base.T)
+    m, v = sym.copy(), np.eye(40)
+    off, sweeps, conv = backend.jacobi_sweeps(m, v, 1e-14, 1)
+    assert not conv and sweeps == 1 and off > 0
+
+
+def test_backend_contract_kats():
+    from paper_1504_05477_b200 import backend
+
+    k = np.load(os.path.join(GOLDEN, "kernels.npz"))
+    assert np.max(np.abs(backend.mm(k["mm_a"], k["mm_b"]) - k["mm_c"])) < 1e-12
+    rows, cols = k["sp_shape"]
+    nt = backend.spmm_nt(rows, k["sp_indptr"], k["sp_col"], k["sp_val"], k["sp_bx"])
+    assert np.max(np.abs(nt - k["sp_nt"])) < 1e-12
+    t = backend.spmm_t(rows, cols, k["sp_indptr"], k["sp_col"], k["sp_val"], k["sp_by"])
+    assert np.max(np.abs(t - k["sp_t"])) < 1e-12
+    out, st = backend.gauss_fill(7, 987654321)
+    g = np.load(os.path.join(GOLDEN, "gauss_fill.npz"))
+    assert np.array_equal(out, g["fill_7"])
+
+
+def test_spmm_csr_ragged_and_empty_rows(ops):
+    rng = np.random.default_rng(0)
+    n, d = 3000, 700
+    nnz_row = rng.integers(0, 90, size=n)
+    nnz_row[::17] = 0
+    nnz_row[5] = 700  # a full row
+    indptr = np.concatenate([[0], np.cumsum(nnz_row)])
+    cols = np.concatenate([np.sort(rng.choice(d, size=c, replace=False)) for c in nnz_row])
+    vals = rng.standard_normal(indptr[-1])
+    b = rng.standard_normal((d, 37))
+    y = rng.standard_normal((n, 37))
+    got = ops.spmm_csr(_t(indptr, torch.int32), _t(cols, torch.int32), _t(vals), d, _t(b),
+                       torch.empty((n, 37), dtype=torch.float64, device="cuda")).cpu().numpy()
+    assert np.max(np.abs(got - o.spmm_nt(n, indptr, cols, vals, b))) < 1e-12
+    tp, tc, tv = ops.csr_transpose(_t(indptr, torch.int32), _t(cols, torch.int32), _t(vals), n, d)
+    got_t = ops.spmm_csr(tp, tc, tv, n, _t(y), torch.empty((d, 37), dtype=torch.float64, device="cuda"))
+    assert np.max(np.abs(got_t.cpu().numpy() - o.spmm_t(n, d, indptr, cols, vals, y))) < 1e-11
+
+
+def test_canonicalize_signs_first_max_tie(ops):
+    z = np.array([[0.5, -1.0, 0.0], [-0.5, 1.0, -0.0], [0.1, 0.2, 0.0]])
+    Z = _t(z)
+    ops.canonicalize_signs(Z)
+    ref = o.canonicalize_signs(z.copy())
+    assert np.array_equal(Z.cpu().numpy(), ref)
+    big = _rand((100000, 13), 21)
+    Z = _t(big)
+    ops.canonicalize_signs(Z)
+    assert np.array_equal(Z.cpu().numpy(), o.canonicalize_signs(big.copy()))

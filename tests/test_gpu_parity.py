@@ -1,0 +1,221 @@
+"""Path-level parity: the public drop-in API on the GPU against the
+reference's own outputs (tests/golden) and the oracle.
+
+Tolerances (north_star): FP64 top-k singular values, captured variance and
+spectral error within 1e-10 relative; FP32 path within 1e-4 relative."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import rsvd_oracle as o
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+FP64_TOL = 1e-10
+FP32_TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def rk():
+    import paper_1504_05477_b200 as rk
+
+    return rk
+
+
+def _cases():
+    c = np.load(os.path.join(GOLDEN, "cases.npz"))
+    return c, sorted({key.split("__")[0] for key in c.files})
+
+
+def _align_signs(z, ref):
+    s = np.sign(np.sum(z * ref, axis=0))
+    s[s == 0] = 1
+    return z * s
+
+
+@pytest.mark.parametrize("name", _cases()[1])
+def test_golden_cases(rk, name):
+    c, _ = _cases()
+    cfg = json.loads(str(c[f"{name}__cfg"]))
+    if f"{name}__A" in c.files:
+        A = c[f"{name}__A"]
+    else:
+        rows, cols = c[f"{name}__csr_shape"]
+        A = rk.SparseMatrixCSR(rows, cols, c[f"{name}__csr_indptr"], c[f"{name}__csr_col"], c[f"{name}__csr_val"])
+    rc = rk.RsvdConfig(k=cfg["k"], variant=cfg["variant"], p=cfg["p"], q=cfg["q"], seed=cfg["seed"],
+                       reorthonormalize_every=cfg["every"])
+    r = rk.factorize(A, rc)
+    sig = c[f"{name}__sigma"]
+    assert r.q_used == int(c[f"{name}__q_used"])
+    scale = max(sig.max(), 1e-300)
+    assert np.max(np.abs(r.approx_singular_values - sig)) <= FP64_TOL * scale, (r.approx_singular_values, sig)
+    z = r.Z.data
+    assert np.max(np.abs(z.T @ z - np.eye(z.shape[1]))) <= 1e-10
+    # Z parity only where the Ritz values are separated (else the basis of a
+    # cluster is not unique); captured variance is checked regardless.
+    Aop = o.DenseOp(A) if isinstance(A, np.ndarray) else o.CsrOp(A.rows, A.cols, A.row_ptr, A.col_idx, A.values)
+    cap = o.captured_variance(Aop, z)
+    cap_ref = o.captured_variance(Aop, c[f"{name}__Z"])
+    assert np.max(np.abs(cap - cap_ref)) <= FP64_TOL * max(cap_ref.max(), 1e-300)
+    gaps = np.abs(np.diff(sig)) / scale
+    if sig.size == 1 or gaps.min() > 1e-6:
+        assert np.max(np.abs(z - c[f"{name}__Z"])) < 1e-7
+
+
+def test_c1_fp64_parity(rk):
+    """BASELINE configs[0]: 2000x1000, sigma_i = 1/i, BK k=20 q=8 (-> 9)."""
+    g = np.load(os.path.join(GOLDEN, "c1.npz"))
+    A = o.synth_matrix(2000, 1000, 1.0 / np.arange(1, 1001), seed=0)
+    r = rk.block_krylov(A, rk.RsvdConfig(k=20, variant="bk", q=8, seed=0))
+    assert r.q_used == 9
+    rel = np.abs(r.approx_singular_values - g["sigma"]) / g["sigma"]
+    assert rel.max() < FP64_TOL, rel.max()
+    cap = o.captured_variance(A, r.Z.data)
+    assert np.max(np.abs(cap - g["captured"]) / g["captured"]) < FP64_TOL
+    spec = o.spectral_error_exact(A, r.Z.data)
+    assert abs(spec - g["spectral_exact"][0]) / g["spectral_exact"][0] < FP64_TOL
+    assert np.max(np.abs(r.Z.data - g["Z"])) < 1e-8
+
+
+def test_bitwise_determinism_and_q0_equivalence(rk):
+    A = o.gaussian(300, 220, o.SeededRng(58))
+    cfg = rk.RsvdConfig(k=7, variant="bk", q=5, seed=11)
+    z1 = rk.block_krylov(A, cfg).Z.data
+    z2 = rk.block_krylov(A, cfg).Z.data
+    assert np.array_equal(z1, z2)
+    outs = [rk.factorize(A, rk.RsvdConfig(k=4, variant=v, q=0, seed=21)).Z.data for v in ("si", "bk", "sketch")]
+    assert np.array_equal(outs[0], outs[2]) and np.array_equal(outs[1], outs[2])
+
+
+def test_validation_errors(rk):
+    with pytest.raises(ValueError):
+        rk.simultaneous_iteration(np.ones((3, 2)), rk.RsvdConfig(k=3, variant="si", q=1))
+    with pytest.raises(ValueError):
+        rk.simultaneous_iteration(np.eye(3), rk.RsvdConfig(k=1, variant="bk", q=1))
+    with pytest.raises(ValueError):
+        rk.block_krylov(o.gaussian(5, 30, o.SeededRng(55)), rk.RsvdConfig(k=5, variant="bk", q=1, p=6))
+    with pytest.raises(ValueError):
+        rk.post_process(np.eye(4), np.eye(4)[:, :2], 3)
+    with pytest.raises(ValueError):
+        rk.post_process(np.eye(4), np.ones((4, 2)), 2)
+    with pytest.raises(ValueError):
+        rk.block_krylov(np.array([[1.0, np.nan], [0.0, 1.0]]), rk.RsvdConfig(k=1, variant="bk", q=1))
+
+
+def test_width_capped_and_rank_deficient(rk):
+    A = o.gaussian(20, 12, o.SeededRng(54))
+    r = rk.block_krylov(A, rk.RsvdConfig(k=4, variant="bk", q=50, seed=8))
+    assert r.q_used == 2
+    u = o.gaussian(20, 2, o.SeededRng(68))
+    v = o.gaussian(8, 2, o.SeededRng(69))
+    r = rk.factorize(u @ v.T, rk.RsvdConfig(k=4, variant="si", q=3, seed=4))
+    z = r.Z.data
+    assert np.max(np.abs(z.T @ z - np.eye(4))) < 1e-10
+    assert r.approx_singular_values[3] < 1e-6 * r.approx_singular_values[0]
+    Z0 = rk.block_krylov(np.zeros((30, 20)), rk.RsvdConfig(k=3, variant="bk", q=3)).Z.data
+    assert np.max(np.abs(Z0.T @ Z0 - np.eye(3))) < 1e-10
+
+
+def test_clustered_deficient_krylov_fp64(rk):
+    """C4-like clustered spectrum: the Krylov basis is numerically singular
+    (the reference replaces columns); top-k must still match the oracle."""
+    clus = np.concatenate([1 - 0.001 * np.arange(1, 61), 0.5 / np.arange(61, 401)])
+    A = o.synth_matrix(1500, 400, clus, seed=3, mm=o.mm_blas)
+    ref = o.factorize(o.DenseOp(A), 30, "bk", q=7, seed=0)
+    assert len(ref.replaced) > 0
+    r = rk.block_krylov(A, rk.RsvdConfig(k=30, variant="bk", q=7, seed=0))
+    rel = np.abs(r.approx_singular_values - ref.sigma) / ref.sigma
+    assert rel.max() < FP64_TOL, rel.max()
+    cap = o.captured_variance(A, r.Z.data)
+    cap_ref = o.captured_variance(A, ref.Z)
+    assert np.max(np.abs(cap - cap_ref) / cap_ref) < FP64_TOL
+
+
+def _fp32_case(n, d, k, q, seed=0):
+    rng = np.random.default_rng(seed)
+    u, _ = np.linalg.qr(rng.standard_normal((n, d)))
+    v, _ = np.linalg.qr(rng.standard_normal((d, d)))
+    s = np.arange(1, d + 1) ** -0.5
+    A = ((u * s) @ v.T + 1e-3 * rng.standard_normal((n, d))).astype(np.float32)
+    return A
+
+
+def test_fp32_path_parity_c2_like(rk):
+    """C2-shaped (scaled down): FP32 A, i^-0.5 spectrum + 1e-3 noise, BK."""
+    A32 = _fp32_case(6000, 1200, 50, 10)
+    A64 = A32.astype(np.float64)
+    ref = o.factorize(o.DenseOp(A64), 50, "bk", q=10, seed=0)
+    r = rk.block_krylov(A32, rk.RsvdConfig(k=50, variant="bk", q=10, seed=0))
+    assert r.q_used == 11
+    rel = np.abs(r.approx_singular_values - ref.sigma) / ref.sigma
+    assert rel.max() < FP32_TOL, rel.max()
+    cap = o.captured_variance(A64, r.Z.data)
+    cap_ref = o.captured_variance(A64, ref.Z)
+    assert np.max(np.abs(cap - cap_ref) / cap_ref) < FP32_TOL
+    z = r.Z.data
+    assert np.max(np.abs(z.T @ z - np.eye(50))) <= 1e-10
+
+
+def test_fp32_si(rk):
+    A32 = _fp32_case(3000, 600, 20, 6, seed=1)
+    A64 = A32.astype(np.float64)
+    ref = o.factorize(o.DenseOp(A64), 20, "si", q=6, seed=2)
+    r = rk.simultaneous_iteration(A32, rk.RsvdConfig(k=20, variant="si", q=6, seed=2))
+    rel = np.abs(r.approx_singular_values - ref.sigma) / ref.sigma
+    assert rel.max() < FP32_TOL
+
+
+def test_implicit_centering_matches_explicit(rk):
+    """C5 semantics: the reference has no centering; its
+    oracle is the reference run on an explicitly centered FP64 matrix."""
+    rng = np.random.default_rng(5)
+    n, d = 4000, 300
+    mu = rng.uniform(-5, 5, d)
+    W, _ = np.linalg.qr(rng.standard_normal((d, d)))
+    lam = np.exp(-np.arange(1, d + 1) / 50.0)
+    X = mu + (rng.standard_normal((n, d)) * np.sqrt(lam)) @ W.T
+    Xc = X - X.mean(axis=0)
+    ref = o.factorize(o.DenseOp(Xc), 20, "bk", q=4, seed=0)
+    r = rk.block_krylov(X, rk.RsvdConfig(k=20, variant="bk", q=4, seed=0), center=True)
+    rel = np.abs(r.approx_singular_values - ref.sigma) / ref.sigma
+    assert rel.max() < 1e-9, rel.max()
+    r32 = rk.block_krylov(X.astype(np.float32), rk.RsvdConfig(k=20, variant="bk", q=4, seed=0), center=True)
+    ref32 = o.factorize(o.DenseOp(X.astype(np.float32).astype(np.float64) - X.astype(np.float32).astype(np.float64).mean(0)),
+                        20, "bk", q=4, seed=0)
+    rel = np.abs(r32.approx_singular_values - ref32.sigma) / ref32.sigma
+    assert rel.max() < FP32_TOL, rel.max()
+
+
+def test_sparse_fp32_and_fp64(rk):
+    rng = np.random.default_rng(7)
+    n, d = 5000, 2000
+    nnz_row = np.clip(np.round(rng.lognormal(np.log(30) - 0.5, 1.0, n)), 1, d).astype(int)
+    indptr = np.concatenate([[0], np.cumsum(nnz_row)])
+    cols = np.concatenate([np.sort(rng.choice(d, size=c, replace=False)) for c in nnz_row])
+    vals = rng.lognormal(0, 1, indptr[-1])
+    A = rk.SparseMatrixCSR(n, d, indptr, cols, vals)
+    ref = o.factorize(o.CsrOp(n, d, indptr, cols, vals), 10, "bk", q=5, seed=0)
+    r = rk.block_krylov(A, rk.RsvdConfig(k=10, variant="bk", q=5, seed=0))
+    rel = np.abs(r.approx_singular_values - ref.sigma) / ref.sigma
+    assert rel.max() < FP64_TOL
+    r32 = rk.block_krylov(A, rk.RsvdConfig(k=10, variant="bk", q=5, seed=0), precision="fp32")
+    rel = np.abs(r32.approx_singular_values - ref.sigma) / ref.sigma
+    assert rel.max() < FP32_TOL
+
+
+def test_torch_cuda_input_and_post_process(rk):
+    A = o.gaussian(400, 300, o.SeededRng(62))
+    q = o.mgs(o.gaussian(400, 12, o.SeededRng(63)))
+    z, s = rk.post_process(A, q, 6)
+    zr, sr = o.post_process(o.DenseOp(A), q, 6)
+    assert np.max(np.abs(s - sr) / sr) < 1e-12
+    assert np.max(np.abs(z.data - zr)) < 1e-9
+    At = torch.from_numpy(A).cuda()
+    r1 = rk.block_krylov(At, rk.RsvdConfig(k=5, variant="bk", q=3, seed=1))
+    r2 = rk.block_krylov(A, rk.RsvdConfig(k=5, variant="bk", q=3, seed=1))
+    assert np.array_equal(r1.Z.data, r2.Z.data)
