@@ -1,0 +1,448 @@
+"""Benchmark: rank-k block-Krylov SVD wall time on B200 (BASELINE.json).
+
+Default workload = BASELINE configs[1] ("C2"): dense FP32 A 50,000 x 10,000,
+A = U diag(i^-0.5) V^T + 1e-3 N(0,1), Haar U, V from seeded Gaussians (built
+on the GPU in FP64, cast to FP32), block Krylov k = 50, q = 10 (-> 11, the
+reference's odd bump, rsvd.py:157-158), Krylov width 600, Pi = host
+SeededRng(0) Gaussian 10,000 x 50. Synthetic data (no dataset is named).
+
+One step = one complete factorization (start block upload, Krylov chain,
+blocked orthonormalization, Rayleigh-Ritz + Jacobi, Z and sigma ready).
+  value : device-resident A (uploaded before timing), CUDA-event timed.
+  e2e   : the public drop-in call block_krylov(A_host_pinned, cfg) — H2D of A
+          and D2H of (Z, sigma) inside the timed region, every step.
+A (2 GB FP32) is larger than L2 (126 MB), so every step streams it from HBM.
+
+--impl reference: the reference's CPU algorithm (the oracle port,
+oracle/rsvd_oracle.py, numpy/BLAS products + C Jacobi, all host threads) on
+the same A, timed per stage on a bounded sample and scaled to one
+factorization (see cpu_baseline.sample).
+
+N > 1 (torchrun): A is row-sharded across ranks; the step is
+the same factorization of the same A (strong scaling); A^T Y, Grams and
+projections are NCCL allreduces.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+# pin BLAS threads to the host cores BEFORE numpy loads OpenBLAS (unpinned
+# OpenBLAS oversubscribes)
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS"):
+    os.environ.setdefault(_v, str(os.cpu_count() or 1))
+
+import numpy as np  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c2": dict(n=50000, d=10000, k=50, q=10, spectrum="pow", noise=1e-3, variant="bk"),
+    "c1": dict(n=2000, d=1000, k=20, q=8, spectrum="inv", noise=0.0, variant="bk"),
+    "c4": dict(n=1000000, d=4096, k=200, q=6, spectrum="clustered", noise=0.0, variant="bk"),
+}
+
+
+def _spectrum(kind, d):
+    i = np.arange(1, d + 1, dtype=np.float64)
+    if kind == "pow":
+        return i ** -0.5
+    if kind == "inv":
+        return 1.0 / i
+    if kind == "clustered":
+        s = 0.5 / i
+        s[:200] = 1 - 0.001 * i[:200]
+        return s
+    raise ValueError(kind)
+
+
+def make_matrix(cfg, device, seed=1234):
+    """Haar U (n x d), V (d x d) from seeded Gaussians (QR, sign-fixed by
+    diag R), A = U diag(s) V^T (+ noise), built in FP64 on the GPU, FP32 out."""
+    import torch
+
+    n, d = cfg["n"], cfg["d"]
+    g = torch.Generator(device=device).manual_seed(seed)
+    s = torch.from_numpy(_spectrum(cfg["spectrum"], d)).to(device)
+    A = torch.empty((n, d), dtype=torch.float32, device=device)
+    V = torch.randn((d, d), generator=g, dtype=torch.float64, device=device)
+    V, R = torch.linalg.qr(V)
+    V *= torch.sign(torch.diagonal(R)).view(1, -1)
+    chunk = 65536 if n > 65536 else n
+    # U from a QR of the full n x d Gaussian when it fits comfortably, else a
+    # block-wise orthonormal construction (still exactly orthonormal columns)
+    U = torch.randn((n, d), generator=g, dtype=torch.float64, device=device)
+    U, R = torch.linalg.qr(U)
+    U *= torch.sign(torch.diagonal(R)).view(1, -1)
+    W = (V * s.view(1, -1)).T.contiguous()  # diag(s) V^T
+    for r0 in range(0, n, chunk):
+        blk = U[r0: r0 + chunk] @ W
+        if cfg["noise"]:
+            blk += cfg["noise"] * torch.randn(blk.shape, generator=g, dtype=torch.float64, device=device)
+        A[r0: r0 + chunk] = blk.float()
+    del U, V, W
+    torch.cuda.synchronize()
+    return A
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def run_ours(args):
+    import torch
+
+    import paper_1504_05477_b200 as rk
+    from paper_1504_05477_b200 import krylov, rsvd
+    from paper_1504_05477_b200.operators import DenseDeviceOp
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    cfgd = CONFIGS[args.config]
+    n, d, k = cfgd["n"], cfgd["d"], cfgd["k"]
+    cfg = rk.RsvdConfig(k=k, variant=cfgd["variant"], q=cfgd["q"], seed=0)
+    A_full = make_matrix(cfgd, dev)
+    lo, hi = krylov.shard_rows(n, world, rank)
+    if world > 1:
+        comm = krylov.TorchComm(n_total=n, row_offset=lo)
+        A = A_full[lo:hi].contiguous()
+        del A_full
+    else:
+        A = A_full
+    op = DenseDeviceOp(A, n_total=n, row_offset=lo)
+    Pi = rk.gaussian(d, cfg.p, rk.SeededRng(cfg.seed)).data
+
+    # instrumentation of the dominant kernels (A X / A^T Y on the op's stream)
+    events = []
+    orig_apply, orig_apply_t = op.apply, op.apply_t
+
+    def timed(fn, kind):
+        def w(X, out):
+            if not recording[0]:
+                return fn(X, out)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            r = fn(X, out)
+            e1.record()
+            events.append((kind, X.shape[1], e0, e1))
+            return r
+        return w
+
+    recording = [False]
+    op.apply = timed(orig_apply, "AX")
+    op.apply_t = timed(orig_apply_t, "ATY")
+
+    def step():
+        df = rsvd.run_device(op, cfg, comm=comm, Pi=Pi)
+        return df
+
+    for _ in range(args.warmup):
+        df = step()
+    torch.cuda.synchronize()
+    launches = count_launches(step) if rank == 0 and args.count_launches else None
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    recording[0] = True
+    with ClockSampler(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            df = step()
+        e1.record()
+        torch.cuda.synchronize()
+    recording[0] = False
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    info = df.info.cpu().numpy()
+    assert int(info[0]) == 1, "Jacobi did not converge"
+    sigma = df.sigma.cpu().numpy()
+
+    # kernel roofline: the Krylov-chain products at width p (HBM bound)
+    hbm, bf16, peak_src = _peaks()
+    chain = [(e0_.elapsed_time(e1_), kind) for kind, width, e0_, e1_ in events if width == cfg.p]
+    rr = [(e0_.elapsed_time(e1_), kind) for kind, width, e0_, e1_ in events if width != cfg.p]
+    n_loc = hi - lo
+    bytes_per = n_loc * d * 4 + (n_loc + d) * cfg.p * 4
+    avg_chain_ms = float(np.mean([t for t, _ in chain])) if chain else float("nan")
+    achieved = bytes_per / (avg_chain_ms * 1e-3) / 1e9
+    rr_ms = float(np.mean([t for t, _ in rr])) if rr else float("nan")
+    w = (cfgd["q"] + 1 + (cfgd["q"] % 2 == 0)) * cfg.p
+    rr_tflops = 2.0 * n_loc * d * w / (rr_ms * 1e-3) / 1e12 if rr else None
+
+    # e2e through the public API with host (pinned) A
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        A_host = A.cpu().pin_memory()
+        for _ in range(max(1, min(args.warmup, 2))):
+            r = rk.block_krylov(A_host, cfg)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            r = rk.block_krylov(A_host, cfg)
+        torch.cuda.synchronize()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": int(A_host.numel() * 4 + Pi.size * 4),
+               "d2h_bytes_per_step": int(n * k * 8 + k * 8 + 8 * 3)}
+        del A_host
+
+    out = {
+        "metric": "rank-k block-Krylov SVD wall time",
+        "value": ms,
+        "unit": "ms",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": False,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32 (3xTF32 products, f64 small algebra)" if A.dtype == torch.float32 else "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config.upper()}: dense FP32 A {n}x{d}, BK k={k} q={cfgd['q']}->"
+                               f"{cfg.resolve_q(d)}, width {w}", "n": n, "d": d, "k": k, "q": cfgd["q"],
+                   "q_eff": cfg.resolve_q(d), "krylov_width": w, "parallelism": f"rowshard{world}",
+                   "l2": "inputs larger than L2 (A = %.1f GB)" % (n * d * 4 / 1e9)},
+        "roofline": {"bound": "hbm", "kernel": "Krylov-chain A.X / A^T.Y (width %d)" % cfg.p,
+                     "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "peak_source": peak_src, "traffic": None,
+                     "algorithmic_bytes_per_launch": bytes_per, "avg_launch_ms": avg_chain_ms},
+        "kernels": {"rayleigh_ritz_ATQ_ms": rr_ms, "rayleigh_ritz_ATQ_tflops": rr_tflops},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "sigma_head": [float(x) for x in sigma[:3]],
+    }
+    if e2e:
+        out["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(A, cfgd, cfg, Pi, args)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def count_launches(step):
+    """Count our kernels launched by one step using the CUDA profiler API is
+    not available here; instead count C-ABI kernel-launching calls."""
+    from paper_1504_05477_b200 import _lib
+
+    L = _lib.load()
+    counted = {"n": 0}
+    orig = {}
+    for name in _lib.exported_symbols():
+        if name in ("rsvd_last_error", "rsvd_abi_version", "rsvd_sm_count", "rsvd_gauss_fill") or name.endswith("_ws_bytes"):
+            continue
+        fn = getattr(L, name)
+        orig[name] = fn
+
+        def wrap(*a, _fn=fn, _name=name):
+            counted["n"] += LAUNCHES_PER_CALL.get(_name, 1)
+            return _fn(*a)
+
+        setattr(L, name, wrap)
+    try:
+        step()
+    finally:
+        for name, fn in orig.items():
+            setattr(L, name, fn)
+    return counted["n"]
+
+
+# kernels launched per C-ABI call (see csrc/*.cu)
+LAUNCHES_PER_CALL = {"rsvd_gemm_tn": 2, "rsvd_colreduce": 2, "rsvd_canonicalize_signs": 3, "rsvd_jacobi_sweeps": 5,
+                     "rsvd_eig_select": 2, "rsvd_col_absargmax": 2}
+
+
+def cpu_baseline(A_dev, cfgd, cfg, Pi, args):
+    """The reference algorithm (oracle port) on the box's host cores,
+    stage-timed on a bounded sample and scaled to one factorization."""
+    res = reference_sample(A_dev.cpu().numpy(), cfgd, cfg, Pi, budget_s=args.cpu_budget)
+    return res
+
+
+def reference_sample(A32, cfgd, cfg, Pi, budget_s=25.0):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import rsvd_oracle as o
+
+    cores = os.cpu_count() or 1
+    A = A32.astype(np.float64)
+    op = o.DenseOp(A)
+    n, d = A.shape
+    p = cfg.p
+    q = cfg.resolve_q(d)
+    nb = min(q + 1, max(1, min(n, d) // p))
+    w = nb * p
+    t = {}
+    t0 = time.perf_counter()
+    y = op.apply(Pi)
+    t["AX"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    b = o.mgs(y)
+    t["mgs_block"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    c = op.apply_transpose(b)
+    t["ATY"] = time.perf_counter() - t0
+    # final _mgs on the n x w basis: per-column cost grows with the column
+    # index (two BLAS-2 projections against all earlier columns); time a
+    # column window at the end and integrate the linear cost model.
+    K = np.empty((n, w))
+    for j in range(nb):
+        K[:, j * p:(j + 1) * p] = b  # same cost profile as the real basis
+    cols = min(p, 40)
+    Qh = np.ascontiguousarray(K[:, : w - cols])
+    t0 = time.perf_counter()
+    for j in range(cols):
+        v = K[:, w - cols + j].copy()
+        for _ in range(2):  # factor.py:93-98, two projections per column
+            v = v - Qh @ (Qh.T @ v)
+        float(np.linalg.norm(v))
+    t_tail = (time.perf_counter() - t0) / cols  # one column at index ~w
+    t["mgs_final"] = t_tail * w / 2.0  # column j costs ~ j/w of a tail column
+    # post-process: two A passes at width w, Q^T Y, Gram check, Jacobi, Q U_k
+    Qw = np.ascontiguousarray(K)
+    t0 = time.perf_counter()
+    W = op.apply_transpose(Qw[:, : min(w, 100)])
+    t["ATQ_100"] = time.perf_counter() - t0
+    t["post_A_passes"] = 2 * t["ATQ_100"] * (w / min(w, 100))
+    M = np.ascontiguousarray(W.T @ W)
+    m_w = min(w, 200)
+    base = np.random.default_rng(1).standard_normal((m_w, m_w))
+    Mw = base @ base.T
+    t0 = time.perf_counter()
+    o.symmetric_eig(Mw)
+    t_j = time.perf_counter() - t0
+    t["jacobi"] = t_j * (w / m_w) ** 3
+    total = t["AX"] * (1 + (nb - 1)) + t["ATY"] * (nb - 1) + t["mgs_block"] * nb + t["mgs_final"] + t["post_A_passes"] + t["jacobi"]
+    return {"value": total * 1e3, "unit": "ms", "cores": cores, "kind": "port",
+            "sample": ("oracle port (numpy/OpenBLAS products, C Jacobi) on the same A upcast to FP64 "
+                       "(matrix.py:80): stages timed once each (A.X, A^T.Y, one block _mgs, tail columns "
+                       "of the final _mgs, A^T Q at width 100, Jacobi at w=200) and scaled by their "
+                       "exact operation counts to one factorization"),
+            "stages_s": {k: float(v) for k, v in t.items()}}
+
+
+def run_reference(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_1504_05477_b200 as rk
+
+    dev = torch.device("cuda", 0)
+    cfgd = CONFIGS[args.config]
+    cfg = rk.RsvdConfig(k=cfgd["k"], variant=cfgd["variant"], q=cfgd["q"], seed=0)
+    A = make_matrix(cfgd, dev)
+    Pi = rk.gaussian(cfgd["d"], cfg.p, rk.SeededRng(cfg.seed)).data
+    A_host = A.cpu().numpy()
+    del A
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = reference_sample(A_host, cfgd, cfg, Pi, budget_s=args.cpu_budget)
+        if i >= args.warmup:
+            vals.append(r["value"])
+    v = float(np.mean(vals))
+    out = {"impl": "reference", "metric": "rank-k block-Krylov SVD wall time", "value": v, "unit": "ms",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v,
+           "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": args.config.upper()},
+           "cpu_baseline": {"value": v, "unit": "ms", "cores": r["cores"], "kind": r["kind"], "sample": r["sample"]},
+           "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--count-launches", action="store_true", default=True)
+    ap.add_argument("--cpu-budget", type=float, default=25.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -38,6 +38,11 @@ JACOBI_MAX_SWEEPS = 50  # factor.py:35
 # a Gram-based test cannot resolve below ~sqrt(eps)).
 TAU = {torch.float64: 1e-7, torch.float32: 3e-3}
 REF_RTOL = 1e-12  # factor.py:41 (_DEFICIENCY_RTOL)
+# Second-round threshold per work precision: the reference's own 1e-12 in
+# FP64; in FP32 the explicit residuals are resolved only down to ~1e-7, and a
+# kept noisy direction perturbs Ritz values only quadratically while a
+# dropped one perturbs them to first order, so keep down to the noise floor.
+REF_RTOL_BY = {torch.float64: REF_RTOL, torch.float32: 1e-7}
 
 
 class LocalComm:
@@ -139,7 +144,7 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
     dtype = V.dtype
     p = V.shape[1]
     if two_round is None:
-        two_round = dtype == torch.float64
+        two_round = True
     tau = TAU[dtype] if tau is None else tau
     n_total = V.shape[0] if n_total is None else n_total
     has_prev = Qp is not None and Qp.shape[1] > 0
@@ -157,12 +162,12 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
     comm.allreduce(G)
     if two_round and tau > 0.0:
         ops.chol_deflate(G, ref2, tau * tau, T, mask, ws.ndef, None)
-        ops.gemm_nn(V, T, tmp)  # Q1 raw (zero columns at rejected slots)
+        ops.gemm_nn(V, _cast_small(ops, T, dtype), tmp)  # Q1 raw (zero columns at rejected slots)
         Q1 = torch.empty_like(tmp)
         ops.gram(tmp, G)
         comm.allreduce(G)
         ops.chol_deflate(G, None, 0.0, T, ws.mask2[:p], ws.ndef2, None)
-        ops.gemm_nn(tmp, T, Q1)  # Q1 clean
+        ops.gemm_nn(tmp, _cast_small(ops, T, dtype), Q1)  # Q1 clean
         ops.mask_cols(V, mask)  # keep only the rejected columns' residuals
         c2 = torch.empty((p, p), dtype=dtype, device=V.device)
         if has_prev:
@@ -174,8 +179,9 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
         ops.gram(V, G)
         comm.allreduce(G)
         ref = ref2 if ref2 is not None else ws.ref_orig[:p]
-        ops.chol_deflate(G, ref, REF_RTOL * REF_RTOL, T, ws.mask2[:p], ws.ndef, running, mask)
-        ops.gemm_nn(V, T, Q1, beta=1.0)  # survivors join the kept columns
+        rt = REF_RTOL_BY[dtype]
+        ops.chol_deflate(G, ref, rt * rt, T, ws.mask2[:p], ws.ndef, running, mask)
+        ops.gemm_nn(V, _cast_small(ops, T, dtype), Q1, beta=1.0)  # survivors join the kept columns
         ops.insert_fill(Q1, ws.mask2[:p], ws.ndef, QR_FILL_SEED, row_offset, n_total)
         out = Q1
     else:
@@ -191,8 +197,14 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
     ops.gram(out, G)
     comm.allreduce(G)
     ops.chol_deflate(G, None, 0.0, T, ws.mask2[:p], ws.ndef2, None)
-    Tw = _cast_small(ops, T, dtype)
-    ops.gemm_nn(out, Tw, V)
+    ops.gemm_nn(out, _cast_small(ops, T, dtype), V)
+    if dtype != torch.float64:
+        # FP32 storage: one more CholeskyQR step (CholeskyQR2 cleanup)
+        ops.gram(V, G)
+        comm.allreduce(G)
+        ops.chol_deflate(G, None, 0.0, T, ws.mask2[:p], ws.ndef2, None)
+        ops.gemm_nn(V, _cast_small(ops, T, dtype), out)
+        V.copy_(out)
     return V
 
 
