@@ -535,7 +535,8 @@ int gemm_nn_tc(int64_t m, int64_t n, int64_t k, double alpha, const float* A, in
 bool gemm_tc_tn_supported(int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, const void* A, const void* B) {
     (void)ldb; (void)B;
     if (getenv("RSVD_DISABLE_TC")) return false;
-    return k >= BM && m >= BK && n >= 1 && (lda % 4) == 0 && aligned16(A) && m < (1ll << 31) && k < (1ll << 31);
+    // any output height: the A^T tile rows past k are TMA zero-fill
+    return k >= 8 && m >= BK && n >= 1 && (lda % 4) == 0 && aligned16(A) && m < (1ll << 31) && k < (1ll << 31);
 }
 
 int64_t gemm_tn_tc_ws_bytes(int64_t m, int64_t n, int64_t k) {

@@ -32,17 +32,27 @@ __device__ __forceinline__ int64_t tri_off(int64_t p, int64_t i, int64_t j) {
     return i * p - (i * (i - 1)) / 2 + (j - i);
 }
 
-constexpr int kCholThreads = 1024;
+constexpr int kCholThreads = 256;
 
+// One CTA. R (upper triangle, packed) lives in shared memory; T = R^{-1} in
+// shared memory too when it fits (else it is built in place in global T).
+// Right-looking Cholesky (p sequential column steps), then T by rows from
+// the bottom: T[a][c] = -(sum_{b=a+1..c} R[a][b] T[b][c]) / R[a][a], all c in
+// parallel per row a.
 __global__ void __launch_bounds__(kCholThreads)
 k_chol_deflate(int64_t p, const double* __restrict__ G, int64_t ldg,
                const double* __restrict__ ref2, double tau2, double* __restrict__ T, int64_t ldt,
                int32_t* __restrict__ mask, int32_t* __restrict__ ndef, int32_t* __restrict__ running,
-               const int32_t* __restrict__ active, double* gws, int use_smem) {
+               const int32_t* __restrict__ active, double* gws, int use_smem, int t_in_smem) {
     extern __shared__ double smem_d[];
     double* S = use_smem ? smem_d : gws;
+    const int64_t tri = p * (p + 1) / 2;
+    double* Ts = t_in_smem ? smem_d + tri : nullptr;
+    const int64_t ldT = t_in_smem ? p : ldt;
+    double* Tw = t_in_smem ? Ts : T;
     __shared__ int s_def;
     __shared__ int s_count;
+    __shared__ double s_rjj;
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     for (int64_t i = warp; i < p; i += nwarps)
@@ -51,66 +61,68 @@ k_chol_deflate(int64_t p, const double* __restrict__ G, int64_t ldg,
     __syncthreads();
     for (int64_t j = 0; j < p; ++j) {
         if (tid == 0) {
-            double d = S[tri_off(p, j, j)];
-            double r = ref2 ? ref2[j] : G[j * ldg + j];
+            const double d = S[tri_off(p, j, j)];
+            const double r = ref2 ? ref2[j] : G[j * ldg + j];
             const int act = active ? active[j] : 1;
-            int def = !act || !(d > tau2 * r) || !(d > 0.0);
+            const int def = !act || !(d > tau2 * r) || !(d > 0.0);
             s_def = def;
             mask[j] = def ? (act ? 1 : 2) : 0;  // 2 = inactive slot (not counted)
             if (def && act) ++s_count;
+            const double rjj = def ? 1.0 : sqrt(d);
+            s_rjj = rjj;
+            S[tri_off(p, j, j)] = rjj;
         }
         __syncthreads();
         const int def = s_def;
+        const double inv = 1.0 / s_rjj;
+        for (int64_t c = j + 1 + tid; c < p; c += blockDim.x) {
+            const int64_t o = tri_off(p, j, c);
+            S[o] = def ? 0.0 : S[o] * inv;
+        }
+        __syncthreads();
         if (!def) {
-            const double rjj = sqrt(S[tri_off(p, j, j)]);
-            const double inv = 1.0 / rjj;
-            for (int64_t c = j + 1 + tid; c < p; c += blockDim.x) S[tri_off(p, j, c)] *= inv;
-            __syncthreads();
-            if (tid == 0) S[tri_off(p, j, j)] = rjj;
-            // trailing update, warp per row
+            // trailing update of the packed upper triangle, warp per row
             for (int64_t a = j + 1 + warp; a < p; a += nwarps) {
                 const double ra = S[tri_off(p, j, a)];
-                for (int64_t b = a + lane; b < p; b += 32) S[tri_off(p, a, b)] -= ra * S[tri_off(p, j, b)];
+                const int64_t rowa = tri_off(p, a, a) - a, rowj = tri_off(p, j, 0);
+                for (int64_t b = a + lane; b < p; b += 32) S[rowa + b] -= ra * S[rowj + b];
             }
-        } else {
-            for (int64_t c = j + 1 + tid; c < p; c += blockDim.x) S[tri_off(p, j, c)] = 0.0;
             __syncthreads();
-            if (tid == 0) S[tri_off(p, j, j)] = 1.0;
+        }
+    }
+    // T = R^{-1}, rows from the bottom
+    for (int64_t a = p - 1; a >= 0; --a) {
+        const double raa = S[tri_off(p, a, a)];
+        const int64_t rowa = tri_off(p, a, a) - a;
+        for (int64_t c = tid; c < p; c += blockDim.x) {
+            double v;
+            if (c < a) {
+                v = 0.0;
+            } else if (c == a) {
+                v = 1.0 / raa;
+            } else {
+                double acc = 0.0;
+                for (int64_t b = a + 1; b <= c; ++b) acc += S[rowa + b] * Tw[b * ldT + c];
+                v = -acc / raa;
+            }
+            Tw[a * ldT + c] = v;
         }
         __syncthreads();
     }
+    // zero row+column of deficient / inactive slots (rows already e_j), copy out
+    for (int64_t e = tid; e < p * p; e += blockDim.x) {
+        const int64_t i = e / p, c = e % p;
+        double v = Tw[i * ldT + c];
+        if (mask[i] || mask[c]) v = 0.0;
+        T[i * ldt + c] = v;
+    }
+    __syncthreads();
     if (tid == 0) {
         const int32_t base = running ? running[0] : 0;
         ndef[0] = s_count;
         ndef[1] = base;
         if (running) running[0] = base + s_count;
     }
-    // Inverse by columns: T(:, c) solves R x = e_c (back substitution), one warp
-    // per column, lanes split the dot products.
-    for (int64_t c = warp; c < p; c += nwarps) {
-        double* Tc = T;  // column c of T, row stride ldt
-        for (int64_t a = c + 1 + lane; a < p; a += 32) Tc[a * ldt + c] = 0.0;
-        const double xc = 1.0 / S[tri_off(p, c, c)];
-        if (lane == 0) Tc[c * ldt + c] = xc;
-        __syncwarp();
-        for (int64_t a = c - 1; a >= 0; --a) {
-            double acc = 0.0;
-            for (int64_t b = a + 1 + lane; b <= c; b += 32) acc += S[tri_off(p, a, b)] * Tc[b * ldt + c];
-            acc = warp_sum(acc);
-            if (lane == 0) Tc[a * ldt + c] = -acc / S[tri_off(p, a, a)];
-            __syncwarp();
-        }
-    }
-    __syncthreads();
-    // zero row+column of deficient / inactive slots (rows already e_j)
-    for (int64_t j = warp; j < p; j += nwarps) {
-        if (!mask[j]) continue;
-        for (int64_t a = lane; a < p; a += 32) {
-            T[a * ldt + j] = 0.0;
-            T[j * ldt + a] = 0.0;
-        }
-    }
-    __syncthreads();
     for (int64_t j = tid; j < p; j += blockDim.x)
         if (mask[j] == 2) mask[j] = 0;
 }
@@ -336,19 +348,22 @@ __global__ void k_eig_gather(int64_t w, int64_t k, const int32_t* __restrict__ o
 
 int64_t chol_deflate_ws_bytes(int64_t p) { return (p * (p + 1) / 2) * (int64_t)sizeof(double); }
 
-int chol_deflate(int64_t p, const double* G, int64_t ldg, const double* ref2, double tau2,
-                 double* T, int64_t ldt, int32_t* mask, int32_t* ndef, int32_t* running,
-                 const int32_t* active, void* ws, int64_t ws_bytes, cudaStream_t st) {
+int chol_deflate(int64_t p, const double* G, int64_t ldg, const double* ref2, double tau2, double* T,
+                 int64_t ldt, int32_t* mask, int32_t* ndef, int32_t* running, const int32_t* active, void* ws,
+                 int64_t ws_bytes, cudaStream_t st) {
     if (p == 0) return RSVD_OK;
-    int64_t bytes = chol_deflate_ws_bytes(p);
-    int use_smem = bytes <= 200 * 1024;
-    if (!use_smem) RSVD_REQUIRE(ws && ws_bytes >= bytes, "chol_deflate: workspace too small");
-    size_t sm = use_smem ? (size_t)bytes : 0;
+    const int64_t rbytes = chol_deflate_ws_bytes(p);
+    const int64_t tbytes = p * p * (int64_t)sizeof(double);
+    const int64_t cap = 200 * 1024;
+    int use_smem = rbytes <= cap;
+    int t_in_smem = use_smem && rbytes + tbytes <= cap;
+    if (!use_smem) RSVD_REQUIRE(ws && ws_bytes >= rbytes, "chol_deflate: workspace too small");
+    size_t sm = (size_t)((use_smem ? rbytes : 0) + (t_in_smem ? tbytes : 0));
     if (sm > 48 * 1024)
         RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_chol_deflate, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)sm));
-    k_chol_deflate<<<1, kCholThreads, sm, st>>>(p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running,
-                                                active, (double*)ws, use_smem);
+    k_chol_deflate<<<1, kCholThreads, sm, st>>>(p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active,
+                                                (double*)ws, use_smem, t_in_smem);
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }
@@ -357,8 +372,7 @@ static int64_t jac_W2(int64_t n) { return n + (n & 1); }
 
 int64_t jacobi_ws_bytes(int64_t n) {
     int64_t W2 = jac_W2(n);
-    int64_t b = 2 * W2 * W2 + 2 * n * W2 + 1024;  // doubles
-    return b * (int64_t)sizeof(double) + 64;
+    return (2 * W2 * W2 + 2 * n * W2 + 1024) * (int64_t)sizeof(double) + 64;
 }
 
 int jacobi_sweeps(int64_t n, double* M, int64_t ldm, double* V, int64_t ldv, double tol,
