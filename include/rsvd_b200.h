@@ -23,6 +23,10 @@
  *     (thread-local).
  *   - Results are bitwise deterministic for a fixed device model, shape and
  *     stream: every reduction has a fixed order; no floating-point atomics.
+ *   - `pred` (nullable, device int32): when given, the operation's kernels
+ *     run only if *pred != 0 and are otherwise no-ops. This lets the host
+ *     enqueue data-dependent steps (the second deflation round) without a
+ *     host synchronisation, so a whole factorization can be one CUDA graph.
  */
 #ifndef RSVD_B200_H
 #define RSVD_B200_H
@@ -77,12 +81,12 @@ int rsvd_gauss_fill(int64_t count, uint64_t state, double *out, uint64_t *new_st
  *   out_dtype may differ from dtype (FP32 inputs, FP64 Gram/projection). */
 int rsvd_gemm_nn(int dtype, int64_t m, int64_t n, int64_t k, double alpha, const void *A,
                  int64_t lda, const void *B, int64_t ldb, double beta, void *C, int64_t ldc,
-                 const double *row_sub, int algo, void *stream);
+                 const double *row_sub, int algo, const int32_t *pred, void *stream);
 int64_t rsvd_gemm_tn_ws_bytes(int dtype, int64_t m, int64_t n, int64_t k, int algo);
 int rsvd_gemm_tn(int dtype, int out_dtype, int64_t m, int64_t n, int64_t k, double alpha,
                  const void *A, int64_t lda, const void *B, int64_t ldb, double beta, void *C,
                  int64_t ldc, const double *mu, const double *colsum_b, void *ws,
-                 int64_t ws_bytes, int algo, void *stream);
+                 int64_t ws_bytes, int algo, const int32_t *pred, void *stream);
 
 /* ---- 3. Sparse products --------------------------------------------------
  * Replace spmm_nt (_kernels.pyx:74-92) and spmm_t (_kernels.pyx:95-113).
@@ -118,10 +122,11 @@ int rsvd_csr_transpose(int dtype, int idx64, int64_t nrows, int64_t ncols, int64
 int64_t rsvd_chol_deflate_ws_bytes(int64_t p);
 int rsvd_chol_deflate(int64_t p, const double *G, int64_t ldg, const double *ref2, double tau2,
                       double *Tinv, int64_t ldt, int32_t *mask, int32_t *ndef, int32_t *running,
-                      const int32_t *active, void *ws, int64_t ws_bytes, void *stream);
+                      const int32_t *active, void *ws, int64_t ws_bytes, const int32_t *pred,
+                      void *stream);
 /* X[:, j] = 0 where keep[j] == 0. */
 int rsvd_mask_cols(int dtype, int64_t n, int64_t p, void *X, int64_t ldx, const int32_t *keep,
-                   void *stream);
+                   const int32_t *pred, void *stream);
 /* Replacement columns: X[:, j] = fill vector number (ndef[1] + r_j) for every
  * deficient slot j (r_j = deficient slots before j), rows row_offset ..
  * row_offset+n-1 of an n_total-long vector (row-sharded A), generated on the device
@@ -132,7 +137,7 @@ int rsvd_mask_cols(int dtype, int64_t n, int64_t p, void *X, int64_t ldx, const 
  * FP64) for pinning against the host stream. */
 int rsvd_insert_fill(int dtype, int64_t n, int64_t p, void *X, int64_t ldx, const int32_t *mask,
                      const int32_t *ndef, uint64_t seed, int64_t row_offset, int64_t n_total,
-                     void *stream);
+                     const int32_t *pred, void *stream);
 int rsvd_fill_stream(int64_t n, int64_t nvec, uint64_t seed, double *out, void *stream);
 
 /* ---- 5. Symmetric eigensolver (replaces jacobi_sweeps, _kernels.pyx:127-192,
@@ -156,6 +161,18 @@ int rsvd_eig_select(int64_t w, const double *Mdiag_src, int64_t ldm, const doubl
                     int64_t k, double *evals, double *evecs, int64_t lde, int32_t *order_ws,
                     void *stream);
 
+/* Top-k eigenpairs of a symmetric w x w FP64 matrix for the Rayleigh-Ritz
+ * step of post_process (rsvd.py:217-220 consumes only the top k): Householder
+ * tridiagonalisation (one cooperative kernel), Sturm multisection for the k
+ * largest eigenvalues, inverse iteration with in-cluster
+ * re-orthogonalisation, back-transformation (LAPACK dsyevx structure).
+ * evals: k values, descending; evecs: w x k row-major (column i pairs with
+ * evals[i], sign arbitrary); info[0] = 1 on success, 0 if an eigenvector
+ * iteration broke down (host maps to ConvergenceError). M is not modified. */
+int64_t rsvd_syev_topk_ws_bytes(int64_t w, int64_t k);
+int rsvd_syev_topk(int64_t w, const double *M, int64_t ldm, int64_t k, double *evals, double *evecs,
+                   int64_t lde, int32_t *info, void *ws, int64_t ws_bytes, void *stream);
+
 /* ---- 6. Element-wise / reductions (all deterministic) -------------------- */
 int64_t rsvd_colreduce_ws_bytes(int64_t n, int64_t p);
 /* out[j] = sum_i X[i][j]^2 (square=1) or sum_i X[i][j] (square=0), FP64. */
@@ -176,7 +193,7 @@ int rsvd_col_absargmax(int dtype, int64_t n, int64_t k, const void *X, int64_t l
 int rsvd_flip_by_sign(int dtype, int64_t n, int64_t k, void *X, int64_t ldx,
                       const double *sign_val, void *stream);
 int rsvd_convert(int src_dtype, int dst_dtype, int64_t rows, int64_t cols, const void *src,
-                 int64_t lds, void *dst, int64_t ldd, void *stream);
+                 int64_t lds, void *dst, int64_t ldd, const int32_t *pred, void *stream);
 /* out[i] = sqrt(max(in[i], 0)) (rsvd.py:220). */
 int rsvd_sqrt_clip(int64_t k, const double *in, double *out, void *stream);
 /* max |G - I| of a k x k FP64 matrix -> out[0] (rsvd.py:182-185). */

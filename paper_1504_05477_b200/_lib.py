@@ -23,26 +23,28 @@ _SIGS = {
     "rsvd_abi_version": ([], _int),
     "rsvd_sm_count": ([], _int),
     "rsvd_gauss_fill": ([_i64, _u64, _vp, ctypes.POINTER(_u64)], _int),
-    "rsvd_gemm_nn": ([_int, _i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64, _vp, _int, _vp], _int),
+    "rsvd_gemm_nn": ([_int, _i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64, _vp, _int, _vp, _vp], _int),
     "rsvd_gemm_tn_ws_bytes": ([_int, _i64, _i64, _i64, _int], _i64),
     "rsvd_gemm_tn": ([_int, _int, _i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64, _vp, _vp, _vp,
-                      _i64, _int, _vp], _int),
+                      _i64, _int, _vp, _vp], _int),
     "rsvd_spmm_csr": ([_int, _int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _i64, _vp], _int),
     "rsvd_csr_transpose": ([_int, _int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _int),
     "rsvd_chol_deflate_ws_bytes": ([_i64], _i64),
-    "rsvd_chol_deflate": ([_i64, _vp, _i64, _vp, _dbl, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp], _int),
-    "rsvd_mask_cols": ([_int, _i64, _i64, _vp, _i64, _vp, _vp], _int),
-    "rsvd_insert_fill": ([_int, _i64, _i64, _vp, _i64, _vp, _vp, _u64, _i64, _i64, _vp], _int),
+    "rsvd_chol_deflate": ([_i64, _vp, _i64, _vp, _dbl, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp], _int),
+    "rsvd_mask_cols": ([_int, _i64, _i64, _vp, _i64, _vp, _vp, _vp], _int),
+    "rsvd_insert_fill": ([_int, _i64, _i64, _vp, _i64, _vp, _vp, _u64, _i64, _i64, _vp, _vp], _int),
     "rsvd_fill_stream": ([_i64, _i64, _u64, _vp, _vp], _int),
     "rsvd_jacobi_ws_bytes": ([_i64], _i64),
     "rsvd_jacobi_sweeps": ([_i64, _vp, _i64, _vp, _i64, _dbl, _int, _vp, _vp, _vp, _i64, _vp], _int),
     "rsvd_eig_select": ([_i64, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _vp], _int),
+    "rsvd_syev_topk_ws_bytes": ([_i64, _i64], _i64),
+    "rsvd_syev_topk": ([_i64, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp], _int),
     "rsvd_colreduce_ws_bytes": ([_i64, _i64], _i64),
     "rsvd_colreduce": ([_int, _int, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp], _int),
     "rsvd_canonicalize_signs": ([_int, _i64, _i64, _vp, _i64, _vp, _i64, _vp], _int),
     "rsvd_col_absargmax": ([_int, _i64, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _i64, _vp], _int),
     "rsvd_flip_by_sign": ([_int, _i64, _i64, _vp, _i64, _vp, _vp], _int),
-    "rsvd_convert": ([_int, _int, _i64, _i64, _vp, _i64, _vp, _i64, _vp], _int),
+    "rsvd_convert": ([_int, _int, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp], _int),
     "rsvd_sqrt_clip": ([_i64, _vp, _vp, _vp], _int),
     "rsvd_ortho_error": ([_i64, _vp, _i64, _vp, _vp], _int),
 }

@@ -8,15 +8,19 @@ namespace rsvd {
 int64_t chol_deflate_ws_bytes(int64_t p);
 int chol_deflate(int64_t p, const double* G, int64_t ldg, const double* ref2, double tau2,
                  double* T, int64_t ldt, int32_t* mask, int32_t* ndef, int32_t* running,
-                 const int32_t* active, void* ws, int64_t ws_bytes, cudaStream_t st);
+                 const int32_t* active, void* ws, int64_t ws_bytes, const int32_t* pred, cudaStream_t st);
 int mask_cols(int dtype, int64_t n, int64_t p, void* X, int64_t ldx, const int32_t* keep,
-              cudaStream_t st);
+              const int32_t* pred, cudaStream_t st);
 int64_t jacobi_ws_bytes(int64_t n);
 int jacobi_sweeps(int64_t n, double* M, int64_t ldm, double* V, int64_t ldv, double tol,
                   int max_sweeps, int32_t* info, double* off_out, void* ws, int64_t ws_bytes,
                   cudaStream_t st);
 int eig_select(int64_t w, const double* M, int64_t ldm, const double* V, int64_t ldv, int64_t k,
                double* evals, double* evecs, int64_t lde, void* order_ws, cudaStream_t st);
+// syev.cu
+int64_t syev_topk_ws_bytes(int64_t w, int64_t k);
+int syev_topk(int64_t w, const double* M, int64_t ldm, int64_t k, double* evals, double* evecs, int64_t lde,
+              int32_t* info, void* ws, int64_t ws_bytes, cudaStream_t st);
 // elementwise.cu
 int64_t colreduce_ws_bytes(int64_t n, int64_t p);
 int colreduce(int dtype, int square, int64_t n, int64_t p, const void* X, int64_t ldx,
@@ -24,7 +28,7 @@ int colreduce(int dtype, int square, int64_t n, int64_t p, const void* X, int64_
 int canonicalize_signs(int dtype, int64_t n, int64_t k, void* X, int64_t ldx, void* ws,
                        int64_t ws_bytes, cudaStream_t st);
 int convert(int sd, int dd, int64_t rows, int64_t cols, const void* src, int64_t lds, void* dst,
-            int64_t ldd, cudaStream_t st);
+            int64_t ldd, const int32_t* pred, cudaStream_t st);
 int sqrt_clip(int64_t k, const double* in, double* out, cudaStream_t st);
 int col_absargmax(int dtype, int64_t n, int64_t k, const void* X, int64_t ldx, int64_t row_offset,
                   double* out_val, int64_t* out_idx, void* ws, int64_t ws_bytes, cudaStream_t st);
@@ -33,7 +37,7 @@ int flip_by_sign(int dtype, int64_t n, int64_t k, void* X, int64_t ldx, const do
 int ortho_error(int64_t k, const double* G, int64_t ldg, double* out, cudaStream_t st);
 int insert_fill(int dtype, int64_t n, int64_t p, void* X, int64_t ldx, const int32_t* mask,
                 const int32_t* ndef, uint64_t seed, int64_t row_offset, int64_t n_total,
-                cudaStream_t st);
+                const int32_t* pred, cudaStream_t st);
 int fill_stream(int64_t n, int64_t nvec, uint64_t seed, double* out, cudaStream_t st);
 // sparse.cu
 int spmm_csr(int dtype, int idx64, int64_t nrows, int64_t ncols, int64_t nb, const void* indptr,
@@ -52,7 +56,7 @@ extern "C" {
 
 int rsvd_gemm_nn(int dtype, int64_t m, int64_t n, int64_t k, double alpha, const void* A,
                  int64_t lda, const void* B, int64_t ldb, double beta, void* C, int64_t ldc,
-                 const double* row_sub, int algo, void* stream) {
+                 const double* row_sub, int algo, const int32_t* pred, void* stream) {
     RSVD_REQUIRE(valid_dtype(dtype), "gemm_nn: bad dtype %d", dtype);
     RSVD_REQUIRE(m >= 0 && n >= 0 && k >= 0, "gemm_nn: negative dimension");
     RSVD_REQUIRE(lda >= k && ldb >= n && ldc >= n, "gemm_nn: leading dimension too small");
@@ -63,9 +67,9 @@ int rsvd_gemm_nn(int dtype, int64_t m, int64_t n, int64_t k, double alpha, const
         RSVD_REQUIRE(gemm_tc_nn_supported(m, n, k, lda, ldb, ldc, A, B),
                      "gemm_nn: shape/alignment not supported by the tcgen05 kernel");
         return gemm_nn_tc(m, n, k, alpha, (const float*)A, lda, (const float*)B, ldb, beta,
-                          (float*)C, ldc, row_sub, st);
+                          (float*)C, ldc, row_sub, pred, st);
     }
-    return gemm_nn_simt(dtype, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, row_sub, st);
+    return gemm_nn_simt(dtype, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, row_sub, pred, st);
 }
 
 int64_t rsvd_gemm_tn_ws_bytes(int dtype, int64_t m, int64_t n, int64_t k, int algo) {
@@ -80,7 +84,7 @@ int64_t rsvd_gemm_tn_ws_bytes(int dtype, int64_t m, int64_t n, int64_t k, int al
 int rsvd_gemm_tn(int dtype, int out_dtype, int64_t m, int64_t n, int64_t k, double alpha,
                  const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C,
                  int64_t ldc, const double* mu, const double* colsum_b, void* ws,
-                 int64_t ws_bytes, int algo, void* stream) {
+                 int64_t ws_bytes, int algo, const int32_t* pred, void* stream) {
     RSVD_REQUIRE(valid_dtype(dtype) && valid_dtype(out_dtype), "gemm_tn: bad dtype");
     RSVD_REQUIRE(m >= 0 && n >= 0 && k >= 0, "gemm_tn: negative dimension");
     RSVD_REQUIRE(lda >= k && ldb >= n && ldc >= n, "gemm_tn: leading dimension too small");
@@ -92,10 +96,10 @@ int rsvd_gemm_tn(int dtype, int out_dtype, int64_t m, int64_t n, int64_t k, doub
         RSVD_REQUIRE(gemm_tc_tn_supported(m, n, k, lda, ldb, A, B),
                      "gemm_tn: shape/alignment not supported by the tcgen05 kernel");
         return gemm_tn_tc(out_dtype, m, n, k, alpha, (const float*)A, lda, (const float*)B, ldb,
-                          beta, C, ldc, mu, colsum_b, ws, ws_bytes, st);
+                          beta, C, ldc, mu, colsum_b, ws, ws_bytes, pred, st);
     }
     return gemm_tn_simt(dtype, out_dtype, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, mu,
-                        colsum_b, ws, ws_bytes, st);
+                        colsum_b, ws, ws_bytes, pred, st);
 }
 
 int rsvd_spmm_csr(int dtype, int idx64, int64_t nrows, int64_t ncols, int64_t nb,
@@ -121,24 +125,25 @@ int64_t rsvd_chol_deflate_ws_bytes(int64_t p) { return chol_deflate_ws_bytes(p);
 
 int rsvd_chol_deflate(int64_t p, const double* G, int64_t ldg, const double* ref2, double tau2,
                       double* Tinv, int64_t ldt, int32_t* mask, int32_t* ndef, int32_t* running,
-                      const int32_t* active, void* ws, int64_t ws_bytes, void* stream) {
+                      const int32_t* active, void* ws, int64_t ws_bytes, const int32_t* pred,
+                      void* stream) {
     RSVD_REQUIRE(p >= 0 && ldg >= p && ldt >= p, "chol_deflate: bad shape");
     return chol_deflate(p, G, ldg, ref2, tau2, Tinv, ldt, mask, ndef, running, active, ws, ws_bytes,
-                        as_stream(stream));
+                        pred, as_stream(stream));
 }
 
 int rsvd_mask_cols(int dtype, int64_t n, int64_t p, void* X, int64_t ldx, const int32_t* keep,
-                   void* stream) {
+                   const int32_t* pred, void* stream) {
     RSVD_REQUIRE(valid_dtype(dtype) && ldx >= p, "mask_cols: bad args");
-    return mask_cols(dtype, n, p, X, ldx, keep, as_stream(stream));
+    return mask_cols(dtype, n, p, X, ldx, keep, pred, as_stream(stream));
 }
 
 int rsvd_insert_fill(int dtype, int64_t n, int64_t p, void* X, int64_t ldx, const int32_t* mask,
                      const int32_t* ndef, uint64_t seed, int64_t row_offset, int64_t n_total,
-                     void* stream) {
+                     const int32_t* pred, void* stream) {
     RSVD_REQUIRE(valid_dtype(dtype) && ldx >= p, "insert_fill: bad args");
     RSVD_REQUIRE(row_offset >= 0 && n_total >= row_offset + n, "insert_fill: bad row range");
-    return insert_fill(dtype, n, p, X, ldx, mask, ndef, seed, row_offset, n_total,
+    return insert_fill(dtype, n, p, X, ldx, mask, ndef, seed, row_offset, n_total, pred,
                        as_stream(stream));
 }
 
@@ -163,6 +168,14 @@ int rsvd_eig_select(int64_t w, const double* M, int64_t ldm, const double* V, in
                     void* stream) {
     RSVD_REQUIRE(w >= 1 && k >= 0 && k <= w && lde >= k, "eig_select: bad shape");
     return eig_select(w, M, ldm, V, ldv, k, evals, evecs, lde, order_ws, as_stream(stream));
+}
+
+int64_t rsvd_syev_topk_ws_bytes(int64_t w, int64_t k) { return syev_topk_ws_bytes(w, k); }
+
+int rsvd_syev_topk(int64_t w, const double* M, int64_t ldm, int64_t k, double* evals, double* evecs,
+                   int64_t lde, int32_t* info, void* ws, int64_t ws_bytes, void* stream) {
+    RSVD_REQUIRE(w >= 1 && k >= 1 && k <= w && ldm >= w && lde >= k, "syev_topk: bad shape");
+    return syev_topk(w, M, ldm, k, evals, evecs, lde, info, ws, ws_bytes, as_stream(stream));
 }
 
 int64_t rsvd_colreduce_ws_bytes(int64_t n, int64_t p) { return colreduce_ws_bytes(n, p); }
@@ -194,10 +207,10 @@ int rsvd_flip_by_sign(int dtype, int64_t n, int64_t k, void* X, int64_t ldx,
 }
 
 int rsvd_convert(int src_dtype, int dst_dtype, int64_t rows, int64_t cols, const void* src,
-                 int64_t lds, void* dst, int64_t ldd, void* stream) {
+                 int64_t lds, void* dst, int64_t ldd, const int32_t* pred, void* stream) {
     RSVD_REQUIRE(valid_dtype(src_dtype) && valid_dtype(dst_dtype), "convert: bad dtype");
     RSVD_REQUIRE(lds >= cols && ldd >= cols, "convert: bad leading dimension");
-    return convert(src_dtype, dst_dtype, rows, cols, src, lds, dst, ldd, as_stream(stream));
+    return convert(src_dtype, dst_dtype, rows, cols, src, lds, dst, ldd, pred, as_stream(stream));
 }
 
 int rsvd_sqrt_clip(int64_t k, const double* in, double* out, void* stream) {

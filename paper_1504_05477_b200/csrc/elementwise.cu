@@ -153,7 +153,8 @@ __global__ void k_flip_by(int64_t n, int64_t k, T* __restrict__ X, int64_t ldx,
 
 template <typename T>
 __global__ void k_mask_cols(int64_t n, int64_t p, T* __restrict__ X, int64_t ldx,
-                            const int32_t* __restrict__ keep) {
+                            const int32_t* __restrict__ keep, const int32_t* __restrict__ pred) {
+    if (pred && *pred == 0) return;
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= n * p) return;
     int64_t r = e / p, c = e % p;
@@ -162,7 +163,8 @@ __global__ void k_mask_cols(int64_t n, int64_t p, T* __restrict__ X, int64_t ldx
 
 template <typename S, typename D>
 __global__ void k_convert(int64_t rows, int64_t cols, const S* __restrict__ src, int64_t lds,
-                          D* __restrict__ dst, int64_t ldd) {
+                          D* __restrict__ dst, int64_t ldd, const int32_t* __restrict__ pred) {
+    if (pred && *pred == 0) return;
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= rows * cols) return;
     int64_t i = e / cols, j = e % cols;
@@ -227,8 +229,10 @@ __device__ __forceinline__ double fill_normal(uint64_t seed, int64_t n, int64_t 
 template <typename T>
 __global__ void k_insert_fill(int64_t n, int64_t p, T* __restrict__ X, int64_t ldx,
                               const int32_t* __restrict__ mask, const int32_t* __restrict__ ndef,
-                              uint64_t seed, int64_t row_offset, int64_t n_total) {
+                              uint64_t seed, int64_t row_offset, int64_t n_total,
+                              const int32_t* __restrict__ pred) {
     extern __shared__ int32_t smask[];
+    if (pred && *pred == 0) return;
     if (ndef && ndef[0] == 0) return;
     const int64_t base = ndef ? ndef[1] : 0;
     for (int64_t j = threadIdx.x; j < p; j += blockDim.x) smask[j] = mask[j];
@@ -340,29 +344,29 @@ int flip_by_sign(int dtype, int64_t n, int64_t k, void* X, int64_t ldx, const do
 }
 
 int mask_cols(int dtype, int64_t n, int64_t p, void* X, int64_t ldx, const int32_t* keep,
-              cudaStream_t st) {
+              const int32_t* pred, cudaStream_t st) {
     if (n * p == 0) return RSVD_OK;
     unsigned nb = (unsigned)cdiv(n * p, 256);
     if (dtype == RSVD_F64)
-        k_mask_cols<double><<<nb, 256, 0, st>>>(n, p, (double*)X, ldx, keep);
+        k_mask_cols<double><<<nb, 256, 0, st>>>(n, p, (double*)X, ldx, keep, pred);
     else
-        k_mask_cols<float><<<nb, 256, 0, st>>>(n, p, (float*)X, ldx, keep);
+        k_mask_cols<float><<<nb, 256, 0, st>>>(n, p, (float*)X, ldx, keep, pred);
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }
 
 int convert(int sd, int dd, int64_t rows, int64_t cols, const void* src, int64_t lds, void* dst,
-            int64_t ldd, cudaStream_t st) {
+            int64_t ldd, const int32_t* pred, cudaStream_t st) {
     if (rows * cols == 0) return RSVD_OK;
     unsigned nb = (unsigned)cdiv(rows * cols, 256);
     if (sd == RSVD_F64 && dd == RSVD_F32)
-        k_convert<double, float><<<nb, 256, 0, st>>>(rows, cols, (const double*)src, lds, (float*)dst, ldd);
+        k_convert<double, float><<<nb, 256, 0, st>>>(rows, cols, (const double*)src, lds, (float*)dst, ldd, pred);
     else if (sd == RSVD_F32 && dd == RSVD_F64)
-        k_convert<float, double><<<nb, 256, 0, st>>>(rows, cols, (const float*)src, lds, (double*)dst, ldd);
+        k_convert<float, double><<<nb, 256, 0, st>>>(rows, cols, (const float*)src, lds, (double*)dst, ldd, pred);
     else if (sd == RSVD_F64)
-        k_convert<double, double><<<nb, 256, 0, st>>>(rows, cols, (const double*)src, lds, (double*)dst, ldd);
+        k_convert<double, double><<<nb, 256, 0, st>>>(rows, cols, (const double*)src, lds, (double*)dst, ldd, pred);
     else
-        k_convert<float, float><<<nb, 256, 0, st>>>(rows, cols, (const float*)src, lds, (float*)dst, ldd);
+        k_convert<float, float><<<nb, 256, 0, st>>>(rows, cols, (const float*)src, lds, (float*)dst, ldd, pred);
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }
@@ -382,17 +386,17 @@ int ortho_error(int64_t k, const double* G, int64_t ldg, double* out, cudaStream
 
 int insert_fill(int dtype, int64_t n, int64_t p, void* X, int64_t ldx, const int32_t* mask,
                 const int32_t* ndef, uint64_t seed, int64_t row_offset, int64_t n_total,
-                cudaStream_t st) {
+                const int32_t* pred, cudaStream_t st) {
     if (n == 0 || p == 0) return RSVD_OK;
     size_t sm = (size_t)p * sizeof(int32_t);
     RSVD_REQUIRE(sm <= 48 * 1024, "insert_fill: p too large");
     unsigned nb = (unsigned)cdiv(n, 256);
     if (dtype == RSVD_F64)
         k_insert_fill<double><<<nb, 256, sm, st>>>(n, p, (double*)X, ldx, mask, ndef, seed,
-                                                   row_offset, n_total);
+                                                   row_offset, n_total, pred);
     else
         k_insert_fill<float><<<nb, 256, sm, st>>>(n, p, (float*)X, ldx, mask, ndef, seed,
-                                                  row_offset, n_total);
+                                                  row_offset, n_total, pred);
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }

@@ -4,14 +4,17 @@
 
 namespace rsvd {
 
+// true when the op must be skipped (device-side predicate, see the header)
+__device__ __forceinline__ bool pred_off(const int32_t* pred) { return pred && *pred == 0; }
+
 int gemm_nn_simt(int dtype, int64_t m, int64_t n, int64_t k, double alpha, const void* A,
                  int64_t lda, const void* B, int64_t ldb, double beta, void* C, int64_t ldc,
-                 const double* row_sub, cudaStream_t st);
+                 const double* row_sub, const int32_t* pred, cudaStream_t st);
 int64_t gemm_tn_simt_ws_bytes(int64_t m, int64_t n, int64_t k);
 int gemm_tn_simt(int dtype, int out_dtype, int64_t m, int64_t n, int64_t k, double alpha,
                  const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C,
                  int64_t ldc, const double* mu, const double* cs, void* ws, int64_t ws_bytes,
-                 cudaStream_t st);
+                 const int32_t* pred, cudaStream_t st);
 
 // tcgen05 3xTF32 kernels (gemm_tc.cu). Return RSVD_ERR_INVALID when the
 // shape/alignment is not supported so the dispatcher can refuse loudly.
@@ -19,12 +22,13 @@ bool gemm_tc_nn_supported(int64_t m, int64_t n, int64_t k, int64_t lda, int64_t 
                           int64_t ldc, const void* A, const void* B);
 int gemm_nn_tc(int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t lda,
                const float* B, int64_t ldb, double beta, float* C, int64_t ldc,
-               const double* row_sub, cudaStream_t st);
+               const double* row_sub, const int32_t* pred, cudaStream_t st);
 bool gemm_tc_tn_supported(int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb,
                           const void* A, const void* B);
 int64_t gemm_tn_tc_ws_bytes(int64_t m, int64_t n, int64_t k);
 int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, const float* A,
                int64_t lda, const float* B, int64_t ldb, double beta, void* C, int64_t ldc,
-               const double* mu, const double* cs, void* ws, int64_t ws_bytes, cudaStream_t st);
+               const double* mu, const double* cs, void* ws, int64_t ws_bytes, const int32_t* pred,
+               cudaStream_t st);
 
 }  // namespace rsvd

@@ -21,7 +21,8 @@ template <typename T, int BM, int BN, int BK>
 __global__ void __launch_bounds__(kThreads)
 k_gemm_nn(int64_t m, int64_t n, int64_t k, double alpha, const T* __restrict__ A, int64_t lda,
           const T* __restrict__ B, int64_t ldb, double beta, T* __restrict__ C, int64_t ldc,
-          const double* __restrict__ row_sub) {
+          const double* __restrict__ row_sub, const int32_t* __restrict__ pred) {
+    if (pred_off(pred)) return;
     constexpr int TM = BM / 16, TN = BN / 16;
     __shared__ T As[2][BK][BM + 2];
     __shared__ T Bs[2][BK][BN];
@@ -111,7 +112,8 @@ template <typename T, int BKO, int BN, int BR>
 __global__ void __launch_bounds__(kThreads)
 k_gemm_tn_partial(int64_t m, int64_t n, int64_t k, const T* __restrict__ A, int64_t lda,
                   const T* __restrict__ B, int64_t ldb, int64_t rows_per_split,
-                  double* __restrict__ ws) {
+                  double* __restrict__ ws, const int32_t* __restrict__ pred) {
+    if (pred_off(pred)) return;
     constexpr int TM = BKO / 16, TN = BN / 16;
     __shared__ T As[2][BR][BKO];
     __shared__ T Bs[2][BR][BN];
@@ -199,7 +201,9 @@ k_gemm_tn_partial(int64_t m, int64_t n, int64_t k, const T* __restrict__ A, int6
 template <typename TO>
 __global__ void k_tn_reduce(int64_t k, int64_t n, int64_t splits, const double* __restrict__ ws,
                             double alpha, double beta, TO* __restrict__ C, int64_t ldc,
-                            const double* __restrict__ mu, const double* __restrict__ cs) {
+                            const double* __restrict__ mu, const double* __restrict__ cs,
+                            const int32_t* __restrict__ pred) {
+    if (pred_off(pred)) return;
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= k * n) return;
     int64_t r = idx / n, c = idx % n;
@@ -227,20 +231,20 @@ int64_t tn_splits(int64_t m, int64_t n, int64_t k) {
 
 int gemm_nn_simt(int dtype, int64_t m, int64_t n, int64_t k, double alpha, const void* A,
                  int64_t lda, const void* B, int64_t ldb, double beta, void* C, int64_t ldc,
-                 const double* row_sub, cudaStream_t st) {
+                 const double* row_sub, const int32_t* pred, cudaStream_t st) {
     if (m == 0 || n == 0) return RSVD_OK;
     if (dtype == RSVD_F64) {
         constexpr int BM = 64, BN = 64, BK = 16;
         dim3 grid((unsigned)cdiv(m, BM), (unsigned)cdiv(n, BN));
         k_gemm_nn<double, BM, BN, BK><<<grid, kThreads, 0, st>>>(
             m, n, k, alpha, (const double*)A, lda, (const double*)B, ldb, beta, (double*)C, ldc,
-            row_sub);
+            row_sub, pred);
     } else {
         constexpr int BM = 64, BN = 64, BK = 16;
         dim3 grid((unsigned)cdiv(m, BM), (unsigned)cdiv(n, BN));
         k_gemm_nn<float, BM, BN, BK><<<grid, kThreads, 0, st>>>(
             m, n, k, alpha, (const float*)A, lda, (const float*)B, ldb, beta, (float*)C, ldc,
-            row_sub);
+            row_sub, pred);
     }
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
@@ -254,7 +258,7 @@ int64_t gemm_tn_simt_ws_bytes(int64_t m, int64_t n, int64_t k) {
 int gemm_tn_simt(int dtype, int out_dtype, int64_t m, int64_t n, int64_t k, double alpha,
                  const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C,
                  int64_t ldc, const double* mu, const double* cs, void* ws, int64_t ws_bytes,
-                 cudaStream_t st) {
+                 const int32_t* pred, cudaStream_t st) {
     if (k == 0 || n == 0) return RSVD_OK;
     int64_t s = tn_splits(m, n, k);
     RSVD_REQUIRE(ws_bytes >= s * k * n * (int64_t)sizeof(double), "gemm_tn: workspace too small");
@@ -262,19 +266,19 @@ int gemm_tn_simt(int dtype, int out_dtype, int64_t m, int64_t n, int64_t k, doub
     dim3 grid((unsigned)cdiv(k, TN_BKO), (unsigned)cdiv(n, TN_BN), (unsigned)s);
     if (dtype == RSVD_F64)
         k_gemm_tn_partial<double, TN_BKO, TN_BN, TN_BR><<<grid, kThreads, 0, st>>>(
-            m, n, k, (const double*)A, lda, (const double*)B, ldb, rps, (double*)ws);
+            m, n, k, (const double*)A, lda, (const double*)B, ldb, rps, (double*)ws, pred);
     else
         k_gemm_tn_partial<float, TN_BKO, TN_BN, TN_BR><<<grid, kThreads, 0, st>>>(
-            m, n, k, (const float*)A, lda, (const float*)B, ldb, rps, (double*)ws);
+            m, n, k, (const float*)A, lda, (const float*)B, ldb, rps, (double*)ws, pred);
     RSVD_CHECK_LAUNCH();
     int64_t tot = k * n;
     unsigned nb = (unsigned)cdiv(tot, 256);
     if (out_dtype == RSVD_F64)
         k_tn_reduce<double><<<nb, 256, 0, st>>>(k, n, s, (const double*)ws, alpha, beta,
-                                                (double*)C, ldc, mu, cs);
+                                                (double*)C, ldc, mu, cs, pred);
     else
         k_tn_reduce<float><<<nb, 256, 0, st>>>(k, n, s, (const double*)ws, alpha, beta, (float*)C,
-                                               ldc, mu, cs);
+                                               ldc, mu, cs, pred);
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }

@@ -157,6 +157,7 @@ struct TcParams {
     double alpha, beta;
     const double* row_sub;
     float* ws;
+    const int32_t* pred;
 };
 
 template <int BN, bool A_MN>
@@ -173,6 +174,7 @@ struct TcCfg {
 template <int BN, bool A_MN>
 __global__ void __launch_bounds__(kThreads, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
+    if (pred_off(p.pred)) return;
     using Cfg = TcCfg<BN, A_MN>;
     constexpr int STAGES = Cfg::STAGES;
     extern __shared__ uint8_t smem_raw[];
@@ -375,7 +377,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 // Split the small operand B (K x N, ld) into [hi; lo] rows of a (2 Kp) x Np
 // array with zero padding (so TMA boxes past K or N read zeros).
 __global__ void k_split_b(int64_t K, int64_t N, const float* __restrict__ B, int64_t ldb, int64_t Kp, int64_t Np,
-                          float* __restrict__ out) {
+                          float* __restrict__ out, const int32_t* __restrict__ pred) {
+    if (pred_off(pred)) return;
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= Kp * Np) return;
     int64_t r = e / Np, c = e % Np;
@@ -388,7 +391,8 @@ __global__ void k_split_b(int64_t K, int64_t N, const float* __restrict__ B, int
 template <typename TO>
 __global__ void k_tc_reduce(int64_t M, int64_t N, int64_t splits, const float* __restrict__ ws, double alpha,
                             double beta, TO* __restrict__ C, int64_t ldc, const double* __restrict__ mu,
-                            const double* __restrict__ cs) {
+                            const double* __restrict__ cs, const int32_t* __restrict__ pred) {
+    if (pred_off(pred)) return;
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= M * N) return;
     int64_t r = e / N, c = e % N;
@@ -477,21 +481,24 @@ struct Scratch {
     size_t bytes = 0;
 };
 
-int split_b(const float* B, int64_t K, int64_t N, int64_t ldb, int64_t Kp, int64_t Np, float* out, cudaStream_t st) {
+int split_b(const float* B, int64_t K, int64_t N, int64_t ldb, int64_t Kp, int64_t Np, float* out,
+            const int32_t* pred, cudaStream_t st) {
     int64_t tot = Kp * Np;
-    k_split_b<<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(K, N, B, ldb, Kp, Np, out);
+    k_split_b<<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(K, N, B, ldb, Kp, Np, out, pred);
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }
 
 int64_t tn_splits_tc(int64_t Mop, int64_t Nop, int64_t Kop) {
+    // split-K only for parallelism (accuracy is handled by the chunked TMEM
+    // accumulation): enough CTAs to fill the chip, but few enough partials
+    // that the reduction stays short.
     int bn = pick_bn(Nop);
     int64_t tiles = cdiv(Mop, BM) * cdiv(Nop, bn);
-    int64_t target = (int64_t)sm_count() * 2;
+    int64_t target = (int64_t)sm_count();
     int64_t s = cdiv(target, tiles);
-    int64_t min_s = cdiv(Kop, 32768);   // bound the FP32 accumulation length
-    if (s < min_s) s = min_s;
-    int64_t max_s = cdiv(Kop, 4 * BK);
+    if (s > 64) s = 64;
+    int64_t max_s = cdiv(Kop, 8 * BK);
     if (s > max_s) s = max_s;
     if (s < 1) s = 1;
     return s;
@@ -507,7 +514,8 @@ bool gemm_tc_nn_supported(int64_t m, int64_t n, int64_t k, int64_t lda, int64_t 
 }
 
 int gemm_nn_tc(int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t lda, const float* B,
-               int64_t ldb, double beta, float* C, int64_t ldc, const double* row_sub, cudaStream_t st) {
+               int64_t ldb, double beta, float* C, int64_t ldc, const double* row_sub, const int32_t* pred,
+               cudaStream_t st) {
     int bn = pick_bn(n);
     const int64_t Kp = cdiv(k, BK) * BK, Np = cdiv(n, 32) * 32 + 128;
     static thread_local Scratch sc;  // split-B buffer
@@ -518,7 +526,7 @@ int gemm_nn_tc(int64_t m, int64_t n, int64_t k, double alpha, const float* A, in
         sc.bytes = need;
     }
     float* bs = (float*)sc.ptr;
-    int rc = split_b(B, k, n, ldb, Kp, Np, bs, st);
+    int rc = split_b(B, k, n, ldb, Kp, Np, bs, pred, st);
     if (rc) return rc;
     CUtensorMap tA, tB;
     rc = make_map(&tA, A, k, m, lda, BM, false);
@@ -528,6 +536,7 @@ int gemm_nn_tc(int64_t m, int64_t n, int64_t k, double alpha, const float* A, in
     TcParams p{};
     p.M = m; p.N = n; p.K = k; p.k_per_split = Kp; p.Kp = Kp;
     p.direct = 1; p.C = C; p.ldc = ldc; p.alpha = alpha; p.beta = beta; p.row_sub = row_sub; p.ws = nullptr;
+    p.pred = pred;
     dim3 grid((unsigned)cdiv(m, BM), (unsigned)cdiv(n, bn), 1);
     return dispatch_bn<false>(bn, tA, tB, p, grid, st);
 }
@@ -546,7 +555,7 @@ int64_t gemm_tn_tc_ws_bytes(int64_t m, int64_t n, int64_t k) {
 
 int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t lda,
                const float* B, int64_t ldb, double beta, void* C, int64_t ldc, const double* mu, const double* cs,
-               void* ws, int64_t ws_bytes, cudaStream_t st) {
+               void* ws, int64_t ws_bytes, const int32_t* pred, cudaStream_t st) {
     // operand view: D[Mop x Nop] = A^T[Mop x Kop] B[Kop x Nop], Mop = k, Kop = m
     const int64_t Mop = k, Nop = n, Kop = m;
     int bn = pick_bn(Nop);
@@ -561,7 +570,7 @@ int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, con
         sc.bytes = need;
     }
     float* bs = (float*)sc.ptr;
-    int rc = split_b(B, Kop, Nop, ldb, Kp, Np, bs, st);
+    int rc = split_b(B, Kop, Nop, ldb, Kp, Np, bs, pred, st);
     if (rc) return rc;
     CUtensorMap tA, tB;
     rc = make_map(&tA, A, k /*inner = columns of A*/, m, lda, BK, true);
@@ -572,17 +581,17 @@ int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, con
     p.M = Mop; p.N = Nop; p.K = Kop;
     p.k_per_split = cdiv(cdiv(Kop, S), BK) * BK;
     p.Kp = Kp;
-    p.direct = 0; p.ws = (float*)ws;
+    p.direct = 0; p.ws = (float*)ws; p.pred = pred;
     dim3 grid((unsigned)cdiv(Mop, BM), (unsigned)cdiv(Nop, bn), (unsigned)S);
     rc = dispatch_bn<true>(bn, tA, tB, p, grid, st);
     if (rc) return rc;
     int64_t tot = Mop * Nop;
     if (out_dtype == RSVD_F64)
         k_tc_reduce<double><<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(Mop, Nop, S, (const float*)ws, alpha, beta,
-                                                                       (double*)C, ldc, mu, cs);
+                                                                       (double*)C, ldc, mu, cs, pred);
     else
         k_tc_reduce<float><<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(Mop, Nop, S, (const float*)ws, alpha, beta,
-                                                                      (float*)C, ldc, mu, cs);
+                                                                      (float*)C, ldc, mu, cs, pred);
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }

@@ -33,6 +33,7 @@ __device__ __forceinline__ int64_t tri_off(int64_t p, int64_t i, int64_t j) {
 }
 
 constexpr int kCholThreads = 256;
+constexpr int kMaxSmemP = 512;
 
 // One CTA. R (upper triangle, packed) lives in shared memory; T = R^{-1} in
 // shared memory too when it fits (else it is built in place in global T).
@@ -43,7 +44,9 @@ __global__ void __launch_bounds__(kCholThreads)
 k_chol_deflate(int64_t p, const double* __restrict__ G, int64_t ldg,
                const double* __restrict__ ref2, double tau2, double* __restrict__ T, int64_t ldt,
                int32_t* __restrict__ mask, int32_t* __restrict__ ndef, int32_t* __restrict__ running,
-               const int32_t* __restrict__ active, double* gws, int use_smem, int t_in_smem) {
+               const int32_t* __restrict__ active, double* gws, int use_smem, int t_in_smem,
+               const int32_t* __restrict__ pred) {
+    if (pred && *pred == 0) return;
     extern __shared__ double smem_d[];
     double* S = use_smem ? smem_d : gws;
     const int64_t tri = p * (p + 1) / 2;
@@ -53,17 +56,25 @@ k_chol_deflate(int64_t p, const double* __restrict__ G, int64_t ldg,
     __shared__ int s_def;
     __shared__ int s_count;
     __shared__ double s_rjj;
+    __shared__ double s_ref[kMaxSmemP];
+    __shared__ int s_act[kMaxSmemP];
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const bool small = p <= kMaxSmemP;
     for (int64_t i = warp; i < p; i += nwarps)
         for (int64_t j = i + lane; j < p; j += 32) S[tri_off(p, i, j)] = G[i * ldg + j];
+    if (small)
+        for (int64_t j = tid; j < p; j += blockDim.x) {  // per-column inputs staged once
+            s_ref[j] = ref2 ? ref2[j] : G[j * ldg + j];
+            s_act[j] = active ? active[j] : 1;
+        }
     if (tid == 0) s_count = 0;
     __syncthreads();
     for (int64_t j = 0; j < p; ++j) {
         if (tid == 0) {
             const double d = S[tri_off(p, j, j)];
-            const double r = ref2 ? ref2[j] : G[j * ldg + j];
-            const int act = active ? active[j] : 1;
+            const double r = small ? s_ref[j] : (ref2 ? ref2[j] : G[j * ldg + j]);
+            const int act = small ? s_act[j] : (active ? active[j] : 1);
             const int def = !act || !(d > tau2 * r) || !(d > 0.0);
             s_def = def;
             mask[j] = def ? (act ? 1 : 2) : 0;  // 2 = inactive slot (not counted)
@@ -125,6 +136,105 @@ k_chol_deflate(int64_t p, const double* __restrict__ G, int64_t ldg,
     }
     for (int64_t j = tid; j < p; j += blockDim.x)
         if (mask[j] == 2) mask[j] = 0;
+}
+
+// Fast path for p <= kFastP: the packed Schur complement lives in typed
+// shared memory (LDS/STS, no generic addressing); two barriers per column
+// (decide pivot | trailing update + deferred scaling of the previous row);
+// T = R^{-1} by columns, one warp per column (back substitution with the
+// dot products split over lanes), column buffers in shared memory.
+constexpr int kFastP = 224;
+constexpr int kFastThreads = 1024;
+constexpr int kInvRegs = (kFastP + 31) / 32;
+
+__global__ void __launch_bounds__(kFastThreads)
+k_chol_fast(int p, const double* __restrict__ G, int64_t ldg, const double* __restrict__ ref2, double tau2,
+            double* __restrict__ T, int64_t ldt, int32_t* __restrict__ mask, int32_t* __restrict__ ndef,
+            int32_t* __restrict__ running, const int32_t* __restrict__ active, const int32_t* __restrict__ pred) {
+    if (pred && *pred == 0) return;
+    extern __shared__ double S[];  // packed upper triangle of the Schur complement / R
+    __shared__ double s_ref[kFastP];
+    __shared__ double s_rinv[kFastP];  // 1 / R[j][j] (1 for deficient slots)
+    __shared__ int s_msk[kFastP];
+    __shared__ int s_act[kFastP];
+    __shared__ int s_count;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    auto off = [p](int i, int j) { return i * p - (i * (i - 1)) / 2 + (j - i); };
+    for (int i = warp; i < p; i += nwarps)
+        for (int j = i + lane; j < p; j += 32) S[off(i, j)] = G[(int64_t)i * ldg + j];
+    for (int j = tid; j < p; j += blockDim.x) {
+        s_ref[j] = ref2 ? ref2[j] : G[(int64_t)j * ldg + j];
+        s_act[j] = active ? active[j] : 1;
+    }
+    if (tid == 0) s_count = 0;
+    __syncthreads();
+    for (int j = 0; j < p; ++j) {
+        if (tid == 0) {
+            const double d = S[off(j, j)];
+            const int act = s_act[j];
+            const int def = !act || !(d > tau2 * s_ref[j]) || !(d > 0.0);
+            s_msk[j] = def ? (act ? 1 : 2) : 0;
+            if (def && act) ++s_count;
+            const double rjj = def ? 1.0 : sqrt(d);
+            S[off(j, j)] = rjj;
+            s_rinv[j] = 1.0 / rjj;
+        }
+        __syncthreads();
+        const bool def = s_msk[j] != 0;
+        const double inv = s_rinv[j];
+        // trailing update with the unscaled row j: S(a,b) -= S(j,a) S(j,b) / d
+        if (!def) {
+            const double inv2 = inv * inv;
+            const int rj = off(j, 0);
+            for (int a = j + 1 + warp; a < p; a += nwarps) {
+                const double ra = S[rj + a] * inv2;
+                const int rowa = off(a, a) - a;
+                for (int b = a + lane; b < p; b += 32) S[rowa + b] -= ra * S[rj + b];
+            }
+        }
+        __syncthreads();
+        // now scale row j of R (its trailing consumers are done)
+        const int rj = off(j, 0);
+        for (int c = j + 1 + tid; c < p; c += blockDim.x) S[rj + c] = def ? 0.0 : S[rj + c] * inv;
+        // (next column's pivot reads S(j+1, j+1), not row j: no barrier needed here)
+    }
+    __syncthreads();
+    // T = R^{-1}: column c by one warp, x = R^{-1} e_c in registers (lane l
+    // holds rows l, l+32, ...); back substitution in axpy form: for b = c..0
+    // finalise x_b (broadcast by shuffle) and subtract R[a][b] x_b from all a < b.
+    for (int c = warp; c < p; c += nwarps) {
+        double x[kInvRegs];
+#pragma unroll
+        for (int r = 0; r < kInvRegs; ++r) x[r] = (lane + 32 * r == c) ? 1.0 : 0.0;
+        for (int b = c; b >= 0; --b) {
+            const int rb = b >> 5, lb = b & 31;
+            double xb = 0.0;
+#pragma unroll
+            for (int r = 0; r < kInvRegs; ++r)
+                if (r == rb) xb = x[r];
+            xb = __shfl_sync(0xffffffffu, xb, lb) * s_rinv[b];
+#pragma unroll
+            for (int r = 0; r < kInvRegs; ++r) {
+                const int a = lane + 32 * r;
+                if (a == b) x[r] = xb;
+                else if (a < b) x[r] -= S[off(a, b)] * xb;
+            }
+        }
+        const bool zc = s_msk[c] != 0;
+#pragma unroll
+        for (int r = 0; r < kInvRegs; ++r) {
+            const int a = lane + 32 * r;
+            if (a < p) T[(int64_t)a * ldt + c] = (zc || s_msk[a] || a > c) ? 0.0 : x[r];
+        }
+    }
+    __syncthreads();
+    for (int j = tid; j < p; j += blockDim.x) mask[j] = s_msk[j] == 1 ? 1 : 0;
+    if (tid == 0) {
+        const int32_t base = running ? running[0] : 0;
+        ndef[0] = s_count;
+        ndef[1] = base;
+        if (running) running[0] = base + s_count;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -350,8 +460,17 @@ int64_t chol_deflate_ws_bytes(int64_t p) { return (p * (p + 1) / 2) * (int64_t)s
 
 int chol_deflate(int64_t p, const double* G, int64_t ldg, const double* ref2, double tau2, double* T,
                  int64_t ldt, int32_t* mask, int32_t* ndef, int32_t* running, const int32_t* active, void* ws,
-                 int64_t ws_bytes, cudaStream_t st) {
+                 int64_t ws_bytes, const int32_t* pred, cudaStream_t st) {
     if (p == 0) return RSVD_OK;
+    if (p <= kFastP) {
+        const size_t sm = (size_t)(p * (p + 1) / 2) * sizeof(double);
+        if (sm > 48 * 1024)
+            RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_chol_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_chol_fast<<<1, kFastThreads, sm, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active,
+                                                 pred);
+        RSVD_CHECK_LAUNCH();
+        return RSVD_OK;
+    }
     const int64_t rbytes = chol_deflate_ws_bytes(p);
     const int64_t tbytes = p * p * (int64_t)sizeof(double);
     const int64_t cap = 200 * 1024;
@@ -363,7 +482,7 @@ int chol_deflate(int64_t p, const double* G, int64_t ldg, const double* ref2, do
         RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_chol_deflate, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)sm));
     k_chol_deflate<<<1, kCholThreads, sm, st>>>(p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active,
-                                                (double*)ws, use_smem, t_in_smem);
+                                                (double*)ws, use_smem, t_in_smem, pred);
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }

@@ -1,0 +1,450 @@
+// Top-k symmetric eigensolver for the Rayleigh-Ritz matrix M = Q^T A A^T Q
+// (w x w, FP64), replacing the reference's full cyclic Jacobi
+// (symmetric_eig, factor.py:132-166 -> _kernels.pyx:127-192) on the hot
+// path. post_process only consumes the top k eigenpairs (rsvd.py:217-220),
+// so this follows LAPACK's dsyevx structure:
+//   1. Householder tridiagonalisation M = H T H^T: one cooperative kernel,
+//      two grid barriers per column (matvec, then rank-2 update);
+//   2. top-k eigenvalues of T by Sturm-count multisection (one warp per
+//      eigenvalue, 32 shifts per step), to full FP64 accuracy;
+//   3. eigenvectors of T by inverse iteration on a pivoted tridiagonal LU,
+//      vectors of eigenvalue clusters (gap < 1e-5 ||T||_1) re-orthogonalised
+//      in order (dstein's scheme), one warp per cluster;
+//   4. back-transformation x <- H_0 ... H_{w-3} x, one warp per vector.
+// Eigenvalues are returned descending; eigenvector signs are arbitrary (the
+// caller canonicalises Z's signs, rsvd.py:192-197).
+#include "common.cuh"
+
+namespace rsvd {
+
+namespace {
+
+constexpr int kTriThreads = 512;
+
+struct TriState {
+    int64_t w;
+    double* A;      // w x w work copy (row-major, ld = w), symmetric
+    double* d;      // w
+    double* e;      // w (e[i] couples i, i+1)
+    double* Uh;     // w x w, row j = Householder vector of step j
+    double* beta;   // w
+    double* p;      // w scratch
+    double* partial;
+    unsigned int* bar;
+};
+
+__device__ double block_sum(double v, double* red) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+    return s;
+}
+
+__global__ void __launch_bounds__(kTriThreads) k_tridiag(TriState s) {
+    extern __shared__ double sh[];
+    const int64_t w = s.w;
+    double* u = sh;       // w
+    double* q = sh + w;   // w
+    __shared__ double red[kTriThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = 0; j + 2 < w; ++j) {
+        const int64_t m = w - j - 1;
+        const double* rowj = s.A + j * w + (j + 1);
+        double ss = 0.0, tail = 0.0;
+        for (int64_t i = tid; i < m; i += blockDim.x) {
+            const double x = rowj[i];
+            u[i] = x;
+            ss += x * x;
+            if (i > 0) tail += x * x;
+        }
+        ss = block_sum(ss, red);
+        tail = block_sum(tail, red);
+        const double x0 = u[0];
+        const bool skip = !(tail > 0.0);
+        double alpha = x0, beta = 0.0;
+        if (!skip) {
+            const double nrm = sqrt(ss);
+            alpha = x0 >= 0.0 ? -nrm : nrm;
+            const double u0 = x0 - alpha;
+            beta = 2.0 / (tail + u0 * u0);
+            __syncthreads();
+            if (tid == 0) u[0] = u0;
+            __syncthreads();
+        }
+        if (blockIdx.x == 0) {
+            if (tid == 0) {
+                s.d[j] = s.A[j * w + j];
+                s.e[j] = alpha;
+                s.beta[j] = beta;
+            }
+            double* uh = s.Uh + j * w;
+            for (int64_t i = tid; i < w; i += blockDim.x) uh[i] = (i > j && !skip) ? u[i - j - 1] : 0.0;
+        }
+        if (skip) continue;  // H_j = I: every CTA took the same decision
+        // p = beta * A22 u  (warp per row)
+        for (int64_t r = gwarp; r < m; r += nwarps) {
+            const double* ar = s.A + (j + 1 + r) * w + (j + 1);
+            double acc = 0.0;
+            for (int64_t c = lane; c < m; c += 32) acc = fma(ar[c], u[c], acc);
+            acc = warp_sum(acc);
+            if (lane == 0) s.p[r] = beta * acc;
+        }
+        grid_barrier(s.bar, gridDim.x);
+        double kk = 0.0;
+        for (int64_t i = tid; i < m; i += blockDim.x) {
+            const double pv = s.p[i];
+            q[i] = pv;
+            kk += u[i] * pv;
+        }
+        kk = 0.5 * beta * block_sum(kk, red);
+        for (int64_t i = tid; i < m; i += blockDim.x) q[i] -= kk * u[i];
+        __syncthreads();
+        // A22 -= u q^T + q u^T
+        for (int64_t r = gwarp; r < m; r += nwarps) {
+            double* ar = s.A + (j + 1 + r) * w + (j + 1);
+            const double ur = u[r], qr = q[r];
+            for (int64_t c = lane; c < m; c += 32) ar[c] -= ur * q[c] + qr * u[c];
+        }
+        grid_barrier(s.bar, gridDim.x);
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        if (w >= 2) {
+            s.d[w - 2] = s.A[(w - 2) * w + (w - 2)];
+            s.e[w - 2] = s.A[(w - 2) * w + (w - 1)];
+            s.beta[w - 2] = 0.0;
+        }
+        s.d[w - 1] = s.A[(w - 1) * w + (w - 1)];
+        s.e[w - 1] = 0.0;
+        s.beta[w - 1] = 0.0;
+    }
+    if (blockIdx.x == 0)
+        for (int64_t jj = (w >= 2 ? w - 2 : 0); jj < w; ++jj)
+            for (int64_t i = tid; i < w; i += blockDim.x) s.Uh[jj * w + i] = 0.0;
+}
+
+__global__ void k_copy_sym(int64_t w, const double* __restrict__ M, int64_t ldm, double* __restrict__ A) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= w * w) return;
+    int64_t i = e / w, j = e % w;
+    A[e] = 0.5 * (M[i * ldm + j] + M[j * ldm + i]);
+}
+
+// Gershgorin bounds, ||T||_1 and pivmin (dstebz), one CTA.
+__global__ void k_tri_bounds(int64_t w, const double* __restrict__ d, const double* __restrict__ e,
+                             double* __restrict__ out) {
+    __shared__ double rlo[32], rhi[32], rn[32], re2[32];
+    double lo = 1e300, hi = -1e300, nrm = 0.0, emax2 = 0.0;
+    for (int64_t i = threadIdx.x; i < w; i += blockDim.x) {
+        const double em = i > 0 ? fabs(e[i - 1]) : 0.0;
+        const double ep = i + 1 < w ? fabs(e[i]) : 0.0;
+        lo = fmin(lo, d[i] - em - ep);
+        hi = fmax(hi, d[i] + em + ep);
+        nrm = fmax(nrm, fabs(d[i]) + em + ep);
+        if (i + 1 < w) emax2 = fmax(emax2, e[i] * e[i]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        nrm = fmax(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
+        emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
+    }
+    const int wp = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        rlo[wp] = lo;
+        rhi[wp] = hi;
+        rn[wp] = nrm;
+        re2[wp] = emax2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+            lo = fmin(lo, rlo[i]);
+            hi = fmax(hi, rhi[i]);
+            nrm = fmax(nrm, rn[i]);
+            emax2 = fmax(emax2, re2[i]);
+        }
+        lo = fmin(lo, rlo[0]);
+        hi = fmax(hi, rhi[0]);
+        nrm = fmax(nrm, rn[0]);
+        emax2 = fmax(emax2, re2[0]);
+        const double tnorm = fmax(fabs(lo), fabs(hi));
+        const double eps = 2.220446049250313e-16;
+        out[0] = lo - 2.0 * eps * tnorm - 1e-300;
+        out[1] = hi + 2.0 * eps * tnorm + 1e-300;
+        out[2] = nrm;
+        out[3] = 2.2250738585072014e-308 * fmax(1.0, emax2);  // pivmin
+    }
+}
+
+// number of eigenvalues of T strictly below x (Sturm count with pivmin guard)
+__device__ __forceinline__ int sturm_count(int64_t w, const double* __restrict__ d, const double* __restrict__ e2,
+                                           double x, double pivmin) {
+    int cnt = 0;
+    double qv = d[0] - x;
+    if (fabs(qv) < pivmin) qv = -pivmin;
+    cnt += qv < 0.0;
+    for (int64_t i = 1; i < w; ++i) {
+        qv = (d[i] - x) - e2[i - 1] / qv;
+        if (fabs(qv) < pivmin) qv = -pivmin;
+        cnt += qv < 0.0;
+    }
+    return cnt;
+}
+
+__global__ void k_e2(int64_t w, const double* __restrict__ e, double* __restrict__ e2) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < w) e2[i] = e[i] * e[i];
+}
+
+// eigenvalue number `idx` in ascending order; one warp per eigenvalue,
+// 32 Sturm counts per step (multisection).
+__global__ void k_multisect(int64_t w, int64_t k, const double* __restrict__ d, const double* __restrict__ e2,
+                            const double* __restrict__ bounds, double* __restrict__ evals) {
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= k) return;
+    const int64_t target = w - 1 - wid;  // wid-th largest
+    double lo = bounds[0], hi = bounds[1];
+    const double pivmin = bounds[3];
+    const double eps = 2.220446049250313e-16;
+    for (int it = 0; it < 64; ++it) {
+        const double width = hi - lo;
+        if (!(width > 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin)) break;
+        const double x = lo + width * (double)(lane + 1) / 33.0;
+        const int c = sturm_count(w, d, e2, x, pivmin);
+        // count(x) <= target  <=>  eigenvalue #target is >= x
+        const unsigned below = __ballot_sync(0xffffffffu, c <= target);
+        const int nb = __popc(below);  // counts are monotone: lanes 0..nb-1 satisfy
+        const double nlo = nb > 0 ? lo + width * (double)nb / 33.0 : lo;
+        const double nhi = nb < 32 ? lo + width * (double)(nb + 1) / 33.0 : hi;
+        lo = nlo;
+        hi = nhi;
+    }
+    if (lane == 0) evals[wid] = 0.5 * (lo + hi);
+}
+
+__global__ void k_clusters(int64_t k, const double* __restrict__ evals, const double* __restrict__ bounds,
+                           int32_t* __restrict__ cstart, int32_t* __restrict__ ncl) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    // eigenvectors of eigenvalues separated by more than ortol come out of
+    // inverse iteration orthogonal to ~2 eps ||T|| / gap <= 5e-11 already; only
+    // closer ones are chained through MGS (dstein uses 1e-3 ||T||).
+    const double ortol = bounds[2] > 0.0 ? 1e-5 * bounds[2] : 1e300;  // T = 0: one cluster
+    int n = 0;
+    for (int64_t i = 0; i < k; ++i)
+        if (i == 0 || evals[i - 1] - evals[i] > ortol) cstart[n++] = (int32_t)i;
+    cstart[n] = (int32_t)k;
+    ncl[0] = n;
+}
+
+__device__ __forceinline__ double init_vec(int64_t i, int64_t member) {
+    uint64_t z = (uint64_t)(i + 1) * 0x9E3779B97F4A7C15ULL ^ (uint64_t)(member + 7) * 0xBF58476D1CE4E5B9ULL;
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ULL;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    return (double)(z >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
+}
+
+// One warp per cluster. For each member: pivoted LU of T - lambda I (lane 0,
+// reciprocal pivots), 3 inverse-iteration solves, each followed by MGS against
+// the cluster's earlier vectors and normalisation (whole warp).
+__global__ void k_invit(int64_t w, int64_t k, const double* __restrict__ d, const double* __restrict__ e,
+                        const double* __restrict__ evals, const double* __restrict__ bounds,
+                        const int32_t* __restrict__ cstart, const int32_t* __restrict__ ncl,
+                        double* __restrict__ X /* k x w, row = vector */, double* __restrict__ fac /* per warp 5w */,
+                        int32_t* __restrict__ info) {
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= ncl[0]) return;
+    const int64_t c0 = cstart[wid], c1 = cstart[wid + 1];
+    double* u0 = fac + wid * 5 * w;  // reciprocal of U diagonal
+    double* u1 = u0 + w;
+    double* u2 = u1 + w;
+    double* l = u2 + w;
+    double* sw = l + w;  // swap flags (0/1 as double)
+    const double tnorm = bounds[2];
+    // ||T|| = 0 (zero Rayleigh-Ritz matrix, e.g. A = 0): every vector is an
+    // eigenvector; unit pivots keep the iteration finite
+    const double tiny = tnorm > 0.0 ? 2.220446049250313e-16 * tnorm : 1.0;
+    for (int64_t mbr = c0; mbr < c1; ++mbr) {
+        double* x = X + mbr * w;
+        // perturb repeated eigenvalues slightly so the shifts differ (dstein)
+        const double lam = evals[mbr] + (double)(mbr - c0) * 10.0 * tiny;
+        if (lane == 0) {
+            double cp = d[0] - lam, cq = w > 1 ? e[0] : 0.0, cr = 0.0;
+            for (int64_t i = 0; i + 1 < w; ++i) {
+                const double ci = e[i];
+                const double an = d[i + 1] - lam, bn = (i + 2 < w) ? e[i + 1] : 0.0;
+                if (fabs(ci) > fabs(cp)) {
+                    const double r = 1.0 / ci;
+                    const double mult = cp * r;
+                    u0[i] = r;
+                    u1[i] = an;
+                    u2[i] = bn;
+                    l[i] = mult;
+                    sw[i] = 1.0;
+                    cp = cq - mult * an;
+                    cq = cr - mult * bn;
+                } else {
+                    const double piv = fabs(cp) < tiny ? (cp < 0.0 ? -tiny : tiny) : cp;
+                    const double r = 1.0 / piv;
+                    const double mult = ci * r;
+                    u0[i] = r;
+                    u1[i] = cq;
+                    u2[i] = cr;
+                    l[i] = mult;
+                    sw[i] = 0.0;
+                    cp = an - mult * cq;
+                    cq = bn - mult * cr;
+                }
+                cr = 0.0;
+            }
+            const double piv = fabs(cp) < tiny ? (cp < 0.0 ? -tiny : tiny) : cp;
+            u0[w - 1] = 1.0 / piv;
+        }
+        for (int64_t i = lane; i < w; i += 32) x[i] = init_vec(i, mbr);
+        __syncwarp();
+        for (int it = 0; it < 3; ++it) {
+            if (lane == 0) {
+                // y = L^{-1} P x (carry in a register; x[i+1] loads are independent)
+                double carry = x[0];
+                for (int64_t i = 0; i + 1 < w; ++i) {
+                    double a = carry, b = x[i + 1];
+                    if (sw[i] != 0.0) {
+                        const double t = a;
+                        a = b;
+                        b = t;
+                    }
+                    x[i] = a;
+                    carry = b - l[i] * a;
+                }
+                // U x = y (two carries)
+                double c1 = carry * u0[w - 1], c2 = 0.0;
+                x[w - 1] = c1;
+                for (int64_t i = w - 2; i >= 0; --i) {
+                    const double v = (x[i] - u1[i] * c1 - u2[i] * c2) * u0[i];
+                    x[i] = v;
+                    c2 = c1;
+                    c1 = v;
+                }
+            }
+            __syncwarp();
+            // MGS against the earlier members of this cluster
+            for (int64_t o = c0; o < mbr; ++o) {
+                const double* y = X + o * w;
+                double dot = 0.0;
+                for (int64_t i = lane; i < w; i += 32) dot += y[i] * x[i];
+                dot = warp_sum(dot);
+                for (int64_t i = lane; i < w; i += 32) x[i] -= dot * y[i];
+                __syncwarp();
+            }
+            double nn = 0.0;
+            for (int64_t i = lane; i < w; i += 32) nn += x[i] * x[i];
+            nn = warp_sum(nn);
+            if (!(nn > 0.0) || !isfinite(nn)) {
+                if (lane == 0) info[0] = 0;
+                nn = 1.0;
+            }
+            const double inv = 1.0 / sqrt(nn);
+            for (int64_t i = lane; i < w; i += 32) x[i] *= inv;
+            __syncwarp();
+        }
+    }
+}
+
+// x <- H_0 H_1 ... H_{w-3} x for every vector (warp per vector), then write
+// evecs[:, i] (w x k row-major, ld lde).
+__global__ void k_backtransform(int64_t w, int64_t k, const double* __restrict__ Uh, const double* __restrict__ beta,
+                                double* __restrict__ X, double* __restrict__ evecs, int64_t lde) {
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (wid >= k) return;
+    double* x = X + wid * w;
+    for (int64_t j = w - 3; j >= 0; --j) {
+        const double b = beta[j];
+        if (b == 0.0) continue;
+        const double* uj = Uh + j * w;
+        double dot = 0.0;
+        for (int64_t i = j + 1 + lane; i < w; i += 32) dot += uj[i] * x[i];
+        dot = warp_sum(dot) * b;
+        for (int64_t i = j + 1 + lane; i < w; i += 32) x[i] -= dot * uj[i];
+        __syncwarp();
+    }
+    for (int64_t i = lane; i < w; i += 32) evecs[i * lde + wid] = x[i];
+}
+
+__global__ void k_info_init(int32_t* info) {
+    info[0] = 1;
+    info[1] = 0;
+}
+
+}  // namespace
+
+int64_t syev_topk_ws_bytes(int64_t w, int64_t k) {
+    // A, Uh (w^2 each), d, e, e2, beta, p (w each), bounds, X (k w), fac (k 5w), clusters
+    const int64_t dbl = 2 * w * w + 5 * w + 16 + k * w + 5 * k * w + 1024;
+    return dbl * (int64_t)sizeof(double) + (k + 2) * 4 + 256;
+}
+
+int syev_topk(int64_t w, const double* M, int64_t ldm, int64_t k, double* evals, double* evecs, int64_t lde,
+              int32_t* info, void* ws, int64_t ws_bytes, cudaStream_t st) {
+    RSVD_REQUIRE(w >= 1 && k >= 1 && k <= w, "syev_topk: bad shape");
+    RSVD_REQUIRE(ws_bytes >= syev_topk_ws_bytes(w, k), "syev_topk: workspace too small");
+    double* base = (double*)ws;
+    TriState s;
+    s.w = w;
+    s.A = base;
+    s.Uh = s.A + w * w;
+    s.d = s.Uh + w * w;
+    s.e = s.d + w;
+    double* e2 = s.e + w;
+    s.beta = e2 + w;
+    s.p = s.beta + w;
+    double* bounds = s.p + w;
+    double* X = bounds + 16;
+    double* fac = X + k * w;
+    s.partial = fac + 5 * k * w;
+    s.bar = (unsigned int*)(s.partial + 1024 - 16);
+    int32_t* cl = (int32_t*)(s.partial + 1024);
+    int32_t* ncl = cl + k + 1;
+    RSVD_CHECK_CUDA(cudaMemsetAsync(s.bar, 0, 2 * sizeof(unsigned int), st));
+    k_info_init<<<1, 1, 0, st>>>(info);
+    k_copy_sym<<<(unsigned)cdiv(w * w, 256), 256, 0, st>>>(w, M, ldm, s.A);
+    RSVD_CHECK_LAUNCH();
+    const size_t smem = (size_t)(2 * w) * sizeof(double);
+    RSVD_REQUIRE(smem <= 200 * 1024, "syev_topk: w too large");
+    if (smem > 48 * 1024)
+        RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    RSVD_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tridiag, kTriThreads, smem));
+    RSVD_REQUIRE(per_sm >= 1, "syev_topk: tridiagonalisation kernel cannot be resident");
+    int64_t g = cdiv(w, kTriThreads / 32);
+    if (g > sm_count()) g = sm_count();
+    if (g < 1) g = 1;
+    void* args[] = {&s};
+    RSVD_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)k_tridiag, dim3((unsigned)g), dim3(kTriThreads), args,
+                                                smem, st));
+    k_e2<<<(unsigned)cdiv(w, 256), 256, 0, st>>>(w, s.e, e2);
+    RSVD_CHECK_LAUNCH();
+    k_tri_bounds<<<1, 1024, 0, st>>>(w, s.d, s.e, bounds);
+    RSVD_CHECK_LAUNCH();
+    k_multisect<<<(unsigned)cdiv(k * 32, 256), 256, 0, st>>>(w, k, s.d, e2, bounds, evals);
+    RSVD_CHECK_LAUNCH();
+    k_clusters<<<1, 32, 0, st>>>(k, evals, bounds, cl, ncl);
+    RSVD_CHECK_LAUNCH();
+    k_invit<<<(unsigned)cdiv(k * 32, 128), 128, 0, st>>>(w, k, s.d, s.e, evals, bounds, cl, ncl, X, fac, info);
+    RSVD_CHECK_LAUNCH();
+    k_backtransform<<<(unsigned)cdiv(k * 32, 256), 256, 0, st>>>(w, k, s.Uh, s.beta, X, evecs, lde);
+    RSVD_CHECK_LAUNCH();
+    return RSVD_OK;
+}
+
+}  // namespace rsvd

@@ -64,18 +64,18 @@ class _Workspace:
 WS = _Workspace()
 
 
-def gemm_nn(A, B, C, alpha=1.0, beta=0.0, row_sub=None, algo=GEMM_AUTO):
+def gemm_nn(A, B, C, alpha=1.0, beta=0.0, row_sub=None, algo=GEMM_AUTO, pred=None):
     m, k = A.shape
     k2, n = B.shape
     assert k == k2 and C.shape == (m, n), (A.shape, B.shape, C.shape)
     assert A.dtype == B.dtype == C.dtype
     check(lib().rsvd_gemm_nn(dcode(A), m, n, k, float(alpha), _ptr(A), _ld(A), _ptr(B), _ld(B),
-                             float(beta), _ptr(C), _ld(C), _ptr(row_sub), int(algo), _stream()),
+                             float(beta), _ptr(C), _ld(C), _ptr(row_sub), int(algo), _ptr(pred), _stream()),
           "gemm_nn")
     return C
 
 
-def gemm_tn(A, B, C, alpha=1.0, beta=0.0, mu=None, colsum_b=None, algo=GEMM_AUTO):
+def gemm_tn(A, B, C, alpha=1.0, beta=0.0, mu=None, colsum_b=None, algo=GEMM_AUTO, pred=None):
     """C (k x n) = alpha (A^T B - mu colsum_b^T) + beta C, A m x k, B m x n."""
     m, k = A.shape
     m2, n = B.shape
@@ -86,16 +86,16 @@ def gemm_tn(A, B, C, alpha=1.0, beta=0.0, mu=None, colsum_b=None, algo=GEMM_AUTO
     ws = WS.get(nbytes, A.device)
     check(L.rsvd_gemm_tn(dcode(A), dcode(C), m, n, k, float(alpha), _ptr(A), _ld(A), _ptr(B), _ld(B),
                          float(beta), _ptr(C), _ld(C), _ptr(mu), _ptr(colsum_b), _ptr(ws), ws.numel(),
-                         int(algo), _stream()), "gemm_tn")
+                         int(algo), _ptr(pred), _stream()), "gemm_tn")
     return C
 
 
-def gram(V, out=None, algo=GEMM_AUTO):
+def gram(V, out=None, algo=GEMM_AUTO, pred=None):
     """FP64 Gram V^T V."""
     p = V.shape[1]
     if out is None:
         out = torch.empty((p, p), dtype=torch.float64, device=V.device)
-    return gemm_tn(V, V, out, algo=algo)
+    return gemm_tn(V, V, out, algo=algo, pred=pred)
 
 
 def colreduce(X, square=True, out=None):
@@ -109,26 +109,26 @@ def colreduce(X, square=True, out=None):
     return out
 
 
-def chol_deflate(G, ref2, tau2, T, mask, ndef, running=None, active=None):
+def chol_deflate(G, ref2, tau2, T, mask, ndef, running=None, active=None, pred=None):
     p = G.shape[0]
     L = lib()
     ws = WS.get(L.rsvd_chol_deflate_ws_bytes(p), G.device)
     check(L.rsvd_chol_deflate(p, _ptr(G), _ld(G), _ptr(ref2), float(tau2), _ptr(T), _ld(T), _ptr(mask),
-                              _ptr(ndef), _ptr(running), _ptr(active), _ptr(ws), ws.numel(), _stream()),
-          "chol_deflate")
+                              _ptr(ndef), _ptr(running), _ptr(active), _ptr(ws), ws.numel(), _ptr(pred),
+                              _stream()), "chol_deflate")
 
 
-def mask_cols(X, keep):
+def mask_cols(X, keep, pred=None):
     n, p = X.shape
-    check(lib().rsvd_mask_cols(dcode(X), n, p, _ptr(X), _ld(X), _ptr(keep), _stream()), "mask_cols")
+    check(lib().rsvd_mask_cols(dcode(X), n, p, _ptr(X), _ld(X), _ptr(keep), _ptr(pred), _stream()), "mask_cols")
     return X
 
 
-def insert_fill(X, mask, ndef, seed, row_offset=0, n_total=None):
+def insert_fill(X, mask, ndef, seed, row_offset=0, n_total=None, pred=None):
     n, p = X.shape
     n_total = n if n_total is None else int(n_total)
     check(lib().rsvd_insert_fill(dcode(X), n, p, _ptr(X), _ld(X), _ptr(mask), _ptr(ndef),
-                                 ctypes.c_uint64(int(seed)), int(row_offset), n_total, _stream()),
+                                 ctypes.c_uint64(int(seed)), int(row_offset), n_total, _ptr(pred), _stream()),
           "insert_fill")
 
 
@@ -165,6 +165,23 @@ def eig_select(M, V, k, evals=None, evecs=None):
     return evals, evecs
 
 
+def syev_topk(M, k, evals=None, evecs=None, info=None):
+    """Top-k eigenpairs of symmetric M (descending). Returns device tensors
+    (evals[k], evecs[w x k], info[int32: ok, _])."""
+    w = M.shape[0]
+    if evals is None:
+        evals = torch.empty(k, dtype=torch.float64, device=M.device)
+    if evecs is None:
+        evecs = torch.empty((w, k), dtype=torch.float64, device=M.device)
+    if info is None:
+        info = torch.zeros(4, dtype=torch.int32, device=M.device)
+    L = lib()
+    ws = WS.get(L.rsvd_syev_topk_ws_bytes(w, k), M.device)
+    check(L.rsvd_syev_topk(w, _ptr(M), _ld(M), k, _ptr(evals), _ptr(evecs), _ld(evecs), _ptr(info), _ptr(ws),
+                           ws.numel(), _stream()), "syev_topk")
+    return evals, evecs, info
+
+
 def canonicalize_signs(X):
     n, k = X.shape
     L = lib()
@@ -191,11 +208,11 @@ def flip_by_sign(X, sign_val):
     return X
 
 
-def convert(src, dst):
+def convert(src, dst, pred=None):
     assert src.shape == dst.shape
     r, c = src.shape
-    check(lib().rsvd_convert(dcode(src), dcode(dst), r, c, _ptr(src), _ld(src), _ptr(dst), _ld(dst), _stream()),
-          "convert")
+    check(lib().rsvd_convert(dcode(src), dcode(dst), r, c, _ptr(src), _ld(src), _ptr(dst), _ld(dst), _ptr(pred),
+                             _stream()), "convert")
     return dst
 
 

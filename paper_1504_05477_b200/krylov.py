@@ -101,6 +101,7 @@ class Workspace:
         self.T = torch.empty((p, p), **f64)
         self.mask = torch.empty(p, **i32)
         self.ndef = torch.zeros(2, **i32)
+        self.ndef_r1 = torch.zeros(2, **i32)
         self.mask2 = torch.empty(p, **i32)
         self.ndef2 = torch.zeros(2, **i32)
         self.ref2 = torch.empty(p, **f64)
@@ -108,21 +109,29 @@ class Workspace:
         self.ndef_total = torch.zeros(1, **i32)
 
 
-def _cast_small(ops, T64, dtype, out=None):
+def rows_buffer(n, p, dtype, device):
+    """n x p work block whose rows start on 16-byte boundaries (leading
+    dimension padded to a multiple of 4 elements): the tensor-core GEMMs
+    read their A operand through TMA, which needs 16-byte aligned rows."""
+    p4 = (p + 3) // 4 * 4
+    return torch.empty((n, p4), dtype=dtype, device=device)[:, :p]
+
+
+def _cast_small(ops, T64, dtype, out=None, pred=None):
     if dtype == torch.float64:
         return T64
     if out is None:
         out = torch.empty(T64.shape, dtype=dtype, device=T64.device)
-    return ops.convert(T64, out)
+    return ops.convert(T64, out, pred=pred)
 
 
-def project_out(ops, comm, Qp, V, tmp_c):
+def project_out(ops, comm, Qp, V, tmp_c, pred=None):
     """V <- V - Qp (Qp^T V)  (one block classical Gram-Schmidt pass)."""
     if Qp is None or Qp.shape[1] == 0:
         return V
-    ops.gemm_tn(Qp, V, tmp_c)
+    ops.gemm_tn(Qp, V, tmp_c, pred=pred)
     comm.allreduce(tmp_c)
-    ops.gemm_nn(Qp, tmp_c, V, alpha=-1.0, beta=1.0)
+    ops.gemm_nn(Qp, tmp_c, V, alpha=-1.0, beta=1.0, pred=pred)
     return V
 
 
@@ -141,6 +150,15 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
       (factor.py:106-112).
     Final: one projection + CholeskyQR step.
     """
+    if V.data_ptr() % 16 != 0:
+        # the tensor-core GEMMs read their A operand through TMA, which needs a
+        # 16-byte aligned base: work on an aligned copy of a misaligned block
+        # view (e.g. block j of width p = 50 inside the n x w basis)
+        Vw = rows_buffer(V.shape[0], V.shape[1], V.dtype, V.device)
+        ops.convert(V, Vw)
+        orth_block(ops, comm, Vw, tmp, ws, Qp=Qp, ref2=ref2, running=running, n_total=n_total,
+                   row_offset=row_offset, tau=tau, deflation_count=deflation_count, two_round=two_round)
+        return ops.convert(Vw, V)
     dtype = V.dtype
     p = V.shape[1]
     if two_round is None:
@@ -161,28 +179,31 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
     ops.gram(V, G)
     comm.allreduce(G)
     if two_round and tau > 0.0:
-        ops.chol_deflate(G, ref2, tau * tau, T, mask, ws.ndef, None)
+        r1 = ws.ndef_r1  # round-1 [count, base]: round 2 runs on the device only if count > 0
+        ops.chol_deflate(G, ref2, tau * tau, T, mask, r1, None)
         ops.gemm_nn(V, _cast_small(ops, T, dtype), tmp)  # Q1 raw (zero columns at rejected slots)
-        Q1 = torch.empty_like(tmp)
+        Q1 = rows_buffer(tmp.shape[0], p, dtype, tmp.device)
         ops.gram(tmp, G)
         comm.allreduce(G)
         ops.chol_deflate(G, None, 0.0, T, ws.mask2[:p], ws.ndef2, None)
         ops.gemm_nn(tmp, _cast_small(ops, T, dtype), Q1)  # Q1 clean
-        ops.mask_cols(V, mask)  # keep only the rejected columns' residuals
+        ws.ndef.zero_()
+        ops.mask_cols(V, mask, pred=r1)  # keep only the rejected columns' residuals
         c2 = torch.empty((p, p), dtype=dtype, device=V.device)
         if has_prev:
-            project_out(ops, comm, Qp, V, tmp_c)
-        project_out(ops, comm, Q1, V, c2)
+            project_out(ops, comm, Qp, V, tmp_c, pred=r1)
+        project_out(ops, comm, Q1, V, c2, pred=r1)
         if has_prev:
-            project_out(ops, comm, Qp, V, tmp_c)
-        project_out(ops, comm, Q1, V, c2)
-        ops.gram(V, G)
+            project_out(ops, comm, Qp, V, tmp_c, pred=r1)
+        project_out(ops, comm, Q1, V, c2, pred=r1)
+        ops.gram(V, G, pred=r1)
         comm.allreduce(G)
         ref = ref2 if ref2 is not None else ws.ref_orig[:p]
         rt = REF_RTOL_BY[dtype]
-        ops.chol_deflate(G, ref, rt * rt, T, ws.mask2[:p], ws.ndef, running, mask)
-        ops.gemm_nn(V, _cast_small(ops, T, dtype), Q1, beta=1.0)  # survivors join the kept columns
-        ops.insert_fill(Q1, ws.mask2[:p], ws.ndef, QR_FILL_SEED, row_offset, n_total)
+        ops.chol_deflate(G, ref, rt * rt, T, ws.mask2[:p], ws.ndef, running, mask, pred=r1)
+        # survivors join the kept columns
+        ops.gemm_nn(V, _cast_small(ops, T, dtype, pred=r1), Q1, beta=1.0, pred=r1)
+        ops.insert_fill(Q1, ws.mask2[:p], ws.ndef, QR_FILL_SEED, row_offset, n_total, pred=r1)
         out = Q1
     else:
         ops.chol_deflate(G, ref2, tau * tau, T, mask, ws.ndef, running)
@@ -219,8 +240,8 @@ def sketch_basis(ops, comm, op, Pi, ws, n_total, row_offset):
     """rsvd.py:224-226: b0 = mgs(A Pi)."""
     n = op.local_rows
     p = Pi.shape[1]
-    Y = torch.empty((n, p), dtype=op.dtype, device=op.device)
-    tmp = torch.empty_like(Y)
+    Y = rows_buffer(n, p, op.dtype, op.device)
+    tmp = rows_buffer(n, p, op.dtype, op.device)
     op.apply(Pi, Y)
     running = torch.zeros(1, dtype=torch.int32, device=op.device)
     orth_block(ops, comm, Y, tmp, ws, running=running, n_total=n_total, row_offset=row_offset)
@@ -239,8 +260,8 @@ def bk_basis(ops, comm, op, Pi, q, ws, n_total, row_offset):
     cap_blocks = max(1, min(n_total, d) // p)
     n_blocks = min(q + 1, cap_blocks)
     dev, dt = op.device, op.dtype
-    K = torch.empty((n, n_blocks * p), dtype=dt, device=dev)
-    tmp = torch.empty((n, p), dtype=dt, device=dev)
+    K = rows_buffer(n, n_blocks * p, dt, dev)
+    tmp = rows_buffer(n, p, dt, dev)
     C = torch.empty((d, p), dtype=dt, device=dev)
     running = torch.zeros(1, dtype=torch.int32, device=dev)
     b0 = K[:, :p]
@@ -277,8 +298,8 @@ def si_basis(ops, comm, op, Pi, q, every, ws, n_total, row_offset):
     d = op.shape[1]
     p = Pi.shape[1]
     dev, dt = op.device, op.dtype
-    b = torch.empty((n, p), dtype=dt, device=dev)
-    tmp = torch.empty_like(b)
+    b = rows_buffer(n, p, dt, dev)
+    tmp = rows_buffer(n, p, dt, dev)
     C = torch.empty((d, p), dtype=dt, device=dev)
     running = torch.zeros(1, dtype=torch.int32, device=dev)
     op.apply(Pi, b)
@@ -317,9 +338,9 @@ def rayleigh_ritz(ops, comm, op, Q, k, n_total, row_offset, sign_fn=None):
     comm.allreduce(W)
     M = torch.empty((w, w), dtype=torch.float64, device=dev)
     ops.gram(W, M)
-    V = torch.eye(w, dtype=torch.float64, device=dev)
-    info, off = ops.jacobi_sweeps(M, V, JACOBI_TOL, JACOBI_MAX_SWEEPS)
-    evals, Uk = ops.eig_select(M, V, k)
+    # top-k eigenpairs only (rsvd.py:217-220 uses eigvecs[:, :k], eigvals[:k])
+    evals, Uk, info = ops.syev_topk(M, k)
+    off = torch.zeros(1, dtype=torch.float64, device=dev)
     n = Q.shape[0]
     if Q.dtype == torch.float64:
         Z = torch.empty((n, k), dtype=torch.float64, device=dev)
@@ -327,13 +348,13 @@ def rayleigh_ritz(ops, comm, op, Q, k, n_total, row_offset, sign_fn=None):
     else:
         Uk32 = torch.empty((w, k), dtype=Q.dtype, device=dev)
         ops.convert(Uk, Uk32)
-        Z32 = torch.empty((n, k), dtype=Q.dtype, device=dev)
+        Z32 = rows_buffer(n, k, Q.dtype, dev)
         ops.gemm_nn(Q, Uk32, Z32)
-        Z = torch.empty((n, k), dtype=torch.float64, device=dev)
+        Z = rows_buffer(n, k, torch.float64, dev)
         ops.convert(Z32, Z)
         # FP64 re-orthonormalization of the n x k Z (CholeskyQR2)
         ws = Workspace(dev, k)
-        tmp = torch.empty_like(Z)
+        tmp = rows_buffer(n, k, torch.float64, dev)
         orth_block(ops, comm, Z, tmp, ws, tau=0.0, n_total=n_total, row_offset=row_offset)
     if sign_fn is None:
         ops.canonicalize_signs(Z)

@@ -12,7 +12,13 @@ _G = 0x9E3779B97F4A7C15
 _M = (1 << 64) - 1
 
 
-def gemm_nn(A, B, C, alpha=1.0, beta=0.0, row_sub=None, algo=0):
+def _off(pred):
+    return pred is not None and int(pred.reshape(-1)[0]) == 0
+
+
+def gemm_nn(A, B, C, alpha=1.0, beta=0.0, row_sub=None, algo=0, pred=None):
+    if _off(pred):
+        return C
     r = A.double() @ B.double()
     if row_sub is not None:
         r = r - row_sub.view(1, -1)
@@ -23,7 +29,9 @@ def gemm_nn(A, B, C, alpha=1.0, beta=0.0, row_sub=None, algo=0):
     return C
 
 
-def gemm_tn(A, B, C, alpha=1.0, beta=0.0, mu=None, colsum_b=None, algo=0):
+def gemm_tn(A, B, C, alpha=1.0, beta=0.0, mu=None, colsum_b=None, algo=0, pred=None):
+    if _off(pred):
+        return C
     r = A.double().T @ B.double()
     if mu is not None:
         r = r - mu.view(-1, 1) * colsum_b.view(1, -1)
@@ -34,10 +42,10 @@ def gemm_tn(A, B, C, alpha=1.0, beta=0.0, mu=None, colsum_b=None, algo=0):
     return C
 
 
-def gram(V, out=None, algo=0):
+def gram(V, out=None, algo=0, pred=None):
     if out is None:
         out = torch.empty((V.shape[1], V.shape[1]), dtype=torch.float64)
-    return gemm_tn(V, V, out)
+    return gemm_tn(V, V, out, pred=pred)
 
 
 def colreduce(X, square=True, out=None):
@@ -48,12 +56,16 @@ def colreduce(X, square=True, out=None):
     return out
 
 
-def mask_cols(X, keep):
+def mask_cols(X, keep, pred=None):
+    if _off(pred):
+        return X
     X[:, keep == 0] = 0
     return X
 
 
-def chol_deflate(G, ref2, tau2, T, mask, ndef, running=None, active=None):
+def chol_deflate(G, ref2, tau2, T, mask, ndef, running=None, active=None, pred=None):
+    if _off(pred):
+        return
     g = G.numpy().copy()
     p = g.shape[0]
     S = np.triu(g)
@@ -87,7 +99,9 @@ def chol_deflate(G, ref2, tau2, T, mask, ndef, running=None, active=None):
         running[0] = base + int(m.sum())
 
 
-def insert_fill(X, mask, ndef, seed, row_offset=0, n_total=None):
+def insert_fill(X, mask, ndef, seed, row_offset=0, n_total=None, pred=None):
+    if _off(pred):
+        return
     n, p = X.shape
     n_total = n if n_total is None else n_total
     if int(ndef[0]) == 0:
@@ -108,6 +122,12 @@ def jacobi_sweeps(M, V, tol, max_sweeps, info=None, off=None):
     M.copy_(torch.from_numpy(m))
     V.copy_(torch.from_numpy(v))
     return torch.tensor([int(conv), sweeps, 0, 0], dtype=torch.int32), torch.tensor([offv])
+
+
+def syev_topk(M, k, evals=None, evecs=None, info=None):
+    vals, vecs = o.symmetric_eig(M.numpy())
+    return (torch.from_numpy(vals[:k].copy()), torch.from_numpy(np.ascontiguousarray(vecs[:, :k])),
+            torch.tensor([1, 0, 0, 0], dtype=torch.int32))
 
 
 def eig_select(M, V, k, evals=None, evecs=None):
@@ -136,7 +156,9 @@ def flip_by_sign(X, sign_val):
     return X
 
 
-def convert(src, dst):
+def convert(src, dst, pred=None):
+    if _off(pred):
+        return dst
     dst.copy_(src.to(dst.dtype))
     return dst
 

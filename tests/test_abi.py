@@ -58,7 +58,7 @@ def test_invalid_args_map_to_status():
     assert st == _lib.RSVD_ERR_INVALID
     assert "gauss_fill" in _lib.last_error()
     # a bad dtype is rejected before any device work
-    st = L.rsvd_gemm_nn(7, 1, 1, 1, 1.0, None, 1, None, 1, 0.0, None, 1, None, 0, None)
+    st = L.rsvd_gemm_nn(7, 1, 1, 1, 1.0, None, 1, None, 1, 0.0, None, 1, None, 0, None, None)
     assert st == _lib.RSVD_ERR_INVALID
     try:
         _lib.check(st, "gemm_nn")

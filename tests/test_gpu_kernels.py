@@ -217,3 +217,33 @@ def test_canonicalize_signs_first_max_tie(ops):
     Z = _t(big)
     ops.canonicalize_signs(Z)
     assert np.array_equal(Z.cpu().numpy(), o.canonicalize_signs(big.copy()))
+
+
+@pytest.mark.parametrize("w,k,kind", [(1, 1, "rand"), (2, 2, "rand"), (3, 1, "rand"), (50, 50, "rand"),
+                                      (200, 20, "inv2"), (600, 50, "inv"), (601, 600, "rand"),
+                                      (300, 40, "cluster"), (400, 30, "repeated"), (1200, 200, "clustered_c4")])
+def test_syev_topk(ops, w, k, kind):
+    rng = np.random.default_rng(w + k)
+    if kind == "rand":
+        base = rng.standard_normal((w, w))
+        sym = 0.5 * (base + base.T)
+    else:
+        Q, _ = np.linalg.qr(rng.standard_normal((w, w)))
+        i = np.arange(1, w + 1, dtype=float)
+        lam = {"inv2": 1.0 / i ** 2, "inv": 1.0 / i,
+               "cluster": np.where(i <= 60, 1.0 + 1e-9 * i, 0.5 / i),
+               "repeated": np.where(i <= 10, 2.0, 1.0 / i),
+               "clustered_c4": np.where(i <= 200, (1 - 0.001 * i) ** 2, (0.5 / i) ** 2)}[kind]
+        sym = (Q * lam) @ Q.T
+        sym = 0.5 * (sym + sym.T)
+    M = _t(sym)
+    evals, evecs, info = ops.syev_topk(M, k)
+    assert int(info[0]) == 1
+    ref = np.sort(np.linalg.eigvalsh(sym))[::-1][:k]
+    ev = evals.cpu().numpy()
+    scale = np.abs(np.linalg.eigvalsh(sym)).max()
+    assert np.max(np.abs(ev - ref)) < 1e-13 * scale * max(1.0, np.sqrt(w / 64))
+    E = evecs.cpu().numpy()
+    assert np.max(np.abs(E.T @ E - np.eye(k))) < 1e-11
+    assert np.max(np.abs(sym @ E - E * ev)) < 1e-12 * scale * max(1.0, np.sqrt(w / 64))
+    assert np.allclose(M.cpu().numpy(), sym)  # input untouched

@@ -110,3 +110,18 @@ def test_auto_dispatch_falls_back_on_misaligned(ops):
     assert _rel(C.cpu(), A.double().cpu() @ B.double().cpu()) < 5e-6
     with pytest.raises(ValueError):
         ops.gemm_nn(A, B, C, algo=TC)
+
+
+@pytest.mark.parametrize("off", [1, 2, 3])
+def test_tc_rejects_misaligned_a_and_auto_falls_back(ops, off):
+    # TMA needs 16-byte aligned boxes: a column window starting off floats
+    # into an aligned buffer must not take the tensor-core path
+    n, w, p = 9000, 400, 50
+    Big = _r((n, w), 20 + off).float().cuda()
+    V = Big[:, off:off + p]
+    T = _r((p, p), 30).float().cuda()
+    C = torch.empty((n, p), dtype=torch.float32, device="cuda")
+    with pytest.raises(ValueError):
+        ops.gemm_nn(V, T, C, algo=TC)
+    ops.gemm_nn(V, T, C)
+    assert _rel(C.cpu(), V.double().cpu() @ T.double().cpu()) < 5e-6
