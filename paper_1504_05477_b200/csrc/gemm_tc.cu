@@ -495,7 +495,7 @@ int64_t tn_splits_tc(int64_t Mop, int64_t Nop, int64_t Kop) {
     // that the reduction stays short.
     int bn = pick_bn(Nop);
     int64_t tiles = cdiv(Mop, BM) * cdiv(Nop, bn);
-    int64_t target = (int64_t)sm_count();
+    int64_t target = (int64_t)sm_count() * 2;
     int64_t s = cdiv(target, tiles);
     if (s > 64) s = 64;
     int64_t max_s = cdiv(Kop, 8 * BK);

@@ -102,6 +102,8 @@ class Workspace:
         self.mask = torch.empty(p, **i32)
         self.ndef = torch.zeros(2, **i32)
         self.ndef_r1 = torch.zeros(2, **i32)
+        self.ndef_r3 = torch.zeros(2, **i32)
+        self.ref_fin = torch.empty(p, **f64)
         self.mask2 = torch.empty(p, **i32)
         self.ndef2 = torch.zeros(2, **i32)
         self.ref2 = torch.empty(p, **f64)
@@ -213,12 +215,31 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
         out = tmp
     if deflation_count is not None:
         deflation_count += ws.ndef[:1]
+    # Final pass. A replacement column that collapses against the columns
+    # before it (residual <= 1e-6 of its norm, factor.py:111) is redrawn from
+    # the next vectors of the same fill stream, as the reference's retry loop
+    # does (factor.py:106-116); the repair steps run only if that happened.
+    ref_f = ws.ref_fin[:p]
+    ops.colreduce(out, True, ref_f)
+    comm.allreduce(ref_f)
     if has_prev:
         project_out(ops, comm, Qp, out, tmp_c)
     ops.gram(out, G)
     comm.allreduce(G)
-    ops.chol_deflate(G, None, 0.0, T, ws.mask2[:p], ws.ndef2, None)
+    r3 = ws.ndef_r3
+    ops.chol_deflate(G, ref_f, 1e-12, T, ws.mask2[:p], r3, running)
     ops.gemm_nn(out, _cast_small(ops, T, dtype), V)
+    # repair (runs only if a column collapsed): next stream vectors into the
+    # collapsed slots, re-project, CholeskyQR
+    ops.insert_fill(V, ws.mask2[:p], r3, QR_FILL_SEED, row_offset, n_total, pred=r3)
+    if has_prev:
+        project_out(ops, comm, Qp, V, tmp_c, pred=r3)
+        project_out(ops, comm, Qp, V, tmp_c, pred=r3)
+    ops.gram(V, G, pred=r3)
+    comm.allreduce(G)
+    ops.chol_deflate(G, None, 0.0, T, ws.mask2[:p], ws.ndef2, None, pred=r3)
+    ops.gemm_nn(V, _cast_small(ops, T, dtype, pred=r3), out, pred=r3)
+    ops.convert(out, V, pred=r3)
     if dtype != torch.float64:
         # FP32 storage: one more CholeskyQR step (CholeskyQR2 cleanup)
         ops.gram(V, G)
