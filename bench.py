@@ -201,18 +201,23 @@ def run_ours(args):
     op.apply = timed(orig_apply, "AX")
     op.apply_t = timed(orig_apply_t, "ATY")
 
+    graphed = rsvd.GraphedFactorization(op, cfg, comm=comm) if args.graph else None
+
     def step():
-        df = rsvd.run_device(op, cfg, comm=comm, Pi=Pi)
-        return df
+        if graphed is not None:
+            return graphed.run(Pi)
+        return rsvd.run_device(op, cfg, comm=comm, Pi=Pi)
 
     for _ in range(args.warmup):
         df = step()
     torch.cuda.synchronize()
-    launches = count_launches(step) if rank == 0 and args.count_launches else None
+    # kernels per factorization, counted on an eager replica of the step (a
+    # graph replay issues the identical kernel sequence in one launch)
+    launches = (count_launches(lambda: rsvd.run_device(op, cfg, comm=comm, Pi=Pi))
+                if rank == 0 and args.count_launches else None)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    recording[0] = True
     with ClockSampler(local) as clk:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -221,7 +226,13 @@ def run_ours(args):
             df = step()
         e1.record()
         torch.cuda.synchronize()
-    recording[0] = False
+    # per-kernel durations of the dominant products: the same step run eagerly
+    # (graph replays cannot host-record events) with CUDA events around every
+    # A.X / A^T.Y launch on the launching stream
+    recording[0] = True
+    for _ in range(2):
+        rsvd.run_device(op, cfg, comm=comm, Pi=Pi)
+    torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -437,6 +448,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--count-launches", action="store_true", default=True)
     ap.add_argument("--cpu-budget", type=float, default=25.0)
+    ap.add_argument("--graph", type=int, default=1, help="replay the factorization as a CUDA graph")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

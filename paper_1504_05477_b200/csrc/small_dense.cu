@@ -139,14 +139,16 @@ k_chol_deflate(int64_t p, const double* __restrict__ G, int64_t ldg,
 }
 
 // Fast path for p <= kFastP: the packed Schur complement lives in typed
-// shared memory (LDS/STS, no generic addressing); two barriers per column
-// (decide pivot | trailing update + deferred scaling of the previous row);
-// T = R^{-1} by columns, one warp per column (back substitution with the
-// dot products split over lanes), column buffers in shared memory.
+// shared memory. Every thread evaluates the pivot test itself (no serial
+// thread-0 step), so a column costs one barrier; R's rows are scaled in one
+// pass at the end. T = R^{-1} is built by ROWS (row c of T solves
+// R^T s = e_c by forward substitution in axpy form), so every shared-memory
+// access walks a row of the packed triangle (no bank conflicts); one warp
+// per row, the row held in registers.
 constexpr int kFastP = 224;
 constexpr int kFastThreads = 1024;
-constexpr int kInvRegs = (kFastP + 31) / 32;
 
+template <int KR>
 __global__ void __launch_bounds__(kFastThreads)
 k_chol_fast(int p, const double* __restrict__ G, int64_t ldg, const double* __restrict__ ref2, double tau2,
             double* __restrict__ T, int64_t ldt, int32_t* __restrict__ mask, int32_t* __restrict__ ndef,
@@ -155,9 +157,9 @@ k_chol_fast(int p, const double* __restrict__ G, int64_t ldg, const double* __re
     extern __shared__ double S[];  // packed upper triangle of the Schur complement / R
     __shared__ double s_ref[kFastP];
     __shared__ double s_rinv[kFastP];  // 1 / R[j][j] (1 for deficient slots)
+    __shared__ double s_rdiag[kFastP];
     __shared__ int s_msk[kFastP];
     __shared__ int s_act[kFastP];
-    __shared__ int s_count;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     auto off = [p](int i, int j) { return i * p - (i * (i - 1)) / 2 + (j - i); };
     for (int i = warp; i < p; i += nwarps)
@@ -166,74 +168,109 @@ k_chol_fast(int p, const double* __restrict__ G, int64_t ldg, const double* __re
         s_ref[j] = ref2 ? ref2[j] : G[(int64_t)j * ldg + j];
         s_act[j] = active ? active[j] : 1;
     }
-    if (tid == 0) s_count = 0;
     __syncthreads();
+    int count = 0;
     for (int j = 0; j < p; ++j) {
+        // pivot test, redundantly in every thread (factor.py:105 analogue)
+        const double d = S[off(j, j)];
+        const int act = s_act[j];
+        const int def = !act || !(d > tau2 * s_ref[j]) || !(d > 0.0);
+        count += def && act;
+        if (!def) {
+            const double inv2 = 1.0 / d;
+            const double* __restrict__ rj = S + (off(j, j) - j);  // row j, unscaled, read-only this step
+            for (int a = j + 1 + warp; a < p; a += nwarps) {
+                const double ra = rj[a] * inv2;
+                double* __restrict__ rowa = S + (off(a, a) - a);
+                // batches of 8 independent elements: all loads, then all stores
+                for (int b0 = a + lane; b0 < p; b0 += 32 * 8) {
+                    double u[8], v[8];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) {
+                        const int b = b0 + 32 * t;
+                        u[t] = b < p ? rj[b] : 0.0;
+                        v[t] = b < p ? rowa[b] : 0.0;
+                    }
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) {
+                        const int b = b0 + 32 * t;
+                        if (b < p) rowa[b] = fma(-ra, u[t], v[t]);
+                    }
+                }
+            }
+        }
         if (tid == 0) {
-            const double d = S[off(j, j)];
-            const int act = s_act[j];
-            const int def = !act || !(d > tau2 * s_ref[j]) || !(d > 0.0);
             s_msk[j] = def ? (act ? 1 : 2) : 0;
-            if (def && act) ++s_count;
             const double rjj = def ? 1.0 : sqrt(d);
-            S[off(j, j)] = rjj;
+            s_rdiag[j] = rjj;
             s_rinv[j] = 1.0 / rjj;
         }
         __syncthreads();
-        const bool def = s_msk[j] != 0;
-        const double inv = s_rinv[j];
-        // trailing update with the unscaled row j: S(a,b) -= S(j,a) S(j,b) / d
-        if (!def) {
-            const double inv2 = inv * inv;
-            const int rj = off(j, 0);
-            for (int a = j + 1 + warp; a < p; a += nwarps) {
-                const double ra = S[rj + a] * inv2;
-                const int rowa = off(a, a) - a;
-                for (int b = a + lane; b < p; b += 32) S[rowa + b] -= ra * S[rj + b];
-            }
+    }
+    // scale the rows of R (deficient rows become e_j)
+    for (int i = warp; i < p; i += nwarps) {
+        const bool di = s_msk[i] != 0;
+        const double inv = s_rinv[i];
+        for (int j = i + lane; j < p; j += 32) {
+            const int o = off(i, j);
+            S[o] = (j == i) ? s_rdiag[i] : (di ? 0.0 : S[o] * inv);
         }
-        __syncthreads();
-        // now scale row j of R (its trailing consumers are done)
-        const int rj = off(j, 0);
-        for (int c = j + 1 + tid; c < p; c += blockDim.x) S[rj + c] = def ? 0.0 : S[rj + c] * inv;
-        // (next column's pivot reads S(j+1, j+1), not row j: no barrier needed here)
     }
     __syncthreads();
-    // T = R^{-1}: column c by one warp, x = R^{-1} e_c in registers (lane l
-    // holds rows l, l+32, ...); back substitution in axpy form: for b = c..0
-    // finalise x_b (broadcast by shuffle) and subtract R[a][b] x_b from all a < b.
-    for (int c = warp; c < p; c += nwarps) {
-        double x[kInvRegs];
+    // rows of T = R^{-1}: row c is s with R^T s = e_c (s_a = 0 for a < c).
+    // Each warp carries NI rows at once (independent chains -> ILP); steps
+    // b < c are exact no-ops for row c (its s_b is 0), so the rows share one
+    // loop starting at the smallest c.
+    constexpr int NI = KR <= 2 ? 4 : (KR <= 4 ? 2 : 1);  // stay within 64 registers
+    for (int c0 = warp; c0 < p; c0 += nwarps * NI) {
+        double x[NI][KR];
 #pragma unroll
-        for (int r = 0; r < kInvRegs; ++r) x[r] = (lane + 32 * r == c) ? 1.0 : 0.0;
-        for (int b = c; b >= 0; --b) {
+        for (int i = 0; i < NI; ++i)
+#pragma unroll
+            for (int r = 0; r < KR; ++r) x[i][r] = (lane + 32 * r == c0 + i * nwarps) ? 1.0 : 0.0;
+        for (int b = c0; b < p; ++b) {
             const int rb = b >> 5, lb = b & 31;
-            double xb = 0.0;
+            const double* rowb = S + (off(b, b) - b);
+            const double rinvb = s_rinv[b];
+            double rrow[KR];
 #pragma unroll
-            for (int r = 0; r < kInvRegs; ++r)
-                if (r == rb) xb = x[r];
-            xb = __shfl_sync(0xffffffffu, xb, lb) * s_rinv[b];
-#pragma unroll
-            for (int r = 0; r < kInvRegs; ++r) {
+            for (int r = 0; r < KR; ++r) {
                 const int a = lane + 32 * r;
-                if (a == b) x[r] = xb;
-                else if (a < b) x[r] -= S[off(a, b)] * xb;
+                rrow[r] = (a > b && a < p) ? rowb[a] : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                double xb = 0.0;
+#pragma unroll
+                for (int r = 0; r < KR; ++r)
+                    if (r == rb) xb = x[i][r];
+                xb = __shfl_sync(0xffffffffu, xb, lb) * rinvb;
+#pragma unroll
+                for (int r = 0; r < KR; ++r) {
+                    const int a = lane + 32 * r;
+                    x[i][r] = (a == b) ? xb : fma(-rrow[r], xb, x[i][r]);
+                }
             }
         }
-        const bool zc = s_msk[c] != 0;
 #pragma unroll
-        for (int r = 0; r < kInvRegs; ++r) {
-            const int a = lane + 32 * r;
-            if (a < p) T[(int64_t)a * ldt + c] = (zc || s_msk[a] || a > c) ? 0.0 : x[r];
+        for (int i = 0; i < NI; ++i) {
+            const int c = c0 + i * nwarps;
+            if (c >= p) continue;
+            const bool zc = s_msk[c] != 0;
+#pragma unroll
+            for (int r = 0; r < KR; ++r) {
+                const int a = lane + 32 * r;
+                if (a < p) T[(int64_t)c * ldt + a] = (zc || s_msk[a] || a < c) ? 0.0 : x[i][r];
+            }
         }
     }
     __syncthreads();
     for (int j = tid; j < p; j += blockDim.x) mask[j] = s_msk[j] == 1 ? 1 : 0;
     if (tid == 0) {
         const int32_t base = running ? running[0] : 0;
-        ndef[0] = s_count;
+        ndef[0] = count;
         ndef[1] = base;
-        if (running) running[0] = base + s_count;
+        if (running) running[0] = base + count;
     }
 }
 
@@ -464,10 +501,27 @@ int chol_deflate(int64_t p, const double* G, int64_t ldg, const double* ref2, do
     if (p == 0) return RSVD_OK;
     if (p <= kFastP) {
         const size_t sm = (size_t)(p * (p + 1) / 2) * sizeof(double);
-        if (sm > 48 * 1024)
-            RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_chol_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k_chol_fast<<<1, kFastThreads, sm, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active,
-                                                 pred);
+        const int threads = kFastThreads;
+        const int kr = (int)((p + 31) / 32);
+#define RSVD_CHOL_CASE(K)                                                                                   \
+    case K: {                                                                                             \
+        if (sm > 48 * 1024)                                                                               \
+            RSVD_CHECK_CUDA(                                                                              \
+                cudaFuncSetAttribute(k_chol_fast<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+        k_chol_fast<K><<<1, threads, sm, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active, \
+                                               pred);                                                     \
+        break;                                                                                            \
+    }
+        switch (kr) {
+            RSVD_CHOL_CASE(1)
+            RSVD_CHOL_CASE(2)
+            RSVD_CHOL_CASE(3)
+            RSVD_CHOL_CASE(4)
+            RSVD_CHOL_CASE(5)
+            RSVD_CHOL_CASE(6)
+            default: RSVD_CHOL_CASE(7)
+        }
+#undef RSVD_CHOL_CASE
         RSVD_CHECK_LAUNCH();
         return RSVD_OK;
     }

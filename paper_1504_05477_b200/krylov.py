@@ -183,12 +183,15 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
     if two_round and tau > 0.0:
         r1 = ws.ndef_r1  # round-1 [count, base]: round 2 runs on the device only if count > 0
         ops.chol_deflate(G, ref2, tau * tau, T, mask, r1, None)
-        ops.gemm_nn(V, _cast_small(ops, T, dtype), tmp)  # Q1 raw (zero columns at rejected slots)
         Q1 = rows_buffer(tmp.shape[0], p, dtype, tmp.device)
-        ops.gram(tmp, G)
+        ops.gemm_nn(V, _cast_small(ops, T, dtype), Q1)  # Q1 (zero columns at rejected slots)
+        # round 2 needs Q1 orthonormal enough to project residuals against:
+        # one CholeskyQR step, only when round 2 will run
+        ops.gram(Q1, G, pred=r1)
         comm.allreduce(G)
-        ops.chol_deflate(G, None, 0.0, T, ws.mask2[:p], ws.ndef2, None)
-        ops.gemm_nn(tmp, _cast_small(ops, T, dtype), Q1)  # Q1 clean
+        ops.chol_deflate(G, None, 0.0, T, ws.mask2[:p], ws.ndef2, None, pred=r1)
+        ops.gemm_nn(Q1, _cast_small(ops, T, dtype, pred=r1), tmp, pred=r1)
+        ops.convert(tmp, Q1, pred=r1)
         ws.ndef.zero_()
         ops.mask_cols(V, mask, pred=r1)  # keep only the rejected columns' residuals
         c2 = torch.empty((p, p), dtype=dtype, device=V.device)

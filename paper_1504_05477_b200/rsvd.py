@@ -286,7 +286,9 @@ def _sign_fn_for(comm):
 
 def run_device(op, cfg, comm=None, Pi=None):
     """The whole path on the device for an already-uploaded operator.
-    Validation as _run (rsvd.py:263-270); no host synchronisation."""
+    Validation as _run (rsvd.py:263-270); no host synchronisation. ``Pi`` is
+    the host start block (default: drawn from SeededRng(cfg.seed)) or an
+    already-uploaded device tensor."""
     n, d = op.shape
     if cfg.k > min(n, d):
         raise ValueError("k must not exceed min(n, d)")
@@ -298,7 +300,10 @@ def run_device(op, cfg, comm=None, Pi=None):
         raise ValueError("block width p exceeds n; no Krylov block fits")
     if Pi is None:
         Pi = gaussian(d, p, SeededRng(cfg.seed)).data
-    pi_dev = torch.from_numpy(np.ascontiguousarray(Pi)).to(device=op.device, dtype=op.dtype, non_blocking=True)
+    if isinstance(Pi, torch.Tensor) and Pi.is_cuda:
+        pi_dev = Pi
+    else:
+        pi_dev = torch.from_numpy(np.array(Pi, copy=True)).to(device=op.device, dtype=op.dtype, non_blocking=True)
     ws = krylov.Workspace(op.device, p)
     deflated = None
     if cfg.variant is Variant.SIMULTANEOUS_ITERATION:
@@ -312,6 +317,44 @@ def run_device(op, cfg, comm=None, Pi=None):
         q_used = 0
     rr = krylov.rayleigh_ritz(ops, c, op, Q, cfg.k, n_total, row_offset, sign_fn=_sign_fn_for(comm))
     return DeviceFactorization(rr.Z, rr.sigma, rr.info, rr.off, rr.zerr, q_used, deflated)
+
+
+class GraphedFactorization:
+    """One factorization of a fixed operator/config captured as a CUDA graph.
+
+    Everything run_device enqueues is stream-ordered and free of host
+    synchronisation (data-dependent steps are device-side predicates), so the
+    ~2000 kernel launches of a factorization replay as one graph launch. The
+    start block is copied into a static device buffer before each replay; the
+    outputs are static device tensors (valid until the next replay)."""
+
+    def __init__(self, op, cfg, comm=None):
+        self.op, self.cfg, self.comm = op, cfg, comm
+        d = op.shape[1]
+        self.pi = torch.empty((d, cfg.p), dtype=op.dtype, device=op.device)
+        self.graph = None
+        self.out = None
+
+    def _capture(self):
+        # two eager runs size every workspace before capture (no allocation
+        # growth may happen while capturing)
+        for _ in range(2):
+            run_device(self.op, self.cfg, comm=self.comm, Pi=self.pi)
+        torch.cuda.synchronize(self.op.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.out = run_device(self.op, self.cfg, comm=self.comm, Pi=self.pi)
+        self.graph = g
+
+    def run(self, Pi=None):
+        if Pi is None:
+            Pi = gaussian(self.op.shape[1], self.cfg.p, SeededRng(self.cfg.seed)).data
+        src = Pi if isinstance(Pi, torch.Tensor) else torch.from_numpy(np.array(Pi, copy=True))
+        self.pi.copy_(src, non_blocking=True)
+        if self.graph is None:
+            self._capture()
+        self.graph.replay()
+        return self.out
 
 
 def _finish(df, cfg, t0, gather_z=None):
