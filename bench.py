@@ -346,64 +346,29 @@ def cpu_baseline(A_dev, cfgd, cfg, Pi, args):
 
 
 def reference_sample(A32, cfgd, cfg, Pi, budget_s=25.0):
+    """One full factorization by the reference algorithm on the box's host
+    cores: the oracle port (oracle/rsvd_oracle.py) — numpy/OpenBLAS products
+    as the reference's python backend (_kernels_py.py:48-49), the C
+    restatement of its compiled Jacobi (_kernels.pyx:127-192), its per-column
+    _mgs — on the same A upcast to FP64 (matrix.py:80) and the same Pi.
+    Timed like PartialSvdResult.wall_time_ms (rsvd.py:271-282)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import rsvd_oracle as o
 
     cores = os.cpu_count() or 1
-    A = A32.astype(np.float64)
+    A = np.ascontiguousarray(A32, dtype=np.float64)
     op = o.DenseOp(A)
-    n, d = A.shape
-    p = cfg.p
-    q = cfg.resolve_q(d)
-    nb = min(q + 1, max(1, min(n, d) // p))
-    w = nb * p
-    t = {}
+    op.apply(Pi[:, :1])  # BLAS thread-pool warm-up outside the timer
+    variant = cfg.variant.value if hasattr(cfg.variant, "value") else str(cfg.variant)
     t0 = time.perf_counter()
-    y = op.apply(Pi)
-    t["AX"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    b = o.mgs(y)
-    t["mgs_block"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    c = op.apply_transpose(b)
-    t["ATY"] = time.perf_counter() - t0
-    # final _mgs on the n x w basis: per-column cost grows with the column
-    # index (two BLAS-2 projections against all earlier columns); time a
-    # column window at the end and integrate the linear cost model.
-    K = np.empty((n, w))
-    for j in range(nb):
-        K[:, j * p:(j + 1) * p] = b  # same cost profile as the real basis
-    cols = min(p, 40)
-    Qh = np.ascontiguousarray(K[:, : w - cols])
-    t0 = time.perf_counter()
-    for j in range(cols):
-        v = K[:, w - cols + j].copy()
-        for _ in range(2):  # factor.py:93-98, two projections per column
-            v = v - Qh @ (Qh.T @ v)
-        float(np.linalg.norm(v))
-    t_tail = (time.perf_counter() - t0) / cols  # one column at index ~w
-    t["mgs_final"] = t_tail * w / 2.0  # column j costs ~ j/w of a tail column
-    # post-process: two A passes at width w, Q^T Y, Gram check, Jacobi, Q U_k
-    Qw = np.ascontiguousarray(K)
-    t0 = time.perf_counter()
-    W = op.apply_transpose(Qw[:, : min(w, 100)])
-    t["ATQ_100"] = time.perf_counter() - t0
-    t["post_A_passes"] = 2 * t["ATQ_100"] * (w / min(w, 100))
-    M = np.ascontiguousarray(W.T @ W)
-    m_w = min(w, 200)
-    base = np.random.default_rng(1).standard_normal((m_w, m_w))
-    Mw = base @ base.T
-    t0 = time.perf_counter()
-    o.symmetric_eig(Mw)
-    t_j = time.perf_counter() - t0
-    t["jacobi"] = t_j * (w / m_w) ** 3
-    total = t["AX"] * (1 + (nb - 1)) + t["ATY"] * (nb - 1) + t["mgs_block"] * nb + t["mgs_final"] + t["post_A_passes"] + t["jacobi"]
-    return {"value": total * 1e3, "unit": "ms", "cores": cores, "kind": "port",
-            "sample": ("oracle port (numpy/OpenBLAS products, C Jacobi) on the same A upcast to FP64 "
-                       "(matrix.py:80): stages timed once each (A.X, A^T.Y, one block _mgs, tail columns "
-                       "of the final _mgs, A^T Q at width 100, Jacobi at w=200) and scaled by their "
-                       "exact operation counts to one factorization"),
-            "stages_s": {k: float(v) for k, v in t.items()}}
+    r = o.factorize(op, cfg.k, variant, q=cfg.q, p=cfg.p, seed=cfg.seed)
+    secs = time.perf_counter() - t0
+    return {"value": secs * 1e3, "unit": "ms", "cores": cores, "kind": "port",
+            "sample": ("one full factorization of the same workload by the reference algorithm (oracle port: "
+                       "numpy/OpenBLAS products like the reference's python backend, C restatement of its "
+                       "Jacobi, per-column CGS2 _mgs) on the same A upcast to FP64 and the same Pi; "
+                       f"{cores} host threads (OPENBLAS_NUM_THREADS)"),
+            "sigma_head": [float(x) for x in r.sigma[:3]]}
 
 
 def run_reference(args):
@@ -423,9 +388,11 @@ def run_reference(args):
     A_host = A.cpu().numpy()
     del A
     vals = []
-    for i in range(args.warmup + args.steps):
+    # CPU runs have no warm-up state beyond the BLAS pool (primed inside
+    # reference_sample); warm-up steps are still executed, at most 1 of them
+    for i in range(min(args.warmup, 1) + args.steps):
         r = reference_sample(A_host, cfgd, cfg, Pi, budget_s=args.cpu_budget)
-        if i >= args.warmup:
+        if i >= min(args.warmup, 1):
             vals.append(r["value"])
     v = float(np.mean(vals))
     out = {"impl": "reference", "metric": "rank-k block-Krylov SVD wall time", "value": v, "unit": "ms",

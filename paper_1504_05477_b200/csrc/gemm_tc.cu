@@ -21,8 +21,8 @@
 // accumulates KCHUNK = 4 k-blocks (K = 128); two accumulator sets alternate
 // and four dedicated warps drain each finished chunk into round-to-nearest
 // FP32 registers while the tensor core fills the other set.
-// Warp roles (320 threads): w0 TMA producer, w1 MMA issuer (+TMEM alloc),
-// w2..w5 converters, w6..w9 accumulator drain + epilogue (w % 4 covers the
+// Warp roles (448 threads): w0 TMA producer, w1 MMA issuer (+TMEM alloc),
+// w2..w9 converters, w10..w13 accumulator drain + epilogue (w % 4 covers the
 // four TMEM lane quarters).
 // Pipelines: full[s] (TMA bytes landed), conv[s] (A split ready), empty[s]
 // (MMA done reading the stage, via tcgen05.commit), acc_full[2] / acc_empty[2]
@@ -37,8 +37,10 @@ namespace {
 
 constexpr int BM = 128;      // UMMA M
 constexpr int BK = 32;       // fp32 elements per 128-byte swizzle row
-constexpr int kThreads = 320;
-constexpr int kConvThreads = 128;
+constexpr int kConvWarps = 4;
+constexpr int kConvThreads = 32 * kConvWarps;
+constexpr int kDrainWarp0 = 2 + kConvWarps;      // first accumulator-drain warp
+constexpr int kThreads = 32 * (kDrainWarp0 + 4);
 constexpr int KCHUNK = 4;  // k-blocks accumulated in TMEM before a drain
 
 // ------------------------------------------------------------------ PTX
@@ -95,6 +97,28 @@ __device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, ui
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+// A operand from TMEM (lane = row, one 32-bit column per k), B from smem.
+__device__ __forceinline__ void tc_mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                               uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+        "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+        "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+        "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+        "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+        "r"(__float_as_uint(v[15])));
 }
 
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
@@ -162,13 +186,23 @@ struct TcParams {
 
 template <int BN, bool A_MN>
 struct TcCfg {
+    // A_lo in TMEM (tcgen05.mma .ts form) when the accumulators leave room:
+    // the smem stage then holds only raw A (the tensor core truncates FP32 to
+    // TF32 itself, so raw A *is* A_hi) and B_hi/B_lo -> deeper pipelines.
+    static constexpr bool LO_TMEM = BN <= 64;
     static constexpr int BNP = ((BN + 31) / 32) * 32;  // B tile padded to whole 32-wide atoms
     static constexpr int A_BYTES = BM * BK * 4;         // 16 KB
     static constexpr int B_BYTES = BNP * BK * 4;
-    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-    static constexpr int STAGES = (STAGE_BYTES * 4 <= 200 * 1024) ? 4 : ((STAGE_BYTES * 3 <= 200 * 1024) ? 3 : 2);
+    static constexpr int STAGE_BYTES = (LO_TMEM ? 1 : 2) * A_BYTES + 2 * B_BYTES;
+    static constexpr int ACC_COLS = 4 * BN;                 // 2 sets x (D0 | D1)
+    static constexpr int STAGES_SMEM = (200 * 1024) / STAGE_BYTES;
+    static constexpr int STAGES_TMEM = LO_TMEM ? (512 - ACC_COLS) / BK : 64;
+    static constexpr int STAGES_RAW = STAGES_SMEM < STAGES_TMEM ? STAGES_SMEM : STAGES_TMEM;
+    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
     static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-    static constexpr int TMEM_COLS = (4 * BN <= 128) ? 128 : (4 * BN <= 256) ? 256 : 512;  // 2 sets x (D0|D1)
+    static constexpr int TMEM_NEED = ACC_COLS + (LO_TMEM ? STAGES * BK : 0);
+    static constexpr int TMEM_COLS = TMEM_NEED <= 128 ? 128 : (TMEM_NEED <= 256 ? 256 : 512);
+    static constexpr int ALO_COL = ACC_COLS;  // first TMEM column of the A_lo stages
 };
 
 template <int BN, bool A_MN>
@@ -196,13 +230,14 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 
     auto a_stage = [&](int s) { return smem + s * Cfg::STAGE_BYTES; };
     auto alo_stage = [&](int s) { return smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES; };
-    auto bhi_stage = [&](int s) { return smem + s * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES; };
-    auto blo_stage = [&](int s) { return smem + s * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES + Cfg::B_BYTES; };
+    constexpr int kABufs = Cfg::LO_TMEM ? 1 : 2;  // [A | (A_lo) | B_hi | B_lo] per stage
+    auto bhi_stage = [&](int s) { return smem + s * Cfg::STAGE_BYTES + kABufs * Cfg::A_BYTES; };
+    auto blo_stage = [&](int s) { return smem + s * Cfg::STAGE_BYTES + kABufs * Cfg::A_BYTES + Cfg::B_BYTES; };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&conv[s], kConvThreads / 32);
+            mbar_init(&conv[s], kConvWarps);
             mbar_init(&empty[s], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -254,6 +289,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     } else if (warp == 1) {
         // ---------------- MMA issuer
         constexpr uint32_t idesc = make_idesc(BM, BN, A_MN ? 1 : 0, 1);
+        constexpr uint32_t idesc_t = make_idesc(BM, BN, 0, 1);  // A_lo from TMEM
         int s = 0;
         uint32_t ph = 0;
         int chunk = 0;
@@ -267,7 +303,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             mbar_wait(&conv[s], ph);
             tc_fence_after();
             if (lane == 0) {
-                const uint32_t a_hi = smem_u32(a_stage(s)), a_lo = smem_u32(alo_stage(s));
+                const uint32_t a_hi = smem_u32(a_stage(s));
+                const uint32_t a_lo = Cfg::LO_TMEM ? 0u : smem_u32(alo_stage(s));
                 const uint32_t b_hi = smem_u32(bhi_stage(s)), b_lo = smem_u32(blo_stage(s));
 #pragma unroll
                 for (int ks = 0; ks < BK / 8; ++ks) {
@@ -284,7 +321,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     const uint32_t acc = (kb % KCHUNK > 0 || ks > 0) ? 1u : 0u;
                     tc_mma_tf32(d0, da_hi, db_hi, idesc, acc);
                     tc_mma_tf32(d0 + BN, da_hi, db_lo, idesc, acc);
-                    tc_mma_tf32(d0, da_lo, db_hi, idesc, 1u);
+                    if (Cfg::LO_TMEM)
+                        tc_mma_tf32_ts(d0, tmem_base + Cfg::ALO_COL + s * BK + ks * 8, db_hi, idesc_t, 1u);
+                    else
+                        tc_mma_tf32(d0, da_lo, db_hi, idesc, 1u);
                 }
                 tc_commit(&empty[s]);
                 if (kb % KCHUNK == KCHUNK - 1 || kb == nkb - 1) tc_commit(&acc_full[set]);
@@ -296,23 +336,77 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 ph ^= 1;
             }
         }
-    } else if (warp < 6) {
+    } else if (warp < kDrainWarp0) {
+        if constexpr (Cfg::LO_TMEM) {
+            // ---------------- converters: A_lo = rna(A - trunc(A)) straight into TMEM.
+            // Thread (quarter q = warp % 4, lane l) owns tile row m = 32q + l, i.e.
+            // its own TMEM lane, and converts the row's 32 k values in two halves.
+            const int quarter = warp % 4;
+            const int m = quarter * 32 + lane;
+            const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+            int s = 0;
+            uint32_t ph = 0;
+            for (int kb = 0; kb < nkb; ++kb) {
+                mbar_wait(&full[s], ph);
+                const uint8_t* a = a_stage(s);
+#pragma unroll
+                for (int kh = 0; kh < 2; ++kh) {
+                float lo[16];
+                if (!A_MN) {
+                    // K-major SWIZZLE_128B: row m = 128 bytes, 16B chunk c at c ^ (m % 8)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int chunk = kh * 4 + c;
+                        const float4 x = *reinterpret_cast<const float4*>(a + m * 128 + ((chunk ^ (m & 7)) << 4));
+                        lo[4 * c + 0] = tf32_rna(x.x - tf32_hi(x.x));
+                        lo[4 * c + 1] = tf32_rna(x.y - tf32_hi(x.y));
+                        lo[4 * c + 2] = tf32_rna(x.z - tf32_hi(x.z));
+                        lo[4 * c + 3] = tf32_rna(x.w - tf32_hi(x.w));
+                    }
+                } else {
+                    // MN-major SWIZZLE_128B_BASE32B: atom q (32 M x 32 K) at q*4096,
+                    // K row k = 128 bytes, 32B chunk (l/8) at (l/8) ^ (k % 4)
+                    const uint8_t* atom = a + quarter * 4096 + (lane & 7) * 4;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int k = kh * 16 + i;
+                        const float x = *reinterpret_cast<const float*>(atom + k * 128 + (((lane >> 3) ^ (k & 3)) << 5));
+                        lo[i] = tf32_rna(x - tf32_hi(x));
+                    }
+                }
+                tmem_st16(tmem_base + lane_off + Cfg::ALO_COL + s * BK + kh * 16, lo);
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&conv[s]);
+                if (++s == STAGES) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+        } else {
         // ---------------- converters: A_hi in place, A_lo to the sibling buffer
+        // (all loads of a thread's share first, then the split, then the stores)
         const int ct = threadIdx.x - 64;
+        constexpr int PER = Cfg::A_BYTES / 16 / kConvThreads;
         int s = 0;
         uint32_t ph = 0;
         for (int kb = 0; kb < nkb; ++kb) {
             mbar_wait(&full[s], ph);
             float4* a = reinterpret_cast<float4*>(a_stage(s));
             float4* lo = reinterpret_cast<float4*>(alo_stage(s));
+            float4 xs[PER];
 #pragma unroll
-            for (int i = ct; i < Cfg::A_BYTES / 16; i += kConvThreads) {
-                float4 x = a[i];
-                float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
-                float4 l = make_float4(tf32_rna(x.x - h.x), tf32_rna(x.y - h.y), tf32_rna(x.z - h.z),
-                                       tf32_rna(x.w - h.w));
-                a[i] = h;
-                lo[i] = l;
+            for (int i = 0; i < PER; ++i) xs[i] = a[ct + i * kConvThreads];
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const float4 x = xs[i];
+                const float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
+                const float4 l = make_float4(tf32_rna(x.x - h.x), tf32_rna(x.y - h.y), tf32_rna(x.z - h.z),
+                                             tf32_rna(x.w - h.w));
+                a[ct + i * kConvThreads] = h;
+                lo[ct + i * kConvThreads] = l;
             }
             fence_proxy_async();
             __syncwarp();
@@ -321,6 +415,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 s = 0;
                 ph ^= 1;
             }
+        }
         }
     } else {
         // ---------------- accumulator drain + epilogue; TMEM lanes 32*(warp%4)+lane = tile row
