@@ -1,32 +1,25 @@
 // tcgen05 3xTF32 tall-skinny GEMMs for the FP32 path (sm_100a).
 //
 //   NN:  C[m x n]  = alpha (A[m x k] B[k x n] - 1 row_sub^T) + beta C
-//        operand A = A (K-major), operand B = B (MN-major), K = k
+//        operand A = A (K-major), K = k
 //   TN:  C[k x n]  = alpha (A^T B - mu colsum^T) + beta C   (reduction over m)
-//        operand A = A^T (MN-major: A's columns are contiguous), operand B = B
-//        (MN-major), K = m, split over K with FP64 reduction of the partials.
+//        operand A = A^T (MN-major: A's columns are contiguous), K = m, split
+//        over K with FP64 reduction of the partials.
+//   Operand B (the small d x p / n x p block) is split once by k_split_b into
+//   two K-major planes [B_hi; B_lo] (row n = column n of B).
 //
 // FP32 accuracy from TF32 tensor cores by the hi/lo split
-//   a = a_hi + a_lo, b = b_hi + b_lo  (hi = top 10 mantissa bits, exact in
-//   TF32; lo = rna_tf32(x - hi)),   a b ~= a_hi b_hi + a_hi b_lo + a_lo b_hi.
-// B (the small d x p / n x p block) is split once into a [hi; lo] array in
-// global memory by k_split_b; A (the large matrix) is split on the fly:
-//   TMA (SWIZZLE_128B) -> smem A stage -> 4 converter warps mask A_hi in
-//   place and write A_lo to a sibling buffer -> fence.proxy.async -> one
-//   elected thread issues 3 tcgen05.mma.kind::tf32 per K=8 step with the
-//   FP32 accumulators in TMEM: D0 += A_hi B_hi, D1 += A_hi B_lo,
-//   D0 += A_lo B_hi -> the epilogue warps tcgen05.ld D0 + D1.
+//   a = a_hi + a_lo, b = b_hi + b_lo  (hi = TF32 truncation, which the tensor
+//   core applies to raw FP32 itself), a b ~= a_hi b_hi + a_hi b_lo + a_lo b_hi
+//   as two MMAs per K=8 step: D0 | D1 += A_hi [B_hi | B_lo] (N = 2 BN) and
+//   D0 += A_lo B_hi (N = BN); the drain sums D0 + D1.
 // The TF32 tensor-core accumulator rounds with a bias (error measured to
 // grow linearly in K: 4e-7 at K=32, 5e-6 at 1e3, 5e-5 at 1e4), so TMEM only
 // accumulates KCHUNK = 4 k-blocks (K = 128); two accumulator sets alternate
 // and four dedicated warps drain each finished chunk into round-to-nearest
 // FP32 registers while the tensor core fills the other set.
-// Warp roles (448 threads): w0 TMA producer, w1 MMA issuer (+TMEM alloc),
-// w2..w9 converters, w10..w13 accumulator drain + epilogue (w % 4 covers the
-// four TMEM lane quarters).
-// Pipelines: full[s] (TMA bytes landed), conv[s] (A split ready), empty[s]
-// (MMA done reading the stage, via tcgen05.commit), acc_full[2] / acc_empty[2]
-// (TMEM accumulator sets).
+// Two kernels: k_tc_gemm_t (BN <= 64, the Krylov-chain widths) keeps A_hi and
+// A_lo in TMEM (.ts MMAs); k_tc_gemm (BN 96 / 128) keeps them in smem.
 #include <cuda.h>
 
 #include "gemm.cuh"
@@ -169,11 +162,12 @@ __device__ __forceinline__ float tf32_rna(float x) {
     return __uint_as_float(r);
 }
 
-// ------------------------------------------------------------------ kernel
+// ------------------------------------------------------------------ kernels
 struct TcParams {
     int64_t M, N, K;        // operand shapes: D[M x N] = Aop[M x K] Bop[K x N]
     int64_t k_per_split;    // K range per blockIdx.z (multiple of BK)
-    int64_t Kp;             // padded K of the split-B array (rows of hi; lo starts at Kp)
+    int64_t Kp;             // padded K of the split-B planes (their row length)
+    int64_t Np;             // rows per split-B plane (hi rows [0, Np), lo rows [Np, 2 Np))
     // epilogue
     int direct;             // 1: write C (NN); 0: FP32 partial to ws[z][M][N]
     float* C;
@@ -184,25 +178,352 @@ struct TcParams {
     const int32_t* pred;
 };
 
+// Profiling ablations (tools/ablate_tc.py builds variants; 0 in the product):
+// 1 converters skip the split, 2 no MMAs issued, 4 drains skip the TMEM
+// reads, 8 one MMA per k-step instead of two.
+#ifndef RSVD_TC_ABLATE
+#define RSVD_TC_ABLATE 0
+#endif
+
+// Pipeline trace (tools/trace_tc.py builds with -DRSVD_TC_TRACE): clock64
+// stamps per k-block of CTA 0 and CTA kTraceCta2, 8 series each.
+#ifdef RSVD_TC_TRACE
+constexpr int kTraceKb = 512, kTraceCta2 = 200;
+__device__ long long g_tc_trace[2][8][kTraceKb];
+#define TC_TRACE(series, kb)                                                                      \
+    do {                                                                                          \
+        if ((blockIdx.x == 0 || blockIdx.x == kTraceCta2) && blockIdx.y == 0 && blockIdx.z == 0 && \
+            (kb) < kTraceKb)                                                                       \
+            g_tc_trace[blockIdx.x == 0 ? 0 : 1][series][kb] = clock64();                          \
+    } while (0)
+#else
+#define TC_TRACE(series, kb) \
+    do {                     \
+    } while (0)
+#endif
+
+// Accumulator drain + epilogue, shared by both kernels. TMEM lane quarter
+// q = warp % 4 holds tile rows 32q..32q+31; D0 | D1 (2 BN columns) of each
+// finished chunk are summed into round-to-nearest FP32 registers.
+template <int BN>
+__device__ __forceinline__ void drain_epilogue(const TcParams& p, uint32_t tmem_base, int warp, int lane, int nkb,
+                                               int64_t m0, int64_t n0, uint64_t* acc_full, uint64_t* acc_empty) {
+    const int quarter = warp % 4;
+    const int64_t row = m0 + quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    float sum[BN];
+#pragma unroll
+    for (int i = 0; i < BN; ++i) sum[i] = 0.f;
+    const int nchunks = (nkb + KCHUNK - 1) / KCHUNK;
+    for (int c = 0; c < nchunks; ++c) {
+        const int set = c & 1;
+        mbar_wait(&acc_full[set], (c >> 1) & 1);
+        tc_fence_after();
+        const uint32_t base = tmem_base + lane_off + set * 2 * BN;
+#pragma unroll
+        for (int j = 0; j < ((RSVD_TC_ABLATE & 4) ? 0 : BN); j += 8) {
+            float v0[8], v1[8];
+            tmem_ld8(base + j, v0);
+            tmem_ld8(base + BN + j, v1);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) sum[j + i] += v0[i] + v1[i];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[set]);
+    }
+    if (warp % 4 == 3 && lane == 0) TC_TRACE(2, 511);
+    if (row < p.M) {
+#pragma unroll
+        for (int i = 0; i < BN; ++i) {
+            const int64_t col = n0 + i;
+            if (col < p.N) {
+                if (p.direct) {
+                    double r = (double)sum[i];
+                    if (p.row_sub) r -= p.row_sub[col];
+                    r *= p.alpha;
+                    if (p.beta != 0.0) r += p.beta * (double)p.C[row * p.ldc + col];
+                    p.C[row * p.ldc + col] = (float)r;
+                } else {
+                    p.ws[((int64_t)blockIdx.z * p.M + row) * p.N + col] = sum[i];
+                }
+            }
+        }
+    }
+}
+
+// ---- kernel 1 (BN <= 64): both A halves in TMEM ---------------------------
+// Rings: A (smem, TMA, one 128 x 32 box per stage; freed by the converters as
+// soon as they have read it), B (smem, TMA, [B_hi | B_lo] K-major for
+// KPS = 2 k-blocks per slot; freed by the MMA commit) and T (TMEM columns
+// [A_hi 64 | A_lo 64] for KPS k-blocks; written by the converters, freed by
+// the MMA commit). An A smem stage is held only for the TMA latency plus one
+// conversion, not for the tensor-core queue. Per K=8 step two .ts MMAs:
+//   D0 | D1 += A_hi [B_hi | B_lo]   (N = 2 BN)
+//   D0      += A_lo  B_hi           (N = BN)
+// These MMAs are short (32-64 tensor cycles) and the tensor pipe queue is
+// shallow, so the issuing thread must not stall: it runs alone (no warp
+// divergence per step), waits on ONE barrier per slot of 2 k-blocks (the
+// converters fold the B-arrival wait into t_full) and commits once per slot.
+// Measured (tools/mma_rate_probe.cu): this stream is tensor-bound at 458
+// cycles per k-block alone; a satisfied wait + fence per k-block adds ~110,
+// busy neighbour warps ~175.
+// Warps: 0 A producer, 1 MMA issuer (+TMEM alloc), 2 B producer, 3..6
+// converters, 7..10 drain; warp % 4 gives each converter / drain warp its
+// TMEM lane quarter.
+constexpr int kTWarpDrain0 = 7, kTThreads = 32 * 11;
+constexpr int KPS = 2;  // k-blocks per T / B slot
+
+template <int BN, bool A_MN>
+struct TmCfg {
+    static constexpr int A_BYTES = BM * BK * 4;        // 16 KB
+    static constexpr int B_BYTES = BN * BK * 4;        // one plane's tile, one k-block
+    static constexpr int B_SLOT = 2 * KPS * B_BYTES;    // [hi | lo] x KPS k-blocks
+    static constexpr int ACC_COLS = 4 * BN;             // 2 sets x (D0 | D1)
+    static constexpr int T_COLS = 2 * KPS * BK;         // [A_hi | A_lo] per slot
+    static constexpr int T_STAGES = (512 - ACC_COLS) / T_COLS;
+    static constexpr int B_STAGES = BN >= 64 ? 3 : 4;
+    static constexpr int A_STAGES_RAW = (200 * 1024 - B_STAGES * B_SLOT) / A_BYTES;
+    static constexpr int A_STAGES = A_STAGES_RAW > 12 ? 12 : A_STAGES_RAW;
+    static constexpr int SMEM = A_STAGES * A_BYTES + B_STAGES * B_SLOT + 1024 + 512;
+    static_assert(T_STAGES >= 2 && A_STAGES >= 2 * KPS, "pipeline too shallow");
+    static_assert(KCHUNK % KPS == 0, "accumulator chunks must hold whole slots");
+};
+
+template <int BN, bool A_MN>
+__global__ void __launch_bounds__(kTThreads, 1)
+k_tc_gemm_t(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
+    if (pred_off(p.pred)) return;
+    if (threadIdx.x == 0) TC_TRACE(0, 511);
+    using Cfg = TmCfg<BN, A_MN>;
+    constexpr int SA = Cfg::A_STAGES, SB = Cfg::B_STAGES, ST = Cfg::T_STAGES;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* a_ring = smem;
+    uint8_t* b_ring = smem + SA * Cfg::A_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(b_ring + SB * Cfg::B_SLOT);
+    uint64_t* a_full = bars;
+    uint64_t* a_empty = a_full + SA;
+    uint64_t* b_full = a_empty + SA;
+    uint64_t* b_empty = b_full + SB;
+    uint64_t* t_full = b_empty + SB;
+    uint64_t* t_empty = t_full + ST;
+    uint64_t* acc_full = t_empty + ST;   // [2]
+    uint64_t* acc_empty = acc_full + 2;  // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t m0 = (int64_t)blockIdx.x * BM;
+    const int64_t n0 = (int64_t)blockIdx.y * BN;
+    const int64_t kbeg = (int64_t)blockIdx.z * p.k_per_split;
+    const int64_t kend = min(p.K, kbeg + p.k_per_split);
+    const int nkb = (int)((kend - kbeg + BK - 1) / BK);
+    const int nslots = (nkb + KPS - 1) / KPS;  // the last slot may hold one k-block (zero-filled)
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < SA; ++s) {
+            mbar_init(&a_full[s], 1);
+            mbar_init(&a_empty[s], 4);
+        }
+        for (int s = 0; s < SB; ++s) {
+            mbar_init(&b_full[s], 1);
+            mbar_init(&b_empty[s], 1);
+        }
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(&t_full[s], 4);
+            mbar_init(&t_empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&acc_full[i], 1);
+            mbar_init(&acc_empty[i], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) TC_TRACE(1, 511);
+    const uint32_t t_col0 = tmem_base + Cfg::ACC_COLS;  // slot s: [hi 64 | lo 64] at t_col0 + T_COLS s
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- A producer (one k-block per stage; TMA zero-fills past K)
+            int s = 0;
+            uint32_t ph = 0;
+            for (int kb = 0; kb < nslots * KPS; ++kb) {
+                mbar_wait(&a_empty[s], ph ^ 1);
+                TC_TRACE(0, kb);
+                const int kk = (int)(kbeg + (int64_t)kb * BK);
+                uint8_t* dst = a_ring + s * Cfg::A_BYTES;
+                if (kb >= nkb) {
+                    mbar_arrive(&a_full[s]);  // padding k-block of the last slot: converters write zeros
+                } else if (mbar_expect_tx(&a_full[s], Cfg::A_BYTES), !A_MN) {
+                    tma_load_2d(&tmA, &a_full[s], dst, kk, (int)m0);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < BM / 32; ++i)
+                        tma_load_2d(&tmA, &a_full[s], dst + i * 32 * BK * 4, (int)(m0 + 32 * i), kk);
+                }
+                if (++s == SA) { s = 0; ph ^= 1; }
+            }
+        }
+    } else if (warp == 2) {
+        if (lane == 0) {  // ---------------- B producer
+            int s = 0;
+            uint32_t ph = 0;
+            for (int sl = 0; sl < nslots; ++sl) {
+                mbar_wait(&b_empty[s], ph ^ 1);
+                uint8_t* dst = b_ring + s * Cfg::B_SLOT;
+                mbar_expect_tx(&b_full[s], Cfg::B_SLOT);
+#pragma unroll
+                for (int j = 0; j < KPS; ++j) {
+                    const int kk = (int)(kbeg + (int64_t)(sl * KPS + j) * BK);
+                    tma_load_2d(&tmB, &b_full[s], dst + j * 2 * Cfg::B_BYTES, kk, (int)n0);
+                    tma_load_2d(&tmB, &b_full[s], dst + j * 2 * Cfg::B_BYTES + Cfg::B_BYTES, kk, (int)(p.Np + n0));
+                }
+                if (++s == SB) { s = 0; ph ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer (one thread, see above)
+            constexpr uint32_t idesc2 = make_idesc(BM, 2 * BN, 0, 0);
+            constexpr uint32_t idesc1 = make_idesc(BM, BN, 0, 0);
+            const uint64_t db0 = make_desc(smem_u32(b_ring), 16, 1024, kLayoutSW128);
+            constexpr uint64_t kSlotDesc = Cfg::B_SLOT >> 4;         // descriptor step per B slot
+            constexpr uint64_t kKbDesc = (2 * Cfg::B_BYTES) >> 4;     // ... per k-block inside it
+            int sb = 0, st = 0;
+            uint32_t phb = 0, pht = 0;
+            int chunk = 0;
+            for (int sl = 0; sl < nslots; ++sl) {
+                const int set = chunk & 1;
+                const uint32_t d0 = tmem_base + set * 2 * BN;
+                const bool first = (sl * KPS) % KCHUNK == 0;
+                if (first) mbar_wait(&acc_empty[set], ((chunk >> 1) & 1) ^ 1);
+                TC_TRACE(4, sl);
+                mbar_wait(&t_full[st], pht);
+                TC_TRACE(6, sl);
+                tc_fence_after();
+                const uint64_t db = db0 + sb * kSlotDesc;
+                const uint32_t ta = t_col0 + st * Cfg::T_COLS;
+#pragma unroll
+                for (int j = 0; j < KPS; ++j) {
+#pragma unroll
+                    for (int ks = 0; ks < BK / 8; ++ks) {
+                        if (RSVD_TC_ABLATE & 2) continue;
+                        const uint64_t dbk = db + j * kKbDesc + 2 * ks;
+                        const uint32_t tk = ta + j * BK + ks * 8;
+                        tc_mma_tf32_ts(d0, tk, dbk, idesc2, (first && j == 0 && ks == 0) ? 0u : 1u);
+                        if (RSVD_TC_ABLATE & 8) continue;
+                        tc_mma_tf32_ts(d0, tk + KPS * BK, dbk, idesc1, 1u);  // D0 += A_lo B_hi
+                    }
+                }
+                tc_commit(&t_empty[st]);
+                tc_commit(&b_empty[sb]);
+                if ((sl * KPS + KPS) % KCHUNK == 0 || sl == nslots - 1) {
+                    tc_commit(&acc_full[set]);
+                    ++chunk;
+                }
+                TC_TRACE(7, sl);
+                if (++sb == SB) { sb = 0; phb ^= 1; }
+                if (++st == ST) { st = 0; pht ^= 1; }
+            }
+        }
+    } else if (warp < kTWarpDrain0) {
+        // ---------------- converters: thread (quarter q, lane l) owns tile row
+        // m = 32q + l = its TMEM lane; per slot it reads the row's 2 x 32 k
+        // values from two A stages (freeing each at once), writes hi = raw A
+        // (the tensor core truncates it to TF32) and lo = A - trunc_tf32(A)
+        // (exact in FP32; truncated to TF32 by the tensor core, an error of
+        // the order of the dropped a_lo b_lo term), then, once the slot's B
+        // tiles have landed, hands the slot to the MMA thread.
+        const int quarter = warp % 4;
+        const int m = quarter * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+        int sa = 0, sb = 0, st = 0;
+        uint32_t pha = 0, phb = 0, pht = 0;
+        for (int sl = 0; sl < nslots; ++sl) {
+            mbar_wait(&t_empty[st], pht ^ 1);
+            tc_fence_after();
+            const uint32_t t = t_col0 + lane_off + st * Cfg::T_COLS;
+#pragma unroll
+            for (int j = 0; j < KPS; ++j) {
+                mbar_wait(&a_full[sa], pha);
+                if (warp == 4 && lane == 0) TC_TRACE(1, sl * KPS + j);
+                const uint8_t* a = a_ring + sa * Cfg::A_BYTES;
+                float x[32];
+                if (sl * KPS + j >= nkb) {
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) x[k] = 0.f;
+                } else if (!A_MN) {
+                    // K-major SWIZZLE_128B: row m = 128 bytes, 16B chunk c at c ^ (m % 8)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const float4 v = *reinterpret_cast<const float4*>(a + m * 128 + ((c ^ (m & 7)) << 4));
+                        x[4 * c + 0] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
+                    }
+                } else {
+                    // MN-major SWIZZLE_128B_BASE32B: atom q (32 M x 32 K) at q*4096,
+                    // K row k = 128 bytes, 32B chunk (l/8) at (l/8) ^ (k % 4)
+                    const uint8_t* atom = a + quarter * 4096 + (lane & 7) * 4;
+#pragma unroll
+                    for (int k = 0; k < 32; ++k)
+                        x[k] = *reinterpret_cast<const float*>(atom + k * 128 + (((lane >> 3) ^ (k & 3)) << 5));
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&a_empty[sa]);
+                float lo[32];
+#pragma unroll
+                for (int k = 0; k < 32; ++k) lo[k] = (RSVD_TC_ABLATE & 1) ? 0.f : x[k] - tf32_hi(x[k]);
+                tmem_st16(t + j * BK, x);
+                tmem_st16(t + j * BK + 16, x + 16);
+                tmem_st16(t + KPS * BK + j * BK, lo);
+                tmem_st16(t + KPS * BK + j * BK + 16, lo + 16);
+                if (++sa == SA) { sa = 0; pha ^= 1; }
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            mbar_wait(&b_full[sb], phb);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&t_full[st]);
+            if (warp == 4 && lane == 0) TC_TRACE(3, sl);
+            if (++sb == SB) { sb = 0; phb ^= 1; }
+            if (++st == ST) { st = 0; pht ^= 1; }
+        }
+    } else {
+        drain_epilogue<BN>(p, tmem_base, warp, lane, (nslots * KPS), m0, n0, acc_full, acc_empty);
+        if (warp == kTWarpDrain0 && lane == 0) TC_TRACE(3, 511);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+    }
+}
+
+// ---- kernel 2 (BN 96 / 128): A_hi / A_lo in smem ---------------------------
+// The accumulators need 4 BN = 384 / 512 TMEM columns, leaving no room for A.
+// Stage = [A | A_lo | B_hi | B_lo]; the converters write A_lo beside the raw
+// A (the tensor core truncates raw FP32 to TF32 itself, so raw A is A_hi).
+// Warps: 0 TMA producer, 1 MMA issuer (+TMEM alloc), 2..5 converters, 6..9
+// drain.
 template <int BN, bool A_MN>
 struct TcCfg {
-    // A_lo in TMEM (tcgen05.mma .ts form) when the accumulators leave room:
-    // the smem stage then holds only raw A (the tensor core truncates FP32 to
-    // TF32 itself, so raw A *is* A_hi) and B_hi/B_lo -> deeper pipelines.
-    static constexpr bool LO_TMEM = BN <= 64;
-    static constexpr int BNP = ((BN + 31) / 32) * 32;  // B tile padded to whole 32-wide atoms
     static constexpr int A_BYTES = BM * BK * 4;         // 16 KB
-    static constexpr int B_BYTES = BNP * BK * 4;
-    static constexpr int STAGE_BYTES = (LO_TMEM ? 1 : 2) * A_BYTES + 2 * B_BYTES;
-    static constexpr int ACC_COLS = 4 * BN;                 // 2 sets x (D0 | D1)
-    static constexpr int STAGES_SMEM = (200 * 1024) / STAGE_BYTES;
-    static constexpr int STAGES_TMEM = LO_TMEM ? (512 - ACC_COLS) / BK : 64;
-    static constexpr int STAGES_RAW = STAGES_SMEM < STAGES_TMEM ? STAGES_SMEM : STAGES_TMEM;
+    static constexpr int B_BYTES = BN * BK * 4;
+    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+    static constexpr int ACC_COLS = 4 * BN;              // 2 sets x (D0 | D1)
+    static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
     static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-    static constexpr int TMEM_NEED = ACC_COLS + (LO_TMEM ? STAGES * BK : 0);
-    static constexpr int TMEM_COLS = TMEM_NEED <= 128 ? 128 : (TMEM_NEED <= 256 ? 256 : 512);
-    static constexpr int ALO_COL = ACC_COLS;  // first TMEM column of the A_lo stages
+    static constexpr int TMEM_COLS = ACC_COLS <= 128 ? 128 : (ACC_COLS <= 256 ? 256 : 512);
 };
 
 template <int BN, bool A_MN>
@@ -230,9 +551,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 
     auto a_stage = [&](int s) { return smem + s * Cfg::STAGE_BYTES; };
     auto alo_stage = [&](int s) { return smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES; };
-    constexpr int kABufs = Cfg::LO_TMEM ? 1 : 2;  // [A | (A_lo) | B_hi | B_lo] per stage
-    auto bhi_stage = [&](int s) { return smem + s * Cfg::STAGE_BYTES + kABufs * Cfg::A_BYTES; };
-    auto blo_stage = [&](int s) { return smem + s * Cfg::STAGE_BYTES + kABufs * Cfg::A_BYTES + Cfg::B_BYTES; };
+    auto b_stage = [&](int s) { return smem + s * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES; };  // [B_hi | B_lo]
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -274,22 +593,17 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     for (int i = 0; i < BM / 32; ++i)
                         tma_load_2d(&tmA, &full[s], a_stage(s) + i * 32 * BK * 4, (int)(m0 + 32 * i), kk);
                 }
-#pragma unroll
-                for (int i = 0; i < Cfg::BNP / 32; ++i) {
-                    tma_load_2d(&tmB, &full[s], bhi_stage(s) + i * 32 * BK * 4, (int)(n0 + 32 * i), kk);
-                    tma_load_2d(&tmB, &full[s], blo_stage(s) + i * 32 * BK * 4, (int)(n0 + 32 * i),
-                                (int)(p.Kp + kk));
-                }
-                if (++s == STAGES) {
-                    s = 0;
-                    ph ^= 1;
-                }
+                // K-major split-B planes: one box of BN rows x 32 k each
+                tma_load_2d(&tmB, &full[s], b_stage(s), kk, (int)n0);
+                tma_load_2d(&tmB, &full[s], b_stage(s) + Cfg::B_BYTES, kk, (int)(p.Np + n0));
+                if (++s == STAGES) { s = 0; ph ^= 1; }
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer
-        constexpr uint32_t idesc = make_idesc(BM, BN, A_MN ? 1 : 0, 1);
-        constexpr uint32_t idesc_t = make_idesc(BM, BN, 0, 1);  // A_lo from TMEM
+        // ---------------- MMA issuer. B_hi and B_lo sit back to back (K-major,
+        // BN rows each), so A_hi [B_hi | B_lo] is one N = 2 BN MMA -> D0 | D1.
+        constexpr uint32_t idesc2 = make_idesc(BM, 2 * BN, A_MN ? 1 : 0, 0);
+        constexpr uint32_t idesc1 = make_idesc(BM, BN, A_MN ? 1 : 0, 0);
         int s = 0;
         uint32_t ph = 0;
         int chunk = 0;
@@ -303,9 +617,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             mbar_wait(&conv[s], ph);
             tc_fence_after();
             if (lane == 0) {
-                const uint32_t a_hi = smem_u32(a_stage(s));
-                const uint32_t a_lo = Cfg::LO_TMEM ? 0u : smem_u32(alo_stage(s));
-                const uint32_t b_hi = smem_u32(bhi_stage(s)), b_lo = smem_u32(blo_stage(s));
+                const uint32_t a_hi = smem_u32(a_stage(s)), a_lo = smem_u32(alo_stage(s));
+                const uint32_t b = smem_u32(b_stage(s));
 #pragma unroll
                 for (int ks = 0; ks < BK / 8; ++ks) {
                     uint64_t da_hi, da_lo;
@@ -316,85 +629,29 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         da_hi = make_desc(a_hi + ks * 1024, 32 * BK * 4, 512, kLayoutSW128Base32);
                         da_lo = make_desc(a_lo + ks * 1024, 32 * BK * 4, 512, kLayoutSW128Base32);
                     }
-                    const uint64_t db_hi = make_desc(b_hi + ks * 1024, 32 * BK * 4, 512, kLayoutSW128Base32);
-                    const uint64_t db_lo = make_desc(b_lo + ks * 1024, 32 * BK * 4, 512, kLayoutSW128Base32);
+                    const uint64_t db = make_desc(b + ks * 32, 16, 1024, kLayoutSW128);
                     const uint32_t acc = (kb % KCHUNK > 0 || ks > 0) ? 1u : 0u;
-                    tc_mma_tf32(d0, da_hi, db_hi, idesc, acc);
-                    tc_mma_tf32(d0 + BN, da_hi, db_lo, idesc, acc);
-                    if (Cfg::LO_TMEM)
-                        tc_mma_tf32_ts(d0, tmem_base + Cfg::ALO_COL + s * BK + ks * 8, db_hi, idesc_t, 1u);
-                    else
-                        tc_mma_tf32(d0, da_lo, db_hi, idesc, 1u);
+                    if (RSVD_TC_ABLATE & 2) continue;
+                    tc_mma_tf32(d0, da_hi, db, idesc2, acc);  // D0 | D1 += A_hi [B_hi | B_lo]
+                    if (RSVD_TC_ABLATE & 8) continue;
+                    tc_mma_tf32(d0, da_lo, db, idesc1, 1u);   // D0 += A_lo B_hi
                 }
                 tc_commit(&empty[s]);
                 if (kb % KCHUNK == KCHUNK - 1 || kb == nkb - 1) tc_commit(&acc_full[set]);
             }
             __syncwarp();
             if (kb % KCHUNK == KCHUNK - 1 || kb == nkb - 1) ++chunk;
-            if (++s == STAGES) {
-                s = 0;
-                ph ^= 1;
-            }
+            if (++s == STAGES) { s = 0; ph ^= 1; }
         }
     } else if (warp < kDrainWarp0) {
-        if constexpr (Cfg::LO_TMEM) {
-            // ---------------- converters: A_lo = rna(A - trunc(A)) straight into TMEM.
-            // Thread (quarter q = warp % 4, lane l) owns tile row m = 32q + l, i.e.
-            // its own TMEM lane, and converts the row's 32 k values in two halves.
-            const int quarter = warp % 4;
-            const int m = quarter * 32 + lane;
-            const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-            int s = 0;
-            uint32_t ph = 0;
-            for (int kb = 0; kb < nkb; ++kb) {
-                mbar_wait(&full[s], ph);
-                const uint8_t* a = a_stage(s);
-#pragma unroll
-                for (int kh = 0; kh < 2; ++kh) {
-                float lo[16];
-                if (!A_MN) {
-                    // K-major SWIZZLE_128B: row m = 128 bytes, 16B chunk c at c ^ (m % 8)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        const int chunk = kh * 4 + c;
-                        const float4 x = *reinterpret_cast<const float4*>(a + m * 128 + ((chunk ^ (m & 7)) << 4));
-                        lo[4 * c + 0] = tf32_rna(x.x - tf32_hi(x.x));
-                        lo[4 * c + 1] = tf32_rna(x.y - tf32_hi(x.y));
-                        lo[4 * c + 2] = tf32_rna(x.z - tf32_hi(x.z));
-                        lo[4 * c + 3] = tf32_rna(x.w - tf32_hi(x.w));
-                    }
-                } else {
-                    // MN-major SWIZZLE_128B_BASE32B: atom q (32 M x 32 K) at q*4096,
-                    // K row k = 128 bytes, 32B chunk (l/8) at (l/8) ^ (k % 4)
-                    const uint8_t* atom = a + quarter * 4096 + (lane & 7) * 4;
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int k = kh * 16 + i;
-                        const float x = *reinterpret_cast<const float*>(atom + k * 128 + (((lane >> 3) ^ (k & 3)) << 5));
-                        lo[i] = tf32_rna(x - tf32_hi(x));
-                    }
-                }
-                tmem_st16(tmem_base + lane_off + Cfg::ALO_COL + s * BK + kh * 16, lo);
-                }
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&conv[s]);
-                if (++s == STAGES) {
-                    s = 0;
-                    ph ^= 1;
-                }
-            }
-        } else {
-        // ---------------- converters: A_hi in place, A_lo to the sibling buffer
-        // (all loads of a thread's share first, then the split, then the stores)
+        // ---------------- converters: A_lo to the sibling buffer
         const int ct = threadIdx.x - 64;
         constexpr int PER = Cfg::A_BYTES / 16 / kConvThreads;
         int s = 0;
         uint32_t ph = 0;
         for (int kb = 0; kb < nkb; ++kb) {
             mbar_wait(&full[s], ph);
-            float4* a = reinterpret_cast<float4*>(a_stage(s));
+            const float4* a = reinterpret_cast<const float4*>(a_stage(s));
             float4* lo = reinterpret_cast<float4*>(alo_stage(s));
             float4 xs[PER];
 #pragma unroll
@@ -402,64 +659,16 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
             for (int i = 0; i < PER; ++i) {
                 const float4 x = xs[i];
-                const float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
-                const float4 l = make_float4(tf32_rna(x.x - h.x), tf32_rna(x.y - h.y), tf32_rna(x.z - h.z),
-                                             tf32_rna(x.w - h.w));
-                a[ct + i * kConvThreads] = h;
-                lo[ct + i * kConvThreads] = l;
+                lo[ct + i * kConvThreads] = make_float4(tf32_rna(x.x - tf32_hi(x.x)), tf32_rna(x.y - tf32_hi(x.y)),
+                                                        tf32_rna(x.z - tf32_hi(x.z)), tf32_rna(x.w - tf32_hi(x.w)));
             }
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) mbar_arrive(&conv[s]);
-            if (++s == STAGES) {
-                s = 0;
-                ph ^= 1;
-            }
-        }
+            if (++s == STAGES) { s = 0; ph ^= 1; }
         }
     } else {
-        // ---------------- accumulator drain + epilogue; TMEM lanes 32*(warp%4)+lane = tile row
-        const int quarter = warp % 4;
-        const int64_t row = m0 + quarter * 32 + lane;
-        const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-        float sum[BN];
-#pragma unroll
-        for (int i = 0; i < BN; ++i) sum[i] = 0.f;
-        const int nchunks = (nkb + KCHUNK - 1) / KCHUNK;
-        for (int c = 0; c < nchunks; ++c) {
-            const int set = c & 1;
-            mbar_wait(&acc_full[set], (c >> 1) & 1);
-            tc_fence_after();
-            const uint32_t base = tmem_base + lane_off + set * 2 * BN;
-#pragma unroll
-            for (int j = 0; j < BN; j += 8) {
-                float v0[8], v1[8];
-                tmem_ld8(base + j, v0);
-                tmem_ld8(base + BN + j, v1);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) sum[j + i] += v0[i] + v1[i];
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[set]);
-        }
-        if (row < p.M) {
-#pragma unroll
-            for (int i = 0; i < BN; ++i) {
-                const int64_t col = n0 + i;
-                if (col < p.N) {
-                    if (p.direct) {
-                        double r = (double)sum[i];
-                        if (p.row_sub) r -= p.row_sub[col];
-                        r *= p.alpha;
-                        if (p.beta != 0.0) r += p.beta * (double)p.C[row * p.ldc + col];
-                        p.C[row * p.ldc + col] = (float)r;
-                    } else {
-                        p.ws[((int64_t)blockIdx.z * p.M + row) * p.N + col] = sum[i];
-                    }
-                }
-            }
-        }
+        drain_epilogue<BN>(p, tmem_base, warp, lane, nkb, m0, n0, acc_full, acc_empty);
     }
     tc_fence_before();
     __syncthreads();
@@ -469,18 +678,27 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     }
 }
 
-// Split the small operand B (K x N, ld) into [hi; lo] rows of a (2 Kp) x Np
-// array with zero padding (so TMA boxes past K or N read zeros).
+// Split the small operand B (K x N, ld) into two K-major planes, hi then lo,
+// each Np x Kp (row n holds column n of B), zero padded so boxes past K or N
+// read zeros. Transposes through a 32 x 33 shared tile.
 __global__ void k_split_b(int64_t K, int64_t N, const float* __restrict__ B, int64_t ldb, int64_t Kp, int64_t Np,
                           float* __restrict__ out, const int32_t* __restrict__ pred) {
     if (pred_off(pred)) return;
-    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= Kp * Np) return;
-    int64_t r = e / Np, c = e % Np;
-    float x = (r < K && c < N) ? B[r * ldb + c] : 0.f;
-    float h = tf32_hi(x);
-    out[e] = h;
-    out[Kp * Np + e] = tf32_rna(x - h);
+    __shared__ float t[32][33];
+    const int64_t k0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+    for (int i = ty; i < 32; i += 8) {
+        const int64_t r = k0 + i, c = c0 + tx;
+        t[i][tx] = (r < K && c < N) ? B[r * ldb + c] : 0.f;
+    }
+    __syncthreads();
+    for (int i = ty; i < 32; i += 8) {
+        const int64_t c = c0 + i, r = k0 + tx;
+        const float x = t[tx][i];
+        const float h = tf32_hi(x);
+        out[c * Kp + r] = h;
+        out[(Np + c) * Kp + r] = tf32_rna(x - h);
+    }
 }
 
 template <typename TO>
@@ -547,14 +765,24 @@ int pick_bn(int64_t n) {
 
 template <int BN, bool A_MN>
 int launch_tc(const CUtensorMap& tA, const CUtensorMap& tB, const TcParams& p, dim3 grid, cudaStream_t st) {
-    using Cfg = TcCfg<BN, A_MN>;
     static bool attr_set = false;
-    if (!attr_set) {
-        RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_tc_gemm<BN, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             Cfg::SMEM));
-        attr_set = true;
+    if constexpr (BN <= 64) {
+        using Cfg = TmCfg<BN, A_MN>;
+        if (!attr_set) {
+            RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_tc_gemm_t<BN, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 Cfg::SMEM));
+            attr_set = true;
+        }
+        k_tc_gemm_t<BN, A_MN><<<grid, kTThreads, Cfg::SMEM, st>>>(tA, tB, p);
+    } else {
+        using Cfg = TcCfg<BN, A_MN>;
+        if (!attr_set) {
+            RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_tc_gemm<BN, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 Cfg::SMEM));
+            attr_set = true;
+        }
+        k_tc_gemm<BN, A_MN><<<grid, kThreads, Cfg::SMEM, st>>>(tA, tB, p);
     }
-    k_tc_gemm<BN, A_MN><<<grid, kThreads, Cfg::SMEM, st>>>(tA, tB, p);
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }
@@ -578,8 +806,8 @@ struct Scratch {
 
 int split_b(const float* B, int64_t K, int64_t N, int64_t ldb, int64_t Kp, int64_t Np, float* out,
             const int32_t* pred, cudaStream_t st) {
-    int64_t tot = Kp * Np;
-    k_split_b<<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(K, N, B, ldb, Kp, Np, out, pred);
+    dim3 grid((unsigned)(Kp / 32), (unsigned)(Np / 32));
+    k_split_b<<<grid, dim3(32, 8), 0, st>>>(K, N, B, ldb, Kp, Np, out, pred);
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }
@@ -612,7 +840,7 @@ int gemm_nn_tc(int64_t m, int64_t n, int64_t k, double alpha, const float* A, in
                int64_t ldb, double beta, float* C, int64_t ldc, const double* row_sub, const int32_t* pred,
                cudaStream_t st) {
     int bn = pick_bn(n);
-    const int64_t Kp = cdiv(k, BK) * BK, Np = cdiv(n, 32) * 32 + 128;
+    const int64_t Kp = cdiv(k, BK) * BK, Np = cdiv(n, bn) * bn;
     static thread_local Scratch sc;  // split-B buffer
     size_t need = (size_t)(2 * Kp * Np * 4);
     if (sc.bytes < need) {
@@ -626,10 +854,10 @@ int gemm_nn_tc(int64_t m, int64_t n, int64_t k, double alpha, const float* A, in
     CUtensorMap tA, tB;
     rc = make_map(&tA, A, k, m, lda, BM, false);
     if (rc) return rc;
-    rc = make_map(&tB, bs, Np, 2 * Kp, Np, BK, true);
+    rc = make_map(&tB, bs, Kp, 2 * Np, Kp, bn, false);
     if (rc) return rc;
     TcParams p{};
-    p.M = m; p.N = n; p.K = k; p.k_per_split = Kp; p.Kp = Kp;
+    p.M = m; p.N = n; p.K = k; p.k_per_split = Kp; p.Kp = Kp; p.Np = Np;
     p.direct = 1; p.C = C; p.ldc = ldc; p.alpha = alpha; p.beta = beta; p.row_sub = row_sub; p.ws = nullptr;
     p.pred = pred;
     dim3 grid((unsigned)cdiv(m, BM), (unsigned)cdiv(n, bn), 1);
@@ -656,7 +884,7 @@ int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, con
     int bn = pick_bn(Nop);
     const int64_t S = tn_splits_tc(Mop, Nop, Kop);
     RSVD_REQUIRE(ws_bytes >= S * Mop * Nop * 4, "gemm_tn_tc: workspace too small");
-    const int64_t Kp = cdiv(Kop, BK) * BK, Np = cdiv(Nop, 32) * 32 + 128;
+    const int64_t Kp = cdiv(Kop, BK) * BK, Np = cdiv(Nop, bn) * bn;
     static thread_local Scratch sc;
     size_t need = (size_t)(2 * Kp * Np * 4);
     if (sc.bytes < need) {
@@ -670,10 +898,10 @@ int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, con
     CUtensorMap tA, tB;
     rc = make_map(&tA, A, k /*inner = columns of A*/, m, lda, BK, true);
     if (rc) return rc;
-    rc = make_map(&tB, bs, Np, 2 * Kp, Np, BK, true);
+    rc = make_map(&tB, bs, Kp, 2 * Np, Kp, bn, false);
     if (rc) return rc;
     TcParams p{};
-    p.M = Mop; p.N = Nop; p.K = Kop;
+    p.M = Mop; p.N = Nop; p.K = Kop; p.Np = Np;
     p.k_per_split = cdiv(cdiv(Kop, S), BK) * BK;
     p.Kp = Kp;
     p.direct = 0; p.ws = (float*)ws; p.pred = pred;
@@ -692,3 +920,9 @@ int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, con
 }
 
 }  // namespace rsvd
+
+#ifdef RSVD_TC_TRACE
+extern "C" int rsvd_debug_tc_trace(long long* host_out) {
+    return (int)cudaMemcpyFromSymbol(host_out, rsvd::g_tc_trace, sizeof(rsvd::g_tc_trace));
+}
+#endif
