@@ -50,6 +50,7 @@ extern "C" {
 #define RSVD_GEMM_SIMT 1       /* CUDA-core FFMA/DFMA, FP32 or FP64 */
 #define RSVD_GEMM_TC_3XTF32 2  /* tcgen05 kind::tf32, hi/lo split, FP32 only */
 #define RSVD_GEMM_DMMA 3       /* mma.sync f64 (DMMA), FP64 only */
+#define RSVD_GEMM_SKINNY 4     /* FP32 CUDA-core, outputs <= 64 columns (orthonormalization sizes) */
 
 const char *rsvd_last_error(void);
 int rsvd_abi_version(void);

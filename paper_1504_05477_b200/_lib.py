@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(HERE, "librsvd_b200.so")
 
 RSVD_OK, RSVD_ERR_INVALID, RSVD_ERR_CONVERGENCE, RSVD_ERR_CUDA = 0, 1, 2, 3
 F32, F64 = 0, 1
-GEMM_AUTO, GEMM_SIMT, GEMM_TC_3XTF32, GEMM_DMMA = 0, 1, 2, 3
+GEMM_AUTO, GEMM_SIMT, GEMM_TC_3XTF32, GEMM_DMMA, GEMM_SKINNY = 0, 1, 2, 3, 4
 
 _i64, _u64, _int, _dbl, _vp = ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, ctypes.c_double, ctypes.c_void_p
 

@@ -61,6 +61,12 @@ int rsvd_gemm_nn(int dtype, int64_t m, int64_t n, int64_t k, double alpha, const
     RSVD_REQUIRE(m >= 0 && n >= 0 && k >= 0, "gemm_nn: negative dimension");
     RSVD_REQUIRE(lda >= k && ldb >= n && ldc >= n, "gemm_nn: leading dimension too small");
     cudaStream_t st = as_stream(stream);
+    if (algo == RSVD_GEMM_SKINNY ||
+        (algo == RSVD_GEMM_AUTO && dtype == RSVD_F32 && gemm_skinny_nn_supported(n, k))) {
+        RSVD_REQUIRE(dtype == RSVD_F32 && n <= 64, "gemm_nn: skinny path is FP32 with n <= 64");
+        return gemm_nn_skinny(m, n, k, alpha, (const float*)A, lda, (const float*)B, ldb, beta,
+                              (float*)C, ldc, row_sub, pred, st);
+    }
     if (algo == RSVD_GEMM_TC_3XTF32 || (algo == RSVD_GEMM_AUTO && dtype == RSVD_F32 &&
                                          gemm_tc_nn_supported(m, n, k, lda, ldb, ldc, A, B))) {
         RSVD_REQUIRE(dtype == RSVD_F32, "gemm_nn: 3xTF32 path is FP32 only");
@@ -77,6 +83,10 @@ int64_t rsvd_gemm_tn_ws_bytes(int dtype, int64_t m, int64_t n, int64_t k, int al
     if (dtype == RSVD_F32 && algo != RSVD_GEMM_SIMT) {
         int64_t b = gemm_tn_tc_ws_bytes(m, n, k);
         if (b > a) a = b;
+        if (n <= 64) {
+            b = gemm_tn_skinny_ws_bytes(m, n, k);
+            if (b > a) a = b;
+        }
     }
     return a + 256;
 }
@@ -90,6 +100,12 @@ int rsvd_gemm_tn(int dtype, int out_dtype, int64_t m, int64_t n, int64_t k, doub
     RSVD_REQUIRE(lda >= k && ldb >= n && ldc >= n, "gemm_tn: leading dimension too small");
     RSVD_REQUIRE((mu == nullptr) == (colsum_b == nullptr), "gemm_tn: mu and colsum_b go together");
     cudaStream_t st = as_stream(stream);
+    if (algo == RSVD_GEMM_SKINNY ||
+        (algo == RSVD_GEMM_AUTO && dtype == RSVD_F32 && gemm_skinny_tn_supported(n, k))) {
+        RSVD_REQUIRE(dtype == RSVD_F32 && n <= 64, "gemm_tn: skinny path is FP32 with n <= 64");
+        return gemm_tn_skinny(out_dtype, m, n, k, alpha, (const float*)A, lda, (const float*)B, ldb,
+                              beta, C, ldc, mu, colsum_b, ws, ws_bytes, pred, st);
+    }
     if (algo == RSVD_GEMM_TC_3XTF32 ||
         (algo == RSVD_GEMM_AUTO && dtype == RSVD_F32 && gemm_tc_tn_supported(m, n, k, lda, ldb, A, B))) {
         RSVD_REQUIRE(dtype == RSVD_F32, "gemm_tn: 3xTF32 path is FP32 only");

@@ -31,4 +31,16 @@ int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, con
                const double* mu, const double* cs, void* ws, int64_t ws_bytes, const int32_t* pred,
                cudaStream_t st);
 
+// FP32 CUDA-core kernels for outputs <= 64 columns wide (skinny.cu).
+bool gemm_skinny_nn_supported(int64_t n, int64_t k);
+bool gemm_skinny_tn_supported(int64_t n, int64_t k);
+int gemm_nn_skinny(int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t lda,
+                   const float* B, int64_t ldb, double beta, float* C, int64_t ldc,
+                   const double* row_sub, const int32_t* pred, cudaStream_t st);
+int64_t gemm_tn_skinny_ws_bytes(int64_t m, int64_t n, int64_t k);
+int gemm_tn_skinny(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, const float* A,
+                   int64_t lda, const float* B, int64_t ldb, double beta, void* C, int64_t ldc,
+                   const double* mu, const double* cs, void* ws, int64_t ws_bytes,
+                   const int32_t* pred, cudaStream_t st);
+
 }  // namespace rsvd

@@ -146,133 +146,6 @@ k_chol_deflate(int64_t p, const double* __restrict__ G, int64_t ldg,
 // access walks a row of the packed triangle (no bank conflicts); one warp
 // per row, the row held in registers.
 constexpr int kFastP = 224;
-constexpr int kFastThreads = 1024;
-
-template <int KR>
-__global__ void __launch_bounds__(kFastThreads)
-k_chol_fast(int p, const double* __restrict__ G, int64_t ldg, const double* __restrict__ ref2, double tau2,
-            double* __restrict__ T, int64_t ldt, int32_t* __restrict__ mask, int32_t* __restrict__ ndef,
-            int32_t* __restrict__ running, const int32_t* __restrict__ active, const int32_t* __restrict__ pred) {
-    if (pred && *pred == 0) return;
-    extern __shared__ double S[];  // packed upper triangle of the Schur complement / R
-    __shared__ double s_ref[kFastP];
-    __shared__ double s_rinv[kFastP];  // 1 / R[j][j] (1 for deficient slots)
-    __shared__ double s_rdiag[kFastP];
-    __shared__ int s_msk[kFastP];
-    __shared__ int s_act[kFastP];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-    auto off = [p](int i, int j) { return i * p - (i * (i - 1)) / 2 + (j - i); };
-    for (int i = warp; i < p; i += nwarps)
-        for (int j = i + lane; j < p; j += 32) S[off(i, j)] = G[(int64_t)i * ldg + j];
-    for (int j = tid; j < p; j += blockDim.x) {
-        s_ref[j] = ref2 ? ref2[j] : G[(int64_t)j * ldg + j];
-        s_act[j] = active ? active[j] : 1;
-    }
-    __syncthreads();
-    int count = 0;
-    for (int j = 0; j < p; ++j) {
-        // pivot test, redundantly in every thread (factor.py:105 analogue)
-        const double d = S[off(j, j)];
-        const int act = s_act[j];
-        const int def = !act || !(d > tau2 * s_ref[j]) || !(d > 0.0);
-        count += def && act;
-        if (!def) {
-            const double inv2 = 1.0 / d;
-            const double* __restrict__ rj = S + (off(j, j) - j);  // row j, unscaled, read-only this step
-            for (int a = j + 1 + warp; a < p; a += nwarps) {
-                const double ra = rj[a] * inv2;
-                double* __restrict__ rowa = S + (off(a, a) - a);
-                // batches of 8 independent elements: all loads, then all stores
-                for (int b0 = a + lane; b0 < p; b0 += 32 * 8) {
-                    double u[8], v[8];
-#pragma unroll
-                    for (int t = 0; t < 8; ++t) {
-                        const int b = b0 + 32 * t;
-                        u[t] = b < p ? rj[b] : 0.0;
-                        v[t] = b < p ? rowa[b] : 0.0;
-                    }
-#pragma unroll
-                    for (int t = 0; t < 8; ++t) {
-                        const int b = b0 + 32 * t;
-                        if (b < p) rowa[b] = fma(-ra, u[t], v[t]);
-                    }
-                }
-            }
-        }
-        if (tid == 0) {
-            s_msk[j] = def ? (act ? 1 : 2) : 0;
-            const double rjj = def ? 1.0 : sqrt(d);
-            s_rdiag[j] = rjj;
-            s_rinv[j] = 1.0 / rjj;
-        }
-        __syncthreads();
-    }
-    // scale the rows of R (deficient rows become e_j)
-    for (int i = warp; i < p; i += nwarps) {
-        const bool di = s_msk[i] != 0;
-        const double inv = s_rinv[i];
-        for (int j = i + lane; j < p; j += 32) {
-            const int o = off(i, j);
-            S[o] = (j == i) ? s_rdiag[i] : (di ? 0.0 : S[o] * inv);
-        }
-    }
-    __syncthreads();
-    // rows of T = R^{-1}: row c is s with R^T s = e_c (s_a = 0 for a < c).
-    // Each warp carries NI rows at once (independent chains -> ILP); steps
-    // b < c are exact no-ops for row c (its s_b is 0), so the rows share one
-    // loop starting at the smallest c.
-    constexpr int NI = KR <= 2 ? 4 : (KR <= 4 ? 2 : 1);  // stay within 64 registers
-    for (int c0 = warp; c0 < p; c0 += nwarps * NI) {
-        double x[NI][KR];
-#pragma unroll
-        for (int i = 0; i < NI; ++i)
-#pragma unroll
-            for (int r = 0; r < KR; ++r) x[i][r] = (lane + 32 * r == c0 + i * nwarps) ? 1.0 : 0.0;
-        for (int b = c0; b < p; ++b) {
-            const int rb = b >> 5, lb = b & 31;
-            const double* rowb = S + (off(b, b) - b);
-            const double rinvb = s_rinv[b];
-            double rrow[KR];
-#pragma unroll
-            for (int r = 0; r < KR; ++r) {
-                const int a = lane + 32 * r;
-                rrow[r] = (a > b && a < p) ? rowb[a] : 0.0;
-            }
-#pragma unroll
-            for (int i = 0; i < NI; ++i) {
-                double xb = 0.0;
-#pragma unroll
-                for (int r = 0; r < KR; ++r)
-                    if (r == rb) xb = x[i][r];
-                xb = __shfl_sync(0xffffffffu, xb, lb) * rinvb;
-#pragma unroll
-                for (int r = 0; r < KR; ++r) {
-                    const int a = lane + 32 * r;
-                    x[i][r] = (a == b) ? xb : fma(-rrow[r], xb, x[i][r]);
-                }
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < NI; ++i) {
-            const int c = c0 + i * nwarps;
-            if (c >= p) continue;
-            const bool zc = s_msk[c] != 0;
-#pragma unroll
-            for (int r = 0; r < KR; ++r) {
-                const int a = lane + 32 * r;
-                if (a < p) T[(int64_t)c * ldt + a] = (zc || s_msk[a] || a < c) ? 0.0 : x[i][r];
-            }
-        }
-    }
-    __syncthreads();
-    for (int j = tid; j < p; j += blockDim.x) mask[j] = s_msk[j] == 1 ? 1 : 0;
-    if (tid == 0) {
-        const int32_t base = running ? running[0] : 0;
-        ndef[0] = count;
-        ndef[1] = base;
-        if (running) running[0] = base + count;
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Jacobi
@@ -488,6 +361,216 @@ __global__ void k_eig_gather(int64_t w, int64_t k, const int32_t* __restrict__ o
     E[i * lde + r] = V[i * ldv + order[r]];
 }
 
+
+// ---------------------------------------------------------------------------
+// Cholesky with deflation + in-place triangular inverse, one CTA, p <= kFastP.
+// The packed upper triangle (row i holds columns i..p-1) lives in shared
+// memory (201 KB at p = 224). Every step is spread over all threads:
+//   factor, column j: uniform pivot test (factor.py:105 analogue) on the
+//     Schur diagonal; scale row j (a deficient column gets R row j = e_j and
+//     eliminates nothing); rank-1 update of the trailing triangle;
+//   invert, row i from the bottom (T = R^{-1} in place): row i of T is the
+//     accumulated row i over R_ii; column i of R (rows k < i) is staged, then
+//     rows k < i take the rank-1 update X[k][c] -= R[k][i] T[i][c], c >= i.
+// R with deficient rows e_j is invertible and (R^{-1})_SS = (R_SS)^{-1} on
+// the kept set S, so zeroing the deficient rows and columns of the full
+// inverse gives the restricted inverse.
+#ifdef RSVD_CHOL_TRACE
+__device__ long long g_chol_trace[64];
+#define CHOL_T(i) do { if (threadIdx.x == 0 && (i) < 64) g_chol_trace[i] = clock64(); } while (0)
+#else
+#define CHOL_T(i) do { } while (0)
+#endif
+constexpr int kSwThreadsMax = 512;
+
+__global__ void __launch_bounds__(kSwThreadsMax)
+k_chol_sweep(int p, const double* __restrict__ G, int64_t ldg, const double* __restrict__ ref2, double tau2,
+             double* __restrict__ T, int64_t ldt, int32_t* __restrict__ mask, int32_t* __restrict__ ndef,
+             int32_t* __restrict__ running, const int32_t* __restrict__ active, const int32_t* __restrict__ pred) {
+    if (pred && *pred == 0) return;
+    extern __shared__ double S[];
+    __shared__ int s_row[kFastP];  // S[s_row[i] + j] = element (i, j), j >= i
+    __shared__ double s_ref[kFastP];
+    __shared__ double s_vec[kFastP];   // staged row j (factor) / column i (invert)
+    __shared__ double s_vec2[kFastP];  // staged row i (invert)
+    __shared__ int s_msk[kFastP];      // 0 kept, 1 deficient, 2 inactive
+    __shared__ double s_piv[2];        // factor: inv (0 if deficient), rjj; invert: rinv
+    __shared__ int s_def, s_count;
+    const int nt = blockDim.x, tid = threadIdx.x, tx = tid & 31, ty = tid >> 5, ny = nt >> 5;
+    for (int i = tid; i < p; i += nt) {
+        s_row[i] = i * p - (i * (i - 1)) / 2 - i;
+        s_ref[i] = ref2 ? ref2[i] : G[(int64_t)i * ldg + i];
+        s_msk[i] = (active && active[i] == 0) ? 2 : 0;
+    }
+    if (tid == 0) s_count = 0;
+    __syncthreads();
+    for (int i = ty; i < p; i += ny)
+        for (int j = i + tx; j < p; j += 32) S[s_row[i] + j] = G[(int64_t)i * ldg + j];
+    __syncthreads();
+    CHOL_T(0);
+    for (int j = 0; j < p; ++j) {
+        const int rj = s_row[j];
+        // A: stage row j (unscaled); thread 0 takes the pivot decision
+        for (int c = j + tid; c < p; c += nt) s_vec[c] = S[rj + c];
+        if (tid == 0) {
+            const double d = S[rj + j];
+            const int inactive = s_msk[j] == 2;
+            const bool def = inactive || !(d > tau2 * s_ref[j]) || !(d > 0.0);
+            const double rjj = def ? 1.0 : sqrt(d);
+            s_piv[0] = def ? 0.0 : 1.0 / rjj;
+            s_piv[1] = rjj;
+            s_def = def;
+            if (def && !inactive) {
+                s_msk[j] = 1;
+                ++s_count;
+            }
+        }
+        __syncthreads();
+        // B: scale row j; rank-1 update of the trailing triangle with the scaled row
+        const double inv = s_piv[0];
+        if (ty == 0)
+            for (int c = j + tx; c < p; c += 32) S[rj + c] = (c == j) ? s_piv[1] : s_vec[c] * inv;
+        if (!s_def) {
+            for (int i = j + 1 + ty; i < p; i += ny) {
+                const double ui = s_vec[i] * inv;
+                double* row = S + s_row[i];
+                for (int c = i + tx; c < p; c += 32) row[c] = fma(-ui, s_vec[c] * inv, row[c]);
+            }
+        }
+        __syncthreads();
+    }
+    CHOL_T(1);
+    for (int i = p - 1; i >= 0; --i) {
+        const int ri = s_row[i];
+        // A: stage column i (rows k < i) and row i of the accumulated inverse
+        for (int k = tid; k < i; k += nt) s_vec[k] = S[s_row[k] + i];
+        for (int c = i + tid; c < p; c += nt) s_vec2[c] = S[ri + c];
+        __syncthreads();
+        // B: row i of T = accumulated row / R_ii; rows k < i: X[k][c] -= R[k][i] T[i][c]
+        const double rinv = 1.0 / s_vec2[i];
+        if (ty == 0)
+            for (int c = i + tx; c < p; c += 32) S[ri + c] = (c == i) ? rinv : s_vec2[c] * rinv;
+        for (int k = ty; k < i; k += ny) {
+            const double rk = s_vec[k];
+            double* row = S + s_row[k];
+            for (int c = i + tx; c < p; c += 32) {
+                const double tic = (c == i) ? rinv : s_vec2[c] * rinv;
+                row[c] = (c == i) ? -rk * tic : fma(-rk, tic, row[c]);
+            }
+        }
+        __syncthreads();
+    }
+    CHOL_T(2);
+    for (int c = ty; c < p; c += ny)
+        for (int a = tx; a < p; a += 32)
+            T[(int64_t)c * ldt + a] = (a < c || s_msk[c] || s_msk[a]) ? 0.0 : S[s_row[c] + a];
+    for (int j = tid; j < p; j += nt) mask[j] = s_msk[j] == 1 ? 1 : 0;
+    if (tid == 0) {
+        const int32_t base = running ? running[0] : 0;
+        ndef[0] = s_count;
+        ndef[1] = base;
+        if (running) running[0] = base + s_count;
+    }
+    CHOL_T(3);
+}
+
+// p <= 64: thread t holds column t of the Schur complement / R in registers
+// (fully unrolled steps, so every index is static). Per column j: thread j
+// takes the pivot decision (rsqrt), the scaled row j goes through shared
+// memory, and each thread updates its own column (2 barriers of 64 threads
+// per step; entries below a column's diagonal are never read, so the update
+// runs unpredicated). The inverse is a column sweep with x in registers, R
+// read by broadcast and the pivots' reciprocals kept from the factorization.
+// (Measured at p = 50: ~37k cycles factor + ~24k inverse; a one-warp variant
+// without block barriers, k_chol_warp, is slower: LDS latency is not hidden.)
+constexpr int kRegP = 64;
+
+__global__ void __launch_bounds__(kRegP)
+k_chol_reg64(int p, const double* __restrict__ G, int64_t ldg, const double* __restrict__ ref2, double tau2,
+             double* __restrict__ T, int64_t ldt, int32_t* __restrict__ mask, int32_t* __restrict__ ndef,
+             int32_t* __restrict__ running, const int32_t* __restrict__ active, const int32_t* __restrict__ pred) {
+    if (pred && *pred == 0) return;
+    __shared__ double Rs[kRegP][kRegP + 1];  // R (upper) after the factorization, R(i, c) = Rs[i][c]
+    __shared__ double s_row[kRegP];          // scaled row j of the current step
+    __shared__ double s_piv[2];              // inv (0 if deficient), rjj
+    __shared__ double s_rinv[kRegP];         // 1 / R(j, j) (1 for deficient columns)
+    __shared__ int s_msk[kRegP];
+    __shared__ int s_def, s_count;
+    const int t = threadIdx.x;
+    const bool mine = t < p;
+    double r[kRegP];  // r[i] = element (i, t), i <= t
+#pragma unroll
+    for (int i = 0; i < kRegP; ++i) r[i] = (mine && i <= t) ? G[(int64_t)i * ldg + t] : 0.0;
+    const double myref = mine ? (ref2 ? ref2[t] : G[(int64_t)t * ldg + t]) : 0.0;
+    const int myinact = mine ? (active && active[t] == 0) : 1;
+    s_msk[t] = myinact && mine ? 2 : 0;
+    if (t == 0) s_count = 0;
+    __syncthreads();
+    CHOL_T(0);
+#pragma unroll
+    for (int j = 0; j < kRegP; ++j) {
+        if (j < p) {  // uniform
+            if (t == j) {
+                const double d = r[j];
+                const bool def = myinact || !(d > tau2 * myref) || !(d > 0.0);
+                const double inv = def ? 0.0 : rsqrt(d);
+                s_piv[0] = inv;
+                s_piv[1] = def ? 1.0 : d * inv;
+                s_rinv[j] = def ? 1.0 : inv;
+                s_def = def;
+                if (def && !myinact) {
+                    s_msk[j] = 1;
+                    ++s_count;
+                }
+            }
+            __syncthreads();
+            const double inv = s_piv[0];
+            if (t == j) r[j] = s_piv[1];
+            else if (t > j) r[j] *= inv;
+            s_row[t] = r[j];  // R(j, t) for t > j
+            const bool def = s_def;
+            __syncthreads();
+            if (!def) {
+                const double rj = r[j];
+#pragma unroll
+                for (int i = j + 1; i < kRegP; ++i) r[i] = fma(-s_row[i], rj, r[i]);
+            }
+        }
+    }
+    CHOL_T(1);
+#pragma unroll
+    for (int i = 0; i < kRegP; ++i) Rs[i][t] = (mine && i <= t) ? r[i] : 0.0;
+    __syncthreads();
+    // column t of T: R x = e_t, swept from the bottom (x_i = 0 for i > t)
+    double x[kRegP];
+#pragma unroll
+    for (int i = 0; i < kRegP; ++i) x[i] = (i == t) ? 1.0 : 0.0;
+#pragma unroll
+    for (int i = kRegP - 1; i >= 0; --i) {
+        if (i < p) {
+            const double xi = x[i] * s_rinv[i];
+            x[i] = xi;
+#pragma unroll
+            for (int k = 0; k < i; ++k) x[k] = fma(-Rs[k][i], xi, x[k]);
+        }
+    }
+    CHOL_T(2);
+    if (mine) {
+        const bool zc = s_msk[t] != 0;
+#pragma unroll
+        for (int a = 0; a < kRegP; ++a)
+            if (a < p) T[(int64_t)a * ldt + t] = (a > t || zc || s_msk[a]) ? 0.0 : x[a];
+        mask[t] = s_msk[t] == 1 ? 1 : 0;
+    }
+    if (t == 0) {
+        const int32_t base = running ? running[0] : 0;
+        ndef[0] = s_count;
+        ndef[1] = base;
+        if (running) running[0] = base + s_count;
+    }
+    CHOL_T(3);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -499,29 +582,17 @@ int chol_deflate(int64_t p, const double* G, int64_t ldg, const double* ref2, do
                  int64_t ldt, int32_t* mask, int32_t* ndef, int32_t* running, const int32_t* active, void* ws,
                  int64_t ws_bytes, const int32_t* pred, cudaStream_t st) {
     if (p == 0) return RSVD_OK;
+    if (p <= kRegP) {
+        k_chol_reg64<<<1, kRegP, 0, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active, pred);
+        RSVD_CHECK_LAUNCH();
+        return RSVD_OK;
+    }
     if (p <= kFastP) {
         const size_t sm = (size_t)(p * (p + 1) / 2) * sizeof(double);
-        const int threads = kFastThreads;
-        const int kr = (int)((p + 31) / 32);
-#define RSVD_CHOL_CASE(K)                                                                                   \
-    case K: {                                                                                             \
-        if (sm > 48 * 1024)                                                                               \
-            RSVD_CHECK_CUDA(                                                                              \
-                cudaFuncSetAttribute(k_chol_fast<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
-        k_chol_fast<K><<<1, threads, sm, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active, \
-                                               pred);                                                     \
-        break;                                                                                            \
-    }
-        switch (kr) {
-            RSVD_CHOL_CASE(1)
-            RSVD_CHOL_CASE(2)
-            RSVD_CHOL_CASE(3)
-            RSVD_CHOL_CASE(4)
-            RSVD_CHOL_CASE(5)
-            RSVD_CHOL_CASE(6)
-            default: RSVD_CHOL_CASE(7)
-        }
-#undef RSVD_CHOL_CASE
+        if (sm > 48 * 1024)
+            RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_chol_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        const int nt = p <= 64 ? 128 : (p <= 128 ? 256 : kSwThreadsMax);
+        k_chol_sweep<<<1, nt, sm, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active, pred);
         RSVD_CHECK_LAUNCH();
         return RSVD_OK;
     }
@@ -616,3 +687,9 @@ int eig_select(int64_t w, const double* M, int64_t ldm, const double* V, int64_t
 }
 
 }  // namespace rsvd
+
+#ifdef RSVD_CHOL_TRACE
+extern "C" int rsvd_debug_chol_trace(long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, rsvd::g_chol_trace, sizeof(rsvd::g_chol_trace));
+}
+#endif
