@@ -63,6 +63,18 @@ def _spectrum(kind, d):
     raise ValueError(kind)
 
 
+def _profiled_traffic():
+    """DRAM bytes per launch of the chain kernel from the committed ncu --set
+    full capture (profiles/r01_chain_kernel_ncu.json: dram__bytes_read.sum +
+    dram__bytes_write.sum), or None when no capture is committed."""
+    path = os.path.join(ROOT, "profiles", "r01_chain_kernel_ncu.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["dram_bytes_per_launch"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def make_matrix(cfg, device, seed=1234):
     """Haar U (n x d), V (d x d) from seeded Gaussians (QR, sign-fixed by
     diag R), A = U diag(s) V^T (+ noise), built in FP64 on the GPU, FP32 out."""
@@ -211,6 +223,15 @@ def run_ours(args):
     for _ in range(args.warmup):
         df = step()
     torch.cuda.synchronize()
+    if args.profile_step:
+        # one factorization, kernels launched individually, inside the profiler window
+        torch.cuda.profiler.start()
+        rsvd.run_device(op, cfg, comm=comm, Pi=Pi)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        if rank == 0:
+            print(json.dumps({"profile_step": args.config, "ok": True}), flush=True)
+        return
     # kernels per factorization, counted on an eager replica of the step (a
     # graph replay issues the identical kernel sequence in one launch)
     launches = (count_launches(lambda: rsvd.run_device(op, cfg, comm=comm, Pi=Pi))
@@ -289,7 +310,7 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (A = %.1f GB)" % (n * d * 4 / 1e9)},
         "roofline": {"bound": "hbm", "kernel": "Krylov-chain A.X / A^T.Y (width %d)" % cfg.p,
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "peak_source": peak_src, "traffic": None,
+                     "peak_source": peak_src, "traffic": _profiled_traffic(),
                      "algorithmic_bytes_per_launch": bytes_per, "avg_launch_ms": avg_chain_ms},
         "kernels": {"rayleigh_ritz_ATQ_ms": rr_ms, "rayleigh_ritz_ATQ_tflops": rr_tflops},
         "gpu_launches": launches,
@@ -416,6 +437,9 @@ def main():
     ap.add_argument("--count-launches", action="store_true", default=True)
     ap.add_argument("--cpu-budget", type=float, default=25.0)
     ap.add_argument("--graph", type=int, default=1, help="replay the factorization as a CUDA graph")
+    ap.add_argument("--profile-step", action="store_true",
+                    help="bracket one eager factorization with cudaProfilerStart/Stop (for ncu "
+                         "--profile-from-start off) after the warm-up, then exit")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
