@@ -320,7 +320,7 @@ def run_ours(args):
     if e2e:
         out["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu:
-        out["cpu_baseline"] = cpu_baseline(A, cfgd, cfg, Pi, args)
+        out["cpu_baseline"] = cpu_baseline(A, cfgd, cfg, Pi, args, df)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -359,14 +359,29 @@ LAUNCHES_PER_CALL = {"rsvd_gemm_tn": 2, "rsvd_colreduce": 2, "rsvd_canonicalize_
                      "rsvd_eig_select": 2, "rsvd_col_absargmax": 2}
 
 
-def cpu_baseline(A_dev, cfgd, cfg, Pi, args):
-    """The reference algorithm (oracle port) on the box's host cores,
-    stage-timed on a bounded sample and scaled to one factorization."""
-    res = reference_sample(A_dev.cpu().numpy(), cfgd, cfg, Pi, budget_s=args.cpu_budget)
+def cpu_baseline(A_dev, cfgd, cfg, Pi, args, df=None):
+    """The reference algorithm (oracle port) on the box's host cores, one
+    full factorization; with the device result `df` also the north_star
+    parity of this run: max relative error of all k singular values and of
+    the per-vector captured variance ||A^T z_i||^2 (metrics.py:136), both
+    evaluated in FP64 on the same A."""
+    res, r = reference_sample(A_dev.cpu().numpy(), cfgd, cfg, Pi, budget_s=args.cpu_budget, return_result=True)
+    if df is not None:
+        import torch
+
+        sig = df.sigma.double().cpu().numpy()
+        A64 = A_dev.double()
+        cap = (A64.T @ df.Z.double()).pow(2).sum(0).cpu().numpy()
+        cap_ref = (A64.T @ torch.from_numpy(np.ascontiguousarray(r.Z)).to(A64.device)).pow(2).sum(0).cpu().numpy()
+        del A64
+        res["parity"] = {"sigma_rel_max": float(np.max(np.abs(sig - r.sigma) / r.sigma)),
+                         "sigma_rel_median": float(np.median(np.abs(sig - r.sigma) / r.sigma)),
+                         "captured_variance_rel_max": float(np.max(np.abs(cap - cap_ref) / cap_ref)),
+                         "tolerance": 1e-4 if A_dev.dtype == torch.float32 else 1e-10}
     return res
 
 
-def reference_sample(A32, cfgd, cfg, Pi, budget_s=25.0):
+def reference_sample(A32, cfgd, cfg, Pi, budget_s=25.0, return_result=False):
     """One full factorization by the reference algorithm on the box's host
     cores: the oracle port (oracle/rsvd_oracle.py) — numpy/OpenBLAS products
     as the reference's python backend (_kernels_py.py:48-49), the C
@@ -384,12 +399,13 @@ def reference_sample(A32, cfgd, cfg, Pi, budget_s=25.0):
     t0 = time.perf_counter()
     r = o.factorize(op, cfg.k, variant, q=cfg.q, p=cfg.p, seed=cfg.seed)
     secs = time.perf_counter() - t0
-    return {"value": secs * 1e3, "unit": "ms", "cores": cores, "kind": "port",
+    out = {"value": secs * 1e3, "unit": "ms", "cores": cores, "kind": "port",
             "sample": ("one full factorization of the same workload by the reference algorithm (oracle port: "
                        "numpy/OpenBLAS products like the reference's python backend, C restatement of its "
                        "Jacobi, per-column CGS2 _mgs) on the same A upcast to FP64 and the same Pi; "
                        f"{cores} host threads (OPENBLAS_NUM_THREADS)"),
             "sigma_head": [float(x) for x in r.sigma[:3]]}
+    return (out, r) if return_result else out
 
 
 def run_reference(args):

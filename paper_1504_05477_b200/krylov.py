@@ -28,6 +28,8 @@ on every rank (deterministic kernels => identical decisions).
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 QR_FILL_SEED = 0x5EED_F111_0C0F_FEE5  # factor.py:40
@@ -137,6 +139,12 @@ def project_out(ops, comm, Qp, V, tmp_c, pred=None):
     return V
 
 
+# A third CholeskyQR pass for FP32 blocks (off by default: the chain blocks
+# are well conditioned after the first pass and Z is re-orthonormalised in
+# FP64; RSVD_FP32_THIRD_PASS=1 restores it for comparison).
+FP32_THIRD_PASS = os.environ.get("RSVD_FP32_THIRD_PASS", "0") == "1"
+
+
 def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=None, row_offset=0,
                tau=None, deflation_count=None, two_round=None):
     """Orthonormalize the n x p block V in place (span-preserving, column
@@ -243,7 +251,7 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
     ops.chol_deflate(G, None, 0.0, T, ws.mask2[:p], ws.ndef2, None, pred=r3)
     ops.gemm_nn(V, _cast_small(ops, T, dtype, pred=r3), out, pred=r3)
     ops.convert(out, V, pred=r3)
-    if dtype != torch.float64:
+    if dtype != torch.float64 and FP32_THIRD_PASS:
         # FP32 storage: one more CholeskyQR step (CholeskyQR2 cleanup)
         ops.gram(V, G)
         comm.allreduce(G)
@@ -272,12 +280,29 @@ def sketch_basis(ops, comm, op, Pi, ws, n_total, row_offset):
     return Y
 
 
+# Block-Krylov basis construction for the reduced-precision (FP32) path:
+# "projected" orthonormalizes each new block A A^T q_{j-1} against all
+# previous blocks as it is produced (block Lanczos with full
+# re-orthogonalization, BCGS2 + CholeskyQR). It spans the same Krylov
+# subspace as the reference's normalized power blocks + final _mgs of their
+# hstack, but represents each block's new directions at full relative
+# precision: for high powers those directions are a ~1e-5 residual of the
+# raw block, below FP32 / 3xTF32 resolution, and the faithful construction
+# measured 2.6e-3 relative error on the C2 tail singular values (median
+# 1.1e-4) against the FP64 reference. FP64 keeps the reference-faithful
+# construction (its deflation pattern, e.g. C1's 39 replaced columns, is
+# part of the parity). RSVD_BK_BASIS=faithful|projected overrides.
+BK_BASIS = os.environ.get("RSVD_BK_BASIS", "")
+
+
 def bk_basis(ops, comm, op, Pi, q, ws, n_total, row_offset):
     """rsvd.py:244-260 — block Krylov basis [b0 .. b_q], orthonormalized.
 
-    Blocks are written straight into the n x w basis buffer K; the final
-    orthonormalization (``_mgs(np.hstack(blocks))``) runs block by block in
-    place (BCGS2 against the already orthonormal prefix)."""
+    Blocks are written straight into the n x w basis buffer K. FP64: the
+    reference's structure — normalized power blocks, then the final
+    orthonormalization (``_mgs(np.hstack(blocks))``) block by block in place
+    (BCGS2 against the already orthonormal prefix). FP32: the projected
+    construction (see BK_BASIS above)."""
     n = op.local_rows
     d = op.shape[1]
     p = Pi.shape[1]
@@ -288,11 +313,27 @@ def bk_basis(ops, comm, op, Pi, q, ws, n_total, row_offset):
     tmp = rows_buffer(n, p, dt, dev)
     C = torch.empty((d, p), dtype=dt, device=dev)
     running = torch.zeros(1, dtype=torch.int32, device=dev)
+    projected = BK_BASIS == "projected" or (BK_BASIS != "faithful" and dt != torch.float64)
     b0 = K[:, :p]
     op.apply(Pi, b0)
     orth_block(ops, comm, b0, tmp, ws, running=running, n_total=n_total, row_offset=row_offset)
     if n_blocks == 1:
         return BasisResult(K, 0, torch.zeros(1, dtype=torch.int32, device=dev))
+    deflated = torch.zeros(1, dtype=torch.int32, device=dev)
+    if projected:
+        # one fill stream across the blocks, as one _mgs of the hstack
+        for j in range(1, n_blocks):
+            prev = K[:, (j - 1) * p: j * p]
+            cur = K[:, j * p: (j + 1) * p]
+            op.apply_t(prev, C)
+            comm.allreduce(C)
+            op.apply(C, cur)
+            ref2 = ws.ref2[:p]
+            ops.colreduce(cur, True, ref2)
+            comm.allreduce(ref2)
+            orth_block(ops, comm, cur, tmp, ws, Qp=K[:, : j * p], ref2=ref2, running=running,
+                       n_total=n_total, row_offset=row_offset, deflation_count=deflated)
+        return BasisResult(K, n_blocks - 1, deflated)
     for j in range(1, n_blocks):
         prev = K[:, (j - 1) * p: j * p]
         cur = K[:, j * p: (j + 1) * p]
@@ -303,7 +344,6 @@ def bk_basis(ops, comm, op, Pi, q, ws, n_total, row_offset):
         orth_block(ops, comm, cur, tmp, ws, running=running, n_total=n_total, row_offset=row_offset)
     # final orthonormalization of hstack(blocks): one _mgs call -> one fill stream
     running.zero_()
-    deflated = torch.zeros(1, dtype=torch.int32, device=dev)
     for j in range(n_blocks):
         cur = K[:, j * p: (j + 1) * p]
         ref2 = ws.ref2[:p]

@@ -161,6 +161,22 @@ def test_fp32_path_parity_c2_like(rk):
     assert np.max(np.abs(z.T @ z - np.eye(50))) <= 1e-10
 
 
+def test_fp32_projected_basis_tail_parity(rk):
+    """A shape where the reference-faithful FP32 construction (normalized
+    power blocks + final _mgs of their hstack) loses the tail: 1.6e-4 max
+    relative sigma error measured; the projected construction (krylov.BK_BASIS)
+    stays at FP32 rounding (7.4e-7 measured)."""
+    A32 = _fp32_case(20000, 4000, 50, 10)
+    A64 = A32.astype(np.float64)
+    ref = o.factorize(o.DenseOp(A64), 50, "bk", q=10, seed=0)
+    r = rk.block_krylov(A32, rk.RsvdConfig(k=50, variant="bk", q=10, seed=0))
+    rel = np.abs(r.approx_singular_values - ref.sigma) / ref.sigma
+    assert rel.max() < FP32_TOL, rel.max()
+    cap = o.captured_variance(A64, r.Z.data)
+    cap_ref = o.captured_variance(A64, ref.Z)
+    assert np.max(np.abs(cap - cap_ref) / cap_ref) < FP32_TOL
+
+
 def test_fp32_si(rk):
     A32 = _fp32_case(3000, 600, 20, 6, seed=1)
     A64 = A32.astype(np.float64)
