@@ -247,3 +247,21 @@ def test_syev_topk(ops, w, k, kind):
     assert np.max(np.abs(E.T @ E - np.eye(k))) < 1e-11
     assert np.max(np.abs(sym @ E - E * ev)) < 1e-12 * scale * max(1.0, np.sqrt(w / 64))
     assert np.allclose(M.cpu().numpy(), sym)  # input untouched
+
+
+def test_syev_topk_grid_and_cluster_paths_agree(ops, monkeypatch):
+    """w = 600 runs the cluster-resident tridiagonalisation; RSVD_TRIDIAG_GRID
+    forces the grid-barrier kernel (the path for w > 608). Same results."""
+    rng = np.random.default_rng(7)
+    Q, _ = np.linalg.qr(rng.standard_normal((600, 600)))
+    lam = 1.0 / np.arange(1, 601, dtype=float)
+    sym = (Q * lam) @ Q.T
+    sym = 0.5 * (sym + sym.T)
+    M = _t(sym)
+    ev_c, _, info_c = ops.syev_topk(M, 50)
+    monkeypatch.setenv("RSVD_TRIDIAG_GRID", "1")
+    ev_g, _, info_g = ops.syev_topk(M, 50)
+    assert int(info_c[0]) == 1 and int(info_g[0]) == 1
+    ref = np.sort(np.linalg.eigvalsh(sym))[::-1][:50]
+    assert np.max(np.abs(ev_c.cpu().numpy() - ref)) < 1e-14
+    assert np.max(np.abs(ev_g.cpu().numpy() - ref)) < 1e-14
