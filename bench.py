@@ -47,7 +47,54 @@ CONFIGS = {
     "c2": dict(n=50000, d=10000, k=50, q=10, spectrum="pow", noise=1e-3, variant="bk"),
     "c1": dict(n=2000, d=1000, k=20, q=8, spectrum="inv", noise=0.0, variant="bk"),
     "c4": dict(n=1000000, d=4096, k=200, q=6, spectrum="clustered", noise=0.0, variant="bk"),
+    "c3": dict(n=200000, d=100000, k=100, q=15, sparse=True, variant="bk"),
 }
+
+
+def make_csr(cfg, device, seed=4321):
+    """C3: per-row nnz m_i = clip(round(LogNormal(ln 100 - 1/2, 1)),
+    1, d); columns drawn Zipf(s = 1.1) over {0..d-1} (p_c ~ (c+1)^-1.1), duplicates
+    within a row dropped (sampling without replacement, approximated), sorted
+    ascending; values LogNormal(0, 1), each row scaled to unit L2 norm. Built
+    on the GPU with a seeded generator; int32 indices, FP32 values."""
+    import torch
+
+    n, d = cfg["n"], cfg["d"]
+    g = torch.Generator(device=device).manual_seed(seed)
+    mu = float(np.log(100.0) - 0.5)
+    m = torch.exp(mu + torch.randn(n, generator=g, device=device, dtype=torch.float64))
+    m = torch.clamp(torch.round(m), 1, d).to(torch.int64)
+    total = int(m.sum())
+    rows = torch.repeat_interleave(torch.arange(n, device=device), m)
+    pz = (torch.arange(1, d + 1, device=device, dtype=torch.float64)) ** -1.1
+    cdf = torch.cumsum(pz, 0)
+    cdf /= cdf[-1].clone()
+    u = torch.rand(total, generator=g, device=device, dtype=torch.float64)
+    cols = torch.searchsorted(cdf, u).clamp_(max=d - 1)
+    key = torch.unique(rows * d + cols)  # sorted, duplicates dropped
+    # without replacement: redraw each row's deficit until it holds m_i
+    # distinct columns (Zipf heads collide often; a few rounds suffice)
+    for _ in range(64):
+        have = torch.bincount(key // d, minlength=n)
+        deficit = (m - have).clamp_(min=0)
+        nd = int(deficit.sum())
+        if nd == 0:
+            break
+        r2 = torch.repeat_interleave(torch.arange(n, device=device), deficit)
+        u2 = torch.rand(nd, generator=g, device=device, dtype=torch.float64)
+        c2 = torch.searchsorted(cdf, u2).clamp_(max=d - 1)
+        key = torch.unique(torch.cat([key, r2 * d + c2]))
+    rows = key // d
+    cols = (key % d).to(torch.int32)
+    nnz = key.numel()
+    vals = torch.exp(torch.randn(nnz, generator=g, device=device, dtype=torch.float64))
+    norms = torch.zeros(n, device=device, dtype=torch.float64).index_add_(0, rows, vals * vals).sqrt_()
+    vals = (vals / norms[rows]).to(torch.float32)
+    counts = torch.bincount(rows, minlength=n)
+    indptr = torch.zeros(n + 1, device=device, dtype=torch.int32)
+    indptr[1:] = torch.cumsum(counts, 0).to(torch.int32)
+    torch.cuda.synchronize()
+    return indptr, cols, vals
 
 
 def _spectrum(kind, d):
@@ -61,6 +108,57 @@ def _spectrum(kind, d):
         s[:200] = 1 - 0.001 * i[:200]
         return s
     raise ValueError(kind)
+
+
+def workload_config(name, cfgd, cfg, world, nnz=None):
+    """The `config` object of the JSON line (shared by both arms)."""
+    n, d, k = cfgd["n"], cfgd["d"], cfgd["k"]
+    w = cfg.p * (cfg.resolve_q(d) + 1)
+    sparse = bool(cfgd.get("sparse"))
+    return {"workload": (f"{name.upper()}: " + (f"CSR FP32 A {n}x{d} nnz {nnz}" if sparse else f"dense FP32 A {n}x{d}")
+                         + f", BK k={k} q={cfgd['q']}->{cfg.resolve_q(d)}, width {w}"),
+            "n": n, "d": d, "k": k, "q": cfgd["q"], "q_eff": cfg.resolve_q(d), "krylov_width": w,
+            "parallelism": f"rowshard{world}",
+            "l2": ("CSR %.0f MB + blocks; dense rows L2-resident by design (gather-bound)" % (nnz * 8 / 1e6)
+                   if sparse else "inputs larger than L2 (A = %.1f GB)" % (n * d * 4 / 1e9))}
+
+
+def spmm_probe(dev, reps=5):
+    """The SpMM half of the metric on the C3 matrix: A.X and
+    A^T.Y at width k = 100 through the load-balanced CSR kernel, CUDA-event
+    timed; GB/s are SURVEY's algorithmic bytes nnz (4 + 4) + (rows + 1) 4 +
+    (d + n) b 4 against the measured HBM copy bandwidth. The kernel is
+    gather-bound: each nonzero reads a 400-byte row of the dense block (L2)."""
+    import torch
+    from paper_1504_05477_b200.operators import CsrDeviceOp
+
+    cfgd = CONFIGS["c3"]
+    n, d, p = cfgd["n"], cfgd["d"], cfgd["k"]
+    indptr, colv, valv = make_csr(cfgd, dev)
+    op = CsrDeviceOp(indptr, colv, valv, d)
+    g = torch.Generator(device=dev).manual_seed(5)
+    X = torch.randn((d, p), generator=g, device=dev)
+    Y = torch.empty((n, p), device=dev)
+    C = torch.empty((d, p), device=dev)
+    nnz = valv.numel()
+    hbm, _, _ = _peaks()
+    res = {"config": f"C3 CSR {n}x{d}, nnz {nnz}, width {p}", "peak_gbs": hbm}
+    for name, fn, rows in (("A.X", lambda: op.apply(X, Y), n), ("A^T.Y", lambda: op.apply_t(Y, C), d)):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        byt = nnz * 8 + (rows + 1) * 4 + (n + d) * p * 4
+        res[name] = {"ms": ms, "algorithmic_gbs": byt / ms / 1e6, "frac": byt / ms / 1e6 / hbm,
+                     "gathered_gbs": (nnz * p * 4 + byt) / ms / 1e6}
+    del op, indptr, colv, valv
+    torch.cuda.empty_cache()
+    return res
 
 
 def _profiled_traffic():
@@ -181,15 +279,29 @@ def run_ours(args):
     cfgd = CONFIGS[args.config]
     n, d, k = cfgd["n"], cfgd["d"], cfgd["k"]
     cfg = rk.RsvdConfig(k=k, variant=cfgd["variant"], q=cfgd["q"], seed=0)
-    A_full = make_matrix(cfgd, dev)
+    sparse = bool(cfgd.get("sparse"))
     lo, hi = krylov.shard_rows(n, world, rank)
     if world > 1:
         comm = krylov.TorchComm(n_total=n, row_offset=lo)
-        A = A_full[lo:hi].contiguous()
-        del A_full
+    if sparse:
+        from paper_1504_05477_b200.operators import CsrDeviceOp
+
+        indptr, colv, valv = make_csr(cfgd, dev)
+        if world > 1:
+            a0, a1 = int(indptr[lo]), int(indptr[hi])
+            indptr = (indptr[lo: hi + 1] - indptr[lo]).contiguous()
+            colv, valv = colv[a0:a1].contiguous(), valv[a0:a1].contiguous()
+        A = None
+        nnz_local = valv.numel()
+        op = CsrDeviceOp(indptr, colv, valv, d, n_total=n, row_offset=lo)
     else:
-        A = A_full
-    op = DenseDeviceOp(A, n_total=n, row_offset=lo)
+        A_full = make_matrix(cfgd, dev)
+        if world > 1:
+            A = A_full[lo:hi].contiguous()
+            del A_full
+        else:
+            A = A_full
+        op = DenseDeviceOp(A, n_total=n, row_offset=lo)
     Pi = rk.gaussian(d, cfg.p, rk.SeededRng(cfg.seed)).data
 
     # instrumentation of the dominant kernels (A X / A^T Y on the op's stream)
@@ -268,16 +380,19 @@ def run_ours(args):
     chain = [(e0_.elapsed_time(e1_), kind) for kind, width, e0_, e1_ in events if width == cfg.p]
     rr = [(e0_.elapsed_time(e1_), kind) for kind, width, e0_, e1_ in events if width != cfg.p]
     n_loc = hi - lo
-    bytes_per = n_loc * d * 4 + (n_loc + d) * cfg.p * 4
+    if sparse:  # nnz (4 + 4) + (rows + 1) 4 + (d + n) b 4 per SpMM
+        bytes_per = nnz_local * 8 + (n_loc + 1) * 4 + (n_loc + d) * cfg.p * 4
+    else:
+        bytes_per = n_loc * d * 4 + (n_loc + d) * cfg.p * 4
     avg_chain_ms = float(np.mean([t for t, _ in chain])) if chain else float("nan")
     achieved = bytes_per / (avg_chain_ms * 1e-3) / 1e9
     rr_ms = float(np.mean([t for t, _ in rr])) if rr else float("nan")
     w = (cfgd["q"] + 1 + (cfgd["q"] % 2 == 0)) * cfg.p
-    rr_tflops = 2.0 * n_loc * d * w / (rr_ms * 1e-3) / 1e12 if rr else None
+    rr_tflops = 2.0 * n_loc * d * w / (rr_ms * 1e-3) / 1e12 if (rr and not sparse) else None
 
     # e2e through the public API with host (pinned) A
     e2e = None
-    if world == 1 and not args.no_e2e:
+    if world == 1 and not args.no_e2e and not sparse:
         A_host = A.cpu().pin_memory()
         for _ in range(max(1, min(args.warmup, 2))):
             r = rk.block_krylov(A_host, cfg)
@@ -302,15 +417,14 @@ def run_ours(args):
         "higher_is_better": False,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "f32 (3xTF32 products, f64 small algebra)" if A.dtype == torch.float32 else "f64",
+        "dtype": ("f32 (CSR SpMM, f64 small algebra)" if sparse else
+                  "f32 (3xTF32 products, f64 small algebra)" if A.dtype == torch.float32 else "f64"),
         "data": "synthetic",
-        "config": {"workload": f"{args.config.upper()}: dense FP32 A {n}x{d}, BK k={k} q={cfgd['q']}->"
-                               f"{cfg.resolve_q(d)}, width {w}", "n": n, "d": d, "k": k, "q": cfgd["q"],
-                   "q_eff": cfg.resolve_q(d), "krylov_width": w, "parallelism": f"rowshard{world}",
-                   "l2": "inputs larger than L2 (A = %.1f GB)" % (n * d * 4 / 1e9)},
-        "roofline": {"bound": "hbm", "kernel": "Krylov-chain A.X / A^T.Y (width %d)" % cfg.p,
+        "config": workload_config(args.config, cfgd, cfg, world, nnz_local if sparse else None),
+        "roofline": {"bound": "hbm", "kernel": ("CSR SpMM A.X / A^T.Y (width %d)" if sparse else
+                                               "Krylov-chain A.X / A^T.Y (width %d)") % cfg.p,
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "peak_source": peak_src, "traffic": _profiled_traffic(),
+                     "peak_source": peak_src, "traffic": None if sparse else _profiled_traffic(),
                      "algorithmic_bytes_per_launch": bytes_per, "avg_launch_ms": avg_chain_ms},
         "kernels": {"rayleigh_ritz_ATQ_ms": rr_ms, "rayleigh_ritz_ATQ_tflops": rr_tflops},
         "gpu_launches": launches,
@@ -319,8 +433,10 @@ def run_ours(args):
     }
     if e2e:
         out["e2e"] = e2e
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and not sparse:
         out["cpu_baseline"] = cpu_baseline(A, cfgd, cfg, Pi, args, df)
+    if rank == 0 and world == 1 and not sparse and not args.no_spmm:
+        out["spmm_c3"] = spmm_probe(dev)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -420,6 +536,10 @@ def run_reference(args):
     dev = torch.device("cuda", 0)
     cfgd = CONFIGS[args.config]
     cfg = rk.RsvdConfig(k=cfgd["k"], variant=cfgd["variant"], q=cfgd["q"], seed=0)
+    if cfgd.get("sparse"):
+        print(json.dumps({"impl": "reference", "unavailable": "sparse configs: the reference arm is wired for dense "
+                          "configs only (C1/C2/C4)"}), flush=True)
+        return
     A = make_matrix(cfgd, dev)
     Pi = rk.gaussian(cfgd["d"], cfg.p, rk.SeededRng(cfg.seed)).data
     A_host = A.cpu().numpy()
@@ -435,7 +555,7 @@ def run_reference(args):
     out = {"impl": "reference", "metric": "rank-k block-Krylov SVD wall time", "value": v, "unit": "ms",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v,
            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic", "config": {"workload": args.config.upper()},
+           "data": "synthetic", "config": workload_config(args.config, cfgd, cfg, world),
            "cpu_baseline": {"value": v, "unit": "ms", "cores": r["cores"], "kind": r["kind"], "sample": r["sample"]},
            "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -450,6 +570,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-spmm", action="store_true", help="skip the C3 SpMM measurement on dense configs")
     ap.add_argument("--count-launches", action="store_true", default=True)
     ap.add_argument("--cpu-budget", type=float, default=25.0)
     ap.add_argument("--graph", type=int, default=1, help="replay the factorization as a CUDA graph")

@@ -98,6 +98,20 @@ int rsvd_gemm_tn(int dtype, int out_dtype, int64_t m, int64_t n, int64_t k, doub
 int rsvd_spmm_csr(int dtype, int idx64, int64_t nrows, int64_t ncols, int64_t nb,
                   const void *indptr, const void *col, const void *val, const void *B,
                   int64_t ldb, double alpha, double beta, void *C, int64_t ldc, void *stream);
+/* Load-balanced variant with a row-split plan built once per operator (host
+ * plumbing, paper_1504_05477_b200/device.py:spmm_plan): chunk c covers the
+ * nonzeros [chunk_lo[c], chunk_hi[c]) of row chunk_row[c]; chunk_slot[c] = -1
+ * writes C directly, otherwise the partial sum goes to workspace slot
+ * chunk_slot[c] (ws: slots x min(nb, 256) elements; wider blocks run in
+ * column panels of 256). Split row s (split_row[s]) sums
+ * slots [split_beg[s], split_beg[s+1]) in order, then applies alpha / beta:
+ * deterministic, no atomics. Rows with no chunk are not touched. */
+int rsvd_spmm_csr_plan(int dtype, int idx64, int64_t nrows, int64_t nb, const void *col, const void *val,
+                       const void *B, int64_t ldb, double alpha, double beta, void *C, int64_t ldc,
+                       int64_t nchunks, const int64_t *chunk_lo, const int64_t *chunk_hi,
+                       const int32_t *chunk_row, const int32_t *chunk_slot, int64_t nsplit,
+                       const int32_t *split_row, const int64_t *split_beg, void *ws, int64_t ws_bytes,
+                       void *stream);
 /* CSR (nrows x ncols, sorted columns) -> CSR of the transpose, stable in row
  * order. perm_by_col[e] must be a stable column-sorted permutation of the
  * nonzeros (supplied by the caller's sort); t_indptr has ncols+1 entries. */

@@ -28,6 +28,8 @@ _SIGS = {
     "rsvd_gemm_tn": ([_int, _int, _i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64, _vp, _vp, _vp,
                       _i64, _int, _vp, _vp], _int),
     "rsvd_spmm_csr": ([_int, _int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _i64, _vp], _int),
+    "rsvd_spmm_csr_plan": ([_int, _int, _i64, _i64, _vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _i64, _i64, _vp, _vp, _vp,
+                            _vp, _i64, _vp, _vp, _vp, _i64, _vp], _int),
     "rsvd_csr_transpose": ([_int, _int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _int),
     "rsvd_chol_deflate_ws_bytes": ([_i64], _i64),
     "rsvd_chol_deflate": ([_i64, _vp, _i64, _vp, _dbl, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp], _int),

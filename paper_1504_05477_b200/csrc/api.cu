@@ -43,6 +43,10 @@ int fill_stream(int64_t n, int64_t nvec, uint64_t seed, double* out, cudaStream_
 int spmm_csr(int dtype, int idx64, int64_t nrows, int64_t ncols, int64_t nb, const void* indptr,
              const void* col, const void* val, const void* B, int64_t ldb, double alpha,
              double beta, void* C, int64_t ldc, cudaStream_t st);
+int spmm_csr_plan(int dtype, int idx64, int64_t nb, const void* col, const void* val, const void* B, int64_t ldb,
+                  double alpha, double beta, void* C, int64_t ldc, int64_t nchunks, const int64_t* clo,
+                  const int64_t* chi, const int32_t* crow, const int32_t* cslot, int64_t nsplit,
+                  const int32_t* srow, const int64_t* sbeg, void* ws, cudaStream_t st);
 int csr_transpose(int dtype, int idx64, int64_t nrows, int64_t ncols, int64_t nnz,
                   const void* indptr, const void* col, const void* val, const int64_t* perm,
                   void* tptr, void* tcol, void* tval, cudaStream_t st);
@@ -125,6 +129,21 @@ int rsvd_spmm_csr(int dtype, int idx64, int64_t nrows, int64_t ncols, int64_t nb
     RSVD_REQUIRE(nrows >= 0 && ncols >= 0 && nb >= 0 && ldb >= nb && ldc >= nb, "spmm: bad shape");
     return spmm_csr(dtype, idx64, nrows, ncols, nb, indptr, col, val, B, ldb, alpha, beta, C, ldc,
                     as_stream(stream));
+}
+
+int rsvd_spmm_csr_plan(int dtype, int idx64, int64_t nrows, int64_t nb, const void* col, const void* val,
+                       const void* B, int64_t ldb, double alpha, double beta, void* C, int64_t ldc,
+                       int64_t nchunks, const int64_t* chunk_lo, const int64_t* chunk_hi,
+                       const int32_t* chunk_row, const int32_t* chunk_slot, int64_t nsplit,
+                       const int32_t* split_row, const int64_t* split_beg, void* ws, int64_t ws_bytes,
+                       void* stream) {
+    RSVD_REQUIRE(valid_dtype(dtype), "spmm_plan: bad dtype");
+    RSVD_REQUIRE(nrows >= 0 && nb >= 0 && ldb >= nb && ldc >= nb && nchunks >= 0 && nsplit >= 0,
+                 "spmm_plan: bad shape");
+    RSVD_REQUIRE(nsplit == 0 || (ws != nullptr && ws_bytes > 0), "spmm_plan: split rows need a workspace");
+    (void)nrows;
+    return spmm_csr_plan(dtype, idx64, nb, col, val, B, ldb, alpha, beta, C, ldc, nchunks, chunk_lo, chunk_hi,
+                         chunk_row, chunk_slot, nsplit, split_row, split_beg, ws, as_stream(stream));
 }
 
 int rsvd_csr_transpose(int dtype, int idx64, int64_t nrows, int64_t ncols, int64_t nnz,

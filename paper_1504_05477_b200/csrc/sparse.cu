@@ -82,6 +82,163 @@ int launch_spmm(int64_t nrows, int64_t nb, const void* indptr, const void* col, 
     return RSVD_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Load-balanced product with a row-split plan (built once per operator): a
+// chunk is (row, nonzeros [lo, hi), slot). Rows of at most `chunk` nonzeros
+// are one chunk written straight to C (slot -1); longer rows (the Zipf
+// columns of A^T: 194k nonzeros in C3's column 0) are cut into chunks whose
+// partial sums go to workspace slots and are added in chunk order by
+// k_spmm_split_reduce (deterministic). Warp per chunk; 4 nonzeros in flight
+// per lane; FP32 rows of B gathered as float4 (VEC) when aligned.
+template <typename T, typename I, int NPL, bool VEC>
+__global__ void __launch_bounds__(256)
+k_spmm_plan(int64_t nchunks, int64_t nb, const I* __restrict__ col, const T* __restrict__ val,
+            const T* __restrict__ B, int64_t ldb, double alpha, double beta, T* __restrict__ C, int64_t ldc,
+            const int64_t* __restrict__ clo, const int64_t* __restrict__ chi, const int32_t* __restrict__ crow,
+            const int32_t* __restrict__ cslot, T* __restrict__ ws) {
+    const int lane = threadIdx.x & 31;
+    const int64_t ch = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (ch >= nchunks) return;
+    constexpr int W = VEC ? 4 * NPL : NPL;  // outputs per lane
+    T acc[W];
+#pragma unroll
+    for (int t = 0; t < W; ++t) acc[t] = T(0);
+    const int64_t lo = clo[ch], hi = chi[ch];
+    auto accum = [&](const T* brow, T v) {
+        if constexpr (VEC) {
+#pragma unroll
+            for (int t = 0; t < NPL; ++t) {
+                const int64_t j = 4 * (lane + 32 * t);
+                if (j < nb) {
+                    const float4 b4 = *reinterpret_cast<const float4*>(brow + j);
+                    acc[4 * t + 0] = fmaf(v, b4.x, acc[4 * t + 0]);
+                    acc[4 * t + 1] = fmaf(v, b4.y, acc[4 * t + 1]);
+                    acc[4 * t + 2] = fmaf(v, b4.z, acc[4 * t + 2]);
+                    acc[4 * t + 3] = fmaf(v, b4.w, acc[4 * t + 3]);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < NPL; ++t) {
+                const int64_t j = lane + 32 * t;
+                if (j < nb) acc[t] = fma(v, brow[j], acc[t]);
+            }
+        }
+    };
+    for (int64_t base = lo; base < hi; base += 32) {
+        const int64_t e = base + lane;
+        int64_t c = 0;
+        T v = T(0);
+        if (e < hi) {
+            c = (int64_t)col[e];
+            v = val[e];
+        }
+        const int cnt = (int)min((int64_t)32, hi - base);
+        int i = 0;
+        for (; i + 4 <= cnt; i += 4) {
+            const int64_t c0 = __shfl_sync(0xffffffffu, c, i), c1 = __shfl_sync(0xffffffffu, c, i + 1);
+            const int64_t c2 = __shfl_sync(0xffffffffu, c, i + 2), c3 = __shfl_sync(0xffffffffu, c, i + 3);
+            const T v0 = __shfl_sync(0xffffffffu, v, i), v1 = __shfl_sync(0xffffffffu, v, i + 1);
+            const T v2 = __shfl_sync(0xffffffffu, v, i + 2), v3 = __shfl_sync(0xffffffffu, v, i + 3);
+            accum(B + c0 * ldb, v0);
+            accum(B + c1 * ldb, v1);
+            accum(B + c2 * ldb, v2);
+            accum(B + c3 * ldb, v3);
+        }
+        for (; i < cnt; ++i) {
+            const int64_t ci = __shfl_sync(0xffffffffu, c, i);
+            const T vi = __shfl_sync(0xffffffffu, v, i);
+            accum(B + ci * ldb, vi);
+        }
+    }
+    const int slot = cslot[ch];
+    const int64_t row = crow[ch];
+#pragma unroll
+    for (int t = 0; t < W; ++t) {
+        const int64_t j = VEC ? 4 * (lane + 32 * (t / 4)) + (t % 4) : lane + 32 * t;
+        if (j >= nb) continue;
+        if (slot >= 0) {
+            ws[(int64_t)slot * nb + j] = acc[t];
+        } else {
+            double r = alpha * (double)acc[t];
+            if (beta != 0.0) r += beta * (double)C[row * ldc + j];
+            C[row * ldc + j] = (T)r;
+        }
+    }
+}
+
+template <typename T>
+__global__ void k_spmm_split_reduce(int64_t nsplit, int64_t nb, const int32_t* __restrict__ srow,
+                                    const int64_t* __restrict__ sbeg, const T* __restrict__ ws, double alpha,
+                                    double beta, T* __restrict__ C, int64_t ldc) {
+    const int lane = threadIdx.x & 31;
+    const int64_t sidx = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (sidx >= nsplit) return;
+    const int64_t row = srow[sidx], b0 = sbeg[sidx], b1 = sbeg[sidx + 1];
+    for (int64_t j = lane; j < nb; j += 32) {
+        double acc = 0.0;
+        for (int64_t sl = b0; sl < b1; ++sl) acc += (double)ws[sl * nb + j];
+        double r = alpha * acc;
+        if (beta != 0.0) r += beta * (double)C[row * ldc + j];
+        C[row * ldc + j] = (T)r;
+    }
+}
+
+template <typename T, typename I>
+int launch_spmm_plan_panel(int64_t nb, const void* col, const void* val, const T* bp, int64_t ldb, double alpha,
+                           double beta, T* cc, int64_t ldc, int64_t nchunks, const int64_t* clo, const int64_t* chi,
+                           const int32_t* crow, const int32_t* cslot, int64_t nsplit, const int32_t* srow,
+                           const int64_t* sbeg, void* ws, cudaStream_t st) {
+    const unsigned grid = (unsigned)cdiv(nchunks * 32, 256);
+    const I* cp = (const I*)col;
+    const T* vp = (const T*)val;
+    T* wp = (T*)ws;
+    const bool vec = sizeof(T) == 4 && ldb % 4 == 0 && nb % 4 == 0 && ((uintptr_t)bp & 15) == 0;
+    if (nchunks > 0) {
+        if (vec && nb <= 128)
+            k_spmm_plan<T, I, 1, true><<<grid, 256, 0, st>>>(nchunks, nb, cp, vp, bp, ldb, alpha, beta, cc, ldc, clo,
+                                                              chi, crow, cslot, wp);
+        else if (vec && nb <= 256)
+            k_spmm_plan<T, I, 2, true><<<grid, 256, 0, st>>>(nchunks, nb, cp, vp, bp, ldb, alpha, beta, cc, ldc, clo,
+                                                              chi, crow, cslot, wp);
+        else if (nb <= 32)
+            k_spmm_plan<T, I, 1, false><<<grid, 256, 0, st>>>(nchunks, nb, cp, vp, bp, ldb, alpha, beta, cc, ldc,
+                                                               clo, chi, crow, cslot, wp);
+        else if (nb <= 64)
+            k_spmm_plan<T, I, 2, false><<<grid, 256, 0, st>>>(nchunks, nb, cp, vp, bp, ldb, alpha, beta, cc, ldc,
+                                                               clo, chi, crow, cslot, wp);
+        else if (nb <= 128)
+            k_spmm_plan<T, I, 4, false><<<grid, 256, 0, st>>>(nchunks, nb, cp, vp, bp, ldb, alpha, beta, cc, ldc,
+                                                               clo, chi, crow, cslot, wp);
+        else
+            k_spmm_plan<T, I, 8, false><<<grid, 256, 0, st>>>(nchunks, nb, cp, vp, bp, ldb, alpha, beta, cc, ldc,
+                                                               clo, chi, crow, cslot, wp);
+        RSVD_CHECK_LAUNCH();
+    }
+    if (nsplit > 0) {
+        k_spmm_split_reduce<T><<<(unsigned)cdiv(nsplit * 32, 256), 256, 0, st>>>(nsplit, nb, srow, sbeg, wp, alpha,
+                                                                                 beta, cc, ldc);
+        RSVD_CHECK_LAUNCH();
+    }
+    return RSVD_OK;
+}
+
+// wide blocks run in column panels of 256 (the workspace holds one panel's
+// partials; panels are stream-ordered)
+template <typename T, typename I>
+int launch_spmm_plan(int64_t nb, const void* col, const void* val, const void* B, int64_t ldb, double alpha,
+                     double beta, void* C, int64_t ldc, int64_t nchunks, const int64_t* clo, const int64_t* chi,
+                     const int32_t* crow, const int32_t* cslot, int64_t nsplit, const int32_t* srow,
+                     const int64_t* sbeg, void* ws, cudaStream_t st) {
+    for (int64_t j0 = 0; j0 < nb; j0 += 256) {
+        const int64_t wdt = nb - j0 < 256 ? nb - j0 : 256;
+        const int rc = launch_spmm_plan_panel<T, I>(wdt, col, val, (const T*)B + j0, ldb, alpha, beta, (T*)C + j0,
+                                                    ldc, nchunks, clo, chi, crow, cslot, nsplit, srow, sbeg, ws, st);
+        if (rc) return rc;
+    }
+    return RSVD_OK;
+}
+
 template <typename T, typename I>
 __global__ void k_csr_transpose_fill(int64_t nrows, int64_t nnz, const I* __restrict__ indptr,
                                      const I* __restrict__ col, const T* __restrict__ val,
@@ -128,6 +285,23 @@ int spmm_csr(int dtype, int idx64, int64_t nrows, int64_t ncols, int64_t nb, con
                      : launch_spmm<double, int32_t>(nrows, nb, indptr, col, val, B, ldb, alpha, beta, C, ldc, st);
     return idx64 ? launch_spmm<float, int64_t>(nrows, nb, indptr, col, val, B, ldb, alpha, beta, C, ldc, st)
                  : launch_spmm<float, int32_t>(nrows, nb, indptr, col, val, B, ldb, alpha, beta, C, ldc, st);
+}
+
+int spmm_csr_plan(int dtype, int idx64, int64_t nb, const void* col, const void* val, const void* B, int64_t ldb,
+                  double alpha, double beta, void* C, int64_t ldc, int64_t nchunks, const int64_t* clo,
+                  const int64_t* chi, const int32_t* crow, const int32_t* cslot, int64_t nsplit,
+                  const int32_t* srow, const int64_t* sbeg, void* ws, cudaStream_t st) {
+    if (nb == 0) return RSVD_OK;
+#define RSVD_SPP(T, I)                                                                                          \
+    return launch_spmm_plan<T, I>(nb, col, val, B, ldb, alpha, beta, C, ldc, nchunks, clo, chi, crow, cslot, \
+                                  nsplit, srow, sbeg, ws, st)
+    if (dtype == RSVD_F64) {
+        if (idx64) RSVD_SPP(double, int64_t);
+        RSVD_SPP(double, int32_t);
+    }
+    if (idx64) RSVD_SPP(float, int64_t);
+    RSVD_SPP(float, int32_t);
+#undef RSVD_SPP
 }
 
 template <typename T, typename I>

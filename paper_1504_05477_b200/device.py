@@ -241,6 +241,50 @@ def spmm_csr(indptr, col, val, ncols, B, C, alpha=1.0, beta=0.0):
     return C
 
 
+class SpmmPlan:
+    """Row-split plan of a CSR matrix for rsvd_spmm_csr_plan (built once per
+    operator): rows longer than `chunk` nonzeros are cut into chunks whose
+    partial sums are added in chunk order."""
+
+    def __init__(self, indptr, chunk=512):
+        dev = indptr.device
+        n = indptr.numel() - 1
+        ip = indptr.to(torch.int64)
+        lens = ip[1:] - ip[:-1]
+        nch = torch.clamp((lens + chunk - 1) // chunk, min=1)  # an empty row still writes beta * C
+        total = int(nch.sum())  # host sync: plan construction is setup, not the hot loop
+        crow = torch.repeat_interleave(torch.arange(n, device=dev), nch)
+        first = torch.cumsum(nch, 0) - nch
+        k_in_row = torch.arange(total, device=dev) - first[crow]
+        self.lo = (ip[crow] + k_in_row * chunk).contiguous()
+        self.hi = torch.minimum(self.lo + chunk, ip[crow + 1]).contiguous()
+        self.row = crow.to(torch.int32).contiguous()
+        split = nch > 1
+        split_chunk = split[crow]
+        nslots = int(split_chunk.sum())
+        self.slot = torch.full((total,), -1, dtype=torch.int32, device=dev)
+        self.slot[split_chunk] = torch.arange(nslots, dtype=torch.int32, device=dev)
+        self.split_row = torch.nonzero(split).flatten().to(torch.int32).contiguous()
+        counts = nch[split]
+        self.split_beg = torch.zeros(self.split_row.numel() + 1, dtype=torch.int64, device=dev)
+        self.split_beg[1:] = torch.cumsum(counts, 0)
+        self.nchunks, self.nsplit, self.nslots, self.nrows = total, self.split_row.numel(), nslots, n
+
+
+def spmm_csr_plan(plan, col, val, B, C, alpha=1.0, beta=0.0):
+    """C = alpha A B + beta C through the load-balanced kernel (rsvd_spmm_csr_plan)."""
+    idx64 = 1 if col.dtype == torch.int64 else 0
+    assert val.dtype == B.dtype == C.dtype
+    nb = B.shape[1]
+    ws = WS.get(max(1, plan.nslots * min(nb, 256) * B.element_size()), B.device) if plan.nsplit else None
+    check(lib().rsvd_spmm_csr_plan(dcode(val), idx64, plan.nrows, nb, _ptr(col), _ptr(val), _ptr(B), _ld(B),
+                                   float(alpha), float(beta), _ptr(C), _ld(C), plan.nchunks, _ptr(plan.lo),
+                                   _ptr(plan.hi), _ptr(plan.row), _ptr(plan.slot), plan.nsplit, _ptr(plan.split_row),
+                                   _ptr(plan.split_beg), _ptr(ws), 0 if ws is None else ws.numel(), _stream()),
+          "spmm_csr_plan")
+    return C
+
+
 def csr_transpose(indptr, col, val, nrows, ncols):
     """Device CSR of A^T (stable in row order). The stable column sort that
     orders the nonzeros is torch plumbing done once per operator."""

@@ -75,7 +75,12 @@ class TorchComm:
         self.row_offset = row_offset
 
     def allreduce(self, t):
-        self.dist.all_reduce(t, group=self.group)
+        if t.is_contiguous():
+            self.dist.all_reduce(t, group=self.group)
+        else:  # padded row buffers (krylov.rows_buffer)
+            tmp = t.contiguous()
+            self.dist.all_reduce(tmp, group=self.group)
+            t.copy_(tmp)
         return t
 
     def all_gather(self, t):
@@ -397,7 +402,12 @@ def rayleigh_ritz(ops, comm, op, Q, k, n_total, row_offset, sign_fn=None):
     dev = op.device
     w = Q.shape[1]
     d = op.shape[1]
-    W = torch.empty((d, w), dtype=torch.float64, device=dev)
+    # W = A^T Q carries the precision of the products: FP64 on the FP64 path;
+    # FP32-accurate on the FP32 path (3xTF32 / FP32 SpMM), where it is stored in
+    # FP32 and M = W^T W runs on the tensor cores with FP64 output (the FP64
+    # CUDA-core Gram of an FP64 copy took 38 ms at C3, w = 1600)
+    wdt = torch.float64 if Q.dtype == torch.float64 else Q.dtype
+    W = rows_buffer(d, w, wdt, dev)
     op.apply_t(Q, W)
     comm.allreduce(W)
     M = torch.empty((w, w), dtype=torch.float64, device=dev)

@@ -67,7 +67,9 @@ class DenseDeviceOp:
 
 class CsrDeviceOp:
     """CSR A on the device; A^T products run as a gather over the CSR of A^T
-    built once (spmm_t, _kernels.pyx:95-113, without atomics)."""
+    built once (spmm_t, _kernels.pyx:95-113, without atomics). Both products
+    go through row-split plans (ops.SpmmPlan) so that the long rows of A^T
+    (Zipf-heavy columns of A) are spread over many warps."""
 
     def __init__(self, indptr, col, val, ncols, n_total=None, row_offset=0):
         self.indptr, self.col, self.val = indptr, col, val
@@ -80,6 +82,8 @@ class CsrDeviceOp:
         self.dtype = val.dtype
         self.device = val.device
         self.t_indptr, self.t_col, self.t_val = ops.csr_transpose(indptr, col, val, nrows, self.ncols)
+        self.plan = ops.SpmmPlan(indptr)
+        self.t_plan = ops.SpmmPlan(self.t_indptr)
         self.mu = None
 
     @property
@@ -92,14 +96,14 @@ class CsrDeviceOp:
 
     def apply(self, X, out):
         if out.dtype == self.dtype:
-            return ops.spmm_csr(self.indptr, self.col, self.val, self.ncols, X, out)
+            return ops.spmm_csr_plan(self.plan, self.col, self.val, X, out)
         tmp = torch.empty(out.shape, dtype=self.dtype, device=out.device)
-        ops.spmm_csr(self.indptr, self.col, self.val, self.ncols, X, tmp)
+        ops.spmm_csr_plan(self.plan, self.col, self.val, X, tmp)
         return ops.convert(tmp, out)
 
     def apply_t(self, Y, out):
         if out.dtype == self.dtype:
-            return ops.spmm_csr(self.t_indptr, self.t_col, self.t_val, self.local_rows, Y, out)
+            return ops.spmm_csr_plan(self.t_plan, self.t_col, self.t_val, Y, out)
         tmp = torch.empty(out.shape, dtype=self.dtype, device=out.device)
-        ops.spmm_csr(self.t_indptr, self.t_col, self.t_val, self.local_rows, Y, tmp)
+        ops.spmm_csr_plan(self.t_plan, self.t_col, self.t_val, Y, tmp)
         return ops.convert(tmp, out)

@@ -265,3 +265,41 @@ def test_syev_topk_grid_and_cluster_paths_agree(ops, monkeypatch):
     ref = np.sort(np.linalg.eigvalsh(sym))[::-1][:50]
     assert np.max(np.abs(ev_c.cpu().numpy() - ref)) < 1e-14
     assert np.max(np.abs(ev_g.cpu().numpy() - ref)) < 1e-14
+
+
+@pytest.mark.parametrize("nb,dtype", [(7, torch.float32), (100, torch.float32), (300, torch.float32),
+                                      (600, torch.float32), (64, torch.float64), (300, torch.float64)])
+def test_spmm_plan_split_rows_and_wide_blocks(ops, nb, dtype):
+    """Load-balanced CSR product: rows longer than the chunk (split, partials
+    summed in order), empty rows, column panels of 256 for wide blocks,
+    alpha / beta; against a dense numpy product."""
+    rng = np.random.default_rng(nb)
+    n, d = 300, 2000
+    lens = rng.integers(0, 40, n)
+    lens[[3, 77, 150]] = [1900, 1300, 700]  # split rows (chunk 512)
+    lens[[10, 11]] = 0
+    rows, cols = [], []
+    for i, m in enumerate(lens):
+        c = np.sort(rng.choice(d, size=int(m), replace=False))
+        rows += [i] * int(m)
+        cols += list(c)
+    rows, cols = np.array(rows), np.array(cols)
+    vals = rng.standard_normal(rows.size)
+    A = np.zeros((n, d))
+    A[rows, cols] = vals
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    indptr[1:] = np.cumsum(np.bincount(rows, minlength=n))
+    dev = "cuda"
+    ip = torch.from_numpy(indptr).to(dev, torch.int32)
+    cl = torch.from_numpy(cols).to(dev, torch.int32)
+    vl = torch.from_numpy(vals).to(dev, dtype)
+    B = rng.standard_normal((d, nb))
+    C0 = rng.standard_normal((n, nb))
+    Bt = torch.from_numpy(B).to(dev, dtype)
+    Ct = torch.from_numpy(C0).to(dev, dtype)
+    plan = ops.SpmmPlan(ip)
+    assert plan.nsplit == 3
+    ops.spmm_csr_plan(plan, cl, vl, Bt, Ct, alpha=0.5, beta=2.0)
+    ref = 0.5 * (A @ B) + 2.0 * C0
+    tol = 1e-4 if dtype == torch.float32 else 1e-12
+    assert np.max(np.abs(Ct.cpu().double().numpy() - ref)) < tol * np.abs(ref).max()

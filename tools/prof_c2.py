@@ -9,10 +9,14 @@ from paper_1504_05477_b200.operators import DenseDeviceOp
 
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "c2"
 cfgd = bench.CONFIGS[cfgname]
-A = bench.make_matrix(cfgd, "cuda")
 cfg = rsvd.RsvdConfig(k=cfgd["k"], variant=cfgd["variant"], q=cfgd["q"], seed=0)
-n, d = A.shape
-op = DenseDeviceOp(A, n_total=n, row_offset=0)
+n, d = cfgd["n"], cfgd["d"]
+if cfgd.get("sparse"):
+    from paper_1504_05477_b200.operators import CsrDeviceOp
+    op = CsrDeviceOp(*bench.make_csr(cfgd, "cuda"), d)
+else:
+    A = bench.make_matrix(cfgd, "cuda")
+    op = DenseDeviceOp(A, n_total=n, row_offset=0)
 Pi = mx.gaussian(d, cfg.p, mx.SeededRng(cfg.seed)).data
 for _ in range(2):
     rsvd.run_device(op, cfg, Pi=Pi)
