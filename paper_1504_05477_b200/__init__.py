@@ -8,6 +8,7 @@ errors.py for the exception types). Compute runs in librsvd_b200.so
 no CPU fallback.
 """
 
+from . import metrics  # noqa: F401  (GPU parity metrics, SURVEY 8(f) f1)
 from .errors import ConvergenceError, ParseError
 from .matrix import DenseMatrix, SeededRng, SparseMatrixCSR, as_dense_array, gaussian
 from .rsvd import (

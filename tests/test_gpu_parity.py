@@ -235,3 +235,29 @@ def test_torch_cuda_input_and_post_process(rk):
     r1 = rk.block_krylov(At, rk.RsvdConfig(k=5, variant="bk", q=3, seed=1))
     r2 = rk.block_krylov(A, rk.RsvdConfig(k=5, variant="bk", q=3, seed=1))
     assert np.array_equal(r1.Z.data, r2.Z.data)
+
+
+def test_gpu_metrics_match_oracle(rk):
+    """captured variance and the restarted power-iteration
+    spectral error on the device match the reference's definitions
+    (metrics.py:65-81, 102-142; factor.py:217-261) evaluated by the oracle."""
+    rng = np.random.default_rng(3)
+    n, d, k = 900, 400, 12
+    u, _ = np.linalg.qr(rng.standard_normal((n, d)))
+    v, _ = np.linalg.qr(rng.standard_normal((d, d)))
+    s = 1.0 / np.arange(1, d + 1)
+    A = (u * s) @ v.T
+    r = rk.block_krylov(A, rk.RsvdConfig(k=k, variant="bk", q=4, seed=0))
+    Z = r.Z.data
+    cap = rk.metrics.captured_variance(A, Z)
+    assert np.max(np.abs(cap - o.captured_variance(A, Z)) / o.captured_variance(A, Z)) < 1e-12
+    est = rk.metrics.spectral_error(A, Z)
+    ref = o.spectral_error(A, Z)
+    assert abs(est - ref) / ref < 1e-7, (est, ref)
+    exact = o.spectral_error_exact(A, Z)
+    assert est <= exact * (1 + 1e-12) and est > exact * (1 - 1e-6)
+    pv = rk.metrics.per_vector_errors(A, Z, s)
+    assert pv.shape == (k,) and np.all(pv < 1e-6)
+    # FP32 path: FP32 A, same Z -> within FP32 tolerance
+    cap32 = rk.metrics.captured_variance(A.astype(np.float32), Z)
+    assert np.max(np.abs(cap32 - cap) / cap) < 1e-5

@@ -49,3 +49,13 @@ s64f = df64f.sigma.cpu().numpy()
 f = lambda a, b: np.max(np.abs(a - b) / b)
 print(f"FP64 projected vs reference {f(s64, r.sigma):.2e}; FP32 projected vs FP64 projected {f(sig, s64):.2e}; "
       f"FP64 faithful (ours) vs reference {f(s64f, r.sigma):.2e}")
+# spectral error ||A - Z Z^T A||_2 (reference estimator, GPU): ours vs the reference's Z
+import paper_1504_05477_b200 as rk
+from paper_1504_05477_b200.operators import DenseDeviceOp as _D
+op32 = _D(A)
+from paper_1504_05477_b200 import metrics as M
+mi = 5000
+b_ours, it_o = M.spectral_norm_batched(M._Deflated(op32, M._as_device_z(Z, op32)), max_iters=mi)
+b_ref, it_r = M.spectral_norm_batched(M._Deflated(op32, M._as_device_z(np.ascontiguousarray(r.Z), op32)), max_iters=mi)
+so, sr = float(b_ours.max()), float(b_ref.max())
+print(f"spectral error (<= {mi} power iterations per start, FP32 A): ours {so:.9f} reference Z {sr:.9f} rel {abs(so-sr)/sr:.2e}; iterations {it_o.tolist()} / {it_r.tolist()}")
