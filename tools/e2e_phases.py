@@ -1,0 +1,45 @@
+"""Phase timing of the public-API call block_krylov(A_host_pinned) at C2."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch, numpy as np
+import bench
+import paper_1504_05477_b200 as rk
+from paper_1504_05477_b200 import rsvd
+cfgd = bench.CONFIGS["c2"]
+A = bench.make_matrix(cfgd, "cuda")
+Ah = A.cpu().pin_memory(); del A
+cfg = rk.RsvdConfig(k=50, variant="bk", q=10, seed=0)
+for _ in range(3):
+    rk.block_krylov(Ah, cfg)
+torch.cuda.synchronize()
+key = list(rsvd._GRAPH_CACHE.keys())[0]
+buf, op, graphed, pi, _ = rsvd._GRAPH_CACHE[key]
+def tm(f):
+    torch.cuda.synchronize(); t0 = time.perf_counter(); r = f(); torch.cuda.synchronize(); return r, (time.perf_counter() - t0) * 1e3
+_, t_up = tm(lambda: buf.copy_(Ah, non_blocking=True))
+_, t_fin = tm(lambda: rsvd._upload_into(buf, Ah))
+df, t_g = tm(lambda: graphed.run(pi))
+_, t_finish = tm(lambda: rsvd._finish(df, cfg, time.perf_counter()))
+_, t_total = tm(lambda: rk.block_krylov(Ah, cfg))
+print(f"upload {t_up:.1f} ms ({2.0/t_up*1e3:.1f} GB/s), upload+validate {t_fin:.1f}, graph {t_g:.1f}, finish {t_finish:.1f}, total call {t_total:.1f} ms")
+# timers around the real call path
+T = {}
+def wrap(mod, name):
+    f = getattr(mod, name)
+    def g(*a, **k):
+        torch.cuda.synchronize(); t0 = time.perf_counter(); r = f(*a, **k); torch.cuda.synchronize()
+        T[name] = T.get(name, 0) + (time.perf_counter() - t0) * 1e3
+        return r
+    setattr(mod, name, g)
+for nm in ("_graph_cache_key", "_upload_into", "_finish"):
+    wrap(rsvd, nm)
+GR = rsvd.GraphedFactorization.run
+def grun(self, *a, **k):
+    torch.cuda.synchronize(); t0 = time.perf_counter(); r = GR(self, *a, **k); torch.cuda.synchronize()
+    T["graph.run"] = T.get("graph.run", 0) + (time.perf_counter() - t0) * 1e3
+    return r
+rsvd.GraphedFactorization.run = grun
+torch.cuda.synchronize(); t0 = time.perf_counter()
+rk.block_krylov(Ah, cfg)
+torch.cuda.synchronize()
+print("call", (time.perf_counter() - t0) * 1e3, {k: round(v, 1) for k, v in T.items()})
