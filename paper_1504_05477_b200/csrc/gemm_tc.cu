@@ -177,6 +177,8 @@ struct TcParams {
     double alpha, beta;
     const double* row_sub;
     float* ws;
+    int64_t ldw;            // row pitch of the partials (multiple of 4 floats)
+    int plain_vec;          // direct, alpha = 1, beta = 0, no row_sub, C rows 16-byte aligned
     const int32_t* pred;
 };
 
@@ -235,7 +237,22 @@ __device__ __forceinline__ void drain_epilogue(const TcParams& p, uint32_t tmem_
         if (lane == 0) mbar_arrive(&acc_empty[set]);
     }
     if (warp % 4 == 3 && lane == 0) TC_TRACE(2, 511);
-    if (row < p.M) {
+    // 16-byte stores where the layout allows: partials (padded pitch) and the
+    // plain direct case; each lane owns one output row
+    if (row < p.M && (!p.direct || p.plain_vec)) {
+        float* out = p.direct ? p.C + row * p.ldc + n0 : p.ws + ((int64_t)blockIdx.z * p.M + row) * p.ldw + n0;
+        const int ncols = (int)min((int64_t)BN, p.N - n0);
+#pragma unroll
+        for (int i = 0; i < BN; i += 4) {
+            if (i + 4 <= ncols) {
+                *reinterpret_cast<float4*>(out + i) = make_float4(sum[i], sum[i + 1], sum[i + 2], sum[i + 3]);
+            } else {
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (i + t < ncols) out[i + t] = sum[i + t];
+            }
+        }
+    } else if (row < p.M) {
 #pragma unroll
         for (int i = 0; i < BN; ++i) {
             const int64_t col = n0 + i;
@@ -246,8 +263,6 @@ __device__ __forceinline__ void drain_epilogue(const TcParams& p, uint32_t tmem_
                     r *= p.alpha;
                     if (p.beta != 0.0) r += p.beta * (double)p.C[row * p.ldc + col];
                     p.C[row * p.ldc + col] = (float)r;
-                } else {
-                    p.ws[((int64_t)blockIdx.z * p.M + row) * p.N + col] = sum[i];
                 }
             }
         }
@@ -704,7 +719,7 @@ __global__ void k_split_b(int64_t K, int64_t N, const float* __restrict__ B, int
 }
 
 template <typename TO>
-__global__ void k_tc_reduce(int64_t M, int64_t N, int64_t splits, const float* __restrict__ ws, double alpha,
+__global__ void k_tc_reduce(int64_t M, int64_t N, int64_t ldw, int64_t splits, const float* __restrict__ ws, double alpha,
                             double beta, TO* __restrict__ C, int64_t ldc, const double* __restrict__ mu,
                             const double* __restrict__ cs, const int32_t* __restrict__ pred) {
     if (pred_off(pred)) return;
@@ -712,7 +727,7 @@ __global__ void k_tc_reduce(int64_t M, int64_t N, int64_t splits, const float* _
     if (e >= M * N) return;
     int64_t r = e / N, c = e % N;
     double v = 0.0;
-    for (int64_t s = 0; s < splits; ++s) v += (double)ws[s * M * N + e];
+    for (int64_t s = 0; s < splits; ++s) v += (double)ws[(s * M + r) * ldw + c];
     if (mu) v -= mu[r] * cs[c];
     v *= alpha;
     if (beta != 0.0) v += beta * (double)C[r * ldc + c];
@@ -871,6 +886,7 @@ int gemm_nn_tc(int64_t m, int64_t n, int64_t k, double alpha, const float* A, in
     TcParams p{};
     p.M = m; p.N = n; p.K = k; p.k_per_split = Kp; p.Kp = Kp; p.Np = Np;
     p.direct = 1; p.C = C; p.ldc = ldc; p.alpha = alpha; p.beta = beta; p.row_sub = row_sub; p.ws = nullptr;
+    p.plain_vec = alpha == 1.0 && beta == 0.0 && row_sub == nullptr && ldc % 4 == 0 && aligned16(C);
     p.pred = pred;
     dim3 grid((unsigned)cdiv(m, BM), (unsigned)cdiv(n, bn), 1);
     return dispatch_bn<false>(bn, tA, tB, p, grid, st);
@@ -885,7 +901,7 @@ bool gemm_tc_tn_supported(int64_t m, int64_t n, int64_t k, int64_t lda, int64_t 
 
 int64_t gemm_tn_tc_ws_bytes(int64_t m, int64_t n, int64_t k) {
     int64_t s = tn_splits_tc(k, n, m);
-    return s * k * n * 4 + 256;
+    return s * k * cdiv(n, 4) * 4 * 4 + 256;  // partial rows padded to 16 bytes
 }
 
 int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t lda,
@@ -895,7 +911,8 @@ int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, con
     const int64_t Mop = k, Nop = n, Kop = m;
     int bn = pick_bn(Nop);
     const int64_t S = tn_splits_tc(Mop, Nop, Kop);
-    RSVD_REQUIRE(ws_bytes >= S * Mop * Nop * 4, "gemm_tn_tc: workspace too small");
+    RSVD_REQUIRE(ws_bytes >= S * Mop * cdiv(Nop, 4) * 4 * 4, "gemm_tn_tc: workspace too small");
+    RSVD_REQUIRE(aligned16(ws), "gemm_tn_tc: workspace must be 16-byte aligned");
     const int64_t Kp = cdiv(Kop, BK) * BK, Np = cdiv(Nop, bn) * bn;
     static thread_local Scratch sc;
     size_t need = (size_t)(2 * Kp * Np * 4);
@@ -917,15 +934,16 @@ int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, con
     p.k_per_split = cdiv(cdiv(Kop, S), BK) * BK;
     p.Kp = Kp;
     p.direct = 0; p.ws = (float*)ws; p.pred = pred;
+    p.ldw = cdiv(Nop, 4) * 4;
     dim3 grid((unsigned)cdiv(Mop, BM), (unsigned)cdiv(Nop, bn), (unsigned)S);
     rc = dispatch_bn<true>(bn, tA, tB, p, grid, st);
     if (rc) return rc;
     int64_t tot = Mop * Nop;
     if (out_dtype == RSVD_F64)
-        k_tc_reduce<double><<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(Mop, Nop, S, (const float*)ws, alpha, beta,
+        k_tc_reduce<double><<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(Mop, Nop, p.ldw, S, (const float*)ws, alpha, beta,
                                                                        (double*)C, ldc, mu, cs, pred);
     else
-        k_tc_reduce<float><<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(Mop, Nop, S, (const float*)ws, alpha, beta,
+        k_tc_reduce<float><<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(Mop, Nop, p.ldw, S, (const float*)ws, alpha, beta,
                                                                       (float*)C, ldc, mu, cs, pred);
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
