@@ -426,7 +426,9 @@ def run_ours(args):
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "peak_source": peak_src, "traffic": None if sparse else _profiled_traffic(),
                      "algorithmic_bytes_per_launch": bytes_per, "avg_launch_ms": avg_chain_ms},
-        "kernels": {"rayleigh_ritz_ATQ_ms": rr_ms, "rayleigh_ritz_ATQ_tflops": rr_tflops},
+        "kernels": ({"rayleigh_ritz_ATQ_ms": rr_ms, "rayleigh_ritz_ATQ_tflops": rr_tflops} if rr else
+                    {"rayleigh_ritz_W": "assembled from the chain's A^T q_j (projected FP32 basis); "
+                                        "no separate width-w pass over A"}),
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "sigma_head": [float(x) for x in sigma[:3]],

@@ -267,10 +267,11 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
 
 
 class BasisResult:
-    def __init__(self, Q, q_used, deflated):
+    def __init__(self, Q, q_used, deflated, W=None):
         self.Q = Q
         self.q_used = q_used
         self.deflated = deflated  # device int32 tensor: columns replaced in the final orth
+        self.W = W  # A^T Q when the construction produced it (projected BK), else None
 
 
 def sketch_basis(ops, comm, op, Pi, ws, n_total, row_offset):
@@ -326,19 +327,28 @@ def bk_basis(ops, comm, op, Pi, q, ws, n_total, row_offset):
         return BasisResult(K, 0, torch.zeros(1, dtype=torch.int32, device=dev))
     deflated = torch.zeros(1, dtype=torch.int32, device=dev)
     if projected:
-        # one fill stream across the blocks, as one _mgs of the hstack
+        # One fill stream across the blocks, as one _mgs of the hstack. The
+        # chain's A^T q_{j-1} are the columns of W = A^T Q that Rayleigh-Ritz
+        # needs (q_{j-1} is final when they are formed), so they are written
+        # into W and only A^T q_last is added at the end: one width-p pass
+        # over A instead of a width-w one.
+        W = rows_buffer(d, n_blocks * p, dt, dev)
         for j in range(1, n_blocks):
             prev = K[:, (j - 1) * p: j * p]
             cur = K[:, j * p: (j + 1) * p]
-            op.apply_t(prev, C)
-            comm.allreduce(C)
-            op.apply(C, cur)
+            Cj = W[:, (j - 1) * p: j * p]
+            op.apply_t(prev, Cj)
+            comm.allreduce(Cj)
+            op.apply(Cj, cur)
             ref2 = ws.ref2[:p]
             ops.colreduce(cur, True, ref2)
             comm.allreduce(ref2)
             orth_block(ops, comm, cur, tmp, ws, Qp=K[:, : j * p], ref2=ref2, running=running,
                        n_total=n_total, row_offset=row_offset, deflation_count=deflated)
-        return BasisResult(K, n_blocks - 1, deflated)
+        last = W[:, (n_blocks - 1) * p:]
+        op.apply_t(K[:, (n_blocks - 1) * p:], last)
+        comm.allreduce(last)
+        return BasisResult(K, n_blocks - 1, deflated, W=W)
     for j in range(1, n_blocks):
         prev = K[:, (j - 1) * p: j * p]
         cur = K[:, j * p: (j + 1) * p]
@@ -397,8 +407,9 @@ class RitzResult:
         self.zerr = zerr  # FP64 [1]: max |Z^T Z - I| (rsvd.py:182-185)
 
 
-def rayleigh_ritz(ops, comm, op, Q, k, n_total, row_offset, sign_fn=None):
-    """rsvd.py:200-221 with M = W^T W, W = A^T Q (one pass over A)."""
+def rayleigh_ritz(ops, comm, op, Q, k, n_total, row_offset, sign_fn=None, W=None):
+    """rsvd.py:200-221 with M = W^T W, W = A^T Q (one pass over A; none when
+    the basis construction already produced W)."""
     dev = op.device
     w = Q.shape[1]
     d = op.shape[1]
@@ -406,10 +417,11 @@ def rayleigh_ritz(ops, comm, op, Q, k, n_total, row_offset, sign_fn=None):
     # FP32-accurate on the FP32 path (3xTF32 / FP32 SpMM), where it is stored in
     # FP32 and M = W^T W runs on the tensor cores with FP64 output (the FP64
     # CUDA-core Gram of an FP64 copy took 38 ms at C3, w = 1600)
-    wdt = torch.float64 if Q.dtype == torch.float64 else Q.dtype
-    W = rows_buffer(d, w, wdt, dev)
-    op.apply_t(Q, W)
-    comm.allreduce(W)
+    if W is None:
+        wdt = torch.float64 if Q.dtype == torch.float64 else Q.dtype
+        W = rows_buffer(d, w, wdt, dev)
+        op.apply_t(Q, W)
+        comm.allreduce(W)
     M = torch.empty((w, w), dtype=torch.float64, device=dev)
     ops.gram(W, M)
     # top-k eigenpairs only (rsvd.py:217-220 uses eigvecs[:, :k], eigvals[:k])

@@ -323,11 +323,12 @@ def run_device(op, cfg, comm=None, Pi=None):
         q_used = q
     elif cfg.variant is Variant.BLOCK_KRYLOV:
         br = krylov.bk_basis(ops, c, op, pi_dev, q, ws, n_total, row_offset)
-        Q, q_used, deflated = br.Q, br.q_used, br.deflated
+        Q, q_used, deflated, W = br.Q, br.q_used, br.deflated, br.W
     else:
         Q = krylov.sketch_basis(ops, c, op, pi_dev, ws, n_total, row_offset)
         q_used = 0
-    rr = krylov.rayleigh_ritz(ops, c, op, Q, cfg.k, n_total, row_offset, sign_fn=_sign_fn_for(comm))
+    rr = krylov.rayleigh_ritz(ops, c, op, Q, cfg.k, n_total, row_offset, sign_fn=_sign_fn_for(comm),
+                              W=W if cfg.variant is Variant.BLOCK_KRYLOV else None)
     return DeviceFactorization(rr.Z, rr.sigma, rr.info, rr.off, rr.zerr, q_used, deflated)
 
 
