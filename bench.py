@@ -48,6 +48,9 @@ CONFIGS = {
     "c1": dict(n=2000, d=1000, k=20, q=8, spectrum="inv", noise=0.0, variant="bk"),
     "c4": dict(n=1000000, d=4096, k=200, q=6, spectrum="clustered", noise=0.0, variant="bk"),
     "c3": dict(n=200000, d=100000, k=100, q=15, sparse=True, variant="bk"),
+    # C5: PCA with implicit mean-centering (rank-1 GEMM-epilogue corrections)
+    "c5": dict(n=500000, d=2000, k=200, q=4, pca=True, variant="bk"),
+    "c5si": dict(n=500000, d=2000, k=200, q=12, pca=True, variant="si"),
 }
 
 
@@ -115,8 +118,14 @@ def workload_config(name, cfgd, cfg, world, nnz=None):
     n, d, k = cfgd["n"], cfgd["d"], cfgd["k"]
     w = cfg.p * (cfg.resolve_q(d) + 1)
     sparse = bool(cfgd.get("sparse"))
-    return {"workload": (f"{name.upper()}: " + (f"CSR FP32 A {n}x{d} nnz {nnz}" if sparse else f"dense FP32 A {n}x{d}")
-                         + f", BK k={k} q={cfgd['q']}->{cfg.resolve_q(d)}, width {w}"),
+    si = cfgd["variant"] == "si"
+    if si:
+        w = cfg.p
+    label = "SI" if si else "BK"
+    what = (f"CSR FP32 A {n}x{d} nnz {nnz}" if sparse else
+            f"PCA (implicit centering) on dense FP32 A {n}x{d}" if cfgd.get("pca") else f"dense FP32 A {n}x{d}")
+    return {"workload": (f"{name.upper()}: " + what
+                         + f", {label} k={k} q={cfgd['q']}->{cfg.resolve_q(d)}, width {w}"),
             "n": n, "d": d, "k": k, "q": cfgd["q"], "q_eff": cfg.resolve_q(d), "krylov_width": w,
             "parallelism": f"rowshard{world}",
             "l2": ("CSR %.0f MB + blocks; dense rows L2-resident by design (gather-bound)" % (nnz * 8 / 1e6)
@@ -161,11 +170,13 @@ def spmm_probe(dev, reps=5):
     return res
 
 
-def _profiled_traffic():
+def _profiled_traffic(config="c2"):
     """DRAM bytes per launch of the chain kernel from the committed ncu --set
-    full capture (profiles/r01_chain_kernel_ncu.json: dram__bytes_read.sum +
-    dram__bytes_write.sum), or None when no capture is committed."""
-    path = os.path.join(ROOT, "profiles", "r01_chain_kernel_ncu.json")
+    full capture (profiles/r01_chain_kernel_ncu.json for C2,
+    profiles/r01_<config>_chain_kernel_ncu.json otherwise: dram__bytes_read.sum
+    + dram__bytes_write.sum), or None when no capture is committed."""
+    name = "r01_chain_kernel_ncu.json" if config == "c2" else f"r01_{config}_chain_kernel_ncu.json"
+    path = os.path.join(ROOT, "profiles", name)
     try:
         with open(path) as f:
             return float(json.load(f)["dram_bytes_per_launch"])
@@ -173,11 +184,38 @@ def _profiled_traffic():
         return None
 
 
+def make_pca_matrix(cfg, device, seed=777):
+    """C5: rows x_r = mu + W diag(sqrt(lambda)) g_r, g_r ~ N(0, I),
+    mu_j ~ U(-5, 5), Haar W (QR of a seeded Gaussian, sign-fixed), lambda_i =
+    exp(-i/50); built in FP64 on the GPU in row chunks, FP32 out."""
+    import torch
+
+    n, d = cfg["n"], cfg["d"]
+    g = torch.Generator(device=device).manual_seed(seed)
+    W = torch.randn((d, d), generator=g, dtype=torch.float64, device=device)
+    W, R = torch.linalg.qr(W)
+    W *= torch.sign(torch.diagonal(R)).view(1, -1)
+    lam = torch.exp(-torch.arange(1, d + 1, dtype=torch.float64, device=device) / 50.0)
+    mu = torch.rand(d, generator=g, dtype=torch.float64, device=device) * 10.0 - 5.0
+    M = (W * lam.sqrt().view(1, -1)).T.contiguous()  # diag(sqrt lambda) W^T
+    A = torch.empty((n, d), dtype=torch.float32, device=device)
+    chunk = 65536
+    for r0 in range(0, n, chunk):
+        r1 = min(n, r0 + chunk)
+        G = torch.randn((r1 - r0, d), generator=g, dtype=torch.float64, device=device)
+        A[r0:r1] = (G @ M + mu.view(1, -1)).float()
+    del W, M, G
+    torch.cuda.synchronize()
+    return A
+
+
 def make_matrix(cfg, device, seed=1234):
     """Haar U (n x d), V (d x d) from seeded Gaussians (QR, sign-fixed by
     diag R), A = U diag(s) V^T (+ noise), built in FP64 on the GPU, FP32 out."""
     import torch
 
+    if cfg.get("pca"):
+        return make_pca_matrix(cfg, device)
     n, d = cfg["n"], cfg["d"]
     g = torch.Generator(device=device).manual_seed(seed)
     s = torch.from_numpy(_spectrum(cfg["spectrum"], d)).to(device)
@@ -301,7 +339,7 @@ def run_ours(args):
             del A_full
         else:
             A = A_full
-        op = DenseDeviceOp(A, n_total=n, row_offset=lo)
+        op = DenseDeviceOp(A, n_total=n, row_offset=lo, center=bool(cfgd.get("pca")), comm=comm)
     Pi = rk.gaussian(d, cfg.p, rk.SeededRng(cfg.seed)).data
 
     # instrumentation of the dominant kernels (A X / A^T Y on the op's stream)
@@ -390,16 +428,37 @@ def run_ours(args):
     w = (cfgd["q"] + 1 + (cfgd["q"] % 2 == 0)) * cfg.p
     rr_tflops = 2.0 * n_loc * d * w / (rr_ms * 1e-3) / 1e12 if (rr and not sparse) else None
 
+    # the chain product's bound: HBM below the 3xTF32 ridge (C2: 25 flop/B),
+    # tensor pipe above it (C4 / C5 at width 200: ~95 flop/B)
+    flops_per = 2.0 * n_loc * d * cfg.p
+    tf_eff = bf16 / 6.0  # TF32 issues at half the bf16 rate; 3xTF32 = 3 MMAs per product
+    kname = ("CSR SpMM A.X / A^T.Y (width %d)" if sparse else "Krylov-chain A.X / A^T.Y (width %d)") % cfg.p
+    traffic = None if sparse else _profiled_traffic(args.config)
+    if sparse or flops_per / bytes_per * hbm / 1e3 < tf_eff:
+        roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved / hbm, "peak_source": peak_src, "traffic": traffic,
+                    "algorithmic_bytes_per_launch": bytes_per, "avg_launch_ms": avg_chain_ms}
+    else:
+        tfl = flops_per / (avg_chain_ms * 1e-3) / 1e12
+        roofline = {"bound": "tensor", "kernel": kname, "achieved": tfl, "peak": tf_eff, "unit": "TFLOP/s",
+                    "frac": tfl / tf_eff,
+                    "peak_source": f"{peak_src} bf16 dense {bf16:.0f} TFLOP/s / 6 (TF32 at half the bf16 rate, "
+                                   "3 TF32 MMAs per 3xTF32 product)",
+                    "traffic": traffic, "algorithmic_flops_per_launch": flops_per,
+                    "algorithmic_bytes_per_launch": bytes_per, "avg_launch_ms": avg_chain_ms,
+                    "hbm_frac": achieved / hbm}
+
     # e2e through the public API with host (pinned) A
     e2e = None
     if world == 1 and not args.no_e2e and not sparse:
         A_host = A.cpu().pin_memory()
+        center = bool(cfgd.get("pca"))
         for _ in range(max(1, min(args.warmup, 2))):
-            r = rk.block_krylov(A_host, cfg)
+            r = rk.factorize(A_host, cfg, center=center)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            r = rk.block_krylov(A_host, cfg)
+            r = rk.factorize(A_host, cfg, center=center)
         torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
         e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": int(A_host.numel() * 4 + Pi.size * 4),
@@ -421,11 +480,7 @@ def run_ours(args):
                   "f32 (3xTF32 products, f64 small algebra)" if A.dtype == torch.float32 else "f64"),
         "data": "synthetic",
         "config": workload_config(args.config, cfgd, cfg, world, nnz_local if sparse else None),
-        "roofline": {"bound": "hbm", "kernel": ("CSR SpMM A.X / A^T.Y (width %d)" if sparse else
-                                               "Krylov-chain A.X / A^T.Y (width %d)") % cfg.p,
-                     "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "peak_source": peak_src, "traffic": None if sparse else _profiled_traffic(),
-                     "algorithmic_bytes_per_launch": bytes_per, "avg_launch_ms": avg_chain_ms},
+        "roofline": roofline,
         "kernels": ({"rayleigh_ritz_ATQ_ms": rr_ms, "rayleigh_ritz_ATQ_tflops": rr_tflops} if rr else
                     {"rayleigh_ritz_W": "assembled from the chain's A^T q_j (projected FP32 basis); "
                                         "no separate width-w pass over A"}),
@@ -489,6 +544,8 @@ def cpu_baseline(A_dev, cfgd, cfg, Pi, args, df=None):
 
         sig = df.sigma.double().cpu().numpy()
         A64 = A_dev.double()
+        if cfgd.get("pca"):
+            A64 -= A64.mean(0, keepdim=True)
         cap = (A64.T @ df.Z.double()).pow(2).sum(0).cpu().numpy()
         cap_ref = (A64.T @ torch.from_numpy(np.ascontiguousarray(r.Z)).to(A64.device)).pow(2).sum(0).cpu().numpy()
         del A64
@@ -496,7 +553,43 @@ def cpu_baseline(A_dev, cfgd, cfg, Pi, args, df=None):
                          "sigma_rel_median": float(np.median(np.abs(sig - r.sigma) / r.sigma)),
                          "captured_variance_rel_max": float(np.max(np.abs(cap - cap_ref) / cap_ref)),
                          "tolerance": 1e-4 if A_dev.dtype == torch.float32 else 1e-10}
+        if A_dev.dtype == torch.float32 and not args.no_fp64:
+            res["parity_fp64_mode"] = fp64_mode_leg(A_dev, cfgd, cfg, Pi, r)
     return res
+
+
+def fp64_mode_leg(A_dev, cfgd, cfg, Pi, r):
+    """The FP64 path (precision="fp64": A upcast on the device as the
+    reference upcasts FP32 input, matrix.py:80; FP64 products and the
+    reference-faithful power-block basis) on the same A and Pi: its time and
+    its parity against the same reference result. This is the mode for
+    reference-exact results; the headline FP32 path trades the reference's
+    own FP64 rounding pattern in the unconverged tail for 3xTF32 speed."""
+    import torch
+
+    from paper_1504_05477_b200 import rsvd
+    from paper_1504_05477_b200.operators import DenseDeviceOp
+
+    A64 = A_dev.double()
+    op = DenseDeviceOp(A64, center=bool(cfgd.get("pca")))
+    g = rsvd.GraphedFactorization(op, cfg)
+    g.run(Pi)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    df = g.run(Pi)
+    e1.record()
+    torch.cuda.synchronize()
+    sig = df.sigma.cpu().numpy()
+    if cfgd.get("pca"):
+        A64 -= A64.mean(0, keepdim=True)
+    cap = (A64.T @ df.Z.double()).pow(2).sum(0).cpu().numpy()
+    cap_ref = (A64.T @ torch.from_numpy(np.ascontiguousarray(r.Z)).to(A64.device)).pow(2).sum(0).cpu().numpy()
+    del A64, op, g
+    torch.cuda.empty_cache()
+    return {"ms": e0.elapsed_time(e1), "sigma_rel_max": float(np.max(np.abs(sig - r.sigma) / r.sigma)),
+            "captured_variance_rel_max": float(np.max(np.abs(cap - cap_ref) / cap_ref)),
+            "tolerance": 1e-4, "dtype": "f64 (A upcast on the device, FP64 products)"}
 
 
 def reference_sample(A32, cfgd, cfg, Pi, budget_s=25.0, return_result=False):
@@ -511,6 +604,8 @@ def reference_sample(A32, cfgd, cfg, Pi, budget_s=25.0, return_result=False):
 
     cores = os.cpu_count() or 1
     A = np.ascontiguousarray(A32, dtype=np.float64)
+    if cfgd.get("pca"):  # no reference function: the reference on explicitly centered A
+        A -= A.mean(axis=0, keepdims=True)
     op = o.DenseOp(A)
     op.apply(Pi[:, :1])  # BLAS thread-pool warm-up outside the timer
     variant = cfg.variant.value if hasattr(cfg.variant, "value") else str(cfg.variant)
@@ -572,6 +667,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-fp64", action="store_true", help="skip the FP64 parity-mode leg on FP32 configs")
     ap.add_argument("--no-spmm", action="store_true", help="skip the C3 SpMM measurement on dense configs")
     ap.add_argument("--count-launches", action="store_true", default=True)
     ap.add_argument("--cpu-budget", type=float, default=25.0)

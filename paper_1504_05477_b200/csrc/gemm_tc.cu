@@ -180,6 +180,7 @@ struct TcParams {
     int64_t ldw;            // row pitch of the partials (multiple of 4 floats)
     int plain_vec;          // direct, alpha = 1, beta = 0, no row_sub, C rows 16-byte aligned
     const int32_t* pred;
+    int n_tiles;            // N tiles per M tile (blockIdx.x = m_tile * n_tiles + n_tile)
 };
 
 // Profiling ablations (tools/ablate_tc.py builds variants; 0 in the product):
@@ -196,7 +197,7 @@ constexpr int kTraceKb = 512, kTraceCta2 = 200;
 __device__ long long g_tc_trace[2][8][kTraceKb];
 #define TC_TRACE(series, kb)                                                                      \
     do {                                                                                          \
-        if ((blockIdx.x == 0 || blockIdx.x == kTraceCta2) && blockIdx.y == 0 && blockIdx.z == 0 && \
+        if ((blockIdx.x == 0 || blockIdx.x == kTraceCta2) && blockIdx.z == 0 && \
             (kb) < kTraceKb)                                                                       \
             g_tc_trace[blockIdx.x == 0 ? 0 : 1][series][kb] = clock64();                          \
     } while (0)
@@ -209,7 +210,7 @@ __device__ long long g_tc_trace[2][8][kTraceKb];
 // Accumulator drain + epilogue, shared by both kernels. TMEM lane quarter
 // q = warp % 4 holds tile rows 32q..32q+31; D0 | D1 (2 BN columns) of each
 // finished chunk are summed into round-to-nearest FP32 registers.
-template <int BN>
+template <int BN, bool MERGED = true>
 __device__ __forceinline__ void drain_epilogue(const TcParams& p, uint32_t tmem_base, int warp, int lane, int nkb,
                                                int64_t m0, int64_t n0, uint64_t* acc_full, uint64_t* acc_empty) {
     const int quarter = warp % 4;
@@ -223,14 +224,20 @@ __device__ __forceinline__ void drain_epilogue(const TcParams& p, uint32_t tmem_
         const int set = c & 1;
         mbar_wait(&acc_full[set], (c >> 1) & 1);
         tc_fence_after();
-        const uint32_t base = tmem_base + lane_off + set * 2 * BN;
+        const uint32_t base = tmem_base + lane_off + set * (MERGED ? 2 : 1) * BN;
 #pragma unroll
         for (int j = 0; j < ((RSVD_TC_ABLATE & 4) ? 0 : BN); j += 8) {
-            float v0[8], v1[8];
+            float v0[8];
             tmem_ld8(base + j, v0);
-            tmem_ld8(base + BN + j, v1);
+            if constexpr (MERGED) {
+                float v1[8];
+                tmem_ld8(base + BN + j, v1);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) sum[j + i] += v0[i] + v1[i];
+                for (int i = 0; i < 8; ++i) sum[j + i] += v0[i] + v1[i];
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) sum[j + i] += v0[i];
+            }
         }
         tc_fence_before();
         __syncwarp();
@@ -293,14 +300,19 @@ constexpr int KPS = 2;  // k-blocks per T / B slot
 
 template <int BN, bool A_MN>
 struct TmCfg {
+    // BN <= 64: D0 | D1 += A_hi [B_hi | B_lo] merged into one N = 2 BN MMA.
+    // BN >= 96: 2 x 2 BN accumulator columns would leave no TMEM for A, so
+    // three N = BN MMAs accumulate into D0 alone (same tensor-pipe time).
+    static constexpr bool MERGE = BN <= 64;
     static constexpr int A_BYTES = BM * BK * 4;        // 16 KB
     static constexpr int B_BYTES = BN * BK * 4;        // one plane's tile, one k-block
     static constexpr int B_SLOT = 2 * KPS * B_BYTES;    // [hi | lo] x KPS k-blocks
-    static constexpr int ACC_COLS = 4 * BN;             // 2 sets x (D0 | D1)
+    static constexpr int ACC_COLS = (MERGE ? 4 : 2) * BN;  // 2 sets x (D0 | D1) or 2 sets x D0
     static constexpr int T_COLS = 2 * KPS * BK;         // [A_hi | A_lo] per slot
     static constexpr int T_STAGES = (512 - ACC_COLS) / T_COLS;
-    static constexpr int B_STAGES = BN >= 64 ? 3 : 4;
-    static constexpr int A_STAGES_RAW = (200 * 1024 - B_STAGES * B_SLOT) / A_BYTES;
+    static constexpr int B_STAGES = BN >= 128 ? 2 : (BN >= 64 ? 3 : 4);
+    static constexpr int SMEM_BUDGET = (BN >= 96 ? 216 : 200) * 1024;
+    static constexpr int A_STAGES_RAW = (SMEM_BUDGET - B_STAGES * B_SLOT) / A_BYTES;
     static constexpr int A_STAGES = A_STAGES_RAW > 12 ? 12 : A_STAGES_RAW;
     static constexpr int SMEM = A_STAGES * A_BYTES + B_STAGES * B_SLOT + 1024 + 512;
     static_assert(T_STAGES >= 2 && A_STAGES >= 2 * KPS, "pipeline too shallow");
@@ -330,8 +342,10 @@ k_tc_gemm_t(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int64_t m0 = (int64_t)blockIdx.x * BM;
-    const int64_t n0 = (int64_t)blockIdx.y * BN;
+    // linear tile index, N tiles of one M tile adjacent (co-resident CTAs
+    // share the A tile through L2 instead of streaming A once per N tile)
+    const int64_t m0 = (int64_t)(blockIdx.x / p.n_tiles) * BM;
+    const int64_t n0 = (int64_t)(blockIdx.x % p.n_tiles) * BN;
     const int64_t kbeg = (int64_t)blockIdx.z * p.k_per_split;
     const int64_t kend = min(p.K, kbeg + p.k_per_split);
     const int nkb = (int)((kend - kbeg + BK - 1) / BK);
@@ -420,7 +434,7 @@ k_tc_gemm_t(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             int chunk = 0;
             for (int sl = 0; sl < nslots; ++sl) {
                 const int set = chunk & 1;
-                const uint32_t d0 = tmem_base + set * 2 * BN;
+                const uint32_t d0 = tmem_base + set * (Cfg::MERGE ? 2 : 1) * BN;
                 const bool first = (sl * KPS) % KCHUNK == 0;
                 if (first) mbar_wait(&acc_empty[set], ((chunk >> 1) & 1) ^ 1);
                 TC_TRACE(4, sl);
@@ -436,7 +450,13 @@ k_tc_gemm_t(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         if (RSVD_TC_ABLATE & 2) continue;
                         const uint64_t dbk = db + j * kKbDesc + 2 * ks;
                         const uint32_t tk = ta + j * BK + ks * 8;
-                        tc_mma_tf32_ts(d0, tk, dbk, idesc2, (first && j == 0 && ks == 0) ? 0u : 1u);
+                        const uint32_t acc0 = (first && j == 0 && ks == 0) ? 0u : 1u;
+                        if constexpr (Cfg::MERGE) {
+                            tc_mma_tf32_ts(d0, tk, dbk, idesc2, acc0);  // D0 | D1 += A_hi [B_hi | B_lo]
+                        } else {
+                            tc_mma_tf32_ts(d0, tk, dbk, idesc1, acc0);                           // A_hi B_hi
+                            tc_mma_tf32_ts(d0, tk, dbk + (Cfg::B_BYTES >> 4), idesc1, 1u);      // A_hi B_lo
+                        }
                         if (RSVD_TC_ABLATE & 8) continue;
                         tc_mma_tf32_ts(d0, tk + KPS * BK, dbk, idesc1, 1u);  // D0 += A_lo B_hi
                     }
@@ -514,7 +534,7 @@ k_tc_gemm_t(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             if (++st == ST) { st = 0; pht ^= 1; }
         }
     } else {
-        drain_epilogue<BN>(p, tmem_base, warp, lane, (nslots * KPS), m0, n0, acc_full, acc_empty);
+        drain_epilogue<BN, Cfg::MERGE>(p, tmem_base, warp, lane, (nslots * KPS), m0, n0, acc_full, acc_empty);
         if (warp == kTWarpDrain0 && lane == 0) TC_TRACE(3, 511);
     }
     tc_fence_before();
@@ -560,8 +580,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int64_t m0 = (int64_t)blockIdx.x * BM;
-    const int64_t n0 = (int64_t)blockIdx.y * BN;
+    const int64_t m0 = (int64_t)(blockIdx.x / p.n_tiles) * BM;
+    const int64_t n0 = (int64_t)(blockIdx.x % p.n_tiles) * BN;
     const int64_t kbeg = (int64_t)blockIdx.z * p.k_per_split;
     const int64_t kend = min(p.K, kbeg + p.k_per_split);
     const int nkb = (int)((kend - kbeg + BK - 1) / BK);
@@ -783,7 +803,8 @@ int pick_bn(int64_t n) {
 template <int BN, bool A_MN>
 int launch_tc(const CUtensorMap& tA, const CUtensorMap& tB, const TcParams& p, dim3 grid, cudaStream_t st) {
     static bool attr_set = false;
-    if constexpr (BN <= 64) {
+    static const bool legacy = getenv("RSVD_TC_LEGACY") != nullptr;  // A/B comparison: smem-A kernel for BN >= 96
+    if (BN <= 64 || !legacy) {
         using Cfg = TmCfg<BN, A_MN>;
         if (!attr_set) {
             RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_tc_gemm_t<BN, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -888,7 +909,8 @@ int gemm_nn_tc(int64_t m, int64_t n, int64_t k, double alpha, const float* A, in
     p.direct = 1; p.C = C; p.ldc = ldc; p.alpha = alpha; p.beta = beta; p.row_sub = row_sub; p.ws = nullptr;
     p.plain_vec = alpha == 1.0 && beta == 0.0 && row_sub == nullptr && ldc % 4 == 0 && aligned16(C);
     p.pred = pred;
-    dim3 grid((unsigned)cdiv(m, BM), (unsigned)cdiv(n, bn), 1);
+    p.n_tiles = (int)cdiv(n, bn);
+    dim3 grid((unsigned)(cdiv(m, BM) * p.n_tiles), 1, 1);
     return dispatch_bn<false>(bn, tA, tB, p, grid, st);
 }
 
@@ -935,7 +957,8 @@ int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, con
     p.Kp = Kp;
     p.direct = 0; p.ws = (float*)ws; p.pred = pred;
     p.ldw = cdiv(Nop, 4) * 4;
-    dim3 grid((unsigned)cdiv(Mop, BM), (unsigned)cdiv(Nop, bn), (unsigned)S);
+    p.n_tiles = (int)cdiv(Nop, bn);
+    dim3 grid((unsigned)(cdiv(Mop, BM) * p.n_tiles), 1, (unsigned)S);
     rc = dispatch_bn<true>(bn, tA, tB, p, grid, st);
     if (rc) return rc;
     int64_t tot = Mop * Nop;

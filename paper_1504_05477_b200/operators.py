@@ -38,6 +38,12 @@ class DenseDeviceOp:
             self.mu = mu / float(self.n_total)
             self._mu_col = self.mu.view(-1, 1)
 
+    def set_column_sums(self, sums):
+        """Re-derive mu in place from the (all-rank) column sums of a freshly
+        uploaded A (the persistent buffer of a cached graph keeps its mu
+        tensor, so a captured factorization sees the new mean)."""
+        torch.div(sums, float(self.n_total), out=self.mu)
+
     @property
     def is_sparse(self):
         return False

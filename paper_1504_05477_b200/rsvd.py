@@ -161,10 +161,10 @@ class RsvdConfig:
         return derive_q(self.variant, d, self.epsilon, self.C)
 
 
-def _wrap_dense(arr):
+def _wrap_dense(arr, finite_checked=False):
     """DenseMatrix around a freshly produced float64 array without a second copy."""
     arr = np.ascontiguousarray(arr, dtype=np.float64)
-    if not np.all(np.isfinite(arr)):
+    if not finite_checked and not np.all(np.isfinite(arr)):
         raise ValueError("dense matrix entries must be finite")
     arr.setflags(write=False)
     obj = object.__new__(DenseMatrix)
@@ -370,6 +370,19 @@ class GraphedFactorization:
         return self.out
 
 
+def _to_host(Z):
+    """D2H of the result through page-locked memory: a DMA at full link
+    speed instead of a staged copy into freshly faulted pageable pages. The
+    returned array owns its buffer (torch's caching host allocator recycles
+    the block once the caller drops the result)."""
+    if not Z.is_cuda:
+        return Z.numpy()
+    h = torch.empty(Z.shape, dtype=Z.dtype, pin_memory=True)
+    h.copy_(Z, non_blocking=True)
+    torch.cuda.current_stream(Z.device).synchronize()
+    return h.numpy()
+
+
 def _finish(df, cfg, t0, gather_z=None):
     info = df.info.cpu()
     off = float(df.off.cpu()[0])
@@ -379,12 +392,20 @@ def _finish(df, cfg, t0, gather_z=None):
             residual=off,
         )
     Z = df.Z if gather_z is None else gather_z(df.Z)
-    z_host = Z.cpu().numpy()
+    finite = False
+    if Z.is_cuda and Z.numel():
+        # DenseMatrix's finiteness rule (matrix.py:80-85) checked on the device:
+        # |z| <= 1 for orthonormal columns, so a column sum is finite iff
+        # every entry of the column is
+        finite = bool(torch.isfinite(ops.colreduce(Z, square=False)).all())
+        if not finite:
+            raise ValueError("dense matrix entries must be finite")
+    z_host = _to_host(Z)
     sigma = df.sigma.cpu().numpy()
     zerr = float(df.zerr.cpu()[0])
     elapsed_ms = (time.perf_counter() - t0) * 1e3
     return PartialSvdResult(
-        Z=_wrap_dense(z_host),
+        Z=_wrap_dense(z_host, finite_checked=finite),
         approx_singular_values=sigma,
         q_used=df.q_used,
         wall_time_ms=elapsed_ms,
@@ -405,7 +426,7 @@ _GRAPH_CACHE = OrderedDict()
 _GRAPH_CACHE_SIZE = 1
 
 
-def _graph_cache_key(A, cfg, precision, device):
+def _graph_cache_key(A, cfg, precision, device, center=False):
     if os.environ.get("RSVD_GRAPH_CACHE", "1") != "1":
         return None
     if isinstance(A, torch.Tensor):
@@ -423,7 +444,8 @@ def _graph_cache_key(A, cfg, precision, device):
         return None
     dt = _work_dtype(src, precision)
     q = cfg.resolve_q(shape[1])
-    return (shape, dt, str(dev), cfg.k, cfg.p, q, cfg.variant, int(cfg.seed), cfg.reorthonormalize_every)
+    return (shape, dt, str(dev), cfg.k, cfg.p, q, cfg.variant, int(cfg.seed), cfg.reorthonormalize_every,
+            bool(center))
 
 
 def _upload_into(buf, A):
@@ -445,14 +467,15 @@ def _upload_into(buf, A):
     ops.colreduce(buf, False, sums)
     if not bool(torch.isfinite(sums).all()):
         raise ValueError("dense matrix entries must be finite")
+    return sums
 
 
 def _run(A, cfg, expected, precision="auto", center=False, device=None, comm=None):
     if cfg.variant is not expected:
         raise ValueError(f"config variant is {cfg.variant.value}, not {expected.value}")
     key = None
-    if not center and (comm is None or getattr(comm, "world", 1) == 1):
-        key = _graph_cache_key(A, cfg, precision, device)
+    if comm is None or getattr(comm, "world", 1) == 1:
+        key = _graph_cache_key(A, cfg, precision, device, center)
     if key is not None:
         shape, dt, dev = key[0], key[1], torch.device(key[2])
         if shape[0] == 0 or shape[1] == 0 or cfg.k > min(shape):
@@ -463,7 +486,9 @@ def _run(A, cfg, expected, precision="auto", center=False, device=None, comm=Non
             while len(_GRAPH_CACHE) >= _GRAPH_CACHE_SIZE:
                 _GRAPH_CACHE.popitem(last=False)
             buf = torch.empty(shape, dtype=dt, device=dev)
-            op = DenseDeviceOp(buf)
+            if center:
+                buf.zero_()
+            op = DenseDeviceOp(buf, center=center)
             pi_host = gaussian(shape[1], cfg.p, SeededRng(cfg.seed)).data
             pi_dev = torch.from_numpy(np.array(pi_host, copy=True)).to(device=dev, dtype=dt)
             entry = [buf, op, GraphedFactorization(op, cfg), pi_dev, 0]
@@ -471,7 +496,9 @@ def _run(A, cfg, expected, precision="auto", center=False, device=None, comm=Non
         buf, op, graphed, pi, calls = entry
         entry[4] = calls + 1
         with torch.cuda.device(dev):
-            _upload_into(buf, A)
+            sums = _upload_into(buf, A)
+            if center:
+                op.set_column_sums(sums)
             t0 = time.perf_counter()
             # the first call of a shape runs eagerly; a repeated shape is
             # captured once and replayed from then on

@@ -205,6 +205,15 @@ def test_implicit_centering_matches_explicit(rk):
                         20, "bk", q=4, seed=0)
     rel = np.abs(r32.approx_singular_values - ref32.sigma) / ref32.sigma
     assert rel.max() < FP32_TOL, rel.max()
+    # repeated shape: the cached CUDA graph re-derives mu from each upload
+    # (a different matrix of the same shape must give its own centered result)
+    for X2 in (X, X + rng.uniform(-3, 3, d)):
+        X2c = X2 - X2.mean(axis=0)
+        ref2 = o.factorize(o.DenseOp(X2c), 20, "si", q=3, seed=0)
+        for _ in range(2):
+            r2 = rk.simultaneous_iteration(X2, rk.RsvdConfig(k=20, variant="si", q=3, seed=0), center=True)
+            rel = np.abs(r2.approx_singular_values - ref2.sigma) / ref2.sigma
+            assert rel.max() < 1e-9, rel.max()
 
 
 def test_sparse_fp32_and_fp64(rk):
