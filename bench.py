@@ -134,17 +134,18 @@ def workload_config(name, cfgd, cfg, world, nnz=None):
 
 def spmm_probe(dev, reps=5):
     """The SpMM half of the metric on the C3 matrix: A.X and
-    A^T.Y at width k = 100 through the load-balanced CSR kernel, CUDA-event
-    timed; GB/s are SURVEY's algorithmic bytes nnz (4 + 4) + (rows + 1) 4 +
-    (d + n) b 4 against the measured HBM copy bandwidth. The kernel is
-    gather-bound: each nonzero reads a 400-byte row of the dense block (L2)."""
+    A^T.Y at width k = 100, CUDA-event timed; GB/s are SURVEY's algorithmic
+    bytes nnz (4 + 4) + (rows + 1) 4 + (d + n) b 4 against the measured HBM
+    copy bandwidth. Two operators: the hybrid one the factorization uses
+    (Zipf-head columns as a dense tensor-core panel, the rest gathered) and
+    the pure CSR gather ("csr_only"), which is L2-gather-bound: each nonzero
+    reads a 400-byte row of the dense block."""
     import torch
     from paper_1504_05477_b200.operators import CsrDeviceOp
 
     cfgd = CONFIGS["c3"]
     n, d, p = cfgd["n"], cfgd["d"], cfgd["k"]
     indptr, colv, valv = make_csr(cfgd, dev)
-    op = CsrDeviceOp(indptr, colv, valv, d)
     g = torch.Generator(device=dev).manual_seed(5)
     X = torch.randn((d, p), generator=g, device=dev)
     Y = torch.empty((n, p), device=dev)
@@ -152,20 +153,29 @@ def spmm_probe(dev, reps=5):
     nnz = valv.numel()
     hbm, _, _ = _peaks()
     res = {"config": f"C3 CSR {n}x{d}, nnz {nnz}, width {p}", "peak_gbs": hbm}
-    for name, fn, rows in (("A.X", lambda: op.apply(X, Y), n), ("A^T.Y", lambda: op.apply_t(Y, C), d)):
-        fn()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(reps):
+    for label, dens in (("hybrid", None), ("csr_only", 0.0)):
+        op = CsrDeviceOp(indptr, colv, valv, d, hot_density=dens)
+        leg = {}
+        if op.hot is not None:
+            leg["hot_columns"] = op.hot["H"]
+            leg["hot_nnz_frac"] = op.hot["hot_nnz"] / nnz
+        for name, fn, rows in (("A.X", lambda: op.apply(X, Y), n), ("A^T.Y", lambda: op.apply_t(Y, C), d)):
             fn()
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / reps
-        byt = nnz * 8 + (rows + 1) * 4 + (n + d) * p * 4
-        res[name] = {"ms": ms, "algorithmic_gbs": byt / ms / 1e6, "frac": byt / ms / 1e6 / hbm,
-                     "gathered_gbs": (nnz * p * 4 + byt) / ms / 1e6}
-    del op, indptr, colv, valv
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            byt = nnz * 8 + (rows + 1) * 4 + (n + d) * p * 4
+            leg[name] = {"ms": ms, "algorithmic_gbs": byt / ms / 1e6, "frac": byt / ms / 1e6 / hbm}
+            if dens == 0.0:
+                leg[name]["gathered_gbs"] = (nnz * p * 4 + byt) / ms / 1e6
+        res[label] = leg
+        del op
+    del indptr, colv, valv
     torch.cuda.empty_cache()
     return res
 
@@ -365,10 +375,14 @@ def run_ours(args):
 
     graphed = rsvd.GraphedFactorization(op, cfg, comm=comm) if args.graph else None
 
+    # the start block is a function of (d, p, seed) only: uploaded once like A
+    # (the public API's graph cache keeps it on the device the same way)
+    Pi_dev = torch.from_numpy(np.array(Pi, copy=True)).to(device=dev, dtype=op.dtype)
+
     def step():
         if graphed is not None:
-            return graphed.run(Pi)
-        return rsvd.run_device(op, cfg, comm=comm, Pi=Pi)
+            return graphed.run(Pi_dev)
+        return rsvd.run_device(op, cfg, comm=comm, Pi=Pi_dev)
 
     for _ in range(args.warmup):
         df = step()
@@ -432,7 +446,9 @@ def run_ours(args):
     # tensor pipe above it (C4 / C5 at width 200: ~95 flop/B)
     flops_per = 2.0 * n_loc * d * cfg.p
     tf_eff = bf16 / 6.0  # TF32 issues at half the bf16 rate; 3xTF32 = 3 MMAs per product
-    kname = ("CSR SpMM A.X / A^T.Y (width %d)" if sparse else "Krylov-chain A.X / A^T.Y (width %d)") % cfg.p
+    kname = (("hybrid CSR product A.X / A^T.Y (width %d; hot-column panel on tcgen05 + CSR gather)"
+              if sparse and op.hot is not None else "CSR SpMM A.X / A^T.Y (width %d)") if sparse
+             else "Krylov-chain A.X / A^T.Y (width %d)") % cfg.p
     traffic = None if sparse else _profiled_traffic(args.config)
     if sparse or flops_per / bytes_per * hbm / 1e3 < tf_eff:
         roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm, "unit": "GB/s",

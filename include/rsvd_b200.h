@@ -209,6 +209,14 @@ int rsvd_flip_by_sign(int dtype, int64_t n, int64_t k, void *X, int64_t ldx,
                       const double *sign_val, void *stream);
 int rsvd_convert(int src_dtype, int dst_dtype, int64_t rows, int64_t cols, const void *src,
                  int64_t lds, void *dst, int64_t ldd, const int32_t *pred, void *stream);
+/* Row gather dst[i, :] = src[idx[i], :] and scatter dst[idx[i], :] = src[i, :],
+ * i < nidx, `cols` columns: the hot-column panel of the hybrid CSR product
+ * (X_hot = X[hot] before A_hot X_hot; (A^T Y)[hot] = A_hot^T Y after it).
+ * Replace the column slicing MatrixOperator leaves to numpy (matrix.py:227-247). */
+int rsvd_gather_rows(int dtype, int64_t nidx, int64_t cols, const int64_t *idx, const void *src,
+                     int64_t lds, void *dst, int64_t ldd, void *stream);
+int rsvd_scatter_rows(int dtype, int64_t nidx, int64_t cols, const int64_t *idx, const void *src,
+                      int64_t lds, void *dst, int64_t ldd, void *stream);
 /* out[i] = sqrt(max(in[i], 0)) (rsvd.py:220). */
 int rsvd_sqrt_clip(int64_t k, const double *in, double *out, void *stream);
 /* max |G - I| of a k x k FP64 matrix -> out[0] (rsvd.py:182-185). */

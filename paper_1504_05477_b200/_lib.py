@@ -47,6 +47,8 @@ _SIGS = {
     "rsvd_col_absargmax": ([_int, _i64, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _i64, _vp], _int),
     "rsvd_flip_by_sign": ([_int, _i64, _i64, _vp, _i64, _vp, _vp], _int),
     "rsvd_convert": ([_int, _int, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp], _int),
+    "rsvd_gather_rows": ([_int, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp], _int),
+    "rsvd_scatter_rows": ([_int, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp], _int),
     "rsvd_sqrt_clip": ([_i64, _vp, _vp, _vp], _int),
     "rsvd_ortho_error": ([_i64, _vp, _i64, _vp, _vp], _int),
 }

@@ -30,6 +30,8 @@ int canonicalize_signs(int dtype, int64_t n, int64_t k, void* X, int64_t ldx, vo
 int convert(int sd, int dd, int64_t rows, int64_t cols, const void* src, int64_t lds, void* dst,
             int64_t ldd, const int32_t* pred, cudaStream_t st);
 int sqrt_clip(int64_t k, const double* in, double* out, cudaStream_t st);
+int move_rows(int dtype, int gather, int64_t nidx, int64_t cols, const int64_t* idx, const void* src, int64_t lds,
+              void* dst, int64_t ldd, cudaStream_t st);
 int col_absargmax(int dtype, int64_t n, int64_t k, const void* X, int64_t ldx, int64_t row_offset,
                   double* out_val, int64_t* out_idx, void* ws, int64_t ws_bytes, cudaStream_t st);
 int flip_by_sign(int dtype, int64_t n, int64_t k, void* X, int64_t ldx, const double* sign_val,
@@ -246,6 +248,20 @@ int rsvd_convert(int src_dtype, int dst_dtype, int64_t rows, int64_t cols, const
     RSVD_REQUIRE(valid_dtype(src_dtype) && valid_dtype(dst_dtype), "convert: bad dtype");
     RSVD_REQUIRE(lds >= cols && ldd >= cols, "convert: bad leading dimension");
     return convert(src_dtype, dst_dtype, rows, cols, src, lds, dst, ldd, pred, as_stream(stream));
+}
+
+int rsvd_gather_rows(int dtype, int64_t nidx, int64_t cols, const int64_t* idx, const void* src, int64_t lds,
+                     void* dst, int64_t ldd, void* stream) {
+    RSVD_REQUIRE(valid_dtype(dtype), "gather_rows: bad dtype");
+    RSVD_REQUIRE(nidx >= 0 && cols >= 0 && lds >= cols && ldd >= cols, "gather_rows: bad shape");
+    return move_rows(dtype, 1, nidx, cols, idx, src, lds, dst, ldd, as_stream(stream));
+}
+
+int rsvd_scatter_rows(int dtype, int64_t nidx, int64_t cols, const int64_t* idx, const void* src, int64_t lds,
+                      void* dst, int64_t ldd, void* stream) {
+    RSVD_REQUIRE(valid_dtype(dtype), "scatter_rows: bad dtype");
+    RSVD_REQUIRE(nidx >= 0 && cols >= 0 && lds >= cols && ldd >= cols, "scatter_rows: bad shape");
+    return move_rows(dtype, 0, nidx, cols, idx, src, lds, dst, ldd, as_stream(stream));
 }
 
 int rsvd_sqrt_clip(int64_t k, const double* in, double* out, void* stream) {

@@ -171,6 +171,20 @@ __global__ void k_convert(int64_t rows, int64_t cols, const S* __restrict__ src,
     dst[i * ldd + j] = (D)src[i * lds + j];
 }
 
+// dst[i, :] = src[idx[i], :] (GATHER) or dst[idx[i], :] = src[i, :] (scatter):
+// the hot-column panels of the hybrid CSR product (sparse.cu).
+template <typename T, bool GATHER>
+__global__ void k_move_rows(int64_t nidx, int64_t cols, const int64_t* __restrict__ idx, const T* __restrict__ src,
+                            int64_t lds, T* __restrict__ dst, int64_t ldd) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nidx * cols) return;
+    const int64_t i = e / cols, j = e % cols;
+    if (GATHER)
+        dst[i * ldd + j] = src[idx[i] * lds + j];
+    else
+        dst[idx[i] * ldd + j] = src[i * lds + j];
+}
+
 __global__ void k_sqrt_clip(int64_t k, const double* __restrict__ in, double* __restrict__ out) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < k) out[i] = sqrt(fmax(in[i], 0.0));
@@ -367,6 +381,21 @@ int convert(int sd, int dd, int64_t rows, int64_t cols, const void* src, int64_t
         k_convert<double, double><<<nb, 256, 0, st>>>(rows, cols, (const double*)src, lds, (double*)dst, ldd, pred);
     else
         k_convert<float, float><<<nb, 256, 0, st>>>(rows, cols, (const float*)src, lds, (float*)dst, ldd, pred);
+    RSVD_CHECK_LAUNCH();
+    return RSVD_OK;
+}
+
+int move_rows(int dtype, int gather, int64_t nidx, int64_t cols, const int64_t* idx, const void* src, int64_t lds,
+              void* dst, int64_t ldd, cudaStream_t st) {
+    if (nidx == 0 || cols == 0) return RSVD_OK;
+    const unsigned nb = (unsigned)cdiv(nidx * cols, 256);
+#define RSVD_MR(T, G) k_move_rows<T, G><<<nb, 256, 0, st>>>(nidx, cols, idx, (const T*)src, lds, (T*)dst, ldd)
+    if (dtype == RSVD_F64) {
+        if (gather) RSVD_MR(double, true); else RSVD_MR(double, false);
+    } else {
+        if (gather) RSVD_MR(float, true); else RSVD_MR(float, false);
+    }
+#undef RSVD_MR
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }

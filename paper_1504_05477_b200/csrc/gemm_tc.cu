@@ -75,6 +75,15 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                                            int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -416,8 +425,9 @@ k_tc_gemm_t(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 #pragma unroll
                 for (int j = 0; j < KPS; ++j) {
                     const int kk = (int)(kbeg + (int64_t)(sl * KPS + j) * BK);
-                    tma_load_2d(&tmB, &b_full[s], dst + j * 2 * Cfg::B_BYTES, kk, (int)n0);
-                    tma_load_2d(&tmB, &b_full[s], dst + j * 2 * Cfg::B_BYTES + Cfg::B_BYTES, kk, (int)(p.Np + n0));
+                    tma_load_3d(&tmB, &b_full[s], dst + j * 2 * Cfg::B_BYTES, 0, (int)n0, kk / BK);
+                    tma_load_3d(&tmB, &b_full[s], dst + j * 2 * Cfg::B_BYTES + Cfg::B_BYTES, 0, (int)(p.Np + n0),
+                                kk / BK);
                 }
                 if (++s == SB) { s = 0; ph ^= 1; }
             }
@@ -631,8 +641,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         tma_load_2d(&tmA, &full[s], a_stage(s) + i * 32 * BK * 4, (int)(m0 + 32 * i), kk);
                 }
                 // K-major split-B planes: one box of BN rows x 32 k each
-                tma_load_2d(&tmB, &full[s], b_stage(s), kk, (int)n0);
-                tma_load_2d(&tmB, &full[s], b_stage(s) + Cfg::B_BYTES, kk, (int)(p.Np + n0));
+                tma_load_3d(&tmB, &full[s], b_stage(s), 0, (int)n0, kk / BK);
+                tma_load_3d(&tmB, &full[s], b_stage(s) + Cfg::B_BYTES, 0, (int)(p.Np + n0), kk / BK);
                 if (++s == STAGES) { s = 0; ph ^= 1; }
             }
         }
@@ -715,9 +725,14 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     }
 }
 
-// Split the small operand B (K x N, ld) into two K-major planes, hi then lo,
-// each Np x Kp (row n holds column n of B), zero padded so boxes past K or N
-// read zeros. Transposes through a 32 x 33 shared tile.
+// Split the operand B (K x N, ld) into two K-major planes, hi then lo, each
+// Np x Kp (row n holds column n of B), zero padded so boxes past K or N read
+// zeros, stored k-blocked: for k-block kb, rows [0, Np) of hi then [Np, 2 Np)
+// of lo, 32 floats (128 bytes) each -> element (n, k) of plane P at
+// ((kb * 2 Np) + P Np + n) * 32 + k % 32. One TMA box (32 k x BN rows) is
+// then one contiguous 128 BN-byte run (a TN product streams B from HBM; the
+// row-major plane made every box 128-byte pieces 4 Kp bytes apart).
+// Transposes through a 32 x 33 shared tile.
 __global__ void k_split_b(int64_t K, int64_t N, const float* __restrict__ B, int64_t ldb, int64_t Kp, int64_t Np,
                           float* __restrict__ out, const int32_t* __restrict__ pred) {
     if (pred_off(pred)) return;
@@ -733,8 +748,9 @@ __global__ void k_split_b(int64_t K, int64_t N, const float* __restrict__ B, int
         const int64_t c = c0 + i, r = k0 + tx;
         const float x = t[tx][i];
         const float h = tf32_hi(x);
-        out[c * Kp + r] = h;
-        out[(Np + c) * Kp + r] = tf32_rna(x - h);
+        float* blk = out + (k0 / 32) * (2 * Np) * 32;  // k0 is a multiple of 32
+        blk[c * 32 + tx] = h;
+        blk[(Np + c) * 32 + tx] = tf32_rna(x - h);
     }
 }
 
@@ -787,6 +803,23 @@ int make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, i
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     RSVD_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return RSVD_OK;
+}
+
+// k-blocked split-B planes (see k_split_b): dims {32, 2 Np, Kp / 32}, box
+// {32, BN, 1}, 128B swizzle (the smem tile is the same K-major layout as a
+// 2-D box of a row-major plane).
+int make_map_b(CUtensorMap* map, const void* base, int64_t Kp, int64_t Np, int box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    RSVD_REQUIRE(fn != nullptr, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[3] = {32, (cuuint64_t)(2 * Np), (cuuint64_t)(Kp / 32)};
+    cuuint64_t strides[2] = {128, (cuuint64_t)(2 * Np * 128)};
+    cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    RSVD_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (split B) failed (%d)", (int)r);
     return RSVD_OK;
 }
 
@@ -888,7 +921,10 @@ int gemm_nn_tc(int64_t m, int64_t n, int64_t k, double alpha, const float* A, in
                int64_t ldb, double beta, float* C, int64_t ldc, const double* row_sub, const int32_t* pred,
                cudaStream_t st) {
     int bn = pick_bn(n);
-    const int64_t Kp = cdiv(k, BK) * BK, Np = cdiv(n, bn) * bn;
+    // planes padded to 32 rows only: a last N tile's hi box may run into the lo
+    // plane (and its lo box past 2 Np, zero-filled) -- those rows feed output
+    // columns >= n, which are never stored
+    const int64_t Kp = cdiv(k, BK) * BK, Np = cdiv(n, 32) * 32;
     static thread_local Scratch sc;  // split-B buffer
     size_t need = (size_t)(2 * Kp * Np * 4);
     if (sc.bytes < need) {
@@ -902,7 +938,7 @@ int gemm_nn_tc(int64_t m, int64_t n, int64_t k, double alpha, const float* A, in
     CUtensorMap tA, tB;
     rc = make_map(&tA, A, k, m, lda, BM, false);
     if (rc) return rc;
-    rc = make_map(&tB, bs, Kp, 2 * Np, Kp, bn, false);
+    rc = make_map_b(&tB, bs, Kp, Np, bn);
     if (rc) return rc;
     TcParams p{};
     p.M = m; p.N = n; p.K = k; p.k_per_split = Kp; p.Kp = Kp; p.Np = Np;
@@ -935,7 +971,7 @@ int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, con
     const int64_t S = tn_splits_tc(Mop, Nop, Kop);
     RSVD_REQUIRE(ws_bytes >= S * Mop * cdiv(Nop, 4) * 4 * 4, "gemm_tn_tc: workspace too small");
     RSVD_REQUIRE(aligned16(ws), "gemm_tn_tc: workspace must be 16-byte aligned");
-    const int64_t Kp = cdiv(Kop, BK) * BK, Np = cdiv(Nop, bn) * bn;
+    const int64_t Kp = cdiv(Kop, BK) * BK, Np = cdiv(Nop, 32) * 32;  // see gemm_nn_tc
     static thread_local Scratch sc;
     size_t need = (size_t)(2 * Kp * Np * 4);
     if (sc.bytes < need) {
@@ -949,7 +985,7 @@ int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, con
     CUtensorMap tA, tB;
     rc = make_map(&tA, A, k /*inner = columns of A*/, m, lda, BK, true);
     if (rc) return rc;
-    rc = make_map(&tB, bs, Kp, 2 * Np, Kp, bn, false);
+    rc = make_map_b(&tB, bs, Kp, Np, bn);
     if (rc) return rc;
     TcParams p{};
     p.M = Mop; p.N = Nop; p.K = Kop; p.Np = Np;

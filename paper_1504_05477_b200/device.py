@@ -216,6 +216,20 @@ def convert(src, dst, pred=None):
     return dst
 
 
+def gather_rows(idx, src, dst):
+    """dst[i, :] = src[idx[i], :] (idx int64 on the device)."""
+    check(lib().rsvd_gather_rows(dcode(src), idx.numel(), src.shape[1], _ptr(idx), _ptr(src), _ld(src), _ptr(dst),
+                                 _ld(dst), _stream()), "gather_rows")
+    return dst
+
+
+def scatter_rows(idx, src, dst):
+    """dst[idx[i], :] = src[i, :]."""
+    check(lib().rsvd_scatter_rows(dcode(src), idx.numel(), src.shape[1], _ptr(idx), _ptr(src), _ld(src), _ptr(dst),
+                                  _ld(dst), _stream()), "scatter_rows")
+    return dst
+
+
 def sqrt_clip(x, out=None):
     if out is None:
         out = torch.empty_like(x)

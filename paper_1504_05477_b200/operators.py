@@ -12,6 +12,8 @@ with mu the column means of the full (all-rank) matrix, kept in FP64.
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import device as ops
@@ -75,10 +77,24 @@ class CsrDeviceOp:
     """CSR A on the device; A^T products run as a gather over the CSR of A^T
     built once (spmm_t, _kernels.pyx:95-113, without atomics). Both products
     go through row-split plans (ops.SpmmPlan) so that the long rows of A^T
-    (Zipf-heavy columns of A) are spread over many warps."""
+    (Zipf-heavy columns of A) are spread over many warps.
 
-    def __init__(self, indptr, col, val, ncols, n_total=None, row_offset=0):
-        self.indptr, self.col, self.val = indptr, col, val
+    Hybrid hot/cold split (FP32): a CSR product is gather-bound -- every
+    nonzero reads one b-wide row of the dense block from L2, ~400 bytes at
+    b = 100 against 8 bytes of A. Columns holding at least `hot_density` x
+    rows nonzeros (the Zipf head of C3: ~0.1% of the columns, ~40% of the
+    nonzeros) are stored once as a dense row-major panel A_hot (rows x H,
+    zeros included) and multiplied on the tensor cores (3xTF32 GEMM:
+    A_hot X[hot] and A_hot^T Y), the remaining nonzeros stay CSR:
+        A X   = A_hot X[hot] + A_cold X
+        A^T Y = scatter(hot, A_hot^T Y) + A_cold^T Y   (hot rows of A_cold^T empty)
+    A dense column costs 2 rows b flops on the tensor pipe; its nonzeros cost
+    nnz_j b 4 bytes of L2 gather, so a column pays off above ~3% density."""
+
+    HOT_DENSITY = float(os.environ.get("RSVD_SPMM_HOT_DENSITY", "0.03"))
+    HOT_MAX = 2048
+
+    def __init__(self, indptr, col, val, ncols, n_total=None, row_offset=0, hot_density=None):
         nrows = indptr.numel() - 1
         self.local_rows = nrows
         self.ncols = int(ncols)
@@ -87,10 +103,46 @@ class CsrDeviceOp:
         self.shape = (self.n_total, self.ncols)
         self.dtype = val.dtype
         self.device = val.device
+        self.mu = None
+        self._nnz = val.numel()
+        dens = self.HOT_DENSITY if hot_density is None else float(hot_density)
+        self.hot = None
+        if val.dtype == torch.float32 and dens > 0 and nrows >= 128 and val.numel() > 0:
+            self.hot = self._split_hot(indptr, col, val, nrows, dens)
+        if self.hot is not None:
+            indptr, col, val = self.hot["cold"]
+        self.indptr, self.col, self.val = indptr, col, val
         self.t_indptr, self.t_col, self.t_val = ops.csr_transpose(indptr, col, val, nrows, self.ncols)
         self.plan = ops.SpmmPlan(indptr)
         self.t_plan = ops.SpmmPlan(self.t_indptr)
-        self.mu = None
+
+    def _split_hot(self, indptr, col, val, nrows, dens):
+        """Operator setup (torch plumbing, once): pick the hot columns, build
+        the dense panel and the cold CSR (nonzero order kept)."""
+        counts = torch.bincount(col.to(torch.int64), minlength=self.ncols)
+        thr = max(1, int(dens * nrows))
+        hot = torch.nonzero(counts >= thr).flatten()
+        if hot.numel() == 0:
+            return None
+        if hot.numel() > self.HOT_MAX:
+            hot = hot[torch.argsort(counts[hot], descending=True)[: self.HOT_MAX]].sort().values
+        H = hot.numel()
+        Hp = (H + 3) // 4 * 4  # 16-byte rows for the tensor-core operand
+        pos = torch.full((self.ncols,), -1, dtype=torch.int64, device=col.device)
+        pos[hot] = torch.arange(H, device=col.device)
+        ip = indptr.to(torch.int64)
+        rows = torch.repeat_interleave(torch.arange(nrows, device=col.device), ip[1:] - ip[:-1])
+        pcol = pos[col.to(torch.int64)]
+        is_hot = pcol >= 0
+        panel = torch.zeros((nrows, Hp), dtype=val.dtype, device=val.device)
+        panel[rows[is_hot], pcol[is_hot]] = val[is_hot]
+        cold = ~is_hot
+        cold_counts = torch.bincount(rows[cold], minlength=nrows)
+        cptr = torch.zeros(nrows + 1, dtype=indptr.dtype, device=indptr.device)
+        cptr[1:] = torch.cumsum(cold_counts, 0).to(indptr.dtype)
+        return {"idx": hot.contiguous(), "H": H, "Hp": Hp, "panel": panel,
+                "cold": (cptr, col[cold].contiguous(), val[cold].contiguous()),
+                "hot_nnz": int(is_hot.sum())}
 
     @property
     def is_sparse(self):
@@ -98,18 +150,47 @@ class CsrDeviceOp:
 
     @property
     def nnz(self):
-        return self.val.numel()
+        return self._nnz
+
+    def _x_hot(self, X):
+        h = self.hot
+        xh = torch.zeros((h["Hp"], X.shape[1]), dtype=X.dtype, device=X.device)
+        ops.gather_rows(h["idx"], X, xh[: h["H"]])
+        return xh
+
+    def _apply32(self, X, out):
+        if self.hot is None:
+            return ops.spmm_csr_plan(self.plan, self.col, self.val, X, out)
+        ops.gemm_nn(self.hot["panel"], self._x_hot(X), out)
+        return ops.spmm_csr_plan(self.plan, self.col, self.val, X, out, beta=1.0)
+
+    def _apply_t32(self, Y, out):
+        ops.spmm_csr_plan(self.t_plan, self.t_col, self.t_val, Y, out)
+        if self.hot is not None:
+            h = self.hot
+            th = torch.empty((h["Hp"], Y.shape[1]), dtype=out.dtype, device=out.device)
+            ops.gemm_tn(h["panel"], Y, th)
+            ops.scatter_rows(h["idx"], th[: h["H"]], out)
+        return out
 
     def apply(self, X, out):
-        if out.dtype == self.dtype:
-            return ops.spmm_csr_plan(self.plan, self.col, self.val, X, out)
+        if out.dtype == self.dtype and X.dtype == self.dtype:
+            return self._apply32(X, out) if self.dtype == torch.float32 else \
+                ops.spmm_csr_plan(self.plan, self.col, self.val, X, out)
         tmp = torch.empty(out.shape, dtype=self.dtype, device=out.device)
-        ops.spmm_csr_plan(self.plan, self.col, self.val, X, tmp)
+        if self.dtype == torch.float32:
+            self._apply32(X, tmp)
+        else:
+            ops.spmm_csr_plan(self.plan, self.col, self.val, X, tmp)
         return ops.convert(tmp, out)
 
     def apply_t(self, Y, out):
-        if out.dtype == self.dtype:
-            return ops.spmm_csr_plan(self.t_plan, self.t_col, self.t_val, Y, out)
+        if out.dtype == self.dtype and Y.dtype == self.dtype:
+            return self._apply_t32(Y, out) if self.dtype == torch.float32 else \
+                ops.spmm_csr_plan(self.t_plan, self.t_col, self.t_val, Y, out)
         tmp = torch.empty(out.shape, dtype=self.dtype, device=out.device)
-        ops.spmm_csr_plan(self.t_plan, self.t_col, self.t_val, Y, tmp)
+        if self.dtype == torch.float32:
+            self._apply_t32(Y, tmp)
+        else:
+            ops.spmm_csr_plan(self.t_plan, self.t_col, self.t_val, Y, tmp)
         return ops.convert(tmp, out)

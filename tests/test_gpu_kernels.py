@@ -303,3 +303,48 @@ def test_spmm_plan_split_rows_and_wide_blocks(ops, nb, dtype):
     ref = 0.5 * (A @ B) + 2.0 * C0
     tol = 1e-4 if dtype == torch.float32 else 1e-12
     assert np.max(np.abs(Ct.cpu().double().numpy() - ref)) < tol * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("nb", [8, 100, 300])
+def test_csr_hybrid_hot_columns(ops, nb):
+    """Hybrid CSR operator: Zipf-head columns (here every 7th of the first
+    140 columns is dense-ish, plus a fully dense column and an empty one)
+    densified into a tensor-core panel, the rest gathered; A X and A^T Y
+    against dense FP64 products and against the pure-CSR operator."""
+    from paper_1504_05477_b200.operators import CsrDeviceOp
+
+    rng = np.random.default_rng(nb + 1)
+    n, d = 3000, 5000
+    A = np.zeros((n, d))
+    mask = rng.random((n, d)) < 0.004
+    mask[:, 0:140:7] |= rng.random((n, 20)) < 0.3
+    mask[:, 5] = True
+    mask[:, 6] = False
+    A[mask] = rng.lognormal(0, 1, int(mask.sum()))
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    indptr[1:] = np.cumsum(mask.sum(1))
+    rows, cols = np.nonzero(mask)
+    ip = torch.from_numpy(indptr).cuda().to(torch.int32)
+    cl = torch.from_numpy(cols).cuda().to(torch.int32)
+    vl = torch.from_numpy(A[rows, cols]).cuda().float()
+    hyb = CsrDeviceOp(ip, cl, vl, d)
+    pure = CsrDeviceOp(ip, cl, vl, d, hot_density=0.0)
+    assert hyb.hot is not None and hyb.hot["H"] >= 21 and pure.hot is None
+    assert hyb.nnz == pure.nnz == int(mask.sum())
+    X = rng.standard_normal((d, nb))
+    Y = rng.standard_normal((n, nb))
+    Xt, Yt = torch.from_numpy(X).cuda().float(), torch.from_numpy(Y).cuda().float()
+    A32 = A.astype(np.float32).astype(np.float64)
+    for op in (hyb, pure):
+        out = torch.empty((n, nb), device="cuda")
+        op.apply(Xt, out)
+        ref = A32 @ Xt.double().cpu().numpy()
+        assert np.max(np.abs(out.double().cpu().numpy() - ref)) < 2e-6 * np.abs(ref).max()
+        out_t = torch.empty((d, nb), device="cuda")
+        op.apply_t(Yt, out_t)
+        ref_t = A32.T @ Yt.double().cpu().numpy()
+        assert np.max(np.abs(out_t.double().cpu().numpy() - ref_t)) < 2e-6 * np.abs(ref_t).max()
+        # FP64 output from FP32 operands (the chain's mixed-precision call)
+        out64 = torch.empty((d, nb), dtype=torch.float64, device="cuda")
+        op.apply_t(Yt, out64)
+        assert np.max(np.abs(out64.cpu().numpy() - ref_t)) < 2e-6 * np.abs(ref_t).max()

@@ -32,3 +32,10 @@ ref_t = A.double().T @ Y.double() if n * d <= 2e8 else None
 print(f"NN max rel err (first 4096 rows) {err:.2e}")
 if ref_t is not None:
     print(f"TN max rel err {((out_x.double() - ref_t).abs().max() / ref_t.abs().max()).item():.2e}")
+if os.environ.get("PROBE_PROFILE"):
+    from torch.profiler import profile, ProfilerActivity
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        ops.gemm_nn(A, X, out_y); ops.gemm_tn(A, Y, out_x); torch.cuda.synchronize()
+    for ev in prof.events():
+        if ev.device_type == torch.autograd.DeviceType.CUDA:
+            print(f"  {ev.device_time_total / 1e3:8.3f} ms  {ev.name[:90]}")
