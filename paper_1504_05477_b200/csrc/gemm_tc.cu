@@ -523,8 +523,15 @@ k_tc_gemm_t(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     for (int k = 0; k < 32; ++k)
                         x[k] = *reinterpret_cast<const float*>(atom + k * 128 + (((lane >> 3) ^ (k & 3)) << 5));
                 }
+#ifndef RSVD_TC_RELEASE_AFTER_ST
+                // the stage is re-filled by TMA (async proxy) once released: the
+                // generic reads above must be complete first. Without the proxy
+                // fence ptxas issued the arrive ahead of the loads' completion
+                // (per-row corruption when a refill landed early).
+                fence_proxy_async();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&a_empty[sa]);
+#endif
                 float lo[32];
 #pragma unroll
                 for (int k = 0; k < 32; ++k) lo[k] = (RSVD_TC_ABLATE & 1) ? 0.f : x[k] - tf32_hi(x[k]);
@@ -532,6 +539,10 @@ k_tc_gemm_t(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 tmem_st16(t + j * BK + 16, x + 16);
                 tmem_st16(t + KPS * BK + j * BK, lo);
                 tmem_st16(t + KPS * BK + j * BK + 16, lo + 16);
+#ifdef RSVD_TC_RELEASE_AFTER_ST
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&a_empty[sa]);
+#endif
                 if (++sa == SA) { sa = 0; pha ^= 1; }
             }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
