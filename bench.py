@@ -45,7 +45,7 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     "c2": dict(n=50000, d=10000, k=50, q=10, spectrum="pow", noise=1e-3, variant="bk"),
-    "c1": dict(n=2000, d=1000, k=20, q=8, spectrum="inv", noise=0.0, variant="bk"),
+    "c1": dict(n=2000, d=1000, k=20, q=8, spectrum="inv", noise=0.0, variant="bk", fp64=True),
     "c4": dict(n=1000000, d=4096, k=200, q=6, spectrum="clustered", noise=0.0, variant="bk"),
     "c3": dict(n=200000, d=100000, k=100, q=15, sparse=True, variant="bk"),
     # C5: PCA with implicit mean-centering (rank-1 GEMM-epilogue corrections)
@@ -176,6 +176,44 @@ def spmm_probe(dev, reps=5):
         res[label] = leg
         del op
     del indptr, colv, valv
+    torch.cuda.empty_cache()
+    return res
+
+
+def gemm_c4_probe(dev, bf16, reps=3):
+    """The Krylov-GEMM half of the metric where it is tensor-bound: the C4
+    chain products A.X and A^T.Y (A 1,000,000 x 4096 FP32, width 200; random
+    operands -- the kernel's work does not depend on the values) through the
+    same 3xTF32 tcgen05 kernel, CUDA-event timed, as algorithmic TFLOP/s
+    (2 n d b) against the measured bf16 dense peak / 6 (TF32 issues at half
+    the bf16 rate and 3xTF32 is three TF32 MMAs). A (16.4 GB) exceeds L2."""
+    import torch
+    from paper_1504_05477_b200 import device as ops
+
+    n, d, b = 1000000, 4096, 200
+    g = torch.Generator(device=dev).manual_seed(11)
+    A = torch.randn((n, d), generator=g, device=dev)
+    X = torch.randn((d, b), generator=g, device=dev)
+    Y = torch.randn((n, b), generator=g, device=dev)
+    out_y = torch.empty((n, b), device=dev)
+    out_x = torch.empty((d, b), device=dev)
+    peak = bf16 / 6.0
+    fl = 2.0 * n * d * b
+    res = {"config": f"C4 chain shape: A {n}x{d} FP32, width {b} (random operands)",
+           "peak_tflops": peak, "peak_source": f"measured bf16 dense {bf16:.0f} TFLOP/s / 6",
+           "ncu": "profiles/r01_c4_chain_kernel_ncu.json (tensor pipe 83% / 86% of peak sustained)"}
+    for name, fn in (("A.X", lambda: ops.gemm_nn(A, X, out_y)), ("A^T.Y", lambda: ops.gemm_tn(A, Y, out_x))):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        res[name] = {"ms": ms, "tflops": fl / ms / 1e9, "frac": fl / ms / 1e9 / peak}
+    del A, X, Y, out_y, out_x
     torch.cuda.empty_cache()
     return res
 
@@ -344,6 +382,8 @@ def run_ours(args):
         op = CsrDeviceOp(indptr, colv, valv, d, n_total=n, row_offset=lo)
     else:
         A_full = make_matrix(cfgd, dev)
+        if cfgd.get("fp64"):  # C1 is an FP64 configuration (BASELINE configs[0])
+            A_full = A_full.double()
         if world > 1:
             A = A_full[lo:hi].contiguous()
             del A_full
@@ -435,7 +475,8 @@ def run_ours(args):
     if sparse:  # nnz (4 + 4) + (rows + 1) 4 + (d + n) b 4 per SpMM
         bytes_per = nnz_local * 8 + (n_loc + 1) * 4 + (n_loc + d) * cfg.p * 4
     else:
-        bytes_per = n_loc * d * 4 + (n_loc + d) * cfg.p * 4
+        es = A.element_size()
+        bytes_per = n_loc * d * es + (n_loc + d) * cfg.p * es
     avg_chain_ms = float(np.mean([t for t, _ in chain])) if chain else float("nan")
     achieved = bytes_per / (avg_chain_ms * 1e-3) / 1e9
     rr_ms = float(np.mean([t for t, _ in rr])) if rr else float("nan")
@@ -477,7 +518,7 @@ def run_ours(args):
             r = rk.factorize(A_host, cfg, center=center)
         torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
-        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": int(A_host.numel() * 4 + Pi.size * 4),
+        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": int(A_host.numel() * A_host.element_size() + Pi.size * 4),
                "d2h_bytes_per_step": int(n * k * 8 + k * 8 + 8 * 3)}
         del A_host
 
@@ -510,6 +551,8 @@ def run_ours(args):
         out["cpu_baseline"] = cpu_baseline(A, cfgd, cfg, Pi, args, df)
     if rank == 0 and world == 1 and not sparse and not args.no_spmm:
         out["spmm_c3"] = spmm_probe(dev)
+    if rank == 0 and world == 1 and args.config == "c2" and not args.no_c4gemm:
+        out["gemm_c4"] = gemm_c4_probe(dev, bf16)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -684,6 +727,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fp64", action="store_true", help="skip the FP64 parity-mode leg on FP32 configs")
+    ap.add_argument("--no-c4gemm", action="store_true", help="skip the tensor-bound C4 chain-GEMM leg of the C2 line")
     ap.add_argument("--no-spmm", action="store_true", help="skip the C3 SpMM measurement on dense configs")
     ap.add_argument("--count-launches", action="store_true", default=True)
     ap.add_argument("--cpu-budget", type=float, default=25.0)

@@ -183,7 +183,9 @@ int rsvd_eig_select(int64_t w, const double *Mdiag_src, int64_t ldm, const doubl
  * re-orthogonalisation, back-transformation (LAPACK dsyevx structure).
  * evals: k values, descending; evecs: w x k row-major (column i pairs with
  * evals[i], sign arbitrary); info[0] = 1 on success, 0 if an eigenvector
- * iteration broke down (host maps to ConvergenceError). M is not modified. */
+ * iteration broke down (host maps to ConvergenceError). M is not modified.
+ * evecs = NULL computes the eigenvalues only (the sweep harness's exact
+ * oracle spectrum, factor.py:170-215 dense_svd_reference). */
 int64_t rsvd_syev_topk_ws_bytes(int64_t w, int64_t k);
 int rsvd_syev_topk(int64_t w, const double *M, int64_t ldm, int64_t k, double *evals, double *evecs,
                    int64_t lde, int32_t *info, void *ws, int64_t ws_bytes, void *stream);

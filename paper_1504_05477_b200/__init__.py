@@ -9,8 +9,12 @@ no CPU fallback.
 """
 
 from . import metrics  # noqa: F401  (GPU parity metrics)
+from .experiment import ExperimentSpec, OracleSpectrum, oracle_spectrum, rows_to_csv, run_experiment  # f4
+from .io import load_dense_csv, load_matrix_market, write_matrix_market  # f3
+from .metrics import ErrorReport, compute_error_report
 from .errors import ConvergenceError, ParseError
 from .matrix import DenseMatrix, SeededRng, SparseMatrixCSR, as_dense_array, gaussian
+from .synth import SyntheticSpec, synth_matrix
 from .rsvd import (
     PartialSvdResult,
     RsvdConfig,
@@ -27,6 +31,18 @@ from .rsvd import (
 __version__ = "0.1.0"
 
 __all__ = [
+    "ExperimentSpec",
+    "OracleSpectrum",
+    "oracle_spectrum",
+    "rows_to_csv",
+    "run_experiment",
+    "load_dense_csv",
+    "load_matrix_market",
+    "write_matrix_market",
+    "ErrorReport",
+    "compute_error_report",
+    "SyntheticSpec",
+    "synth_matrix",
     "ConvergenceError",
     "ParseError",
     "DenseMatrix",

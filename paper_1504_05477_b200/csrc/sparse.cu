@@ -90,8 +90,14 @@ int launch_spmm(int64_t nrows, int64_t nb, const void* indptr, const void* col, 
 // partial sums go to workspace slots and are added in chunk order by
 // k_spmm_split_reduce (deterministic). Warp per chunk; 4 nonzeros in flight
 // per lane; FP32 rows of B gathered as float4 (VEC) when aligned.
+#ifndef RSVD_SPMM_UNROLL
+#define RSVD_SPMM_UNROLL 4
+#endif
+#ifndef RSVD_SPMM_MINB
+#define RSVD_SPMM_MINB 1
+#endif
 template <typename T, typename I, int NPL, bool VEC>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, RSVD_SPMM_MINB)
 k_spmm_plan(int64_t nchunks, int64_t nb, const I* __restrict__ col, const T* __restrict__ val,
             const T* __restrict__ B, int64_t ldb, double alpha, double beta, T* __restrict__ C, int64_t ldc,
             const int64_t* __restrict__ clo, const int64_t* __restrict__ chi, const int32_t* __restrict__ crow,
@@ -135,15 +141,17 @@ k_spmm_plan(int64_t nchunks, int64_t nb, const I* __restrict__ col, const T* __r
         }
         const int cnt = (int)min((int64_t)32, hi - base);
         int i = 0;
-        for (; i + 4 <= cnt; i += 4) {
-            const int64_t c0 = __shfl_sync(0xffffffffu, c, i), c1 = __shfl_sync(0xffffffffu, c, i + 1);
-            const int64_t c2 = __shfl_sync(0xffffffffu, c, i + 2), c3 = __shfl_sync(0xffffffffu, c, i + 3);
-            const T v0 = __shfl_sync(0xffffffffu, v, i), v1 = __shfl_sync(0xffffffffu, v, i + 1);
-            const T v2 = __shfl_sync(0xffffffffu, v, i + 2), v3 = __shfl_sync(0xffffffffu, v, i + 3);
-            accum(B + c0 * ldb, v0);
-            accum(B + c1 * ldb, v1);
-            accum(B + c2 * ldb, v2);
-            accum(B + c3 * ldb, v3);
+        constexpr int U = RSVD_SPMM_UNROLL;  // nonzeros (row gathers) in flight per warp
+        for (; i + U <= cnt; i += U) {
+            int64_t cu[U];
+            T vu[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                cu[u] = __shfl_sync(0xffffffffu, c, i + u);
+                vu[u] = __shfl_sync(0xffffffffu, v, i + u);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) accum(B + cu[u] * ldb, vu[u]);
         }
         for (; i < cnt; ++i) {
             const int64_t ci = __shfl_sync(0xffffffffu, c, i);

@@ -700,6 +700,7 @@ int syev_topk(int64_t w, const double* M, int64_t ldm, int64_t k, double* evals,
     RSVD_CHECK_LAUNCH();
     k_multisect<<<(unsigned)cdiv(k * 32, 256), 256, 0, st>>>(w, k, s.d, e2, bounds, evals);
     RSVD_CHECK_LAUNCH();
+    if (evecs == nullptr) return RSVD_OK;  // eigenvalues only (the sweep harness's oracle spectrum)
     k_clusters<<<1, 32, 0, st>>>(k, evals, bounds, cl, ncl);
     RSVD_CHECK_LAUNCH();
     k_invit<<<(unsigned)cdiv(k * 32, 128), 128, 0, st>>>(w, k, s.d, s.e, evals, bounds, cl, ncl, X, fac, info);

@@ -165,19 +165,20 @@ def eig_select(M, V, k, evals=None, evecs=None):
     return evals, evecs
 
 
-def syev_topk(M, k, evals=None, evecs=None, info=None):
+def syev_topk(M, k, evals=None, evecs=None, info=None, values_only=False):
     """Top-k eigenpairs of symmetric M (descending). Returns device tensors
-    (evals[k], evecs[w x k], info[int32: ok, _])."""
+    (evals[k], evecs[w x k] or None with values_only, info[int32: ok, _])."""
     w = M.shape[0]
     if evals is None:
         evals = torch.empty(k, dtype=torch.float64, device=M.device)
-    if evecs is None:
+    if evecs is None and not values_only:
         evecs = torch.empty((w, k), dtype=torch.float64, device=M.device)
     if info is None:
         info = torch.zeros(4, dtype=torch.int32, device=M.device)
     L = lib()
     ws = WS.get(L.rsvd_syev_topk_ws_bytes(w, k), M.device)
-    check(L.rsvd_syev_topk(w, _ptr(M), _ld(M), k, _ptr(evals), _ptr(evecs), _ld(evecs), _ptr(info), _ptr(ws),
+    check(L.rsvd_syev_topk(w, _ptr(M), _ld(M), k, _ptr(evals), _ptr(evecs), k if evecs is None else _ld(evecs),
+                           _ptr(info), _ptr(ws),
                            ws.numel(), _stream()), "syev_topk")
     return evals, evecs, info
 

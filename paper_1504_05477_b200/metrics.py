@@ -21,6 +21,8 @@ estimator reads a 4 GB FP64 copy twice per start.
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 import torch
 
@@ -34,8 +36,13 @@ RESTART_SEEDS = (101, 202, 303)  # metrics.py:38
 
 
 def _operator(A, precision="auto"):
+    """A device operator for A (an already-built DenseDeviceOp / CsrDeviceOp
+    is used as is, so a sweep uploads its input once)."""
+    from .operators import CsrDeviceOp, DenseDeviceOp
     from .rsvd import make_operator
 
+    if isinstance(A, (DenseDeviceOp, CsrDeviceOp)):
+        return A
     return make_operator(A, precision=precision)
 
 
@@ -160,3 +167,114 @@ def per_vector_errors(A, Z, sigma, precision="auto"):
     errs = np.abs(sigma[:k] ** 2 - cap)
     denom = sigma[k] ** 2 if sigma.shape[0] > k else 0.0
     return errs if denom == 0.0 else errs / denom
+
+
+# ---------------------------------------------------------------------------
+# the full error report (metrics.py:32-38, 65-99, 184-252): Frobenius ratio,
+# spectral ratio, per-vector errors, against oracle singular values
+
+Z_ORTHO_TOL = 1e-8        # metrics.py:38
+EXACT_RANK_RTOL = 1e-14   # metrics.py:37
+
+
+def frobenius_sq(A, precision="auto"):
+    """||A||_F^2 in FP64 (MatrixOperator.frobenius_sq)."""
+    op = _operator(A, precision)
+    parts = [op.val.view(-1, 1)] if op.is_sparse else [op.A]
+    if op.is_sparse and op.hot is not None:  # hybrid operator: cold CSR + dense hot panel
+        parts.append(op.hot["panel"])
+    total = 0.0
+    for x in parts:
+        if x.numel():
+            cols = torch.empty(x.shape[1], dtype=torch.float64, device=op.device)
+            ops.colreduce(x, True, cols)
+            total += float(cols.sum().item())
+    return total
+
+
+def check_orthonormal(Z, device):
+    """metrics.py:41-45: ValueError if max |Z^T Z - I| > 1e-8 (FP64 Gram of
+    the FP64 Z, whatever precision the operator runs in)."""
+    from .matrix import DenseMatrix
+
+    z = Z.data if isinstance(Z, DenseMatrix) else Z
+    if not isinstance(z, torch.Tensor):
+        z = torch.from_numpy(np.ascontiguousarray(z))
+    z = z.to(device=device, dtype=torch.float64).contiguous()
+    g = ops.gram(z)
+    err = float(ops.ortho_error(g).item())
+    if err > Z_ORTHO_TOL:
+        raise ValueError(f"Z is not orthonormal (max deviation {err:.3e})")
+
+
+def _tail_sq(sigma, k):
+    return float(np.sum(sigma[k:] ** 2)) if k < sigma.shape[0] else 0.0
+
+
+def _sig(sigma, i):
+    return float(sigma[i]) if i < sigma.shape[0] else 0.0
+
+
+def frob_error_ratio(A, Z, sigma, precision="auto"):
+    """metrics.py:84-99: ||A - Z Z^T A||_F / ||A - A_k||_F through
+    ||A||_F^2 - ||Z^T A||_F^2; exact-rank inputs report 1.0."""
+    op = _operator(A, precision)
+    check_orthonormal(Z, op.device)
+    z = _as_device_z(Z, op)
+    sigma = np.asarray(sigma, dtype=np.float64)
+    k = z.shape[1]
+    fro_sq = frobenius_sq(op)
+    captured = float(np.sum(captured_variance(op, z)))
+    num_sq = max(fro_sq - captured, 0.0)
+    tail = _tail_sq(sigma, k)
+    if np.sqrt(tail) < EXACT_RANK_RTOL * np.sqrt(fro_sq):
+        return 1.0
+    return float(np.sqrt(num_sq / tail))
+
+
+@dataclass(frozen=True)
+class ErrorReport:
+    """metrics.py:184-216 — the three measures for one run."""
+
+    frob_ratio: float
+    spectral_ratio: float
+    per_vector: np.ndarray
+    per_vector_max: float
+    exact_rank: bool
+    absolute_per_vector: bool
+    k: int
+    q: int | None = None
+    variant: str | None = None
+    seed: int | None = None
+
+    def __post_init__(self):
+        pv = np.array(self.per_vector, dtype=np.float64, copy=True)
+        pv.setflags(write=False)
+        object.__setattr__(self, "per_vector", pv)
+        if self.per_vector_max != (float(np.max(pv)) if pv.size else 0.0):
+            raise ValueError("per_vector_max must equal max(per_vector)")
+
+
+def compute_error_report(A, Z, sigma, q=None, variant=None, seed=None, precision="auto"):
+    """metrics.py:236-252 on the GPU, A uploaded once: frob and spectral
+    ratios, per-vector errors against the oracle singular values `sigma`."""
+    op = _operator(A, precision)
+    check_orthonormal(Z, op.device)
+    z = _as_device_z(Z, op)
+    sigma = np.asarray(sigma, dtype=np.float64)
+    k = z.shape[1]
+    pv = per_vector_errors(op, z, sigma)
+    fro_sq = frobenius_sq(op)
+    sk = _sig(sigma, k)
+    spec = 1.0 if sk == 0.0 else spectral_error(op, z) / sk
+    if variant is not None:
+        variant = getattr(variant, "value", str(variant))
+    return ErrorReport(
+        frob_ratio=frob_error_ratio(op, Z, sigma),
+        spectral_ratio=spec,
+        per_vector=pv,
+        per_vector_max=float(np.max(pv)) if pv.size else 0.0,
+        exact_rank=bool(np.sqrt(_tail_sq(sigma, k)) < EXACT_RANK_RTOL * np.sqrt(fro_sq)),
+        absolute_per_vector=sk == 0.0,
+        k=k, q=q, variant=variant, seed=seed,
+    )

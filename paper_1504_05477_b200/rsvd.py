@@ -27,6 +27,7 @@ import enum
 import math
 import os
 import time
+import warnings
 from dataclasses import dataclass, field
 
 from collections import OrderedDict
@@ -459,7 +460,9 @@ def _upload_into(buf, A):
             buf.copy_(src.to(device=buf.device, non_blocking=(not src.is_cuda) and src.is_pinned()))
     else:
         arr = as_dense_array(A) if not (isinstance(A, np.ndarray) and A.dtype == np.float32) else np.asarray(A)
-        buf.copy_(torch.from_numpy(np.ascontiguousarray(arr)))
+        with warnings.catch_warnings():  # read-only source (DenseMatrix data): only read by the copy
+            warnings.simplefilter("ignore", UserWarning)
+            buf.copy_(torch.from_numpy(np.ascontiguousarray(arr)))
     # one pass, no temporaries: FP64 column sums are finite iff every entry is
     # (an FP32 column cannot overflow an FP64 sum; for FP64 input a sum could
     # only overflow with entries near 1e308)

@@ -270,3 +270,18 @@ def test_gpu_metrics_match_oracle(rk):
     # FP32 path: FP32 A, same Z -> within FP32 tolerance
     cap32 = rk.metrics.captured_variance(A.astype(np.float32), Z)
     assert np.max(np.abs(cap32 - cap) / cap) < 1e-5
+
+
+def test_sweep_harness_matches_reference(rk):
+    """Row f4: the GPU sweep harness (device factorization + device error
+    report + device oracle spectrum) against the reference's own
+    run_experiment rows on the same synthetic spec (tests/golden/
+    sweep_golden.json, made by make_sweep_golden.py)."""
+    g = json.load(open(os.path.join(GOLDEN, "sweep_golden.json")))
+    rows, summary = rk.run_experiment(rk.ExperimentSpec.from_dict(g["spec"]))
+    assert np.max(np.abs(np.array(summary["oracle_top_singular_values"]) - g["oracle_top"])) < 1e-12
+    assert [(r["algo"], r["q"], r["seed"]) for r in rows] == [(r["algo"], r["q"], r["seed"]) for r in g["rows"]]
+    for r, ref in zip(rows, g["rows"]):
+        for m in ("frob_ratio", "spectral_ratio", "per_vector_max"):
+            assert abs(r[m] - ref[m]) <= 1e-7 * max(1.0, abs(ref[m])), (r, ref, m)
+    assert rk.rows_to_csv(rows).split("\n")[0] == g["csv_header"]
