@@ -30,13 +30,42 @@ __global__ void k_colreduce_partial(int64_t n, int64_t p, const T* __restrict__ 
     }
 }
 
+// Warp per column: lane l sums partials l, l + 32, ... then a fixed xor tree
+// (deterministic; the chunk count is ~600 at p = 50, which one thread per
+// column summed serially in ~25 us).
 __global__ void k_colreduce_final(int64_t p, int64_t chunks, const double* __restrict__ ws,
                                   double* __restrict__ out) {
-    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (c >= p) return;
     double s = 0.0;
-    for (int64_t i = 0; i < chunks; ++i) s += ws[i * p + c];
-    out[c] = s;
+    for (int64_t i = lane; i < chunks; i += 32) s += ws[i * p + c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[c] = s;
+}
+
+// (|x|, index) candidate order of the argmax reductions: larger |x| wins, the
+// smaller row index on ties (numpy argmax semantics); INT64_MAX marks none.
+struct AbsArg {
+    double v, x;
+    int64_t i;
+};
+
+__device__ __forceinline__ void absarg_take(AbsArg& a, double x, int64_t ix) {
+    if (ix == INT64_MAX) return;
+    const double v = fabs(x);
+    if (v > a.v || (v == a.v && ix < a.i)) a = {v, x, ix};
+}
+
+__device__ __forceinline__ AbsArg absarg_warp(AbsArg a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        AbsArg b{__shfl_xor_sync(0xffffffffu, a.v, o), __shfl_xor_sync(0xffffffffu, a.x, o),
+                 (int64_t)__shfl_xor_sync(0xffffffffu, (long long)a.i, o)};
+        if (b.v > a.v || (b.v == a.v && b.i < a.i)) a = b;
+    }
+    return a;
 }
 
 int64_t col_chunks(int64_t n, int64_t p) {
@@ -93,22 +122,13 @@ __global__ void k_absargmax_partial(int64_t n, int64_t k, const T* __restrict__ 
 
 __global__ void k_sign_decide(int64_t k, int64_t chunks, const double* __restrict__ wv,
                               const int64_t* __restrict__ wi, int32_t* __restrict__ flip) {
-    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (c >= k) return;
-    double best = -1.0, bsig = 0.0;
-    int64_t bi = INT64_MAX;
-    for (int64_t i = 0; i < chunks; ++i) {
-        double x = wv[i * k + c];
-        double v = fabs(x);
-        int64_t ix = wi[i * k + c];
-        if (ix == INT64_MAX) continue;
-        if (v > best || (v == best && ix < bi)) {
-            best = v;
-            bsig = x;
-            bi = ix;
-        }
-    }
-    flip[c] = bsig < 0.0;
+    AbsArg a{-1.0, 0.0, INT64_MAX};
+    for (int64_t i = lane; i < chunks; i += 32) absarg_take(a, wv[i * k + c], wi[i * k + c]);
+    a = absarg_warp(a);
+    if (lane == 0) flip[c] = a.x < 0.0;
 }
 
 template <typename T>
@@ -123,23 +143,16 @@ __global__ void k_sign_flip(int64_t n, int64_t k, T* __restrict__ X, int64_t ldx
 __global__ void k_absargmax_final(int64_t k, int64_t chunks, const double* __restrict__ wv,
                                   const int64_t* __restrict__ wi, int64_t row_offset,
                                   double* __restrict__ out_val, int64_t* __restrict__ out_idx) {
-    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (c >= k) return;
-    double best = -1.0, bsig = 0.0;
-    int64_t bi = INT64_MAX;
-    for (int64_t i = 0; i < chunks; ++i) {
-        double x = wv[i * k + c];
-        int64_t ix = wi[i * k + c];
-        if (ix == INT64_MAX) continue;
-        double v = fabs(x);
-        if (v > best || (v == best && ix < bi)) {
-            best = v;
-            bsig = x;
-            bi = ix;
-        }
+    AbsArg a{-1.0, 0.0, INT64_MAX};
+    for (int64_t i = lane; i < chunks; i += 32) absarg_take(a, wv[i * k + c], wi[i * k + c]);
+    a = absarg_warp(a);
+    if (lane == 0) {
+        out_val[c] = a.x;
+        out_idx[c] = a.i == INT64_MAX ? INT64_MAX : a.i + row_offset;
     }
-    out_val[c] = bsig;
-    out_idx[c] = bi == INT64_MAX ? INT64_MAX : bi + row_offset;
 }
 
 template <typename T>
@@ -288,7 +301,7 @@ int colreduce(int dtype, int square, int64_t n, int64_t p, const void* X, int64_
         k_colreduce_partial<float><<<grid, 32 * kColRows, 0, st>>>(n, p, (const float*)X, ldx,
                                                                   square, rpc, (double*)ws);
     RSVD_CHECK_LAUNCH();
-    k_colreduce_final<<<(unsigned)cdiv(p, 128), 128, 0, st>>>(p, ch, (const double*)ws, out);
+    k_colreduce_final<<<(unsigned)cdiv(p * 32, 256), 256, 0, st>>>(p, ch, (const double*)ws, out);
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }
@@ -312,7 +325,7 @@ int canonicalize_signs(int dtype, int64_t n, int64_t k, void* X, int64_t ldx, vo
         k_absargmax_partial<float><<<grid, 32 * kColRows, 0, st>>>(n, k, (const float*)X, ldx, rpc,
                                                                   wv, wi);
     RSVD_CHECK_LAUNCH();
-    k_sign_decide<<<(unsigned)cdiv(k, 128), 128, 0, st>>>(k, ch, wv, wi, flip);
+    k_sign_decide<<<(unsigned)cdiv(k * 32, 256), 256, 0, st>>>(k, ch, wv, wi, flip);
     RSVD_CHECK_LAUNCH();
     if (dtype == RSVD_F64)
         k_sign_flip<double><<<nb, 256, 0, st>>>(n, k, (double*)X, ldx, flip);
@@ -339,7 +352,7 @@ int col_absargmax(int dtype, int64_t n, int64_t k, const void* X, int64_t ldx, i
         k_absargmax_partial<float><<<grid, 32 * kColRows, 0, st>>>(n, k, (const float*)X, ldx, rpc,
                                                                   wv, wi);
     RSVD_CHECK_LAUNCH();
-    k_absargmax_final<<<(unsigned)cdiv(k, 128), 128, 0, st>>>(k, ch, wv, wi, row_offset, out_val,
+    k_absargmax_final<<<(unsigned)cdiv(k * 32, 256), 256, 0, st>>>(k, ch, wv, wi, row_offset, out_val,
                                                               out_idx);
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
