@@ -880,6 +880,19 @@ struct Scratch {
     size_t bytes = 0;
 };
 
+// Grow-only scratch. A superseded buffer is never freed: a CUDA graph captured
+// earlier (GraphedFactorization, the public API's graph cache) holds its
+// address, and a later, larger product must not free it under the graph.
+float* scratch_get(Scratch& sc, size_t need, cudaStream_t st) {
+    if (sc.bytes < need) {
+        void* p = nullptr;
+        if (cudaMallocAsync(&p, need, st) != cudaSuccess) return nullptr;
+        sc.ptr = p;  // the previous buffer stays allocated (see above)
+        sc.bytes = need;
+    }
+    return (float*)sc.ptr;
+}
+
 int split_b(const float* B, int64_t K, int64_t N, int64_t ldb, int64_t Kp, int64_t Np, float* out,
             const int32_t* pred, cudaStream_t st) {
     dim3 grid((unsigned)(Kp / 32), (unsigned)(Np / 32));
@@ -913,6 +926,7 @@ int64_t tn_splits_tc(int64_t Mop, int64_t Nop, int64_t Kop) {
     return best;
 }
 
+
 }  // namespace
 
 bool gemm_tc_nn_supported(int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_t ldc, const void* A,
@@ -931,13 +945,8 @@ int gemm_nn_tc(int64_t m, int64_t n, int64_t k, double alpha, const float* A, in
     // columns >= n, which are never stored
     const int64_t Kp = cdiv(k, BK) * BK, Np = cdiv(n, 32) * 32;
     static thread_local Scratch sc;  // split-B buffer
-    size_t need = (size_t)(2 * Kp * Np * 4);
-    if (sc.bytes < need) {
-        if (sc.ptr) cudaFreeAsync(sc.ptr, st);
-        RSVD_CHECK_CUDA(cudaMallocAsync(&sc.ptr, need, st));
-        sc.bytes = need;
-    }
-    float* bs = (float*)sc.ptr;
+    float* bs = scratch_get(sc, (size_t)(2 * Kp * Np * 4), st);
+    RSVD_REQUIRE(bs != nullptr, "gemm_nn_tc: scratch allocation failed");
     int rc = split_b(B, k, n, ldb, Kp, Np, bs, pred, st);
     if (rc) return rc;
     CUtensorMap tA, tB;
@@ -951,6 +960,8 @@ int gemm_nn_tc(int64_t m, int64_t n, int64_t k, double alpha, const float* A, in
     p.plain_vec = alpha == 1.0 && beta == 0.0 && row_sub == nullptr && ldc % 4 == 0 && aligned16(C);
     p.pred = pred;
     p.n_tiles = (int)cdiv(n, bn);
+    // (a split-K variant for wave balance -- C2: 391 tiles = 2.64 waves -- was
+    // measured no faster: 2 / 3 / 4 splits 0.452 / 0.443 / 0.454 ms vs 0.441)
     dim3 grid((unsigned)(cdiv(m, BM) * p.n_tiles), 1, 1);
     return dispatch_bn<false>(bn, tA, tB, p, grid, st);
 }
@@ -978,13 +989,8 @@ int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, con
     RSVD_REQUIRE(aligned16(ws), "gemm_tn_tc: workspace must be 16-byte aligned");
     const int64_t Kp = cdiv(Kop, BK) * BK, Np = cdiv(Nop, 32) * 32;  // see gemm_nn_tc
     static thread_local Scratch sc;
-    size_t need = (size_t)(2 * Kp * Np * 4);
-    if (sc.bytes < need) {
-        if (sc.ptr) cudaFreeAsync(sc.ptr, st);
-        RSVD_CHECK_CUDA(cudaMallocAsync(&sc.ptr, need, st));
-        sc.bytes = need;
-    }
-    float* bs = (float*)sc.ptr;
+    float* bs = scratch_get(sc, (size_t)(2 * Kp * Np * 4), st);
+    RSVD_REQUIRE(bs != nullptr, "gemm_tn_tc: scratch allocation failed");
     int rc = split_b(B, Kop, Nop, ldb, Kp, Np, bs, pred, st);
     if (rc) return rc;
     CUtensorMap tA, tB;
