@@ -147,7 +147,51 @@ __global__ void __launch_bounds__(kTriThreads) k_tridiag(TriState s) {
 constexpr int kClTri = 16;
 constexpr int kClTriThreads = 512;
 constexpr int kClTriMaxW = 608;
+constexpr int kClRegs = (kClTriMaxW + 31) / 32;  // u / q entries per lane
 
+// Householder vector of row j (entries j+1 .. w-1 of the current row, `rowj`
+// points at entry j+1; m = w - j - 1) into u, scalars (beta, alpha, skip) into
+// sc, and the step's d / e / beta / Uh outputs. Whole CTA (two block sums).
+__device__ void cl_householder(TriState& s, int j, int m, const double* rowj, double dj, double* u, double* sc,
+                               double* red) {
+    const int tid = threadIdx.x, w = (int)s.w;
+    double ss = 0.0, tail = 0.0;
+    for (int i = tid; i < m; i += kClTriThreads) {
+        const double x = rowj[i];
+        u[i] = x;
+        ss += x * x;
+        if (i > 0) tail += x * x;
+    }
+    ss = block_sum(ss, red);
+    tail = block_sum(tail, red);
+    const double x0 = u[0];
+    const bool skip = !(tail > 0.0);
+    double alpha = x0, beta = 0.0;
+    if (!skip) {
+        const double nrm = sqrt(ss);
+        alpha = x0 >= 0.0 ? -nrm : nrm;
+        const double u0 = x0 - alpha;
+        beta = 2.0 / (tail + u0 * u0);
+        __syncthreads();
+        if (tid == 0) u[0] = u0;
+    }
+    if (tid == 0) {
+        sc[0] = beta;
+        sc[1] = alpha;
+        sc[2] = skip ? 1.0 : 0.0;
+        s.d[j] = dj;
+        s.e[j] = alpha;
+        s.beta[j] = beta;
+    }
+    __syncthreads();
+    double* uh = s.Uh + (size_t)j * w;
+    for (int i = tid; i < w; i += kClTriThreads) uh[i] = (i > j && !skip) ? u[i - j - 1] : 0.0;
+}
+
+// Look-ahead: the owner of row j+1 applies column j's rank-2 update to that
+// row first and computes the next Householder vector while the other CTAs
+// are still updating their rows, so step j+1 starts with u already in place
+// (one Householder computation off the per-column critical path).
 __global__ void __launch_bounds__(kClTriThreads, 1) k_tridiag_cluster(TriState s) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
@@ -166,65 +210,47 @@ __global__ void __launch_bounds__(kClTriThreads, 1) k_tridiag_cluster(TriState s
         const int r = rank + kClTri * lr;
         for (int c = tid; c < w; c += kClTriThreads) Aloc[(size_t)lr * w + c] = r < w ? s.A[(size_t)r * w + c] : 0.0;
     }
-    cluster.sync();
+    __syncthreads();
+    if (w > 2 && rank == 0)  // step 0's vector (row 0 lives in CTA 0)
+        cl_householder(s, 0, w - 1, Aloc + 1, Aloc[0], ubuf, &scal[0][0], red);
     for (int j = 0; j + 2 < w; ++j) {
         const int par = j & 1;
         const int m = w - j - 1;
         double* u = ubuf + par * w;      // u[0..m): entries for columns j+1 ..
         double* pp = pbuf + par * w;
         const int owner = j % kClTri;
-        if (rank == owner) {
-            const double* rowj = Aloc + (size_t)(j / kClTri) * w + (j + 1);
-            double ss = 0.0, tail = 0.0;
-            for (int i = tid; i < m; i += kClTriThreads) {
-                const double x = rowj[i];
-                u[i] = x;
-                ss += x * x;
-                if (i > 0) tail += x * x;
-            }
-            ss = block_sum(ss, red);
-            tail = block_sum(tail, red);
-            const double x0 = u[0];
-            const bool skip = !(tail > 0.0);
-            double alpha = x0, beta = 0.0;
-            if (!skip) {
-                const double nrm = sqrt(ss);
-                alpha = x0 >= 0.0 ? -nrm : nrm;
-                const double u0 = x0 - alpha;
-                beta = 2.0 / (tail + u0 * u0);
-                __syncthreads();
-                if (tid == 0) u[0] = u0;
-            }
-            if (tid == 0) {
-                scal[par][0] = beta;
-                scal[par][1] = alpha;
-                scal[par][2] = skip ? 1.0 : 0.0;
-                s.d[j] = Aloc[(size_t)(j / kClTri) * w + j];
-                s.e[j] = alpha;
-                s.beta[j] = beta;
-            }
-            __syncthreads();
-            double* uh = s.Uh + (size_t)j * w;
-            for (int i = tid; i < w; i += kClTriThreads) uh[i] = (i > j && !skip) ? u[i - j - 1] : 0.0;
-        }
+        const int nxt = (j + 1) % kClTri;                 // owner of row j+1
+        const bool look = j + 3 < w && rank == nxt;       // computes step j+1's vector here
+        double* un = ubuf + (par ^ 1) * w;
+        double* rown = Aloc + (size_t)((j + 1) / kClTri) * w + (j + 1);  // row j+1 from column j+1 (nxt only)
         cluster.sync();
         // fetch u and the scalars from the owner (DSMEM)
         const double* uo = cluster.map_shared_rank(u, owner);
         const double* so = cluster.map_shared_rank(&scal[par][0], owner);
         const double beta = so[0];
         const bool skip = so[2] != 0.0;
-        if (skip) continue;  // uniform: every CTA read the same flag
+        if (skip) {  // uniform: row j is already reduced; row j+1 is unchanged
+            if (look) cl_householder(s, j + 1, m - 1, rown + 1, rown[0], un, &scal[par ^ 1][0], red);
+            continue;
+        }
         if (rank != owner)
             for (int i = tid; i < m; i += kClTriThreads) u[i] = uo[i];
         __syncthreads();
-        // p_r = beta * A22[r, :] . u for this CTA's trailing rows (warp per row)
+        // p_r = beta * A22[r, :] . u for this CTA's trailing rows (warp per row);
+        // lane l touches columns l + 32 i of every row, so its u entries stay in
+        // registers (one shared-memory read per matrix element instead of two)
         const int lr0 = (j + 1 - rank + kClTri - 1) / kClTri;  // first local row with global r > j
+        double ureg[kClRegs];
+#pragma unroll
+        for (int i = 0; i < kClRegs; ++i) ureg[i] = lane + 32 * i < m ? u[lane + 32 * i] : 0.0;
         for (int lr = lr0 + warp; lr < nloc; lr += nw) {
             const int r = rank + kClTri * lr;
             if (r >= w) break;
             const double* ar = Aloc + (size_t)lr * w + (j + 1);
             double acc = 0.0;
-            for (int c = lane; c < m; c += 32) acc = fma(ar[c], u[c], acc);
+#pragma unroll
+            for (int i = 0; i < kClRegs; ++i)
+                if (lane + 32 * i < m) acc = fma(ar[lane + 32 * i], ureg[i], acc);
             acc = warp_sum(acc);
             if (lane == 0) pp[r] = beta * acc;
         }
@@ -241,13 +267,25 @@ __global__ void __launch_bounds__(kClTriThreads, 1) k_tridiag_cluster(TriState s
         kk = 0.5 * beta * block_sum(kk, red);
         for (int i = tid; i < m; i += kClTriThreads) q[i] -= kk * u[i];
         __syncthreads();
+        if (look) {  // row j+1 first (ir = 0), then its Householder vector
+            const double u0 = u[0], q0 = q[0];
+            for (int c = tid; c < m; c += kClTriThreads) rown[c] -= u0 * q[c] + q0 * u[c];
+            __syncthreads();
+            cl_householder(s, j + 1, m - 1, rown + 1, rown[0], un, &scal[par ^ 1][0], red);
+        }
+        double qreg[kClRegs];
+#pragma unroll
+        for (int i = 0; i < kClRegs; ++i) qreg[i] = lane + 32 * i < m ? q[lane + 32 * i] : 0.0;
         for (int lr = lr0 + warp; lr < nloc; lr += nw) {
             const int r = rank + kClTri * lr;
             if (r >= w) break;
+            if (look && r == j + 1) continue;  // done above
             double* ar = Aloc + (size_t)lr * w + (j + 1);
             const int ir = r - j - 1;
             const double ur = u[ir], qr = q[ir];
-            for (int c = lane; c < m; c += 32) ar[c] -= ur * q[c] + qr * u[c];
+#pragma unroll
+            for (int i = 0; i < kClRegs; ++i)
+                if (lane + 32 * i < m) ar[lane + 32 * i] -= ur * qreg[i] + qr * ureg[i];
         }
         __syncthreads();
     }
