@@ -355,13 +355,22 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # RSVD_DIST_BACKEND=gloo (with --graph 0) exercises the N > 1 path on a box
+    # with fewer GPUs than ranks: ranks share devices round-robin and the
+    # collectives run through gloo on the host (no kernel waits on another rank)
+    backend = os.environ.get("RSVD_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     cfgd = CONFIGS[args.config]
     n, d, k = cfgd["n"], cfgd["d"], cfgd["k"]
     cfg = rk.RsvdConfig(k=k, variant=cfgd["variant"], q=cfgd["q"], seed=0)
@@ -424,6 +433,21 @@ def run_ours(args):
             return graphed.run(Pi_dev)
         return rsvd.run_device(op, cfg, comm=comm, Pi=Pi_dev)
 
+    if graphed is not None and world > 1:
+        # capture the sharded factorization (its allreduces included) once up
+        # front; should the process group refuse capture, every rank falls
+        # back to eager launches together (the outcome is agreed by a MIN)
+        ok = 1
+        try:
+            graphed.run(Pi_dev)
+            torch.cuda.synchronize()
+        except Exception as exc:  # noqa: BLE001 - reported, then eager
+            print(f"rank {rank}: graph capture failed ({exc!r}); running eager", file=sys.stderr, flush=True)
+            ok = 0
+        flag = torch.tensor([ok], device=dev if backend == "nccl" else "cpu")
+        torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            graphed = None
     for _ in range(args.warmup):
         df = step()
     torch.cuda.synchronize()
@@ -438,8 +462,8 @@ def run_ours(args):
         return
     # kernels per factorization, counted on an eager replica of the step (a
     # graph replay issues the identical kernel sequence in one launch)
-    launches = (count_launches(lambda: rsvd.run_device(op, cfg, comm=comm, Pi=Pi))
-                if rank == 0 and args.count_launches else None)
+    # (every rank runs it: the factorization's collectives need all ranks)
+    launches = count_launches(lambda: rsvd.run_device(op, cfg, comm=comm, Pi=Pi)) if args.count_launches else None
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -460,7 +484,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device=dev if backend == "nccl" else "cpu")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     info = df.info.cpu().numpy()

@@ -73,9 +73,16 @@ class TorchComm:
         self.rank = dist.get_rank(group)
         self.n_total = n_total
         self.row_offset = row_offset
+        # gloo with CUDA tensors (the CPU tests; bench.py's RSVD_DIST_BACKEND=gloo
+        # check of the N > 1 path on one GPU): stage through host memory
+        self.host_staged = dist.get_backend(group) == "gloo"
 
     def allreduce(self, t):
-        if t.is_contiguous():
+        if self.host_staged and t.is_cuda:
+            tmp = t.cpu()
+            self.dist.all_reduce(tmp, group=self.group)
+            t.copy_(tmp)
+        elif t.is_contiguous():
             self.dist.all_reduce(t, group=self.group)
         else:  # padded row buffers (krylov.rows_buffer)
             tmp = t.contiguous()
@@ -84,6 +91,11 @@ class TorchComm:
         return t
 
     def all_gather(self, t):
+        if self.host_staged and t.is_cuda:
+            src = t.cpu()
+            out = [torch.empty_like(src) for _ in range(self.world)]
+            self.dist.all_gather(out, src, group=self.group)
+            return [o.to(t.device) for o in out]
         out = [torch.empty_like(t) for _ in range(self.world)]
         self.dist.all_gather(out, t, group=self.group)
         return out
