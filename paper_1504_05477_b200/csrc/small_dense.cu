@@ -582,7 +582,8 @@ int chol_deflate(int64_t p, const double* G, int64_t ldg, const double* ref2, do
                  int64_t ldt, int32_t* mask, int32_t* ndef, int32_t* running, const int32_t* active, void* ws,
                  int64_t ws_bytes, const int32_t* pred, cudaStream_t st) {
     if (p == 0) return RSVD_OK;
-    if (p <= kRegP) {
+    static const bool force_sweep = getenv("RSVD_CHOL_SWEEP") != nullptr;  // A/B experiments
+    if (p <= kRegP && !force_sweep) {
         k_chol_reg64<<<1, kRegP, 0, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active, pred);
         RSVD_CHECK_LAUNCH();
         return RSVD_OK;
