@@ -543,7 +543,6 @@ __global__ void k_invit(int64_t w, int64_t k, const double* __restrict__ d, cons
 // rows stream through shared memory in blocks of kBtRows rows, double
 // buffered with cp.async, so the L2 latency is paid once per block and each
 // row is read once per CTA instead of once per vector.
-constexpr int kBtVec = 8;
 constexpr int kBtChunks = 64;  // w <= 2048
 constexpr int kBtRows = 8;
 
@@ -553,12 +552,17 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
                  : "memory");
 }
 
-__global__ void __launch_bounds__(32 * kBtVec)
+// NC = register chunks per lane (w <= 32 NC, instantiated per width class so
+// the unrolled loops carry no dead predicated chunks), VPB = vectors (warps)
+// per CTA (small k: fewer vectors per CTA, more CTAs).
+template <int NC, int VPB>
+__global__ void __launch_bounds__(32 * VPB)
 k_backtransform(int64_t w, int64_t k, const double* __restrict__ Uh, const double* __restrict__ beta,
                 const double* __restrict__ X, double* __restrict__ evecs, int64_t lde) {
+    constexpr int kBtChunks = NC;
     extern __shared__ __align__(16) double ubuf[];  // [2][kBtRows][wp]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t v = (int64_t)blockIdx.x * kBtVec + warp;
+    const int64_t v = (int64_t)blockIdx.x * VPB + warp;
     const int nc = (int)((w + 31) / 32);
     const int64_t wp = (w + 1) & ~int64_t(1);  // rows padded to 16 bytes
     double x[kBtChunks];
@@ -746,11 +750,21 @@ int syev_topk(int64_t w, const double* M, int64_t ldm, int64_t k, double* evals,
     RSVD_REQUIRE(w <= 32 * kBtChunks, "syev_topk: w > %d", 32 * kBtChunks);
     {
         const size_t bsm = (size_t)(2 * kBtRows * ((w + 1) & ~int64_t(1))) * sizeof(double);
-        if (bsm > 48 * 1024)
-            RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_backtransform, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
-        k_backtransform<<<(unsigned)cdiv(k, kBtVec), 32 * kBtVec, bsm, st>>>(w, k, s.Uh, s.beta, X, evecs, lde);
+        // one vector per CTA below 300 vectors (k = 50: 50 CTAs instead of 7)
+        const int vpb = k >= 300 ? 4 : 1;
+        auto launch = [&](auto kern, int vp) -> int {
+            if (bsm > 48 * 1024)
+                RSVD_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+            kern<<<(unsigned)cdiv(k, vp), 32 * vp, bsm, st>>>(w, k, s.Uh, s.beta, X, evecs, lde);
+            RSVD_CHECK_LAUNCH();
+            return RSVD_OK;
+        };
+#define RSVD_BT(NC)                                                                                    \
+        if (w <= 32 * NC)                                                                              \
+            return vpb == 1 ? launch(k_backtransform<NC, 1>, 1) : launch(k_backtransform<NC, 4>, 4);
+        RSVD_BT(8) RSVD_BT(16) RSVD_BT(20) RSVD_BT(24) RSVD_BT(32) RSVD_BT(40) RSVD_BT(52) RSVD_BT(64)
+#undef RSVD_BT
     }
-    RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }
 
