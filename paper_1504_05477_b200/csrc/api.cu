@@ -2,6 +2,7 @@
 // kernel dispatch. No entry point synchronises the stream.
 #include "common.cuh"
 #include "gemm.cuh"
+#include <stdlib.h>
 
 namespace rsvd {
 // small_dense.cu
@@ -58,6 +59,17 @@ using namespace rsvd;
 
 static bool valid_dtype(int d) { return d == RSVD_F32 || d == RSVD_F64; }
 
+// FP64 products default to the DMMA kernels; RSVD_DISABLE_DMMA=1 selects the
+// CUDA-core FP64 kernels (A/B measurement switch).
+static bool dmma_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("RSVD_DISABLE_DMMA");
+        on = (e && e[0] == '1') ? 0 : 1;
+    }
+    return on == 1;
+}
+
 extern "C" {
 
 int rsvd_gemm_nn(int dtype, int64_t m, int64_t n, int64_t k, double alpha, const void* A,
@@ -81,11 +93,20 @@ int rsvd_gemm_nn(int dtype, int64_t m, int64_t n, int64_t k, double alpha, const
         return gemm_nn_tc(m, n, k, alpha, (const float*)A, lda, (const float*)B, ldb, beta,
                           (float*)C, ldc, row_sub, pred, st);
     }
+    if (algo == RSVD_GEMM_DMMA || (algo == RSVD_GEMM_AUTO && dtype == RSVD_F64 && dmma_enabled())) {
+        RSVD_REQUIRE(dtype == RSVD_F64, "gemm_nn: DMMA path is FP64 only");
+        return gemm_nn_dmma(m, n, k, alpha, (const double*)A, lda, (const double*)B, ldb, beta,
+                            (double*)C, ldc, row_sub, pred, st);
+    }
     return gemm_nn_simt(dtype, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, row_sub, pred, st);
 }
 
 int64_t rsvd_gemm_tn_ws_bytes(int dtype, int64_t m, int64_t n, int64_t k, int algo) {
     int64_t a = gemm_tn_simt_ws_bytes(m, n, k);
+    if (dtype == RSVD_F64 && algo != RSVD_GEMM_SIMT) {
+        int64_t b = gemm_tn_dmma_ws_bytes(m, n, k);
+        if (b > a) a = b;
+    }
     if (dtype == RSVD_F32 && algo != RSVD_GEMM_SIMT) {
         int64_t b = gemm_tn_tc_ws_bytes(m, n, k);
         if (b > a) a = b;
@@ -119,6 +140,11 @@ int rsvd_gemm_tn(int dtype, int out_dtype, int64_t m, int64_t n, int64_t k, doub
                      "gemm_tn: shape/alignment not supported by the tcgen05 kernel");
         return gemm_tn_tc(out_dtype, m, n, k, alpha, (const float*)A, lda, (const float*)B, ldb,
                           beta, C, ldc, mu, colsum_b, ws, ws_bytes, pred, st);
+    }
+    if (algo == RSVD_GEMM_DMMA || (algo == RSVD_GEMM_AUTO && dtype == RSVD_F64 && dmma_enabled())) {
+        RSVD_REQUIRE(dtype == RSVD_F64, "gemm_tn: DMMA path is FP64 only");
+        return gemm_tn_dmma(out_dtype, m, n, k, alpha, (const double*)A, lda, (const double*)B, ldb,
+                            beta, C, ldc, mu, colsum_b, ws, ws_bytes, pred, st);
     }
     return gemm_tn_simt(dtype, out_dtype, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, mu,
                         colsum_b, ws, ws_bytes, pred, st);

@@ -31,6 +31,16 @@ int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, con
                const double* mu, const double* cs, void* ws, int64_t ws_bytes, const int32_t* pred,
                cudaStream_t st);
 
+// FP64 tensor-core (mma.sync f64) kernels (gemm_dmma.cu).
+int gemm_nn_dmma(int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda,
+                 const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                 const double* row_sub, const int32_t* pred, cudaStream_t st);
+int64_t gemm_tn_dmma_ws_bytes(int64_t m, int64_t n, int64_t k);
+int gemm_tn_dmma(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+                 int64_t lda, const double* B, int64_t ldb, double beta, void* C, int64_t ldc,
+                 const double* mu, const double* cs, void* ws, int64_t ws_bytes, const int32_t* pred,
+                 cudaStream_t st);
+
 // FP32 CUDA-core kernels for outputs <= 64 columns wide (skinny.cu).
 bool gemm_skinny_nn_supported(int64_t n, int64_t k);
 bool gemm_skinny_tn_supported(int64_t n, int64_t k);
