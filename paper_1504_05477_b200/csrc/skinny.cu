@@ -11,6 +11,7 @@
 // FP64 accumulators and writes FP64 split partials that k_skinny_reduce sums
 // in a fixed order (deterministic, no atomics).
 #include "gemm.cuh"
+#include <stdlib.h>
 
 namespace rsvd {
 
@@ -91,6 +92,94 @@ k_skinny_nn(int64_t m, int n, int k, double alpha, const float* __restrict__ A, 
             if (beta != 0.0) r += beta * (double)C[row * ldc + c];
             C[row * ldc + c] = (float)r;
         }
+    }
+}
+
+// NN (v2): 256 threads, 128 rows per CTA. The CTA stages B (k x 64, zero
+// columns past n) and its 128 x k slab of A in shared memory (16-byte loads
+// when A's rows are 16-byte aligned, as rows_buffer guarantees; pitch k + 1
+// so the 4 rows a warp reads per step fall in distinct banks); thread
+// (tx, ty) owns rows 4 ty .. 4 ty + 3 and columns 8 tx .. 8 tx + 7. The
+// results go back through shared memory so the epilogue (row_sub, alpha,
+// beta C) reads and writes C row-contiguously.
+constexpr int kNn2Threads = 256, kNn2Rows = 128, kNn2CPitch = 65;
+
+__host__ __device__ constexpr int nn2_a_floats(int k) {
+    return kNn2Rows * (k + 1) > kNn2Rows * kNn2CPitch ? kNn2Rows * (k + 1) : kNn2Rows * kNn2CPitch;
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kNn2Threads, 3)
+k_skinny_nn2(int64_t m, int n, int k, double alpha, const float* __restrict__ A, int64_t lda,
+             const float* __restrict__ B, int64_t ldb, double beta, float* __restrict__ C, int64_t ldc,
+             const double* __restrict__ row_sub, const int32_t* __restrict__ pred) {
+    if (pred_off(pred)) return;
+    extern __shared__ __align__(16) float sm2[];
+    float* Bs = sm2;              // k x 64
+    float* As = sm2 + k * 64;     // 128 x (k + 1), later the 128 x 65 result tile
+    const int t = threadIdx.x;
+    const int64_t r0 = (int64_t)blockIdx.x * kNn2Rows;
+    const int PA = k + 1;
+    if (VEC) {
+        const int k4 = (k + 3) / 4;
+#pragma unroll 4
+        for (int idx = t; idx < kNn2Rows * k4; idx += kNn2Threads) {
+            const int r = idx / k4, c = 4 * (idx % k4);
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (r0 + r < m) v = __ldg(reinterpret_cast<const float4*>(A + (r0 + r) * lda + c));
+            float* d = As + r * PA + c;
+            d[0] = v.x;
+            if (c + 1 < k) d[1] = v.y;
+            if (c + 2 < k) d[2] = v.z;
+            if (c + 3 < k) d[3] = v.w;
+        }
+    } else {
+#pragma unroll 4
+        for (int idx = t; idx < kNn2Rows * k; idx += kNn2Threads) {
+            const int r = idx / k, c = idx % k;
+            As[r * PA + c] = (r0 + r < m) ? __ldg(A + (r0 + r) * lda + c) : 0.f;
+        }
+    }
+    for (int idx = t; idx < k * 64; idx += kNn2Threads) {
+        const int kk = idx / 64, c = idx % 64;
+        Bs[idx] = c < n ? __ldg(B + (int64_t)kk * ldb + c) : 0.f;
+    }
+    __syncthreads();
+    const int tx = t % 8, ty = t / 8;
+    float acc[4][8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    const float* a_row = As + 4 * ty * PA;
+#pragma unroll 2
+    for (int kk = 0; kk < k; ++kk) {
+        const float4 b0 = *reinterpret_cast<const float4*>(Bs + kk * 64 + 8 * tx);
+        const float4 b1 = *reinterpret_cast<const float4*>(Bs + kk * 64 + 8 * tx + 4);
+        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float a = a_row[i * PA + kk];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a, bv[j], acc[i][j]);
+        }
+    }
+    __syncthreads();  // As is reused for the result tile
+    float* Cs = As;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) Cs[(4 * ty + i) * kNn2CPitch + 8 * tx + j] = acc[i][j];
+    __syncthreads();
+    const int rows = (int)min((int64_t)kNn2Rows, m - r0);
+    for (int idx = t; idx < rows * n; idx += kNn2Threads) {
+        const int r = idx / n, c = idx % n;
+        double v = (double)Cs[r * kNn2CPitch + c];
+        if (row_sub) v -= row_sub[c];
+        v *= alpha;
+        float* out = C + (r0 + r) * ldc + c;
+        if (beta != 0.0) v += beta * (double)*out;
+        *out = (float)v;
     }
 }
 
@@ -217,8 +306,36 @@ int gemm_nn_skinny(int64_t m, int64_t n, int64_t k, double alpha, const float* A
                    cudaStream_t st) {
     RSVD_REQUIRE(n <= 64, "gemm_nn_skinny: n = %lld > 64", (long long)n);
     if (m == 0 || n == 0) return RSVD_OK;
-    k_skinny_nn<<<(unsigned)cdiv(m, kNnRows), kNnThreads, 0, st>>>(m, (int)n, (int)k, alpha, A, lda, B, ldb, beta,
-                                                                  C, ldc, row_sub, pred);
+    static const bool v1 = getenv("RSVD_SKINNY_NN_V1") != nullptr;  // A/B switch
+    if (v1 || k > 128) {
+        k_skinny_nn<<<(unsigned)cdiv(m, kNnRows), kNnThreads, 0, st>>>(m, (int)n, (int)k, alpha, A, lda, B, ldb,
+                                                                      beta, C, ldc, row_sub, pred);
+        RSVD_CHECK_LAUNCH();
+        return RSVD_OK;
+    }
+    const int kk = k < 1 ? 1 : (int)k;
+    const size_t smem = (size_t)(kk * 64 + nn2_a_floats(kk)) * sizeof(float);
+    const bool vec = lda % 4 == 0 && ((uintptr_t)A % 16) == 0;
+    const unsigned grid = (unsigned)cdiv(m, kNn2Rows);
+    if (vec) {
+        static bool attr = false;
+        if (!attr) {
+            RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_skinny_nn2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)(128 * 64 * 4 + nn2_a_floats(128) * 4)));
+            attr = true;
+        }
+        k_skinny_nn2<true><<<grid, kNn2Threads, smem, st>>>(m, (int)n, (int)k, alpha, A, lda, B, ldb, beta, C, ldc,
+                                                             row_sub, pred);
+    } else {
+        static bool attr = false;
+        if (!attr) {
+            RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_skinny_nn2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)(128 * 64 * 4 + nn2_a_floats(128) * 4)));
+            attr = true;
+        }
+        k_skinny_nn2<false><<<grid, kNn2Threads, smem, st>>>(m, (int)n, (int)k, alpha, A, lda, B, ldb, beta, C,
+                                                              ldc, row_sub, pred);
+    }
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }

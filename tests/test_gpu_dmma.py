@@ -104,3 +104,31 @@ def test_dmma_rejects_fp32(ops):
     A = torch.zeros((8, 8), dtype=torch.float32, device="cuda")
     with pytest.raises(ValueError):
         ops.gemm_nn(A, A, torch.zeros_like(A), algo=GEMM_DMMA)
+
+
+@pytest.mark.parametrize("m,n,k,pad", [(1, 1, 1, 0), (50000, 50, 50, 2), (777, 64, 128, 0), (300, 17, 33, 1),
+                                       (129, 50, 100, 0), (5000, 64, 3, 3)])
+def test_skinny_fp32_products(ops, m, n, k, pad):
+    """FP32 CUDA-core products of the orthonormalization (V R^-1, Grams):
+    NN with k <= 128 / n <= 64 and TN with k, n <= 64, against FP64 numpy."""
+    from paper_1504_05477_b200._lib import GEMM_SKINNY
+
+    a = _g((m, k), 51).astype(np.float32)
+    b = _g((k, n), 52).astype(np.float32)
+    c0 = _g((m, n), 53).astype(np.float32)
+    rs = _g((1, n), 54)[0]
+    buf = torch.zeros((m, k + pad), dtype=torch.float32, device="cuda")
+    buf[:, :k] = torch.from_numpy(a).cuda()
+    A = buf[:, :k]
+    C = torch.from_numpy(c0).cuda()
+    ops.gemm_nn(A, torch.from_numpy(b).cuda(), C, alpha=-1.0, beta=1.0, row_sub=torch.from_numpy(rs).cuda(),
+                algo=GEMM_SKINNY)
+    ref = -(a.astype(np.float64) @ b.astype(np.float64) - rs[None, :]) + c0
+    scale = np.abs(a).max() * np.abs(b).max() * k + np.abs(c0).max()
+    assert np.max(np.abs(C.cpu().numpy() - ref)) <= 4e-7 * scale
+    if k <= 64:
+        y = _g((m, n), 55).astype(np.float32)
+        G = torch.empty((k, n), dtype=torch.float64, device="cuda")
+        ops.gemm_tn(A, torch.from_numpy(y).cuda(), G, algo=GEMM_SKINNY)
+        ref = a.astype(np.float64).T @ y.astype(np.float64)
+        assert np.max(np.abs(G.cpu().numpy() - ref)) <= 1e-6 * max(1.0, np.abs(ref).max())

@@ -34,7 +34,7 @@ X = rows_buffer(n, p, torch.float32, "cuda"); X.copy_(torch.randn(n, p, generato
 Y = rows_buffer(n, p, torch.float32, "cuda")
 T = torch.randn(p, p, generator=g, device="cuda")
 G = torch.empty(p, p, dtype=torch.float64, device="cuda")
-for w in (0, 100, 550):
+for w in (0, 100, 300, 550):
     if w:
         Qp = rows_buffer(n, w, torch.float32, "cuda"); Qp.copy_(torch.randn(n, w, generator=g, device="cuda"))
         C = torch.empty(w, p, dtype=torch.float32, device="cuda")
