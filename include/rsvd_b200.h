@@ -46,7 +46,7 @@ extern "C" {
 #define RSVD_F64 1
 
 /* GEMM algorithm selector (rsvd_gemm_nn / rsvd_gemm_tn `algo`). */
-#define RSVD_GEMM_AUTO 0
+#define RSVD_GEMM_AUTO 0       /* FP32: 3xTF32 / skinny / SIMT by shape; FP64: DMMA */
 #define RSVD_GEMM_SIMT 1       /* CUDA-core FFMA/DFMA, FP32 or FP64 */
 #define RSVD_GEMM_TC_3XTF32 2  /* tcgen05 kind::tf32, hi/lo split, FP32 only */
 #define RSVD_GEMM_DMMA 3       /* mma.sync f64 (DMMA), FP64 only */

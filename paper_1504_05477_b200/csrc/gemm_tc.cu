@@ -738,24 +738,32 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 // then one contiguous 128 BN-byte run (a TN product streams B from HBM; the
 // row-major plane made every box 128-byte pieces 4 Kp bytes apart).
 // Transposes through a 32 x 33 shared tile.
-__global__ void k_split_b(int64_t K, int64_t N, const float* __restrict__ B, int64_t ldb, int64_t Kp, int64_t Np,
-                          float* __restrict__ out, const int32_t* __restrict__ pred) {
+// Grid-stride over the 32 x 32 tiles (at most a few CTAs per SM), so a
+// launch whose device predicate is off retires in microseconds even when B
+// is an n x p block (C4: 218k tiles).
+__global__ void __launch_bounds__(256) k_split_b(int64_t K, int64_t N, const float* __restrict__ B, int64_t ldb,
+                                                 int64_t Kp, int64_t Np, float* __restrict__ out,
+                                                 const int32_t* __restrict__ pred) {
     if (pred_off(pred)) return;
     __shared__ float t[32][33];
-    const int64_t k0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
-    for (int i = ty; i < 32; i += 8) {
-        const int64_t r = k0 + i, c = c0 + tx;
-        t[i][tx] = (r < K && c < N) ? B[r * ldb + c] : 0.f;
-    }
-    __syncthreads();
-    for (int i = ty; i < 32; i += 8) {
-        const int64_t c = c0 + i, r = k0 + tx;
-        const float x = t[tx][i];
-        const float h = tf32_hi(x);
+    const int64_t tk = Kp / 32, tiles = tk * (Np / 32);
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int64_t k0 = (tile % tk) * 32, c0 = (tile / tk) * 32;
+        for (int i = ty; i < 32; i += 8) {
+            const int64_t r = k0 + i, c = c0 + tx;
+            t[i][tx] = (r < K && c < N) ? B[r * ldb + c] : 0.f;
+        }
+        __syncthreads();
         float* blk = out + (k0 / 32) * (2 * Np) * 32;  // k0 is a multiple of 32
-        blk[c * 32 + tx] = h;
-        blk[(Np + c) * 32 + tx] = tf32_rna(x - h);
+        for (int i = ty; i < 32; i += 8) {
+            const int64_t c = c0 + i;
+            const float x = t[tx][i];
+            const float h = tf32_hi(x);
+            blk[c * 32 + tx] = h;
+            blk[(Np + c) * 32 + tx] = tf32_rna(x - h);
+        }
+        __syncthreads();
     }
 }
 
@@ -895,8 +903,9 @@ float* scratch_get(Scratch& sc, size_t need, cudaStream_t st) {
 
 int split_b(const float* B, int64_t K, int64_t N, int64_t ldb, int64_t Kp, int64_t Np, float* out,
             const int32_t* pred, cudaStream_t st) {
-    dim3 grid((unsigned)(Kp / 32), (unsigned)(Np / 32));
-    k_split_b<<<grid, dim3(32, 8), 0, st>>>(K, N, B, ldb, Kp, Np, out, pred);
+    const int64_t tiles = (Kp / 32) * (Np / 32);
+    const int64_t cap = (int64_t)sm_count() * 8;
+    k_split_b<<<(unsigned)(tiles < cap ? tiles : cap), dim3(32, 8), 0, st>>>(K, N, B, ldb, Kp, Np, out, pred);
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }
