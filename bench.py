@@ -638,7 +638,45 @@ def cpu_baseline(A_dev, cfgd, cfg, Pi, args, df=None):
                          "tolerance": 1e-4 if A_dev.dtype == torch.float32 else 1e-10}
         if A_dev.dtype == torch.float32 and not args.no_fp64:
             res["parity_fp64_mode"] = fp64_mode_leg(A_dev, cfgd, cfg, Pi, r)
+            if not cfgd.get("sparse"):
+                res["parity_decomposition"] = parity_decomposition(A_dev, cfgd, cfg, Pi, r, sig, cap)
     return res
+
+
+def parity_decomposition(A_dev, cfgd, cfg, Pi, r, sig32, cap32):
+    """Where the FP32 path's distance to the reference comes from: the same
+    projected (block-Lanczos) construction run in FP64 on the same A and Pi.
+    fp32_vs_fp64_same_construction = rounding of the FP32 / 3xTF32 path;
+    reference_vs_fp64_projected = the reference's own FP64 power-block
+    basis (rsvd.py:244-260) against the same Krylov space built without its
+    rounding loss."""
+    import torch
+
+    from paper_1504_05477_b200 import krylov, rsvd
+    from paper_1504_05477_b200.operators import DenseDeviceOp
+
+    A64 = A_dev.double()
+    op = DenseDeviceOp(A64, center=bool(cfgd.get("pca")))
+    saved = krylov.BK_BASIS
+    krylov.BK_BASIS = "projected"
+    try:
+        df = rsvd.run_device(op, cfg, Pi=torch.from_numpy(np.ascontiguousarray(Pi)).to(A64.device))
+        torch.cuda.synchronize()
+    finally:
+        krylov.BK_BASIS = saved
+    sig = df.sigma.double().cpu().numpy()
+    if cfgd.get("pca"):
+        A64 -= A64.mean(0, keepdim=True)
+    cap = (A64.T @ df.Z.double()).pow(2).sum(0).cpu().numpy()
+    del A64, op, df
+    torch.cuda.empty_cache()
+
+    def rel(a, b):
+        return float(np.max(np.abs(a - b) / np.abs(b)))
+
+    return {"fp32_vs_fp64_same_construction": {"sigma_rel_max": rel(sig32, sig), "captured_variance_rel_max": rel(cap32, cap)},
+            "reference_vs_fp64_projected": {"sigma_rel_max": rel(r.sigma, sig)},
+            "note": "FP64 run of this path's projected construction on the same A and Pi"}
 
 
 def fp64_mode_leg(A_dev, cfgd, cfg, Pi, r):

@@ -224,6 +224,16 @@ int rsvd_sqrt_clip(int64_t k, const double *in, double *out, void *stream);
 /* max |G - I| of a k x k FP64 matrix -> out[0] (rsvd.py:182-185). */
 int rsvd_ortho_error(int64_t k, const double *G, int64_t ldg, double *out, void *stream);
 
+/* ---- Device-predicated sections as CUDA-graph IF nodes -------------------
+ * While `stream` is being captured: adds a conditional node whose condition
+ * is (*flag != 0) at graph execution, and starts capturing `body_stream` into
+ * the node's body; the caller issues the section on `body_stream`, then calls
+ * rsvd_cond_end. Not capturing: *opened = 0 and nothing happens (the caller
+ * issues the section on `stream`). The sections are the orthonormalization's
+ * device-decided branches (factor.py:105-116). */
+int rsvd_cond_begin(void *stream, const int32_t *flag, void *body_stream, int32_t *opened);
+int rsvd_cond_end(void *body_stream);
+
 #ifdef __cplusplus
 }
 #endif

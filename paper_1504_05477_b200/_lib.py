@@ -51,6 +51,8 @@ _SIGS = {
     "rsvd_scatter_rows": ([_int, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp], _int),
     "rsvd_sqrt_clip": ([_i64, _vp, _vp, _vp], _int),
     "rsvd_ortho_error": ([_i64, _vp, _i64, _vp, _vp], _int),
+    "rsvd_cond_begin": ([_vp, _vp, _vp, _vp], _int),
+    "rsvd_cond_end": ([_vp], _int),
 }
 
 _lib = None

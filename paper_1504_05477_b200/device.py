@@ -42,6 +42,46 @@ def _stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+_BODY_STREAMS = {}
+
+
+class cond_section:
+    """``with cond_section(flag): ...`` — a device-decided section. Under CUDA
+    graph capture the section becomes an IF node on ``*flag != 0`` (csrc/
+    graph_cond.cu) and its launches go to the node's body; eagerly it runs
+    inline (its kernels keep their own ``pred`` checks, so both behave the
+    same). The section must not allocate memory (graph body restriction)."""
+
+    def __init__(self, flag, enabled=True):
+        self.flag = flag
+        self.enabled = enabled
+        self.body = None
+        self.ctx = None
+
+    def __enter__(self):
+        if not self.enabled or not torch.cuda.is_current_stream_capturing():
+            return self
+        dev = self.flag.device
+        body = _BODY_STREAMS.get(dev)
+        if body is None:
+            body = _BODY_STREAMS[dev] = torch.cuda.Stream(device=dev)
+        opened = ctypes.c_int32(0)
+        check(lib().rsvd_cond_begin(_stream(), _ptr(self.flag), ctypes.c_void_p(body.cuda_stream),
+                                         ctypes.byref(opened)), "cond_begin")
+        if opened.value:
+            self.body = body
+            self.ctx = torch.cuda.stream(body)
+            self.ctx.__enter__()
+        return self
+
+    def __exit__(self, *exc):
+        if self.body is not None:
+            self.ctx.__exit__(*exc)
+            check(lib().rsvd_cond_end(ctypes.c_void_p(self.body.cuda_stream)), "cond_end")
+            self.body = None
+        return False
+
+
 class _Workspace:
     """One growing scratch buffer per device. Safe because every user runs in
     stream order on the same stream."""

@@ -168,6 +168,9 @@ FP32_THIRD_PASS = os.environ.get("RSVD_FP32_THIRD_PASS", "0") == "1"
 # variance identical to 1e-9 relative, 24.06 -> 22.94 ms.
 # RSVD_PROJ_PASSES overrides both (A/B measurement).
 _PROJ_ENV = os.environ.get("RSVD_PROJ_PASSES")
+# Device-decided sections as CUDA-graph conditional nodes (RSVD_GRAPH_COND=0:
+# predicated kernels only, for A/B measurement).
+GRAPH_COND = os.environ.get("RSVD_GRAPH_COND", "1") != "0"
 
 
 def proj_passes(dtype):
@@ -203,7 +206,7 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
     dtype = V.dtype
     p = V.shape[1]
     if two_round is None:
-        two_round = True
+        two_round = os.environ.get("RSVD_TWO_ROUND", "1") != "0"  # "0": A/B timing of round 2's launches
     tau = TAU[dtype] if tau is None else tau
     n_total = V.shape[0] if n_total is None else n_total
     has_prev = Qp is not None and Qp.shape[1] > 0
@@ -219,35 +222,41 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
         comm.allreduce(ws.ref_orig[:p])
     ops.gram(V, G)
     comm.allreduce(G)
+    # device-decided sections become CUDA-graph IF nodes under capture
+    # (device.cond_section); they must not allocate, so their buffers are
+    # made here. NCCL collectives stay out of conditional bodies (world 1 only).
+    use_cond = GRAPH_COND and isinstance(comm, LocalComm)
+    T32 = torch.empty((p, p), dtype=dtype, device=V.device) if dtype != torch.float64 else None
     if two_round and tau > 0.0:
         r1 = ws.ndef_r1  # round-1 [count, base]: round 2 runs on the device only if count > 0
         ops.chol_deflate(G, ref2, tau * tau, T, mask, r1, None)
         Q1 = rows_buffer(tmp.shape[0], p, dtype, tmp.device)
         ops.gemm_nn(V, _cast_small(ops, T, dtype), Q1)  # Q1 (zero columns at rejected slots)
-        # round 2 needs Q1 orthonormal enough to project residuals against:
-        # one CholeskyQR step, only when round 2 will run
-        ops.gram(Q1, G, pred=r1)
-        comm.allreduce(G)
-        ops.chol_deflate(G, None, 0.0, T, ws.mask2[:p], ws.ndef2, None, pred=r1)
-        ops.gemm_nn(Q1, _cast_small(ops, T, dtype, pred=r1), tmp, pred=r1)
-        ops.convert(tmp, Q1, pred=r1)
         ws.ndef.zero_()
-        ops.mask_cols(V, mask, pred=r1)  # keep only the rejected columns' residuals
         c2 = torch.empty((p, p), dtype=dtype, device=V.device)
-        if has_prev:
-            project_out(ops, comm, Qp, V, tmp_c, pred=r1)
-        project_out(ops, comm, Q1, V, c2, pred=r1)
-        if has_prev:
-            project_out(ops, comm, Qp, V, tmp_c, pred=r1)
-        project_out(ops, comm, Q1, V, c2, pred=r1)
-        ops.gram(V, G, pred=r1)
-        comm.allreduce(G)
-        ref = ref2 if ref2 is not None else ws.ref_orig[:p]
-        rt = REF_RTOL_BY[dtype]
-        ops.chol_deflate(G, ref, rt * rt, T, ws.mask2[:p], ws.ndef, running, mask, pred=r1)
-        # survivors join the kept columns
-        ops.gemm_nn(V, _cast_small(ops, T, dtype, pred=r1), Q1, beta=1.0, pred=r1)
-        ops.insert_fill(Q1, ws.mask2[:p], ws.ndef, QR_FILL_SEED, row_offset, n_total, pred=r1)
+        with ops.cond_section(r1, use_cond):
+            # round 2 needs Q1 orthonormal enough to project residuals against:
+            # one CholeskyQR step, only when round 2 will run
+            ops.gram(Q1, G, pred=r1)
+            comm.allreduce(G)
+            ops.chol_deflate(G, None, 0.0, T, ws.mask2[:p], ws.ndef2, None, pred=r1)
+            ops.gemm_nn(Q1, _cast_small(ops, T, dtype, out=T32, pred=r1), tmp, pred=r1)
+            ops.convert(tmp, Q1, pred=r1)
+            ops.mask_cols(V, mask, pred=r1)  # keep only the rejected columns' residuals
+            if has_prev:
+                project_out(ops, comm, Qp, V, tmp_c, pred=r1)
+            project_out(ops, comm, Q1, V, c2, pred=r1)
+            if has_prev:
+                project_out(ops, comm, Qp, V, tmp_c, pred=r1)
+            project_out(ops, comm, Q1, V, c2, pred=r1)
+            ops.gram(V, G, pred=r1)
+            comm.allreduce(G)
+            ref = ref2 if ref2 is not None else ws.ref_orig[:p]
+            rt = REF_RTOL_BY[dtype]
+            ops.chol_deflate(G, ref, rt * rt, T, ws.mask2[:p], ws.ndef, running, mask, pred=r1)
+            # survivors join the kept columns
+            ops.gemm_nn(V, _cast_small(ops, T, dtype, out=T32, pred=r1), Q1, beta=1.0, pred=r1)
+            ops.insert_fill(Q1, ws.mask2[:p], ws.ndef, QR_FILL_SEED, row_offset, n_total, pred=r1)
         out = Q1
     else:
         ops.chol_deflate(G, ref2, tau * tau, T, mask, ws.ndef, running)
@@ -273,15 +282,16 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
     ops.gemm_nn(out, _cast_small(ops, T, dtype), V)
     # repair (runs only if a column collapsed): next stream vectors into the
     # collapsed slots, re-project, CholeskyQR
-    ops.insert_fill(V, ws.mask2[:p], r3, QR_FILL_SEED, row_offset, n_total, pred=r3)
-    if has_prev:
-        project_out(ops, comm, Qp, V, tmp_c, pred=r3)
-        project_out(ops, comm, Qp, V, tmp_c, pred=r3)
-    ops.gram(V, G, pred=r3)
-    comm.allreduce(G)
-    ops.chol_deflate(G, None, 0.0, T, ws.mask2[:p], ws.ndef2, None, pred=r3)
-    ops.gemm_nn(V, _cast_small(ops, T, dtype, pred=r3), out, pred=r3)
-    ops.convert(out, V, pred=r3)
+    with ops.cond_section(r3, use_cond):
+        ops.insert_fill(V, ws.mask2[:p], r3, QR_FILL_SEED, row_offset, n_total, pred=r3)
+        if has_prev:
+            project_out(ops, comm, Qp, V, tmp_c, pred=r3)
+            project_out(ops, comm, Qp, V, tmp_c, pred=r3)
+        ops.gram(V, G, pred=r3)
+        comm.allreduce(G)
+        ops.chol_deflate(G, None, 0.0, T, ws.mask2[:p], ws.ndef2, None, pred=r3)
+        ops.gemm_nn(V, _cast_small(ops, T, dtype, out=T32, pred=r3), out, pred=r3)
+        ops.convert(out, V, pred=r3)
     if dtype != torch.float64 and FP32_THIRD_PASS:
         # FP32 storage: one more CholeskyQR step (CholeskyQR2 cleanup)
         ops.gram(V, G)

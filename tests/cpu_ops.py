@@ -196,3 +196,17 @@ class CpuDenseOp:
     def apply_t(self, Y, out):
         cs = Y.double().sum(0) if self.mu is not None else None
         return gemm_tn(self.A, Y.to(self.A.dtype), out, mu=self.mu, colsum_b=cs)
+
+
+class cond_section:
+    """No graph capture on the CPU path: the section runs inline (its ops keep
+    their own predicates), as device.cond_section does outside capture."""
+
+    def __init__(self, flag, enabled=True):
+        pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False

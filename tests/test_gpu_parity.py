@@ -285,3 +285,34 @@ def test_sweep_harness_matches_reference(rk):
         for m in ("frob_ratio", "spectral_ratio", "per_vector_max"):
             assert abs(r[m] - ref[m]) <= 1e-7 * max(1.0, abs(ref[m])), (r, ref, m)
     assert rk.rows_to_csv(rows).split("\n")[0] == g["csv_header"]
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_graph_replay_matches_eager_with_deflation(rk, dtype):
+    """A captured factorization (device-decided branches as CUDA-graph IF
+    nodes, device.cond_section) reproduces the eager run bit for bit, on a
+    problem whose Krylov basis deflates (round 2 and the fill path taken) and
+    on one that does not (branches skipped)."""
+    from paper_1504_05477_b200 import rsvd
+    from paper_1504_05477_b200.operators import DenseDeviceOp
+
+    clus = np.concatenate([1 - 0.001 * np.arange(1, 61), 0.5 / np.arange(61, 401)])
+    A_def = o.synth_matrix(1500, 400, clus, seed=3, mm=o.mm_blas)
+    A_full = o.gaussian(1200, 300, o.SeededRng(77))
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    for A, k, q in ((A_def, 30, 7), (A_full, 20, 3)):
+        op = DenseDeviceOp(torch.from_numpy(np.ascontiguousarray(A)).to("cuda", tdt))
+        cfg = rk.RsvdConfig(k=k, variant="bk", q=q, seed=0)
+        Pi = torch.from_numpy(o.gaussian(A.shape[1], k, o.SeededRng(0))).to("cuda", tdt)
+        eager = rsvd.run_device(op, cfg, Pi=Pi)
+        torch.cuda.synchronize()
+        s_e, z_e, d_e = eager.sigma.clone(), eager.Z.clone(), eager.deflated.clone()
+        if A is A_def and dtype == "f64":
+            assert int(d_e[0]) > 0  # the deflation branches are exercised
+        g = rsvd.GraphedFactorization(op, cfg)
+        for _ in range(2):  # capture + a second replay
+            out = g.run(Pi)
+            torch.cuda.synchronize()
+            assert torch.equal(out.sigma, s_e)
+            assert torch.equal(out.Z, z_e)
+            assert torch.equal(out.deflated, d_e)
