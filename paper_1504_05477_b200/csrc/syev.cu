@@ -31,6 +31,7 @@ struct TriState {
     double* Uh;     // w x w, row j = Householder vector of step j
     double* beta;   // w
     double* p;      // w scratch
+    double* p2;     // w scratch (second p buffer of the one-barrier kernel)
     double* partial;
     unsigned int* bar;
 };
@@ -128,6 +129,165 @@ __global__ void __launch_bounds__(kTriThreads) k_tridiag(TriState s) {
     if (blockIdx.x == 0)
         for (int64_t jj = (w >= 2 ? w - 2 : 0); jj < w; ++jj)
             for (int64_t i = tid; i < w; i += blockDim.x) s.Uh[jj * w + i] = 0.0;
+}
+
+// Householder vector of x[0..m) into u (skip: beta = 0, u = x); alpha out.
+// Whole CTA, two block sums (the same arithmetic as k_tridiag's inline copy).
+__device__ double tri_hh(const double* x, int64_t m, double* u, double* red, double& alpha, bool& skip) {
+    const int tid = threadIdx.x;
+    double ss = 0.0, tail = 0.0;
+    for (int64_t i = tid; i < m; i += blockDim.x) {
+        const double v = x[i];
+        u[i] = v;
+        ss += v * v;
+        if (i > 0) tail += v * v;
+    }
+    ss = block_sum(ss, red);
+    tail = block_sum(tail, red);
+    const double x0 = u[0];
+    skip = !(tail > 0.0);
+    alpha = x0;
+    double beta = 0.0;
+    if (!skip) {
+        const double nrm = sqrt(ss);
+        alpha = x0 >= 0.0 ? -nrm : nrm;
+        const double u0 = x0 - alpha;
+        beta = 2.0 / (tail + u0 * u0);
+        __syncthreads();
+        if (tid == 0) u[0] = u0;
+    }
+    __syncthreads();
+    return beta;
+}
+
+// One grid barrier per column (k_tridiag takes two). After the barrier of
+// column j every CTA holds p_j = beta_j A22 u_j; each CTA then redundantly
+// forms q_j, the updated row j + 1 (nobody stores it: it leaves the trailing
+// matrix) and from it u_{j+1}; one fused pass per trailing row applies the
+// rank-2 update of column j and dots the updated row with u_{j+1}, giving
+// p_{j+1} for the next barrier (p double-buffered). Every entry sees the
+// same operations in the same order as in k_tridiag, so d, e, beta and the
+// reflectors are bitwise identical; the matrix is read and written once per
+// column instead of read twice and written once.
+__global__ void __launch_bounds__(kTriThreads) k_tridiag1(TriState s) {
+    extern __shared__ double sh[];
+    const int64_t w = s.w;  // >= 4
+    double* u = sh;           // u_j      (entries for columns j+1 ..)
+    double* q = sh + w;       // q_j
+    double* rn = sh + 2 * w;  // row j+1 of A^(j+1), columns j+1 ..
+    double* un = sh + 3 * w;  // u_{j+1}  (entries for columns j+2 ..)
+    __shared__ double red[kTriThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double* pc = s.p;   // p_j
+    double* pn = s.p2;  // p_{j+1}
+    double alpha;
+    bool skip;
+    double beta = tri_hh(s.A + 1, w - 1, u, red, alpha, skip);
+    if (blockIdx.x == 0) {
+        if (tid == 0) {
+            s.d[0] = s.A[0];
+            s.e[0] = alpha;
+            s.beta[0] = beta;
+        }
+        for (int64_t i = tid; i < w; i += blockDim.x) s.Uh[i] = (i > 0 && !skip) ? u[i - 1] : 0.0;
+    }
+    // p_0 = beta_0 A22 u_0
+    for (int64_t r = gwarp; r < w - 1; r += nwarps) {
+        const double* ar = s.A + (1 + r) * w + 1;
+        double acc = 0.0;
+        for (int64_t c = lane; c < w - 1; c += 32) acc = fma(ar[c], u[c], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) pc[r] = beta * acc;
+    }
+    grid_barrier(s.bar, gridDim.x);
+    for (int64_t j = 0; j + 2 < w; ++j) {
+        const int64_t m = w - j - 1;
+        const bool last = j + 3 == w;
+        // q_j = p_j - (beta_j / 2)(u_j . p_j) u_j
+        double kk = 0.0;
+        for (int64_t i = tid; i < m; i += blockDim.x) {
+            const double pv = pc[i];
+            q[i] = pv;
+            kk += u[i] * pv;
+        }
+        kk = 0.5 * beta * block_sum(kk, red);
+        for (int64_t i = tid; i < m; i += blockDim.x) q[i] -= kk * u[i];
+        __syncthreads();
+        // row j+1 after column j's update
+        const double* rowo = s.A + (j + 1) * w + (j + 1);
+        const double u0 = u[0], q0 = q[0];
+        for (int64_t c = tid; c < m; c += blockDim.x) rn[c] = rowo[c] - (u0 * q[c] + q0 * u[c]);
+        __syncthreads();
+        double beta_n = 0.0;
+        if (!last) {
+            double alpha_n;
+            bool skip_n;
+            beta_n = tri_hh(rn + 1, m - 1, un, red, alpha_n, skip_n);
+            if (blockIdx.x == 0) {
+                if (tid == 0) {
+                    s.d[j + 1] = rn[0];
+                    s.e[j + 1] = alpha_n;
+                    s.beta[j + 1] = beta_n;
+                }
+                double* uh = s.Uh + (j + 1) * w;
+                for (int64_t i = tid; i < w; i += blockDim.x) uh[i] = (i > j + 1 && !skip_n) ? un[i - j - 2] : 0.0;
+            }
+        } else if (blockIdx.x == 0 && tid == 0) {
+            s.d[j + 1] = rn[0];
+            s.e[j + 1] = rn[1];
+            s.beta[j + 1] = 0.0;
+        }
+        // rows j+2 .. : update (columns j+2 ..) fused with the dot against u_{j+1}
+        for (int64_t rr = gwarp; rr < m - 1; rr += nwarps) {
+            double* ar = s.A + (j + 2 + rr) * w + (j + 2);
+            const double ur = u[rr + 1], qr = q[rr + 1];
+            double acc = 0.0;
+            const int64_t mm = m - 1;
+            int64_t cc = lane;
+            // 8 independent L2 loads in flight per lane (the pass is latency
+            // bound); the dot accumulates in column order as before
+            for (; cc + 32 * 7 < mm; cc += 32 * 8) {
+                double v[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) v[t] = ar[cc + 32 * t];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    const int64_t c = cc + 32 * t;
+                    v[t] = v[t] - (ur * q[c + 1] + qr * u[c + 1]);
+                    ar[c] = v[t];
+                    if (!last) acc = fma(v[t], un[c], acc);
+                }
+            }
+            for (; cc < mm; cc += 32) {
+                const double v = ar[cc] - (ur * q[cc + 1] + qr * u[cc + 1]);
+                ar[cc] = v;
+                if (!last) acc = fma(v, un[cc], acc);
+            }
+            if (!last) {
+                acc = warp_sum(acc);
+                if (lane == 0) pn[rr] = beta_n * acc;
+            }
+        }
+        grid_barrier(s.bar, gridDim.x);
+        double* t = u;
+        u = un;
+        un = t;
+        t = pc;
+        pc = pn;
+        pn = t;
+        beta = beta_n;
+    }
+    if (blockIdx.x == 0) {
+        if (tid == 0) {
+            s.d[w - 1] = s.A[(w - 1) * w + (w - 1)];
+            s.e[w - 1] = 0.0;
+            s.beta[w - 1] = 0.0;
+        }
+        for (int64_t jj = w - 2; jj < w; ++jj)
+            for (int64_t i = tid; i < w; i += blockDim.x) s.Uh[jj * w + i] = 0.0;
+    }
 }
 
 // Cluster-resident tridiagonalisation (w <= kClTriMaxW): the whole w x w
@@ -635,6 +795,236 @@ store:
     }
 }
 
+// Blocked variant: the kBtRows reflectors of a staged block are applied to
+// a vector together. With D_r = u_r . x (x at the block start, all r at
+// once: kBtRows independent dot chains instead of one), the sequential
+// product H_{r0} H_{r1} ... applied to x is x - sum_r c_r u_r with
+//   c_r = beta_r (D_r - sum_{s<r} G_rs c_s),   G_rs = u_r . u_s,
+// G precomputed per block by k_bt_gram. Same Householder product, more
+// instruction-level parallelism per warp (the one-by-one form is a chain of
+// dependent dot -> warp_sum -> axpy steps per reflector).
+constexpr int kBtG = kBtRows * kBtRows;
+
+__global__ void k_bt_gram(int64_t w, const double* __restrict__ Uh, double* __restrict__ G) {
+    const int64_t jtop = w - 3;
+    const int64_t b = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double* g = G + b * kBtG;
+    for (int pr = warp; pr < kBtG; pr += nw) {
+        const int r = pr / kBtRows, c = pr % kBtRows;
+        const int64_t jr = jtop - b * kBtRows - r, jc = jtop - b * kBtRows - c;
+        double acc = 0.0;
+        if (c < r && jc >= 0 && jr >= 0) {
+            const double* ur = Uh + jr * w;
+            const double* uc = Uh + jc * w;
+            for (int64_t i = lane; i < w; i += 32) acc = fma(ur[i], uc[i], acc);
+            acc = warp_sum(acc);
+        }
+        if (lane == 0) g[pr] = acc;
+    }
+}
+
+template <int NC, int VPB>
+__global__ void __launch_bounds__(32 * VPB)
+k_backtransform_blk(int64_t w, int64_t k, const double* __restrict__ Uh, const double* __restrict__ beta,
+                    const double* __restrict__ G, const double* __restrict__ X, double* __restrict__ evecs,
+                    int64_t lde) {
+    extern __shared__ __align__(16) double ubuf[];  // [2][kBtRows][wp]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t v = (int64_t)blockIdx.x * VPB + warp;
+    const int nc = (int)((w + 31) / 32);
+    const int64_t wp = (w + 1) & ~int64_t(1);
+    double x[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const int64_t i = lane + 32 * c;
+        x[c] = (c < nc && v < k && i < w) ? X[v * w + i] : 0.0;
+    }
+    const int64_t jtop = w - 3;
+    if (jtop >= 0) {
+        const int64_t nblk = (jtop + kBtRows) / kBtRows;
+        auto issue = [&](int64_t b) {
+            double* dst = ubuf + (b & 1) * kBtRows * wp;
+            const bool vec = (w % 2) == 0;
+            for (int rr = 0; rr < kBtRows; ++rr) {
+                const int64_t j = jtop - b * kBtRows - rr;
+                if (j < 0) break;
+                if (vec) {
+                    for (int64_t i = 2 * threadIdx.x; i < w; i += 2 * blockDim.x)
+                        cp_async16(dst + rr * wp + i, Uh + j * w + i);
+                } else {
+                    for (int64_t i = threadIdx.x; i < w; i += blockDim.x) dst[rr * wp + i] = Uh[j * w + i];
+                }
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        issue(0);
+        for (int64_t b = 0; b < nblk; ++b) {
+            if (b + 1 < nblk) {
+                issue(b + 1);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+            __syncthreads();
+            const double* blk = ubuf + (b & 1) * kBtRows * wp;
+            const int nr = (int)min((int64_t)kBtRows, jtop - b * kBtRows + 1);  // valid rows (uniform)
+            double dd[kBtRows];
+#pragma unroll
+            for (int r = 0; r < kBtRows; ++r) dd[r] = 0.0;
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                if (c < nc) {
+                    const int64_t i = lane + 32 * c;
+                    if (i < w) {
+#pragma unroll
+                        for (int r = 0; r < kBtRows; ++r)
+                            if (r < nr) dd[r] = fma(blk[r * wp + i], x[c], dd[r]);
+                    }
+                }
+#pragma unroll
+            for (int r = 0; r < kBtRows; ++r) dd[r] = warp_sum(dd[r]);
+            const double* g = G + b * kBtG;
+            double cf[kBtRows];
+#pragma unroll
+            for (int r = 0; r < kBtRows; ++r) {
+                double t = dd[r];
+#pragma unroll
+                for (int s2 = 0; s2 < r; ++s2) t = fma(-g[r * kBtRows + s2], cf[s2], t);
+                const int64_t j = jtop - b * kBtRows - r;
+                cf[r] = r < nr ? beta[j] * t : 0.0;
+            }
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                if (c < nc) {
+                    const int64_t i = lane + 32 * c;
+                    if (i < w) {
+                        double xc = x[c];
+#pragma unroll
+                        for (int r = 0; r < kBtRows; ++r)
+                            if (r < nr) xc = fma(-cf[r], blk[r * wp + i], xc);
+                        x[c] = xc;
+                    }
+                }
+            __syncthreads();  // buffer (b & 1) is refilled by issue(b + 2)
+        }
+    }
+    if (v < k) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const int64_t i = lane + 32 * c;
+            if (c < nc && i < w) evecs[i * lde + v] = x[c];
+        }
+    }
+}
+
+// Row-split blocked back-transformation: a CTA of 8 warps serves VPB vectors;
+// warp ww owns rows [ww S, (ww + 1) S) of all of them (S = NCW x 32), so the
+// FP64 pipe sees 8 warps per SM instead of one. Per block of kBtRows
+// reflectors each lane loads its slice of the reflectors straight from L2
+// (prefetched one block ahead, no shared-memory staging), forms partial dots
+// for every (reflector, vector) pair, the CTA sums them (one round through
+// shared memory), and every thread runs the kBtRows-step recurrence of
+// k_backtransform_blk and applies the rank-kBtRows update to its rows.
+constexpr int kRsWarps = 8;
+
+template <int NCW, int VPB>
+__global__ void __launch_bounds__(32 * kRsWarps)
+k_backtransform_rs(int64_t w, int64_t k, const double* __restrict__ Uh, const double* __restrict__ beta,
+                   const double* __restrict__ G, const double* __restrict__ X, double* __restrict__ evecs,
+                   int64_t lde) {
+    constexpr int R = kBtRows, NP = R * VPB;  // (reflector, vector) pairs
+    __shared__ double red[kRsWarps][NP];
+    __shared__ double dsum[NP];
+    const int lane = threadIdx.x & 31, ww = threadIdx.x >> 5;
+    const int64_t v0 = (int64_t)blockIdx.x * VPB;
+    const int64_t S = (int64_t)NCW * 32;
+    const int64_t i0 = ww * S + lane;
+    double x[VPB][NCW];
+#pragma unroll
+    for (int v = 0; v < VPB; ++v)
+#pragma unroll
+        for (int c = 0; c < NCW; ++c) {
+            const int64_t i = i0 + 32 * c;
+            x[v][c] = (v0 + v < k && i < w) ? X[(v0 + v) * w + i] : 0.0;
+        }
+    const int64_t jtop = w - 3;
+    const int64_t nblk = jtop >= 0 ? (jtop + R) / R : 0;
+    // prefetch one block ahead when the registers allow it (NCW <= 4)
+    constexpr bool PF = NCW <= 4;
+    double u[R][NCW], un[PF ? R : 1][PF ? NCW : 1];
+    auto load = [&](int64_t b, auto& dst) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int64_t j = jtop - b * R - r;
+#pragma unroll
+            for (int c = 0; c < NCW; ++c) {
+                const int64_t i = i0 + 32 * c;
+                dst[r][c] = (j >= 0 && i < w) ? __ldg(Uh + j * w + i) : 0.0;
+            }
+        }
+    };
+    if (nblk > 0) load(0, u);
+    for (int64_t b = 0; b < nblk; ++b) {
+        if (PF) {
+            if (b + 1 < nblk) load(b + 1, un);
+        } else if (b > 0) {
+            load(b, u);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int v = 0; v < VPB; ++v) {
+                double a = 0.0;
+#pragma unroll
+                for (int c = 0; c < NCW; ++c) a = fma(u[r][c], x[v][c], a);
+                a = warp_sum(a);
+                if (lane == 0) red[ww][r * VPB + v] = a;
+            }
+        __syncthreads();
+        if (threadIdx.x < NP) {
+            double t = 0.0;
+#pragma unroll
+            for (int q = 0; q < kRsWarps; ++q) t += red[q][threadIdx.x];
+            dsum[threadIdx.x] = t;
+        }
+        __syncthreads();
+        const double* g = G + b * kBtG;
+        const int nr = (int)min((int64_t)R, jtop - b * R + 1);
+#pragma unroll
+        for (int v = 0; v < VPB; ++v) {
+            double cf[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                double t = dsum[r * VPB + v];
+#pragma unroll
+                for (int s2 = 0; s2 < r; ++s2) t = fma(-g[r * R + s2], cf[s2], t);
+                cf[r] = r < nr ? beta[jtop - b * R + (int64_t)(-r)] * t : 0.0;
+            }
+#pragma unroll
+            for (int c = 0; c < NCW; ++c) {
+                double xc = x[v][c];
+#pragma unroll
+                for (int r = 0; r < R; ++r) xc = fma(-cf[r], u[r][c], xc);
+                x[v][c] = xc;
+            }
+        }
+        if (PF && b + 1 < nblk) {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int c = 0; c < NCW; ++c) u[r][c] = un[PF ? r : 0][PF ? c : 0];
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < VPB; ++v)
+#pragma unroll
+        for (int c = 0; c < NCW; ++c) {
+            const int64_t i = i0 + 32 * c;
+            if (v0 + v < k && i < w) evecs[i * lde + v0 + v] = x[v][c];
+        }
+}
+
 __global__ void k_info_init(int32_t* info) {
     info[0] = 1;
     info[1] = 0;
@@ -644,7 +1034,7 @@ __global__ void k_info_init(int32_t* info) {
 
 int64_t syev_topk_ws_bytes(int64_t w, int64_t k) {
     // A, Uh (w^2 each), d, e, e2, beta, p (w each), bounds, X (k w), fac (k 5w), clusters
-    const int64_t dbl = 2 * w * w + 5 * w + 16 + k * w + 5 * k * w + 1024;
+    const int64_t dbl = 2 * w * w + 6 * w + 16 + k * w + 5 * k * w + 1024 + (w / kBtRows + 2) * kBtG;
     return dbl * (int64_t)sizeof(double) + (k + 2) * 4 + 256;
 }
 
@@ -662,12 +1052,14 @@ int syev_topk(int64_t w, const double* M, int64_t ldm, int64_t k, double* evals,
     double* e2 = s.e + w;
     s.beta = e2 + w;
     s.p = s.beta + w;
-    double* bounds = s.p + w;
+    s.p2 = s.p + w;
+    double* bounds = s.p2 + w;
     double* X = bounds + 16;
     double* fac = X + k * w;
     s.partial = fac + 5 * k * w;
     s.bar = (unsigned int*)(s.partial + 1024 - 16);
-    int32_t* cl = (int32_t*)(s.partial + 1024);
+    double* btg = s.partial + 1024;  // (w / kBtRows + 2) x kBtRows^2 block Grams
+    int32_t* cl = (int32_t*)(btg + (w / kBtRows + 2) * kBtG);
     int32_t* ncl = cl + k + 1;
     RSVD_CHECK_CUDA(cudaMemsetAsync(s.bar, 0, 2 * sizeof(unsigned int), st));
     k_info_init<<<1, 1, 0, st>>>(info);
@@ -722,19 +1114,22 @@ int syev_topk(int64_t w, const double* M, int64_t ldm, int64_t k, double* evals,
         }
     }
     if (!done) {
-        const size_t smem = (size_t)(2 * w) * sizeof(double);
+        // one barrier per column (k_tridiag1) unless RSVD_TRIDIAG_TWO_BARRIER is set (A/B)
+        const bool two = getenv("RSVD_TRIDIAG_TWO_BARRIER") != nullptr;
+        const bool one = w >= 4 && !two;
+        const void* kern = one ? (const void*)k_tridiag1 : (const void*)k_tridiag;
+        const size_t smem = (size_t)((one ? 4 : 2) * w) * sizeof(double);
         RSVD_REQUIRE(smem <= 200 * 1024, "syev_topk: w too large");
         if (smem > 48 * 1024)
-            RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            RSVD_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int per_sm = 0;
-        RSVD_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tridiag, kTriThreads, smem));
+        RSVD_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTriThreads, smem));
         RSVD_REQUIRE(per_sm >= 1, "syev_topk: tridiagonalisation kernel cannot be resident");
         int64_t g = cdiv(w, kTriThreads / 32);
         if (g > sm_count()) g = sm_count();
         if (g < 1) g = 1;
         void* args[] = {&s};
-        RSVD_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)k_tridiag, dim3((unsigned)g), dim3(kTriThreads),
-                                                    args, smem, st));
+        RSVD_CHECK_CUDA(cudaLaunchCooperativeKernel(kern, dim3((unsigned)g), dim3(kTriThreads), args, smem, st));
     }
     k_e2<<<(unsigned)cdiv(w, 256), 256, 0, st>>>(w, s.e, e2);
     RSVD_CHECK_LAUNCH();
@@ -752,16 +1147,46 @@ int syev_topk(int64_t w, const double* M, int64_t ldm, int64_t k, double* evals,
         const size_t bsm = (size_t)(2 * kBtRows * ((w + 1) & ~int64_t(1))) * sizeof(double);
         // one vector per CTA below 300 vectors (k = 50: 50 CTAs instead of 7)
         const int vpb = k >= 300 ? 4 : 1;
-        auto launch = [&](auto kern, int vp) -> int {
-            if (bsm > 48 * 1024)
-                RSVD_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
-            kern<<<(unsigned)cdiv(k, vp), 32 * vp, bsm, st>>>(w, k, s.Uh, s.beta, X, evecs, lde);
+        const bool seq = getenv("RSVD_BT_SEQ") != nullptr;  // one-by-one reflectors (A/B)
+        const bool staged = getenv("RSVD_BT_STAGED") != nullptr;  // smem-staged blocked kernel (A/B)
+        if (!seq && w >= 3) {
+            const int64_t nblk = (w - 3 + kBtRows) / kBtRows;
+            k_bt_gram<<<(unsigned)nblk, 256, 0, st>>>(w, s.Uh, btg);
+            RSVD_CHECK_LAUNCH();
+        }
+        if (!seq && !staged && w >= 3) {
+            // row-split kernel: kRsWarps warps x NCW x 32 rows >= w
+            const int64_t ncw = cdiv(cdiv(w, kRsWarps), 32);
+            auto rs = [&](auto kern, int vp) -> int {
+                kern<<<(unsigned)cdiv(k, vp), 32 * kRsWarps, 0, st>>>(w, k, s.Uh, s.beta, btg, X, evecs, lde);
+                RSVD_CHECK_LAUNCH();
+                return RSVD_OK;
+            };
+#define RSVD_RS(N)                                                                                     \
+            if (ncw <= N) return k >= 64 ? rs(k_backtransform_rs<N, 4>, 4) : rs(k_backtransform_rs<N, 2>, 2);
+#define RSVD_RS2(N) \
+            if (ncw <= N) return rs(k_backtransform_rs<N, 2>, 2);
+            RSVD_RS(1) RSVD_RS(2) RSVD_RS(3) RSVD_RS2(4) RSVD_RS2(5) RSVD_RS2(6) RSVD_RS2(7) RSVD_RS2(8)
+#undef RSVD_RS2
+#undef RSVD_RS
+        }
+        auto launch = [&](auto kern, auto kernb, int vp) -> int {
+            if (seq || w < 3) {
+                if (bsm > 48 * 1024)
+                    RSVD_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+                kern<<<(unsigned)cdiv(k, vp), 32 * vp, bsm, st>>>(w, k, s.Uh, s.beta, X, evecs, lde);
+            } else {
+                if (bsm > 48 * 1024)
+                    RSVD_CHECK_CUDA(cudaFuncSetAttribute(kernb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+                kernb<<<(unsigned)cdiv(k, vp), 32 * vp, bsm, st>>>(w, k, s.Uh, s.beta, btg, X, evecs, lde);
+            }
             RSVD_CHECK_LAUNCH();
             return RSVD_OK;
         };
 #define RSVD_BT(NC)                                                                                    \
         if (w <= 32 * NC)                                                                              \
-            return vpb == 1 ? launch(k_backtransform<NC, 1>, 1) : launch(k_backtransform<NC, 4>, 4);
+            return vpb == 1 ? launch(k_backtransform<NC, 1>, k_backtransform_blk<NC, 1>, 1)            \
+                            : launch(k_backtransform<NC, 4>, k_backtransform_blk<NC, 4>, 4);
         RSVD_BT(8) RSVD_BT(16) RSVD_BT(20) RSVD_BT(24) RSVD_BT(32) RSVD_BT(40) RSVD_BT(52) RSVD_BT(64)
 #undef RSVD_BT
     }

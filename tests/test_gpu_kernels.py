@@ -267,6 +267,37 @@ def test_syev_topk_grid_and_cluster_paths_agree(ops, monkeypatch):
     assert np.max(np.abs(ev_g.cpu().numpy() - ref)) < 1e-14
 
 
+@pytest.mark.parametrize("w,k", [(4, 2), (5, 5), (37, 8), (700, 40), (1300, 100)])
+def test_tridiag_one_barrier_matches_two_barrier(ops, monkeypatch, w, k):
+    """The one-barrier-per-column grid tridiagonalisation (k_tridiag1, the
+    path for w > 608: C3-C5) performs the same operations in the same order
+    as the two-barrier kernel: eigenvalues and vectors bitwise equal. A
+    repeated eigenvalue block exercises the zero-tail (skipped reflector)
+    path on the small sizes."""
+    rng = np.random.default_rng(w)
+    Q, _ = np.linalg.qr(rng.standard_normal((w, w)))
+    lam = 1.0 / np.arange(1, w + 1, dtype=float)
+    lam[w // 2:] = lam[w // 2]
+    sym = (Q * lam) @ Q.T
+    sym = 0.5 * (sym + sym.T)
+    if w == 5:
+        sym = np.diag(np.arange(5.0, 0.0, -1.0))  # already tridiagonal: every reflector skipped
+    M = _t(sym)
+    monkeypatch.setenv("RSVD_TRIDIAG_GRID", "1")
+    ev1, V1, i1 = ops.syev_topk(M, k)
+    monkeypatch.setenv("RSVD_TRIDIAG_TWO_BARRIER", "1")
+    ev2, V2, i2 = ops.syev_topk(M, k)
+    assert int(i1[0]) == 1 and int(i2[0]) == 1
+    assert torch.equal(ev1, ev2) and torch.equal(V1, V2)
+    # blocked back-transformation (k_backtransform_blk) vs one reflector at a time
+    monkeypatch.setenv("RSVD_BT_SEQ", "1")
+    ev3, V3, _ = ops.syev_topk(M, k)
+    assert torch.equal(ev1, ev3)
+    assert torch.max(torch.abs(V1 - V3)).item() < 1e-13
+    ref = np.sort(np.linalg.eigvalsh(sym))[::-1][:k]
+    assert np.max(np.abs(ev1.cpu().numpy() - ref)) < 1e-13 * max(1.0, abs(ref[0]))
+
+
 @pytest.mark.parametrize("nb,dtype", [(7, torch.float32), (100, torch.float32), (300, torch.float32),
                                       (600, torch.float32), (64, torch.float64), (300, torch.float64)])
 def test_spmm_plan_split_rows_and_wide_blocks(ops, nb, dtype):

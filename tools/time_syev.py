@@ -3,7 +3,10 @@ import os, sys, time
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1504_05477_b200 import device as ops
-for w, k in [(200, 20), (600, 50), (1200, 200), (1600, 200)]:
+SH = [(200, 20), (600, 50), (1200, 200), (1600, 200)]
+if len(sys.argv) > 1:
+    SH = [tuple(int(x) for x in sys.argv[1].split(','))]
+for w, k in SH:
     rng = np.random.default_rng(w)
     Q, _ = np.linalg.qr(rng.standard_normal((w, w)))
     lam = (np.arange(1, w + 1) ** -0.5) ** 2
