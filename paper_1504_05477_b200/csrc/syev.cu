@@ -131,6 +131,26 @@ __global__ void __launch_bounds__(kTriThreads) k_tridiag(TriState s) {
             for (int64_t i = tid; i < w; i += blockDim.x) s.Uh[jj * w + i] = 0.0;
 }
 
+// Two block sums with one pair of barriers (same per-value order as block_sum).
+__device__ void block_sum2(double& a, double& b, double* red2) {
+    a = warp_sum(a);
+    b = warp_sum(b);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+    __syncthreads();
+    if (lane == 0) {
+        red2[warp] = a;
+        red2[nw + warp] = b;
+    }
+    __syncthreads();
+    double sa = 0.0, sb = 0.0;
+    for (int i = 0; i < nw; ++i) {
+        sa += red2[i];
+        sb += red2[nw + i];
+    }
+    a = sa;
+    b = sb;
+}
+
 // Householder vector of x[0..m) into u (skip: beta = 0, u = x); alpha out.
 // Whole CTA, two block sums (the same arithmetic as k_tridiag's inline copy).
 __device__ double tri_hh(const double* x, int64_t m, double* u, double* red, double& alpha, bool& skip) {
@@ -142,8 +162,7 @@ __device__ double tri_hh(const double* x, int64_t m, double* u, double* red, dou
         ss += v * v;
         if (i > 0) tail += v * v;
     }
-    ss = block_sum(ss, red);
-    tail = block_sum(tail, red);
+    block_sum2(ss, tail, red);  // red holds 2 x (warps) doubles
     const double x0 = u[0];
     skip = !(tail > 0.0);
     alpha = x0;
@@ -169,14 +188,14 @@ __device__ double tri_hh(const double* x, int64_t m, double* u, double* red, dou
 // same operations in the same order as in k_tridiag, so d, e, beta and the
 // reflectors are bitwise identical; the matrix is read and written once per
 // column instead of read twice and written once.
-__global__ void __launch_bounds__(kTriThreads) k_tridiag1(TriState s) {
+__global__ void __launch_bounds__(kTriThreads, 1) k_tridiag1(TriState s) {
     extern __shared__ double sh[];
     const int64_t w = s.w;  // >= 4
     double* u = sh;           // u_j      (entries for columns j+1 ..)
     double* q = sh + w;       // q_j
     double* rn = sh + 2 * w;  // row j+1 of A^(j+1), columns j+1 ..
     double* un = sh + 3 * w;  // u_{j+1}  (entries for columns j+2 ..)
-    __shared__ double red[kTriThreads / 32];
+    __shared__ double red[2 * (kTriThreads / 32)];
     const int tid = threadIdx.x, lane = tid & 31;
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + tid) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -461,6 +480,165 @@ __global__ void __launch_bounds__(kClTriThreads, 1) k_tridiag_cluster(TriState s
     }
     if (rank == 0)
         for (int jj = jl; jj < w; ++jj)
+            for (int i = tid; i < w; i += kClTriThreads) s.Uh[(size_t)jj * w + i] = 0.0;
+    cluster.sync();  // keep every CTA's shared memory alive until remote reads are done
+}
+
+// One cluster barrier per column (k_tridiag_cluster takes two), the
+// k_tridiag1 scheme on distributed shared memory: after the barrier of
+// column j every CTA gathers p_j, forms q_j, reads row j + 1 from its owner
+// (nobody updates that row in column j: it leaves the trailing matrix) and
+// builds u_{j+1} itself; then one pass over its trailing rows applies the
+// rank-2 update and dots each updated row with u_{j+1}, leaving p_{j+1} for
+// the next barrier. u, p double-buffered by column parity.
+__global__ void __launch_bounds__(kClTriThreads, 1) k_tridiag_cluster1(TriState s) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ double sh[];
+    const int w = (int)s.w;  // >= 4
+    const int rank = (int)cluster.block_rank();
+    const int nloc = (w + kClTri - 1) / kClTri;
+    double* Aloc = sh;                        // nloc x w
+    double* ubuf = Aloc + (size_t)nloc * w;  // [2][w]
+    double* pbuf = ubuf + 2 * w;             // [2][w]  (indexed by global row)
+    double* q = pbuf + 2 * w;                // w
+    double* rn = q + w;                      // w
+    __shared__ double red[2 * (kClTriThreads / 32)];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kClTriThreads / 32;
+    for (int lr = 0; lr < nloc; ++lr) {
+        const int r = rank + kClTri * lr;
+        for (int c = tid; c < w; c += kClTriThreads) Aloc[(size_t)lr * w + c] = r < w ? s.A[(size_t)r * w + c] : 0.0;
+    }
+    cluster.sync();
+    // column 0: every CTA forms u_0 from row 0 (CTA 0) and p_0 for its rows
+    double beta;
+    {
+        const double* row0 = cluster.map_shared_rank(Aloc, 0);
+        for (int c = tid; c < w; c += kClTriThreads) rn[c] = row0[c];
+        __syncthreads();
+        double alpha;
+        bool skip;
+        beta = tri_hh(rn + 1, w - 1, ubuf, red, alpha, skip);
+        if (rank == 0) {
+            if (tid == 0) {
+                s.d[0] = rn[0];
+                s.e[0] = alpha;
+                s.beta[0] = beta;
+            }
+            for (int i = tid; i < w; i += kClTriThreads) s.Uh[i] = (i > 0 && !skip) ? ubuf[i - 1] : 0.0;
+        }
+        const int lr0 = (1 - rank + kClTri - 1) / kClTri;
+        for (int lr = lr0 + warp; lr < nloc; lr += nw) {
+            const int r = rank + kClTri * lr;
+            if (r >= w) break;
+            const double* ar = Aloc + (size_t)lr * w + 1;
+            double acc = 0.0;
+            for (int c = lane; c < w - 1; c += 32) acc = fma(ar[c], ubuf[c], acc);
+            acc = warp_sum(acc);
+            if (lane == 0) pbuf[r] = beta * acc;
+        }
+    }
+    cluster.sync();
+    for (int j = 0; j + 2 < w; ++j) {
+        const int par = j & 1;
+        const int m = w - j - 1;
+        const bool last = j + 3 == w;
+        double* u = ubuf + par * w;
+        double* un = ubuf + (par ^ 1) * w;
+        double* pp = pbuf + par * w;
+        double* pn = pbuf + (par ^ 1) * w;
+        // q_j from the gathered p_j; row j+1 (owner's smem) fetched alongside
+        constexpr int kRowPer = (kClTriMaxW + kClTriThreads - 1) / kClTriThreads;
+        double rowv[kRowPer];
+        {
+            const double* ro = cluster.map_shared_rank(Aloc + (size_t)((j + 1) / kClTri) * w + (j + 1), (j + 1) % kClTri);
+#pragma unroll
+            for (int t = 0; t < kRowPer; ++t) {
+                const int c = tid + t * kClTriThreads;
+                rowv[t] = c < m ? ro[c] : 0.0;
+            }
+        }
+        double kk = 0.0;
+        for (int i = tid; i < m; i += kClTriThreads) {
+            const int r = j + 1 + i;
+            const double* pr = cluster.map_shared_rank(pp, r % kClTri);
+            const double pv = pr[r];
+            q[i] = pv;
+            kk += u[i] * pv;
+        }
+        kk = 0.5 * beta * block_sum(kk, red);
+        for (int i = tid; i < m; i += kClTriThreads) q[i] -= kk * u[i];
+        __syncthreads();
+        // row j+1 after column j's update
+        {
+            const double u0 = u[0], q0 = q[0];
+#pragma unroll
+            for (int t = 0; t < kRowPer; ++t) {
+                const int c = tid + t * kClTriThreads;
+                if (c < m) rn[c] = rowv[t] - (u0 * q[c] + q0 * u[c]);
+            }
+        }
+        __syncthreads();
+        double beta_n = 0.0;
+        if (!last) {
+            double alpha_n;
+            bool skip_n;
+            beta_n = tri_hh(rn + 1, m - 1, un, red, alpha_n, skip_n);
+            if (rank == 0) {
+                if (tid == 0) {
+                    s.d[j + 1] = rn[0];
+                    s.e[j + 1] = alpha_n;
+                    s.beta[j + 1] = beta_n;
+                }
+                double* uh = s.Uh + (size_t)(j + 1) * w;
+                for (int i = tid; i < w; i += kClTriThreads) uh[i] = (i > j + 1 && !skip_n) ? un[i - j - 2] : 0.0;
+            }
+        } else if (rank == 0 && tid == 0) {
+            s.d[j + 1] = rn[0];
+            s.e[j + 1] = rn[1];
+            s.beta[j + 1] = 0.0;
+        }
+        // fused pass over this CTA's rows j+2 ..; lane l handles columns
+        // j+2+l+32i, so its q / u_{j+1} entries sit in registers (u from smem)
+        double qreg[kClRegs], nreg[kClRegs];
+#pragma unroll
+        for (int i = 0; i < kClRegs; ++i) {
+            const int c = lane + 32 * i;
+            qreg[i] = c < m - 1 ? q[c + 1] : 0.0;
+            nreg[i] = (c < m - 1 && !last) ? un[c] : 0.0;
+        }
+        const int lr0 = (j + 2 - rank + kClTri - 1) / kClTri;  // first local row with global r > j + 1
+        for (int lr = lr0 + warp; lr < nloc; lr += nw) {
+            const int r = rank + kClTri * lr;
+            if (r >= w) break;
+            double* ar = Aloc + (size_t)lr * w + (j + 2);
+            const int ir = r - j - 1;
+            const double ur = u[ir], qr = q[ir];
+            double acc = 0.0;
+#pragma unroll
+            for (int i = 0; i < kClRegs; ++i) {
+                const int c = lane + 32 * i;
+                if (c < m - 1) {
+                    const double v = ar[c] - (ur * qreg[i] + qr * u[c + 1]);
+                    ar[c] = v;
+                    acc = fma(v, nreg[i], acc);
+                }
+            }
+            if (!last) {
+                acc = warp_sum(acc);
+                if (lane == 0) pn[r] = beta_n * acc;
+            }
+        }
+        beta = beta_n;
+        cluster.sync();
+    }
+    if (rank == (w - 1) % kClTri && tid == 0) {
+        s.d[w - 1] = Aloc[(size_t)((w - 1) / kClTri) * w + (w - 1)];
+        s.e[w - 1] = 0.0;
+        s.beta[w - 1] = 0.0;
+    }
+    if (rank == 0)
+        for (int jj = w - 2; jj < w; ++jj)
             for (int i = tid; i < w; i += kClTriThreads) s.Uh[(size_t)jj * w + i] = 0.0;
     cluster.sync();  // keep every CTA's shared memory alive until remote reads are done
 }
@@ -1068,15 +1246,21 @@ int syev_topk(int64_t w, const double* M, int64_t ldm, int64_t k, double* evals,
     bool done = false;
     if (w <= kClTriMaxW && !getenv("RSVD_TRIDIAG_GRID")) {
         const int nloc = (int)((w + kClTri - 1) / kClTri);
-        const size_t csm = ((size_t)nloc * w + 5 * (size_t)w) * sizeof(double);
+        // one cluster barrier per column unless RSVD_TRIDIAG_TWO_BARRIER (A/B)
+        const bool one = w >= 4 && getenv("RSVD_TRIDIAG_TWO_BARRIER") == nullptr;
+        const size_t csm = ((size_t)nloc * w + 6 * (size_t)w) * sizeof(double);
         static int cluster_ok = -1;  // cluster launch supported and schedulable (checked once)
         if (cluster_ok < 0) {
             cluster_ok = 0;
-            const int maxsm = (int)(((size_t)((kClTriMaxW + kClTri - 1) / kClTri) * kClTriMaxW + 5 * (size_t)kClTriMaxW) *
+            const int maxsm = (int)(((size_t)((kClTriMaxW + kClTri - 1) / kClTri) * kClTriMaxW + 6 * (size_t)kClTriMaxW) *
                                     sizeof(double));
             if (cudaFuncSetAttribute(k_tridiag_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
                     cudaSuccess &&
                 cudaFuncSetAttribute(k_tridiag_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) ==
+                    cudaSuccess &&
+                cudaFuncSetAttribute(k_tridiag_cluster1, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                    cudaSuccess &&
+                cudaFuncSetAttribute(k_tridiag_cluster1, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm) ==
                     cudaSuccess) {
                 cudaLaunchConfig_t qc = {};
                 qc.gridDim = dim3(kClTri);
@@ -1109,7 +1293,10 @@ int syev_topk(int64_t w, const double* M, int64_t ldm, int64_t k, double* evals,
             at[0].val.clusterDim.z = 1;
             cfg.attrs = at;
             cfg.numAttrs = 1;
-            RSVD_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_tridiag_cluster, s));
+            if (one)
+                RSVD_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_tridiag_cluster1, s));
+            else
+                RSVD_CHECK_CUDA(cudaLaunchKernelEx(&cfg, k_tridiag_cluster, s));
             done = true;
         }
     }

@@ -267,6 +267,22 @@ def test_syev_topk_grid_and_cluster_paths_agree(ops, monkeypatch):
     assert np.max(np.abs(ev_g.cpu().numpy() - ref)) < 1e-14
 
 
+@pytest.mark.parametrize("w,k", [(4, 2), (40, 10), (600, 50), (608, 30)])
+def test_tridiag_cluster_one_barrier_matches_two_barrier(ops, monkeypatch, w, k):
+    """Cluster-resident tridiagonalisation (w <= 608, C2): the one-barrier
+    kernel (k_tridiag_cluster1) against the two-barrier one, bitwise."""
+    rng = np.random.default_rng(w + 1)
+    Q, _ = np.linalg.qr(rng.standard_normal((w, w)))
+    lam = np.arange(1, w + 1, dtype=float) ** -0.5
+    sym = (Q * lam) @ Q.T
+    M = _t(0.5 * (sym + sym.T))
+    ev1, V1, i1 = ops.syev_topk(M, k)
+    monkeypatch.setenv("RSVD_TRIDIAG_TWO_BARRIER", "1")
+    ev2, V2, i2 = ops.syev_topk(M, k)
+    assert int(i1[0]) == 1 and int(i2[0]) == 1
+    assert torch.equal(ev1, ev2) and torch.equal(V1, V2)
+
+
 @pytest.mark.parametrize("w,k", [(4, 2), (5, 5), (37, 8), (700, 40), (1300, 100)])
 def test_tridiag_one_barrier_matches_two_barrier(ops, monkeypatch, w, k):
     """The one-barrier-per-column grid tridiagonalisation (k_tridiag1, the
