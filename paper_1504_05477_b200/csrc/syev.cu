@@ -309,6 +309,145 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_tridiag1(TriState s) {
     }
 }
 
+// k_tridiag1 with the matrix distributed over the CTAs' shared memory (row r
+// in CTA r % G): the fused update+matvec pass reads shared memory instead of
+// L2. The one row every CTA needs from another (row j+1 at column j) is
+// published to global memory by its owner in the pass that last updates it;
+// p goes through global memory as before. For w where the rows fit
+// (ceil(w / G) * w doubles plus 4 w of vectors), else k_tridiag1.
+__global__ void __launch_bounds__(kTriThreads, 1) k_tridiag_sm(TriState s) {
+    extern __shared__ double sh[];
+    const int64_t w = s.w;  // >= 4
+    const int G = gridDim.x, rank = blockIdx.x;
+    const int nloc = (int)((w + G - 1) / G);
+    double* Aloc = sh;                         // nloc x w
+    double* u = Aloc + (size_t)nloc * w;       // u_j
+    double* q = u + w;                         // q_j
+    double* rn = q + w;                        // row j+1 of A^(j+1)
+    double* un = rn + w;                       // u_{j+1}
+    __shared__ double red[2 * (kTriThreads / 32)];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kTriThreads / 32;
+    for (int lr = 0; lr < nloc; ++lr) {
+        const int64_t r = rank + (int64_t)G * lr;
+        for (int64_t c = tid; c < w; c += kTriThreads) Aloc[(size_t)lr * w + c] = r < w ? s.A[r * w + c] : 0.0;
+    }
+    double* pc = s.p;
+    double* pn = s.p2;
+    double alpha;
+    bool skip;
+    double beta = tri_hh(s.A + 1, w - 1, u, red, alpha, skip);
+    if (rank == 0) {
+        if (tid == 0) {
+            s.d[0] = s.A[0];
+            s.e[0] = alpha;
+            s.beta[0] = beta;
+        }
+        for (int64_t i = tid; i < w; i += kTriThreads) s.Uh[i] = (i > 0 && !skip) ? u[i - 1] : 0.0;
+    }
+    {
+        const int lr0 = rank >= 1 ? 0 : 1;  // rows r >= 1
+        for (int lr = lr0 + warp; lr < nloc; lr += nw) {
+            const int64_t r = rank + (int64_t)G * lr;
+            if (r >= w) break;
+            const double* ar = Aloc + (size_t)lr * w + 1;
+            double acc = 0.0;
+            for (int64_t c = lane; c < w - 1; c += 32) acc = fma(ar[c], u[c], acc);
+            acc = warp_sum(acc);
+            if (lane == 0) pc[r - 1] = beta * acc;
+        }
+    }
+    grid_barrier(s.bar, gridDim.x);
+    for (int64_t j = 0; j + 2 < w; ++j) {
+        const int64_t m = w - j - 1;
+        const bool last = j + 3 == w;
+        // p_j and row j+1 (published) from L2, loads issued together
+        constexpr int kPer = 4;  // w <= kPer * kTriThreads
+        double rowv[kPer];
+        const double* rowo = s.A + (j + 1) * w + (j + 1);
+#pragma unroll
+        for (int t = 0; t < kPer; ++t) {
+            const int64_t c = tid + (int64_t)t * kTriThreads;
+            rowv[t] = c < m ? __ldcg(rowo + c) : 0.0;
+        }
+        double kk = 0.0;
+        for (int64_t i = tid; i < m; i += kTriThreads) {
+            const double pv = __ldcg(pc + i);
+            q[i] = pv;
+            kk += u[i] * pv;
+        }
+        kk = 0.5 * beta * block_sum(kk, red);
+        for (int64_t i = tid; i < m; i += kTriThreads) q[i] -= kk * u[i];
+        __syncthreads();
+        {
+            const double u0 = u[0], q0 = q[0];
+#pragma unroll
+            for (int t = 0; t < kPer; ++t) {
+                const int64_t c = tid + (int64_t)t * kTriThreads;
+                if (c < m) rn[c] = rowv[t] - (u0 * q[c] + q0 * u[c]);
+            }
+        }
+        __syncthreads();
+        double beta_n = 0.0;
+        if (!last) {
+            double alpha_n;
+            bool skip_n;
+            beta_n = tri_hh(rn + 1, m - 1, un, red, alpha_n, skip_n);
+            if (rank == 0) {
+                if (tid == 0) {
+                    s.d[j + 1] = rn[0];
+                    s.e[j + 1] = alpha_n;
+                    s.beta[j + 1] = beta_n;
+                }
+                double* uh = s.Uh + (j + 1) * w;
+                for (int64_t i = tid; i < w; i += kTriThreads) uh[i] = (i > j + 1 && !skip_n) ? un[i - j - 2] : 0.0;
+            }
+        } else if (rank == 0 && tid == 0) {
+            s.d[j + 1] = rn[0];
+            s.e[j + 1] = rn[1];
+            s.beta[j + 1] = 0.0;
+        }
+        // own rows j+2 ..: update + dot with u_{j+1}; row j+2 is published
+        const int64_t first = j + 2;
+        const int lr0 = (int)((first - rank + G - 1) / G);
+        for (int lr = (lr0 > 0 ? lr0 : 0) + warp; lr < nloc; lr += nw) {
+            const int64_t r = rank + (int64_t)G * lr;
+            if (r >= w) break;
+            double* ar = Aloc + (size_t)lr * w + (j + 2);
+            const int64_t ir = r - j - 1;
+            const double ur = u[ir], qr = q[ir];
+            const bool pub = r == j + 2;
+            double* gout = s.A + r * w + (j + 2);
+            double acc = 0.0;
+            for (int64_t cc = lane; cc < m - 1; cc += 32) {
+                const double v = ar[cc] - (ur * q[cc + 1] + qr * u[cc + 1]);
+                ar[cc] = v;
+                if (pub) gout[cc] = v;
+                if (!last) acc = fma(v, un[cc], acc);
+            }
+            if (!last) {
+                acc = warp_sum(acc);
+                if (lane == 0) pn[r - j - 2] = beta_n * acc;
+            }
+        }
+        grid_barrier(s.bar, gridDim.x);
+        double* t = u;
+        u = un;
+        un = t;
+        t = pc;
+        pc = pn;
+        pn = t;
+        beta = beta_n;
+    }
+    if (rank == (int)((w - 1) % G) && tid == 0) {
+        s.d[w - 1] = Aloc[(size_t)((w - 1) / G) * w + (w - 1)];
+        s.e[w - 1] = 0.0;
+        s.beta[w - 1] = 0.0;
+    }
+    if (rank == 0)
+        for (int64_t jj = w - 2; jj < w; ++jj)
+            for (int64_t i = tid; i < w; i += kTriThreads) s.Uh[jj * w + i] = 0.0;
+}
+
 // Cluster-resident tridiagonalisation (w <= kClTriMaxW): the whole w x w
 // matrix lives in the distributed shared memory of one cluster of kClTri
 // CTAs (row r in CTA r % kClTri), so a column step costs two cluster
@@ -1301,7 +1440,25 @@ int syev_topk(int64_t w, const double* M, int64_t ldm, int64_t k, double* evals,
         }
     }
     if (!done) {
-        // one barrier per column (k_tridiag1) unless RSVD_TRIDIAG_TWO_BARRIER is set (A/B)
+        // one barrier per column (k_tridiag1) unless RSVD_TRIDIAG_TWO_BARRIER is set (A/B);
+        // the matrix in distributed shared memory (k_tridiag_sm) when it fits
+        const bool two = getenv("RSVD_TRIDIAG_TWO_BARRIER") != nullptr;
+        const bool one = w >= 4 && !two;
+        const int64_t gsm = sm_count();
+        const size_t smsz = ((size_t)cdiv(w, gsm) * w + 4 * w) * sizeof(double);
+        const bool dsm = one && w <= 4 * kTriThreads && smsz <= 220 * 1024 && getenv("RSVD_TRIDIAG_L2") == nullptr;
+        if (dsm) {
+            RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_tridiag_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smsz));
+            int per = 0;
+            RSVD_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tridiag_sm, kTriThreads, smsz));
+            RSVD_REQUIRE(per >= 1, "syev_topk: distributed tridiagonalisation cannot be resident");
+            void* args[] = {&s};
+            RSVD_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)k_tridiag_sm, dim3((unsigned)gsm),
+                                                        dim3(kTriThreads), args, smsz, st));
+            done = true;
+        }
+    }
+    if (!done) {
         const bool two = getenv("RSVD_TRIDIAG_TWO_BARRIER") != nullptr;
         const bool one = w >= 4 && !two;
         const void* kern = one ? (const void*)k_tridiag1 : (const void*)k_tridiag;
@@ -1312,7 +1469,9 @@ int syev_topk(int64_t w, const double* M, int64_t ldm, int64_t k, double* evals,
         int per_sm = 0;
         RSVD_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTriThreads, smem));
         RSVD_REQUIRE(per_sm >= 1, "syev_topk: tridiagonalisation kernel cannot be resident");
-        int64_t g = cdiv(w, kTriThreads / 32);
+        // one warp per trailing row at most; the one-barrier kernel's fused
+        // pass is latency bound, so it takes every SM (more rows in flight)
+        int64_t g = one ? cdiv(w, 8) : cdiv(w, kTriThreads / 32);
         if (g > sm_count()) g = sm_count();
         if (g < 1) g = 1;
         void* args[] = {&s};
