@@ -837,32 +837,61 @@ __global__ void k_tri_bounds(int64_t w, const double* __restrict__ d, const doub
 }
 
 // number of eigenvalues of T strictly below x (Sturm count with pivmin guard)
-__device__ __forceinline__ int sturm_count(int64_t w, const double* __restrict__ d, const double* __restrict__ e2,
-                                           double x, double pivmin) {
-    int cnt = 0;
-    double qv = d[0] - x;
-    if (fabs(qv) < pivmin) qv = -pivmin;
-    cnt += qv < 0.0;
-    for (int64_t i = 1; i < w; ++i) {
-        qv = (d[i] - x) - e2[i - 1] / qv;
-        if (fabs(qv) < pivmin) qv = -pivmin;
-        cnt += qv < 0.0;
-    }
-    return cnt;
-}
-
 __global__ void k_e2(int64_t w, const double* __restrict__ e, double* __restrict__ e2) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < w) e2[i] = e[i] * e[i];
 }
 
+// 1/q for the Sturm recurrence: the approximate FP64 reciprocal refined by two
+// Newton steps (a few ulp; the count is then exact for a tridiagonal within a
+// few ulp of T, the same backward-error class as with IEEE division, which
+// costs ~3x the instructions on this issue-bound recurrence).
+__device__ __forceinline__ double sturm_rcp(double q) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+    double e = fma(-q, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-q, r, 1.0);
+    return fma(r, e, r);
+}
+
+// NS Sturm sequences evaluated together (independent division chains: the
+// recurrence is latency bound, so interleaving hides most of it).
+#ifndef RSVD_STURM_DIV
+#define RSVD_STURM_DIV 0
+#endif
+template <int NS>
+__device__ __forceinline__ void sturm_count_n(int64_t w, const double* __restrict__ d, const double* __restrict__ e2,
+                                              const double* x, double pivmin, int* cnt) {
+    double qv[NS];
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+        qv[t] = d[0] - x[t];
+        if (fabs(qv[t]) < pivmin) qv[t] = -pivmin;
+        cnt[t] = qv[t] < 0.0;
+    }
+    for (int64_t i = 1; i < w; ++i) {
+        const double di = d[i], ei = e2[i - 1];
+#pragma unroll
+        for (int t = 0; t < NS; ++t) {
+            qv[t] = (di - x[t]) - ei * (RSVD_STURM_DIV ? 1.0 / qv[t] : sturm_rcp(qv[t]));
+            if (fabs(qv[t]) < pivmin) qv[t] = -pivmin;
+            cnt[t] += qv[t] < 0.0;
+        }
+    }
+}
+
 // eigenvalue number `idx` in ascending order; one warp per eigenvalue,
-// 32 Sturm counts per step (multisection).
+// 32 x kMsShifts Sturm counts per step (multisection: the bracket shrinks by
+// 32 kMsShifts + 1 per step).
+constexpr int kMsShifts = 1;  // 2 and 4 measured slower (w = 600: 4.6 -> 5.6 ms at 4): the divisions are issue bound
+
 __global__ void k_multisect(int64_t w, int64_t k, const double* __restrict__ d, const double* __restrict__ e2,
                             const double* __restrict__ bounds, double* __restrict__ evals) {
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (wid >= k) return;
+    constexpr int NP = 32 * kMsShifts;  // points per step
     const int64_t target = w - 1 - wid;  // wid-th largest
     double lo = bounds[0], hi = bounds[1];
     const double pivmin = bounds[3];
@@ -870,13 +899,18 @@ __global__ void k_multisect(int64_t w, int64_t k, const double* __restrict__ d, 
     for (int it = 0; it < 64; ++it) {
         const double width = hi - lo;
         if (!(width > 2.0 * eps * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin)) break;
-        const double x = lo + width * (double)(lane + 1) / 33.0;
-        const int c = sturm_count(w, d, e2, x, pivmin);
-        // count(x) <= target  <=>  eigenvalue #target is >= x
-        const unsigned below = __ballot_sync(0xffffffffu, c <= target);
-        const int nb = __popc(below);  // counts are monotone: lanes 0..nb-1 satisfy
-        const double nlo = nb > 0 ? lo + width * (double)nb / 33.0 : lo;
-        const double nhi = nb < 32 ? lo + width * (double)(nb + 1) / 33.0 : hi;
+        double x[kMsShifts];
+        int c[kMsShifts];
+#pragma unroll
+        for (int t = 0; t < kMsShifts; ++t) x[t] = lo + width * (double)(lane + 32 * t + 1) / (double)(NP + 1);
+        sturm_count_n<kMsShifts>(w, d, e2, x, pivmin, c);
+        // count(x) <= target  <=>  eigenvalue #target is >= x; counts are
+        // monotone in x, so points 0 .. nb-1 satisfy
+        int nb = 0;
+#pragma unroll
+        for (int t = 0; t < kMsShifts; ++t) nb += __popc(__ballot_sync(0xffffffffu, c[t] <= target));
+        const double nlo = nb > 0 ? lo + width * (double)nb / (double)(NP + 1) : lo;
+        const double nhi = nb < NP ? lo + width * (double)(nb + 1) / (double)(NP + 1) : hi;
         lo = nlo;
         hi = nhi;
     }
