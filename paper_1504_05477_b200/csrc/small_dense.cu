@@ -382,11 +382,13 @@ __device__ long long g_chol_trace[64];
 #define CHOL_T(i) do { } while (0)
 #endif
 constexpr int kSwThreadsMax = 512;
+constexpr int kChNB = 16;  // block-row height of the blocked factorization
 
 __global__ void __launch_bounds__(kSwThreadsMax)
 k_chol_sweep(int p, const double* __restrict__ G, int64_t ldg, const double* __restrict__ ref2, double tau2,
              double* __restrict__ T, int64_t ldt, int32_t* __restrict__ mask, int32_t* __restrict__ ndef,
-             int32_t* __restrict__ running, const int32_t* __restrict__ active, const int32_t* __restrict__ pred) {
+             int32_t* __restrict__ running, const int32_t* __restrict__ active, const int32_t* __restrict__ pred,
+             int blocked) {
     if (pred && *pred == 0) return;
     extern __shared__ double S[];
     __shared__ int s_row[kFastP];  // S[s_row[i] + j] = element (i, j), j >= i
@@ -408,33 +410,76 @@ k_chol_sweep(int p, const double* __restrict__ G, int64_t ldg, const double* __r
         for (int j = i + tx; j < p; j += 32) S[s_row[i] + j] = G[(int64_t)i * ldg + j];
     __syncthreads();
     CHOL_T(0);
-    for (int j = 0; j < p; ++j) {
-        const int rj = s_row[j];
-        // A: stage row j (unscaled); thread 0 takes the pivot decision
-        for (int c = j + tid; c < p; c += nt) s_vec[c] = S[rj + c];
-        if (tid == 0) {
-            const double d = S[rj + j];
-            const int inactive = s_msk[j] == 2;
-            const bool def = inactive || !(d > tau2 * s_ref[j]) || !(d > 0.0);
-            const double rjj = def ? 1.0 : sqrt(d);
-            s_piv[0] = def ? 0.0 : 1.0 / rjj;
-            s_piv[1] = rjj;
-            s_def = def;
-            if (def && !inactive) {
-                s_msk[j] = 1;
-                ++s_count;
+    // Right-looking, blocked by kChNB columns: a column step updates only the
+    // rows of its block row (all their columns); after the block row is done,
+    // the trailing triangle takes one rank-kChNB update (each element read and
+    // written once per block instead of once per column). Thread mapping of
+    // that update: one warp per (4-row group, 64-column chunk), lanes on
+    // columns c and c + 32, the 4 rows' R entries read by broadcast.
+    const int nb = blocked ? kChNB : p;
+    for (int k0 = 0; k0 < p; k0 += nb) {
+        const int k1 = min(k0 + nb, p);
+        for (int j = k0; j < k1; ++j) {
+            const int rj = s_row[j];
+            // A: stage row j (unscaled); thread 0 takes the pivot decision
+            for (int c = j + tid; c < p; c += nt) s_vec[c] = S[rj + c];
+            if (tid == 0) {
+                const double d = S[rj + j];
+                const int inactive = s_msk[j] == 2;
+                const bool def = inactive || !(d > tau2 * s_ref[j]) || !(d > 0.0);
+                const double rjj = def ? 1.0 : sqrt(d);
+                s_piv[0] = def ? 0.0 : 1.0 / rjj;
+                s_piv[1] = rjj;
+                s_def = def;
+                if (def && !inactive) {
+                    s_msk[j] = 1;
+                    ++s_count;
+                }
             }
+            __syncthreads();
+            // B: scale row j; rank-1 update of the block row's remaining rows
+            const double inv = s_piv[0];
+            if (ty == 0)
+                for (int c = j + tx; c < p; c += 32) S[rj + c] = (c == j) ? s_piv[1] : s_vec[c] * inv;
+            if (!s_def) {
+                for (int i = j + 1 + ty; i < k1; i += ny) {
+                    const double ui = s_vec[i] * inv;
+                    double* row = S + s_row[i];
+                    for (int c = i + tx; c < p; c += 32) row[c] = fma(-ui, s_vec[c] * inv, row[c]);
+                }
+            }
+            __syncthreads();
         }
-        __syncthreads();
-        // B: scale row j; rank-1 update of the trailing triangle with the scaled row
-        const double inv = s_piv[0];
-        if (ty == 0)
-            for (int c = j + tx; c < p; c += 32) S[rj + c] = (c == j) ? s_piv[1] : s_vec[c] * inv;
-        if (!s_def) {
-            for (int i = j + 1 + ty; i < p; i += ny) {
-                const double ui = s_vec[i] * inv;
+        if (k1 >= p) break;
+        // C: trailing update S[i][c] -= sum_{j in [k0,k1)} R[j][i] R[j][c], k1 <= i <= c
+        const int mt = p - k1;
+        const int ngr = (mt + 3) / 4, nch = (mt + 63) / 64;
+        for (int item = ty; item < ngr * nch; item += ny) {
+            const int g = item / nch, ch = item % nch;
+            const int i0 = k1 + 4 * g;
+            const int cbase = k1 + 64 * ch;
+            if (cbase + 63 < i0) continue;  // chunk entirely below the diagonal (warp-uniform)
+            const int c0 = cbase + tx, c1 = c0 + 32;
+            double acc[4][2];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) acc[a][0] = acc[a][1] = 0.0;
+            for (int j = k0; j < k1; ++j) {
+                const double* rjp = S + s_row[j];
+                const double b0 = c0 < p ? rjp[c0] : 0.0, b1 = c1 < p ? rjp[c1] : 0.0;
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const double ra = i0 + a < p ? rjp[i0 + a] : 0.0;
+                    acc[a][0] = fma(ra, b0, acc[a][0]);
+                    acc[a][1] = fma(ra, b1, acc[a][1]);
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int i = i0 + a;
+                if (i >= p) break;
                 double* row = S + s_row[i];
-                for (int c = i + tx; c < p; c += 32) row[c] = fma(-ui, s_vec[c] * inv, row[c]);
+                if (c0 >= i && c0 < p) row[c0] -= acc[a][0];
+                if (c1 >= i && c1 < p) row[c1] -= acc[a][1];
             }
         }
         __syncthreads();
@@ -593,7 +638,9 @@ int chol_deflate(int64_t p, const double* G, int64_t ldg, const double* ref2, do
         if (sm > 48 * 1024)
             RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_chol_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         const int nt = p <= 64 ? 128 : (p <= 128 ? 256 : kSwThreadsMax);
-        k_chol_sweep<<<1, nt, sm, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active, pred);
+        const int blocked = getenv("RSVD_CHOL_UNBLOCKED") == nullptr;  // A/B switch
+        k_chol_sweep<<<1, nt, sm, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active, pred,
+                                         blocked);
         RSVD_CHECK_LAUNCH();
         return RSVD_OK;
     }

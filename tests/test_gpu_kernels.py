@@ -107,6 +107,38 @@ def test_chol_deflate_full_rank_and_deficient(ops):
     assert np.max(np.abs(qk.T @ qk - np.eye(len(keep)))) < 1e-10
 
 
+@pytest.mark.parametrize("p", [65, 100, 200, 224])
+def test_chol_deflate_blocked_wide(ops, monkeypatch, p):
+    """Blocked right-looking factorization (p > 64, k_chol_sweep): the same
+    deflation decisions, ndef/running bookkeeping and R^-1 (to rounding) as
+    the column-by-column sweep, with deficient columns inside and across the
+    16-column block rows, and an inactive column."""
+    v = _rand((3 * p, p), 40 + p)
+    for j, (a, b) in {5: (0, 3), 17: (2, 9), 40: (16, 33), p - 2: (1, p - 3)}.items():
+        v[:, j] = v[:, a] - 0.5 * v[:, b]
+    G = _t(v.T @ v)
+    active = torch.ones(p, dtype=torch.int32, device="cuda")
+    active[p // 2] = 0
+    out = {}
+    for mode in ("blocked", "unblocked"):
+        if mode == "unblocked":
+            monkeypatch.setenv("RSVD_CHOL_UNBLOCKED", "1")
+        T = torch.empty((p, p), dtype=torch.float64, device="cuda")
+        mask = torch.empty(p, dtype=torch.int32, device="cuda")
+        ndef = torch.zeros(2, dtype=torch.int32, device="cuda")
+        running = torch.tensor([3], dtype=torch.int32, device="cuda")
+        ops.chol_deflate(G, None, 1e-14, T, mask, ndef, running, active)
+        out[mode] = (T.cpu().numpy(), mask.cpu().numpy(), ndef.cpu().tolist(), int(running[0]))
+    Tb, mb, nb, rb = out["blocked"]
+    Tu, mu, nu, ru = out["unblocked"]
+    assert list(np.nonzero(mb)[0]) == [5, 17, 40, p - 2]
+    assert np.array_equal(mb, mu) and nb == nu == [4, 3] and rb == ru == 7
+    assert np.max(np.abs(Tb - Tu)) <= 1e-9 * np.max(np.abs(Tu))
+    keep = [j for j in range(p) if not mb[j] and j != p // 2]
+    qk = (v @ Tb)[:, keep]
+    assert np.max(np.abs(qk.T @ qk - np.eye(len(keep)))) < 1e-9
+
+
 def test_fill_stream_matches_host_stream(ops):
     n = 1001  # odd: each vector consumes n+1 uniforms (matrix.py:44-47)
     dev = ops.fill_stream(n, 3, o.QR_FILL_SEED, "cuda").cpu().numpy()
