@@ -616,6 +616,98 @@ k_chol_reg64(int p, const double* __restrict__ G, int64_t ldg, const double* __r
     CHOL_T(3);
 }
 
+#ifndef RSVD_CHOL_UNROLL
+#define RSVD_CHOL_UNROLL 1
+#endif
+constexpr int kChUnroll = RSVD_CHOL_UNROLL;
+// Compact form of k_chol_reg64 (same arithmetic, same order, bitwise equal
+// results): the steps are a real loop and every register index is static
+// because the register window rotates by one each step (r[0] is always the
+// current pivot row's entry). The fully unrolled kernel is 64 KB of
+// straight-line code, fetched cold from HBM on every call inside a
+// factorization (the chain's 2 GB stream evicts it from L2): 83 us cold vs
+// 34 us warm at p = 50. This one is ~3 KB.
+__global__ void __launch_bounds__(kRegP)
+k_chol_reg64c(int p, const double* __restrict__ G, int64_t ldg, const double* __restrict__ ref2, double tau2,
+              double* __restrict__ T, int64_t ldt, int32_t* __restrict__ mask, int32_t* __restrict__ ndef,
+              int32_t* __restrict__ running, const int32_t* __restrict__ active, const int32_t* __restrict__ pred) {
+    if (pred && *pred == 0) return;
+    __shared__ double Rs[kRegP][kRegP + 1];  // R(i, c) = Rs[i][c]
+    __shared__ double s_row[2 * kRegP];      // scaled row j (entries >= kRegP stay 0)
+    __shared__ double s_piv[2];
+    __shared__ double s_rinv[kRegP];
+    __shared__ int s_msk[kRegP];
+    __shared__ int s_def, s_count;
+    const int t = threadIdx.x;
+    const bool mine = t < p;
+    double r[kRegP];  // r[i] = element (j + i, t) at step j
+#pragma unroll
+    for (int i = 0; i < kRegP; ++i) r[i] = (mine && i <= t) ? G[(int64_t)i * ldg + t] : 0.0;
+    const double myref = mine ? (ref2 ? ref2[t] : G[(int64_t)t * ldg + t]) : 0.0;
+    const int myinact = mine ? (active && active[t] == 0) : 1;
+    s_msk[t] = myinact && mine ? 2 : 0;
+    s_row[kRegP + t] = 0.0;
+    if (t == 0) s_count = 0;
+    __syncthreads();
+#pragma unroll (kChUnroll)
+    for (int j = 0; j < p; ++j) {
+        if (t == j) {
+            const double d = r[0];
+            const bool def = myinact || !(d > tau2 * myref) || !(d > 0.0);
+            const double inv = def ? 0.0 : rsqrt(d);
+            s_piv[0] = inv;
+            s_piv[1] = def ? 1.0 : d * inv;
+            s_rinv[j] = def ? 1.0 : inv;
+            s_def = def;
+            if (def && !myinact) {
+                s_msk[j] = 1;
+                ++s_count;
+            }
+        }
+        __syncthreads();
+        const double inv = s_piv[0];
+        if (t == j) r[0] = s_piv[1];
+        else if (t > j) r[0] *= inv;
+        s_row[t] = r[0];  // R(j, t) for t > j
+        Rs[j][t] = (mine && j <= t) ? r[0] : 0.0;
+        const bool def = s_def;
+        __syncthreads();
+        if (!def) {
+            const double rj = r[0];
+#pragma unroll
+            for (int i = 1; i < kRegP; ++i) r[i] = fma(-s_row[j + i], rj, r[i]);
+        }
+#pragma unroll
+        for (int i = 0; i + 1 < kRegP; ++i) r[i] = r[i + 1];
+        r[kRegP - 1] = 0.0;
+    }
+    for (int j = p; j < kRegP; ++j) Rs[j][t] = 0.0;
+    __syncthreads();
+    // column t of T: R x = e_t from the bottom; y[m] = x[i - m] at step i
+    double y[kRegP];
+#pragma unroll
+    for (int m = 0; m < kRegP; ++m) y[m] = (p - 1 - m == t) ? 1.0 : 0.0;
+    const bool zc = mine && s_msk[t] != 0;
+#pragma unroll (kChUnroll)
+    for (int i = p - 1; i >= 0; --i) {
+        const double xi = y[0] * s_rinv[i];
+        if (mine) T[(int64_t)i * ldt + t] = (i > t || zc || s_msk[i]) ? 0.0 : xi;
+#pragma unroll
+        for (int m = 1; m < kRegP; ++m)
+            if (i - m >= 0) y[m] = fma(-Rs[i - m][i], xi, y[m]);
+#pragma unroll
+        for (int m = 0; m + 1 < kRegP; ++m) y[m] = y[m + 1];
+        y[kRegP - 1] = 0.0;
+    }
+    if (mine) mask[t] = s_msk[t] == 1 ? 1 : 0;
+    if (t == 0) {
+        const int32_t base = running ? running[0] : 0;
+        ndef[0] = s_count;
+        ndef[1] = base;
+        if (running) running[0] = base + s_count;
+    }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -629,7 +721,11 @@ int chol_deflate(int64_t p, const double* G, int64_t ldg, const double* ref2, do
     if (p == 0) return RSVD_OK;
     static const bool force_sweep = getenv("RSVD_CHOL_SWEEP") != nullptr;  // A/B experiments
     if (p <= kRegP && !force_sweep) {
-        k_chol_reg64<<<1, kRegP, 0, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active, pred);
+        if (getenv("RSVD_CHOL_REG_UNROLLED") != nullptr)  // A/B: the fully unrolled kernel
+            k_chol_reg64<<<1, kRegP, 0, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active, pred);
+        else
+            k_chol_reg64c<<<1, kRegP, 0, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active,
+                                               pred);
         RSVD_CHECK_LAUNCH();
         return RSVD_OK;
     }

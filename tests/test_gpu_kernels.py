@@ -107,6 +107,34 @@ def test_chol_deflate_full_rank_and_deficient(ops):
     assert np.max(np.abs(qk.T @ qk - np.eye(len(keep)))) < 1e-10
 
 
+@pytest.mark.parametrize("p", [1, 7, 33, 50, 64])
+def test_chol_reg64_compact_matches_unrolled(ops, monkeypatch, p):
+    """p <= 64: the compact rotating-register kernel (default) against the
+    fully unrolled one -- same operations in the same order, bitwise equal
+    T, mask and counts (deficient and inactive columns included)."""
+    v = _rand((4 * p + 8, p), 60 + p)
+    if p >= 7:
+        v[:, 5] = v[:, 1] - 2.0 * v[:, 3]
+    G = _t(v.T @ v)
+    active = torch.ones(p, dtype=torch.int32, device="cuda")
+    if p >= 33:
+        active[p - 3] = 0
+    outs = []
+    for mode in ("compact", "unrolled"):
+        if mode == "unrolled":
+            monkeypatch.setenv("RSVD_CHOL_REG_UNROLLED", "1")
+        T = torch.empty((p, p), dtype=torch.float64, device="cuda")
+        mask = torch.empty(p, dtype=torch.int32, device="cuda")
+        ndef = torch.zeros(2, dtype=torch.int32, device="cuda")
+        running = torch.tensor([2], dtype=torch.int32, device="cuda")
+        ops.chol_deflate(G, None, 1e-14, T, mask, ndef, running, active)
+        outs.append((T.clone(), mask.clone(), ndef.clone(), running.clone()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    if p >= 7:
+        assert int(outs[0][1][5]) == 1
+
+
 @pytest.mark.parametrize("p", [65, 100, 200, 224])
 def test_chol_deflate_blocked_wide(ops, monkeypatch, p):
     """Blocked right-looking factorization (p > 64, k_chol_sweep): the same
