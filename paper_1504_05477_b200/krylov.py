@@ -171,6 +171,9 @@ _PROJ_ENV = os.environ.get("RSVD_PROJ_PASSES")
 # Device-decided sections as CUDA-graph conditional nodes (RSVD_GRAPH_COND=0:
 # predicated kernels only, for A/B measurement).
 GRAPH_COND = os.environ.get("RSVD_GRAPH_COND", "1") != "0"
+# Projected block-Krylov basis: first projection's coefficients formed in
+# d-space from W = A^T Q (RSVD_DSPACE_PASS1=0: from Q^T V, A/B).
+D_SPACE_PASS1 = os.environ.get("RSVD_DSPACE_PASS1", "1") != "0"
 
 
 def proj_passes(dtype):
@@ -180,7 +183,7 @@ def proj_passes(dtype):
 
 
 def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=None, row_offset=0,
-               tau=None, deflation_count=None, two_round=None):
+               tau=None, deflation_count=None, two_round=None, pass1_coef=None):
     """Orthonormalize the n x p block V in place (span-preserving, column
     order preserving), against the orthonormal columns Qp when given.
 
@@ -212,7 +215,14 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
     has_prev = Qp is not None and Qp.shape[1] > 0
     tmp_c = torch.empty((Qp.shape[1], p), dtype=dtype, device=V.device) if has_prev else None
     if has_prev:
-        for _ in range(proj_passes(dtype)):
+        npass = proj_passes(dtype)
+        if pass1_coef is not None:
+            # first pass with coefficients formed in d-space by the caller
+            # (bk_basis: Qp^T A C = (A^T Qp)^T C); the remaining passes and
+            # the final pass project with Qp^T V itself
+            ops.gemm_nn(Qp, pass1_coef, V, alpha=-1.0, beta=1.0)
+            npass -= 1
+        for _ in range(npass):
             project_out(ops, comm, Qp, V, tmp_c)
     G = ws.G[:p, :p]
     T = ws.T[:p, :p]
@@ -369,6 +379,7 @@ def bk_basis(ops, comm, op, Pi, q, ws, n_total, row_offset):
         # into W and only A^T q_last is added at the end: one width-p pass
         # over A instead of a width-w one.
         W = rows_buffer(d, n_blocks * p, dt, dev)
+        coef = torch.empty((n_blocks * p, p), dtype=dt, device=dev)
         for j in range(1, n_blocks):
             prev = K[:, (j - 1) * p: j * p]
             cur = K[:, j * p: (j + 1) * p]
@@ -379,8 +390,16 @@ def bk_basis(ops, comm, op, Pi, q, ws, n_total, row_offset):
             ref2 = ws.ref2[:p]
             ops.colreduce(cur, True, ref2)
             comm.allreduce(ref2)
+            c1 = None
+            if D_SPACE_PASS1:
+                # cur = A Cj, so Qp^T cur = (A^T Qp)^T Cj = W[:, :jp]^T Cj: the
+                # first projection's coefficients from the d x jp prefix of W
+                # (replicated across ranks: no allreduce) instead of a pass
+                # over the n x jp basis
+                c1 = coef[: j * p]
+                ops.gemm_tn(W[:, : j * p], Cj, c1)
             orth_block(ops, comm, cur, tmp, ws, Qp=K[:, : j * p], ref2=ref2, running=running,
-                       n_total=n_total, row_offset=row_offset, deflation_count=deflated)
+                       n_total=n_total, row_offset=row_offset, deflation_count=deflated, pass1_coef=c1)
         last = W[:, (n_blocks - 1) * p:]
         op.apply_t(K[:, (n_blocks - 1) * p:], last)
         comm.allreduce(last)
