@@ -740,7 +740,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 // Transposes through a 32 x 33 shared tile.
 // Grid-stride over the 32 x 32 tiles (at most a few CTAs per SM), so a
 // launch whose device predicate is off retires in microseconds even when B
-// is an n x p block (C4: 218k tiles).
+// is an n x p block (C4: 218k tiles). The next tile's loads are issued before
+// the current tile is transposed and stored (register double buffer). Plane
+// columns >= N are left unwritten: they only feed output columns >= n, which
+// are never stored.
 __global__ void __launch_bounds__(256) k_split_b(int64_t K, int64_t N, const float* __restrict__ B, int64_t ldb,
                                                  int64_t Kp, int64_t Np, float* __restrict__ out,
                                                  const int32_t* __restrict__ pred) {
@@ -748,22 +751,38 @@ __global__ void __launch_bounds__(256) k_split_b(int64_t K, int64_t N, const flo
     __shared__ float t[32][33];
     const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
     const int64_t tk = Kp / 32, tiles = tk * (Np / 32);
-    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    auto load = [&](int64_t tile, float (&v)[4]) {
         const int64_t k0 = (tile % tk) * 32, c0 = (tile / tk) * 32;
-        for (int i = ty; i < 32; i += 8) {
-            const int64_t r = k0 + i, c = c0 + tx;
-            t[i][tx] = (r < K && c < N) ? B[r * ldb + c] : 0.f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t r = k0 + ty + 8 * q, c = c0 + tx;
+            v[q] = (r < K && c < N) ? __ldg(B + r * ldb + c) : 0.f;
         }
+    };
+    float cur[4], nxt[4];
+    int64_t tile = blockIdx.x;
+    if (tile < tiles) load(tile, cur);
+    for (; tile < tiles; tile += gridDim.x) {
+        const int64_t nt = tile + gridDim.x;
+        if (nt < tiles) load(nt, nxt);
+        const int64_t k0 = (tile % tk) * 32, c0 = (tile / tk) * 32;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) t[ty + 8 * q][tx] = cur[q];
         __syncthreads();
         float* blk = out + (k0 / 32) * (2 * Np) * 32;  // k0 is a multiple of 32
-        for (int i = ty; i < 32; i += 8) {
-            const int64_t c = c0 + i;
-            const float x = t[tx][i];
-            const float h = tf32_hi(x);
-            blk[c * 32 + tx] = h;
-            blk[(Np + c) * 32 + tx] = tf32_rna(x - h);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t c = c0 + ty + 8 * q;
+            if (c < N) {
+                const float x = t[tx][ty + 8 * q];
+                const float h = tf32_hi(x);
+                blk[c * 32 + tx] = h;
+                blk[(Np + c) * 32 + tx] = tf32_rna(x - h);
+            }
         }
         __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
     }
 }
 
