@@ -16,11 +16,23 @@ __global__ void k_colreduce_partial(int64_t n, int64_t p, const T* __restrict__ 
     const int64_t r0 = (int64_t)blockIdx.y * rows_per_chunk;
     const int64_t r1 = min(n, r0 + rows_per_chunk);
     double acc = 0.0;
-    if (c < p)
-        for (int64_t r = r0 + ly; r < r1; r += kColRows) {
+    if (c < p) {
+        // 8 rows' loads in flight per thread (the chunk is thousands of rows
+        // long; one load at a time made this latency bound); the sum is still
+        // accumulated in row order
+        int64_t r = r0 + ly;
+        for (; r + 7 * kColRows < r1; r += 8 * kColRows) {
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = (double)X[(r + q * kColRows) * ldx + c];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc += square ? v[q] * v[q] : v[q];
+        }
+        for (; r < r1; r += kColRows) {
             double v = (double)X[r * ldx + c];
             acc += square ? v * v : v;
         }
+    }
     red[ly][lx] = acc;
     __syncthreads();
     if (ly == 0 && c < p) {
