@@ -105,16 +105,33 @@ __global__ void k_absargmax_partial(int64_t n, int64_t k, const T* __restrict__ 
     const int64_t r1 = min(n, r0 + rows_per_chunk);
     double best = -1.0, bsig = 0.0;
     int64_t bi = INT64_MAX;
-    if (c < k)
-        for (int64_t r = r0 + ly; r < r1; r += kColRows) {
+    if (c < k) {
+        // rows visited in increasing order (first max kept); 8 loads in flight
+        int64_t r = r0 + ly;
+        for (; r + 7 * kColRows < r1; r += 8 * kColRows) {
+            double xs[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) xs[q] = (double)X[(r + q * kColRows) * ldx + c];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const double v = fabs(xs[q]);
+                if (v > best) {
+                    best = v;
+                    bsig = xs[q];
+                    bi = r + q * kColRows;
+                }
+            }
+        }
+        for (; r < r1; r += kColRows) {
             double x = (double)X[r * ldx + c];
             double v = fabs(x);
-            if (v > best) {  // rows visited in increasing order: first max kept
+            if (v > best) {
                 best = v;
                 bsig = x;
                 bi = r;
             }
         }
+    }
     sv[ly][lx] = best;
     ss[ly][lx] = bsig;
     si[ly][lx] = bi;
