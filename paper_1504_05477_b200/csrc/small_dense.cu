@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(kSwThreadsMax)
 k_chol_sweep(int p, const double* __restrict__ G, int64_t ldg, const double* __restrict__ ref2, double tau2,
              double* __restrict__ T, int64_t ldt, int32_t* __restrict__ mask, int32_t* __restrict__ ndef,
              int32_t* __restrict__ running, const int32_t* __restrict__ active, const int32_t* __restrict__ pred,
-             int blocked) {
+             int blocked, int inv_blocked) {
     if (pred && *pred == 0) return;
     extern __shared__ double S[];
     __shared__ int s_row[kFastP];  // S[s_row[i] + j] = element (i, j), j >= i
@@ -485,22 +485,71 @@ k_chol_sweep(int p, const double* __restrict__ G, int64_t ldg, const double* __r
         __syncthreads();
     }
     CHOL_T(1);
-    for (int i = p - 1; i >= 0; --i) {
-        const int ri = s_row[i];
-        // A: stage column i (rows k < i) and row i of the accumulated inverse
-        for (int k = tid; k < i; k += nt) s_vec[k] = S[s_row[k] + i];
-        for (int c = i + tid; c < p; c += nt) s_vec2[c] = S[ri + c];
+    // In-place inversion from the bottom. Blocked (inv_blocked): the rows of a
+    // kChNB-row block are finalised one by one updating only the block's own
+    // rows; then every row above takes the block's contribution in one pass
+    //   X[k][c] = -sum_{i0 <= i <= c} R[k][i] T[i][c]   (c inside the block:
+    //             the entry held R[k][c] and is replaced, as the column step does)
+    //   X[k][c] -= sum_{i in block} R[k][i] T[i][c]     (c past the block)
+    // with the block's R[k][i] staged in Rb first (the pass overwrites them).
+    const int nbi = inv_blocked ? kChNB : p;
+    double* Rb = S + (p * (p + 1)) / 2;  // [p][kChNB] (inv_blocked only)
+    for (int i1 = p; i1 > 0; i1 -= nbi) {
+        const int i0 = max(0, i1 - nbi);
+        for (int i = i1 - 1; i >= i0; --i) {
+            const int ri = s_row[i];
+            // A: stage column i (block rows k < i) and row i of the accumulated inverse
+            for (int k = i0 + tid; k < i; k += nt) s_vec[k] = S[s_row[k] + i];
+            for (int c = i + tid; c < p; c += nt) s_vec2[c] = S[ri + c];
+            __syncthreads();
+            // B: row i of T = accumulated row / R_ii; block rows k < i: X[k][c] -= R[k][i] T[i][c]
+            const double rinv = 1.0 / s_vec2[i];
+            if (ty == 0)
+                for (int c = i + tx; c < p; c += 32) S[ri + c] = (c == i) ? rinv : s_vec2[c] * rinv;
+            for (int k = i0 + ty; k < i; k += ny) {
+                const double rk = s_vec[k];
+                double* row = S + s_row[k];
+                for (int c = i + tx; c < p; c += 32) {
+                    const double tic = (c == i) ? rinv : s_vec2[c] * rinv;
+                    row[c] = (c == i) ? -rk * tic : fma(-rk, tic, row[c]);
+                }
+            }
+            __syncthreads();
+        }
+        if (i0 == 0 || !inv_blocked) continue;
+        const int nb = i1 - i0;
+        for (int e = tid; e < i0 * kChNB; e += nt) {
+            const int k = e / kChNB, ii = e % kChNB;
+            Rb[e] = ii < nb ? S[s_row[k] + i0 + ii] : 0.0;
+        }
         __syncthreads();
-        // B: row i of T = accumulated row / R_ii; rows k < i: X[k][c] -= R[k][i] T[i][c]
-        const double rinv = 1.0 / s_vec2[i];
-        if (ty == 0)
-            for (int c = i + tx; c < p; c += 32) S[ri + c] = (c == i) ? rinv : s_vec2[c] * rinv;
-        for (int k = ty; k < i; k += ny) {
-            const double rk = s_vec[k];
-            double* row = S + s_row[k];
-            for (int c = i + tx; c < p; c += 32) {
-                const double tic = (c == i) ? rinv : s_vec2[c] * rinv;
-                row[c] = (c == i) ? -rk * tic : fma(-rk, tic, row[c]);
+        const int ngr = (i0 + 3) / 4, nch = (p - i0 + 63) / 64;
+        for (int item = ty; item < ngr * nch; item += ny) {
+            const int g = item / nch, ch = item % nch;
+            const int k0 = 4 * g;
+            const int c0 = i0 + 64 * ch + tx, c1 = c0 + 32;
+            double acc[4][2];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) acc[a][0] = acc[a][1] = 0.0;
+            for (int ii = 0; ii < nb; ++ii) {
+                const int i = i0 + ii;
+                const double* ti = S + s_row[i];
+                const double t0 = (c0 >= i && c0 < p) ? ti[c0] : 0.0;
+                const double t1 = (c1 >= i && c1 < p) ? ti[c1] : 0.0;
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const double rk = k0 + a < i0 ? Rb[(k0 + a) * kChNB + ii] : 0.0;
+                    acc[a][0] = fma(rk, t0, acc[a][0]);
+                    acc[a][1] = fma(rk, t1, acc[a][1]);
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int k = k0 + a;
+                if (k >= i0) break;
+                double* row = S + s_row[k];
+                if (c0 < p) row[c0] = c0 < i1 ? -acc[a][0] : row[c0] - acc[a][0];
+                if (c1 < p) row[c1] = c1 < i1 ? -acc[a][1] : row[c1] - acc[a][1];
             }
         }
         __syncthreads();
@@ -730,13 +779,17 @@ int chol_deflate(int64_t p, const double* G, int64_t ldg, const double* ref2, do
         return RSVD_OK;
     }
     if (p <= kFastP) {
-        const size_t sm = (size_t)(p * (p + 1) / 2) * sizeof(double);
+        const size_t tri = (size_t)(p * (p + 1) / 2) * sizeof(double);
+        const int blocked = getenv("RSVD_CHOL_UNBLOCKED") == nullptr;  // A/B switch
+        // blocked inversion needs a p x kChNB staging block next to the triangle
+        const size_t smb = tri + (size_t)p * kChNB * sizeof(double);
+        const int inv_blocked = blocked && smb <= 200 * 1024;
+        const size_t sm = inv_blocked ? smb : tri;
         if (sm > 48 * 1024)
             RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_chol_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         const int nt = p <= 64 ? 128 : (p <= 128 ? 256 : kSwThreadsMax);
-        const int blocked = getenv("RSVD_CHOL_UNBLOCKED") == nullptr;  // A/B switch
         k_chol_sweep<<<1, nt, sm, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active, pred,
-                                         blocked);
+                                         blocked, inv_blocked);
         RSVD_CHECK_LAUNCH();
         return RSVD_OK;
     }
