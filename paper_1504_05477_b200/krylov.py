@@ -128,6 +128,7 @@ class Workspace:
         self.ref2 = torch.empty(p, **f64)
         self.ref_orig = torch.empty(p, **f64)
         self.ndef_total = torch.zeros(1, **i32)
+        self.flag_bool = torch.zeros(1, dtype=torch.bool, device=device)
 
 
 def rows_buffer(n, p, dtype, device):
@@ -171,6 +172,9 @@ _PROJ_ENV = os.environ.get("RSVD_PROJ_PASSES")
 # Device-decided sections as CUDA-graph conditional nodes (RSVD_GRAPH_COND=0:
 # predicated kernels only, for A/B measurement).
 GRAPH_COND = os.environ.get("RSVD_GRAPH_COND", "1") != "0"
+# Second FP64 CholeskyQR step on the Ritz vectors only when one step leaves
+# ||Z^T Z - I||max above this (or a column was refilled).
+Z_REORTH_TOL = 1e-13
 # Projected block-Krylov basis: first projection's coefficients formed in
 # d-space from W = A^T Q (RSVD_DSPACE_PASS1=0: from Q^T V, A/B).
 D_SPACE_PASS1 = os.environ.get("RSVD_DSPACE_PASS1", "1") != "0"
@@ -491,19 +495,46 @@ def rayleigh_ritz(ops, comm, op, Q, k, n_total, row_offset, sign_fn=None, W=None
         ops.convert(Uk, Uk32)
         Z32 = rows_buffer(n, k, Q.dtype, dev)
         ops.gemm_nn(Q, Uk32, Z32)
-        Z = rows_buffer(n, k, torch.float64, dev)
-        ops.convert(Z32, Z)
-        # FP64 re-orthonormalization of the n x k Z (CholeskyQR2)
+        Z0 = rows_buffer(n, k, torch.float64, dev)
+        ops.convert(Z32, Z0)
+        # FP64 re-orthonormalization of the n x k Z. Z = Q U_k
+        # with Q orthonormal to FP32 precision, so cond(Z) ~ 1 and one FP64
+        # CholeskyQR step leaves ||Z^T Z - I|| at ~1e-15; the second step runs
+        # (device-decided, a graph IF node under capture) only if the check
+        # Gram says otherwise (or a column had to be refilled). The check Gram
+        # also gives the orthogonality error reported with the result (the
+        # sign canonicalization below only negates columns).
         ws = Workspace(dev, k)
-        tmp = rows_buffer(n, k, torch.float64, dev)
-        orth_block(ops, comm, Z, tmp, ws, tau=0.0, n_total=n_total, row_offset=row_offset)
+        Z = rows_buffer(n, k, torch.float64, dev)
+        G = ws.G
+        ops.gram(Z0, G)
+        comm.allreduce(G)
+        ops.chol_deflate(G, None, 0.0, ws.T, ws.mask, ws.ndef)
+        ops.gemm_nn(Z0, ws.T, Z)
+        ops.insert_fill(Z, ws.mask, ws.ndef, QR_FILL_SEED, row_offset, n_total, pred=ws.ndef)
+        G2 = torch.empty((k, k), dtype=torch.float64, device=dev)
+        ops.gram(Z, G2)
+        comm.allreduce(G2)
+        zerr = ops.ortho_error(G2)
+        again = ws.ndef2[:1]
+        torch.gt(zerr, Z_REORTH_TOL, out=ws.flag_bool)
+        again.copy_(ws.flag_bool)
+        again.add_(ws.ndef[:1])
+        with ops.cond_section(again, GRAPH_COND and isinstance(comm, LocalComm)):
+            ops.chol_deflate(G2, None, 0.0, ws.T, ws.mask2, ws.ndef_r3, pred=again)
+            ops.gemm_nn(Z, ws.T, Z0, pred=again)
+            ops.convert(Z0, Z, pred=again)
+            ops.gram(Z, G2, pred=again)
+            comm.allreduce(G2)
+            ops.ortho_error(G2, zerr)  # unchanged G2 (gram skipped) gives the same zerr
     if sign_fn is None:
         ops.canonicalize_signs(Z)
     else:
         sign_fn(Z)
     sigma = ops.sqrt_clip(evals)
-    G = torch.empty((k, k), dtype=torch.float64, device=dev)
-    ops.gram(Z, G)
-    comm.allreduce(G)
-    zerr = ops.ortho_error(G)
+    if Q.dtype == torch.float64:
+        G = torch.empty((k, k), dtype=torch.float64, device=dev)
+        ops.gram(Z, G)
+        comm.allreduce(G)
+        zerr = ops.ortho_error(G)
     return RitzResult(Z, sigma, info, off, zerr)

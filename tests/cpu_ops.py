@@ -173,6 +173,9 @@ def sqrt_clip(x, out=None):
 
 def ortho_error(G, out=None):
     e = (G - torch.eye(G.shape[0], dtype=G.dtype)).abs().max().view(1)
+    if out is not None:
+        out.copy_(e)
+        return out
     return e
 
 
