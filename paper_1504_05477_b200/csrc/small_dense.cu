@@ -757,6 +757,128 @@ k_chol_reg64c(int p, const double* __restrict__ G, int64_t ldg, const double* __
     }
 }
 
+// k_chol_reg64c with two threads per column (128 threads): thread (c, h)
+// holds rows 32h .. 32h+31 of column c, and only the half that contains the
+// current pivot row rotates its window, so each thread shifts and updates at
+// most 32 registers per step. Every matrix entry still sees the same
+// operations in the same order (bitwise equal to k_chol_reg64c); the
+// inversion needs one extra barrier per row to hand x_i to the other half.
+constexpr int kRegH = 32;
+
+__global__ void __launch_bounds__(2 * kRegP)
+k_chol_reg64h(int p, const double* __restrict__ G, int64_t ldg, const double* __restrict__ ref2, double tau2,
+              double* __restrict__ T, int64_t ldt, int32_t* __restrict__ mask, int32_t* __restrict__ ndef,
+              int32_t* __restrict__ running, const int32_t* __restrict__ active, const int32_t* __restrict__ pred) {
+    if (pred && *pred == 0) return;
+    __shared__ double Rs[kRegP][kRegP + 1];
+    __shared__ double s_row[2 * kRegP];
+    __shared__ double s_x[kRegP];
+    __shared__ double s_piv[2];
+    __shared__ double s_rinv[kRegP];
+    __shared__ int s_msk[kRegP];
+    __shared__ int s_def, s_count;
+    const int c = threadIdx.x & (kRegP - 1), h = threadIdx.x >> 6;
+    const bool mine = c < p;
+    const int rbase = kRegH * h;  // first row of this half
+    double r[kRegH];              // r[i] = element (row_lo + i, c); row_lo = rbase, or j while rotating
+#pragma unroll
+    for (int i = 0; i < kRegH; ++i) {
+        const int row = rbase + i;
+        r[i] = (mine && row <= c) ? G[(int64_t)row * ldg + c] : 0.0;
+    }
+    const double myref = mine ? (ref2 ? ref2[c] : G[(int64_t)c * ldg + c]) : 0.0;
+    const int myinact = mine ? (active && active[c] == 0) : 1;
+    if (h == 0) {
+        s_msk[c] = myinact && mine ? 2 : 0;
+        s_row[kRegP + c] = 0.0;
+    }
+    if (threadIdx.x == 0) s_count = 0;
+    __syncthreads();
+#pragma unroll 1
+    for (int j = 0; j < p; ++j) {
+        const int hj = j >> 5;
+        const bool rot = h == hj;  // this half holds row j (its r[0])
+        if (rot && c == j) {
+            const double d = r[0];
+            const bool def = myinact || !(d > tau2 * myref) || !(d > 0.0);
+            const double inv = def ? 0.0 : rsqrt(d);
+            s_piv[0] = inv;
+            s_piv[1] = def ? 1.0 : d * inv;
+            s_rinv[j] = def ? 1.0 : inv;
+            s_def = def;
+            if (def && !myinact) {
+                s_msk[j] = 1;
+                ++s_count;
+            }
+        }
+        __syncthreads();
+        if (rot) {
+            const double inv = s_piv[0];
+            if (c == j) r[0] = s_piv[1];
+            else if (c > j) r[0] *= inv;
+            s_row[c] = r[0];  // R(j, c) for c > j
+            Rs[j][c] = (mine && j <= c) ? r[0] : 0.0;
+        }
+        const bool def = s_def;
+        __syncthreads();
+        if (!def) {
+            const double rj = s_row[c];
+            if (rot) {
+#pragma unroll
+                for (int i = 1; i < kRegH; ++i) r[i] = fma(-s_row[j + i], rj, r[i]);
+            } else if (h > hj) {
+#pragma unroll
+                for (int i = 0; i < kRegH; ++i) r[i] = fma(-s_row[rbase + i], rj, r[i]);
+            }
+        }
+        if (rot) {
+#pragma unroll
+            for (int i = 0; i + 1 < kRegH; ++i) r[i] = r[i + 1];
+            r[kRegH - 1] = 0.0;
+        }
+    }
+    if (h == 0)
+        for (int j = p; j < kRegP; ++j) Rs[j][c] = 0.0;
+    __syncthreads();
+    // inversion: column c of T, R x = e_c from the bottom. Half h keeps
+    // y[m] = x[top_h - m], top_h = min(i, 32h + 31) (rotating while i is in it)
+    double y[kRegH];
+    const int top0 = min(p - 1, rbase + kRegH - 1);
+#pragma unroll
+    for (int m = 0; m < kRegH; ++m) y[m] = (top0 - m == c && top0 - m >= rbase) ? 1.0 : 0.0;
+    const bool zc = mine && s_msk[c] != 0;
+#pragma unroll 1
+    for (int i = p - 1; i >= 0; --i) {
+        const int hi = i >> 5;
+        if (h == hi) {
+            const double xi = y[0] * s_rinv[i];
+            s_x[c] = xi;
+            if (mine) T[(int64_t)i * ldt + c] = (i > c || zc || s_msk[i]) ? 0.0 : xi;
+        }
+        __syncthreads();
+        const double xi = s_x[c];
+        if (h == hi) {
+#pragma unroll
+            for (int m = 1; m < kRegH; ++m)
+                if (i - m >= rbase) y[m] = fma(-Rs[i - m][i], xi, y[m]);
+#pragma unroll
+            for (int m = 0; m + 1 < kRegH; ++m) y[m] = y[m + 1];
+            y[kRegH - 1] = 0.0;
+        } else if (h < hi) {
+#pragma unroll
+            for (int m = 0; m < kRegH; ++m) y[m] = fma(-Rs[rbase + kRegH - 1 - m][i], xi, y[m]);
+        }
+        __syncthreads();  // s_x is rewritten next row
+    }
+    if (h == 0 && mine) mask[c] = s_msk[c] == 1 ? 1 : 0;
+    if (threadIdx.x == 0) {
+        const int32_t base = running ? running[0] : 0;
+        ndef[0] = s_count;
+        ndef[1] = base;
+        if (running) running[0] = base + s_count;
+    }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -772,6 +894,9 @@ int chol_deflate(int64_t p, const double* G, int64_t ldg, const double* ref2, do
     if (p <= kRegP && !force_sweep) {
         if (getenv("RSVD_CHOL_REG_UNROLLED") != nullptr)  // A/B: the fully unrolled kernel
             k_chol_reg64<<<1, kRegP, 0, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active, pred);
+        else if (getenv("RSVD_CHOL_REG_ONE") == nullptr)  // default: two threads per column
+            k_chol_reg64h<<<1, 2 * kRegP, 0, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active,
+                                                   pred);
         else
             k_chol_reg64c<<<1, kRegP, 0, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active,
                                                pred);

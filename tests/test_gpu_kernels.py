@@ -109,9 +109,10 @@ def test_chol_deflate_full_rank_and_deficient(ops):
 
 @pytest.mark.parametrize("p", [1, 7, 33, 50, 64])
 def test_chol_reg64_compact_matches_unrolled(ops, monkeypatch, p):
-    """p <= 64: the compact rotating-register kernel (default) against the
-    fully unrolled one -- same operations in the same order, bitwise equal
-    T, mask and counts (deficient and inactive columns included)."""
+    """p <= 64: the two-threads-per-column kernel (default), the compact
+    rotating-register kernel and the fully unrolled one -- same operations in
+    the same order, bitwise equal T, mask and counts (deficient and inactive
+    columns included)."""
     v = _rand((4 * p + 8, p), 60 + p)
     if p >= 7:
         v[:, 5] = v[:, 1] - 2.0 * v[:, 3]
@@ -120,7 +121,9 @@ def test_chol_reg64_compact_matches_unrolled(ops, monkeypatch, p):
     if p >= 33:
         active[p - 3] = 0
     outs = []
-    for mode in ("compact", "unrolled"):
+    for mode in ("halves", "compact", "unrolled"):
+        if mode == "compact":
+            monkeypatch.setenv("RSVD_CHOL_REG_ONE", "1")
         if mode == "unrolled":
             monkeypatch.setenv("RSVD_CHOL_REG_UNROLLED", "1")
         T = torch.empty((p, p), dtype=torch.float64, device="cuda")
@@ -129,8 +132,9 @@ def test_chol_reg64_compact_matches_unrolled(ops, monkeypatch, p):
         running = torch.tensor([2], dtype=torch.int32, device="cuda")
         ops.chol_deflate(G, None, 1e-14, T, mask, ndef, running, active)
         outs.append((T.clone(), mask.clone(), ndef.clone(), running.clone()))
-    for a, b in zip(*outs):
-        assert torch.equal(a, b)
+    for other in outs[1:]:
+        for a, b in zip(outs[0], other):
+            assert torch.equal(a, b)
     if p >= 7:
         assert int(outs[0][1][5]) == 1
 
