@@ -802,6 +802,36 @@ __global__ void k_tc_reduce(int64_t M, int64_t N, int64_t ldw, int64_t splits, c
     C[r * ldc + c] = (TO)v;
 }
 
+// Same sum for outputs with few CTAs' worth of threads (projection-sized M):
+// block = 32 outputs x 8 split groups, group g sums splits g, g + 8, ... and
+// the group sums are added in group order (deterministic), so each thread
+// issues splits / 8 loads instead of all of them back to back.
+template <typename TO>
+__global__ void __launch_bounds__(256)
+k_tc_reduce_g(int64_t M, int64_t N, int64_t ldw, int64_t splits, const float* __restrict__ ws, double alpha,
+              double beta, TO* __restrict__ C, int64_t ldc, const double* __restrict__ mu,
+              const double* __restrict__ cs, const int32_t* __restrict__ pred) {
+    if (pred_off(pred)) return;
+    __shared__ double part[8][33];
+    const int o = threadIdx.x % 32, g = threadIdx.x / 32;
+    const int64_t e = (int64_t)blockIdx.x * 32 + o;
+    const bool ok = e < M * N;
+    const int64_t r = ok ? e / N : 0, c = ok ? e % N : 0;
+    double v = 0.0;
+    if (ok)
+        for (int64_t s = g; s < splits; s += 8) v += (double)ws[(s * M + r) * ldw + c];
+    part[g][o] = v;
+    __syncthreads();
+    if (g != 0 || !ok) return;
+    double t = part[0][o];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) t += part[i][o];
+    if (mu) t -= mu[r] * cs[c];
+    t *= alpha;
+    if (beta != 0.0) t += beta * (double)C[r * ldc + c];
+    C[r * ldc + c] = (TO)t;
+}
+
 // ------------------------------------------------------------------ host
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1037,7 +1067,16 @@ int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, con
     rc = dispatch_bn<true>(bn, tA, tB, p, grid, st);
     if (rc) return rc;
     int64_t tot = Mop * Nop;
-    if (out_dtype == RSVD_F64)
+    // few outputs, many splits (projection coefficients): split-grouped reduce
+    const bool grouped = S >= 16 && tot * 8 <= (int64_t)sm_count() * 2048;
+    if (grouped) {
+        if (out_dtype == RSVD_F64)
+            k_tc_reduce_g<double><<<(unsigned)cdiv(tot, 32), 256, 0, st>>>(Mop, Nop, p.ldw, S, (const float*)ws, alpha,
+                                                                            beta, (double*)C, ldc, mu, cs, pred);
+        else
+            k_tc_reduce_g<float><<<(unsigned)cdiv(tot, 32), 256, 0, st>>>(Mop, Nop, p.ldw, S, (const float*)ws, alpha,
+                                                                           beta, (float*)C, ldc, mu, cs, pred);
+    } else if (out_dtype == RSVD_F64)
         k_tc_reduce<double><<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(Mop, Nop, p.ldw, S, (const float*)ws, alpha, beta,
                                                                        (double*)C, ldc, mu, cs, pred);
     else
