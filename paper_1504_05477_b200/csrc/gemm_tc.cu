@@ -188,6 +188,7 @@ struct TcParams {
     float* ws;
     int64_t ldw;            // row pitch of the partials (multiple of 4 floats)
     int plain_vec;          // direct, alpha = 1, beta = 0, no row_sub, C rows 16-byte aligned
+    int c_vec;              // direct and C rows 16-byte aligned (float4 epilogue with alpha/beta/row_sub)
     const int32_t* pred;
     int n_tiles;            // N tiles per M tile (blockIdx.x = m_tile * n_tiles + n_tile)
 };
@@ -269,16 +270,38 @@ __device__ __forceinline__ void drain_epilogue(const TcParams& p, uint32_t tmem_
             }
         }
     } else if (row < p.M) {
+        // general direct epilogue; 16-byte loads/stores of 4 columns where the
+        // layout allows (one lane per row: scalar accesses touched a separate
+        // sector per element -- X -= Q C at n = 5e4: 47 us for a 40 MB product)
+        const int ncols = (int)min((int64_t)BN, p.N - n0);
 #pragma unroll
-        for (int i = 0; i < BN; ++i) {
-            const int64_t col = n0 + i;
-            if (col < p.N) {
-                if (p.direct) {
-                    double r = (double)sum[i];
-                    if (p.row_sub) r -= p.row_sub[col];
+        for (int i = 0; i < BN; i += 4) {
+            float* crow = p.C + row * p.ldc + n0 + i;
+            if (p.direct && p.c_vec && i + 4 <= ncols) {
+                float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (p.beta != 0.0) cv = *reinterpret_cast<const float4*>(crow);
+                const float cin[4] = {cv.x, cv.y, cv.z, cv.w};
+                float res[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    double r = (double)sum[i + t];
+                    if (p.row_sub) r -= p.row_sub[n0 + i + t];
                     r *= p.alpha;
-                    if (p.beta != 0.0) r += p.beta * (double)p.C[row * p.ldc + col];
-                    p.C[row * p.ldc + col] = (float)r;
+                    if (p.beta != 0.0) r += p.beta * (double)cin[t];
+                    res[t] = (float)r;
+                }
+                *reinterpret_cast<float4*>(crow) = make_float4(res[0], res[1], res[2], res[3]);
+            } else if (p.direct) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int64_t col = n0 + i + t;
+                    if (i + t < ncols) {
+                        double r = (double)sum[i + t];
+                        if (p.row_sub) r -= p.row_sub[col];
+                        r *= p.alpha;
+                        if (p.beta != 0.0) r += p.beta * (double)p.C[row * p.ldc + col];
+                        p.C[row * p.ldc + col] = (float)r;
+                    }
                 }
             }
         }
@@ -1016,6 +1039,7 @@ int gemm_nn_tc(int64_t m, int64_t n, int64_t k, double alpha, const float* A, in
     p.M = m; p.N = n; p.K = k; p.k_per_split = Kp; p.Kp = Kp; p.Np = Np;
     p.direct = 1; p.C = C; p.ldc = ldc; p.alpha = alpha; p.beta = beta; p.row_sub = row_sub; p.ws = nullptr;
     p.plain_vec = alpha == 1.0 && beta == 0.0 && row_sub == nullptr && ldc % 4 == 0 && aligned16(C);
+    p.c_vec = ldc % 4 == 0 && aligned16(C);
     p.pred = pred;
     p.n_tiles = (int)cdiv(n, bn);
     // (a split-K variant for wave balance -- C2: 391 tiles = 2.64 waves -- was
