@@ -299,9 +299,44 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self._stop = threading.Event()
+        self._ready = threading.Event()
         self._t = None
+        self.source = None
+
+    def _nvml_handle(self):
+        """NVML handle of this process's CUDA device, matched by PCI bus id
+        (a CUDA ordinal is not an NVML index under CUDA_VISIBLE_DEVICES)."""
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = "%08X:%02X:%02X.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _run_nvml(self):
+        nv, h = self._nvml_handle()
+        bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while True:
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.rows.append([str(sm), str(mx), "", hex(rs)] + ["Active" if rs & b else "Not Active" for b in bits])
+            self._ready.set()
+            if self._stop.wait(0.002):  # ~2 ms: dozens of samples inside a 100 ms timed region
+                return
 
     def _run(self):
+        try:
+            self._run_nvml()
+            self.source = "nvml"
+            return
+        except Exception:
+            pass
+        self.source = "nvidia-smi"
         while not self._stop.is_set():
             try:
                 out = subprocess.run(
@@ -311,11 +346,13 @@ class ClockSampler:
                     self.rows.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
+            self._ready.set()
             self._stop.wait(0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        self._ready.wait(10)  # the sampler is live before the timed region starts
         return self
 
     def __exit__(self, *a):
@@ -334,7 +371,7 @@ class ClockSampler:
                 if v.strip().lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+                "reasons": sorted(reasons), "samples": len(self.rows), "source": self.source}
 
 
 def _peaks():
