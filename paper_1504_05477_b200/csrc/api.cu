@@ -101,6 +101,33 @@ int rsvd_gemm_nn(int dtype, int64_t m, int64_t n, int64_t k, double alpha, const
     return gemm_nn_simt(dtype, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, row_sub, pred, st);
 }
 
+int64_t rsvd_oz_planes_ld(int64_t d) { return d < 0 ? 0 : oz_planes_ld(d); }
+
+int rsvd_oz_num_planes(void) { return oz_num_planes(); }
+
+int rsvd_oz_prepare(int64_t n, int64_t d, const float* A, int64_t lda, int8_t* planes, int64_t ldq,
+                    int32_t* row_exp, void* stream) {
+    RSVD_REQUIRE(n >= 0 && d >= 0, "oz_prepare: negative dimension");
+    RSVD_REQUIRE(lda >= d && ldq >= oz_planes_ld(d), "oz_prepare: pitch too small");
+    RSVD_REQUIRE(n == 0 || (A && planes && row_exp), "oz_prepare: null pointer");
+    return oz_prepare(n, d, A, lda, planes, ldq, row_exp, as_stream(stream));
+}
+
+int64_t rsvd_oz_gemm_ws_bytes(int trans, int64_t n, int64_t d, int64_t p) {
+    if (n < 0 || d < 0 || p < 0) return 0;
+    return oz_gemm_ws_bytes(trans, n, d, p);
+}
+
+int rsvd_oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t* planes, int64_t ldq,
+                 const int32_t* row_exp, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                 void* ws, int64_t ws_bytes, const int32_t* pred, void* stream) {
+    RSVD_REQUIRE(trans == 0 || trans == 1, "oz_gemm: trans must be 0 or 1");
+    RSVD_REQUIRE(n >= 0 && d >= 0 && p >= 0, "oz_gemm: negative dimension");
+    RSVD_REQUIRE(ldq >= oz_planes_ld(d) && ldb >= p && ldc >= p, "oz_gemm: leading dimension too small");
+    return oz_gemm(trans, n, d, p, alpha, planes, ldq, row_exp, B, ldb, beta, C, ldc, ws, ws_bytes, pred,
+                   as_stream(stream));
+}
+
 int64_t rsvd_gemm_tn_ws_bytes(int dtype, int64_t m, int64_t n, int64_t k, int algo) {
     int64_t a = gemm_tn_simt_ws_bytes(m, n, k);
     if (dtype == RSVD_F64 && algo != RSVD_GEMM_SIMT) {

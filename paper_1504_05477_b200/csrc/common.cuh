@@ -33,6 +33,19 @@ void set_error(const char* fmt, ...);
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int sm_count();
+int current_device();  // cudaGetDevice, clamped to [0, kMaxDevices)
+
+// Process state keyed by the calling thread's current CUDA device: the
+// once-per-device cudaFuncSetAttribute flags and the grow-only scratch
+// buffers. A process that drives several GPUs gets a separate slot per
+// device (kernel attributes are per device; a scratch pointer of one device
+// must never reach another device's kernels).
+constexpr int kMaxDevices = 64;
+template <typename T>
+struct PerDevice {
+    T slot[kMaxDevices]{};
+    T& get() { return slot[current_device()]; }
+};
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

@@ -267,7 +267,8 @@ int launch_one(dim3 grid, cudaStream_t st, int64_t mout, int64_t n, int64_t kred
                int64_t ldc, const double* row_sub, double* ws, const int32_t* pred) {
     constexpr int smem = dmma_smem<TRANS, BM, BN, BK>();
     auto kern = k_dmma<TRANS, VEC, BM, BN, BK, WGM>;
-    static bool attr = false;  // per instantiation; idempotent
+    static PerDevice<bool> attr_dev;  // per instantiation and device; idempotent
+    bool& attr = attr_dev.get();
     if (!attr) {
         RSVD_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;

@@ -1,0 +1,599 @@
+// FP64-accurate products of an FP32 A on the int8 tensor cores (sm_100a,
+// tcgen05 kind::i8): the Ozaki splitting scheme with exact int32 accumulation.
+//
+// Why: the reference builds its block-Krylov basis from normalized power
+// blocks whose newest directions sit ~1e-11 below the block norm
+// (rsvd.py:244-260, factor.py:79-118). Reproducing its sigma to 1e-4 needs
+// products accurate to ~1e-15 relative (measured on the C2 matrix: product
+// noise 1e-15 -> sigma 1.7e-6 off, 1e-13 -> 1.4e-4 and different deflation
+// decisions). 3xTF32 gives ~1e-7; FP64 DMMA gives 1e-16 at ~37 TFLOP/s.
+//
+// Scheme (per product D = A X, A FP32 n x d held in HBM as slices):
+//   * every row r of A is scaled by 2^-E_r (2^E_r > max_c |A[r,c]|) and cut
+//     into SA = 6 signed 7-bit digits: A[r,c] = 2^E_r sum_i a_i[r,c] 2^-7(i+1),
+//     a_i in [-127, 127] (truncation; exact for every entry >= 2^-18 of the row
+//     maximum since FP32 carries 24 bits, 2^-42 absolute below);
+//   * every column c of the FP64 operand X likewise into SB = 7 digits with
+//     its own exponent F_c (2^-49 relative to the column maximum);
+//   * D = 2^(E_r + F_c - 14) sum_{i+j <= 6} 2^-7(i+j) (a_i x_j): 27 int8 GEMMs
+//     whose int32 sums are EXACT (|digit products| <= 127^2, at most 7 pairs
+//     per level, K <= 16384 per CTA keeps every level below 2^31); the levels
+//     are combined in FP64 in the epilogue. Neglected terms are ~2^-56 of
+//     |A||X| per entry: FP64-class accuracy (tests: ~1e-16 vs cuBLAS DGEMM).
+//   * A^T Y uses the same row-scaled slices: A^T Y = sum_r (2^-E_r A[r,:])^T
+//     (2^E_r Y[r,:]); the row scale is folded into Y before it is sliced, so
+//     the A operand is read in place as an MN-major int8 tile.
+// Per K = 32 step one A digit plane i multiplies the stacked digit planes
+// [x_0 | x_1 | ... | x_(6-i)] (N = (7-i) BN, split into <= 256-column MMAs)
+// into TMEM columns [i BN, 7 BN): level L = i + j accumulates at column L BN
+// without any per-pair bookkeeping. TMEM holds all 7 levels (448 columns at
+// BN = 64) for the whole K range of the CTA; the epilogue reads them once.
+#include <cuda.h>
+
+#include <cmath>
+
+#include "gemm.cuh"
+#include "umma.cuh"
+
+namespace rsvd {
+
+namespace {
+
+constexpr int OZ_BM = 128;
+constexpr int OZ_KS = 32;        // int8 K per MMA = bytes per smem tile row
+constexpr int OZ_SA = 6;         // A digit planes
+constexpr int OZ_SB = 7;         // B digit planes
+constexpr int OZ_L = 6;          // kept levels i + j <= OZ_L
+constexpr int OZ_LEVELS = OZ_L + 1;
+constexpr int OZ_STAGES = 5;
+constexpr int64_t OZ_MAX_K = 16384;  // int32 exactness bound per CTA
+constexpr int OZ_THREADS = 6 * 32;   // 0 TMA, 1 MMA, 2..5 epilogue
+constexpr uint32_t kLayoutSW32 = 6;
+
+template <int BN>
+struct OzCfg {
+    static constexpr int A_TILE = OZ_BM * OZ_KS;            // 4 KB per digit plane
+    static constexpr int B_TILE = BN * OZ_KS;               // per digit plane
+    static constexpr int STAGE = OZ_SA * A_TILE + OZ_SB * B_TILE;
+    static constexpr int SMEM = OZ_STAGES * STAGE + 1024 + 256;
+    static constexpr int ACC_COLS = OZ_LEVELS * BN;
+    static_assert(ACC_COLS <= 512, "levels do not fit TMEM");
+    static_assert(STAGE % 1024 == 0, "stage must keep 1024-byte swizzle alignment");
+};
+
+struct OzParams {
+    int64_t M, N, K;         // D[M x N] = Aop[M x K] Bop[K x N]
+    int64_t k_per_split;     // multiple of OZ_KS
+    const int32_t* ea;       // per-M exponent (NN: A row exponents), nullptr for TN
+    const int32_t* fb;       // per-N exponent of B's columns
+    int direct;              // 1: C = alpha D + beta C (FP64); 0: FP64 partial to ws[z]
+    double* C;
+    int64_t ldc;
+    double alpha, beta;
+    double* ws;
+    int64_t ldw;
+    const int32_t* pred;
+    int n_tiles;
+};
+
+// kind::i8 instruction descriptor: S32 accumulate, signed int8 A / B.
+__host__ __device__ constexpr uint32_t oz_idesc(int M, int N, int a_mn_major) {
+    return (2u << 4)                        // c_format S32
+           | (1u << 7)                      // a_format signed 8 bit
+           | (1u << 10)                     // b_format signed 8 bit
+           | ((uint32_t)a_mn_major << 15)   // a major
+           | ((uint32_t)(N >> 3) << 17)     // N
+           | ((uint32_t)(M >> 4) << 24);    // M
+}
+
+__device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_ld16_s32(uint32_t taddr, int32_t* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = (int32_t)r[i];
+}
+
+template <int BN, bool A_MN>
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, OzParams p) {
+    if (pred_off(p.pred)) return;
+    using Cfg = OzCfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OZ_STAGES * Cfg::STAGE);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + OZ_STAGES;
+    uint64_t* acc_full = bars + 2 * OZ_STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t m0 = (int64_t)(blockIdx.x / p.n_tiles) * OZ_BM;
+    const int64_t n0 = (int64_t)(blockIdx.x % p.n_tiles) * BN;
+    const int64_t kbeg = (int64_t)blockIdx.z * p.k_per_split;
+    const int64_t kend = min(p.K, kbeg + p.k_per_split);
+    const int nks = kend > kbeg ? (int)((kend - kbeg + OZ_KS - 1) / OZ_KS) : 0;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < OZ_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(acc_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer: SA A planes + SB B planes per K step
+            int s = 0;
+            uint32_t ph = 0;
+            for (int kb = 0; kb < nks; ++kb) {
+                mbar_wait(&empty[s], ph ^ 1);
+                const int kk = (int)(kbeg + (int64_t)kb * OZ_KS);
+                uint8_t* st = smem + s * Cfg::STAGE;
+                mbar_expect_tx(&full[s], Cfg::STAGE);
+#pragma unroll
+                for (int i = 0; i < OZ_SA; ++i) {
+                    if (!A_MN)
+                        tma_load_3d(&tmA, &full[s], st + i * Cfg::A_TILE, kk, (int)m0, i);
+                    else
+                        tma_load_3d(&tmA, &full[s], st + i * Cfg::A_TILE, (int)m0, kk, i);
+                }
+#pragma unroll
+                for (int j = 0; j < OZ_SB; ++j)
+                    tma_load_3d(&tmB, &full[s], st + OZ_SA * Cfg::A_TILE + j * Cfg::B_TILE, kk, (int)n0, j);
+                if (++s == OZ_STAGES) { s = 0; ph ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer
+            int s = 0;
+            uint32_t ph = 0;
+            for (int kb = 0; kb < nks; ++kb) {
+                mbar_wait(&full[s], ph);
+                tc_fence_after();
+                const uint32_t st = smem_u32(smem + s * Cfg::STAGE);
+                const uint32_t bst = st + OZ_SA * Cfg::A_TILE;
+#pragma unroll
+                for (int i = 0; i < OZ_SA; ++i) {
+                    // K-major A: 128 rows x 32 B, SWIZZLE_32B (8-row groups, SBO 256 B);
+                    // MN-major A: 32 K rows x 128 B, SWIZZLE_128B (8-row groups, SBO 1024 B)
+                    const uint64_t da = A_MN ? make_desc(st + i * Cfg::A_TILE, 4096, 1024, kLayoutSW128)
+                                             : make_desc(st + i * Cfg::A_TILE, 16, 256, kLayoutSW32);
+                    constexpr int kMaxJ = OZ_SB;
+                    const int nj = (OZ_L - i + 1) < kMaxJ ? (OZ_L - i + 1) : kMaxJ;
+                    const int rows = nj * BN;
+#pragma unroll
+                    for (int r0 = 0; r0 < OZ_SB * BN; r0 += 256) {
+                        if (r0 >= rows) break;
+                        const int nn = (rows - r0) < 256 ? (rows - r0) : 256;
+                        const uint64_t db = make_desc(bst + r0 * OZ_KS, 16, 256, kLayoutSW32);
+                        const uint32_t acc = (kb == 0 && i == 0) ? 0u : 1u;
+                        tc_mma_i8(tmem_base + (uint32_t)(i * BN + r0), da, db, oz_idesc(OZ_BM, nn, A_MN ? 1 : 0), acc);
+                    }
+                }
+                tc_commit(&empty[s]);
+                if (++s == OZ_STAGES) { s = 0; ph ^= 1; }
+            }
+            tc_commit(acc_full);
+        }
+    } else {
+        // ---------------- epilogue: thread = one output row (its TMEM lane)
+        const int quarter = warp % 4;
+        const int64_t row = m0 + quarter * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+        if (nks > 0) {
+            mbar_wait(acc_full, 0);
+            tc_fence_after();
+        }
+        int ea = 0;
+        if (p.ea && row < p.M) ea = p.ea[row];
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+            double v[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) v[t] = 0.0;
+            if (nks > 0) {
+                // Horner from the smallest level: v = sum_L acc_L 2^-7L
+#pragma unroll
+                for (int L = OZ_L; L >= 0; --L) {
+                    int32_t a[16];
+                    tmem_ld16_s32(tmem_base + lane_off + (uint32_t)(L * BN + c0), a);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int t = 0; t < 16; ++t) v[t] = fma(v[t], 0.0078125, (double)a[t]);
+                }
+            }
+            if (row < p.M) {
+#pragma unroll
+                for (int t = 0; t < 16; ++t) {
+                    const int64_t col = n0 + c0 + t;
+                    if (col < p.N) {
+                        const double val = ldexp(v[t], ea + p.fb[col] - 14);
+                        if (p.direct) {
+                            double* c = p.C + row * p.ldc + col;
+                            *c = p.beta != 0.0 ? p.alpha * val + p.beta * *c : p.alpha * val;
+                        } else {
+                            p.ws[((int64_t)blockIdx.z * p.M + row) * p.ldw + col] = val;
+                        }
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+    }
+}
+
+// ---------------------------------------------------------------- slicing
+__device__ __forceinline__ int exp_above(double m) {
+    // smallest E with 2^E > m (m > 0): frexp gives m = f 2^e, f in [0.5, 1)
+    int e;
+    frexp(m, &e);
+    return e;
+}
+
+__device__ __forceinline__ float block_max(float v) {
+    __shared__ float red[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = l < (int)(blockDim.x / 32) ? red[l] : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (l == 0) red[0] = v;
+    }
+    __syncthreads();
+    v = red[0];
+    __syncthreads();
+    return v;
+}
+
+// digit i of u in (-1, 1): t = 128 u; a_i = trunc(t); t = 128 (t - a_i). Exact in FP32 for FP32 input
+// (t keeps <= 24 significant bits; removing the integer part and scaling by 2^7 are exact).
+__device__ __forceinline__ uint32_t pack4(const int (&q)[4]) {
+    return (uint32_t)(q[0] & 0xFF) | ((uint32_t)(q[1] & 0xFF) << 8) | ((uint32_t)(q[2] & 0xFF) << 16) |
+           ((uint32_t)(q[3] & 0xFF) << 24);
+}
+
+// One CTA per row of A: row maximum, exponent, then the SA digit planes.
+// planes[i][r][c], row pitch ldq bytes (multiple of 16), plane pitch n ldq.
+__global__ void __launch_bounds__(256) k_oz_slice_a(int64_t n, int64_t d, const float* __restrict__ A, int64_t lda,
+                                                    int8_t* __restrict__ planes, int64_t ldq,
+                                                    int32_t* __restrict__ row_exp) {
+    const int64_t r = blockIdx.x;
+    if (r >= n) return;
+    const float* a = A + r * lda;
+    const bool vec = (lda % 4 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+    float m = 0.f;
+    const int64_t d4 = vec ? d / 4 : 0;
+    for (int64_t c = threadIdx.x; c < d4; c += blockDim.x) {
+        const float4 v = reinterpret_cast<const float4*>(a)[c];
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+    for (int64_t c = d4 * 4 + threadIdx.x; c < d; c += blockDim.x) m = fmaxf(m, fabsf(a[c]));
+    m = block_max(m);
+    const int E = m > 0.f ? exp_above((double)m) : 0;
+    if (threadIdx.x == 0) row_exp[r] = E;
+    const float sc = ldexpf(1.0f, -E);
+    const int64_t pp = n * ldq;
+    int8_t* out = planes + r * ldq;
+    const int64_t dq = (d + 3) / 4;  // groups of 4 columns (the last one zero padded up to ldq)
+    for (int64_t g = threadIdx.x; g < dq; g += blockDim.x) {
+        float x[4];
+        if (vec && g < d4) {
+            const float4 v = reinterpret_cast<const float4*>(a)[g];
+            x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+        } else {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) x[t] = (g * 4 + t < d) ? a[g * 4 + t] : 0.f;
+        }
+        float t4[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) t4[t] = x[t] * sc * 128.0f;
+#pragma unroll
+        for (int i = 0; i < OZ_SA; ++i) {
+            int q[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const float tr = truncf(t4[t]);
+                q[t] = (int)tr;
+                t4[t] = (t4[t] - tr) * 128.0f;
+            }
+            *reinterpret_cast<uint32_t*>(out + i * pp + g * 4) = pack4(q);
+        }
+    }
+}
+
+// B operand (K x N FP64, row pitch ldb), optional per-row exponent e_k folded
+// in (A^T Y: Y[k, :] 2^E_k). Pass 1: per-column max of |2^e_k B[k, c]| as
+// ordered bit patterns (atomicMax on the FP64 bits of a non-negative value).
+__global__ void __launch_bounds__(256) k_oz_colmax_b(int64_t K, int64_t N, const double* __restrict__ B, int64_t ldb,
+                                                     const int32_t* __restrict__ ek,
+                                                     unsigned long long* __restrict__ colmax) {
+    const int c = threadIdx.x % 32;  // 32 columns x 8 row groups per CTA
+    const int g = threadIdx.x / 32;
+    const int64_t col = (int64_t)blockIdx.y * 32 + c;
+    double m = 0.0;
+    if (col < N)
+        for (int64_t k = (int64_t)blockIdx.x * 8 + g; k < K; k += (int64_t)gridDim.x * 8) {
+            double v = fabs(B[k * ldb + col]);
+            if (ek) v = ldexp(v, ek[k]);
+            m = fmax(m, v);
+        }
+    __shared__ double red[8][32];
+    red[g][c] = m;
+    __syncthreads();
+    if (g == 0 && col < N) {
+#pragma unroll
+        for (int i = 1; i < 8; ++i) m = fmax(m, red[i][c]);
+        atomicMax(colmax + col, (unsigned long long)__double_as_longlong(m));
+    }
+}
+
+__global__ void k_oz_col_exp(int64_t N, const unsigned long long* __restrict__ colmax, int32_t* __restrict__ fb) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= N) return;
+    const double m = __longlong_as_double((long long)colmax[c]);
+    fb[c] = m > 0.0 ? exp_above(m) : 0;
+}
+
+// Pass 2: transposed digit planes planes[j][c][k] (K-major rows of Kp bytes,
+// rows c in [N, Np) written as zeros), through a 32 (k) x 32 (c) smem tile.
+__global__ void __launch_bounds__(256) k_oz_slice_b(int64_t K, int64_t N, const double* __restrict__ B, int64_t ldb,
+                                                    const int32_t* __restrict__ ek, const int32_t* __restrict__ fb,
+                                                    int64_t Np, int64_t Kp, int8_t* __restrict__ planes) {
+    __shared__ uint32_t tile[OZ_SB][32][9];  // [plane][c][k / 4] packed digits
+    const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8
+    const int64_t k0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+    // load: thread (tx = c, ty) handles rows k0 + 4 ty .. 4 ty + 3 of column c0 + tx
+    const int64_t col = c0 + tx;
+    const double sc = col < N ? ldexp(1.0, -fb[col]) : 0.0;
+    int q[OZ_SB][4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const int64_t k = k0 + 4 * ty + t;
+        double u = 0.0;
+        if (k < K && col < N) {
+            u = B[k * ldb + col];
+            if (ek) u = ldexp(u, ek[k]);
+            u *= sc;
+        }
+        double x = u * 128.0;
+#pragma unroll
+        for (int j = 0; j < OZ_SB; ++j) {
+            const double tr = trunc(x);
+            q[j][t] = (int)tr;
+            x = (x - tr) * 128.0;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < OZ_SB; ++j) tile[j][tx][ty] = pack4(q[j]);
+    __syncthreads();
+    // store: rows c = c0 + (warp), 8 words of 4 k each per (plane, row)
+    for (int e = threadIdx.x; e < OZ_SB * 32 * 8; e += blockDim.x) {
+        const int w = e % 8, cc = (e / 8) % 32, j = e / 256;
+        const int64_t c = c0 + cc;
+        const int64_t k = k0 + 4 * w;
+        if (c < Np && k < Kp)
+            *reinterpret_cast<uint32_t*>(planes + ((int64_t)j * Np + c) * Kp + k) = tile[j][cc][w];
+    }
+}
+
+__global__ void k_oz_reduce(int64_t M, int64_t N, int64_t ldw, int64_t splits, const double* __restrict__ ws,
+                            double alpha, double beta, double* __restrict__ C, int64_t ldc,
+                            const int32_t* __restrict__ pred) {
+    if (pred_off(pred)) return;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= M * N) return;
+    const int64_t r = e / N, c = e % N;
+    double v = 0.0;
+    for (int64_t s = 0; s < splits; ++s) v += ws[(s * M + r) * ldw + c];
+    v *= alpha;
+    if (beta != 0.0) v += beta * C[r * ldc + c];
+    C[r * ldc + c] = v;
+}
+
+// ---------------------------------------------------------------- host
+int oz_map_a(CUtensorMap* map, const int8_t* planes, int64_t n, int64_t d, int64_t ldq, bool mn_major) {
+    EncodeTiledFn fn = encode_fn();
+    RSVD_REQUIRE(fn != nullptr, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)n, (cuuint64_t)OZ_SA};
+    cuuint64_t strides[2] = {(cuuint64_t)ldq, (cuuint64_t)(n * ldq)};
+    cuuint32_t box[3] = {mn_major ? 128u : (cuuint32_t)OZ_KS, mn_major ? (cuuint32_t)OZ_KS : 128u, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(planes), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, mn_major ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    RSVD_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (Ozaki A planes) failed (%d)", (int)r);
+    return RSVD_OK;
+}
+
+int oz_map_b(CUtensorMap* map, const int8_t* planes, int64_t K, int64_t Np, int64_t Kp, int bn) {
+    EncodeTiledFn fn = encode_fn();
+    RSVD_REQUIRE(fn != nullptr, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)Np, (cuuint64_t)OZ_SB};
+    cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)(Np * Kp)};
+    cuuint32_t box[3] = {(cuuint32_t)OZ_KS, (cuuint32_t)bn, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(planes), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    RSVD_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (Ozaki B planes) failed (%d)", (int)r);
+    return RSVD_OK;
+}
+
+int oz_bn(int64_t n) { return n <= 32 ? 32 : 64; }
+
+// split count: K per CTA <= OZ_MAX_K (exactness), then the smallest count
+// whose CTAs fill the SMs in waves >= 90% full (at most 64, >= 4 K steps each)
+int64_t oz_splits(int64_t tiles, int64_t K) {
+    const int64_t min_s = cdiv(K, OZ_MAX_K);
+    const int64_t G = sm_count();
+    int64_t max_s = cdiv(K, 4 * OZ_KS);
+    if (max_s > 64) max_s = 64;
+    if (max_s < min_s) max_s = min_s;
+    int64_t best = min_s;
+    double best_e = 0.0;
+    for (int64_t S = min_s; S <= max_s; ++S) {
+        const double u = (double)(tiles * S) / (double)G;
+        const double e = u / std::ceil(u);
+        if (e > best_e + 1e-9) {
+            best_e = e;
+            best = S;
+        }
+        if (e >= 0.90) return S;
+    }
+    return best;
+}
+
+struct OzLayout {
+    int bn;
+    int64_t Np, Kp, splits, n_tiles, m_tiles;
+    int64_t planes_off, colmax_off, fb_off, part_off, total;
+};
+
+OzLayout oz_layout(bool trans, int64_t n, int64_t d, int64_t p) {
+    OzLayout L{};
+    L.bn = oz_bn(p);
+    const int64_t Mop = trans ? d : n, Kop = trans ? n : d;
+    L.Np = cdiv(p, L.bn) * L.bn;
+    L.Kp = cdiv(Kop, 16) * 16;
+    L.n_tiles = cdiv(p, L.bn);
+    L.m_tiles = cdiv(Mop, OZ_BM);
+    L.splits = oz_splits(L.m_tiles * L.n_tiles, Kop);
+    int64_t off = 0;
+    auto take = [&](int64_t bytes) {
+        int64_t o = off;
+        off += cdiv(bytes, 256) * 256;
+        return o;
+    };
+    L.planes_off = take((int64_t)OZ_SB * L.Np * L.Kp);
+    L.colmax_off = take(p * 8);
+    L.fb_off = take(p * 4);
+    L.part_off = take(L.splits > 1 ? L.splits * Mop * p * 8 : 0);
+    L.total = off + 256;
+    return L;
+}
+
+template <int BN, bool A_MN>
+int launch_oz(const CUtensorMap& tA, const CUtensorMap& tB, const OzParams& p, dim3 grid, cudaStream_t st) {
+    using Cfg = OzCfg<BN>;
+    static PerDevice<bool> attr_dev;
+    bool& attr = attr_dev.get();
+    if (!attr) {
+        RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_oz_gemm<BN, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Cfg::SMEM));
+        attr = true;
+    }
+    k_oz_gemm<BN, A_MN><<<grid, OZ_THREADS, Cfg::SMEM, st>>>(tA, tB, p);
+    RSVD_CHECK_LAUNCH();
+    return RSVD_OK;
+}
+
+}  // namespace
+
+int64_t oz_planes_ld(int64_t d) { return cdiv(d, 16) * 16; }
+int oz_num_planes() { return OZ_SA; }
+
+int oz_prepare(int64_t n, int64_t d, const float* A, int64_t lda, int8_t* planes, int64_t ldq, int32_t* row_exp,
+               cudaStream_t st) {
+    if (n == 0) return RSVD_OK;
+    k_oz_slice_a<<<(unsigned)n, 256, 0, st>>>(n, d, A, lda, planes, ldq, row_exp);
+    RSVD_CHECK_LAUNCH();
+    return RSVD_OK;
+}
+
+int64_t oz_gemm_ws_bytes(int trans, int64_t n, int64_t d, int64_t p) {
+    return oz_layout(trans != 0, n, d, p).total;
+}
+
+// trans = 0: C (n x p) = alpha A X + beta C, X d x p.
+// trans = 1: C (d x p) = alpha A^T Y + beta C, Y n x p.
+int oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t* planes, int64_t ldq,
+            const int32_t* row_exp, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* ws,
+            int64_t ws_bytes, const int32_t* pred, cudaStream_t st) {
+    const bool tr = trans != 0;
+    const OzLayout L = oz_layout(tr, n, d, p);
+    RSVD_REQUIRE(ws_bytes >= L.total, "oz_gemm: workspace too small (%lld < %lld)", (long long)ws_bytes,
+                 (long long)L.total);
+    RSVD_REQUIRE((reinterpret_cast<uintptr_t>(planes) & 15) == 0 && ldq % 16 == 0,
+                 "oz_gemm: digit planes must be 16-byte aligned with a 16-byte-multiple pitch");
+    const int64_t Mop = tr ? d : n, Kop = tr ? n : d;
+    if (Mop == 0 || p == 0) return RSVD_OK;
+    uint8_t* w = reinterpret_cast<uint8_t*>(ws);
+    int8_t* bpl = reinterpret_cast<int8_t*>(w + L.planes_off);
+    unsigned long long* cmax = reinterpret_cast<unsigned long long*>(w + L.colmax_off);
+    int32_t* fb = reinterpret_cast<int32_t*>(w + L.fb_off);
+    double* part = reinterpret_cast<double*>(w + L.part_off);
+    // B digit planes (row exponents of A folded in for A^T Y)
+    const int32_t* ek = tr ? row_exp : nullptr;
+    RSVD_CHECK_CUDA(cudaMemsetAsync(cmax, 0, p * 8, st));
+    {
+        dim3 g((unsigned)std::min<int64_t>(cdiv(Kop, 8), 2 * sm_count()), (unsigned)cdiv(p, 32));
+        k_oz_colmax_b<<<g, 256, 0, st>>>(Kop, p, B, ldb, ek, cmax);
+        k_oz_col_exp<<<(unsigned)cdiv(p, 128), 128, 0, st>>>(p, cmax, fb);
+        dim3 g2((unsigned)cdiv(L.Kp, 32), (unsigned)cdiv(L.Np, 32));
+        k_oz_slice_b<<<g2, 256, 0, st>>>(Kop, p, B, ldb, ek, fb, L.Np, L.Kp, bpl);
+        RSVD_CHECK_LAUNCH();
+    }
+    CUtensorMap tA, tB;
+    int rc = oz_map_a(&tA, planes, n, d, ldq, tr);
+    if (rc) return rc;
+    rc = oz_map_b(&tB, bpl, Kop, L.Np, L.Kp, L.bn);
+    if (rc) return rc;
+    OzParams prm{};
+    prm.M = Mop; prm.N = p; prm.K = Kop;
+    prm.k_per_split = cdiv(cdiv(Kop, L.splits), OZ_KS) * OZ_KS;
+    prm.ea = tr ? nullptr : row_exp;
+    prm.fb = fb;
+    prm.direct = L.splits == 1;
+    prm.C = C; prm.ldc = ldc; prm.alpha = alpha; prm.beta = beta;
+    prm.ws = part; prm.ldw = p;
+    prm.pred = pred;
+    prm.n_tiles = (int)L.n_tiles;
+    dim3 grid((unsigned)(L.m_tiles * L.n_tiles), 1, (unsigned)L.splits);
+    if (L.bn == 32)
+        rc = tr ? launch_oz<32, true>(tA, tB, prm, grid, st) : launch_oz<32, false>(tA, tB, prm, grid, st);
+    else
+        rc = tr ? launch_oz<64, true>(tA, tB, prm, grid, st) : launch_oz<64, false>(tA, tB, prm, grid, st);
+    if (rc) return rc;
+    if (L.splits > 1) {
+        const int64_t tot = Mop * p;
+        k_oz_reduce<<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(Mop, p, p, L.splits, part, alpha, beta, C, ldc, pred);
+        RSVD_CHECK_LAUNCH();
+    }
+    return RSVD_OK;
+}
+
+}  // namespace rsvd

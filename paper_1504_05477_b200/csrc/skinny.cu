@@ -321,7 +321,8 @@ int gemm_nn_skinny(int64_t m, int64_t n, int64_t k, double alpha, const float* A
     const bool vec = lda % 4 == 0 && ((uintptr_t)A % 16) == 0;
     const unsigned grid = (unsigned)cdiv(m, kNn2Rows);
     if (vec) {
-        static bool attr = false;
+        static PerDevice<bool> attr_dev;
+        bool& attr = attr_dev.get();
         if (!attr) {
             RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_skinny_nn2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)(128 * 64 * 4 + nn2_a_floats(128) * 4)));
@@ -330,7 +331,8 @@ int gemm_nn_skinny(int64_t m, int64_t n, int64_t k, double alpha, const float* A
         k_skinny_nn2<true><<<grid, kNn2Threads, smem, st>>>(m, (int)n, (int)k, alpha, A, lda, B, ldb, beta, C, ldc,
                                                              row_sub, pred);
     } else {
-        static bool attr = false;
+        static PerDevice<bool> attr_dev;
+        bool& attr = attr_dev.get();
         if (!attr) {
             RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_skinny_nn2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)(128 * 64 * 4 + nn2_a_floats(128) * 4)));

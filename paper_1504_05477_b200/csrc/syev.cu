@@ -1422,7 +1422,11 @@ int syev_topk(int64_t w, const double* M, int64_t ldm, int64_t k, double* evals,
         // one cluster barrier per column unless RSVD_TRIDIAG_TWO_BARRIER (A/B)
         const bool one = w >= 4 && getenv("RSVD_TRIDIAG_TWO_BARRIER") == nullptr;
         const size_t csm = ((size_t)nloc * w + 6 * (size_t)w) * sizeof(double);
-        static int cluster_ok = -1;  // cluster launch supported and schedulable (checked once)
+        // cluster launch supported and schedulable (checked once per device;
+        // slot value 0 = unchecked, 1 = no, 2 = yes)
+        static PerDevice<int> cluster_dev;
+        int& cluster_slot = cluster_dev.get();
+        int cluster_ok = cluster_slot - 1;
         if (cluster_ok < 0) {
             cluster_ok = 0;
             const int maxsm = (int)(((size_t)((kClTriMaxW + kClTri - 1) / kClTri) * kClTriMaxW + 6 * (size_t)kClTriMaxW) *
@@ -1452,6 +1456,7 @@ int syev_topk(int64_t w, const double* M, int64_t ldm, int64_t k, double* evals,
                     cluster_ok = 1;
             }
             cudaGetLastError();  // clear a refused attribute / query (grid kernel below)
+            cluster_slot = cluster_ok + 1;
         }
         if (cluster_ok == 1) {
             cudaLaunchConfig_t cfg = {};

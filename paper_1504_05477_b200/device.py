@@ -84,15 +84,25 @@ class cond_section:
 
 class _Workspace:
     """One growing scratch buffer per device. Safe because every user runs in
-    stream order on the same stream."""
+    stream order on the same stream.
+
+    Grow-only: a superseded buffer is kept referenced for the life of the
+    process, never handed back to torch's caching allocator. A CUDA graph
+    captured earlier (rsvd.GraphedFactorization, the public API's graph
+    cache) has the old address baked into its kernel parameters; an eager
+    call that grows the scratch in between must not let that memory be
+    reused by live tensors before the next replay."""
 
     def __init__(self):
         self.buf = {}
+        self.retired = []
 
     def get(self, nbytes, device):
         key = torch.device(device).index
         b = self.buf.get(key)
         if b is None or b.numel() < nbytes:
+            if b is not None:
+                self.retired.append(b)
             b = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=device)
             self.buf[key] = b
         return b
@@ -127,6 +137,42 @@ def gemm_tn(A, B, C, alpha=1.0, beta=0.0, mu=None, colsum_b=None, algo=GEMM_AUTO
     check(L.rsvd_gemm_tn(dcode(A), dcode(C), m, n, k, float(alpha), _ptr(A), _ld(A), _ptr(B), _ld(B),
                          float(beta), _ptr(C), _ld(C), _ptr(mu), _ptr(colsum_b), _ptr(ws), ws.numel(),
                          int(algo), _ptr(pred), _stream()), "gemm_tn")
+    return C
+
+
+class OzPlanes:
+    """FP32 A cut once into signed 7-bit digit planes + per-row exponents for
+    the FP64-accurate int8 tensor-core products (csrc/gemm_oz.cu)."""
+
+    def __init__(self, A):
+        assert A.dtype == torch.float32 and A.dim() == 2 and A.stride(1) == 1
+        n, d = A.shape
+        L = lib()
+        self.n, self.d = n, d
+        self.ldq = int(L.rsvd_oz_planes_ld(d))
+        self.planes = torch.empty((int(L.rsvd_oz_num_planes()), n, self.ldq), dtype=torch.int8, device=A.device)
+        self.row_exp = torch.empty(n, dtype=torch.int32, device=A.device)
+        self.refresh(A)
+
+    def refresh(self, A):
+        """Re-cut the planes from A (same shape), stream-ordered."""
+        check(lib().rsvd_oz_prepare(self.n, self.d, _ptr(A), _ld(A), _ptr(self.planes), self.ldq,
+                                    _ptr(self.row_exp), _stream()), "oz_prepare")
+        return self
+
+
+def oz_gemm(P, B, C, trans, alpha=1.0, beta=0.0, pred=None):
+    """trans=0: C (n x p) = alpha A B + beta C; trans=1: C (d x p) = alpha A^T B
+    + beta C; A given by its digit planes P, B and C FP64."""
+    assert B.dtype == torch.float64 and C.dtype == torch.float64
+    p = B.shape[1]
+    assert B.shape[0] == (P.n if trans else P.d) and C.shape == ((P.d if trans else P.n), p), (B.shape, C.shape)
+    L = lib()
+    nbytes = L.rsvd_oz_gemm_ws_bytes(int(trans), P.n, P.d, p)
+    ws = WS.get(nbytes, B.device)
+    check(L.rsvd_oz_gemm(int(trans), P.n, P.d, p, float(alpha), _ptr(P.planes), P.ldq, _ptr(P.row_exp),
+                         _ptr(B), _ld(B), float(beta), _ptr(C), _ld(C), _ptr(ws), ws.numel(), _ptr(pred),
+                         _stream()), "oz_gemm")
     return C
 
 

@@ -20,7 +20,13 @@ from . import device as ops
 
 
 class DenseDeviceOp:
-    def __init__(self, A, n_total=None, row_offset=0, center=False, comm=None):
+    """``exact=True`` (FP32 A only): the Krylov blocks are FP64 and both
+    products are FP64-accurate int8 tensor-core GEMMs (Ozaki digit planes of
+    A, csrc/gemm_oz.cu) -- the reference's float64 arithmetic on an A that
+    stays FP32 in HBM. ``prepare()`` (called at the start of every
+    factorization, inside its CUDA graph) re-cuts the digit planes from A."""
+
+    def __init__(self, A, n_total=None, row_offset=0, center=False, comm=None, exact=False):
         if A.dim() != 2 or not A.is_cuda:
             raise ValueError("DenseDeviceOp needs a 2-D CUDA tensor")
         if A.dtype not in (torch.float32, torch.float64):
@@ -33,6 +39,12 @@ class DenseDeviceOp:
         self.dtype = A.dtype
         self.device = A.device
         self.mu = None
+        self.oz = None
+        if exact:
+            if A.dtype != torch.float32:
+                raise ValueError("exact (Ozaki) products are for FP32 A; FP64 A uses FP64 products already")
+            self.oz = ops.OzPlanes(self.A)
+            self.dtype = torch.float64  # work precision of the Krylov blocks
         if center:
             mu = ops.colreduce(self.A, square=False)
             if comm is not None:
@@ -50,7 +62,20 @@ class DenseDeviceOp:
     def is_sparse(self):
         return False
 
+    def prepare(self):
+        """Per-factorization setup on the stream (exact mode: digit planes)."""
+        if self.oz is not None:
+            self.oz.refresh(self.A)
+
     def apply(self, X, out):
+        if self.oz is not None:
+            ops.oz_gemm(self.oz, X, out, trans=0)
+            if self.mu is not None:
+                # (A - 1 mu^T) X = A X - 1 (mu^T X), all FP64
+                row_sub = torch.empty((1, X.shape[1]), dtype=torch.float64, device=X.device)
+                ops.gemm_tn(self._mu_col, X, row_sub)
+                ops.gemm_nn(self._ones_col(), row_sub, out, alpha=-1.0, beta=1.0)
+            return out
         row_sub = None
         if self.mu is not None:
             X64 = X if X.dtype == torch.float64 else ops.convert(X, torch.empty(X.shape, dtype=torch.float64,
@@ -63,7 +88,19 @@ class DenseDeviceOp:
         ops.gemm_nn(self.A, X, tmp, row_sub=row_sub)
         return ops.convert(tmp, out)
 
+    def _ones_col(self):
+        if getattr(self, "_ones", None) is None:
+            self._ones = torch.ones((self.local_rows, 1), dtype=torch.float64, device=self.device)
+        return self._ones
+
     def apply_t(self, Y, out):
+        if self.oz is not None:
+            ops.oz_gemm(self.oz, Y, out, trans=1)
+            if self.mu is not None:
+                # (A - 1 mu^T)^T Y = A^T Y - mu (1^T Y) over the local rows
+                cs = ops.colreduce(Y, square=False).view(1, -1)
+                ops.gemm_nn(self._mu_col, cs, out, alpha=-1.0, beta=1.0)
+            return out
         mu = cs = None
         if self.mu is not None:
             # 1^T Y over the LOCAL rows; the caller's allreduce of out sums the
@@ -115,6 +152,9 @@ class CsrDeviceOp:
         self.t_indptr, self.t_col, self.t_val = ops.csr_transpose(indptr, col, val, nrows, self.ncols)
         self.plan = ops.SpmmPlan(indptr)
         self.t_plan = ops.SpmmPlan(self.t_indptr)
+
+    def prepare(self):
+        """Per-factorization setup (nothing for CSR)."""
 
     def _split_hot(self, indptr, col, val, nrows, dens):
         """Operator setup (torch plumbing, once): pick the hot columns, build

@@ -11,9 +11,16 @@ everything after that runs on the GPU (krylov.py).
 
 Extra keyword arguments (outside RsvdConfig, so reference configs validate
 unchanged):
-  precision  "auto" (default: FP32 path for float32 input, else FP64),
-             "fp64" or "fp32" (3xTF32 tensor-core products, FP64 small
-             algebra, FP64 re-orthonormalized Z).
+  precision  "auto" (default): float32 input -> "exact", anything else ->
+             "fp64" -- the reference's float64 arithmetic (matrix.py:80).
+             "exact": A stays FP32 in HBM, Krylov blocks and small algebra
+             are FP64 and both products A X / A^T Y are FP64-accurate int8
+             tensor-core GEMMs (Ozaki digit planes, csrc/gemm_oz.cu); the
+             reference's construction and deflation decisions are kept.
+             "fp64": A upcast to FP64 on the device, FP64 DMMA products.
+             "fp32": 3xTF32 tensor-core products, FP32 blocks with the
+             projected (block-Lanczos) basis, FP64 small algebra, FP64
+             re-orthonormalized Z -- fastest, FP32-accurate (opt-in).
   center     implicit mean-centering (PCA): factorizes A - 1 mu^T without
              forming it.
   device     CUDA device for host inputs (default: current device).
@@ -217,14 +224,23 @@ def _resolve_device(device):
     return torch.device(device)
 
 
+PRECISIONS = ("auto", "exact", "fp64", "fp32")
+
+
+def _mode(src_dtype, precision):
+    """Resolved arithmetic mode: "exact" (FP32 A, FP64-accurate products),
+    "fp64" or "fp32". "exact" only differs from "fp64" for FP32 input."""
+    if precision not in PRECISIONS:
+        raise ValueError("precision must be 'auto', 'exact', 'fp64' or 'fp32'")
+    f32 = src_dtype in (np.float32, torch.float32)
+    if precision in ("auto", "exact"):
+        return "exact" if f32 else "fp64"
+    return precision
+
+
 def _work_dtype(src_dtype, precision):
-    if precision == "fp64":
-        return torch.float64
-    if precision == "fp32":
-        return torch.float32
-    if precision != "auto":
-        raise ValueError("precision must be 'auto', 'fp64' or 'fp32'")
-    return torch.float32 if src_dtype in (np.float32, torch.float32) else torch.float64
+    """dtype A is stored in on the device."""
+    return torch.float64 if _mode(src_dtype, precision) == "fp64" else torch.float32
 
 
 def make_operator(A, precision="auto", center=False, device=None, comm=None, n_total=None, row_offset=0):
@@ -245,6 +261,7 @@ def make_operator(A, precision="auto", center=False, device=None, comm=None, n_t
     if isinstance(A, torch.Tensor):
         dev = A.device if A.is_cuda else _resolve_device(device)
         dt = _work_dtype(A.dtype, precision)
+        exact = _mode(A.dtype, precision) == "exact"
         if A.dim() != 2:
             raise ValueError("dense matrix data must be 2-D")
         if A.is_cuda:
@@ -259,7 +276,8 @@ def make_operator(A, precision="auto", center=False, device=None, comm=None, n_t
             t = raw if raw.dtype == dt else raw.to(dt)
         if not bool(torch.isfinite(t).all()):
             raise ValueError("dense matrix entries must be finite")
-        return DenseDeviceOp(t.contiguous(), n_total=n_total, row_offset=row_offset, center=center, comm=comm)
+        return DenseDeviceOp(t.contiguous(), n_total=n_total, row_offset=row_offset, center=center, comm=comm,
+                             exact=exact)
     src_dtype = np.asarray(A).dtype if not isinstance(A, DenseMatrix) else np.float64
     arr = as_dense_array(A) if not (isinstance(A, np.ndarray) and A.dtype == np.float32) else np.asarray(A)
     if arr.ndim != 2:
@@ -269,7 +287,8 @@ def make_operator(A, precision="auto", center=False, device=None, comm=None, n_t
     dev = _resolve_device(device)
     dt = _work_dtype(src_dtype, precision)
     t = torch.from_numpy(np.ascontiguousarray(arr)).to(device=dev, dtype=dt, non_blocking=False)
-    return DenseDeviceOp(t, n_total=n_total, row_offset=row_offset, center=center, comm=comm)
+    return DenseDeviceOp(t, n_total=n_total, row_offset=row_offset, center=center, comm=comm,
+                         exact=_mode(src_dtype, precision) == "exact")
 
 
 # --------------------------------------------------------------------------
@@ -318,6 +337,7 @@ def run_device(op, cfg, comm=None, Pi=None):
     else:
         pi_dev = torch.from_numpy(np.array(Pi, copy=True)).to(device=op.device, dtype=op.dtype, non_blocking=True)
     ws = krylov.Workspace(op.device, p)
+    op.prepare()  # exact mode: digit planes of A, inside the timed / captured region
     deflated = None
     if cfg.variant is Variant.SIMULTANEOUS_ITERATION:
         Q = krylov.si_basis(ops, c, op, pi_dev, q, cfg.reorthonormalize_every, ws, n_total, row_offset)
@@ -446,7 +466,7 @@ def _graph_cache_key(A, cfg, precision, device, center=False):
     dt = _work_dtype(src, precision)
     q = cfg.resolve_q(shape[1])
     return (shape, dt, str(dev), cfg.k, cfg.p, q, cfg.variant, int(cfg.seed), cfg.reorthonormalize_every,
-            bool(center))
+            bool(center), _mode(src, precision))
 
 
 def _upload_into(buf, A):
@@ -491,7 +511,7 @@ def _run(A, cfg, expected, precision="auto", center=False, device=None, comm=Non
             buf = torch.empty(shape, dtype=dt, device=dev)
             if center:
                 buf.zero_()
-            op = DenseDeviceOp(buf, center=center)
+            op = DenseDeviceOp(buf, center=center, exact=key[-1] == "exact")
             pi_host = gaussian(shape[1], cfg.p, SeededRng(cfg.seed)).data
             pi_dev = torch.from_numpy(np.array(pi_host, copy=True)).to(device=dev, dtype=dt)
             entry = [buf, op, GraphedFactorization(op, cfg), pi_dev, 0]

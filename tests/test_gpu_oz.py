@@ -1,0 +1,124 @@
+"""FP64-accurate int8 tensor-core products of an FP32 A (csrc/gemm_oz.cu)
+against cuBLAS FP64 GEMMs of the same (exactly upcast) operands.
+
+The reference computes every product in float64 on A upcast from float32
+(matrix.py:80, _kernels.pyx:56-71); the Ozaki digit-plane kernels must match
+that arithmetic to FP64 rounding: normwise relative error <= 1e-14 (the
+scheme's neglected terms are ~2^-56 |A||X| per entry)."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-14
+# against cuBLAS DGEMM (whose own blocked FP64 accumulation is ~1e-13 off at
+# K ~ 1e4); the exact check against 80-bit host sums is test_oz_vs_extended
+TOL_DGEMM = 3e-13
+
+
+def _ops():
+    from paper_1504_05477_b200 import device as ops
+
+    return ops
+
+
+def _case(n, d, seed, row_spread=0.0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    A = torch.randn((n, d), generator=g, device="cuda", dtype=torch.float64)
+    if row_spread:
+        # rows of very different magnitude (per-row exponents must follow)
+        A *= torch.exp(row_spread * torch.randn((n, 1), generator=g, device="cuda", dtype=torch.float64))
+    return A.float()
+
+
+def _normwise(C, ref, left, right):
+    """max_ij |C - ref|_ij / (|left_i| |right_j|) (normwise per entry)."""
+    den = torch.outer(left.norm(dim=1), right.norm(dim=0)).clamp_min(1e-300)
+    return float(((C - ref).abs() / den).max())
+
+
+@pytest.mark.parametrize("n,d,p", [(1000, 700, 50), (4133, 2051, 20), (3000, 1000, 64), (2000, 1500, 130),
+                                   (257, 33, 7), (20000, 400, 50)])
+def test_oz_nn_tn_match_fp64(n, d, p):
+    ops = _ops()
+    A = _case(n, d, n + d + p, row_spread=2.0)
+    A64 = A.double()
+    g = torch.Generator(device="cuda").manual_seed(7)
+    X = torch.randn((d, p), generator=g, device="cuda", dtype=torch.float64)
+    Y = torch.randn((n, p), generator=g, device="cuda", dtype=torch.float64)
+    P = ops.OzPlanes(A)
+    C = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    ops.oz_gemm(P, X, C, trans=0)
+    W = torch.empty((d, p), dtype=torch.float64, device="cuda")
+    ops.oz_gemm(P, Y, W, trans=1)
+    torch.cuda.synchronize()
+    e_nn = _normwise(C, A64 @ X, A64, X)
+    e_tn = _normwise(W, A64.T @ Y, A64.T, Y)
+    assert e_nn < TOL_DGEMM, e_nn
+    assert e_tn < TOL_DGEMM, e_tn
+
+
+def test_oz_vs_extended():
+    """Against 80-bit extended-precision host sums (numpy longdouble): the
+    digit-plane products are FP64-accurate, at least as close as cuBLAS DGEMM."""
+    import numpy as np
+
+    ops = _ops()
+    n, d, p = 700, 900, 24
+    A = _case(n, d, 5, row_spread=1.0)
+    g = torch.Generator(device="cuda").manual_seed(2)
+    X = torch.randn((d, p), generator=g, device="cuda", dtype=torch.float64)
+    Y = torch.randn((n, p), generator=g, device="cuda", dtype=torch.float64)
+    P = ops.OzPlanes(A)
+    C = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    W = torch.empty((d, p), dtype=torch.float64, device="cuda")
+    ops.oz_gemm(P, X, C, trans=0)
+    ops.oz_gemm(P, Y, W, trans=1)
+    torch.cuda.synchronize()
+    Ah = A.double().cpu().numpy().astype(np.longdouble)
+    Xh = X.cpu().numpy().astype(np.longdouble)
+    Yh = Y.cpu().numpy().astype(np.longdouble)
+    for ours, blas, exact, left, right in (
+            (C, A.double() @ X, Ah @ Xh, Ah, Xh), (W, A.double().T @ Y, Ah.T @ Yh, Ah.T, Yh)):
+        den = np.outer(np.linalg.norm(left.astype(np.float64), axis=1), np.linalg.norm(right.astype(np.float64), axis=0))
+        e_ours = float(np.max(np.abs(ours.cpu().numpy() - exact).astype(np.float64) / den))
+        e_blas = float(np.max(np.abs(blas.cpu().numpy() - exact).astype(np.float64) / den))
+        assert e_ours < TOL, (e_ours, e_blas)
+        assert e_ours <= 2 * e_blas + 1e-17, (e_ours, e_blas)
+
+
+def test_oz_long_reduction_splits():
+    """A^T Y with n > 16384 (several K splits: int32 exactness bound) and
+    alpha / beta handling."""
+    ops = _ops()
+    n, d, p = 70000, 300, 50
+    A = _case(n, d, 3)
+    A64 = A.double()
+    g = torch.Generator(device="cuda").manual_seed(9)
+    Y = torch.randn((n, p), generator=g, device="cuda", dtype=torch.float64)
+    W0 = torch.randn((d, p), generator=g, device="cuda", dtype=torch.float64)
+    P = ops.OzPlanes(A)
+    W = W0.clone()
+    ops.oz_gemm(P, Y, W, trans=1, alpha=-0.5, beta=2.0)
+    ref = -0.5 * (A64.T @ Y) + 2.0 * W0
+    torch.cuda.synchronize()
+    err = float(((W - ref).abs()).max() / (A64.T.abs() @ Y.abs()).max())
+    assert err < TOL_DGEMM, err
+
+
+def test_oz_zero_rows_and_columns():
+    """All-zero rows of A and zero columns of B give exact zeros."""
+    ops = _ops()
+    n, d, p = 600, 300, 40
+    A = _case(n, d, 11)
+    A[17] = 0.0
+    A[:, 5] = 0.0
+    X = torch.randn((d, p), device="cuda", dtype=torch.float64)
+    X[:, 3] = 0.0
+    P = ops.OzPlanes(A)
+    C = torch.empty((n, p), dtype=torch.float64, device="cuda")
+    ops.oz_gemm(P, X, C, trans=0)
+    torch.cuda.synchronize()
+    assert bool((C[17] == 0).all()) and bool((C[:, 3] == 0).all())
+    assert _normwise(C, A.double() @ X, A.double(), X) < TOL_DGEMM
