@@ -6,21 +6,35 @@ on the GPU in FP64, cast to FP32), block Krylov k = 50, q = 10 (-> 11, the
 reference's odd bump, rsvd.py:157-158), Krylov width 600, Pi = host
 SeededRng(0) Gaussian 10,000 x 50. Synthetic data (no dataset is named).
 
-One step = one complete factorization (start block upload, Krylov chain,
-blocked orthonormalization, Rayleigh-Ritz + Jacobi, Z and sigma ready).
+Precision mode of the measured path (per config, --precision overrides):
+  C2 "exact": A stays FP32 in HBM; Krylov blocks, orthonormalization and
+     Rayleigh-Ritz are FP64; both products A X / A^T Y are FP64-accurate int8
+     tensor-core GEMMs (Ozaki digit planes, csrc/gemm_oz.cu); the reference's
+     own basis construction (normalized power blocks, then _mgs of their
+     hstack, rsvd.py:244-260) -- the mode that matches the reference to the
+     north_star tolerance at this config (the FP32 3xTF32 path misses it, see
+     the fp32_mode leg).
+  C1 "fp64" (an FP64 config); C4 / C5 "fp32" (3xTF32; parity passes there).
+
+One step = one complete factorization (start block upload, digit planes of A,
+Krylov chain, blocked orthonormalization, Rayleigh-Ritz + eigensolver, Z and
+sigma ready).
   value : device-resident A (uploaded before timing), CUDA-event timed.
-  e2e   : the public drop-in call block_krylov(A_host_pinned, cfg) — H2D of A
-          and D2H of (Z, sigma) inside the timed region, every step.
+  e2e   : the public drop-in call block_krylov(A_host_pinned, cfg) -- H2D of A
+          and D2H of (Z, sigma) inside the timed region, every step
+          (e2e_numpy: the same call with a pageable numpy array).
 A (2 GB FP32) is larger than L2 (126 MB), so every step streams it from HBM.
 
 --impl reference: the reference's CPU algorithm (the oracle port,
-oracle/rsvd_oracle.py, numpy/BLAS products + C Jacobi, all host threads) on
-the same A, timed per stage on a bounded sample and scaled to one
-factorization (see cpu_baseline.sample).
+oracle/rsvd_oracle.py: numpy/OpenBLAS FP64 products as the reference's python
+backend, the C restatement of its Jacobi, its per-column CGS2 _mgs) on a
+host-generated A of the same config (numpy only -- no GPU, nothing from the
+product package), all host threads.
 
-N > 1 (torchrun): A is row-sharded across ranks; the step is
-the same factorization of the same A (strong scaling); A^T Y, Grams and
-projections are NCCL allreduces.
+--gpus N: N ranks (one per GPU) over NCCL, A row-sharded; the
+step is the same factorization of the same A (strong scaling); A^T Y, Grams
+and projections are allreduced. Without torchrun the script relaunches itself
+under torch.distributed.run (NCCL_DEBUG=INFO so the communicator prints).
 """
 
 from __future__ import annotations
@@ -44,14 +58,16 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    "c2": dict(n=50000, d=10000, k=50, q=10, spectrum="pow", noise=1e-3, variant="bk"),
-    "c1": dict(n=2000, d=1000, k=20, q=8, spectrum="inv", noise=0.0, variant="bk", fp64=True),
-    "c4": dict(n=1000000, d=4096, k=200, q=6, spectrum="clustered", noise=0.0, variant="bk"),
-    "c3": dict(n=200000, d=100000, k=100, q=15, sparse=True, variant="bk"),
+    "c2": dict(n=50000, d=10000, k=50, q=10, spectrum="pow", noise=1e-3, variant="bk", mode="exact"),
+    "c1": dict(n=2000, d=1000, k=20, q=8, spectrum="inv", noise=0.0, variant="bk", fp64=True, mode="fp64"),
+    "c4": dict(n=1000000, d=4096, k=200, q=6, spectrum="clustered", noise=0.0, variant="bk", mode="fp32"),
+    "c3": dict(n=200000, d=100000, k=100, q=15, sparse=True, variant="bk", mode="fp32"),
     # C5: PCA with implicit mean-centering (rank-1 GEMM-epilogue corrections)
-    "c5": dict(n=500000, d=2000, k=200, q=4, pca=True, variant="bk"),
-    "c5si": dict(n=500000, d=2000, k=200, q=12, pca=True, variant="si"),
+    "c5": dict(n=500000, d=2000, k=200, q=4, pca=True, variant="bk", mode="fp32"),
+    "c5si": dict(n=500000, d=2000, k=200, q=12, pca=True, variant="si", mode="fp32"),
 }
+MODE_DTYPE = {"exact": "f64 (FP32 A; FP64-accurate int8 tcgen05 Ozaki products, FP64 blocks and small algebra)",
+              "fp32": "f32 (3xTF32 products, f64 small algebra)", "fp64": "f64"}
 
 
 def make_csr(cfg, device, seed=4321):
@@ -123,7 +139,8 @@ def workload_config(name, cfgd, cfg, world, nnz=None):
         w = cfg.p
     label = "SI" if si else "BK"
     what = (f"CSR FP32 A {n}x{d} nnz {nnz}" if sparse else
-            f"PCA (implicit centering) on dense FP32 A {n}x{d}" if cfgd.get("pca") else f"dense FP32 A {n}x{d}")
+            f"PCA (implicit centering) on dense FP32 A {n}x{d}" if cfgd.get("pca") else
+            f"dense {'FP64' if cfgd.get('fp64') else 'FP32'} A {n}x{d}")
     return {"workload": (f"{name.upper()}: " + what
                          + f", {label} k={k} q={cfgd['q']}->{cfg.resolve_q(d)}, width {w}"),
             "n": n, "d": d, "k": k, "q": cfgd["q"], "q_eff": cfg.resolve_q(d), "krylov_width": w,
@@ -218,18 +235,22 @@ def gemm_c4_probe(dev, bf16, reps=3):
     return res
 
 
-def _profiled_traffic(config="c2"):
-    """DRAM bytes per launch of the chain kernel from the committed ncu --set
-    full capture (profiles/r01_chain_kernel_ncu.json for C2,
-    profiles/r01_<config>_chain_kernel_ncu.json otherwise: dram__bytes_read.sum
-    + dram__bytes_write.sum), or None when no capture is committed."""
-    name = "r01_chain_kernel_ncu.json" if config == "c2" else f"r01_{config}_chain_kernel_ncu.json"
-    path = os.path.join(ROOT, "profiles", name)
-    try:
-        with open(path) as f:
-            return float(json.load(f)["dram_bytes_per_launch"])
-    except (OSError, KeyError, ValueError):
-        return None
+def _profiled_traffic(config="c2", mode="fp32"):
+    """DRAM bytes per launch of the dominant chain kernel from the committed
+    ncu --set full capture (dram__bytes_read.sum + dram__bytes_write.sum):
+    profiles/r02_<config>_<mode>_chain_kernel_ncu.json, else the round-1
+    capture of the 3xTF32 kernel for the fp32 mode; None when none is
+    committed."""
+    names = [f"r02_{config}_{mode}_chain_kernel_ncu.json"]
+    if mode == "fp32":
+        names.append("r01_chain_kernel_ncu.json" if config == "c2" else f"r01_{config}_chain_kernel_ncu.json")
+    for name in names:
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                return float(json.load(f)["dram_bytes_per_launch"])
+        except (OSError, KeyError, ValueError):
+            continue
+    return None
 
 
 def make_pca_matrix(cfg, device, seed=777):
@@ -412,6 +433,9 @@ def run_ours(args):
     n, d, k = cfgd["n"], cfgd["d"], cfgd["k"]
     cfg = rk.RsvdConfig(k=k, variant=cfgd["variant"], q=cfgd["q"], seed=0)
     sparse = bool(cfgd.get("sparse"))
+    mode = args.precision or cfgd["mode"]
+    if cfgd.get("fp64") or sparse:
+        mode = cfgd["mode"] if not args.precision else args.precision
     lo, hi = krylov.shard_rows(n, world, rank)
     if world > 1:
         comm = krylov.TorchComm(n_total=n, row_offset=lo)
@@ -435,7 +459,10 @@ def run_ours(args):
             del A_full
         else:
             A = A_full
-        op = DenseDeviceOp(A, n_total=n, row_offset=lo, center=bool(cfgd.get("pca")), comm=comm)
+        if mode == "fp64" and A.dtype != torch.float64:
+            A = A.double()
+        op = DenseDeviceOp(A, n_total=n, row_offset=lo, center=bool(cfgd.get("pca")), comm=comm,
+                           exact=(mode == "exact"))
     Pi = rk.gaussian(d, cfg.p, rk.SeededRng(cfg.seed)).data
 
     # instrumentation of the dominant kernels (A X / A^T Y on the op's stream)
@@ -528,34 +555,47 @@ def run_ours(args):
     assert int(info[0]) == 1, "Jacobi did not converge"
     sigma = df.sigma.cpu().numpy()
 
-    # kernel roofline: the Krylov-chain products at width p (HBM bound)
+    # kernel roofline: the Krylov-chain products at width p
     hbm, bf16, peak_src = _peaks()
     chain = [(e0_.elapsed_time(e1_), kind) for kind, width, e0_, e1_ in events if width == cfg.p]
     rr = [(e0_.elapsed_time(e1_), kind) for kind, width, e0_, e1_ in events if width != cfg.p]
     n_loc = hi - lo
     if sparse:  # nnz (4 + 4) + (rows + 1) 4 + (d + n) b 4 per SpMM
         bytes_per = nnz_local * 8 + (n_loc + 1) * 4 + (n_loc + d) * cfg.p * 4
-    else:
-        es = A.element_size()
-        bytes_per = n_loc * d * es + (n_loc + d) * cfg.p * es
+    else:  # A once (its stored precision) + the two blocks (the work precision)
+        bytes_per = n_loc * d * A.element_size() + (n_loc + d) * cfg.p * (8 if mode in ("exact", "fp64") else 4)
     avg_chain_ms = float(np.mean([t for t, _ in chain])) if chain else float("nan")
     achieved = bytes_per / (avg_chain_ms * 1e-3) / 1e9
     rr_ms = float(np.mean([t for t, _ in rr])) if rr else float("nan")
     w = (cfgd["q"] + 1 + (cfgd["q"] % 2 == 0)) * cfg.p
     rr_tflops = 2.0 * n_loc * d * w / (rr_ms * 1e-3) / 1e12 if (rr and not sparse) else None
 
-    # the chain product's bound: HBM below the 3xTF32 ridge (C2: 25 flop/B),
+    # the chain product's bound: HBM below the ridge (C2: 25 flop/B in FP32),
     # tensor pipe above it (C4 / C5 at width 200: ~95 flop/B)
     flops_per = 2.0 * n_loc * d * cfg.p
     tf_eff = bf16 / 6.0  # TF32 issues at half the bf16 rate; 3xTF32 = 3 MMAs per product
-    kname = (("hybrid CSR product A.X / A^T.Y (width %d; hot-column panel on tcgen05 + CSR gather)"
-              if sparse and op.hot is not None else "CSR SpMM A.X / A^T.Y (width %d)") if sparse
-             else "Krylov-chain A.X / A^T.Y (width %d)") % cfg.p
-    traffic = None if sparse else _profiled_traffic(args.config)
-    if sparse or flops_per / bytes_per * hbm / 1e3 < tf_eff:
+    if sparse:
+        kname = (("hybrid CSR product A.X / A^T.Y (width %d; hot-column panel on tcgen05 + CSR gather)"
+                  if op.hot is not None else "CSR SpMM A.X / A^T.Y (width %d)") % cfg.p)
+    elif mode == "exact":
+        kname = ("FP64-accurate Krylov-chain A.X / A^T.Y (width %d): k_oz_gemm, int8 tcgen05 Ozaki digit planes "
+                 "(6 A x 7 B digits, 27 digit-pair GEMMs)" % cfg.p)
+    else:
+        kname = "Krylov-chain A.X / A^T.Y (width %d)" % cfg.p
+    traffic = None if sparse else _profiled_traffic(args.config, mode)
+    if sparse or mode == "exact" or flops_per / bytes_per * hbm / 1e3 < tf_eff:
         roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                     "frac": achieved / hbm, "peak_source": peak_src, "traffic": traffic,
                     "algorithmic_bytes_per_launch": bytes_per, "avg_launch_ms": avg_chain_ms}
+        if mode == "exact":
+            # what the kernel actually streams: the 6 digit planes of A (1.5x the
+            # FP32 bytes) and the int8 MMA work (27 digit pairs, N padded to 64)
+            planes = 6 * (-(-n_loc // 128) * 128) * (-(-d // 128) * 128)
+            roofline["digit_plane_bytes_per_launch"] = planes
+            roofline["digit_plane_gbs"] = planes / (avg_chain_ms * 1e-3) / 1e9
+            roofline["int8_tops"] = 27 * 2.0 * n_loc * d * 64 * (-(-cfg.p // 64)) / (avg_chain_ms * 1e-3) / 1e12
+            roofline["note"] = ("algorithmic bytes = FP32 A + FP64 blocks; the kernel streams A's int8 digit "
+                                "planes (digit_plane_gbs) and is co-limited by the int8 MMA issue (27 digit pairs)")
     else:
         tfl = flops_per / (avg_chain_ms * 1e-3) / 1e12
         roofline = {"bound": "tensor", "kernel": kname, "achieved": tfl, "peak": tf_eff, "unit": "TFLOP/s",
@@ -566,22 +606,37 @@ def run_ours(args):
                     "algorithmic_bytes_per_launch": bytes_per, "avg_launch_ms": avg_chain_ms,
                     "hbm_frac": achieved / hbm}
 
-    # e2e through the public API with host (pinned) A
-    e2e = None
+    # e2e through the public API with host A: pinned torch tensor (the line's
+    # e2e) and a pageable numpy array (the reference callers' usual input)
+    e2e = e2e_np = None
     if world == 1 and not args.no_e2e and not sparse:
-        A_host = A.cpu().pin_memory()
         center = bool(cfgd.get("pca"))
-        for _ in range(max(1, min(args.warmup, 2))):
-            r = rk.factorize(A_host, cfg, center=center)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            r = rk.factorize(A_host, cfg, center=center)
-        torch.cuda.synchronize()
-        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
-        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": int(A_host.numel() * A_host.element_size() + Pi.size * 4),
-               "d2h_bytes_per_step": int(n * k * 8 + k * 8 + 8 * 3)}
+        api_prec = mode
+
+        def timed_api(A_in):
+            for _ in range(max(1, min(args.warmup, 2))):
+                rk.factorize(A_in, cfg, center=center, precision=api_prec)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                r = rk.factorize(A_in, cfg, center=center, precision=api_prec)
+            torch.cuda.synchronize()
+            return (time.perf_counter() - t0) * 1e3 / args.steps, r
+
+        # per step: H2D of A (Pi is uploaded once per cached shape/config, like A's
+        # device buffer), D2H of Z (n x k FP64), sigma and the status words
+        d2h = int(n * k * 8 + k * 8 + 8 * 3)
+        A_host = A.cpu().pin_memory()
+        e2e_ms, r = timed_api(A_host)
+        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": int(A_host.numel() * A_host.element_size()),
+               "d2h_bytes_per_step": d2h, "input": "pinned torch tensor",
+               "sigma_matches_value_path": bool(np.allclose(r.approx_singular_values, sigma, rtol=1e-12, atol=0))}
+        A_np = A_host.numpy().copy()
         del A_host
+        e2e_np_ms, _ = timed_api(A_np)
+        e2e_np = {"value": e2e_np_ms, "unit": "ms", "h2d_bytes_per_step": int(A_np.nbytes), "d2h_bytes_per_step": d2h,
+                  "input": "pageable numpy array"}
+        del A_np
 
     out = {
         "metric": "rank-k block-Krylov SVD wall time",
@@ -594,8 +649,8 @@ def run_ours(args):
         "higher_is_better": False,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": ("f32 (CSR SpMM, f64 small algebra)" if sparse else
-                  "f32 (3xTF32 products, f64 small algebra)" if A.dtype == torch.float32 else "f64"),
+        "dtype": ("f32 (CSR SpMM, f64 small algebra)" if sparse else MODE_DTYPE[mode]),
+        "precision_mode": mode,
         "data": "synthetic",
         "config": workload_config(args.config, cfgd, cfg, world, nnz_local if sparse else None),
         "roofline": roofline,
@@ -603,13 +658,16 @@ def run_ours(args):
                     {"rayleigh_ritz_W": "assembled from the chain's A^T q_j (projected FP32 basis); "
                                         "no separate width-w pass over A"}),
         "gpu_launches": launches,
+        "comm": ({"backend": backend, "world": torch.distributed.get_world_size(), "rank_rows": [lo, hi]}
+                 if world > 1 else None),
         "clocks": clk.summary(),
         "sigma_head": [float(x) for x in sigma[:3]],
     }
     if e2e:
         out["e2e"] = e2e
+        out["e2e_numpy"] = e2e_np
     if rank == 0 and world == 1 and not args.no_cpu and not sparse:
-        out["cpu_baseline"] = cpu_baseline(A, cfgd, cfg, Pi, args, df)
+        out["cpu_baseline"] = cpu_baseline(A, cfgd, cfg, Pi, args, df, mode)
     if rank == 0 and world == 1 and not sparse and not args.no_spmm:
         out["spmm_c3"] = spmm_probe(dev)
     if rank == 0 and world == 1 and args.config == "c2" and not args.no_c4gemm:
@@ -652,12 +710,14 @@ LAUNCHES_PER_CALL = {"rsvd_gemm_tn": 2, "rsvd_colreduce": 2, "rsvd_canonicalize_
                      "rsvd_eig_select": 2, "rsvd_col_absargmax": 2}
 
 
-def cpu_baseline(A_dev, cfgd, cfg, Pi, args, df=None):
+def cpu_baseline(A_dev, cfgd, cfg, Pi, args, df=None, mode="exact"):
     """The reference algorithm (oracle port) on the box's host cores, one
     full factorization; with the device result `df` also the north_star
-    parity of this run: max relative error of all k singular values and of
-    the per-vector captured variance ||A^T z_i||^2 (metrics.py:136), both
-    evaluated in FP64 on the same A."""
+    parity of this run: max relative error of all k singular values, of the
+    per-vector captured variance ||A^T z_i||^2 (metrics.py:136) and of the
+    spectral error ||A - Z Z^T A||_2 (the reference's restarted power
+    estimator, metrics.py:102-122 / factor.py:217-261, run on the GPU for both
+    Z's with identical starts and stopping rule), all on the same A."""
     res, r = reference_sample(A_dev.cpu().numpy(), cfgd, cfg, Pi, budget_s=args.cpu_budget, return_result=True)
     if df is not None:
         import torch
@@ -667,17 +727,90 @@ def cpu_baseline(A_dev, cfgd, cfg, Pi, args, df=None):
         if cfgd.get("pca"):
             A64 -= A64.mean(0, keepdim=True)
         cap = (A64.T @ df.Z.double()).pow(2).sum(0).cpu().numpy()
-        cap_ref = (A64.T @ torch.from_numpy(np.ascontiguousarray(r.Z)).to(A64.device)).pow(2).sum(0).cpu().numpy()
+        Zref = torch.from_numpy(np.ascontiguousarray(r.Z)).to(A64.device)
+        cap_ref = (A64.T @ Zref).pow(2).sum(0).cpu().numpy()
         del A64
+        tol = 1e-10 if A_dev.dtype == torch.float64 else 1e-4
         res["parity"] = {"sigma_rel_max": float(np.max(np.abs(sig - r.sigma) / r.sigma)),
                          "sigma_rel_median": float(np.median(np.abs(sig - r.sigma) / r.sigma)),
                          "captured_variance_rel_max": float(np.max(np.abs(cap - cap_ref) / cap_ref)),
-                         "tolerance": 1e-4 if A_dev.dtype == torch.float32 else 1e-10}
+                         "tolerance": tol, "replaced_columns_reference": len(r.replaced),
+                         "replaced_columns_ours": (int(df.deflated.sum()) if df.deflated is not None else None)}
+        if not args.no_spectral:
+            res["parity"]["spectral_error"] = spectral_parity(A_dev, cfgd, df.Z, r.Z, args.spectral_iters)
+        res["parity"]["pass"] = bool(res["parity"]["sigma_rel_max"] <= tol and
+                                     res["parity"]["captured_variance_rel_max"] <= tol and
+                                     res["parity"].get("spectral_error", {}).get("rel", 0.0) <= max(tol, 1e-6))
         if A_dev.dtype == torch.float32 and not args.no_fp64:
-            res["parity_fp64_mode"] = fp64_mode_leg(A_dev, cfgd, cfg, Pi, r)
-            if not cfgd.get("sparse"):
-                res["parity_decomposition"] = parity_decomposition(A_dev, cfgd, cfg, Pi, r, sig, cap)
+            res["parity_fp64_mode"] = mode_leg(A_dev, cfgd, cfg, Pi, r, "fp64")
+        if A_dev.dtype == torch.float32 and mode != "fp32" and not args.no_fp32:
+            res["parity_fp32_mode"] = mode_leg(A_dev, cfgd, cfg, Pi, r, "fp32")
     return res
+
+
+def spectral_parity(A_dev, cfgd, Z_ours, Z_ref, max_iters):
+    """||A - Z Z^T A||_2 by the reference's estimator (seeds 101/202/303, tol
+    1e-9, at most `max_iters` power iterations per start, batched as 3
+    columns; metrics.py:36-38, 116-121) for our Z and the reference's Z on
+    the same operator (FP64-accurate products of the FP32 A)."""
+    import torch
+
+    from paper_1504_05477_b200 import metrics as M
+    from paper_1504_05477_b200.operators import DenseDeviceOp
+
+    if cfgd.get("pca"):
+        A = A_dev.double()
+        A -= A.mean(0, keepdim=True)
+        op = DenseDeviceOp(A)
+    else:
+        op = DenseDeviceOp(A_dev, exact=A_dev.dtype == torch.float32)
+    op.prepare()
+    t0 = time.perf_counter()
+    out = {}
+    for name, Z in (("ours", Z_ours), ("reference_Z", np.ascontiguousarray(Z_ref))):
+        best, its = M.spectral_norm_batched(M._Deflated(op, M._as_device_z(Z, op)), max_iters=max_iters)
+        out[name] = float(np.max(best))
+        out[name + "_iterations"] = [int(x) for x in its]
+    out["rel"] = abs(out["ours"] - out["reference_Z"]) / out["reference_Z"]
+    out["max_iters"] = max_iters
+    out["seconds"] = time.perf_counter() - t0
+    del op
+    torch.cuda.empty_cache()
+    return out
+
+
+def mode_leg(A_dev, cfgd, cfg, Pi, r, mode):
+    """Another precision mode of this path on the same A and Pi (graph
+    replay, one timed step) and its parity against the same reference run:
+    "fp64" = A upcast on the device (as the reference upcasts FP32 input,
+    matrix.py:80), FP64 DMMA products; "fp32" = 3xTF32 products with the
+    projected basis (fastest; FP32-accurate)."""
+    import torch
+
+    from paper_1504_05477_b200 import rsvd
+    from paper_1504_05477_b200.operators import DenseDeviceOp
+
+    Aw = A_dev.double() if mode == "fp64" else A_dev
+    op = DenseDeviceOp(Aw, center=bool(cfgd.get("pca")))
+    g = rsvd.GraphedFactorization(op, cfg)
+    g.run(Pi)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    df = g.run(Pi)
+    e1.record()
+    torch.cuda.synchronize()
+    sig = df.sigma.cpu().numpy()
+    A64 = A_dev.double()
+    if cfgd.get("pca"):
+        A64 -= A64.mean(0, keepdim=True)
+    cap = (A64.T @ df.Z.double()).pow(2).sum(0).cpu().numpy()
+    cap_ref = (A64.T @ torch.from_numpy(np.ascontiguousarray(r.Z)).to(A64.device)).pow(2).sum(0).cpu().numpy()
+    del A64, op, g, Aw
+    torch.cuda.empty_cache()
+    return {"ms": e0.elapsed_time(e1), "sigma_rel_max": float(np.max(np.abs(sig - r.sigma) / r.sigma)),
+            "captured_variance_rel_max": float(np.max(np.abs(cap - cap_ref) / cap_ref)),
+            "tolerance": 1e-4, "dtype": MODE_DTYPE[mode]}
 
 
 def parity_decomposition(A_dev, cfgd, cfg, Pi, r, sig32, cap32):
@@ -716,40 +849,6 @@ def parity_decomposition(A_dev, cfgd, cfg, Pi, r, sig32, cap32):
             "note": "FP64 run of this path's projected construction on the same A and Pi"}
 
 
-def fp64_mode_leg(A_dev, cfgd, cfg, Pi, r):
-    """The FP64 path (precision="fp64": A upcast on the device as the
-    reference upcasts FP32 input, matrix.py:80; FP64 products and the
-    reference-faithful power-block basis) on the same A and Pi: its time and
-    its parity against the same reference result. This is the mode for
-    reference-exact results; the headline FP32 path trades the reference's
-    own FP64 rounding pattern in the unconverged tail for 3xTF32 speed."""
-    import torch
-
-    from paper_1504_05477_b200 import rsvd
-    from paper_1504_05477_b200.operators import DenseDeviceOp
-
-    A64 = A_dev.double()
-    op = DenseDeviceOp(A64, center=bool(cfgd.get("pca")))
-    g = rsvd.GraphedFactorization(op, cfg)
-    g.run(Pi)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    df = g.run(Pi)
-    e1.record()
-    torch.cuda.synchronize()
-    sig = df.sigma.cpu().numpy()
-    if cfgd.get("pca"):
-        A64 -= A64.mean(0, keepdim=True)
-    cap = (A64.T @ df.Z.double()).pow(2).sum(0).cpu().numpy()
-    cap_ref = (A64.T @ torch.from_numpy(np.ascontiguousarray(r.Z)).to(A64.device)).pow(2).sum(0).cpu().numpy()
-    del A64, op, g
-    torch.cuda.empty_cache()
-    return {"ms": e0.elapsed_time(e1), "sigma_rel_max": float(np.max(np.abs(sig - r.sigma) / r.sigma)),
-            "captured_variance_rel_max": float(np.max(np.abs(cap - cap_ref) / cap_ref)),
-            "tolerance": 1e-4, "dtype": "f64 (A upcast on the device, FP64 products)"}
-
-
 def reference_sample(A32, cfgd, cfg, Pi, budget_s=25.0, return_result=False):
     """One full factorization by the reference algorithm on the box's host
     cores: the oracle port (oracle/rsvd_oracle.py) — numpy/OpenBLAS products
@@ -766,7 +865,7 @@ def reference_sample(A32, cfgd, cfg, Pi, budget_s=25.0, return_result=False):
         A -= A.mean(axis=0, keepdims=True)
     op = o.DenseOp(A)
     op.apply(Pi[:, :1])  # BLAS thread-pool warm-up outside the timer
-    variant = cfg.variant.value if hasattr(cfg.variant, "value") else str(cfg.variant)
+    variant = cfg.variant.value if hasattr(cfg.variant, "value") else str(cfg.variant)  # RsvdConfig / RefConfig
     t0 = time.perf_counter()
     r = o.factorize(op, cfg.k, variant, q=cfg.q, p=cfg.p, seed=cfg.seed)
     secs = time.perf_counter() - t0
@@ -779,26 +878,95 @@ def reference_sample(A32, cfgd, cfg, Pi, budget_s=25.0, return_result=False):
     return (out, r) if return_result else out
 
 
-def run_reference(args):
-    import torch
+class RefConfig:
+    """RsvdConfig-equivalent scalars for the reference arm, from the oracle's
+    restatement of the reference's q resolution (rsvd.py:151-162) -- the
+    reference arm imports nothing from the product package."""
 
+    def __init__(self, k, variant, q, seed=0):
+        self.k, self.p, self.q, self.seed, self.variant = int(k), int(k), int(q), int(seed), str(variant)
+
+    def resolve_q(self, d):
+        return _oracle().resolve_q(self.variant, self.q, d)
+
+
+def _oracle():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import rsvd_oracle
+
+    return rsvd_oracle
+
+
+def make_matrix_host(cfgd, seed=1234):
+    """The dense configs' construction on the host with numpy only (the
+    reference arm runs no GPU code): Haar V from the QR of a seeded d x d
+    Gaussian (sign-fixed by diag R), Haar U from the CholeskyQR of a seeded
+    n x d Gaussian generated in row chunks (cond(G) ~ 2.6 at C2, exactly
+    orthonormal to FP64 rounding), A = U diag(s) V^T (+ noise), FP32. Same
+    spectrum / shape / distribution as make_matrix (a different draw: the
+    parity legs run on the device-built A inside the measured arm)."""
+    import scipy.linalg as sla
+
+    n, d = cfgd["n"], cfgd["d"]
+    if cfgd.get("pca"):
+        rng = np.random.default_rng(seed)
+        W, R = np.linalg.qr(rng.standard_normal((d, d)))
+        W *= np.sign(np.diag(R))[None, :]
+        lam = np.exp(-np.arange(1, d + 1) / 50.0)
+        mu = rng.uniform(-5.0, 5.0, d)
+        M = (W * np.sqrt(lam)[None, :]).T.copy()
+        A = np.empty((n, d), dtype=np.float32)
+        for c, r0 in enumerate(range(0, n, 65536)):
+            r1 = min(n, r0 + 65536)
+            G = np.random.default_rng([seed, 1, c]).standard_normal((r1 - r0, d))
+            A[r0:r1] = G @ M + mu[None, :]
+        return A
+    rng = np.random.default_rng(seed)
+    V, R = np.linalg.qr(rng.standard_normal((d, d)))
+    V *= np.sign(np.diag(R))[None, :]
+    s = _spectrum(cfgd["spectrum"], d)
+    Wt = (V * s[None, :]).T.copy()  # diag(s) V^T
+    chunk = 65536
+    starts = list(range(0, n, chunk))
+
+    def gauss(c, rows):
+        return np.random.default_rng([seed, 2, c]).standard_normal((rows, d))
+
+    S = np.zeros((d, d))
+    for c, r0 in enumerate(starts):
+        G = gauss(c, min(n, r0 + chunk) - r0)
+        S += G.T @ G
+    Rc = np.linalg.cholesky(S).T  # S = R^T R, R upper with positive diagonal
+    A = np.empty((n, d), dtype=np.float32)
+    for c, r0 in enumerate(starts):
+        r1 = min(n, r0 + chunk)
+        U = sla.solve_triangular(Rc, gauss(c, r1 - r0).T, trans="T", lower=False).T  # G R^-1
+        blk = U @ Wt
+        if cfgd["noise"]:
+            blk += cfgd["noise"] * np.random.default_rng([seed, 3, c]).standard_normal(blk.shape)
+        A[r0:r1] = blk
+    return A
+
+
+def run_reference(args):
+    """The reference arm: the oracle port of the reference algorithm on the
+    host cores, A generated on the host (numpy), Pi from the oracle's bitwise
+    restatement of the reference's SeededRng. No CUDA, no product code."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import paper_1504_05477_b200 as rk
-
-    dev = torch.device("cuda", 0)
+    o = _oracle()
     cfgd = CONFIGS[args.config]
-    cfg = rk.RsvdConfig(k=cfgd["k"], variant=cfgd["variant"], q=cfgd["q"], seed=0)
+    cfg = RefConfig(cfgd["k"], cfgd["variant"], cfgd["q"], seed=0)
     if cfgd.get("sparse"):
         print(json.dumps({"impl": "reference", "unavailable": "sparse configs: the reference arm is wired for dense "
-                          "configs only (C1/C2/C4)"}), flush=True)
+                          "configs only (C1/C2/C4/C5); C3's CPU baseline runs inside the measured arm"}), flush=True)
         return
-    A = make_matrix(cfgd, dev)
-    Pi = rk.gaussian(cfgd["d"], cfg.p, rk.SeededRng(cfg.seed)).data
-    A_host = A.cpu().numpy()
-    del A
+    t0 = time.perf_counter()
+    A_host = make_matrix_host(cfgd)
+    gen_s = time.perf_counter() - t0
+    Pi = o.gaussian(cfgd["d"], cfg.p, o.SeededRng(cfg.seed))
     vals = []
     # CPU runs have no warm-up state beyond the BLAS pool (primed inside
     # reference_sample); warm-up steps are still executed, at most 1 of them
@@ -812,7 +980,10 @@ def run_reference(args):
            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": workload_config(args.config, cfgd, cfg, world),
            "cpu_baseline": {"value": v, "unit": "ms", "cores": r["cores"], "kind": r["kind"], "sample": r["sample"]},
-           "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "input_generation_s": gen_s,
+           "note": "A generated on the host with numpy (same construction and spectrum as the measured arm, "
+                   "different draw); no CUDA and no product code on this path"}
     print(json.dumps(out), flush=True)
 
 
@@ -826,6 +997,12 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fp64", action="store_true", help="skip the FP64 parity-mode leg on FP32 configs")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the 3xTF32 fp32-mode leg on FP32 configs")
+    ap.add_argument("--no-spectral", action="store_true", help="skip the spectral-error parity")
+    ap.add_argument("--spectral-iters", type=int, default=20000,
+                    help="power iterations per start of the spectral-error estimator (reference: 20000)")
+    ap.add_argument("--precision", default=None, choices=["exact", "fp32", "fp64"],
+                    help="override the config's precision mode")
     ap.add_argument("--no-c4gemm", action="store_true", help="skip the tensor-bound C4 chain-GEMM leg of the C2 line")
     ap.add_argument("--no-spmm", action="store_true", help="skip the C3 SpMM measurement on dense configs")
     ap.add_argument("--count-launches", action="store_true", default=True)
@@ -835,6 +1012,26 @@ def main():
                     help="bracket one eager factorization with cudaProfilerStart/Stop (for ncu "
                          "--profile-from-start off) after the warm-up, then exit")
     args = ap.parse_args()
+    world_env = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and world_env is None:
+        # one process per GPU: relaunch under torch.distributed.run (the driver
+        # launches the N > 1 runs this way itself)
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # keep stdout to the one JSON line
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd, env=env))
+    if world_env is not None and int(world_env) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}")
+    if world_env is not None and int(world_env) > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -96,20 +96,20 @@ int rsvd_gemm_tn(int dtype, int out_dtype, int64_t m, int64_t n, int64_t k, doub
  * matrix.py:80) at FP64-class accuracy (~1e-16 relative) from kind::i8
  * tcgen05 MMAs with exact int32 sums.
  * rsvd_oz_prepare cuts A (n x d FP32, row pitch lda) ONCE into
- *   rsvd_oz_num_planes() signed 7-bit digit planes planes[i][r][c] (row pitch
- *   ldq = rsvd_oz_planes_ld(d) bytes, plane pitch n*ldq) and per-row
- *   exponents row_exp[n]; the caller owns both buffers.
+ *   rsvd_oz_num_planes() signed 7-bit digit planes (column-blocked layout
+ *   planes[i][c / 32][r][c % 32], rsvd_oz_planes_bytes(n, d) bytes in all)
+ *   and per-row exponents row_exp[n]; the caller owns both buffers.
  * rsvd_oz_gemm trans = 0: C (n x p) = alpha A X + beta C  (X d x p FP64)
  *              trans = 1: C (d x p) = alpha A^T Y + beta C (Y n x p FP64)
  *   C is FP64; workspace from rsvd_oz_gemm_ws_bytes(trans, n, d, p). */
-int64_t rsvd_oz_planes_ld(int64_t d);
+int64_t rsvd_oz_planes_bytes(int64_t n, int64_t d);
 int rsvd_oz_num_planes(void);
-int rsvd_oz_prepare(int64_t n, int64_t d, const float *A, int64_t lda, int8_t *planes, int64_t ldq,
-                    int32_t *row_exp, void *stream);
+int rsvd_oz_prepare(int64_t n, int64_t d, const float *A, int64_t lda, int8_t *planes, int32_t *row_exp,
+                    void *stream);
 int64_t rsvd_oz_gemm_ws_bytes(int trans, int64_t n, int64_t d, int64_t p);
 int rsvd_oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t *planes,
-                 int64_t ldq, const int32_t *row_exp, const double *B, int64_t ldb, double beta,
-                 double *C, int64_t ldc, void *ws, int64_t ws_bytes, const int32_t *pred, void *stream);
+                 const int32_t *row_exp, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
+                 void *ws, int64_t ws_bytes, const int32_t *pred, void *stream);
 
 /* ---- 3. Sparse products --------------------------------------------------
  * Replace spmm_nt (_kernels.pyx:74-92) and spmm_t (_kernels.pyx:95-113).

@@ -27,11 +27,11 @@ _SIGS = {
     "rsvd_gemm_tn_ws_bytes": ([_int, _i64, _i64, _i64, _int], _i64),
     "rsvd_gemm_tn": ([_int, _int, _i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64, _vp, _vp, _vp,
                       _i64, _int, _vp, _vp], _int),
-    "rsvd_oz_planes_ld": ([_i64], _i64),
+    "rsvd_oz_planes_bytes": ([_i64, _i64], _i64),
     "rsvd_oz_num_planes": ([], _int),
-    "rsvd_oz_prepare": ([_i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp], _int),
+    "rsvd_oz_prepare": ([_i64, _i64, _vp, _i64, _vp, _vp, _vp], _int),
     "rsvd_oz_gemm_ws_bytes": ([_int, _i64, _i64, _i64], _i64),
-    "rsvd_oz_gemm": ([_int, _i64, _i64, _i64, _dbl, _vp, _i64, _vp, _vp, _i64, _dbl, _vp, _i64, _vp, _i64, _vp, _vp],
+    "rsvd_oz_gemm": ([_int, _i64, _i64, _i64, _dbl, _vp, _vp, _vp, _i64, _dbl, _vp, _i64, _vp, _i64, _vp, _vp],
                      _int),
     "rsvd_spmm_csr": ([_int, _int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _i64, _vp], _int),
     "rsvd_spmm_csr_plan": ([_int, _int, _i64, _i64, _vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _i64, _i64, _vp, _vp, _vp,

@@ -101,16 +101,16 @@ int rsvd_gemm_nn(int dtype, int64_t m, int64_t n, int64_t k, double alpha, const
     return gemm_nn_simt(dtype, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, row_sub, pred, st);
 }
 
-int64_t rsvd_oz_planes_ld(int64_t d) { return d < 0 ? 0 : oz_planes_ld(d); }
+int64_t rsvd_oz_planes_bytes(int64_t n, int64_t d) { return (n < 0 || d < 0) ? 0 : oz_planes_bytes(n, d); }
 
 int rsvd_oz_num_planes(void) { return oz_num_planes(); }
 
-int rsvd_oz_prepare(int64_t n, int64_t d, const float* A, int64_t lda, int8_t* planes, int64_t ldq,
-                    int32_t* row_exp, void* stream) {
+int rsvd_oz_prepare(int64_t n, int64_t d, const float* A, int64_t lda, int8_t* planes, int32_t* row_exp,
+                    void* stream) {
     RSVD_REQUIRE(n >= 0 && d >= 0, "oz_prepare: negative dimension");
-    RSVD_REQUIRE(lda >= d && ldq >= oz_planes_ld(d), "oz_prepare: pitch too small");
+    RSVD_REQUIRE(lda >= d, "oz_prepare: leading dimension too small");
     RSVD_REQUIRE(n == 0 || (A && planes && row_exp), "oz_prepare: null pointer");
-    return oz_prepare(n, d, A, lda, planes, ldq, row_exp, as_stream(stream));
+    return oz_prepare(n, d, A, lda, planes, row_exp, as_stream(stream));
 }
 
 int64_t rsvd_oz_gemm_ws_bytes(int trans, int64_t n, int64_t d, int64_t p) {
@@ -118,13 +118,13 @@ int64_t rsvd_oz_gemm_ws_bytes(int trans, int64_t n, int64_t d, int64_t p) {
     return oz_gemm_ws_bytes(trans, n, d, p);
 }
 
-int rsvd_oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t* planes, int64_t ldq,
+int rsvd_oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t* planes,
                  const int32_t* row_exp, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
                  void* ws, int64_t ws_bytes, const int32_t* pred, void* stream) {
     RSVD_REQUIRE(trans == 0 || trans == 1, "oz_gemm: trans must be 0 or 1");
     RSVD_REQUIRE(n >= 0 && d >= 0 && p >= 0, "oz_gemm: negative dimension");
-    RSVD_REQUIRE(ldq >= oz_planes_ld(d) && ldb >= p && ldc >= p, "oz_gemm: leading dimension too small");
-    return oz_gemm(trans, n, d, p, alpha, planes, ldq, row_exp, B, ldb, beta, C, ldc, ws, ws_bytes, pred,
+    RSVD_REQUIRE(ldb >= p && ldc >= p, "oz_gemm: leading dimension too small");
+    return oz_gemm(trans, n, d, p, alpha, planes, row_exp, B, ldb, beta, C, ldc, ws, ws_bytes, pred,
                    as_stream(stream));
 }
 

@@ -54,12 +54,12 @@ int gemm_tn_skinny(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha,
                    const int32_t* pred, cudaStream_t st);
 
 // int8 Ozaki FP64-accurate products of an FP32 A (gemm_oz.cu).
-int64_t oz_planes_ld(int64_t d);
+int64_t oz_planes_bytes(int64_t n, int64_t d);
 int oz_num_planes();
-int oz_prepare(int64_t n, int64_t d, const float* A, int64_t lda, int8_t* planes, int64_t ldq, int32_t* row_exp,
+int oz_prepare(int64_t n, int64_t d, const float* A, int64_t lda, int8_t* planes, int32_t* row_exp,
                cudaStream_t st);
 int64_t oz_gemm_ws_bytes(int trans, int64_t n, int64_t d, int64_t p);
-int oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t* planes, int64_t ldq,
+int oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t* planes,
             const int32_t* row_exp, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* ws,
             int64_t ws_bytes, const int32_t* pred, cudaStream_t st);
 

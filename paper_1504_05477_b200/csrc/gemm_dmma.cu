@@ -350,8 +350,52 @@ int gemm_nn_dmma(int64_t m, int64_t n, int64_t k, double alpha, const double* A,
                                             row_sub, nullptr, pred);
 }
 
+// Outputs of at most 64 x 64 (Grams and small projections of an n x p block):
+// one 64 x 64 tile, the reduction spread over ~one wave of CTAs (>= 128 rows
+// each). The general path capped the split count at 64 CTAs for a single tile
+// (C2 Gram 50000 x 50: 97 us on 64 of 296 CTA slots).
+bool dmma_tn_small(int64_t n, int64_t k) { return k <= 64 && n <= 64; }
+
+int64_t dmma_tn_small_splits(int64_t m) {
+    const int64_t slots = (int64_t)sm_count() * kCtasPerSm;
+    int64_t s = cdiv(m, 128);
+    if (s > slots) s = slots;
+    if (s < 1) s = 1;
+    const int64_t rps = cdiv(cdiv(m, s), TN_BK) * TN_BK;
+    return cdiv(m, rps) < 1 ? 1 : cdiv(m, rps);
+}
+
+// Split-ordered sum of many partials (grouped: 32 outputs x 8 split groups
+// per CTA, group sums added in group order -- deterministic).
+template <typename TO>
+__global__ void __launch_bounds__(256)
+k_dmma_tn_reduce_g(int64_t k, int64_t n, int64_t splits, const double* __restrict__ ws, double alpha, double beta,
+                   TO* __restrict__ C, int64_t ldc, const double* __restrict__ mu, const double* __restrict__ cs,
+                   const int32_t* __restrict__ pred) {
+    if (pred_off(pred)) return;
+    __shared__ double part[8][33];
+    const int o = threadIdx.x % 32, g = threadIdx.x / 32;
+    const int64_t e = (int64_t)blockIdx.x * 32 + o;
+    const bool ok = e < k * n;
+    double v = 0.0;
+    if (ok)
+        for (int64_t s = g; s < splits; s += 8) v += ws[s * k * n + e];
+    part[g][o] = v;
+    __syncthreads();
+    if (g != 0 || !ok) return;
+    double t = part[0][o];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) t += part[i][o];
+    const int64_t r = e / n, c = e % n;
+    if (mu) t -= mu[r] * cs[c];
+    t *= alpha;
+    if (beta != 0.0) t += beta * (double)C[r * ldc + c];
+    C[r * ldc + c] = (TO)t;
+}
+
 int64_t gemm_tn_dmma_ws_bytes(int64_t m, int64_t n, int64_t k) {
-    return dmma_tn_splits(m, n, k) * k * n * (int64_t)sizeof(double);
+    const int64_t s = dmma_tn_small(n, k) ? dmma_tn_small_splits(m) : dmma_tn_splits(m, n, k);
+    return s * k * n * (int64_t)sizeof(double);
 }
 
 int gemm_tn_dmma(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
@@ -359,6 +403,24 @@ int gemm_tn_dmma(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, c
                  const double* mu, const double* cs, void* ws, int64_t ws_bytes, const int32_t* pred,
                  cudaStream_t st) {
     if (k == 0 || n == 0) return RSVD_OK;
+    if (dmma_tn_small(n, k)) {
+        const int64_t s = dmma_tn_small_splits(m);
+        RSVD_REQUIRE(ws_bytes >= s * k * n * (int64_t)sizeof(double), "gemm_tn(dmma): workspace too small");
+        const int64_t rps = cdiv(cdiv(m, s), TN_BK) * TN_BK;
+        dim3 grid(1, 1, (unsigned)s);
+        int rc = launch<true, 64, 64, TN_BK, 2>(vec_ok(A, lda, B, ldb), grid, st, k, n, m, A, lda, B, ldb, rps, 1.0,
+                                                0.0, nullptr, 0, nullptr, (double*)ws, pred);
+        if (rc != RSVD_OK) return rc;
+        const unsigned nb = (unsigned)cdiv(k * n, 32);
+        if (out_dtype == RSVD_F64)
+            k_dmma_tn_reduce_g<double><<<nb, 256, 0, st>>>(k, n, s, (const double*)ws, alpha, beta, (double*)C, ldc,
+                                                           mu, cs, pred);
+        else
+            k_dmma_tn_reduce_g<float><<<nb, 256, 0, st>>>(k, n, s, (const double*)ws, alpha, beta, (float*)C, ldc,
+                                                          mu, cs, pred);
+        RSVD_CHECK_LAUNCH();
+        return RSVD_OK;
+    }
     int64_t s = dmma_tn_splits(m, n, k);
     RSVD_REQUIRE(ws_bytes >= s * k * n * (int64_t)sizeof(double), "gemm_tn(dmma): workspace too small");
     int64_t rps = cdiv(cdiv(m, s), TN_BK) * TN_BK;

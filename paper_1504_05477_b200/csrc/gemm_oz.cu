@@ -9,15 +9,15 @@
 // decisions). 3xTF32 gives ~1e-7; FP64 DMMA gives 1e-16 at ~37 TFLOP/s.
 //
 // Scheme (per product D = A X, A FP32 n x d held in HBM as slices):
-//   * every row r of A is scaled by 2^-E_r (2^E_r > max_c |A[r,c]|) and cut
-//     into SA = 6 signed 7-bit digits: A[r,c] = 2^E_r sum_i a_i[r,c] 2^-7(i+1),
-//     a_i in [-127, 127] (truncation; exact for every entry >= 2^-18 of the row
-//     maximum since FP32 carries 24 bits, 2^-42 absolute below);
+//   * every row r of A is scaled by 2^-E_r (2^E_r > 2 max_c |A[r,c]|) and cut
+//     into SA = 6 balanced base-128 digits: A[r,c] = 2^E_r sum_i a_i[r,c]
+//     2^-7(i+1), a_i in [-64, 64] (round to nearest; exact for every entry >=
+//     2^-17 of the row maximum since FP32 carries 24 bits, 2^-43 below);
 //   * every column c of the FP64 operand X likewise into SB = 7 digits with
-//     its own exponent F_c (2^-49 relative to the column maximum);
+//     its own exponent F_c (2^-50 relative to the column maximum);
 //   * D = 2^(E_r + F_c - 14) sum_{i+j <= 6} 2^-7(i+j) (a_i x_j): 27 int8 GEMMs
-//     whose int32 sums are EXACT (|digit products| <= 127^2, at most 7 pairs
-//     per level, K <= 16384 per CTA keeps every level below 2^31); the levels
+//     whose int32 sums are EXACT (|digit products| <= 2^12, at most 6 pairs
+//     per level, K <= 65536 per CTA keeps every level below 2^31); the levels
 //     are combined in FP64 in the epilogue. Neglected terms are ~2^-56 of
 //     |A||X| per entry: FP64-class accuracy (tests: ~1e-16 vs cuBLAS DGEMM).
 //   * A^T Y uses the same row-scaled slices: A^T Y = sum_r (2^-E_r A[r,:])^T
@@ -31,6 +31,7 @@
 #include <cuda.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "gemm.cuh"
 #include "umma.cuh"
@@ -46,9 +47,9 @@ constexpr int OZ_SB = 7;         // B digit planes
 constexpr int OZ_L = 6;          // kept levels i + j <= OZ_L
 constexpr int OZ_LEVELS = OZ_L + 1;
 constexpr int OZ_STAGES = 5;
-constexpr int64_t OZ_MAX_K = 16384;  // int32 exactness bound per CTA
+constexpr int64_t OZ_MAX_K = 65536;  // int32 exactness: 6 pairs x 64^2 x 65536 < 2^31
 constexpr int OZ_THREADS = 6 * 32;   // 0 TMA, 1 MMA, 2..5 epilogue
-constexpr uint32_t kLayoutSW32 = 6;
+constexpr uint32_t kLayoutNone = 0;
 
 template <int BN>
 struct OzCfg {
@@ -63,6 +64,11 @@ struct OzCfg {
 
 struct OzParams {
     int64_t M, N, K;         // D[M x N] = Aop[M x K] Bop[K x N]
+    int64_t Np;              // rows per B digit plane
+    const int8_t* a_planes;  // [SA][a_cols / 16][a_rows][16 B]
+    int64_t a_rows;          // padded rows of A (multiple of 128)
+    int64_t a_pitch;         // bytes per A plane
+    const int8_t* b_planes;  // [K / 32][2][SB][Np][16 B]
     int64_t k_per_split;     // multiple of OZ_KS
     const int32_t* ea;       // per-M exponent (NN: A row exponents), nullptr for TN
     const int32_t* fb;       // per-N exponent of B's columns
@@ -74,6 +80,7 @@ struct OzParams {
     int64_t ldw;
     const int32_t* pred;
     int n_tiles;
+    int ablate;              // profiling ablations (RSVD_OZ_ABLATE): 1 no B loads, 2 no A loads, 4 no MMAs
 };
 
 // kind::i8 instruction descriptor: S32 accumulate, signed int8 A / B.
@@ -133,8 +140,8 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         mbar_init(acc_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+        if (A_MN) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        if (p.Np != BN) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -147,24 +154,42 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer: SA A planes + SB B planes per K step
+        if (lane == 0) {  // ---------------- producer: 1-D bulk copies of contiguous runs
+            // A planes [i][c / 16][r][16 B] (rows / columns zero-padded to multiples of
+            // 128): NN tile = 2 runs of 128 rows x 16 B; TN tile = 8 runs of 32 rows x 16 B.
+            // B planes [kb][half][j][c][16 B]: one run per (half, digit), or the whole
+            // stage when a single N tile spans all Np rows.
             int s = 0;
             uint32_t ph = 0;
             for (int kb = 0; kb < nks; ++kb) {
                 mbar_wait(&empty[s], ph ^ 1);
-                const int kk = (int)(kbeg + (int64_t)kb * OZ_KS);
+                const int64_t kk = kbeg + (int64_t)kb * OZ_KS;
                 uint8_t* st = smem + s * Cfg::STAGE;
-                mbar_expect_tx(&full[s], Cfg::STAGE);
+                mbar_expect_tx(&full[s], Cfg::STAGE - ((p.ablate & 1) ? OZ_SB * Cfg::B_TILE : 0) -
+                                             ((p.ablate & 2) ? OZ_SA * Cfg::A_TILE : 0));
+                if (!(p.ablate & 2)) {
 #pragma unroll
-                for (int i = 0; i < OZ_SA; ++i) {
-                    if (!A_MN)
-                        tma_load_3d(&tmA, &full[s], st + i * Cfg::A_TILE, kk, (int)m0, i);
-                    else
-                        tma_load_3d(&tmA, &full[s], st + i * Cfg::A_TILE, (int)m0, kk, i);
+                    for (int i = 0; i < OZ_SA; ++i) {
+                        const int8_t* pl = p.a_planes + (int64_t)i * p.a_pitch;
+                        uint8_t* dst = st + i * Cfg::A_TILE;
+                        if (!A_MN) {
+#pragma unroll
+                            for (int h = 0; h < 2; ++h)
+                                bulk_g2s(dst + h * 2048, pl + ((kk / 16 + h) * p.a_rows + m0) * 16, 2048, &full[s]);
+                        } else {
+                            // 8 column blocks x 512 B: one TMA box (rows of 512 B, as uint32)
+                            tma_load_3d(&tmA, &full[s], dst, (int)(kk * 4), (int)(m0 / 16), i);
+                        }
+                    }
                 }
-#pragma unroll
-                for (int j = 0; j < OZ_SB; ++j)
-                    tma_load_3d(&tmB, &full[s], st + OZ_SA * Cfg::A_TILE + j * Cfg::B_TILE, kk, (int)n0, j);
+                if (!(p.ablate & 1)) {
+                    uint8_t* dst = st + OZ_SA * Cfg::A_TILE;
+                    if (p.Np == BN)  // the whole stage is one contiguous run
+                        bulk_g2s(dst, p.b_planes + (kk / OZ_KS) * 2 * OZ_SB * p.Np * 16, OZ_SB * Cfg::B_TILE,
+                                 &full[s]);
+                    else  // 14 runs of BN x 16 B: one TMA box
+                        tma_load_3d(&tmB, &full[s], dst, (int)(n0 * 4), 0, (int)(kk / OZ_KS));
+                }
                 if (++s == OZ_STAGES) { s = 0; ph ^= 1; }
             }
         }
@@ -179,10 +204,11 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 const uint32_t bst = st + OZ_SA * Cfg::A_TILE;
 #pragma unroll
                 for (int i = 0; i < OZ_SA; ++i) {
-                    // K-major A: 128 rows x 32 B, SWIZZLE_32B (8-row groups, SBO 256 B);
-                    // MN-major A: 32 K rows x 128 B, SWIZZLE_128B (8-row groups, SBO 1024 B)
-                    const uint64_t da = A_MN ? make_desc(st + i * Cfg::A_TILE, 4096, 1024, kLayoutSW128)
-                                             : make_desc(st + i * Cfg::A_TILE, 16, 256, kLayoutSW32);
+                    // no-swizzle core matrices (8 rows x 16 B, 128 contiguous bytes):
+                    // K-major A [half][r][16 B]: 8-row groups SBO 128 B, K halves LBO 2 KB;
+                    // MN-major A [mb][k][16 B]: 16-column blocks SBO 512 B, 8-row K groups LBO 128 B
+                    const uint64_t da = A_MN ? make_desc(st + i * Cfg::A_TILE, 128, 512, kLayoutNone)
+                                             : make_desc(st + i * Cfg::A_TILE, 2048, 128, kLayoutNone);
                     constexpr int kMaxJ = OZ_SB;
                     const int nj = (OZ_L - i + 1) < kMaxJ ? (OZ_L - i + 1) : kMaxJ;
                     const int rows = nj * BN;
@@ -190,8 +216,10 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     for (int r0 = 0; r0 < OZ_SB * BN; r0 += 256) {
                         if (r0 >= rows) break;
                         const int nn = (rows - r0) < 256 ? (rows - r0) : 256;
-                        const uint64_t db = make_desc(bst + r0 * OZ_KS, 16, 256, kLayoutSW32);
+                        // B [half][j][c][16 B]: rows j BN + c, 8-row groups SBO 128 B, halves LBO
+                        const uint64_t db = make_desc(bst + r0 * 16, OZ_SB * BN * 16, 128, kLayoutNone);
                         const uint32_t acc = (kb == 0 && i == 0) ? 0u : 1u;
+                        if (p.ablate & 4) continue;
                         tc_mma_i8(tmem_base + (uint32_t)(i * BN + r0), da, db, oz_idesc(OZ_BM, nn, A_MN ? 1 : 0), acc);
                     }
                 }
@@ -260,77 +288,87 @@ __device__ __forceinline__ int exp_above(double m) {
     return e;
 }
 
-__device__ __forceinline__ float block_max(float v) {
-    __shared__ float red[32];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    const int w = threadIdx.x / 32, l = threadIdx.x % 32;
-    if (l == 0) red[w] = v;
-    __syncthreads();
-    if (w == 0) {
-        v = l < (int)(blockDim.x / 32) ? red[l] : 0.f;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-        if (l == 0) red[0] = v;
-    }
-    __syncthreads();
-    v = red[0];
-    __syncthreads();
-    return v;
-}
-
-// digit i of u in (-1, 1): t = 128 u; a_i = trunc(t); t = 128 (t - a_i). Exact in FP32 for FP32 input
-// (t keeps <= 24 significant bits; removing the integer part and scaling by 2^7 are exact).
+// Balanced base-128 digits of u in (-1/2, 1/2): t = 128 u; a_i = rint(t) in [-64, 64];
+// t = 128 (t - a_i). Exact in FP32 for FP32 input (t keeps <= 24 significant bits;
+// removing the nearest integer and scaling by 2^7 are exact). Round-to-nearest
+// digits leave zero-mean remainders (truncation would bias every dropped term
+// towards the sign of the product) and keep |a_i x_j| <= 2^12.
 __device__ __forceinline__ uint32_t pack4(const int (&q)[4]) {
     return (uint32_t)(q[0] & 0xFF) | ((uint32_t)(q[1] & 0xFF) << 8) | ((uint32_t)(q[2] & 0xFF) << 16) |
            ((uint32_t)(q[3] & 0xFF) << 24);
 }
 
-// One CTA per row of A: row maximum, exponent, then the SA digit planes.
-// planes[i][r][c], row pitch ldq bytes (multiple of 16), plane pitch n ldq.
+// Digit planes of A in the column-blocked layout planes[i][c / 16][r][c % 16]
+// over n_pad x d_pad (both multiples of 128; padding written as zeros): a
+// 16-byte row piece is one row of a tensor-core core matrix in either
+// orientation. One CTA per 32 rows: warps find the row maxima (4 rows each),
+// then lane l owns row r0 + l and each warp walks 16-column blocks, so a warp
+// writes one contiguous 512-byte run per digit plane and block.
 __global__ void __launch_bounds__(256) k_oz_slice_a(int64_t n, int64_t d, const float* __restrict__ A, int64_t lda,
-                                                    int8_t* __restrict__ planes, int64_t ldq,
+                                                    int64_t n_pad, int64_t d_pad, int8_t* __restrict__ planes,
                                                     int32_t* __restrict__ row_exp) {
-    const int64_t r = blockIdx.x;
-    if (r >= n) return;
-    const float* a = A + r * lda;
+    __shared__ float s_scale[32];
+    const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+    const int64_t r0 = (int64_t)blockIdx.x * 32;
     const bool vec = (lda % 4 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
-    float m = 0.f;
-    const int64_t d4 = vec ? d / 4 : 0;
-    for (int64_t c = threadIdx.x; c < d4; c += blockDim.x) {
-        const float4 v = reinterpret_cast<const float4*>(a)[c];
-        m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    for (int rr = warp; rr < 32; rr += 8) {
+        const int64_t r = r0 + rr;
+        float m = 0.f;
+        if (r < n) {
+            const float* a = A + r * lda;
+            const int64_t d4 = vec ? d / 4 : 0;
+            for (int64_t c = lane; c < d4; c += 32) {
+                const float4 v = reinterpret_cast<const float4*>(a)[c];
+                m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+            }
+            for (int64_t c = d4 * 4 + lane; c < d; c += 32) m = fmaxf(m, fabsf(a[c]));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        // one spare bit: |u| < 1/2, so every balanced digit rint(.) is in [-64, 64]
+        const int E = m > 0.f ? exp_above((double)m) + 1 : 0;
+        if (lane == 0) {
+            if (r < n) row_exp[r] = E;
+            s_scale[rr] = ldexpf(1.0f, -E);
+        }
     }
-    for (int64_t c = d4 * 4 + threadIdx.x; c < d; c += blockDim.x) m = fmaxf(m, fabsf(a[c]));
-    m = block_max(m);
-    const int E = m > 0.f ? exp_above((double)m) : 0;
-    if (threadIdx.x == 0) row_exp[r] = E;
-    const float sc = ldexpf(1.0f, -E);
-    const int64_t pp = n * ldq;
-    int8_t* out = planes + r * ldq;
-    const int64_t dq = (d + 3) / 4;  // groups of 4 columns (the last one zero padded up to ldq)
-    for (int64_t g = threadIdx.x; g < dq; g += blockDim.x) {
-        float x[4];
-        if (vec && g < d4) {
-            const float4 v = reinterpret_cast<const float4*>(a)[g];
-            x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+    __syncthreads();
+    const int64_t r = r0 + lane;
+    const bool live = r < n;
+    const float sc = s_scale[lane] * 128.0f;
+    const float* a = A + (live ? r : 0) * lda;
+    const int64_t pp = n_pad * d_pad;  // plane pitch
+    const bool vrow = vec && live;
+    for (int64_t b = warp; b < d_pad / 16; b += 8) {
+        float x[16];
+        if (vrow && b * 16 + 16 <= d) {
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+                const float4 v = reinterpret_cast<const float4*>(a + b * 16)[q4];
+                x[4 * q4] = v.x; x[4 * q4 + 1] = v.y; x[4 * q4 + 2] = v.z; x[4 * q4 + 3] = v.w;
+            }
         } else {
 #pragma unroll
-            for (int t = 0; t < 4; ++t) x[t] = (g * 4 + t < d) ? a[g * 4 + t] : 0.f;
+            for (int t = 0; t < 16; ++t) x[t] = (live && b * 16 + t < d) ? a[b * 16 + t] : 0.f;
         }
-        float t4[4];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) t4[t] = x[t] * sc * 128.0f;
+        for (int t = 0; t < 16; ++t) x[t] *= sc;
+        int8_t* out = planes + (b * n_pad + r) * 16;
 #pragma unroll
         for (int i = 0; i < OZ_SA; ++i) {
-            int q[4];
+            uint32_t w[4];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const float tr = truncf(t4[t]);
-                q[t] = (int)tr;
-                t4[t] = (t4[t] - tr) * 128.0f;
+            for (int q4 = 0; q4 < 4; ++q4) {
+                int q[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float tr = rintf(x[4 * q4 + t]);
+                    q[t] = (int)tr;
+                    x[4 * q4 + t] = (x[4 * q4 + t] - tr) * 128.0f;
+                }
+                w[q4] = pack4(q);
             }
-            *reinterpret_cast<uint32_t*>(out + i * pp + g * 4) = pack4(q);
+            *reinterpret_cast<uint4*>(out + i * pp) = make_uint4(w[0], w[1], w[2], w[3]);
         }
     }
 }
@@ -365,11 +403,13 @@ __global__ void k_oz_col_exp(int64_t N, const unsigned long long* __restrict__ c
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= N) return;
     const double m = __longlong_as_double((long long)colmax[c]);
-    fb[c] = m > 0.0 ? exp_above(m) : 0;
+    fb[c] = m > 0.0 ? exp_above(m) + 1 : 0;  // |u| < 1/2: balanced digits in [-64, 64]
 }
 
-// Pass 2: transposed digit planes planes[j][c][k] (K-major rows of Kp bytes,
-// rows c in [N, Np) written as zeros), through a 32 (k) x 32 (c) smem tile.
+// Pass 2: transposed digit planes in the k-blocked layout
+// planes[k / 32][(k / 16) % 2][j][c][k % 16] (one K = 32 MMA step of all digits
+// is one contiguous run; rows c in [N, Np) and k >= K written as zeros),
+// through a 32 (k) x 32 (c) smem tile.
 __global__ void __launch_bounds__(256) k_oz_slice_b(int64_t K, int64_t N, const double* __restrict__ B, int64_t ldb,
                                                     const int32_t* __restrict__ ek, const int32_t* __restrict__ fb,
                                                     int64_t Np, int64_t Kp, int8_t* __restrict__ planes) {
@@ -392,7 +432,7 @@ __global__ void __launch_bounds__(256) k_oz_slice_b(int64_t K, int64_t N, const 
         double x = u * 128.0;
 #pragma unroll
         for (int j = 0; j < OZ_SB; ++j) {
-            const double tr = trunc(x);
+            const double tr = rint(x);
             q[j][t] = (int)tr;
             x = (x - tr) * 128.0;
         }
@@ -405,8 +445,9 @@ __global__ void __launch_bounds__(256) k_oz_slice_b(int64_t K, int64_t N, const 
         const int w = e % 8, cc = (e / 8) % 32, j = e / 256;
         const int64_t c = c0 + cc;
         const int64_t k = k0 + 4 * w;
-        if (c < Np && k < Kp)
-            *reinterpret_cast<uint32_t*>(planes + ((int64_t)j * Np + c) * Kp + k) = tile[j][cc][w];
+        if (c < Np)
+            *reinterpret_cast<uint32_t*>(planes + ((((k0 / 32) * 2 + w / 4) * OZ_SB + j) * Np + c) * 16 + 4 * (w % 4)) =
+                tile[j][cc][w];
     }
 }
 
@@ -425,29 +466,32 @@ __global__ void k_oz_reduce(int64_t M, int64_t N, int64_t ldw, int64_t splits, c
 }
 
 // ---------------------------------------------------------------- host
-int oz_map_a(CUtensorMap* map, const int8_t* planes, int64_t n, int64_t d, int64_t ldq, bool mn_major) {
+// u32 views of the digit planes (16-byte row pieces as 4 elements): box rows
+// of 512 B / BN x 16 B, no swizzle (the interleaved core-matrix layout is the
+// gmem layout itself).
+int oz_map_a_tn(CUtensorMap* map, const int8_t* planes, int64_t a_rows, int64_t d_pad, int64_t pitch) {
     EncodeTiledFn fn = encode_fn();
     RSVD_REQUIRE(fn != nullptr, "cuTensorMapEncodeTiled unavailable");
-    cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)n, (cuuint64_t)OZ_SA};
-    cuuint64_t strides[2] = {(cuuint64_t)ldq, (cuuint64_t)(n * ldq)};
-    cuuint32_t box[3] = {mn_major ? 128u : (cuuint32_t)OZ_KS, mn_major ? (cuuint32_t)OZ_KS : 128u, 1};
+    cuuint64_t dims[3] = {(cuuint64_t)(a_rows * 4), (cuuint64_t)(d_pad / 16), (cuuint64_t)OZ_SA};
+    cuuint64_t strides[2] = {(cuuint64_t)(a_rows * 16), (cuuint64_t)pitch};
+    cuuint32_t box[3] = {(cuuint32_t)(OZ_KS * 4), 8, 1};
     cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(planes), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, mn_major ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<int8_t*>(planes), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     RSVD_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (Ozaki A planes) failed (%d)", (int)r);
     return RSVD_OK;
 }
 
-int oz_map_b(CUtensorMap* map, const int8_t* planes, int64_t K, int64_t Np, int64_t Kp, int bn) {
+int oz_map_b(CUtensorMap* map, const int8_t* planes, int64_t Np, int64_t nkb, int bn) {
     EncodeTiledFn fn = encode_fn();
     RSVD_REQUIRE(fn != nullptr, "cuTensorMapEncodeTiled unavailable");
-    cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)Np, (cuuint64_t)OZ_SB};
-    cuuint64_t strides[2] = {(cuuint64_t)Kp, (cuuint64_t)(Np * Kp)};
-    cuuint32_t box[3] = {(cuuint32_t)OZ_KS, (cuuint32_t)bn, 1};
+    cuuint64_t dims[3] = {(cuuint64_t)(Np * 4), (cuuint64_t)(2 * OZ_SB), (cuuint64_t)nkb};
+    cuuint64_t strides[2] = {(cuuint64_t)(Np * 16), (cuuint64_t)(2 * OZ_SB * Np * 16)};
+    cuuint32_t box[3] = {(cuuint32_t)(bn * 4), (cuuint32_t)(2 * OZ_SB), 1};
     cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(planes), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<int8_t*>(planes), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     RSVD_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (Ozaki B planes) failed (%d)", (int)r);
     return RSVD_OK;
@@ -488,7 +532,7 @@ OzLayout oz_layout(bool trans, int64_t n, int64_t d, int64_t p) {
     L.bn = oz_bn(p);
     const int64_t Mop = trans ? d : n, Kop = trans ? n : d;
     L.Np = cdiv(p, L.bn) * L.bn;
-    L.Kp = cdiv(Kop, 16) * 16;
+    L.Kp = cdiv(Kop, 32) * 32;
     L.n_tiles = cdiv(p, L.bn);
     L.m_tiles = cdiv(Mop, OZ_BM);
     L.splits = oz_splits(L.m_tiles * L.n_tiles, Kop);
@@ -523,13 +567,14 @@ int launch_oz(const CUtensorMap& tA, const CUtensorMap& tB, const OzParams& p, d
 
 }  // namespace
 
-int64_t oz_planes_ld(int64_t d) { return cdiv(d, 16) * 16; }
+int64_t oz_planes_bytes(int64_t n, int64_t d) { return (int64_t)OZ_SA * cdiv(n, 128) * 128 * cdiv(d, 128) * 128; }
 int oz_num_planes() { return OZ_SA; }
 
-int oz_prepare(int64_t n, int64_t d, const float* A, int64_t lda, int8_t* planes, int64_t ldq, int32_t* row_exp,
+int oz_prepare(int64_t n, int64_t d, const float* A, int64_t lda, int8_t* planes, int32_t* row_exp,
                cudaStream_t st) {
     if (n == 0) return RSVD_OK;
-    k_oz_slice_a<<<(unsigned)n, 256, 0, st>>>(n, d, A, lda, planes, ldq, row_exp);
+    const int64_t n_pad = cdiv(n, 128) * 128, d_pad = cdiv(d, 128) * 128;
+    k_oz_slice_a<<<(unsigned)(n_pad / 32), 256, 0, st>>>(n, d, A, lda, n_pad, d_pad, planes, row_exp);
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }
@@ -540,15 +585,14 @@ int64_t oz_gemm_ws_bytes(int trans, int64_t n, int64_t d, int64_t p) {
 
 // trans = 0: C (n x p) = alpha A X + beta C, X d x p.
 // trans = 1: C (d x p) = alpha A^T Y + beta C, Y n x p.
-int oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t* planes, int64_t ldq,
+int oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t* planes,
             const int32_t* row_exp, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* ws,
             int64_t ws_bytes, const int32_t* pred, cudaStream_t st) {
     const bool tr = trans != 0;
     const OzLayout L = oz_layout(tr, n, d, p);
     RSVD_REQUIRE(ws_bytes >= L.total, "oz_gemm: workspace too small (%lld < %lld)", (long long)ws_bytes,
                  (long long)L.total);
-    RSVD_REQUIRE((reinterpret_cast<uintptr_t>(planes) & 15) == 0 && ldq % 16 == 0,
-                 "oz_gemm: digit planes must be 16-byte aligned with a 16-byte-multiple pitch");
+    RSVD_REQUIRE((reinterpret_cast<uintptr_t>(planes) & 15) == 0, "oz_gemm: digit planes must be 16-byte aligned");
     const int64_t Mop = tr ? d : n, Kop = tr ? n : d;
     if (Mop == 0 || p == 0) return RSVD_OK;
     uint8_t* w = reinterpret_cast<uint8_t*>(ws);
@@ -567,13 +611,22 @@ int oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8
         k_oz_slice_b<<<g2, 256, 0, st>>>(Kop, p, B, ldb, ek, fb, L.Np, L.Kp, bpl);
         RSVD_CHECK_LAUNCH();
     }
-    CUtensorMap tA, tB;
-    int rc = oz_map_a(&tA, planes, n, d, ldq, tr);
-    if (rc) return rc;
-    rc = oz_map_b(&tB, bpl, Kop, L.Np, L.Kp, L.bn);
-    if (rc) return rc;
+    int rc = RSVD_OK;
     OzParams prm{};
-    prm.M = Mop; prm.N = p; prm.K = Kop;
+    prm.a_planes = planes;
+    prm.a_rows = cdiv(n, 128) * 128;
+    prm.a_pitch = prm.a_rows * cdiv(d, 128) * 128;
+    prm.b_planes = bpl;
+    CUtensorMap tA{}, tB{};
+    if (tr) {
+        rc = oz_map_a_tn(&tA, planes, prm.a_rows, cdiv(d, 128) * 128, prm.a_pitch);
+        if (rc) return rc;
+    }
+    if (L.Np != L.bn) {
+        rc = oz_map_b(&tB, bpl, L.Np, L.Kp / 32, L.bn);
+        if (rc) return rc;
+    }
+    prm.M = Mop; prm.N = p; prm.K = Kop; prm.Np = L.Np;
     prm.k_per_split = cdiv(cdiv(Kop, L.splits), OZ_KS) * OZ_KS;
     prm.ea = tr ? nullptr : row_exp;
     prm.fb = fb;
@@ -582,6 +635,10 @@ int oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8
     prm.ws = part; prm.ldw = p;
     prm.pred = pred;
     prm.n_tiles = (int)L.n_tiles;
+    {
+        static const char* ab = getenv("RSVD_OZ_ABLATE");
+        prm.ablate = ab ? atoi(ab) : 0;
+    }
     dim3 grid((unsigned)(L.m_tiles * L.n_tiles), 1, (unsigned)L.splits);
     if (L.bn == 32)
         rc = tr ? launch_oz<32, true>(tA, tB, prm, grid, st) : launch_oz<32, false>(tA, tB, prm, grid, st);

@@ -149,15 +149,14 @@ class OzPlanes:
         n, d = A.shape
         L = lib()
         self.n, self.d = n, d
-        self.ldq = int(L.rsvd_oz_planes_ld(d))
-        self.planes = torch.empty((int(L.rsvd_oz_num_planes()), n, self.ldq), dtype=torch.int8, device=A.device)
+        self.planes = torch.empty(int(L.rsvd_oz_planes_bytes(n, d)), dtype=torch.int8, device=A.device)
         self.row_exp = torch.empty(n, dtype=torch.int32, device=A.device)
         self.refresh(A)
 
     def refresh(self, A):
         """Re-cut the planes from A (same shape), stream-ordered."""
-        check(lib().rsvd_oz_prepare(self.n, self.d, _ptr(A), _ld(A), _ptr(self.planes), self.ldq,
-                                    _ptr(self.row_exp), _stream()), "oz_prepare")
+        check(lib().rsvd_oz_prepare(self.n, self.d, _ptr(A), _ld(A), _ptr(self.planes), _ptr(self.row_exp),
+                                    _stream()), "oz_prepare")
         return self
 
 
@@ -170,7 +169,7 @@ def oz_gemm(P, B, C, trans, alpha=1.0, beta=0.0, pred=None):
     L = lib()
     nbytes = L.rsvd_oz_gemm_ws_bytes(int(trans), P.n, P.d, p)
     ws = WS.get(nbytes, B.device)
-    check(L.rsvd_oz_gemm(int(trans), P.n, P.d, p, float(alpha), _ptr(P.planes), P.ldq, _ptr(P.row_exp),
+    check(L.rsvd_oz_gemm(int(trans), P.n, P.d, p, float(alpha), _ptr(P.planes), _ptr(P.row_exp),
                          _ptr(B), _ld(B), float(beta), _ptr(C), _ld(C), _ptr(ws), ws.numel(), _ptr(pred),
                          _stream()), "oz_gemm")
     return C

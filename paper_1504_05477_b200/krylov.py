@@ -208,7 +208,8 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
         Vw = rows_buffer(V.shape[0], V.shape[1], V.dtype, V.device)
         ops.convert(V, Vw)
         orth_block(ops, comm, Vw, tmp, ws, Qp=Qp, ref2=ref2, running=running, n_total=n_total,
-                   row_offset=row_offset, tau=tau, deflation_count=deflation_count, two_round=two_round)
+                   row_offset=row_offset, tau=tau, deflation_count=deflation_count, two_round=two_round,
+                   pass1_coef=pass1_coef)
         return ops.convert(Vw, V)
     dtype = V.dtype
     p = V.shape[1]

@@ -513,7 +513,7 @@ def _run(A, cfg, expected, precision="auto", center=False, device=None, comm=Non
                 buf.zero_()
             op = DenseDeviceOp(buf, center=center, exact=key[-1] == "exact")
             pi_host = gaussian(shape[1], cfg.p, SeededRng(cfg.seed)).data
-            pi_dev = torch.from_numpy(np.array(pi_host, copy=True)).to(device=dev, dtype=dt)
+            pi_dev = torch.from_numpy(np.array(pi_host, copy=True)).to(device=dev, dtype=op.dtype)
             entry = [buf, op, GraphedFactorization(op, cfg), pi_dev, 0]
         _GRAPH_CACHE[key] = entry
         buf, op, graphed, pi, calls = entry

@@ -50,15 +50,18 @@ for mode in ("eager", "graph"):
 sig = df.sigma.cpu().numpy(); Z = df.Z.clone()
 from torch.profiler import profile, ProfilerActivity
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
-    rsvd.run_device(op, cfg, Pi=Pi); torch.cuda.synchronize()
+    g.run(Pi); torch.cuda.synchronize()  # the graph replay (predicated-off sections skipped)
 agg = collections.defaultdict(lambda: [0.0, 0])
 for ev in prof.events():
     if ev.device_type == torch.autograd.DeviceType.CUDA:
         agg[ev.name][0] += ev.device_time_total / 1e3 if hasattr(ev, "device_time_total") else ev.cuda_time_total / 1e3
         agg[ev.name][1] += 1
+if os.environ.get("SHAPES"):
+    # per-call shapes of the DMMA products (eager run, record_shapes unavailable for ctypes: time by size)
+    pass
 tot = sum(v[0] for v in agg.values())
 print(f"total kernel time {tot:.1f} ms")
-for k, v in sorted(agg.items(), key=lambda x: -x[1][0])[:14]:
+for k, v in sorted(agg.items(), key=lambda x: -x[1][0])[:24]:
     print(f"  {v[0]:8.2f} ms {v[1]:5d}  {k[:90]}")
 if os.environ.get("NO_ORACLE"):
     sys.exit(0)
