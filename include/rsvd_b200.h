@@ -111,6 +111,27 @@ int rsvd_oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const
                  const int32_t *row_exp, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,
                  void *ws, int64_t ws_bytes, const int32_t *pred, void *stream);
 
+/* The same digit-plane products for an FP64 basis Q (n x w): _mgs's
+ * projections v <- v - Q_p (Q_p^T v) (factor.py:93-98) against the
+ * already-final prefix Q_p = Q[:, :jp]. rsvd_oz_basis_slice cuts columns
+ * [c0, c0 + ncols) of Q into rsvd_oz_basis_planes() digit planes with
+ * per-column exponents col_exp[c0 .. c0 + ncols) (planes of
+ * rsvd_oz_basis_bytes(n, w) bytes; workspace rsvd_oz_basis_ws_bytes(ncols)),
+ * one block at a time as blocks become final.
+ * rsvd_oz_gemm_planes is rsvd_oz_gemm on any digit planes (nplanes of them,
+ * allocated rows_alloc x cols_alloc, multiples of 128; exponents per row of
+ * the planes, or per column when col_scaled = 1) using their leading n x d
+ * corner: trans = 1 gives Q_p^T V (d = jp), trans = 0 gives Q_p C. */
+int rsvd_oz_basis_planes(void);
+int64_t rsvd_oz_basis_bytes(int64_t n, int64_t w);
+int64_t rsvd_oz_basis_ws_bytes(int64_t ncols);
+int rsvd_oz_basis_slice(int64_t n, int64_t w, const double *Q, int64_t ldq, int64_t c0, int64_t ncols,
+                        int8_t *planes, int32_t *col_exp, void *ws, int64_t ws_bytes, void *stream);
+int rsvd_oz_gemm_planes(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t *planes, int nplanes,
+                        int64_t rows_alloc, int64_t cols_alloc, const int32_t *exps, int col_scaled, const double *B,
+                        int64_t ldb, double beta, double *C, int64_t ldc, void *ws, int64_t ws_bytes,
+                        const int32_t *pred, void *stream);
+
 /* ---- 3. Sparse products --------------------------------------------------
  * Replace spmm_nt (_kernels.pyx:74-92) and spmm_t (_kernels.pyx:95-113).
  * C[nrows x nb] = alpha * A . B + beta * C for CSR A (nrows x ncols).

@@ -33,6 +33,12 @@ _SIGS = {
     "rsvd_oz_gemm_ws_bytes": ([_int, _i64, _i64, _i64], _i64),
     "rsvd_oz_gemm": ([_int, _i64, _i64, _i64, _dbl, _vp, _vp, _vp, _i64, _dbl, _vp, _i64, _vp, _i64, _vp, _vp],
                      _int),
+    "rsvd_oz_basis_planes": ([], _int),
+    "rsvd_oz_basis_bytes": ([_i64, _i64], _i64),
+    "rsvd_oz_basis_ws_bytes": ([_i64], _i64),
+    "rsvd_oz_basis_slice": ([_i64, _i64, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _i64, _vp], _int),
+    "rsvd_oz_gemm_planes": ([_int, _i64, _i64, _i64, _dbl, _vp, _int, _i64, _i64, _vp, _int, _vp, _i64, _dbl, _vp,
+                             _i64, _vp, _i64, _vp, _vp], _int),
     "rsvd_spmm_csr": ([_int, _int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _i64, _vp], _int),
     "rsvd_spmm_csr_plan": ([_int, _int, _i64, _i64, _vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _i64, _i64, _vp, _vp, _vp,
                             _vp, _i64, _vp, _vp, _vp, _i64, _vp], _int),

@@ -128,6 +128,30 @@ int rsvd_oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const
                    as_stream(stream));
 }
 
+int rsvd_oz_basis_planes(void) { return oz_basis_planes(); }
+
+int64_t rsvd_oz_basis_bytes(int64_t n, int64_t w) { return (n < 0 || w < 0) ? 0 : oz_basis_bytes(n, w); }
+
+int64_t rsvd_oz_basis_ws_bytes(int64_t ncols) { return ncols < 0 ? 0 : oz_basis_ws_bytes(ncols); }
+
+int rsvd_oz_basis_slice(int64_t n, int64_t w, const double* Q, int64_t ldq, int64_t c0, int64_t ncols,
+                        int8_t* planes, int32_t* col_exp, void* ws, int64_t ws_bytes, void* stream) {
+    RSVD_REQUIRE(n >= 0 && w >= 0 && ldq >= w, "oz_basis_slice: bad shape");
+    RSVD_REQUIRE(n == 0 || (Q && planes && col_exp), "oz_basis_slice: null pointer");
+    return oz_basis_slice(n, w, Q, ldq, c0, ncols, planes, col_exp, ws, ws_bytes, as_stream(stream));
+}
+
+int rsvd_oz_gemm_planes(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t* planes, int nplanes,
+                        int64_t rows_alloc, int64_t cols_alloc, const int32_t* exps, int col_scaled, const double* B,
+                        int64_t ldb, double beta, double* C, int64_t ldc, void* ws, int64_t ws_bytes,
+                        const int32_t* pred, void* stream) {
+    RSVD_REQUIRE(trans == 0 || trans == 1, "oz_gemm: trans must be 0 or 1");
+    RSVD_REQUIRE(n >= 0 && d >= 0 && p >= 0, "oz_gemm: negative dimension");
+    RSVD_REQUIRE(ldb >= p && ldc >= p, "oz_gemm: leading dimension too small");
+    return oz_gemm_planes(trans, n, d, p, alpha, planes, nplanes, rows_alloc, cols_alloc, exps, col_scaled, B, ldb,
+                          beta, C, ldc, ws, ws_bytes, pred, as_stream(stream));
+}
+
 int64_t rsvd_gemm_tn_ws_bytes(int dtype, int64_t m, int64_t n, int64_t k, int algo) {
     int64_t a = gemm_tn_simt_ws_bytes(m, n, k);
     if (dtype == RSVD_F64 && algo != RSVD_GEMM_SIMT) {

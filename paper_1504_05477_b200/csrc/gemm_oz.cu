@@ -42,22 +42,26 @@ namespace {
 
 constexpr int OZ_BM = 128;
 constexpr int OZ_KS = 32;        // int8 K per MMA = bytes per smem tile row
-constexpr int OZ_SA = 6;         // A digit planes
-constexpr int OZ_SB = 7;         // B digit planes
-constexpr int OZ_L = 6;          // kept levels i + j <= OZ_L
-constexpr int OZ_LEVELS = OZ_L + 1;
+constexpr int OZ_SA = 6;         // digit planes of an FP32 A (24-bit mantissas)
+constexpr int OZ_SQ = 7;         // digit planes of an FP64 orthonormal basis (global scale 2^1)
+constexpr int OZ_LV_A = 7;       // A products: kept levels i + j <= 6, 7 B digits
+constexpr int OZ_LV_Q = 8;       // basis products: levels i + j <= 7, 8 B digits (512 TMEM columns at BN 64)
+constexpr int OZ_SB_MAX = 8;
 constexpr int OZ_STAGES = 5;
 constexpr int64_t OZ_MAX_K = 65536;  // int32 exactness: 6 pairs x 64^2 x 65536 < 2^31
 constexpr int OZ_THREADS = 6 * 32;   // 0 TMA, 1 MMA, 2..5 epilogue
 constexpr uint32_t kLayoutNone = 0;
 
-template <int BN>
+// SA digit planes of the A operand, LV kept levels i + j < LV, as many B digits
+template <int BN, int SA, int LV>
 struct OzCfg {
+    static constexpr int SB = LV;
     static constexpr int A_TILE = OZ_BM * OZ_KS;            // 4 KB per digit plane
     static constexpr int B_TILE = BN * OZ_KS;               // per digit plane
-    static constexpr int STAGE = OZ_SA * A_TILE + OZ_SB * B_TILE;
+    static constexpr int STAGE = SA * A_TILE + SB * B_TILE;
     static constexpr int SMEM = OZ_STAGES * STAGE + 1024 + 256;
-    static constexpr int ACC_COLS = OZ_LEVELS * BN;
+    static constexpr int ACC_COLS = LV * BN;
+    static_assert(SMEM <= 227 * 1024, "stages do not fit shared memory");
     static_assert(ACC_COLS <= 512, "levels do not fit TMEM");
     static_assert(STAGE % 1024 == 0, "stage must keep 1024-byte swizzle alignment");
 };
@@ -113,11 +117,12 @@ __device__ __forceinline__ void tmem_ld16_s32(uint32_t taddr, int32_t* v) {
     for (int i = 0; i < 16; ++i) v[i] = (int32_t)r[i];
 }
 
-template <int BN, bool A_MN>
+template <int BN, bool A_MN, int SA, int LV>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
 k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, OzParams p) {
     if (pred_off(p.pred)) return;
-    using Cfg = OzCfg<BN>;
+    using Cfg = OzCfg<BN, SA, LV>;
+    constexpr int SB = Cfg::SB;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OZ_STAGES * Cfg::STAGE);
@@ -165,11 +170,11 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 mbar_wait(&empty[s], ph ^ 1);
                 const int64_t kk = kbeg + (int64_t)kb * OZ_KS;
                 uint8_t* st = smem + s * Cfg::STAGE;
-                mbar_expect_tx(&full[s], Cfg::STAGE - ((p.ablate & 1) ? OZ_SB * Cfg::B_TILE : 0) -
-                                             ((p.ablate & 2) ? OZ_SA * Cfg::A_TILE : 0));
+                mbar_expect_tx(&full[s], Cfg::STAGE - ((p.ablate & 1) ? SB * Cfg::B_TILE : 0) -
+                                             ((p.ablate & 2) ? SA * Cfg::A_TILE : 0));
                 if (!(p.ablate & 2)) {
 #pragma unroll
-                    for (int i = 0; i < OZ_SA; ++i) {
+                    for (int i = 0; i < SA; ++i) {
                         const int8_t* pl = p.a_planes + (int64_t)i * p.a_pitch;
                         uint8_t* dst = st + i * Cfg::A_TILE;
                         if (!A_MN) {
@@ -183,9 +188,9 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     }
                 }
                 if (!(p.ablate & 1)) {
-                    uint8_t* dst = st + OZ_SA * Cfg::A_TILE;
+                    uint8_t* dst = st + SA * Cfg::A_TILE;
                     if (p.Np == BN)  // the whole stage is one contiguous run
-                        bulk_g2s(dst, p.b_planes + (kk / OZ_KS) * 2 * OZ_SB * p.Np * 16, OZ_SB * Cfg::B_TILE,
+                        bulk_g2s(dst, p.b_planes + (kk / OZ_KS) * 2 * SB * p.Np * 16, SB * Cfg::B_TILE,
                                  &full[s]);
                     else  // 14 runs of BN x 16 B: one TMA box
                         tma_load_3d(&tmB, &full[s], dst, (int)(n0 * 4), 0, (int)(kk / OZ_KS));
@@ -201,23 +206,22 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 mbar_wait(&full[s], ph);
                 tc_fence_after();
                 const uint32_t st = smem_u32(smem + s * Cfg::STAGE);
-                const uint32_t bst = st + OZ_SA * Cfg::A_TILE;
+                const uint32_t bst = st + SA * Cfg::A_TILE;
 #pragma unroll
-                for (int i = 0; i < OZ_SA; ++i) {
+                for (int i = 0; i < SA; ++i) {
                     // no-swizzle core matrices (8 rows x 16 B, 128 contiguous bytes):
                     // K-major A [half][r][16 B]: 8-row groups SBO 128 B, K halves LBO 2 KB;
                     // MN-major A [mb][k][16 B]: 16-column blocks SBO 512 B, 8-row K groups LBO 128 B
                     const uint64_t da = A_MN ? make_desc(st + i * Cfg::A_TILE, 128, 512, kLayoutNone)
                                              : make_desc(st + i * Cfg::A_TILE, 2048, 128, kLayoutNone);
-                    constexpr int kMaxJ = OZ_SB;
-                    const int nj = (OZ_L - i + 1) < kMaxJ ? (OZ_L - i + 1) : kMaxJ;
+                    const int nj = LV - i;  // B digits j with i + j < LV
                     const int rows = nj * BN;
 #pragma unroll
-                    for (int r0 = 0; r0 < OZ_SB * BN; r0 += 256) {
+                    for (int r0 = 0; r0 < SB * BN; r0 += 256) {
                         if (r0 >= rows) break;
                         const int nn = (rows - r0) < 256 ? (rows - r0) : 256;
                         // B [half][j][c][16 B]: rows j BN + c, 8-row groups SBO 128 B, halves LBO
-                        const uint64_t db = make_desc(bst + r0 * 16, OZ_SB * BN * 16, 128, kLayoutNone);
+                        const uint64_t db = make_desc(bst + r0 * 16, SB * BN * 16, 128, kLayoutNone);
                         const uint32_t acc = (kb == 0 && i == 0) ? 0u : 1u;
                         if (p.ablate & 4) continue;
                         tc_mma_i8(tmem_base + (uint32_t)(i * BN + r0), da, db, oz_idesc(OZ_BM, nn, A_MN ? 1 : 0), acc);
@@ -247,7 +251,7 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             if (nks > 0) {
                 // Horner from the smallest level: v = sum_L acc_L 2^-7L
 #pragma unroll
-                for (int L = OZ_L; L >= 0; --L) {
+                for (int L = LV - 1; L >= 0; --L) {
                     int32_t a[16];
                     tmem_ld16_s32(tmem_base + lane_off + (uint32_t)(L * BN + c0), a);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -256,17 +260,23 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 }
             }
             if (row < p.M) {
+                // all loads of the chunk before any store: a load after a store to
+                // the same array would otherwise wait for it (C is read and written)
+                double cin[16];
+#pragma unroll
+                for (int t = 0; t < 16; ++t) {
+                    const int64_t col = n0 + c0 + t;
+                    cin[t] = (p.direct && p.beta != 0.0 && col < p.N) ? p.C[row * p.ldc + col] : 0.0;
+                }
 #pragma unroll
                 for (int t = 0; t < 16; ++t) {
                     const int64_t col = n0 + c0 + t;
                     if (col < p.N) {
                         const double val = ldexp(v[t], ea + p.fb[col] - 14);
-                        if (p.direct) {
-                            double* c = p.C + row * p.ldc + col;
-                            *c = p.beta != 0.0 ? p.alpha * val + p.beta * *c : p.alpha * val;
-                        } else {
+                        if (p.direct)
+                            p.C[row * p.ldc + col] = p.beta != 0.0 ? p.alpha * val + p.beta * cin[t] : p.alpha * val;
+                        else
                             p.ws[((int64_t)blockIdx.z * p.M + row) * p.ldw + col] = val;
-                        }
                     }
                 }
             }
@@ -373,6 +383,46 @@ __global__ void __launch_bounds__(256) k_oz_slice_a(int64_t n, int64_t d, const 
     }
 }
 
+// Digit planes of columns [c0, c0 + ncols) of a basis Q (row pitch ldq), each
+// column with its own exponent col_exp[c] (2^E > 2 max_r |Q[r, c]|): thread =
+// one row of one 16-column block; bytes of columns outside the range are kept
+// (read-modify-write of the 16-byte row piece), rows >= n written as zeros.
+__global__ void __launch_bounds__(256) k_oz_slice_cols(int64_t n, const double* __restrict__ Q, int64_t ldq,
+                                                       int64_t c0, int64_t ncols, int64_t n_pad, int64_t w_pad,
+                                                       int8_t* __restrict__ planes, const int32_t* __restrict__ col_exp) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_pad) return;
+    const int64_t b = c0 / 16 + blockIdx.y;
+    const int64_t pp = n_pad * w_pad;
+    int q[OZ_SQ][16];
+    bool mine[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+        const int64_t c = b * 16 + t;
+        mine[t] = c >= c0 && c < c0 + ncols;
+        double x = (mine[t] && r < n) ? ldexp(Q[r * ldq + c], 7 - col_exp[c]) : 0.0;  // 128 u, u = q 2^-E
+#pragma unroll
+        for (int i = 0; i < OZ_SQ; ++i) {
+            const double tr = rint(x);
+            q[i][t] = (int)tr;
+            x = (x - tr) * 128.0;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < OZ_SQ; ++i) {
+        uint4* dst = reinterpret_cast<uint4*>(planes + i * pp + (b * n_pad + r) * 16);
+        uint4 old = *dst;
+        uint32_t wv[4] = {old.x, old.y, old.z, old.w};
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+            if (mine[t]) {
+                const int sh = (t % 4) * 8;
+                wv[t / 4] = (wv[t / 4] & ~(0xFFu << sh)) | ((uint32_t)(q[i][t] & 0xFF) << sh);
+            }
+        *dst = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    }
+}
+
 // B operand (K x N FP64, row pitch ldb), optional per-row exponent e_k folded
 // in (A^T Y: Y[k, :] 2^E_k). Pass 1: per-column max of |2^e_k B[k, c]| as
 // ordered bit patterns (atomicMax on the FP64 bits of a non-negative value).
@@ -410,16 +460,17 @@ __global__ void k_oz_col_exp(int64_t N, const unsigned long long* __restrict__ c
 // planes[k / 32][(k / 16) % 2][j][c][k % 16] (one K = 32 MMA step of all digits
 // is one contiguous run; rows c in [N, Np) and k >= K written as zeros),
 // through a 32 (k) x 32 (c) smem tile.
+template <int SB>
 __global__ void __launch_bounds__(256) k_oz_slice_b(int64_t K, int64_t N, const double* __restrict__ B, int64_t ldb,
                                                     const int32_t* __restrict__ ek, const int32_t* __restrict__ fb,
                                                     int64_t Np, int64_t Kp, int8_t* __restrict__ planes) {
-    __shared__ uint32_t tile[OZ_SB][32][9];  // [plane][c][k / 4] packed digits
+    __shared__ uint32_t tile[SB][32][9];  // [plane][c][k / 4] packed digits
     const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8
     const int64_t k0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
     // load: thread (tx = c, ty) handles rows k0 + 4 ty .. 4 ty + 3 of column c0 + tx
     const int64_t col = c0 + tx;
     const double sc = col < N ? ldexp(1.0, -fb[col]) : 0.0;
-    int q[OZ_SB][4];
+    int q[SB][4];
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
         const int64_t k = k0 + 4 * ty + t;
@@ -431,22 +482,22 @@ __global__ void __launch_bounds__(256) k_oz_slice_b(int64_t K, int64_t N, const 
         }
         double x = u * 128.0;
 #pragma unroll
-        for (int j = 0; j < OZ_SB; ++j) {
+        for (int j = 0; j < SB; ++j) {
             const double tr = rint(x);
             q[j][t] = (int)tr;
             x = (x - tr) * 128.0;
         }
     }
 #pragma unroll
-    for (int j = 0; j < OZ_SB; ++j) tile[j][tx][ty] = pack4(q[j]);
+    for (int j = 0; j < SB; ++j) tile[j][tx][ty] = pack4(q[j]);
     __syncthreads();
     // store: rows c = c0 + (warp), 8 words of 4 k each per (plane, row)
-    for (int e = threadIdx.x; e < OZ_SB * 32 * 8; e += blockDim.x) {
+    for (int e = threadIdx.x; e < SB * 32 * 8; e += blockDim.x) {
         const int w = e % 8, cc = (e / 8) % 32, j = e / 256;
         const int64_t c = c0 + cc;
         const int64_t k = k0 + 4 * w;
         if (c < Np)
-            *reinterpret_cast<uint32_t*>(planes + ((((k0 / 32) * 2 + w / 4) * OZ_SB + j) * Np + c) * 16 + 4 * (w % 4)) =
+            *reinterpret_cast<uint32_t*>(planes + ((((k0 / 32) * 2 + w / 4) * SB + j) * Np + c) * 16 + 4 * (w % 4)) =
                 tile[j][cc][w];
     }
 }
@@ -469,10 +520,10 @@ __global__ void k_oz_reduce(int64_t M, int64_t N, int64_t ldw, int64_t splits, c
 // u32 views of the digit planes (16-byte row pieces as 4 elements): box rows
 // of 512 B / BN x 16 B, no swizzle (the interleaved core-matrix layout is the
 // gmem layout itself).
-int oz_map_a_tn(CUtensorMap* map, const int8_t* planes, int64_t a_rows, int64_t d_pad, int64_t pitch) {
+int oz_map_a_tn(CUtensorMap* map, const int8_t* planes, int64_t a_rows, int64_t d_pad, int64_t pitch, int nplanes) {
     EncodeTiledFn fn = encode_fn();
     RSVD_REQUIRE(fn != nullptr, "cuTensorMapEncodeTiled unavailable");
-    cuuint64_t dims[3] = {(cuuint64_t)(a_rows * 4), (cuuint64_t)(d_pad / 16), (cuuint64_t)OZ_SA};
+    cuuint64_t dims[3] = {(cuuint64_t)(a_rows * 4), (cuuint64_t)(d_pad / 16), (cuuint64_t)nplanes};
     cuuint64_t strides[2] = {(cuuint64_t)(a_rows * 16), (cuuint64_t)pitch};
     cuuint32_t box[3] = {(cuuint32_t)(OZ_KS * 4), 8, 1};
     cuuint32_t estr[3] = {1, 1, 1};
@@ -483,12 +534,12 @@ int oz_map_a_tn(CUtensorMap* map, const int8_t* planes, int64_t a_rows, int64_t 
     return RSVD_OK;
 }
 
-int oz_map_b(CUtensorMap* map, const int8_t* planes, int64_t Np, int64_t nkb, int bn) {
+int oz_map_b(CUtensorMap* map, const int8_t* planes, int64_t Np, int64_t nkb, int bn, int sb) {
     EncodeTiledFn fn = encode_fn();
     RSVD_REQUIRE(fn != nullptr, "cuTensorMapEncodeTiled unavailable");
-    cuuint64_t dims[3] = {(cuuint64_t)(Np * 4), (cuuint64_t)(2 * OZ_SB), (cuuint64_t)nkb};
-    cuuint64_t strides[2] = {(cuuint64_t)(Np * 16), (cuuint64_t)(2 * OZ_SB * Np * 16)};
-    cuuint32_t box[3] = {(cuuint32_t)(bn * 4), (cuuint32_t)(2 * OZ_SB), 1};
+    cuuint64_t dims[3] = {(cuuint64_t)(Np * 4), (cuuint64_t)(2 * sb), (cuuint64_t)nkb};
+    cuuint64_t strides[2] = {(cuuint64_t)(Np * 16), (cuuint64_t)(2 * sb * Np * 16)};
+    cuuint32_t box[3] = {(cuuint32_t)(bn * 4), (cuuint32_t)(2 * sb), 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<int8_t*>(planes), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -500,11 +551,14 @@ int oz_map_b(CUtensorMap* map, const int8_t* planes, int64_t Np, int64_t nkb, in
 int oz_bn(int64_t n) { return n <= 32 ? 32 : 64; }
 
 // split count: K per CTA <= OZ_MAX_K (exactness), then the smallest count
-// whose CTAs fill the SMs in waves >= 90% full (at most 64, >= 4 K steps each)
+// whose CTAs fill the SMs in waves >= 90% full (at most 64, >= 16 K steps
+// each: a split's FP64 partials cost a write + read of the output, which a
+// short reduction -- a projection against a 50..550-column prefix -- does
+// not pay back)
 int64_t oz_splits(int64_t tiles, int64_t K) {
     const int64_t min_s = cdiv(K, OZ_MAX_K);
     const int64_t G = sm_count();
-    int64_t max_s = cdiv(K, 4 * OZ_KS);
+    int64_t max_s = cdiv(K, 16 * OZ_KS);
     if (max_s > 64) max_s = 64;
     if (max_s < min_s) max_s = min_s;
     int64_t best = min_s;
@@ -542,7 +596,7 @@ OzLayout oz_layout(bool trans, int64_t n, int64_t d, int64_t p) {
         off += cdiv(bytes, 256) * 256;
         return o;
     };
-    L.planes_off = take((int64_t)OZ_SB * L.Np * L.Kp);
+    L.planes_off = take((int64_t)OZ_SB_MAX * L.Np * L.Kp);
     L.colmax_off = take(p * 8);
     L.fb_off = take(p * 4);
     L.part_off = take(L.splits > 1 ? L.splits * Mop * p * 8 : 0);
@@ -550,17 +604,17 @@ OzLayout oz_layout(bool trans, int64_t n, int64_t d, int64_t p) {
     return L;
 }
 
-template <int BN, bool A_MN>
+template <int BN, bool A_MN, int SA, int LV>
 int launch_oz(const CUtensorMap& tA, const CUtensorMap& tB, const OzParams& p, dim3 grid, cudaStream_t st) {
-    using Cfg = OzCfg<BN>;
+    using Cfg = OzCfg<BN, SA, LV>;
     static PerDevice<bool> attr_dev;
     bool& attr = attr_dev.get();
     if (!attr) {
-        RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_oz_gemm<BN, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             Cfg::SMEM));
+        RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_oz_gemm<BN, A_MN, SA, LV>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
         attr = true;
     }
-    k_oz_gemm<BN, A_MN><<<grid, OZ_THREADS, Cfg::SMEM, st>>>(tA, tB, p);
+    k_oz_gemm<BN, A_MN, SA, LV><<<grid, OZ_THREADS, Cfg::SMEM, st>>>(tA, tB, p);
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }
@@ -585,10 +639,20 @@ int64_t oz_gemm_ws_bytes(int trans, int64_t n, int64_t d, int64_t p) {
 
 // trans = 0: C (n x p) = alpha A X + beta C, X d x p.
 // trans = 1: C (d x p) = alpha A^T Y + beta C, Y n x p.
-int oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t* planes,
-            const int32_t* row_exp, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* ws,
-            int64_t ws_bytes, const int32_t* pred, cudaStream_t st) {
+// A is given by `nplanes` digit planes [i][c / 16][r][16 B] allocated for
+// rows_alloc x cols_alloc (multiples of 128) and per-row exponents; the
+// product uses its leading n x d corner (an orthonormal basis' prefix).
+int oz_gemm_planes(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t* planes, int nplanes,
+                   int64_t rows_alloc, int64_t cols_alloc, const int32_t* exps, int col_scaled, const double* B,
+                   int64_t ldb, double beta, double* C, int64_t ldc, void* ws, int64_t ws_bytes, const int32_t* pred,
+                   cudaStream_t st) {
     const bool tr = trans != 0;
+    // exponents of the contraction index are folded into B before slicing it;
+    // exponents of the output-row index scale the epilogue
+    const bool fold = tr != (col_scaled != 0);
+    RSVD_REQUIRE(nplanes == OZ_SA || nplanes == OZ_SQ, "oz_gemm: %d digit planes not supported", nplanes);
+    RSVD_REQUIRE(rows_alloc % 128 == 0 && cols_alloc % 128 == 0 && rows_alloc >= n && cols_alloc >= d,
+                 "oz_gemm: plane geometry does not cover the product");
     const OzLayout L = oz_layout(tr, n, d, p);
     RSVD_REQUIRE(ws_bytes >= L.total, "oz_gemm: workspace too small (%lld < %lld)", (long long)ws_bytes,
                  (long long)L.total);
@@ -600,35 +664,38 @@ int oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8
     unsigned long long* cmax = reinterpret_cast<unsigned long long*>(w + L.colmax_off);
     int32_t* fb = reinterpret_cast<int32_t*>(w + L.fb_off);
     double* part = reinterpret_cast<double*>(w + L.part_off);
-    // B digit planes (row exponents of A folded in for A^T Y)
-    const int32_t* ek = tr ? row_exp : nullptr;
+    const int32_t* ek = fold ? exps : nullptr;
     RSVD_CHECK_CUDA(cudaMemsetAsync(cmax, 0, p * 8, st));
     {
         dim3 g((unsigned)std::min<int64_t>(cdiv(Kop, 8), 2 * sm_count()), (unsigned)cdiv(p, 32));
         k_oz_colmax_b<<<g, 256, 0, st>>>(Kop, p, B, ldb, ek, cmax);
         k_oz_col_exp<<<(unsigned)cdiv(p, 128), 128, 0, st>>>(p, cmax, fb);
         dim3 g2((unsigned)cdiv(L.Kp, 32), (unsigned)cdiv(L.Np, 32));
-        k_oz_slice_b<<<g2, 256, 0, st>>>(Kop, p, B, ldb, ek, fb, L.Np, L.Kp, bpl);
+        if (nplanes == OZ_SA)
+            k_oz_slice_b<OZ_LV_A><<<g2, 256, 0, st>>>(Kop, p, B, ldb, ek, fb, L.Np, L.Kp, bpl);
+        else
+            k_oz_slice_b<OZ_LV_Q><<<g2, 256, 0, st>>>(Kop, p, B, ldb, ek, fb, L.Np, L.Kp, bpl);
         RSVD_CHECK_LAUNCH();
     }
+    const int sb = nplanes == OZ_SA ? OZ_LV_A : OZ_LV_Q;
     int rc = RSVD_OK;
     OzParams prm{};
     prm.a_planes = planes;
-    prm.a_rows = cdiv(n, 128) * 128;
-    prm.a_pitch = prm.a_rows * cdiv(d, 128) * 128;
+    prm.a_rows = rows_alloc;
+    prm.a_pitch = rows_alloc * cols_alloc;
     prm.b_planes = bpl;
     CUtensorMap tA{}, tB{};
     if (tr) {
-        rc = oz_map_a_tn(&tA, planes, prm.a_rows, cdiv(d, 128) * 128, prm.a_pitch);
+        rc = oz_map_a_tn(&tA, planes, rows_alloc, cols_alloc, prm.a_pitch, nplanes);
         if (rc) return rc;
     }
     if (L.Np != L.bn) {
-        rc = oz_map_b(&tB, bpl, L.Np, L.Kp / 32, L.bn);
+        rc = oz_map_b(&tB, bpl, L.Np, L.Kp / 32, L.bn, sb);
         if (rc) return rc;
     }
     prm.M = Mop; prm.N = p; prm.K = Kop; prm.Np = L.Np;
     prm.k_per_split = cdiv(cdiv(Kop, L.splits), OZ_KS) * OZ_KS;
-    prm.ea = tr ? nullptr : row_exp;
+    prm.ea = fold ? nullptr : exps;
     prm.fb = fb;
     prm.direct = L.splits == 1;
     prm.C = C; prm.ldc = ldc; prm.alpha = alpha; prm.beta = beta;
@@ -640,16 +707,62 @@ int oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8
         prm.ablate = ab ? atoi(ab) : 0;
     }
     dim3 grid((unsigned)(L.m_tiles * L.n_tiles), 1, (unsigned)L.splits);
-    if (L.bn == 32)
-        rc = tr ? launch_oz<32, true>(tA, tB, prm, grid, st) : launch_oz<32, false>(tA, tB, prm, grid, st);
-    else
-        rc = tr ? launch_oz<64, true>(tA, tB, prm, grid, st) : launch_oz<64, false>(tA, tB, prm, grid, st);
+    if (nplanes == OZ_SA) {
+        if (L.bn == 32)
+            rc = tr ? launch_oz<32, true, OZ_SA, OZ_LV_A>(tA, tB, prm, grid, st)
+                    : launch_oz<32, false, OZ_SA, OZ_LV_A>(tA, tB, prm, grid, st);
+        else
+            rc = tr ? launch_oz<64, true, OZ_SA, OZ_LV_A>(tA, tB, prm, grid, st)
+                    : launch_oz<64, false, OZ_SA, OZ_LV_A>(tA, tB, prm, grid, st);
+    } else {
+        if (L.bn == 32)
+            rc = tr ? launch_oz<32, true, OZ_SQ, OZ_LV_Q>(tA, tB, prm, grid, st)
+                    : launch_oz<32, false, OZ_SQ, OZ_LV_Q>(tA, tB, prm, grid, st);
+        else
+            rc = tr ? launch_oz<64, true, OZ_SQ, OZ_LV_Q>(tA, tB, prm, grid, st)
+                    : launch_oz<64, false, OZ_SQ, OZ_LV_Q>(tA, tB, prm, grid, st);
+    }
     if (rc) return rc;
     if (L.splits > 1) {
         const int64_t tot = Mop * p;
         k_oz_reduce<<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(Mop, p, p, L.splits, part, alpha, beta, C, ldc, pred);
         RSVD_CHECK_LAUNCH();
     }
+    return RSVD_OK;
+}
+
+int oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t* planes,
+            const int32_t* row_exp, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* ws,
+            int64_t ws_bytes, const int32_t* pred, cudaStream_t st) {
+    return oz_gemm_planes(trans, n, d, p, alpha, planes, OZ_SA, cdiv(n, 128) * 128, cdiv(d, 128) * 128, row_exp, 0,
+                          B, ldb, beta, C, ldc, ws, ws_bytes, pred, st);
+}
+
+// ---- FP64 basis (n x w): OZ_SQ digit planes with per-COLUMN exponents
+// (col_exp[w]), filled one block of columns at a time as the blocks become
+// final. Column scaling makes both products exact-scaled: Q_p^T V scales its
+// output rows by col_exp, Q_p C folds col_exp into C's rows (the contraction
+// index), mirroring the row-scaled A planes.
+int oz_basis_planes() { return OZ_SQ; }
+int64_t oz_basis_bytes(int64_t n, int64_t w) { return (int64_t)OZ_SQ * cdiv(n, 128) * 128 * cdiv(w, 128) * 128; }
+
+int64_t oz_basis_ws_bytes(int64_t ncols) { return ncols * 8 + 256; }
+
+int oz_basis_slice(int64_t n, int64_t w, const double* Q, int64_t ldq, int64_t c0, int64_t ncols, int8_t* planes,
+                   int32_t* col_exp, void* ws, int64_t ws_bytes, cudaStream_t st) {
+    RSVD_REQUIRE(c0 >= 0 && ncols >= 0 && c0 + ncols <= w, "oz_basis_slice: column range outside the basis");
+    RSVD_REQUIRE(ws_bytes >= oz_basis_ws_bytes(ncols), "oz_basis_slice: workspace too small");
+    if (n == 0 || ncols == 0) return RSVD_OK;
+    const int64_t n_pad = cdiv(n, 128) * 128, w_pad = cdiv(w, 128) * 128;
+    unsigned long long* cmax = reinterpret_cast<unsigned long long*>(ws);
+    RSVD_CHECK_CUDA(cudaMemsetAsync(cmax, 0, ncols * 8, st));
+    dim3 g0((unsigned)std::min<int64_t>(cdiv(n, 8), 2 * sm_count()), (unsigned)cdiv(ncols, 32));
+    k_oz_colmax_b<<<g0, 256, 0, st>>>(n, ncols, Q + c0, ldq, nullptr, cmax);
+    k_oz_col_exp<<<(unsigned)cdiv(ncols, 128), 128, 0, st>>>(ncols, cmax, col_exp + c0);
+    const int64_t b0 = c0 / 16, b1 = cdiv(c0 + ncols, 16);
+    dim3 g((unsigned)cdiv(n_pad, 256), (unsigned)(b1 - b0));
+    k_oz_slice_cols<<<g, 256, 0, st>>>(n, Q, ldq, c0, ncols, n_pad, w_pad, planes, col_exp);
+    RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }
 

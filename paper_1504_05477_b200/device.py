@@ -175,6 +175,42 @@ def oz_gemm(P, B, C, trans, alpha=1.0, beta=0.0, pred=None):
     return C
 
 
+class OzBasis:
+    """Digit planes of an orthonormal FP64 basis Q (n x w) for FP64-accurate
+    int8 tensor-core projections against its final prefix Q[:, :jp]
+    (csrc/gemm_oz.cu). Blocks are sliced in as they become final."""
+
+    def __init__(self, n, w, device):
+        L = lib()
+        self.n, self.w = n, w
+        self.rows_alloc = -(-n // 128) * 128
+        self.cols_alloc = -(-w // 128) * 128
+        self.nplanes = int(L.rsvd_oz_basis_planes())
+        self.planes = torch.zeros(int(L.rsvd_oz_basis_bytes(n, w)), dtype=torch.int8, device=device)
+        self.col_exp = torch.zeros(w, dtype=torch.int32, device=device)
+
+    def slice(self, Q, c0, ncols):
+        """Digit planes of Q[:, c0:c0 + ncols] (Q = the full n x w basis)."""
+        assert Q.dtype == torch.float64 and Q.shape == (self.n, self.w)
+        L = lib()
+        ws = WS.get(L.rsvd_oz_basis_ws_bytes(int(ncols)), Q.device)
+        check(L.rsvd_oz_basis_slice(self.n, self.w, _ptr(Q), _ld(Q), int(c0), int(ncols), _ptr(self.planes),
+                                    _ptr(self.col_exp), _ptr(ws), ws.numel(), _stream()), "oz_basis_slice")
+
+    def gemm(self, trans, jp, B, C, alpha=1.0, beta=0.0, pred=None):
+        """trans=1: C (jp x p) = alpha Q_p^T B + beta C (B n x p);
+        trans=0: C (n x p) = alpha Q_p B + beta C (B jp x p); Q_p = Q[:, :jp]."""
+        p = B.shape[1]
+        L = lib()
+        nbytes = L.rsvd_oz_gemm_ws_bytes(int(trans), self.n, int(jp), p)
+        ws = WS.get(nbytes, B.device)
+        check(L.rsvd_oz_gemm_planes(int(trans), self.n, int(jp), p, float(alpha), _ptr(self.planes), self.nplanes,
+                                    self.rows_alloc, self.cols_alloc, _ptr(self.col_exp), 1, _ptr(B), _ld(B),
+                                    float(beta), _ptr(C), _ld(C), _ptr(ws), ws.numel(), _ptr(pred), _stream()),
+              "oz_gemm_planes")
+        return C
+
+
 def gram(V, out=None, algo=GEMM_AUTO, pred=None):
     """FP64 Gram V^T V."""
     p = V.shape[1]

@@ -147,9 +147,18 @@ def _cast_small(ops, T64, dtype, out=None, pred=None):
     return ops.convert(T64, out, pred=pred)
 
 
-def project_out(ops, comm, Qp, V, tmp_c, pred=None):
-    """V <- V - Qp (Qp^T V)  (one block classical Gram-Schmidt pass)."""
+def project_out(ops, comm, Qp, V, tmp_c, pred=None, basis=None):
+    """V <- V - Qp (Qp^T V)  (one block classical Gram-Schmidt pass).
+    ``basis`` (exact mode): the digit planes of the basis Qp is the prefix of
+    (device.OzBasis) -- both products run as FP64-accurate int8 tensor-core
+    GEMMs instead of FP64 DMMA."""
     if Qp is None or Qp.shape[1] == 0:
+        return V
+    if basis is not None:
+        jp = Qp.shape[1]
+        basis.gemm(1, jp, V, tmp_c, pred=pred)
+        comm.allreduce(tmp_c)
+        basis.gemm(0, jp, tmp_c, V, alpha=-1.0, beta=1.0, pred=pred)
         return V
     ops.gemm_tn(Qp, V, tmp_c, pred=pred)
     comm.allreduce(tmp_c)
@@ -178,6 +187,9 @@ Z_REORTH_TOL = 1e-13
 # Projected block-Krylov basis: first projection's coefficients formed in
 # d-space from W = A^T Q (RSVD_DSPACE_PASS1=0: from Q^T V, A/B).
 D_SPACE_PASS1 = os.environ.get("RSVD_DSPACE_PASS1", "1") != "0"
+# Exact mode: projections against the final prefix on its int8 digit planes
+# (RSVD_OZ_PROJ=0: FP64 DMMA, for A/B measurement).
+OZ_PROJECTIONS = os.environ.get("RSVD_OZ_PROJ", "1") != "0"
 
 
 def proj_passes(dtype):
@@ -187,7 +199,7 @@ def proj_passes(dtype):
 
 
 def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=None, row_offset=0,
-               tau=None, deflation_count=None, two_round=None, pass1_coef=None):
+               tau=None, deflation_count=None, two_round=None, pass1_coef=None, basis=None):
     """Orthonormalize the n x p block V in place (span-preserving, column
     order preserving), against the orthonormal columns Qp when given.
 
@@ -209,7 +221,7 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
         ops.convert(V, Vw)
         orth_block(ops, comm, Vw, tmp, ws, Qp=Qp, ref2=ref2, running=running, n_total=n_total,
                    row_offset=row_offset, tau=tau, deflation_count=deflation_count, two_round=two_round,
-                   pass1_coef=pass1_coef)
+                   pass1_coef=pass1_coef, basis=basis)
         return ops.convert(Vw, V)
     dtype = V.dtype
     p = V.shape[1]
@@ -228,7 +240,7 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
             ops.gemm_nn(Qp, pass1_coef, V, alpha=-1.0, beta=1.0)
             npass -= 1
         for _ in range(npass):
-            project_out(ops, comm, Qp, V, tmp_c)
+            project_out(ops, comm, Qp, V, tmp_c, basis=basis)
     G = ws.G[:p, :p]
     T = ws.T[:p, :p]
     mask = ws.mask[:p]
@@ -259,10 +271,10 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
             ops.convert(tmp, Q1, pred=r1)
             ops.mask_cols(V, mask, pred=r1)  # keep only the rejected columns' residuals
             if has_prev:
-                project_out(ops, comm, Qp, V, tmp_c, pred=r1)
+                project_out(ops, comm, Qp, V, tmp_c, pred=r1, basis=basis)
             project_out(ops, comm, Q1, V, c2, pred=r1)
             if has_prev:
-                project_out(ops, comm, Qp, V, tmp_c, pred=r1)
+                project_out(ops, comm, Qp, V, tmp_c, pred=r1, basis=basis)
             project_out(ops, comm, Q1, V, c2, pred=r1)
             ops.gram(V, G, pred=r1)
             comm.allreduce(G)
@@ -289,7 +301,7 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
     ops.colreduce(out, True, ref_f)
     comm.allreduce(ref_f)
     if has_prev:
-        project_out(ops, comm, Qp, out, tmp_c)
+        project_out(ops, comm, Qp, out, tmp_c, basis=basis)
     ops.gram(out, G)
     comm.allreduce(G)
     r3 = ws.ndef_r3
@@ -300,8 +312,8 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
     with ops.cond_section(r3, use_cond):
         ops.insert_fill(V, ws.mask2[:p], r3, QR_FILL_SEED, row_offset, n_total, pred=r3)
         if has_prev:
-            project_out(ops, comm, Qp, V, tmp_c, pred=r3)
-            project_out(ops, comm, Qp, V, tmp_c, pred=r3)
+            project_out(ops, comm, Qp, V, tmp_c, pred=r3, basis=basis)
+            project_out(ops, comm, Qp, V, tmp_c, pred=r3, basis=basis)
         ops.gram(V, G, pred=r3)
         comm.allreduce(G)
         ops.chol_deflate(G, None, 0.0, T, ws.mask2[:p], ws.ndef2, None, pred=r3)
@@ -419,13 +431,19 @@ def bk_basis(ops, comm, op, Pi, q, ws, n_total, row_offset):
         orth_block(ops, comm, cur, tmp, ws, running=running, n_total=n_total, row_offset=row_offset)
     # final orthonormalization of hstack(blocks): one _mgs call -> one fill stream
     running.zero_()
+    # exact mode (FP32 A, FP64 blocks): the projections against the final
+    # prefix run on its int8 digit planes, each block sliced in once final
+    basis = ops.OzBasis(n, n_blocks * p, dev) if (getattr(op, "oz", None) is not None and
+                                                  dt == torch.float64 and OZ_PROJECTIONS) else None
     for j in range(n_blocks):
         cur = K[:, j * p: (j + 1) * p]
         ref2 = ws.ref2[:p]
         ops.colreduce(cur, True, ref2)
         comm.allreduce(ref2)
         orth_block(ops, comm, cur, tmp, ws, Qp=K[:, : j * p] if j else None, ref2=ref2, running=running,
-                   n_total=n_total, row_offset=row_offset, deflation_count=deflated)
+                   n_total=n_total, row_offset=row_offset, deflation_count=deflated, basis=basis)
+        if basis is not None and j + 1 < n_blocks:
+            basis.slice(K, j * p, p)
     return BasisResult(K, n_blocks - 1, deflated)
 
 

@@ -129,3 +129,32 @@ def test_oz_zero_rows_and_columns():
     torch.cuda.synchronize()
     assert bool((C[17] == 0).all()) and bool((C[:, 3] == 0).all())
     assert _normwise(C, A.double() @ X, A.double(), X) < TOL_DGEMM
+
+
+@pytest.mark.parametrize("jp", [50, 200, 550])
+def test_oz_basis_projections(jp):
+    """Digit planes of an orthonormal FP64 basis, sliced one block at a time
+    (column offsets not aligned to the 16-column storage blocks): Q_p^T V and
+    V - Q_p C against cuBLAS FP64, normwise (|q| <= 1, ||q_c|| = 1)."""
+    ops = _ops()
+    n, w, p = 30000, 600, 50
+    g = torch.Generator(device="cuda").manual_seed(jp)
+    Q, _ = torch.linalg.qr(torch.randn((n, w), generator=g, device="cuda", dtype=torch.float64))
+    Q = Q.contiguous()
+    B = ops.OzBasis(n, w, Q.device)
+    for c0 in range(0, w, p):
+        B.slice(Q, c0, p)
+    V = torch.randn((n, p), generator=g, device="cuda", dtype=torch.float64)
+    C = torch.empty((jp, p), dtype=torch.float64, device="cuda")
+    B.gemm(1, jp, V, C)
+    Qp = Q[:, :jp]
+    ref = Qp.T @ V
+    torch.cuda.synchronize()
+    e_tn = float(((C - ref).abs() / V.norm(dim=0).view(1, -1)).max())
+    V2 = V.clone()
+    B.gemm(0, jp, C, V2, alpha=-1.0, beta=1.0)
+    ref2 = V - Qp @ C
+    torch.cuda.synchronize()
+    e_nn = float(((V2 - ref2).abs() / C.norm(dim=0).view(1, -1)).max())
+    assert e_tn < TOL, e_tn
+    assert e_nn < TOL, e_nn
