@@ -462,14 +462,24 @@ __global__ void k_oz_col_exp(int64_t N, const unsigned long long* __restrict__ c
 // through a 32 (k) x 32 (c) smem tile.
 template <int SB>
 __global__ void __launch_bounds__(256) k_oz_slice_b(int64_t K, int64_t N, const double* __restrict__ B, int64_t ldb,
-                                                    const int32_t* __restrict__ ek, const int32_t* __restrict__ fb,
+                                                    const int32_t* __restrict__ ek,
+                                                    const unsigned long long* __restrict__ colmax,
+                                                    int32_t* __restrict__ fb,
                                                     int64_t Np, int64_t Kp, int8_t* __restrict__ planes) {
     __shared__ uint32_t tile[SB][32][9];  // [plane][c][k / 4] packed digits
     const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8
     const int64_t k0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
     // load: thread (tx = c, ty) handles rows k0 + 4 ty .. 4 ty + 3 of column c0 + tx
     const int64_t col = c0 + tx;
-    const double sc = col < N ? ldexp(1.0, -fb[col]) : 0.0;
+    // column exponent from the column maximum (pass 1); the k-block-0 CTAs
+    // publish it for the GEMM epilogue
+    int f = 0;
+    if (col < N) {
+        const double m = __longlong_as_double((long long)colmax[col]);
+        f = m > 0.0 ? exp_above(m) + 1 : 0;  // |u| < 1/2: balanced digits in [-64, 64]
+        if (blockIdx.x == 0 && ty == 0) fb[col] = f;
+    }
+    const double sc = col < N ? ldexp(1.0, -f) : 0.0;
     int q[SB][4];
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
@@ -669,12 +679,11 @@ int oz_gemm_planes(int trans, int64_t n, int64_t d, int64_t p, double alpha, con
     {
         dim3 g((unsigned)std::min<int64_t>(cdiv(Kop, 8), 2 * sm_count()), (unsigned)cdiv(p, 32));
         k_oz_colmax_b<<<g, 256, 0, st>>>(Kop, p, B, ldb, ek, cmax);
-        k_oz_col_exp<<<(unsigned)cdiv(p, 128), 128, 0, st>>>(p, cmax, fb);
         dim3 g2((unsigned)cdiv(L.Kp, 32), (unsigned)cdiv(L.Np, 32));
         if (nplanes == OZ_SA)
-            k_oz_slice_b<OZ_LV_A><<<g2, 256, 0, st>>>(Kop, p, B, ldb, ek, fb, L.Np, L.Kp, bpl);
+            k_oz_slice_b<OZ_LV_A><<<g2, 256, 0, st>>>(Kop, p, B, ldb, ek, cmax, fb, L.Np, L.Kp, bpl);
         else
-            k_oz_slice_b<OZ_LV_Q><<<g2, 256, 0, st>>>(Kop, p, B, ldb, ek, fb, L.Np, L.Kp, bpl);
+            k_oz_slice_b<OZ_LV_Q><<<g2, 256, 0, st>>>(Kop, p, B, ldb, ek, cmax, fb, L.Np, L.Kp, bpl);
         RSVD_CHECK_LAUNCH();
     }
     const int sb = nplanes == OZ_SA ? OZ_LV_A : OZ_LV_Q;

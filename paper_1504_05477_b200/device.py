@@ -43,6 +43,7 @@ def _stream():
 
 
 _BODY_STREAMS = {}
+_WS_ALIAS = {}  # conditional-body stream -> the stream it was opened from
 
 
 class cond_section:
@@ -69,6 +70,8 @@ class cond_section:
         check(lib().rsvd_cond_begin(_stream(), _ptr(self.flag), ctypes.c_void_p(body.cuda_stream),
                                          ctypes.byref(opened)), "cond_begin")
         if opened.value:
+            # the body's launches run in the parent stream's order: they share its workspace
+            _WS_ALIAS[body.cuda_stream] = torch.cuda.current_stream(dev).cuda_stream
             self.body = body
             self.ctx = torch.cuda.stream(body)
             self.ctx.__enter__()
@@ -83,8 +86,9 @@ class cond_section:
 
 
 class _Workspace:
-    """One growing scratch buffer per device. Safe because every user runs in
-    stream order on the same stream.
+    """One growing scratch buffer per (device, stream). Safe because every
+    user of a buffer runs in stream order on that stream (threads driving
+    separate streams -- e.g. virtual row shards -- get separate buffers).
 
     Grow-only: a superseded buffer is kept referenced for the life of the
     process, never handed back to torch's caching allocator. A CUDA graph
@@ -98,7 +102,9 @@ class _Workspace:
         self.retired = []
 
     def get(self, nbytes, device):
-        key = torch.device(device).index
+        dev = torch.device(device)
+        sp = torch.cuda.current_stream(dev).cuda_stream
+        key = (dev.index, _WS_ALIAS.get(sp, sp))
         b = self.buf.get(key)
         if b is None or b.numel() < nbytes:
             if b is not None:
