@@ -470,13 +470,13 @@ def run_ours(args):
     orig_apply, orig_apply_t = op.apply, op.apply_t
 
     def timed(fn, kind):
-        def w(X, out):
+        def w(X, out, **kw):
             if not recording[0]:
-                return fn(X, out)
+                return fn(X, out, **kw)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            r = fn(X, out)
+            r = fn(X, out, **kw)
             e1.record()
             events.append((kind, X.shape[1], e0, e1))
             return r

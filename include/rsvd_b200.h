@@ -101,7 +101,9 @@ int rsvd_gemm_tn(int dtype, int out_dtype, int64_t m, int64_t n, int64_t k, doub
  *   and per-row exponents row_exp[n]; the caller owns both buffers.
  * rsvd_oz_gemm trans = 0: C (n x p) = alpha A X + beta C  (X d x p FP64)
  *              trans = 1: C (d x p) = alpha A^T Y + beta C (Y n x p FP64)
- *   C is FP64; workspace from rsvd_oz_gemm_ws_bytes(trans, n, d, p). */
+ *   (+2: reduced accuracy, ~3e-11 relative instead of ~5e-15: digit levels
+ *   i + j <= 4, 15 instead of 27 digit-pair GEMMs; the Rayleigh-Ritz W = A^T Q)
+ *   C is FP64; workspace from rsvd_oz_gemm_ws_bytes(trans & 1, n, d, p). */
 int64_t rsvd_oz_planes_bytes(int64_t n, int64_t d);
 int rsvd_oz_num_planes(void);
 int rsvd_oz_prepare(int64_t n, int64_t d, const float *A, int64_t lda, int8_t *planes, int32_t *row_exp,

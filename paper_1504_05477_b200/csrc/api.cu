@@ -121,7 +121,7 @@ int64_t rsvd_oz_gemm_ws_bytes(int trans, int64_t n, int64_t d, int64_t p) {
 int rsvd_oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t* planes,
                  const int32_t* row_exp, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
                  void* ws, int64_t ws_bytes, const int32_t* pred, void* stream) {
-    RSVD_REQUIRE(trans == 0 || trans == 1, "oz_gemm: trans must be 0 or 1");
+    RSVD_REQUIRE(trans >= 0 && trans <= 3, "oz_gemm: trans must be 0 / 1 (+2: reduced accuracy)");
     RSVD_REQUIRE(n >= 0 && d >= 0 && p >= 0, "oz_gemm: negative dimension");
     RSVD_REQUIRE(ldb >= p && ldc >= p, "oz_gemm: leading dimension too small");
     return oz_gemm(trans, n, d, p, alpha, planes, row_exp, B, ldb, beta, C, ldc, ws, ws_bytes, pred,

@@ -62,7 +62,7 @@ int64_t oz_gemm_ws_bytes(int trans, int64_t n, int64_t d, int64_t p);
 int oz_gemm_planes(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t* planes, int nplanes,
                    int64_t rows_alloc, int64_t cols_alloc, const int32_t* exps, int col_scaled, const double* B,
                    int64_t ldb, double beta, double* C, int64_t ldc, void* ws, int64_t ws_bytes, const int32_t* pred,
-                   cudaStream_t st);
+                   cudaStream_t st, int reduced = 0);
 int oz_basis_planes();
 int64_t oz_basis_bytes(int64_t n, int64_t w);
 int64_t oz_basis_ws_bytes(int64_t ncols);

@@ -46,6 +46,9 @@ constexpr int OZ_SA = 6;         // digit planes of an FP32 A (24-bit mantissas)
 constexpr int OZ_SQ = 7;         // digit planes of an FP64 orthonormal basis (global scale 2^1)
 constexpr int OZ_LV_A = 7;       // A products: kept levels i + j <= 6, 7 B digits
 constexpr int OZ_LV_Q = 8;       // basis products: levels i + j <= 7, 8 B digits (512 TMEM columns at BN 64)
+constexpr int OZ_LV_R = 5;       // reduced A products (levels i + j <= 4, A digits 0..4, 15 pairs): ~3e-11
+                                 // relative, for the Rayleigh-Ritz W = A^T Q (its error enters sigma^2
+                                 // linearly, against the chain's 1e-15 amplified ~1e9 by the basis)
 constexpr int OZ_SB_MAX = 8;
 constexpr int OZ_STAGES = 5;
 constexpr int64_t OZ_MAX_K = 65536;  // int32 exactness: 6 pairs x 64^2 x 65536 < 2^31
@@ -655,8 +658,9 @@ int64_t oz_gemm_ws_bytes(int trans, int64_t n, int64_t d, int64_t p) {
 int oz_gemm_planes(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t* planes, int nplanes,
                    int64_t rows_alloc, int64_t cols_alloc, const int32_t* exps, int col_scaled, const double* B,
                    int64_t ldb, double beta, double* C, int64_t ldc, void* ws, int64_t ws_bytes, const int32_t* pred,
-                   cudaStream_t st) {
+                   cudaStream_t st, int reduced) {
     const bool tr = trans != 0;
+    RSVD_REQUIRE(!reduced || nplanes == OZ_SA, "oz_gemm: reduced accuracy is for the A planes");
     // exponents of the contraction index are folded into B before slicing it;
     // exponents of the output-row index scale the epilogue
     const bool fold = tr != (col_scaled != 0);
@@ -680,13 +684,15 @@ int oz_gemm_planes(int trans, int64_t n, int64_t d, int64_t p, double alpha, con
         dim3 g((unsigned)std::min<int64_t>(cdiv(Kop, 8), 2 * sm_count()), (unsigned)cdiv(p, 32));
         k_oz_colmax_b<<<g, 256, 0, st>>>(Kop, p, B, ldb, ek, cmax);
         dim3 g2((unsigned)cdiv(L.Kp, 32), (unsigned)cdiv(L.Np, 32));
-        if (nplanes == OZ_SA)
+        if (reduced)
+            k_oz_slice_b<OZ_LV_R><<<g2, 256, 0, st>>>(Kop, p, B, ldb, ek, cmax, fb, L.Np, L.Kp, bpl);
+        else if (nplanes == OZ_SA)
             k_oz_slice_b<OZ_LV_A><<<g2, 256, 0, st>>>(Kop, p, B, ldb, ek, cmax, fb, L.Np, L.Kp, bpl);
         else
             k_oz_slice_b<OZ_LV_Q><<<g2, 256, 0, st>>>(Kop, p, B, ldb, ek, cmax, fb, L.Np, L.Kp, bpl);
         RSVD_CHECK_LAUNCH();
     }
-    const int sb = nplanes == OZ_SA ? OZ_LV_A : OZ_LV_Q;
+    const int sb = reduced ? OZ_LV_R : (nplanes == OZ_SA ? OZ_LV_A : OZ_LV_Q);
     int rc = RSVD_OK;
     OzParams prm{};
     prm.a_planes = planes;
@@ -716,7 +722,14 @@ int oz_gemm_planes(int trans, int64_t n, int64_t d, int64_t p, double alpha, con
         prm.ablate = ab ? atoi(ab) : 0;
     }
     dim3 grid((unsigned)(L.m_tiles * L.n_tiles), 1, (unsigned)L.splits);
-    if (nplanes == OZ_SA) {
+    if (reduced) {
+        if (L.bn == 32)
+            rc = tr ? launch_oz<32, true, OZ_LV_R, OZ_LV_R>(tA, tB, prm, grid, st)
+                    : launch_oz<32, false, OZ_LV_R, OZ_LV_R>(tA, tB, prm, grid, st);
+        else
+            rc = tr ? launch_oz<64, true, OZ_LV_R, OZ_LV_R>(tA, tB, prm, grid, st)
+                    : launch_oz<64, false, OZ_LV_R, OZ_LV_R>(tA, tB, prm, grid, st);
+    } else if (nplanes == OZ_SA) {
         if (L.bn == 32)
             rc = tr ? launch_oz<32, true, OZ_SA, OZ_LV_A>(tA, tB, prm, grid, st)
                     : launch_oz<32, false, OZ_SA, OZ_LV_A>(tA, tB, prm, grid, st);
@@ -743,8 +756,8 @@ int oz_gemm_planes(int trans, int64_t n, int64_t d, int64_t p, double alpha, con
 int oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t* planes,
             const int32_t* row_exp, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* ws,
             int64_t ws_bytes, const int32_t* pred, cudaStream_t st) {
-    return oz_gemm_planes(trans, n, d, p, alpha, planes, OZ_SA, cdiv(n, 128) * 128, cdiv(d, 128) * 128, row_exp, 0,
-                          B, ldb, beta, C, ldc, ws, ws_bytes, pred, st);
+    return oz_gemm_planes(trans & 1, n, d, p, alpha, planes, OZ_SA, cdiv(n, 128) * 128, cdiv(d, 128) * 128, row_exp,
+                          0, B, ldb, beta, C, ldc, ws, ws_bytes, pred, st, (trans & 2) != 0);
 }
 
 // ---- FP64 basis (n x w): OZ_SQ digit planes with per-COLUMN exponents

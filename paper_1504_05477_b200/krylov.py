@@ -498,7 +498,10 @@ def rayleigh_ritz(ops, comm, op, Q, k, n_total, row_offset, sign_fn=None, W=None
     if W is None:
         wdt = torch.float64 if Q.dtype == torch.float64 else Q.dtype
         W = rows_buffer(d, w, wdt, dev)
-        op.apply_t(Q, W)
+        if getattr(op, "oz", None) is not None:
+            op.apply_t(Q, W, rayleigh_ritz=True)
+        else:
+            op.apply_t(Q, W)
         comm.allreduce(W)
     M = torch.empty((w, w), dtype=torch.float64, device=dev)
     ops.gram(W, M)

@@ -18,6 +18,10 @@ import torch
 
 from . import device as ops
 
+# Exact mode: Rayleigh-Ritz W = A^T Q with reduced digit levels
+# (RSVD_OZ_REDUCED_RR=0: full accuracy, for A/B measurement).
+OZ_REDUCED_RR = os.environ.get("RSVD_OZ_REDUCED_RR", "1") != "0"
+
 
 class DenseDeviceOp:
     """``exact=True`` (FP32 A only): the Krylov blocks are FP64 and both
@@ -93,9 +97,13 @@ class DenseDeviceOp:
             self._ones = torch.ones((self.local_rows, 1), dtype=torch.float64, device=self.device)
         return self._ones
 
-    def apply_t(self, Y, out):
+    def apply_t(self, Y, out, rayleigh_ritz=False):
+        """``rayleigh_ritz`` (exact mode): W = A^T Q of post_process at ~3e-11
+        relative accuracy (reduced digit levels); W's error enters the Ritz
+        values linearly, unlike the Krylov chain's, which the reference's
+        power-block basis amplifies ~1e9-fold."""
         if self.oz is not None:
-            ops.oz_gemm(self.oz, Y, out, trans=1)
+            ops.oz_gemm(self.oz, Y, out, trans=1, reduced=rayleigh_ritz and OZ_REDUCED_RR)
             if self.mu is not None:
                 # (A - 1 mu^T)^T Y = A^T Y - mu (1^T Y) over the local rows
                 cs = ops.colreduce(Y, square=False).view(1, -1)

@@ -158,3 +158,18 @@ def test_oz_basis_projections(jp):
     e_nn = float(((V2 - ref2).abs() / C.norm(dim=0).view(1, -1)).max())
     assert e_tn < TOL, e_tn
     assert e_nn < TOL, e_nn
+
+
+def test_oz_reduced_levels():
+    """The Rayleigh-Ritz variant (digit levels i + j <= 4): ~3e-11 normwise."""
+    ops = _ops()
+    n, d, p = 5000, 700, 64
+    A = _case(n, d, 21)
+    A64 = A.double()
+    Y = torch.randn((n, p), device="cuda", dtype=torch.float64)
+    P = ops.OzPlanes(A)
+    W = torch.empty((d, p), dtype=torch.float64, device="cuda")
+    ops.oz_gemm(P, Y, W, trans=1, reduced=True)
+    torch.cuda.synchronize()
+    e = _normwise(W, A64.T @ Y, A64.T, Y)
+    assert 1e-15 < e < 1e-9, e
