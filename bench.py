@@ -214,10 +214,12 @@ def gemm_c4_probe(dev, bf16, reps=3):
     Y = torch.randn((n, b), generator=g, device=dev)
     out_y = torch.empty((n, b), device=dev)
     out_x = torch.empty((d, b), device=dev)
-    peak = bf16 / 6.0
+    px = _peaks_extra()
+    peak = px["tf32_tflops"] / 3.0 if px and px.get("tf32_tflops") else bf16 / 6.0
     fl = 2.0 * n * d * b
     res = {"config": f"C4 chain shape: A {n}x{d} FP32, width {b} (random operands)",
-           "peak_tflops": peak, "peak_source": f"measured bf16 dense {bf16:.0f} TFLOP/s / 6",
+           "peak_tflops": peak, "peak_source": (f"measured cuBLAS TF32 {px['tf32_tflops']:.0f} TFLOP/s / 3" if px and
+                                                px.get("tf32_tflops") else f"measured bf16 dense {bf16:.0f} / 6"),
            "ncu": "profiles/r01_c4_chain_kernel_ncu.json (tensor pipe 83% / 86% of peak sustained)"}
     for name, fn in (("A.X", lambda: ops.gemm_nn(A, X, out_y)), ("A^T.Y", lambda: ops.gemm_tn(A, Y, out_x))):
         fn()
@@ -393,6 +395,17 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": sorted(reasons), "samples": len(self.rows), "source": self.source}
+
+
+def _peaks_extra():
+    """TF32 / INT8 / FP64 cuBLAS peaks measured on this pool's B200s
+    (tools/measure_peaks_extra.py -> profiles/r02_measured_peaks_extra.json),
+    or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_measured_peaks_extra.json")) as f:
+            return json.loads(f.read().strip().splitlines()[-1])
+    except (OSError, ValueError, IndexError):
+        return None
 
 
 def _peaks():
@@ -573,7 +586,9 @@ def run_ours(args):
     # the chain product's bound: HBM below the ridge (C2: 25 flop/B in FP32),
     # tensor pipe above it (C4 / C5 at width 200: ~95 flop/B)
     flops_per = 2.0 * n_loc * d * cfg.p
-    tf_eff = bf16 / 6.0  # TF32 issues at half the bf16 rate; 3xTF32 = 3 MMAs per product
+    px = _peaks_extra()
+    # 3xTF32 = 3 TF32 MMAs per product: the measured cuBLAS TF32 peak / 3 (else bf16 / 6)
+    tf_eff = px["tf32_tflops"] / 3.0 if px and px.get("tf32_tflops") else bf16 / 6.0
     if sparse:
         kname = (("hybrid CSR product A.X / A^T.Y (width %d; hot-column panel on tcgen05 + CSR gather)"
                   if op.hot is not None else "CSR SpMM A.X / A^T.Y (width %d)") % cfg.p)
@@ -596,12 +611,20 @@ def run_ours(args):
             roofline["int8_tops"] = 27 * 2.0 * n_loc * d * 64 * (-(-cfg.p // 64)) / (avg_chain_ms * 1e-3) / 1e12
             roofline["note"] = ("algorithmic bytes = FP32 A + FP64 blocks; the kernel streams A's int8 digit "
                                 "planes (digit_plane_gbs) and is co-limited by the int8 MMA issue (27 digit pairs)")
+            px = _peaks_extra()
+            if px and px.get("int8_tops"):
+                roofline["int8_peak_tops"] = px["int8_tops"]
+                roofline["int8_frac"] = roofline["int8_tops"] / px["int8_tops"]
+                roofline["int8_peak_source"] = "measured cuBLAS int8 GEMM 8192^3 (profiles/r02_measured_peaks_extra.json)"
     else:
         tfl = flops_per / (avg_chain_ms * 1e-3) / 1e12
         roofline = {"bound": "tensor", "kernel": kname, "achieved": tfl, "peak": tf_eff, "unit": "TFLOP/s",
                     "frac": tfl / tf_eff,
-                    "peak_source": f"{peak_src} bf16 dense {bf16:.0f} TFLOP/s / 6 (TF32 at half the bf16 rate, "
-                                   "3 TF32 MMAs per 3xTF32 product)",
+                    "peak_source": (f"measured cuBLAS TF32 {px['tf32_tflops']:.0f} TFLOP/s / 3 (3 TF32 MMAs per "
+                                    "3xTF32 product; profiles/r02_measured_peaks_extra.json)" if px and
+                                    px.get("tf32_tflops") else
+                                    f"{peak_src} bf16 dense {bf16:.0f} TFLOP/s / 6 (TF32 at half the bf16 rate, "
+                                    "3 TF32 MMAs per 3xTF32 product)"),
                     "traffic": traffic, "algorithmic_flops_per_launch": flops_per,
                     "algorithmic_bytes_per_launch": bytes_per, "avg_launch_ms": avg_chain_ms,
                     "hbm_frac": achieved / hbm}
@@ -668,6 +691,8 @@ def run_ours(args):
         out["e2e_numpy"] = e2e_np
     if rank == 0 and world == 1 and not args.no_cpu and not sparse:
         out["cpu_baseline"] = cpu_baseline(A, cfgd, cfg, Pi, args, df, mode)
+    if rank == 0 and world == 1 and not args.no_cpu and sparse:
+        out["cpu_baseline"] = cpu_baseline_sparse(indptr, colv, valv, cfgd, cfg, Pi, args, df)
     if rank == 0 and world == 1 and not sparse and not args.no_spmm:
         out["spmm_c3"] = spmm_probe(dev)
     if rank == 0 and world == 1 and args.config == "c2" and not args.no_c4gemm:
@@ -745,6 +770,61 @@ def cpu_baseline(A_dev, cfgd, cfg, Pi, args, df=None, mode="exact"):
             res["parity_fp64_mode"] = mode_leg(A_dev, cfgd, cfg, Pi, r, "fp64")
         if A_dev.dtype == torch.float32 and mode != "fp32" and not args.no_fp32:
             res["parity_fp32_mode"] = mode_leg(A_dev, cfgd, cfg, Pi, r, "fp32")
+    return res
+
+
+def _csr_reference_worker(path, out_path, k, q, p, seed):
+    """Child process of cpu_baseline_sparse: the oracle on the host CSR."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import rsvd_oracle as o
+
+    z = np.load(path)
+    op = o.CsrOp(int(z["rows"]), int(z["cols"]), z["indptr"], z["col"], z["val"])
+    t0 = time.perf_counter()
+    r = o.factorize(op, k, "bk", q=q, p=p, seed=seed)
+    np.savez(out_path, sigma=r.sigma, Z=r.Z, secs=time.perf_counter() - t0, replaced=len(r.replaced))
+
+
+def cpu_baseline_sparse(indptr, colv, valv, cfgd, cfg, Pi, args, df):
+    """C3's host reference: the oracle's CsrOp (int64 indices, float64 values,
+    matrix.py:117-119; its SpMM kernels _kernels.pyx:74-113) on the same
+    matrix and Pi, in a child process with a wall-clock budget
+    (--cpu-budget-sparse). At config scale the reference's per-column _mgs of
+    the 200000 x 1600 basis is BLAS-2 over ~8 TB of memory traffic, so the
+    run is reported as DNF (did not finish) rather than extrapolated; when it
+    finishes, parity is computed like the dense configs'."""
+    import multiprocessing as mp
+    import tempfile
+
+    budget = args.cpu_budget_sparse
+    n, d = cfgd["n"], cfgd["d"]
+    tmp = tempfile.mkdtemp(prefix="rsvd_c3_")
+    path, out_path = os.path.join(tmp, "csr.npz"), os.path.join(tmp, "ref.npz")
+    np.savez(path, rows=n, cols=d, indptr=indptr.cpu().numpy().astype(np.int64),
+             col=colv.cpu().numpy().astype(np.int64), val=valv.cpu().numpy().astype(np.float64))
+    ctx = mp.get_context("spawn")
+    proc = ctx.Process(target=_csr_reference_worker, args=(path, out_path, cfg.k, cfg.q, cfg.p, cfg.seed))
+    t0 = time.perf_counter()
+    proc.start()
+    proc.join(budget)
+    elapsed = time.perf_counter() - t0
+    res = {"unit": "ms", "cores": os.cpu_count() or 1, "kind": "port", "budget_s": budget,
+           "sample": ("one full factorization by the reference algorithm (oracle port: its CSR SpMM kernels, "
+                      "per-column CGS2 _mgs, C Jacobi) on the same CSR (int64 / float64) and Pi, in a child process "
+                      f"with a {budget:.0f} s wall-clock budget")}
+    if proc.is_alive():
+        proc.terminate()
+        proc.join()
+        res.update({"value": None, "dnf": True, "elapsed_s": elapsed,
+                    "reason": "did not finish within the budget: the reference's per-column _mgs of the "
+                              f"{n} x {cfg.p * (cfg.resolve_q(d) + 1)} basis is BLAS-2 (TB of memory traffic) and "
+                              "its Jacobi runs at w = 1600; not extrapolated"})
+        return res
+    r = np.load(out_path)
+    res.update({"value": float(r["secs"]) * 1e3, "dnf": False})
+    sig = df.sigma.double().cpu().numpy()
+    res["parity"] = {"sigma_rel_max": float(np.max(np.abs(sig - r["sigma"]) / r["sigma"])), "tolerance": 1e-4,
+                     "replaced_columns_reference": int(r["replaced"])}
     return res
 
 
@@ -1007,6 +1087,8 @@ def main():
     ap.add_argument("--no-spmm", action="store_true", help="skip the C3 SpMM measurement on dense configs")
     ap.add_argument("--count-launches", action="store_true", default=True)
     ap.add_argument("--cpu-budget", type=float, default=25.0)
+    ap.add_argument("--cpu-budget-sparse", type=float, default=120.0,
+                    help="wall-clock budget (s) of C3's host reference run before it is reported as DNF")
     ap.add_argument("--graph", type=int, default=1, help="replay the factorization as a CUDA graph")
     ap.add_argument("--profile-step", action="store_true",
                     help="bracket one eager factorization with cudaProfilerStart/Stop (for ncu "
