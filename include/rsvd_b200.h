@@ -279,6 +279,27 @@ int rsvd_ortho_error(int64_t k, const double *G, int64_t ldg, double *out, void 
 int rsvd_cond_begin(void *stream, const int32_t *flag, void *body_stream, int32_t *opened);
 int rsvd_cond_end(void *body_stream);
 
+/* ---- 8. Per-device handle and communicator injection -----
+ * An opaque handle bound to one CUDA device (thread-compatible, not
+ * thread-safe) that carries the row-sharded run's communicator. The product
+ * needs one collective: the in-place sum-allreduce of every reduction over
+ * rows (A^T Y partials, Grams, projection coefficients, W = A^T Q).
+ * Inject an existing ncclComm_t (rsvd_handle_set_comm; the caller keeps
+ * ownership) or build one from a NCCL unique id distributed by the caller
+ * (rsvd_nccl_unique_id on one rank, rsvd_handle_init_comm on every rank; the
+ * handle owns it). NCCL is resolved at run time (dlopen "libnccl.so.2").
+ * rsvd_handle_allreduce_sum is stream-ordered; without a communicator it is a
+ * no-op (one rank). */
+typedef struct rsvd_handle_s *rsvd_handle;
+int rsvd_handle_create(int device, rsvd_handle *out);
+int rsvd_handle_destroy(rsvd_handle h);
+int rsvd_handle_device(rsvd_handle h, int *device);
+int rsvd_handle_world(rsvd_handle h, int *world, int *rank);
+int rsvd_handle_set_comm(rsvd_handle h, void *nccl_comm, int world, int rank);
+int rsvd_nccl_unique_id(char *id_out, int64_t id_bytes);
+int rsvd_handle_init_comm(rsvd_handle h, const char *id, int64_t id_bytes, int world, int rank);
+int rsvd_handle_allreduce_sum(rsvd_handle h, void *buf, int64_t count, int dtype, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

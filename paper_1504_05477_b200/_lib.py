@@ -64,6 +64,14 @@ _SIGS = {
     "rsvd_sqrt_clip": ([_i64, _vp, _vp, _vp], _int),
     "rsvd_ortho_error": ([_i64, _vp, _i64, _vp, _vp], _int),
     "rsvd_cond_begin": ([_vp, _vp, _vp, _vp], _int),
+    "rsvd_handle_create": ([_int, _vp], _int),
+    "rsvd_handle_destroy": ([_vp], _int),
+    "rsvd_handle_device": ([_vp, _vp], _int),
+    "rsvd_handle_world": ([_vp, _vp, _vp], _int),
+    "rsvd_handle_set_comm": ([_vp, _vp, _int, _int], _int),
+    "rsvd_nccl_unique_id": ([_vp, _i64], _int),
+    "rsvd_handle_init_comm": ([_vp, _vp, _i64, _int, _int], _int),
+    "rsvd_handle_allreduce_sum": ([_vp, _vp, _i64, _int, _vp], _int),
     "rsvd_cond_end": ([_vp], _int),
 }
 

@@ -101,6 +101,81 @@ class TorchComm:
         return out
 
 
+class HandleComm:
+    """The C ABI's own communicator (include/rsvd_b200.h section 8): a per-device
+    rsvd_handle carrying an injected / library-built NCCL communicator;
+    allreduce is rsvd_handle_allreduce_sum on the current stream. all_gather
+    (the sharded sign choice) is a sum-allreduce of zero-padded rank slots.
+    ``unique_id`` (128 bytes, from ``nccl_unique_id()`` on one rank and
+    distributed by the caller) builds the communicator; ``from_torch`` does
+    that over an existing torch.distributed group."""
+
+    def __init__(self, device, world=1, rank=0, unique_id=None, n_total=None, row_offset=0):
+        import ctypes
+
+        from . import _lib
+
+        self._L = _lib.load()
+        self._ct = ctypes
+        h = ctypes.c_void_p()
+        _lib.check(self._L.rsvd_handle_create(int(torch.device(device).index or 0), ctypes.byref(h)), "handle_create")
+        self.h = h
+        if unique_id is not None:
+            buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+            _lib.check(self._L.rsvd_handle_init_comm(h, buf, 128, int(world), int(rank)), "handle_init_comm")
+        self.world, self.rank = int(world), int(rank)
+        self.n_total, self.row_offset = n_total, row_offset
+
+    @staticmethod
+    def nccl_unique_id():
+        import ctypes
+
+        from . import _lib
+
+        buf = ctypes.create_string_buffer(128)
+        _lib.check(_lib.load().rsvd_nccl_unique_id(buf, 128), "nccl_unique_id")
+        return buf.raw
+
+    @classmethod
+    def from_torch(cls, device, group=None, n_total=None, row_offset=0):
+        import torch.distributed as dist
+
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        obj = [cls.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(device, world, rank, obj[0], n_total=n_total, row_offset=row_offset)
+
+    def allreduce(self, t):
+        from . import _lib
+        from .device import dcode
+
+        buf = t if t.is_contiguous() else t.contiguous()
+        _lib.check(self._L.rsvd_handle_allreduce_sum(self.h, self._ct.c_void_p(buf.data_ptr()), buf.numel(),
+                                                     dcode(buf), self._ct.c_void_p(
+                                                         torch.cuda.current_stream(buf.device).cuda_stream)),
+                   "handle_allreduce_sum")
+        if buf is not t:
+            t.copy_(buf)
+        return t
+
+    def all_gather(self, t):
+        slots = torch.zeros((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        slots[self.rank] = t
+        if t.dtype in (torch.float32, torch.float64):
+            self.allreduce(slots)
+        else:  # indices: exact through FP64 (|i| < 2^53)
+            f = slots.double()
+            self.allreduce(f)
+            slots = f.to(t.dtype)
+        return [slots[i] for i in range(self.world)]
+
+    def __del__(self):
+        try:
+            self._L.rsvd_handle_destroy(self.h)
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
 def shard_rows(n, world, rank):
     """Contiguous row shard [lo, hi) of rank (rows [g n/G, (g+1) n/G))."""
     lo = (n * rank) // world

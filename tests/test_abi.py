@@ -66,3 +66,21 @@ def test_invalid_args_map_to_status():
         assert "dtype" in str(e)
     else:
         raise AssertionError("expected ValueError")
+
+
+def test_handle_without_gpu_and_argument_checks():
+    """The per-device handle fails cleanly (status, message) where there is
+    no device, and validates its arguments before touching CUDA / NCCL."""
+    import torch
+
+    from paper_1504_05477_b200 import _lib
+
+    L = _lib.load()
+    h = ctypes.c_void_p()
+    if not torch.cuda.is_available():
+        assert L.rsvd_handle_create(0, ctypes.byref(h)) == _lib.RSVD_ERR_CUDA
+        assert b"no CUDA device" in L.rsvd_last_error()
+    assert L.rsvd_handle_create(-1, ctypes.byref(h)) != _lib.RSVD_OK
+    assert L.rsvd_handle_allreduce_sum(None, None, 1, 1, None) == _lib.RSVD_ERR_INVALID
+    assert L.rsvd_nccl_unique_id(None, 128) == _lib.RSVD_ERR_INVALID
+    assert L.rsvd_handle_destroy(None) == _lib.RSVD_OK
