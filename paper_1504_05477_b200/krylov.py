@@ -265,6 +265,9 @@ D_SPACE_PASS1 = os.environ.get("RSVD_DSPACE_PASS1", "1") != "0"
 # Exact mode: projections against the final prefix on its int8 digit planes
 # (RSVD_OZ_PROJ=0: FP64 DMMA, for A/B measurement).
 OZ_PROJECTIONS = os.environ.get("RSVD_OZ_PROJ", "1") != "0"
+# Reference-faithful basis: the power chain and the final orthonormalization
+# on two streams (RSVD_OVERLAP_FINAL=0: one stream, for A/B measurement).
+OVERLAP_FINAL = os.environ.get("RSVD_OVERLAP_FINAL", "1") != "0"
 
 
 def proj_passes(dtype):
@@ -496,6 +499,8 @@ def bk_basis(ops, comm, op, Pi, q, ws, n_total, row_offset):
         op.apply_t(K[:, (n_blocks - 1) * p:], last)
         comm.allreduce(last)
         return BasisResult(K, n_blocks - 1, deflated, W=W)
+    if OVERLAP_FINAL and isinstance(comm, LocalComm) and dev.type == "cuda":
+        return _bk_faithful_overlapped(ops, comm, op, K, C, tmp, ws, n_blocks, p, n_total, row_offset, deflated)
     for j in range(1, n_blocks):
         prev = K[:, (j - 1) * p: j * p]
         cur = K[:, j * p: (j + 1) * p]
@@ -519,6 +524,71 @@ def bk_basis(ops, comm, op, Pi, q, ws, n_total, row_offset):
                    n_total=n_total, row_offset=row_offset, deflation_count=deflated, basis=basis)
         if basis is not None and j + 1 < n_blocks:
             basis.slice(K, j * p, p)
+    return BasisResult(K, n_blocks - 1, deflated)
+
+
+_SIDE_STREAMS = {}
+
+
+def _bk_faithful_overlapped(ops, comm, op, K, C, tmp, ws, n_blocks, p, n_total, row_offset, deflated):
+    """The reference-faithful block-Krylov basis with its two sequences on
+    two streams: the power chain b_j = mgs(A A^T b_{j-1}) on the caller's
+    stream, and the final orthonormalization of hstack(blocks) (block j
+    against the final prefix, in place) on a side stream. The only
+    dependency between them is that block j may be overwritten by its final
+    orthonormalization once the chain has read it (A^T b_j), which an event
+    orders; everything else is independent, so the final pass's
+    latency-bound small kernels (Grams, Cholesky, projections) fill the gaps
+    of the chain's tensor-core products. Same arithmetic, same order per
+    block, same results (single rank: NCCL collectives on two streams could
+    interleave differently on different ranks, so the sharded path stays
+    sequential)."""
+    dev, dt = op.device, op.dtype
+    n = op.local_rows
+    main = torch.cuda.current_stream(dev)
+    side = _SIDE_STREAMS.get(dev)
+    if side is None:
+        side = _SIDE_STREAMS[dev] = torch.cuda.Stream(device=dev)
+    ws2 = Workspace(dev, p)
+    tmp2 = rows_buffer(n, p, dt, dev)
+    running_chain = torch.zeros(1, dtype=torch.int32, device=dev)
+    running_final = torch.zeros(1, dtype=torch.int32, device=dev)
+    basis = ops.OzBasis(n, n_blocks * p, dev) if (getattr(op, "oz", None) is not None and
+                                                  dt == torch.float64 and OZ_PROJECTIONS) else None
+    ready = torch.cuda.Event()
+    ready.record(main)
+    side.wait_event(ready)
+
+    def final(j):
+        with torch.cuda.stream(side):
+            cur = K[:, j * p: (j + 1) * p]
+            ref2 = ws2.ref2[:p]
+            ops.colreduce(cur, True, ref2)
+            comm.allreduce(ref2)
+            orth_block(ops, comm, cur, tmp2, ws2, Qp=K[:, : j * p] if j else None, ref2=ref2, running=running_final,
+                       n_total=n_total, row_offset=row_offset, deflation_count=deflated, basis=basis)
+            if basis is not None and j + 1 < n_blocks:
+                basis.slice(K, j * p, p)
+
+    for j in range(1, n_blocks):
+        prev = K[:, (j - 1) * p: j * p]
+        cur = K[:, j * p: (j + 1) * p]
+        op.apply_t(prev, C)
+        comm.allreduce(C)
+        consumed = torch.cuda.Event()
+        consumed.record(main)  # b_{j-1} has been read by the chain
+        side.wait_event(consumed)
+        final(j - 1)
+        op.apply(C, cur)
+        running_chain.zero_()
+        orth_block(ops, comm, cur, tmp, ws, running=running_chain, n_total=n_total, row_offset=row_offset)
+    last = torch.cuda.Event()
+    last.record(main)
+    side.wait_event(last)
+    final(n_blocks - 1)
+    done = torch.cuda.Event()
+    done.record(side)
+    main.wait_event(done)
     return BasisResult(K, n_blocks - 1, deflated)
 
 
