@@ -469,6 +469,64 @@ def _graph_cache_key(A, cfg, precision, device, center=False):
             bool(center), _mode(src, precision))
 
 
+class _PageableUploader:
+    """H2D of a pageable host array through two pinned staging buffers: host
+    threads copy chunk i + 1 into one buffer while the DMA engine moves chunk
+    i out of the other (a plain copy from pageable memory goes through the
+    driver's own single-threaded staging: ~14 GB/s measured at C2, 2 GB in
+    ~140 ms). Casting to the device dtype happens in the host copy."""
+
+    CHUNK_BYTES = 64 << 20
+    THREADS = min(16, os.cpu_count() or 1)
+
+    def __init__(self):
+        self.bufs = None
+        self.events = None
+        self.pool = None
+
+    def _setup(self):
+        if self.bufs is None:
+            from concurrent.futures import ThreadPoolExecutor
+
+            self.bufs = [torch.empty(self.CHUNK_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+            self.events = [None, None]
+            self.pool = ThreadPoolExecutor(max_workers=self.THREADS)
+
+    def upload(self, dst, arr):
+        self._setup()
+        src = arr.reshape(-1)
+        flat = dst.view(-1)
+        esize = dst.element_size()
+        npdt = np.float32 if dst.dtype == torch.float32 else np.float64
+        per = self.CHUNK_BYTES // esize
+        stream = torch.cuda.current_stream(dst.device)
+        for i, off in enumerate(range(0, src.size, per)):
+            m = min(per, src.size - off)
+            slot = i % 2
+            if self.events[slot] is not None:
+                self.events[slot].synchronize()  # the DMA out of this buffer is done
+            host = self.bufs[slot][: m * esize].numpy().view(npdt)
+            nt = self.THREADS if m >= (1 << 20) else 1
+            bounds = [(m * t) // nt for t in range(nt + 1)]
+
+            def cp(t, host=host, off=off, bounds=bounds):
+                a, b = bounds[t], bounds[t + 1]
+                if b > a:  # numpy releases the GIL for the copy
+                    np.copyto(host[a:b], src[off + a: off + b], casting="unsafe")
+
+            list(self.pool.map(cp, range(nt)))
+            flat[off: off + m].copy_(self.bufs[slot][: m * esize].view(dst.dtype), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            self.events[slot] = ev
+        for ev in self.events:
+            if ev is not None:
+                ev.synchronize()
+
+
+_UPLOADER = _PageableUploader()
+
+
 def _upload_into(buf, A):
     """Copy host / device A into the persistent buffer (DMA from pinned
     memory), with the dense-input validation of make_operator."""
@@ -480,9 +538,13 @@ def _upload_into(buf, A):
             buf.copy_(src.to(device=buf.device, non_blocking=(not src.is_cuda) and src.is_pinned()))
     else:
         arr = as_dense_array(A) if not (isinstance(A, np.ndarray) and A.dtype == np.float32) else np.asarray(A)
-        with warnings.catch_warnings():  # read-only source (DenseMatrix data): only read by the copy
-            warnings.simplefilter("ignore", UserWarning)
-            buf.copy_(torch.from_numpy(np.ascontiguousarray(arr)))
+        arr = np.ascontiguousarray(arr)
+        if arr.nbytes >= 2 * _PageableUploader.CHUNK_BYTES:
+            _UPLOADER.upload(buf, arr)
+        else:
+            with warnings.catch_warnings():  # read-only source (DenseMatrix data): only read by the copy
+                warnings.simplefilter("ignore", UserWarning)
+                buf.copy_(torch.from_numpy(arr))
     # one pass, no temporaries: FP64 column sums are finite iff every entry is
     # (an FP32 column cannot overflow an FP64 sum; for FP64 input a sum could
     # only overflow with entries near 1e308)
