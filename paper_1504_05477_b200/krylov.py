@@ -245,13 +245,8 @@ def project_out(ops, comm, Qp, V, tmp_c, pred=None, basis=None):
 # are well conditioned after the first pass and Z is re-orthonormalised in
 # FP64; RSVD_FP32_THIRD_PASS=1 restores it for comparison).
 FP32_THIRD_PASS = os.environ.get("RSVD_FP32_THIRD_PASS", "0") == "1"
-# Projection passes against the prefix before the round-1 Gram. FP64 keeps
-# two (BCGS2; the reference-faithful path's deflation decisions depend on the
-# round-1 residuals). FP32 takes one: the final pass re-projects after the
-# CholeskyQR step, so the block still gets two projections in total
-# (project, CholQR, project, CholQR); measured at C2: sigma and captured
-# variance identical to 1e-9 relative, 24.06 -> 22.94 ms.
-# RSVD_PROJ_PASSES overrides both (A/B measurement).
+# Projection passes against the prefix before the round-1 Gram (see
+# proj_passes); RSVD_PROJ_PASSES overrides (A/B measurement).
 _PROJ_ENV = os.environ.get("RSVD_PROJ_PASSES")
 # Device-decided sections as CUDA-graph conditional nodes (RSVD_GRAPH_COND=0:
 # predicated kernels only, for A/B measurement).
@@ -271,9 +266,16 @@ OVERLAP_FINAL = os.environ.get("RSVD_OVERLAP_FINAL", "1") != "0"
 
 
 def proj_passes(dtype):
+    """One projection pass before the round-1 Gram in every precision: the
+    decisions that matter for parity (residual <= 1e-12 x original norm,
+    factor.py:105) are made in round 2 on explicitly re-projected residuals
+    (two more passes), and the final pass projects again after the
+    CholeskyQR step. Measured at C2 (exact mode): 39.3 -> 37.2 ms, sigma /
+    captured variance / replaced columns unchanged; C1 and the reference
+    goldens unchanged to 1e-10 (tests)."""
     if _PROJ_ENV:
         return int(_PROJ_ENV)
-    return 2 if dtype == torch.float64 else 1
+    return 1
 
 
 def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=None, row_offset=0,
