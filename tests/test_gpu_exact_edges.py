@@ -1,0 +1,77 @@
+"""Exact mode (FP32 A, FP64-accurate int8 digit-plane products, the
+reference's faithful basis) on the edge shapes the reference's own suite
+exercises (test_rsvd.py: tiny and ragged matrices, k = min(n, d), width
+capped by min(n, d) // p, rank-deficient and all-zero inputs, q = 0 sketch),
+each against the oracle run on the same float32 A upcast to float64."""
+
+import numpy as np
+import pytest
+
+import rsvd_oracle as o
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rk():
+    import paper_1504_05477_b200 as rk
+
+    return rk
+
+
+def _check(rk, A32, k, variant, q, p=None, seed=0, tol=1e-9):
+    A64 = A32.astype(np.float64)
+    ref = o.factorize(o.DenseOp(A64), k, variant, q=q, p=p, seed=seed)
+    cfg = rk.RsvdConfig(k=k, variant=variant, q=q, p=p, seed=seed)
+    r = rk.factorize(A32, cfg)  # float32 input: exact mode by default
+    assert r.q_used == ref.q_used
+    s, sr = r.approx_singular_values, ref.sigma
+    scale = max(sr.max(), 1e-300)
+    assert np.max(np.abs(s - sr)) <= tol * scale, (s, sr)
+    z = r.Z.data
+    assert np.max(np.abs(z.T @ z - np.eye(z.shape[1]))) <= 1e-10
+    return r, ref
+
+
+@pytest.mark.parametrize("n,d,k,q", [(5, 3, 1, 2), (7, 7, 7, 0), (130, 33, 4, 3), (257, 129, 9, 5),
+                                     (1000, 17, 5, 2), (33, 1000, 6, 4)])
+def test_exact_ragged_and_tiny(rk, n, d, k, q):
+    rng = np.random.default_rng(n * 31 + d)
+    A = (rng.standard_normal((n, d)) * np.exp(rng.standard_normal((1, d)))).astype(np.float32)
+    _check(rk, A, k, "bk", q)
+
+
+def test_exact_width_capped_and_rank_deficient(rk):
+    rng = np.random.default_rng(3)
+    U = rng.standard_normal((400, 6))
+    V = rng.standard_normal((6, 90))
+    A = (U @ V).astype(np.float32)  # rank 6, cap min(n, d) // p = 4 blocks at p = 20
+    r, ref = _check(rk, A, 20, "bk", 9, tol=1e-8)
+    assert r.q_used == 3
+
+
+def test_exact_all_zero_and_zero_rows(rk):
+    A = np.zeros((300, 80), dtype=np.float32)
+    r, _ = _check(rk, A, 5, "bk", 3)
+    assert np.all(r.approx_singular_values == 0.0)
+    rng = np.random.default_rng(9)
+    B = rng.standard_normal((300, 80)).astype(np.float32)
+    B[::7] = 0.0
+    B[:, 11] = 0.0
+    _check(rk, B, 8, "bk", 4)
+
+
+def test_exact_wide_dynamic_range(rk):
+    """Rows spanning 1e-30 .. 1e30 (per-row digit exponents) and FP32
+    subnormal entries."""
+    rng = np.random.default_rng(4)
+    A = rng.standard_normal((500, 120)) * np.logspace(-30, 30, 500)[:, None]
+    A[3, :5] = 1e-42  # FP32 subnormals
+    _check(rk, A.astype(np.float32), 6, "bk", 3, tol=1e-8)
+
+
+@pytest.mark.parametrize("variant,q", [("si", 4), ("sketch", 0)])
+def test_exact_si_and_sketch(rk, variant, q):
+    rng = np.random.default_rng(5)
+    A = (rng.standard_normal((700, 300)) * (np.arange(1, 301) ** -0.7)).astype(np.float32)
+    _check(rk, A, 10, variant, q, tol=1e-8)
