@@ -148,7 +148,7 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         mbar_init(acc_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (A_MN) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         if (p.Np != BN) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     }
     if (warp == 1) {
@@ -176,19 +176,15 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 mbar_expect_tx(&full[s], Cfg::STAGE - ((p.ablate & 1) ? SB * Cfg::B_TILE : 0) -
                                              ((p.ablate & 2) ? SA * Cfg::A_TILE : 0));
                 if (!(p.ablate & 2)) {
-#pragma unroll
-                    for (int i = 0; i < SA; ++i) {
-                        const int8_t* pl = p.a_planes + (int64_t)i * p.a_pitch;
-                        uint8_t* dst = st + i * Cfg::A_TILE;
-                        if (!A_MN) {
-#pragma unroll
-                            for (int h = 0; h < 2; ++h)
-                                bulk_g2s(dst + h * 2048, pl + ((kk / 16 + h) * p.a_rows + m0) * 16, 2048, &full[s]);
-                        } else {
-                            // 8 column blocks x 512 B: one TMA box (rows of 512 B, as uint32)
-                            tma_load_3d(&tmA, &full[s], dst, (int)(kk * 4), (int)(m0 / 16), i);
-                        }
-                    }
+                    // all SA digit planes of the tile in ONE TMA box (u64 view of the 16-byte
+                    // row pieces): NN 128 rows x 2 column blocks, TN 32 rows x 8 column blocks,
+                    // landing as [plane][block][row][16 B]. (Per-plane bulk copies -- 13 to 15
+                    // issues per K step from the one producer thread -- capped the short-K
+                    // basis products at ~2 TB/s.)
+                    if (!A_MN)
+                        tma_load_3d(&tmA, &full[s], st, (int)(m0 * 2), (int)(kk / 16), 0);
+                    else
+                        tma_load_3d(&tmA, &full[s], st, (int)(kk * 2), (int)(m0 / 16), 0);
                 }
                 if (!(p.ablate & 1)) {
                     uint8_t* dst = st + SA * Cfg::A_TILE;
@@ -530,17 +526,20 @@ __global__ void k_oz_reduce(int64_t M, int64_t N, int64_t ldw, int64_t splits, c
 }
 
 // ---------------------------------------------------------------- host
-// u32 views of the digit planes (16-byte row pieces as 4 elements): box rows
-// of 512 B / BN x 16 B, no swizzle (the interleaved core-matrix layout is the
-// gmem layout itself).
-int oz_map_a_tn(CUtensorMap* map, const int8_t* planes, int64_t a_rows, int64_t d_pad, int64_t pitch, int nplanes) {
+// u64 views of the digit planes (a 16-byte row piece = 2 elements), no swizzle
+// (the interleaved core-matrix layout is the gmem layout itself): one box =
+// every used digit plane of a tile -- NN {128 rows, 2 column blocks, used},
+// TN {32 rows, 8 column blocks, used}. B: u32 view, BN x 16 B rows.
+int oz_map_a(CUtensorMap* map, const int8_t* planes, int64_t a_rows, int64_t d_pad, int64_t pitch, int nplanes,
+             int used, bool mn_major) {
     EncodeTiledFn fn = encode_fn();
     RSVD_REQUIRE(fn != nullptr, "cuTensorMapEncodeTiled unavailable");
-    cuuint64_t dims[3] = {(cuuint64_t)(a_rows * 4), (cuuint64_t)(d_pad / 16), (cuuint64_t)nplanes};
+    cuuint64_t dims[3] = {(cuuint64_t)(a_rows * 2), (cuuint64_t)(d_pad / 16), (cuuint64_t)nplanes};
     cuuint64_t strides[2] = {(cuuint64_t)(a_rows * 16), (cuuint64_t)pitch};
-    cuuint32_t box[3] = {(cuuint32_t)(OZ_KS * 4), 8, 1};
+    cuuint32_t box[3] = {mn_major ? (cuuint32_t)(OZ_KS * 2) : (cuuint32_t)(OZ_BM * 2), mn_major ? 8u : 2u,
+                         (cuuint32_t)used};
     cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<int8_t*>(planes), dims, strides, box, estr,
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<int8_t*>(planes), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     RSVD_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (Ozaki A planes) failed (%d)", (int)r);
@@ -700,10 +699,9 @@ int oz_gemm_planes(int trans, int64_t n, int64_t d, int64_t p, double alpha, con
     prm.a_pitch = rows_alloc * cols_alloc;
     prm.b_planes = bpl;
     CUtensorMap tA{}, tB{};
-    if (tr) {
-        rc = oz_map_a_tn(&tA, planes, rows_alloc, cols_alloc, prm.a_pitch, nplanes);
-        if (rc) return rc;
-    }
+    rc = oz_map_a(&tA, planes, rows_alloc, cols_alloc, prm.a_pitch, nplanes,
+                  reduced ? OZ_LV_R : nplanes, tr);
+    if (rc) return rc;
     if (L.Np != L.bn) {
         rc = oz_map_b(&tB, bpl, L.Np, L.Kp / 32, L.bn, sb);
         if (rc) return rc;
