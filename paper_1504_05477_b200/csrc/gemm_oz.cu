@@ -52,7 +52,7 @@ constexpr int OZ_LV_R = 5;       // reduced A products (levels i + j <= 4, A dig
 constexpr int OZ_SB_MAX = 8;
 constexpr int OZ_STAGES = 5;
 constexpr int64_t OZ_MAX_K = 65536;  // int32 exactness: 6 pairs x 64^2 x 65536 < 2^31
-constexpr int OZ_THREADS = 6 * 32;   // 0 TMA, 1 MMA, 2..5 epilogue
+constexpr int OZ_THREADS = 10 * 32;  // 0 TMA, 1 MMA, 2..9 epilogue (two warps per TMEM lane quarter)
 constexpr uint32_t kLayoutNone = 0;
 
 // SA digit planes of the A operand, LV kept levels i + j < LV, as many B digits
@@ -120,10 +120,25 @@ __device__ __forceinline__ void tmem_ld16_s32(uint32_t taddr, int32_t* v) {
     for (int i = 0; i < 16; ++i) v[i] = (int32_t)r[i];
 }
 
+#ifdef RSVD_OZ_TRACE
+// clock64 / globaltimer stamps of the first 512 CTAs: start, after setup,
+// acc_full seen, epilogue done (tools/oz_trace.py builds with -DRSVD_OZ_TRACE)
+__device__ unsigned long long g_oz_trace[512][5];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define OZ_STAMP(i) do { if (blockIdx.x < 512 && blockIdx.z == 0) g_oz_trace[blockIdx.x][i] = gtime(); } while (0)
+#else
+#define OZ_STAMP(i) do { } while (0)
+#endif
+
 template <int BN, bool A_MN, int SA, int LV>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
 k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, OzParams p) {
     if (pred_off(p.pred)) return;
+    if (threadIdx.x == 0) OZ_STAMP(0);
     using Cfg = OzCfg<BN, SA, LV>;
     constexpr int SB = Cfg::SB;
     extern __shared__ uint8_t smem_raw[];
@@ -160,6 +175,7 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) OZ_STAMP(1);
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- producer: 1-D bulk copies of contiguous runs
@@ -236,57 +252,128 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const int quarter = warp % 4;
         const int64_t row = m0 + quarter * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+        if (p.direct && p.beta != 0.0 && row < p.M) {
+            // C is read back by the epilogue (beta != 0): pull this thread's row
+            // segment into L2 while the main loop runs
+            const int hf = (warp - 2) / 4;
+            for (int c = hf * (BN / 2); c < (hf + 1) * (BN / 2) && n0 + c < p.N; c += 16)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(p.C + row * p.ldc + n0 + c));
+        }
         if (nks > 0) {
             mbar_wait(acc_full, 0);
             tc_fence_after();
         }
+        if (warp == 2 && lane == 0) OZ_STAMP(2);
         int ea = 0;
         if (p.ea && row < p.M) ea = p.ea[row];
+        // per-column scale 2^(ea + fb - 14) as an exact power-of-two multiply
+        // (ldexp's general path, 64 calls per thread, was a large part of a
+        // ~20 us per-CTA epilogue), with ldexp kept for exponents outside the
+        // normal range
+        auto scale_of = [&](int e) -> double {
+            return (e > -1022 && e < 1023) ? __longlong_as_double((long long)(e + 1023) << 52) : 0.0;
+        };
+        // The epilogue is latency-bound (one warp per SM sub-partition): the
+        // levels are combined in 64-bit integer arithmetic -- hi = sum_{L<4}
+        // acc_L 2^7(3-L), lo = sum_{L>=4} acc_L 2^7(LV-1-L), each < 2^53 so its
+        // conversion is exact -- and v = hi 2^-21 + lo 2^-7(LV-1): two int->FP64
+        // conversions and one FMA per output instead of LV of each (the Horner
+        // form made the epilogue ~14-16 us per CTA, 20 % of a chain product).
+        constexpr int LH = LV < 4 ? LV : 4;
+        const double lo_w = ldexp(1.0, -7 * (LV - 1));
+        double sc[16];
+        // two epilogue warps per lane quarter, each drains half of the columns
+        const int half = (warp - 2) / 4;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
+        for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 16) {
             double v[16];
-#pragma unroll
-            for (int t = 0; t < 16; ++t) v[t] = 0.0;
             if (nks > 0) {
-                // Horner from the smallest level: v = sum_L acc_L 2^-7L
+                int64_t hi[16], lo[16];
+                {
+                    int32_t a[LH][16];
 #pragma unroll
-                for (int L = LV - 1; L >= 0; --L) {
-                    int32_t a[16];
-                    tmem_ld16_s32(tmem_base + lane_off + (uint32_t)(L * BN + c0), a);
+                    for (int L = 0; L < LH; ++L) tmem_ld16_s32(tmem_base + lane_off + (uint32_t)(L * BN + c0), a[L]);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                    for (int t = 0; t < 16; ++t) v[t] = fma(v[t], 0.0078125, (double)a[t]);
+                    for (int t = 0; t < 16; ++t) {
+                        int64_t h = 0;
+#pragma unroll
+                        for (int L = 0; L < LH; ++L) h = h * 128 + a[L][t];
+                        hi[t] = h;
+                    }
                 }
+                if constexpr (LV > 4) {
+                    int32_t a[LV - 4][16];
+#pragma unroll
+                    for (int L = 4; L < LV; ++L)
+                        tmem_ld16_s32(tmem_base + lane_off + (uint32_t)(L * BN + c0), a[L - 4]);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int t = 0; t < 16; ++t) {
+                        int64_t l = 0;
+#pragma unroll
+                        for (int L = 0; L < LV - 4; ++L) l = l * 128 + a[L][t];
+                        lo[t] = l;
+                    }
+                } else {
+#pragma unroll
+                    for (int t = 0; t < 16; ++t) lo[t] = 0;
+                }
+                const double hi_w = ldexp(1.0, -7 * (LH - 1));
+#pragma unroll
+                for (int t = 0; t < 16; ++t) v[t] = fma((double)lo[t], lo_w, (double)hi[t] * hi_w);
+            } else {
+#pragma unroll
+                for (int t = 0; t < 16; ++t) v[t] = 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+                const int64_t col = n0 + c0 + t;
+                sc[t] = col < p.N ? scale_of(ea + p.fb[col] - 14) : 0.0;
             }
             if (row < p.M) {
-                // all loads of the chunk before any store: a load after a store to
-                // the same array would otherwise wait for it (C is read and written)
+                const int64_t base = p.direct ? row * p.ldc + n0 + c0 : ((int64_t)blockIdx.z * p.M + row) * p.ldw + n0 + c0;
+                double* out = p.direct ? p.C + base : p.ws + base;
+                const bool full16 = n0 + c0 + 16 <= p.N && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+                // all loads of the chunk before any store (C is read and written)
                 double cin[16];
+                const bool rmw = p.direct && p.beta != 0.0;
+                if (rmw && full16) {
 #pragma unroll
-                for (int t = 0; t < 16; ++t) {
-                    const int64_t col = n0 + c0 + t;
-                    cin[t] = (p.direct && p.beta != 0.0 && col < p.N) ? p.C[row * p.ldc + col] : 0.0;
-                }
-#pragma unroll
-                for (int t = 0; t < 16; ++t) {
-                    const int64_t col = n0 + c0 + t;
-                    if (col < p.N) {
-                        const double val = ldexp(v[t], ea + p.fb[col] - 14);
-                        if (p.direct)
-                            p.C[row * p.ldc + col] = p.beta != 0.0 ? p.alpha * val + p.beta * cin[t] : p.alpha * val;
-                        else
-                            p.ws[((int64_t)blockIdx.z * p.M + row) * p.ldw + col] = val;
+                    for (int t = 0; t < 16; t += 2) {
+                        const double2 c2 = *reinterpret_cast<const double2*>(out + t);
+                        cin[t] = c2.x;
+                        cin[t + 1] = c2.y;
                     }
+                } else {
+#pragma unroll
+                    for (int t = 0; t < 16; ++t) cin[t] = (rmw && n0 + c0 + t < p.N) ? out[t] : 0.0;
+                }
+                double res[16];
+#pragma unroll
+                for (int t = 0; t < 16; ++t) {
+                    const double val = sc[t] != 0.0 ? v[t] * sc[t] : ldexp(v[t], ea + p.fb[min(n0 + c0 + t, p.N - 1)] - 14);
+                    res[t] = p.direct ? (rmw ? p.alpha * val + p.beta * cin[t] : p.alpha * val) : val;
+                }
+                if (full16) {
+#pragma unroll
+                    for (int t = 0; t < 16; t += 2) *reinterpret_cast<double2*>(out + t) = make_double2(res[t], res[t + 1]);
+                } else {
+#pragma unroll
+                    for (int t = 0; t < 16; ++t)
+                        if (n0 + c0 + t < p.N) out[t] = res[t];
                 }
             }
         }
     }
+    if (warp == 2 && lane == 0) OZ_STAMP(3);
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
     }
+    if (threadIdx.x == 32) OZ_STAMP(4);
 }
 
 // ---------------------------------------------------------------- slicing
@@ -787,3 +874,9 @@ int oz_basis_slice(int64_t n, int64_t w, const double* Q, int64_t ldq, int64_t c
 }
 
 }  // namespace rsvd
+
+#ifdef RSVD_OZ_TRACE
+extern "C" int rsvd_debug_oz_trace(unsigned long long* host_out) {
+    return (int)cudaMemcpyFromSymbol(host_out, rsvd::g_oz_trace, sizeof(rsvd::g_oz_trace));
+}
+#endif

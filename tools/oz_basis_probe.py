@@ -22,3 +22,15 @@ for name, fn in (("tn", lambda: B.gemm(1, jp, V, C)), ("nn", lambda: B.gemm(0, j
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     print(f"basis {name} jp={jp}: {ms*1e3:.1f} us; planes {7*n*jp/ms/1e6:.0f} GB/s", flush=True)
+from torch.profiler import profile, ProfilerActivity
+import collections
+for name, fn in (("tn", lambda: B.gemm(1, jp, V, C)), ("nn", lambda: B.gemm(0, jp, C, V, alpha=-1.0, beta=1.0))):
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+    agg = collections.defaultdict(float)
+    for ev in prof.events():
+        if ev.device_type == torch.autograd.DeviceType.CUDA:
+            agg[ev.name[:60]] += ev.device_time_total / 3.0
+    print(name, {k: round(v, 1) for k, v in sorted(agg.items(), key=lambda x: -x[1])})

@@ -23,7 +23,7 @@ if sys.argv[1] == "build":
     obj = os.path.join(VBIN, f"{fname}_{name}.o")
     subprocess.check_call([B.NVCC] + B.NVCC_FLAGS + ["-I", B.CSRC] + defs + ["-c", src, "-o", obj])
     lib = os.path.join(VBIN, f"librsvd_{name}.so")
-    subprocess.check_call([B.NVCC] + B.ARCH + ["-shared", "-o", lib, obj] + objs + ["-lcudart", "-lcuda"])
+    subprocess.check_call([B.NVCC] + B.ARCH + ["-shared", "-o", lib, obj] + objs + ["-lcudart", "-lcuda", "-ldl"])
     print("built", lib)
 else:
     from paper_1504_05477_b200 import _lib
