@@ -263,6 +263,8 @@ OZ_PROJECTIONS = os.environ.get("RSVD_OZ_PROJ", "1") != "0"
 # Reference-faithful basis: the power chain and the final orthonormalization
 # on two streams (RSVD_OVERLAP_FINAL=0: one stream, for A/B measurement).
 OVERLAP_FINAL = os.environ.get("RSVD_OVERLAP_FINAL", "1") != "0"
+# Projections against Qp inside the second deflation round (see orth_block).
+ROUND2_QP_PASSES = int(os.environ.get("RSVD_ROUND2_QP_PASSES", "1"))
 
 
 def proj_passes(dtype):
@@ -350,12 +352,22 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
             ops.gemm_nn(Q1, _cast_small(ops, T, dtype, out=T32, pred=r1), tmp, pred=r1)
             ops.convert(tmp, Q1, pred=r1)
             ops.mask_cols(V, mask, pred=r1)  # keep only the rejected columns' residuals
-            if has_prev:
-                project_out(ops, comm, Qp, V, tmp_c, pred=r1, basis=basis)
-            project_out(ops, comm, Q1, V, c2, pred=r1)
-            if has_prev:
-                project_out(ops, comm, Qp, V, tmp_c, pred=r1, basis=basis)
-            project_out(ops, comm, Q1, V, c2, pred=r1)
+            # the residuals were projected against Qp once before round 1: two
+            # passes against Q1 around one more against Qp give each of them the
+            # reference's two Gram-Schmidt passes (factor.py:93-98) against every
+            # earlier column (RSVD_ROUND2_QP_PASSES=2: the previous Qp, Q1, Qp, Q1)
+            if ROUND2_QP_PASSES == 1:
+                project_out(ops, comm, Q1, V, c2, pred=r1)
+                if has_prev:
+                    project_out(ops, comm, Qp, V, tmp_c, pred=r1, basis=basis)
+                project_out(ops, comm, Q1, V, c2, pred=r1)
+            else:
+                if has_prev:
+                    project_out(ops, comm, Qp, V, tmp_c, pred=r1, basis=basis)
+                project_out(ops, comm, Q1, V, c2, pred=r1)
+                if has_prev:
+                    project_out(ops, comm, Qp, V, tmp_c, pred=r1, basis=basis)
+                project_out(ops, comm, Q1, V, c2, pred=r1)
             ops.gram(V, G, pred=r1)
             comm.allreduce(G)
             ref = ref2 if ref2 is not None else ws.ref_orig[:p]
