@@ -13,6 +13,9 @@
 #include <math.h>
 #include <stdint.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 /* SplitMix64 finaliser — follows _kernels.pyx:22-28. */
 static inline uint64_t splitmix_final(uint64_t z) {
@@ -58,11 +61,15 @@ void oracle_mm(int64_t m, int64_t kk, int64_t n, const double *a,
         }
 }
 
-/* CSR times dense, storage-order accumulation — _kernels.pyx:74-92. */
+/* CSR times dense, storage-order accumulation — _kernels.pyx:74-92.
+ * Rows are independent, so they are split over OpenMP threads: every output
+ * element is summed in the reference's order (bitwise identical to the
+ * serial loop). */
 void oracle_spmm_nt(int64_t nrows, int64_t m, const int64_t *indptr,
                     const int64_t *col, const double *val, const double *b,
                     double *out) {
     memset(out, 0, sizeof(double) * (size_t)(nrows * m));
+#pragma omp parallel for schedule(dynamic, 256)
     for (int64_t i = 0; i < nrows; ++i)
         for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
             double v = val[e];
@@ -72,18 +79,31 @@ void oracle_spmm_nt(int64_t nrows, int64_t m, const int64_t *indptr,
         }
 }
 
-/* CSR-transpose times dense, row-order scatter — _kernels.pyx:95-113. */
+/* CSR-transpose times dense, row-order scatter — _kernels.pyx:95-113.
+ * Each OpenMP thread owns a slice of the m output columns and runs the
+ * reference's full (i, e) scatter over it, so every output element still
+ * accumulates its terms in row order (bitwise identical to the serial loop). */
 void oracle_spmm_t(int64_t nrows, int64_t ncols, int64_t m,
                    const int64_t *indptr, const int64_t *col,
                    const double *val, const double *b, double *out) {
     memset(out, 0, sizeof(double) * (size_t)(ncols * m));
-    for (int64_t i = 0; i < nrows; ++i)
-        for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
-            double v = val[e];
-            const double *brow = b + i * m;
-            double *orow = out + col[e] * m;
-            for (int64_t j = 0; j < m; ++j) orow[j] += v * brow[j];
-        }
+#pragma omp parallel
+    {
+        int64_t nt = 1, t = 0;
+#ifdef _OPENMP
+        nt = omp_get_num_threads();
+        t = omp_get_thread_num();
+#endif
+        int64_t j0 = m * t / nt, j1 = m * (t + 1) / nt;
+        if (j1 > j0)
+            for (int64_t i = 0; i < nrows; ++i)
+                for (int64_t e = indptr[i]; e < indptr[i + 1]; ++e) {
+                    double v = val[e];
+                    const double *brow = b + i * m;
+                    double *orow = out + col[e] * m;
+                    for (int64_t j = j0; j < j1; ++j) orow[j] += v * brow[j];
+                }
+    }
 }
 
 static double offdiag_mass(int64_t n, const double *a) {

@@ -31,13 +31,14 @@ _lib = None
 
 
 def build(force=False):
-    """Compile kernels_oracle.c with the reference's flags (setup.py:15-19)."""
+    """Compile kernels_oracle.c with the reference's flags (setup.py:15-19),
+    plus -fopenmp for the row/column-sliced CSR loops (bitwise identical)."""
     src = os.path.join(_HERE, "kernels_oracle.c")
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
         import subprocess
 
         subprocess.check_call(
-            ["gcc", "-O3", "-ffp-contract=off", "-fno-builtin-sin", "-fno-builtin-cos",
+            ["gcc", "-O3", "-ffp-contract=off", "-fno-builtin-sin", "-fno-builtin-cos", "-fopenmp",
              "-shared", "-fPIC", "-o", _LIB_PATH, src, "-lm"]
         )
     return _LIB_PATH
