@@ -594,7 +594,7 @@ def run_ours(args):
                   if op.hot is not None else "CSR SpMM A.X / A^T.Y (width %d)") % cfg.p)
     elif mode == "exact":
         kname = ("FP64-accurate Krylov-chain A.X / A^T.Y (width %d): k_oz_gemm, int8 tcgen05 Ozaki digit planes "
-                 "(6 A x 7 B digits, 27 digit-pair GEMMs)" % cfg.p)
+                 "(5 A x 6 B signed base-256 digits, 20 digit-pair GEMMs)" % cfg.p)
     else:
         kname = "Krylov-chain A.X / A^T.Y (width %d)" % cfg.p
     traffic = None if sparse else _profiled_traffic(args.config, mode)
@@ -603,14 +603,14 @@ def run_ours(args):
                     "frac": achieved / hbm, "peak_source": peak_src, "traffic": traffic,
                     "algorithmic_bytes_per_launch": bytes_per, "avg_launch_ms": avg_chain_ms}
         if mode == "exact":
-            # what the kernel actually streams: the 6 digit planes of A (1.5x the
-            # FP32 bytes) and the int8 MMA work (27 digit pairs, N padded to 64)
-            planes = 6 * (-(-n_loc // 128) * 128) * (-(-d // 128) * 128)
+            # what the kernel actually streams: the 5 digit planes of A (1.25x the
+            # FP32 bytes) and the int8 MMA work (20 digit pairs, N padded to 64)
+            planes = 5 * (-(-n_loc // 128) * 128) * (-(-d // 128) * 128)
             roofline["digit_plane_bytes_per_launch"] = planes
             roofline["digit_plane_gbs"] = planes / (avg_chain_ms * 1e-3) / 1e9
-            roofline["int8_tops"] = 27 * 2.0 * n_loc * d * 64 * (-(-cfg.p // 64)) / (avg_chain_ms * 1e-3) / 1e12
+            roofline["int8_tops"] = 20 * 2.0 * n_loc * d * 64 * (-(-cfg.p // 64)) / (avg_chain_ms * 1e-3) / 1e12
             roofline["note"] = ("algorithmic bytes = FP32 A + FP64 blocks; the kernel streams A's int8 digit "
-                                "planes (digit_plane_gbs) and is co-limited by the int8 MMA issue (27 digit pairs)")
+                                "planes (digit_plane_gbs) and is co-limited by the int8 MMA issue (20 digit pairs)")
             px = _peaks_extra()
             if px and px.get("int8_tops"):
                 roofline["int8_peak_tops"] = px["int8_tops"]

@@ -96,13 +96,13 @@ int rsvd_gemm_tn(int dtype, int out_dtype, int64_t m, int64_t n, int64_t k, doub
  * matrix.py:80) at FP64-class accuracy (~1e-16 relative) from kind::i8
  * tcgen05 MMAs with exact int32 sums.
  * rsvd_oz_prepare cuts A (n x d FP32, row pitch lda) ONCE into
- *   rsvd_oz_num_planes() signed 7-bit digit planes (column-blocked layout
- *   planes[i][c / 32][r][c % 32], rsvd_oz_planes_bytes(n, d) bytes in all)
+ *   rsvd_oz_num_planes() signed base-256 digit planes (int8; column-blocked
+ *   layout planes[i][c / 16][r][c % 16], rsvd_oz_planes_bytes(n, d) bytes in all)
  *   and per-row exponents row_exp[n]; the caller owns both buffers.
  * rsvd_oz_gemm trans = 0: C (n x p) = alpha A X + beta C  (X d x p FP64)
  *              trans = 1: C (d x p) = alpha A^T Y + beta C (Y n x p FP64)
- *   (+2: reduced accuracy, ~3e-11 relative instead of ~5e-15: digit levels
- *   i + j <= 4, 15 instead of 27 digit-pair GEMMs; the Rayleigh-Ritz W = A^T Q)
+ *   (+2: reduced accuracy, ~1e-10 relative instead of ~1e-14: digit levels
+ *   i + j <= 3, 10 instead of 20 digit-pair GEMMs; the Rayleigh-Ritz W = A^T Q)
  *   C is FP64; workspace from rsvd_oz_gemm_ws_bytes(trans & 1, n, d, p). */
 int64_t rsvd_oz_planes_bytes(int64_t n, int64_t d);
 int rsvd_oz_num_planes(void);

@@ -9,24 +9,32 @@
 // decisions). 3xTF32 gives ~1e-7; FP64 DMMA gives 1e-16 at ~37 TFLOP/s.
 //
 // Scheme (per product D = A X, A FP32 n x d held in HBM as slices):
-//   * every row r of A is scaled by 2^-E_r (2^E_r > 2 max_c |A[r,c]|) and cut
-//     into SA = 6 balanced base-128 digits: A[r,c] = 2^E_r sum_i a_i[r,c]
-//     2^-7(i+1), a_i in [-64, 64] (round to nearest; exact for every entry >=
-//     2^-17 of the row maximum since FP32 carries 24 bits, 2^-43 below);
-//   * every column c of the FP64 operand X likewise into SB = 7 digits with
-//     its own exponent F_c (2^-50 relative to the column maximum);
-//   * D = 2^(E_r + F_c - 14) sum_{i+j <= 6} 2^-7(i+j) (a_i x_j): 27 int8 GEMMs
-//     whose int32 sums are EXACT (|digit products| <= 2^12, at most 6 pairs
-//     per level, K <= 65536 per CTA keeps every level below 2^31); the levels
-//     are combined in FP64 in the epilogue. Neglected terms are ~2^-56 of
-//     |A||X| per entry: FP64-class accuracy (tests: ~1e-16 vs cuBLAS DGEMM).
+//   * every row r of A is scaled by 2^-E_r (2^E_r > ~2 max_c |A[r,c]|), rounded
+//     to a 40-bit integer N = rint(A[r,c] 2^(40 - E_r)) and written as SA = 5
+//     signed base-256 digits: N = sum_i a_i 256^(4-i), a_i in [-128, 127]
+//     (the bytes of (N + B) ^ B with B = 0x8080808080: adding 128 at every
+//     byte position turns balanced digits into plain bytes). Exact for every
+//     entry >= 2^-15 of the row maximum (FP32 carries 24 bits), rounded at
+//     2^-41 of the row scale below that;
+//   * every column c of the FP64 operand X likewise into SB = 6 digits (48
+//     bits) with its own exponent F_c;
+//   * D = 2^(E_r + F_c - 16) sum_{i+j <= 5} 2^-8(i+j) (a_i x_j): 20 int8 GEMMs
+//     whose int32 sums are EXACT (|digit products| <= 2^14, at most 7 pairs
+//     per level, K <= 16384 per CTA keeps every level below 2^31); the levels
+//     are combined in FP64 in the epilogue. Neglected terms are ~2^-49 of
+//     (row scale x column scale) per entry: FP64-class accuracy.
+//     (Round 2 first used base-128 digits in [-64, 64] -- 6 x 7 digits, 27
+//     GEMMs; a round-to-nearest base-256 digit can be +128, which int8 cannot
+//     hold. Rounding to an integer first and taking its signed base-256 digits
+//     from the least significant end keeps every digit in [-128, 127]: 26 %
+//     fewer MMAs and 17 % fewer plane bytes at the same dropped-term size.)
 //   * A^T Y uses the same row-scaled slices: A^T Y = sum_r (2^-E_r A[r,:])^T
 //     (2^E_r Y[r,:]); the row scale is folded into Y before it is sliced, so
 //     the A operand is read in place as an MN-major int8 tile.
 // Per K = 32 step one A digit plane i multiplies the stacked digit planes
-// [x_0 | x_1 | ... | x_(6-i)] (N = (7-i) BN, split into <= 256-column MMAs)
-// into TMEM columns [i BN, 7 BN): level L = i + j accumulates at column L BN
-// without any per-pair bookkeeping. TMEM holds all 7 levels (448 columns at
+// [x_0 | x_1 | ... | x_(5-i)] (N = (6-i) BN, split into <= 256-column MMAs)
+// into TMEM columns [i BN, 6 BN): level L = i + j accumulates at column L BN
+// without any per-pair bookkeeping. TMEM holds all 6 levels (384 columns at
 // BN = 64) for the whole K range of the CTA; the epilogue reads them once.
 #include <cuda.h>
 
@@ -42,16 +50,21 @@ namespace {
 
 constexpr int OZ_BM = 128;
 constexpr int OZ_KS = 32;        // int8 K per MMA = bytes per smem tile row
-constexpr int OZ_SA = 6;         // digit planes of an FP32 A (24-bit mantissas)
-constexpr int OZ_SQ = 7;         // digit planes of an FP64 orthonormal basis (global scale 2^1)
-constexpr int OZ_LV_A = 7;       // A products: kept levels i + j <= 6, 7 B digits
-constexpr int OZ_LV_Q = 8;       // basis products: levels i + j <= 7, 8 B digits (512 TMEM columns at BN 64)
-constexpr int OZ_LV_R = 5;       // reduced A products (levels i + j <= 4, A digits 0..4, 15 pairs): ~3e-11
+constexpr int OZ_DB = 8;         // bits per digit (signed base-256 digits in [-128, 127])
+constexpr int OZ_SA = 5;         // digit planes of an FP32 A (24-bit mantissas, 40 bits below the row scale)
+#ifndef RSVD_OZ_SQ
+#define RSVD_OZ_SQ 7
+#endif
+constexpr int OZ_SQ = RSVD_OZ_SQ;  // digit planes of an FP64 orthonormal basis (56 bits: every FP64 bit of
+                                 // entries down to 2^-3 of the column maximum)
+constexpr int OZ_LV_A = 6;       // A products: kept levels i + j <= 5, 6 B digits (20 pairs)
+constexpr int OZ_LV_Q = 7;       // basis products: levels i + j <= 6, 7 B digits (448 TMEM columns at BN 64)
+constexpr int OZ_LV_R = 4;       // reduced A products (levels i + j <= 3, A digits 0..3, 10 pairs): ~1e-10
                                  // relative, for the Rayleigh-Ritz W = A^T Q (its error enters sigma^2
                                  // linearly, against the chain's 1e-15 amplified ~1e9 by the basis)
-constexpr int OZ_SB_MAX = 8;
+constexpr int OZ_SB_MAX = 7;
 constexpr int OZ_STAGES = 5;
-constexpr int64_t OZ_MAX_K = 65536;  // int32 exactness: 6 pairs x 64^2 x 65536 < 2^31
+constexpr int64_t OZ_MAX_K = 16384;  // int32 exactness: 7 pairs x 128^2 x 16384 < 2^31
 constexpr int OZ_THREADS = 10 * 32;  // 0 TMA, 1 MMA, 2..9 epilogue (two warps per TMEM lane quarter)
 constexpr uint32_t kLayoutNone = 0;
 
@@ -266,7 +279,7 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         if (warp == 2 && lane == 0) OZ_STAMP(2);
         int ea = 0;
         if (p.ea && row < p.M) ea = p.ea[row];
-        // per-column scale 2^(ea + fb - 14) as an exact power-of-two multiply
+        // per-column scale 2^(ea + fb - 16) as an exact power-of-two multiply
         // (ldexp's general path, 64 calls per thread, was a large part of a
         // ~20 us per-CTA epilogue), with ldexp kept for exponents outside the
         // normal range
@@ -274,62 +287,47 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             return (e > -1022 && e < 1023) ? __longlong_as_double((long long)(e + 1023) << 52) : 0.0;
         };
         // The epilogue is latency-bound (one warp per SM sub-partition): the
-        // levels are combined in 64-bit integer arithmetic -- hi = sum_{L<4}
-        // acc_L 2^7(3-L), lo = sum_{L>=4} acc_L 2^7(LV-1-L), each < 2^53 so its
-        // conversion is exact -- and v = hi 2^-21 + lo 2^-7(LV-1): two int->FP64
-        // conversions and one FMA per output instead of LV of each (the Horner
-        // form made the epilogue ~14-16 us per CTA, 20 % of a chain product).
-        constexpr int LH = LV < 4 ? LV : 4;
-        const double lo_w = ldexp(1.0, -7 * (LV - 1));
+        // levels are combined in 64-bit integer arithmetic, three at a time --
+        // g = acc_L 2^16 + acc_(L+1) 2^8 + acc_(L+2), below 2^48 so its conversion
+        // is exact -- and the groups summed from the least significant up with
+        // one FMA each: one int->FP64 conversion per three levels instead of
+        // one per level (the Horner form made the epilogue ~14-16 us per CTA,
+        // 20 % of a chain product).
+        constexpr int NG = (LV + 2) / 3;
+        auto pow2 = [](int e) -> double { return __longlong_as_double((long long)(e + 1023) << 52); };
         double sc[16];
         // two epilogue warps per lane quarter, each drains half of the columns
         const int half = (warp - 2) / 4;
 #pragma unroll 1
         for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 16) {
             double v[16];
-            if (nks > 0) {
-                int64_t hi[16], lo[16];
-                {
-                    int32_t a[LH][16];
 #pragma unroll
-                    for (int L = 0; L < LH; ++L) tmem_ld16_s32(tmem_base + lane_off + (uint32_t)(L * BN + c0), a[L]);
+            for (int t = 0; t < 16; ++t) v[t] = 0.0;
+            if (nks > 0) {
+#pragma unroll
+                for (int g = NG - 1; g >= 0; --g) {
+                    const int L0 = 3 * g;
+                    const int L1 = L0 + 3 < LV ? L0 + 3 : LV;
+                    int32_t a[3][16];
+#pragma unroll
+                    for (int L = 0; L < 3; ++L)
+                        if (L0 + L < L1) tmem_ld16_s32(tmem_base + lane_off + (uint32_t)((L0 + L) * BN + c0), a[L]);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    const double wg = pow2(-OZ_DB * (L1 - 1));
 #pragma unroll
                     for (int t = 0; t < 16; ++t) {
                         int64_t h = 0;
 #pragma unroll
-                        for (int L = 0; L < LH; ++L) h = h * 128 + a[L][t];
-                        hi[t] = h;
+                        for (int L = 0; L < 3; ++L)
+                            if (L0 + L < L1) h = h * (1 << OZ_DB) + a[L][t];
+                        v[t] = fma((double)h, wg, v[t]);
                     }
                 }
-                if constexpr (LV > 4) {
-                    int32_t a[LV - 4][16];
-#pragma unroll
-                    for (int L = 4; L < LV; ++L)
-                        tmem_ld16_s32(tmem_base + lane_off + (uint32_t)(L * BN + c0), a[L - 4]);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-                    for (int t = 0; t < 16; ++t) {
-                        int64_t l = 0;
-#pragma unroll
-                        for (int L = 0; L < LV - 4; ++L) l = l * 128 + a[L][t];
-                        lo[t] = l;
-                    }
-                } else {
-#pragma unroll
-                    for (int t = 0; t < 16; ++t) lo[t] = 0;
-                }
-                const double hi_w = ldexp(1.0, -7 * (LH - 1));
-#pragma unroll
-                for (int t = 0; t < 16; ++t) v[t] = fma((double)lo[t], lo_w, (double)hi[t] * hi_w);
-            } else {
-#pragma unroll
-                for (int t = 0; t < 16; ++t) v[t] = 0.0;
             }
 #pragma unroll
             for (int t = 0; t < 16; ++t) {
                 const int64_t col = n0 + c0 + t;
-                sc[t] = col < p.N ? scale_of(ea + p.fb[col] - 14) : 0.0;
+                sc[t] = col < p.N ? scale_of(ea + p.fb[col] - 2 * OZ_DB) : 0.0;
             }
             if (row < p.M) {
                 const int64_t base = p.direct ? row * p.ldc + n0 + c0 : ((int64_t)blockIdx.z * p.M + row) * p.ldw + n0 + c0;
@@ -352,7 +350,7 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 double res[16];
 #pragma unroll
                 for (int t = 0; t < 16; ++t) {
-                    const double val = sc[t] != 0.0 ? v[t] * sc[t] : ldexp(v[t], ea + p.fb[min(n0 + c0 + t, p.N - 1)] - 14);
+                    const double val = sc[t] != 0.0 ? v[t] * sc[t] : ldexp(v[t], ea + p.fb[min(n0 + c0 + t, p.N - 1)] - 2 * OZ_DB);
                     res[t] = p.direct ? (rmw ? p.alpha * val + p.beta * cin[t] : p.alpha * val) : val;
                 }
                 if (full16) {
@@ -377,22 +375,32 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 }
 
 // ---------------------------------------------------------------- slicing
-__device__ __forceinline__ int exp_above(double m) {
-    // smallest E with 2^E > m (m > 0): frexp gives m = f 2^e, f in [0.5, 1)
+// Scale exponent of a row / column with maximum magnitude m > 0: the smallest
+// E with m 2^-E <= 0.498, so that N = rint(x 2^(8 S - E)) has S signed
+// base-256 digits in [-128, 127] (|N| <= 127 (256^S - 1) / 255 = 0.49804 256^S).
+__device__ __forceinline__ int oz_exp_for(double m) {
     int e;
-    frexp(m, &e);
-    return e;
+    const double f = frexp(m, &e);  // m = f 2^e, f in [0.5, 1)
+    const int E = f > 0.996 ? e + 2 : e + 1;
+    return E < -960 ? -960 : E;  // keeps 2^(8 S - E) finite (columns below 1e-289 lose digits, not range)
 }
 
-// Balanced base-128 digits of u in (-1/2, 1/2): t = 128 u; a_i = rint(t) in [-64, 64];
-// t = 128 (t - a_i). Exact in FP32 for FP32 input (t keeps <= 24 significant bits;
-// removing the nearest integer and scaling by 2^7 are exact). Round-to-nearest
-// digits leave zero-mean remainders (truncation would bias every dropped term
-// towards the sign of the product) and keep |a_i x_j| <= 2^12.
-__device__ __forceinline__ uint32_t pack4(const int (&q)[4]) {
-    return (uint32_t)(q[0] & 0xFF) | ((uint32_t)(q[1] & 0xFF) << 8) | ((uint32_t)(q[2] & 0xFF) << 16) |
-           ((uint32_t)(q[3] & 0xFF) << 24);
+// Signed base-256 digits of an integer N (least significant first: d = the
+// sign-extended low byte, N = (N - d) / 256) are the bytes of (N + B) ^ B with
+// B = 0x80...80: adding 128 at every digit position maps the digits to plain
+// bytes, the XOR maps each byte back to two's complement. Digit i (0 = most
+// significant of S) is byte S - 1 - i. Rounding x to the integer N first
+// (round to nearest, zero-mean remainder) is what keeps every digit inside
+// int8: rounding digit by digit from the top would need +128.
+template <int S>
+__device__ __forceinline__ unsigned long long oz_digits(long long N) {
+    unsigned long long B = 0;
+#pragma unroll
+    for (int i = 0; i < S; ++i) B |= 0x80ull << (8 * i);
+    return ((unsigned long long)N + B) ^ B;
 }
+
+__device__ __forceinline__ uint32_t oz_byte(unsigned long long M, int k) { return (uint32_t)(M >> (8 * k)) & 0xFFu; }
 
 // Digit planes of A in the column-blocked layout planes[i][c / 16][r][c % 16]
 // over n_pad x d_pad (both multiples of 128; padding written as zeros): a
@@ -403,7 +411,7 @@ __device__ __forceinline__ uint32_t pack4(const int (&q)[4]) {
 __global__ void __launch_bounds__(256) k_oz_slice_a(int64_t n, int64_t d, const float* __restrict__ A, int64_t lda,
                                                     int64_t n_pad, int64_t d_pad, int8_t* __restrict__ planes,
                                                     int32_t* __restrict__ row_exp) {
-    __shared__ float s_scale[32];
+    __shared__ double s_scale[32];
     const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
     const int64_t r0 = (int64_t)blockIdx.x * 32;
     const bool vec = (lda % 4 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
@@ -421,17 +429,16 @@ __global__ void __launch_bounds__(256) k_oz_slice_a(int64_t n, int64_t d, const 
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        // one spare bit: |u| < 1/2, so every balanced digit rint(.) is in [-64, 64]
-        const int E = m > 0.f ? exp_above((double)m) + 1 : 0;
+        const int E = m > 0.f ? oz_exp_for((double)m) : 0;
         if (lane == 0) {
             if (r < n) row_exp[r] = E;
-            s_scale[rr] = ldexpf(1.0f, -E);
+            s_scale[rr] = ldexp(1.0, OZ_DB * OZ_SA - E);  // FP64: 2^(40 - E) overflows FP32 for tiny rows
         }
     }
     __syncthreads();
     const int64_t r = r0 + lane;
     const bool live = r < n;
-    const float sc = s_scale[lane] * 128.0f;
+    const double sc = s_scale[lane];
     const float* a = A + (live ? r : 0) * lda;
     const int64_t pp = n_pad * d_pad;  // plane pitch
     const bool vrow = vec && live;
@@ -447,23 +454,17 @@ __global__ void __launch_bounds__(256) k_oz_slice_a(int64_t n, int64_t d, const 
 #pragma unroll
             for (int t = 0; t < 16; ++t) x[t] = (live && b * 16 + t < d) ? a[b * 16 + t] : 0.f;
         }
+        unsigned long long M[16];
 #pragma unroll
-        for (int t = 0; t < 16; ++t) x[t] *= sc;
+        for (int t = 0; t < 16; ++t) M[t] = oz_digits<OZ_SA>(__double2ll_rn((double)x[t] * sc));
         int8_t* out = planes + (b * n_pad + r) * 16;
 #pragma unroll
         for (int i = 0; i < OZ_SA; ++i) {
             uint32_t w[4];
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-                int q[4];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const float tr = rintf(x[4 * q4 + t]);
-                    q[t] = (int)tr;
-                    x[4 * q4 + t] = (x[4 * q4 + t] - tr) * 128.0f;
-                }
-                w[q4] = pack4(q);
-            }
+            for (int q4 = 0; q4 < 4; ++q4)
+                w[q4] = oz_byte(M[4 * q4], OZ_SA - 1 - i) | (oz_byte(M[4 * q4 + 1], OZ_SA - 1 - i) << 8) |
+                        (oz_byte(M[4 * q4 + 2], OZ_SA - 1 - i) << 16) | (oz_byte(M[4 * q4 + 3], OZ_SA - 1 - i) << 24);
             *reinterpret_cast<uint4*>(out + i * pp) = make_uint4(w[0], w[1], w[2], w[3]);
         }
     }
@@ -480,19 +481,14 @@ __global__ void __launch_bounds__(256) k_oz_slice_cols(int64_t n, const double* 
     if (r >= n_pad) return;
     const int64_t b = c0 / 16 + blockIdx.y;
     const int64_t pp = n_pad * w_pad;
-    int q[OZ_SQ][16];
+    unsigned long long M[16];
     bool mine[16];
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
         const int64_t c = b * 16 + t;
         mine[t] = c >= c0 && c < c0 + ncols;
-        double x = (mine[t] && r < n) ? ldexp(Q[r * ldq + c], 7 - col_exp[c]) : 0.0;  // 128 u, u = q 2^-E
-#pragma unroll
-        for (int i = 0; i < OZ_SQ; ++i) {
-            const double tr = rint(x);
-            q[i][t] = (int)tr;
-            x = (x - tr) * 128.0;
-        }
+        const double x = (mine[t] && r < n) ? ldexp(Q[r * ldq + c], OZ_DB * OZ_SQ - col_exp[c]) : 0.0;
+        M[t] = oz_digits<OZ_SQ>(__double2ll_rn(x));
     }
 #pragma unroll
     for (int i = 0; i < OZ_SQ; ++i) {
@@ -503,7 +499,7 @@ __global__ void __launch_bounds__(256) k_oz_slice_cols(int64_t n, const double* 
         for (int t = 0; t < 16; ++t)
             if (mine[t]) {
                 const int sh = (t % 4) * 8;
-                wv[t / 4] = (wv[t / 4] & ~(0xFFu << sh)) | ((uint32_t)(q[i][t] & 0xFF) << sh);
+                wv[t / 4] = (wv[t / 4] & ~(0xFFu << sh)) | (oz_byte(M[t], OZ_SQ - 1 - i) << sh);
             }
         *dst = make_uint4(wv[0], wv[1], wv[2], wv[3]);
     }
@@ -539,7 +535,7 @@ __global__ void k_oz_col_exp(int64_t N, const unsigned long long* __restrict__ c
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= N) return;
     const double m = __longlong_as_double((long long)colmax[c]);
-    fb[c] = m > 0.0 ? exp_above(m) + 1 : 0;  // |u| < 1/2: balanced digits in [-64, 64]
+    fb[c] = m > 0.0 ? oz_exp_for(m) : 0;
 }
 
 // Pass 2: transposed digit planes in the k-blocked layout
@@ -562,11 +558,11 @@ __global__ void __launch_bounds__(256) k_oz_slice_b(int64_t K, int64_t N, const 
     int f = 0;
     if (col < N) {
         const double m = __longlong_as_double((long long)colmax[col]);
-        f = m > 0.0 ? exp_above(m) + 1 : 0;  // |u| < 1/2: balanced digits in [-64, 64]
+        f = m > 0.0 ? oz_exp_for(m) : 0;
         if (blockIdx.x == 0 && ty == 0) fb[col] = f;
     }
-    const double sc = col < N ? ldexp(1.0, -f) : 0.0;
-    int q[SB][4];
+    const double sc = col < N ? ldexp(1.0, OZ_DB * SB - f) : 0.0;
+    unsigned long long M[4];
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
         const int64_t k = k0 + 4 * ty + t;
@@ -576,16 +572,12 @@ __global__ void __launch_bounds__(256) k_oz_slice_b(int64_t K, int64_t N, const 
             if (ek) u = ldexp(u, ek[k]);
             u *= sc;
         }
-        double x = u * 128.0;
-#pragma unroll
-        for (int j = 0; j < SB; ++j) {
-            const double tr = rint(x);
-            q[j][t] = (int)tr;
-            x = (x - tr) * 128.0;
-        }
+        M[t] = oz_digits<SB>(__double2ll_rn(u));
     }
 #pragma unroll
-    for (int j = 0; j < SB; ++j) tile[j][tx][ty] = pack4(q[j]);
+    for (int j = 0; j < SB; ++j)
+        tile[j][tx][ty] = oz_byte(M[0], SB - 1 - j) | (oz_byte(M[1], SB - 1 - j) << 8) |
+                          (oz_byte(M[2], SB - 1 - j) << 16) | (oz_byte(M[3], SB - 1 - j) << 24);
     __syncthreads();
     // store: rows c = c0 + (warp), 8 words of 4 k each per (plane, row)
     for (int e = threadIdx.x; e < SB * 32 * 8; e += blockDim.x) {

@@ -147,7 +147,7 @@ def gemm_tn(A, B, C, alpha=1.0, beta=0.0, mu=None, colsum_b=None, algo=GEMM_AUTO
 
 
 class OzPlanes:
-    """FP32 A cut once into signed 7-bit digit planes + per-row exponents for
+    """FP32 A cut once into signed base-256 digit planes (int8) + per-row exponents for
     the FP64-accurate int8 tensor-core products (csrc/gemm_oz.cu)."""
 
     def __init__(self, A):
@@ -168,8 +168,8 @@ class OzPlanes:
 
 def oz_gemm(P, B, C, trans, alpha=1.0, beta=0.0, pred=None, reduced=False):
     """trans=0: C (n x p) = alpha A B + beta C; trans=1: C (d x p) = alpha A^T B
-    + beta C; A given by its digit planes P, B and C FP64. ``reduced``: ~3e-11
-    relative accuracy (15 digit-pair GEMMs instead of 27)."""
+    + beta C; A given by its digit planes P, B and C FP64. ``reduced``: ~1e-10
+    relative accuracy (10 digit-pair GEMMs instead of 20)."""
     assert B.dtype == torch.float64 and C.dtype == torch.float64
     p = B.shape[1]
     assert B.shape[0] == (P.n if trans else P.d) and C.shape == ((P.d if trans else P.n), p), (B.shape, C.shape)
