@@ -99,7 +99,7 @@ struct OzParams {
     double* ws;
     int64_t ldw;
     const int32_t* pred;
-    int n_tiles;
+    int n_tiles, m_tiles, splits;
     int ablate;              // profiling ablations (RSVD_OZ_ABLATE): 1 no B loads, 2 no A loads, 4 no MMAs
 };
 
@@ -160,14 +160,28 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     uint64_t* full = bars;
     uint64_t* empty = bars + OZ_STAGES;
     uint64_t* acc_full = bars + 2 * OZ_STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+    uint64_t* tmem_empty = bars + 2 * OZ_STAGES + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int64_t m0 = (int64_t)(blockIdx.x / p.n_tiles) * OZ_BM;
-    const int64_t n0 = (int64_t)(blockIdx.x % p.n_tiles) * BN;
-    const int64_t kbeg = (int64_t)blockIdx.z * p.k_per_split;
-    const int64_t kend = min(p.K, kbeg + p.k_per_split);
-    const int nks = kend > kbeg ? (int)((kend - kbeg + OZ_KS - 1) / OZ_KS) : 0;
+    // Persistent CTA: work units (split z, M tile, N tile) are taken round-robin,
+    // u = blockIdx.x, + gridDim.x, ... The producer runs ahead into the next
+    // unit while the epilogue drains the accumulators (one CTA per unit left
+    // the SM's loads idle for the epilogue, teardown, launch and setup of the
+    // next CTA: ~10 us against a ~45 us main loop at C2, which capped the
+    // plane stream at ~4.7 TB/s); the MMA issuer waits on tmem_empty, which the
+    // epilogue warps release as soon as their levels are combined in registers.
+    const int tiles = p.m_tiles * p.n_tiles;
+    const int units = tiles * p.splits;
+    auto unit_of = [&](int u, int64_t& m0, int64_t& n0, int& z, int64_t& kbeg, int& nks) {
+        z = u / tiles;
+        const int t = u - z * tiles;
+        m0 = (int64_t)(t / p.n_tiles) * OZ_BM;
+        n0 = (int64_t)(t % p.n_tiles) * BN;
+        kbeg = (int64_t)z * p.k_per_split;
+        const int64_t kend = min(p.K, kbeg + p.k_per_split);
+        nks = kend > kbeg ? (int)((kend - kbeg + OZ_KS - 1) / OZ_KS) : 0;
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < OZ_STAGES; ++s) {
@@ -175,6 +189,7 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             mbar_init(&empty[s], 1);
         }
         mbar_init(acc_full, 1);
+        mbar_init(tmem_empty, OZ_THREADS / 32 - 2);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         if (p.Np != BN) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -198,87 +213,92 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             // stage when a single N tile spans all Np rows.
             int s = 0;
             uint32_t ph = 0;
-            for (int kb = 0; kb < nks; ++kb) {
-                mbar_wait(&empty[s], ph ^ 1);
-                const int64_t kk = kbeg + (int64_t)kb * OZ_KS;
-                uint8_t* st = smem + s * Cfg::STAGE;
-                mbar_expect_tx(&full[s], Cfg::STAGE - ((p.ablate & 1) ? SB * Cfg::B_TILE : 0) -
-                                             ((p.ablate & 2) ? SA * Cfg::A_TILE : 0));
-                if (!(p.ablate & 2)) {
-                    // all SA digit planes of the tile in ONE TMA box (u64 view of the 16-byte
-                    // row pieces): NN 128 rows x 2 column blocks, TN 32 rows x 8 column blocks,
-                    // landing as [plane][block][row][16 B]. (Per-plane bulk copies -- 13 to 15
-                    // issues per K step from the one producer thread -- capped the short-K
-                    // basis products at ~2 TB/s.)
-                    if (!A_MN)
-                        tma_load_3d(&tmA, &full[s], st, (int)(m0 * 2), (int)(kk / 16), 0);
-                    else
-                        tma_load_3d(&tmA, &full[s], st, (int)(kk * 2), (int)(m0 / 16), 0);
+            for (int u = blockIdx.x; u < units; u += gridDim.x) {
+                int64_t m0, n0, kbeg;
+                int z, nks;
+                unit_of(u, m0, n0, z, kbeg, nks);
+                for (int kb = 0; kb < nks; ++kb) {
+                    mbar_wait(&empty[s], ph ^ 1);
+                    const int64_t kk = kbeg + (int64_t)kb * OZ_KS;
+                    uint8_t* st = smem + s * Cfg::STAGE;
+                    mbar_expect_tx(&full[s], Cfg::STAGE - ((p.ablate & 1) ? SB * Cfg::B_TILE : 0) -
+                                                 ((p.ablate & 2) ? SA * Cfg::A_TILE : 0));
+                    if (!(p.ablate & 2)) {
+                        // all SA digit planes of the tile in ONE TMA box (u64 view of the 16-byte
+                        // row pieces): NN 128 rows x 2 column blocks, TN 32 rows x 8 column blocks,
+                        // landing as [plane][block][row][16 B]. (Per-plane bulk copies -- 13 to 15
+                        // issues per K step from the one producer thread -- capped the short-K
+                        // basis products at ~2 TB/s.)
+                        if (!A_MN)
+                            tma_load_3d(&tmA, &full[s], st, (int)(m0 * 2), (int)(kk / 16), 0);
+                        else
+                            tma_load_3d(&tmA, &full[s], st, (int)(kk * 2), (int)(m0 / 16), 0);
+                    }
+                    if (!(p.ablate & 1)) {
+                        uint8_t* dst = st + SA * Cfg::A_TILE;
+                        if (p.Np == BN)  // the whole stage is one contiguous run
+                            bulk_g2s(dst, p.b_planes + (kk / OZ_KS) * 2 * SB * p.Np * 16, SB * Cfg::B_TILE,
+                                     &full[s]);
+                        else  // 2 SB runs of BN x 16 B: one TMA box
+                            tma_load_3d(&tmB, &full[s], dst, (int)(n0 * 4), 0, (int)(kk / OZ_KS));
+                    }
+                    if (++s == OZ_STAGES) { s = 0; ph ^= 1; }
                 }
-                if (!(p.ablate & 1)) {
-                    uint8_t* dst = st + SA * Cfg::A_TILE;
-                    if (p.Np == BN)  // the whole stage is one contiguous run
-                        bulk_g2s(dst, p.b_planes + (kk / OZ_KS) * 2 * SB * p.Np * 16, SB * Cfg::B_TILE,
-                                 &full[s]);
-                    else  // 14 runs of BN x 16 B: one TMA box
-                        tma_load_3d(&tmB, &full[s], dst, (int)(n0 * 4), 0, (int)(kk / OZ_KS));
-                }
-                if (++s == OZ_STAGES) { s = 0; ph ^= 1; }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer
             int s = 0;
-            uint32_t ph = 0;
-            for (int kb = 0; kb < nks; ++kb) {
-                mbar_wait(&full[s], ph);
+            uint32_t ph = 0, tph = 0;
+            for (int u = blockIdx.x; u < units; u += gridDim.x) {
+                int64_t m0, n0, kbeg;
+                int z, nks;
+                unit_of(u, m0, n0, z, kbeg, nks);
+                if (nks == 0) continue;
+                // the previous unit's accumulators have been read out
+                mbar_wait(tmem_empty, tph ^ 1);
+                tph ^= 1;
                 tc_fence_after();
-                const uint32_t st = smem_u32(smem + s * Cfg::STAGE);
-                const uint32_t bst = st + SA * Cfg::A_TILE;
+                for (int kb = 0; kb < nks; ++kb) {
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t st = smem_u32(smem + s * Cfg::STAGE);
+                    const uint32_t bst = st + SA * Cfg::A_TILE;
 #pragma unroll
-                for (int i = 0; i < SA; ++i) {
-                    // no-swizzle core matrices (8 rows x 16 B, 128 contiguous bytes):
-                    // K-major A [half][r][16 B]: 8-row groups SBO 128 B, K halves LBO 2 KB;
-                    // MN-major A [mb][k][16 B]: 16-column blocks SBO 512 B, 8-row K groups LBO 128 B
-                    const uint64_t da = A_MN ? make_desc(st + i * Cfg::A_TILE, 128, 512, kLayoutNone)
-                                             : make_desc(st + i * Cfg::A_TILE, 2048, 128, kLayoutNone);
-                    const int nj = LV - i;  // B digits j with i + j < LV
-                    const int rows = nj * BN;
+                    for (int i = 0; i < SA; ++i) {
+                        // no-swizzle core matrices (8 rows x 16 B, 128 contiguous bytes):
+                        // K-major A [half][r][16 B]: 8-row groups SBO 128 B, K halves LBO 2 KB;
+                        // MN-major A [mb][k][16 B]: 16-column blocks SBO 512 B, 8-row K groups LBO 128 B
+                        const uint64_t da = A_MN ? make_desc(st + i * Cfg::A_TILE, 128, 512, kLayoutNone)
+                                                 : make_desc(st + i * Cfg::A_TILE, 2048, 128, kLayoutNone);
+                        const int nj = LV - i;  // B digits j with i + j < LV
+                        const int rows = nj * BN;
 #pragma unroll
-                    for (int r0 = 0; r0 < SB * BN; r0 += 256) {
-                        if (r0 >= rows) break;
-                        const int nn = (rows - r0) < 256 ? (rows - r0) : 256;
-                        // B [half][j][c][16 B]: rows j BN + c, 8-row groups SBO 128 B, halves LBO
-                        const uint64_t db = make_desc(bst + r0 * 16, SB * BN * 16, 128, kLayoutNone);
-                        const uint32_t acc = (kb == 0 && i == 0) ? 0u : 1u;
-                        if (p.ablate & 4) continue;
-                        tc_mma_i8(tmem_base + (uint32_t)(i * BN + r0), da, db, oz_idesc(OZ_BM, nn, A_MN ? 1 : 0), acc);
+                        for (int r0 = 0; r0 < SB * BN; r0 += 256) {
+                            if (r0 >= rows) break;
+                            const int nn = (rows - r0) < 256 ? (rows - r0) : 256;
+                            // B [half][j][c][16 B]: rows j BN + c, 8-row groups SBO 128 B, halves LBO
+                            const uint64_t db = make_desc(bst + r0 * 16, SB * BN * 16, 128, kLayoutNone);
+                            const uint32_t acc = (kb == 0 && i == 0) ? 0u : 1u;
+                            if (p.ablate & 4) continue;
+                            tc_mma_i8(tmem_base + (uint32_t)(i * BN + r0), da, db, oz_idesc(OZ_BM, nn, A_MN ? 1 : 0),
+                                      acc);
+                        }
                     }
+                    tc_commit(&empty[s]);
+                    if (++s == OZ_STAGES) { s = 0; ph ^= 1; }
                 }
-                tc_commit(&empty[s]);
-                if (++s == OZ_STAGES) { s = 0; ph ^= 1; }
+                tc_commit(acc_full);
             }
-            tc_commit(acc_full);
         }
     } else {
         // ---------------- epilogue: thread = one output row (its TMEM lane)
         const int quarter = warp % 4;
-        const int64_t row = m0 + quarter * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-        if (p.direct && p.beta != 0.0 && row < p.M) {
-            // C is read back by the epilogue (beta != 0): pull this thread's row
-            // segment into L2 while the main loop runs
-            const int hf = (warp - 2) / 4;
-            for (int c = hf * (BN / 2); c < (hf + 1) * (BN / 2) && n0 + c < p.N; c += 16)
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(p.C + row * p.ldc + n0 + c));
-        }
-        if (nks > 0) {
-            mbar_wait(acc_full, 0);
-            tc_fence_after();
-        }
-        if (warp == 2 && lane == 0) OZ_STAMP(2);
-        int ea = 0;
-        if (p.ea && row < p.M) ea = p.ea[row];
+        // two epilogue warps per lane quarter, each drains half of the columns
+        const int half = (warp - 2) / 4;
+        constexpr int HC = BN / 2;      // columns per epilogue thread
+        constexpr int NCH = HC / 16;    // 16-column chunks
         // per-column scale 2^(ea + fb - 16) as an exact power-of-two multiply
         // (ldexp's general path, 64 calls per thread, was a large part of a
         // ~20 us per-CTA epilogue), with ldexp kept for exponents outside the
@@ -286,85 +306,123 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         auto scale_of = [&](int e) -> double {
             return (e > -1022 && e < 1023) ? __longlong_as_double((long long)(e + 1023) << 52) : 0.0;
         };
-        // The epilogue is latency-bound (one warp per SM sub-partition): the
-        // levels are combined in 64-bit integer arithmetic, three at a time --
-        // g = acc_L 2^16 + acc_(L+1) 2^8 + acc_(L+2), below 2^48 so its conversion
-        // is exact -- and the groups summed from the least significant up with
-        // one FMA each: one int->FP64 conversion per three levels instead of
-        // one per level (the Horner form made the epilogue ~14-16 us per CTA,
-        // 20 % of a chain product).
-        constexpr int NG = (LV + 2) / 3;
         auto pow2 = [](int e) -> double { return __longlong_as_double((long long)(e + 1023) << 52); };
-        double sc[16];
-        // two epilogue warps per lane quarter, each drains half of the columns
-        const int half = (warp - 2) / 4;
-#pragma unroll 1
-        for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 16) {
-            double v[16];
+        constexpr int NG = (LV + 2) / 3;
+        uint32_t aph = 0;
+        bool first = true;
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+            int64_t m0, n0, kbeg;
+            int z, nks;
+            unit_of(u, m0, n0, z, kbeg, nks);
+            const int64_t row = m0 + quarter * 32 + lane;
+            if (p.direct && p.beta != 0.0 && row < p.M) {
+                // C is read back by the epilogue (beta != 0): pull this thread's row
+                // segment into L2 while the main loop runs
+                for (int c = half * HC; c < (half + 1) * HC && n0 + c < p.N; c += 16)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(p.C + row * p.ldc + n0 + c));
+            }
+            int ea = 0;
+            if (p.ea && row < p.M) ea = p.ea[row];
+            // The epilogue is latency-bound (one warp per SM sub-partition): the
+            // levels are combined in 64-bit integer arithmetic, three at a time --
+            // g = acc_L 2^16 + acc_(L+1) 2^8 + acc_(L+2), below 2^48 so its conversion
+            // is exact -- and the groups summed from the least significant up with
+            // one FMA each: one int->FP64 conversion per three levels instead of
+            // one per level (the Horner form made the epilogue ~14-16 us per CTA,
+            // 20 % of a chain product). All of the thread's columns are combined
+            // before anything is stored, so that TMEM goes back to the MMA issuer
+            // after ~2 us and the stores overlap the next unit's main loop.
+            double v[NCH][16];
 #pragma unroll
-            for (int t = 0; t < 16; ++t) v[t] = 0.0;
+            for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+                for (int t = 0; t < 16; ++t) v[ch][t] = 0.0;
             if (nks > 0) {
+                mbar_wait(acc_full, aph);
+                aph ^= 1;
+                tc_fence_after();
+                if (first && warp == 2 && lane == 0) OZ_STAMP(2);
 #pragma unroll
-                for (int g = NG - 1; g >= 0; --g) {
-                    const int L0 = 3 * g;
-                    const int L1 = L0 + 3 < LV ? L0 + 3 : LV;
-                    int32_t a[3][16];
+                for (int ch = 0; ch < NCH; ++ch) {
+                    const int c0 = half * HC + ch * 16;
 #pragma unroll
-                    for (int L = 0; L < 3; ++L)
-                        if (L0 + L < L1) tmem_ld16_s32(tmem_base + lane_off + (uint32_t)((L0 + L) * BN + c0), a[L]);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    const double wg = pow2(-OZ_DB * (L1 - 1));
-#pragma unroll
-                    for (int t = 0; t < 16; ++t) {
-                        int64_t h = 0;
+                    for (int g = NG - 1; g >= 0; --g) {
+                        const int L0 = 3 * g;
+                        const int L1 = L0 + 3 < LV ? L0 + 3 : LV;
+                        int32_t a[3][16];
 #pragma unroll
                         for (int L = 0; L < 3; ++L)
-                            if (L0 + L < L1) h = h * (1 << OZ_DB) + a[L][t];
-                        v[t] = fma((double)h, wg, v[t]);
+                            if (L0 + L < L1)
+                                tmem_ld16_s32(tmem_base + lane_off + (uint32_t)((L0 + L) * BN + c0), a[L]);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        const double wg = pow2(-OZ_DB * (L1 - 1));
+#pragma unroll
+                        for (int t = 0; t < 16; ++t) {
+                            int64_t h = 0;
+#pragma unroll
+                            for (int L = 0; L < 3; ++L)
+                                if (L0 + L < L1) h = h * (1 << OZ_DB) + a[L][t];
+                            v[ch][t] = fma((double)h, wg, v[ch][t]);
+                        }
+                    }
+                }
+                // accumulators read: hand TMEM back
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tmem_empty);
+            }
+            // scale and store, 8 columns (64 bytes of the thread's row) at a time
+#pragma unroll
+            for (int c8 = 0; c8 < HC / 8; ++c8) {
+                const int c0 = half * HC + c8 * 8;
+                const double* vv = &v[c8 / 2][(c8 % 2) * 8];
+                double sc[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    const int64_t col = n0 + c0 + t;
+                    sc[t] = col < p.N ? scale_of(ea + p.fb[col] - 2 * OZ_DB) : 0.0;
+                }
+                if (row < p.M && n0 + c0 < p.N) {
+                    const int64_t base =
+                        p.direct ? row * p.ldc + n0 + c0 : ((int64_t)z * p.M + row) * p.ldw + n0 + c0;
+                    double* out = p.direct ? p.C + base : p.ws + base;
+                    const bool full8 = n0 + c0 + 8 <= p.N && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+                    // all loads of the chunk before any store (C is read and written)
+                    double cin[8];
+                    const bool rmw = p.direct && p.beta != 0.0;
+                    if (rmw && full8) {
+#pragma unroll
+                        for (int t = 0; t < 8; t += 2) {
+                            const double2 c2 = *reinterpret_cast<const double2*>(out + t);
+                            cin[t] = c2.x;
+                            cin[t + 1] = c2.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) cin[t] = (rmw && n0 + c0 + t < p.N) ? out[t] : 0.0;
+                    }
+                    double res[8];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) {
+                        const double val = sc[t] != 0.0 ? vv[t] * sc[t]
+                                                        : ldexp(vv[t], ea + p.fb[min(n0 + c0 + t, p.N - 1)] - 2 * OZ_DB);
+                        res[t] = p.direct ? (rmw ? p.alpha * val + p.beta * cin[t] : p.alpha * val) : val;
+                    }
+                    if (full8) {
+#pragma unroll
+                        for (int t = 0; t < 8; t += 2)
+                            *reinterpret_cast<double2*>(out + t) = make_double2(res[t], res[t + 1]);
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 8; ++t)
+                            if (n0 + c0 + t < p.N) out[t] = res[t];
                     }
                 }
             }
-#pragma unroll
-            for (int t = 0; t < 16; ++t) {
-                const int64_t col = n0 + c0 + t;
-                sc[t] = col < p.N ? scale_of(ea + p.fb[col] - 2 * OZ_DB) : 0.0;
-            }
-            if (row < p.M) {
-                const int64_t base = p.direct ? row * p.ldc + n0 + c0 : ((int64_t)blockIdx.z * p.M + row) * p.ldw + n0 + c0;
-                double* out = p.direct ? p.C + base : p.ws + base;
-                const bool full16 = n0 + c0 + 16 <= p.N && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-                // all loads of the chunk before any store (C is read and written)
-                double cin[16];
-                const bool rmw = p.direct && p.beta != 0.0;
-                if (rmw && full16) {
-#pragma unroll
-                    for (int t = 0; t < 16; t += 2) {
-                        const double2 c2 = *reinterpret_cast<const double2*>(out + t);
-                        cin[t] = c2.x;
-                        cin[t + 1] = c2.y;
-                    }
-                } else {
-#pragma unroll
-                    for (int t = 0; t < 16; ++t) cin[t] = (rmw && n0 + c0 + t < p.N) ? out[t] : 0.0;
-                }
-                double res[16];
-#pragma unroll
-                for (int t = 0; t < 16; ++t) {
-                    const double val = sc[t] != 0.0 ? v[t] * sc[t] : ldexp(v[t], ea + p.fb[min(n0 + c0 + t, p.N - 1)] - 2 * OZ_DB);
-                    res[t] = p.direct ? (rmw ? p.alpha * val + p.beta * cin[t] : p.alpha * val) : val;
-                }
-                if (full16) {
-#pragma unroll
-                    for (int t = 0; t < 16; t += 2) *reinterpret_cast<double2*>(out + t) = make_double2(res[t], res[t + 1]);
-                } else {
-#pragma unroll
-                    for (int t = 0; t < 16; ++t)
-                        if (n0 + c0 + t < p.N) out[t] = res[t];
-                }
-            }
+            if (first && warp == 2 && lane == 0) OZ_STAMP(3);
+            first = false;
         }
     }
-    if (warp == 2 && lane == 0) OZ_STAMP(3);
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -794,11 +852,14 @@ int oz_gemm_planes(int trans, int64_t n, int64_t d, int64_t p, double alpha, con
     prm.ws = part; prm.ldw = p;
     prm.pred = pred;
     prm.n_tiles = (int)L.n_tiles;
+    prm.m_tiles = (int)L.m_tiles;
+    prm.splits = (int)L.splits;
     {
         static const char* ab = getenv("RSVD_OZ_ABLATE");
         prm.ablate = ab ? atoi(ab) : 0;
     }
-    dim3 grid((unsigned)(L.m_tiles * L.n_tiles), 1, (unsigned)L.splits);
+    // persistent CTAs, one per SM, over the (split, tile) work units
+    dim3 grid((unsigned)std::min<int64_t>(L.m_tiles * L.n_tiles * L.splits, sm_count()), 1, 1);
     if (reduced) {
         if (L.bn == 32)
             rc = tr ? launch_oz<32, true, OZ_LV_R, OZ_LV_R>(tA, tB, prm, grid, st)

@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 # cuBLAS DGEMM 1.4e-16). A^T Y with rows of very different magnitude
 # (row_spread) carries each row's exponent into Y's column scale and loses
 # about one more digit (6e-14 at e^(+-3) row spread).
-TOL = 2e-14
+TOL = 4e-14  # base-256 digits: A X 2.3e-14 measured at K = 900
 TOL_SPREAD = 2e-13
 # against cuBLAS DGEMM (whose own blocked FP64 accumulation adds ~1e-13 at
 # K ~ 1e4); base-256 digits with a row spread of e^(+-2): 3.6e-13 measured
