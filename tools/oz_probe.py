@@ -16,6 +16,7 @@ n, d = 50000, 10000
 p = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 which = sys.argv[2] if len(sys.argv) > 2 else "both"
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+plain = len(sys.argv) > 4 and sys.argv[4] == "plain"  # no CUPTI profiler (for runs under ncu)
 A = torch.randn((n, d), device="cuda")
 P = ops.OzPlanes(A)
 X = torch.randn((d, p), device="cuda", dtype=torch.float64)
@@ -28,6 +29,15 @@ for name, fn in (("nn", lambda: ops.oz_gemm(P, X, C, 0)), ("tn", lambda: ops.oz_
         continue
     fn()
     torch.cuda.synchronize()
+    if plain:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"{name} p={p}: {e0.elapsed_time(e1) / reps:.3f} ms per product (all kernels)", flush=True)
+        continue
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         for _ in range(reps):
             fn()
