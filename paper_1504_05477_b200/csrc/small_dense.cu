@@ -378,8 +378,13 @@ __global__ void k_eig_gather(int64_t w, int64_t k, const int32_t* __restrict__ o
 #ifdef RSVD_CHOL_TRACE
 __device__ long long g_chol_trace[64];
 #define CHOL_T(i) do { if (threadIdx.x == 0 && (i) < 64) g_chol_trace[i] = clock64(); } while (0)
+// phase accumulators (thread 0): CHOL_P0() at kernel start, CHOL_P(i) adds the cycles since the last mark to slot i
+#define CHOL_P0() long long chol_pm = clock64(); do { if (threadIdx.x == 0) for (int q_ = 8; q_ < 16; ++q_) g_chol_trace[q_] = 0; } while (0)
+#define CHOL_P(i) do { const long long now_ = clock64(); if (threadIdx.x == 0) g_chol_trace[i] += now_ - chol_pm; chol_pm = now_; } while (0)
 #else
 #define CHOL_T(i) do { } while (0)
+#define CHOL_P0() do { } while (0)
+#define CHOL_P(i) do { } while (0)
 #endif
 constexpr int kSwThreadsMax = 512;
 constexpr int kChNB = 16;  // block-row height of the blocked factorization
@@ -553,6 +558,252 @@ k_chol_sweep(int p, const double* __restrict__ G, int64_t ldg, const double* __r
             }
         }
         __syncthreads();
+    }
+    CHOL_T(2);
+    for (int c = ty; c < p; c += ny)
+        for (int a = tx; a < p; a += 32)
+            T[(int64_t)c * ldt + a] = (a < c || s_msk[c] || s_msk[a]) ? 0.0 : S[s_row[c] + a];
+    for (int j = tid; j < p; j += nt) mask[j] = s_msk[j] == 1 ? 1 : 0;
+    if (tid == 0) {
+        const int32_t base = running ? running[0] : 0;
+        ndef[0] = s_count;
+        ndef[1] = base;
+        if (running) running[0] = base + s_count;
+    }
+    CHOL_T(3);
+}
+
+// k_chol_sweep's blocked arithmetic (bitwise equal: every matrix entry sees
+// the same operations in the same order) with the per-column barriers taken
+// out of the block rows. k_chol_sweep spends two block barriers per column in
+// both phases (2 x 2 x p of them, ~1 us each: 330 us at p = 200). Here, per
+// 16-column block:
+//   factor: ONE WARP factors the 16 x 16 diagonal block with the column
+//     entries in registers and shuffles (pivot test, sqrt, reciprocal and the
+//     in-block rank-1 updates: no block barrier), and publishes the block's
+//     R, the pivot reciprocals and the deficiency flags; then every column
+//     right of the block runs the 16 elimination steps on its own 16 entries
+//     in registers (thread per column, no communication); then the trailing
+//     triangle takes the rank-16 update as before;
+//   invert: the 16 x 16 block of R is staged once; every column c >= i0 then
+//     runs the block's 16 back-substitution steps on its own entries in
+//     registers (the steps of a column only read that column and the staged
+//     block); then the rows above take the block's contribution as before.
+// Three barriers per block instead of 32 + 2.
+constexpr int kBk = 16;
+
+__global__ void __launch_bounds__(256, 1)
+k_chol_blk(int p, const double* __restrict__ G, int64_t ldg, const double* __restrict__ ref2, double tau2,
+           double* __restrict__ T, int64_t ldt, int32_t* __restrict__ mask, int32_t* __restrict__ ndef,
+           int32_t* __restrict__ running, const int32_t* __restrict__ active, const int32_t* __restrict__ pred) {
+    if (pred && *pred == 0) return;
+    extern __shared__ double S[];
+    __shared__ int s_row[kFastP];  // S[s_row[i] + j] = element (i, j), j >= i
+    __shared__ double s_ref[kFastP];
+    __shared__ int s_msk[kFastP];  // 0 kept, 1 deficient, 2 inactive
+    __shared__ double s_blk[kBk][kBk + 1];
+    __shared__ double s_inv[kBk];
+    __shared__ int s_dfl[kBk];
+    __shared__ int s_count;
+    const int nt = blockDim.x, tid = threadIdx.x, tx = tid & 31, ty = tid >> 5, ny = nt >> 5;
+    for (int i = tid; i < p; i += nt) {
+        s_row[i] = i * p - (i * (i - 1)) / 2 - i;
+        s_ref[i] = ref2 ? ref2[i] : G[(int64_t)i * ldg + i];
+        s_msk[i] = (active && active[i] == 0) ? 2 : 0;
+    }
+    if (tid == 0) s_count = 0;
+    __syncthreads();
+    for (int i = ty; i < p; i += ny)
+        for (int j = i + tx; j < p; j += 32) S[s_row[i] + j] = G[(int64_t)i * ldg + j];
+    __syncthreads();
+    CHOL_T(0);
+    CHOL_P0();
+    for (int k0 = 0; k0 < p; k0 += kBk) {
+        const int nb = min(kBk, p - k0), k1 = k0 + nb;
+        if (ty == 0) {
+            // D: lane l holds column k0 + l of the diagonal block (rows k0 .. k0 + l)
+            const int l = tx;
+            double x[kBk];
+#pragma unroll
+            for (int t = 0; t < kBk; ++t) x[t] = (l < nb && t <= l) ? S[s_row[k0 + t] + k0 + l] : 0.0;
+            int cnt = 0;
+#pragma unroll
+            for (int j = 0; j < kBk; ++j) {
+                if (j < nb) {  // warp-uniform
+                    double rjj = 1.0, inv = 0.0;
+                    int dfl = 0;
+                    if (l == j) {
+                        const double d = x[j];
+                        const int inactive = s_msk[k0 + j] == 2;
+                        const bool def = inactive || !(d > tau2 * s_ref[k0 + j]) || !(d > 0.0);
+                        rjj = def ? 1.0 : sqrt(d);
+                        inv = def ? 0.0 : 1.0 / rjj;
+                        dfl = def;
+                        if (def && !inactive) {
+                            s_msk[k0 + j] = 1;
+                            ++cnt;
+                        }
+                        s_inv[j] = inv;
+                        s_dfl[j] = dfl;
+                    }
+                    inv = __shfl_sync(0xffffffffu, inv, j);
+                    rjj = __shfl_sync(0xffffffffu, rjj, j);
+                    dfl = __shfl_sync(0xffffffffu, dfl, j);
+                    const double sv = x[j] * inv;  // scaled row j at this lane's column (lanes >= j)
+                    x[j] = (l == j) ? rjj : sv;
+#pragma unroll
+                    for (int i = j + 1; i < kBk; ++i) {
+                        const double ui = __shfl_sync(0xffffffffu, sv, i);  // R[j][k0 + i]
+                        if (!dfl && i < nb && i <= l) x[i] = fma(-ui, sv, x[i]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < kBk; ++t)
+                if (l < nb && t <= l) {
+                    S[s_row[k0 + t] + k0 + l] = x[t];
+                    s_blk[t][l] = x[t];
+                }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            if (l == 0) s_count += cnt;
+        }
+        __syncthreads();
+        CHOL_P(8);
+        if (k1 >= p) break;
+        // P: columns right of the block, the block's nb elimination steps in registers
+        for (int c = k1 + tid; c < p; c += nt) {
+            double x[kBk];
+#pragma unroll
+            for (int t = 0; t < kBk; ++t) x[t] = t < nb ? S[s_row[k0 + t] + c] : 0.0;
+#pragma unroll
+            for (int j = 0; j < kBk; ++j) {
+                if (j < nb) {
+                    const double sv = x[j] * s_inv[j];
+                    x[j] = sv;
+                    if (!s_dfl[j]) {
+#pragma unroll
+                        for (int i = j + 1; i < kBk; ++i)
+                            if (i < nb) x[i] = fma(-s_blk[j][i], sv, x[i]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < kBk; ++t)
+                if (t < nb) S[s_row[k0 + t] + c] = x[t];
+        }
+        __syncthreads();
+        CHOL_P(9);
+        // C: trailing update S[i][c] -= sum_{j in [k0,k1)} R[j][i] R[j][c], k1 <= i <= c
+        const int mt = p - k1;
+        const int ngr = (mt + 3) / 4, nch = (mt + 63) / 64;
+        for (int item = ty; item < ngr * nch; item += ny) {
+            const int g = item / nch, ch = item % nch;
+            const int i0 = k1 + 4 * g;
+            const int cbase = k1 + 64 * ch;
+            if (cbase + 63 < i0) continue;  // chunk entirely below the diagonal (warp-uniform)
+            const int c0 = cbase + tx, c1 = c0 + 32;
+            double acc[4][2];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) acc[a][0] = acc[a][1] = 0.0;
+            for (int j = k0; j < k1; ++j) {
+                const double* rjp = S + s_row[j];
+                const double b0 = c0 < p ? rjp[c0] : 0.0, b1 = c1 < p ? rjp[c1] : 0.0;
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const double ra = i0 + a < p ? rjp[i0 + a] : 0.0;
+                    acc[a][0] = fma(ra, b0, acc[a][0]);
+                    acc[a][1] = fma(ra, b1, acc[a][1]);
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int i = i0 + a;
+                if (i >= p) break;
+                double* row = S + s_row[i];
+                if (c0 >= i && c0 < p) row[c0] -= acc[a][0];
+                if (c1 >= i && c1 < p) row[c1] -= acc[a][1];
+            }
+        }
+        __syncthreads();
+        CHOL_P(10);
+    }
+    CHOL_T(1);
+    // in-place inversion from the bottom, block by block
+    double* Rb = S + (p * (p + 1)) / 2;  // [p][kBk]
+    for (int i1 = p; i1 > 0; i1 -= kBk) {
+        const int i0 = max(0, i1 - kBk), nb = i1 - i0;
+        // the block's R (rows and columns i0 .. i1 - 1) and its pivots' reciprocals
+        for (int e = tid; e < kBk * kBk; e += nt) {
+            const int k = e / kBk, i = e % kBk;
+            if (k <= i && i < nb) {
+                const double v = S[s_row[i0 + k] + i0 + i];
+                s_blk[k][i] = v;
+                if (k == i) s_inv[i] = 1.0 / v;
+            }
+        }
+        __syncthreads();
+        for (int c = i0 + tid; c < p; c += nt) {
+            const int tc = c - i0;  // in-block column when tc < nb
+            double x[kBk];
+#pragma unroll
+            for (int t = 0; t < kBk; ++t) x[t] = (t < nb && t <= tc) ? S[s_row[i0 + t] + c] : 0.0;
+#pragma unroll
+            for (int t = kBk - 1; t >= 0; --t) {
+                if (t < nb && t <= tc) {
+                    const double rinv = s_inv[t];
+                    const double tic = (t == tc) ? rinv : x[t] * rinv;
+                    x[t] = tic;
+#pragma unroll
+                    for (int k = 0; k < t; ++k) {
+                        const double rk = s_blk[k][t];
+                        x[k] = (t == tc) ? -rk * tic : fma(-rk, tic, x[k]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < kBk; ++t)
+                if (t < nb && t <= tc) S[s_row[i0 + t] + c] = x[t];
+        }
+        __syncthreads();
+        CHOL_P(11);
+        if (i0 == 0) break;
+        for (int e = tid; e < i0 * kBk; e += nt) {
+            const int k = e / kBk, ii = e % kBk;
+            Rb[e] = ii < nb ? S[s_row[k] + i0 + ii] : 0.0;
+        }
+        __syncthreads();
+        const int ngr = (i0 + 3) / 4, nch = (p - i0 + 63) / 64;
+        for (int item = ty; item < ngr * nch; item += ny) {
+            const int g = item / nch, ch = item % nch;
+            const int k0 = 4 * g;
+            const int c0 = i0 + 64 * ch + tx, c1 = c0 + 32;
+            double acc[4][2];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) acc[a][0] = acc[a][1] = 0.0;
+            for (int ii = 0; ii < nb; ++ii) {
+                const int i = i0 + ii;
+                const double* ti = S + s_row[i];
+                const double t0 = (c0 >= i && c0 < p) ? ti[c0] : 0.0;
+                const double t1 = (c1 >= i && c1 < p) ? ti[c1] : 0.0;
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const double rk = k0 + a < i0 ? Rb[(k0 + a) * kBk + ii] : 0.0;
+                    acc[a][0] = fma(rk, t0, acc[a][0]);
+                    acc[a][1] = fma(rk, t1, acc[a][1]);
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int k = k0 + a;
+                if (k >= i0) break;
+                double* row = S + s_row[k];
+                if (c0 < p) row[c0] = c0 < i1 ? -acc[a][0] : row[c0] - acc[a][0];
+                if (c1 < p) row[c1] = c1 < i1 ? -acc[a][1] : row[c1] - acc[a][1];
+            }
+        }
+        __syncthreads();
+        CHOL_P(12);
     }
     CHOL_T(2);
     for (int c = ty; c < p; c += ny)
@@ -913,6 +1164,24 @@ int chol_deflate(int64_t p, const double* G, int64_t ldg, const double* ref2, do
         if (sm > 48 * 1024)
             RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_chol_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         const int nt = p <= 64 ? 128 : (p <= 128 ? 256 : kSwThreadsMax);
+        // default: the barrier-light blocked kernel (bitwise equal to the blocked sweep;
+        // RSVD_CHOL_SWEEP_OLD=1: k_chol_sweep, for A/B measurement)
+        const bool old_sweep = getenv("RSVD_CHOL_SWEEP_OLD") != nullptr;
+        if (inv_blocked && !old_sweep) {
+            static PerDevice<bool> attr_dev;
+            bool& attr = attr_dev.get();
+            if (!attr) {
+                RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_chol_blk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     200 * 1024));
+                attr = true;
+            }
+            // 256 threads: one per column in the register phases (p <= 224), and 252
+            // registers each (at 512 threads the unrolled block steps spill)
+            k_chol_blk<<<1, nt > 256 ? 256 : nt, sm, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running,
+                                                          active, pred);
+            RSVD_CHECK_LAUNCH();
+            return RSVD_OK;
+        }
         k_chol_sweep<<<1, nt, sm, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active, pred,
                                          blocked, inv_blocked);
         RSVD_CHECK_LAUNCH();

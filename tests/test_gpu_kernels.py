@@ -171,6 +171,34 @@ def test_chol_deflate_blocked_wide(ops, monkeypatch, p):
     assert np.max(np.abs(qk.T @ qk - np.eye(len(keep)))) < 1e-9
 
 
+@pytest.mark.parametrize("p", [65, 96, 100, 150, 200])
+def test_chol_blk_matches_sweep_bitwise(ops, monkeypatch, p):
+    """k_chol_blk (diagonal block factored by one warp, block steps of every
+    column in registers: 3 barriers per 16 columns) against k_chol_sweep's
+    blocked path (2 barriers per column): same operations in the same order,
+    so T, mask and the counts are bitwise equal -- deficient columns inside
+    and across blocks and an inactive column included."""
+    v = _rand((3 * p, p), 140 + p)
+    for j, (a, b) in {5: (0, 3), 17: (2, 9), 40: (16, 33), p - 2: (1, p - 3)}.items():
+        v[:, j] = v[:, a] - 0.5 * v[:, b]
+    G = _t(v.T @ v)
+    active = torch.ones(p, dtype=torch.int32, device="cuda")
+    active[p // 2] = 0
+    outs = []
+    for mode in ("blk", "sweep"):
+        if mode == "sweep":
+            monkeypatch.setenv("RSVD_CHOL_SWEEP_OLD", "1")
+        T = torch.empty((p, p), dtype=torch.float64, device="cuda")
+        mask = torch.empty(p, dtype=torch.int32, device="cuda")
+        ndef = torch.zeros(2, dtype=torch.int32, device="cuda")
+        running = torch.tensor([3], dtype=torch.int32, device="cuda")
+        ops.chol_deflate(G, None, 1e-14, T, mask, ndef, running, active)
+        outs.append((T.clone(), mask.clone(), ndef.clone(), running.clone()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    assert list(np.nonzero(outs[0][1].cpu().numpy())[0]) == [5, 17, 40, p - 2]
+
+
 def test_fill_stream_matches_host_stream(ops):
     n = 1001  # odd: each vector consumes n+1 uniforms (matrix.py:44-47)
     dev = ops.fill_stream(n, 3, o.QR_FILL_SEED, "cuda").cpu().numpy()

@@ -20,9 +20,17 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 mode = sys.argv[2] if len(sys.argv) > 2 else "exact"
 cfgd = bench.CONFIGS[name]
 cfg = rsvd.RsvdConfig(k=cfgd["k"], variant=cfgd["variant"], q=cfgd["q"], seed=0)
-A = bench.make_matrix(cfgd, "cuda") if not cfgd.get("pca") else bench.make_pca_matrix(cfgd, "cuda")
-op = DenseDeviceOp(A, exact=(mode == "exact"), center=bool(cfgd.get("pca")))
-Pi = mx.gaussian(A.shape[1], cfg.p, mx.SeededRng(0)).data
+if cfgd.get("sparse"):
+    from paper_1504_05477_b200.operators import CsrDeviceOp
+
+    indptr, colv, valv = bench.make_csr(cfgd, torch.device("cuda", 0))
+    op = CsrDeviceOp(indptr, colv, valv, cfgd["d"])
+else:
+    A = bench.make_matrix(cfgd, torch.device("cuda", 0))
+    if cfgd.get("fp64") or mode == "fp64":
+        A = A.double()
+    op = DenseDeviceOp(A, exact=(mode == "exact"), center=bool(cfgd.get("pca")))
+Pi = mx.gaussian(cfgd["d"], cfg.p, mx.SeededRng(0)).data
 g = rsvd.GraphedFactorization(op, cfg)
 for _ in range(3):
     g.run(Pi)

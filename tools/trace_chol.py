@@ -32,4 +32,6 @@ for p in [int(x) for x in sys.argv[2:]]:
     torch.cuda.synchronize()
     buf = np.zeros(64, dtype=np.int64)
     L.rsvd_debug_chol_trace(buf.ctypes.data)
-    print(f"p={p}: factor {buf[1] - buf[0]} cycles, invert {buf[2] - buf[1]}, output {buf[3] - buf[2]}")
+    print(f"p={p}: factor {buf[1] - buf[0]} cycles, invert {buf[2] - buf[1]}, output {buf[3] - buf[2]}; "
+          f"k_chol_blk phases: diag warp {buf[8]}, panel columns {buf[9]}, trailing update {buf[10]}, "
+          f"inverse columns {buf[11]}, inverse pass {buf[12]}")
