@@ -157,6 +157,15 @@ int rsvd_spmm_csr_plan(int dtype, int idx64, int64_t nrows, int64_t nb, const vo
                        const int32_t *chunk_row, const int32_t *chunk_slot, int64_t nsplit,
                        const int32_t *split_row, const int64_t *split_beg, void *ws, int64_t ws_bytes,
                        void *stream);
+/* Slab tier of the hybrid CSR product (FP32): C += A_slab X, where A_slab holds
+ * the nonzeros of `nslab` chosen columns (slab_cols[s] = the column of slab
+ * row s) as a CSR over slab row indices (slab_ptr[nrows + 1], slab_idx,
+ * slab_val). The X rows of those columns are staged in shared memory, one
+ * column chunk of the block at a time (spmm_nt, _kernels.pyx:74-92, for the
+ * columns frequent enough that every SM reuses them). Deterministic. */
+int rsvd_spmm_slab(int64_t nrows, int64_t nb, const int32_t *slab_ptr, const int32_t *slab_idx,
+                   const float *slab_val, const int64_t *slab_cols, int64_t nslab, const float *X,
+                   int64_t ldx, float *C, int64_t ldc, void *stream);
 /* CSR (nrows x ncols, sorted columns) -> CSR of the transpose, stable in row
  * order. perm_by_col[e] must be a stable column-sorted permutation of the
  * nonzeros (supplied by the caller's sort); t_indptr has ncols+1 entries. */

@@ -46,6 +46,9 @@ int fill_stream(int64_t n, int64_t nvec, uint64_t seed, double* out, cudaStream_
 int spmm_csr(int dtype, int idx64, int64_t nrows, int64_t ncols, int64_t nb, const void* indptr,
              const void* col, const void* val, const void* B, int64_t ldb, double alpha,
              double beta, void* C, int64_t ldc, cudaStream_t st);
+int spmm_slab(int64_t nrows, int64_t nb, const int32_t* mptr, const int32_t* midx, const float* mval,
+              const int64_t* slab_cols, int64_t M, const float* X, int64_t ldx, float* C, int64_t ldc,
+              cudaStream_t st);
 int spmm_csr_plan(int dtype, int idx64, int64_t nb, const void* col, const void* val, const void* B, int64_t ldb,
                   double alpha, double beta, void* C, int64_t ldc, int64_t nchunks, const int64_t* clo,
                   const int64_t* chi, const int32_t* crow, const int32_t* cslot, int64_t nsplit,
@@ -208,6 +211,17 @@ int rsvd_spmm_csr(int dtype, int idx64, int64_t nrows, int64_t ncols, int64_t nb
     RSVD_REQUIRE(nrows >= 0 && ncols >= 0 && nb >= 0 && ldb >= nb && ldc >= nb, "spmm: bad shape");
     return spmm_csr(dtype, idx64, nrows, ncols, nb, indptr, col, val, B, ldb, alpha, beta, C, ldc,
                     as_stream(stream));
+}
+
+int rsvd_spmm_slab(int64_t nrows, int64_t nb, const int32_t* slab_ptr, const int32_t* slab_idx,
+                   const float* slab_val, const int64_t* slab_cols, int64_t nslab, const float* X, int64_t ldx,
+                   float* C, int64_t ldc, void* stream) {
+    RSVD_REQUIRE(nrows >= 0 && nb >= 0 && nslab >= 0, "spmm_slab: negative dimension");
+    RSVD_REQUIRE(ldx >= nb && ldc >= nb, "spmm_slab: leading dimension too small");
+    RSVD_REQUIRE(nslab * 4 <= 200 * 1024, "spmm_slab: at most 51200 slab columns");
+    RSVD_REQUIRE(nrows == 0 || nslab == 0 || (slab_ptr && slab_idx && slab_val && slab_cols && X && C),
+                 "spmm_slab: null pointer");
+    return spmm_slab(nrows, nb, slab_ptr, slab_idx, slab_val, slab_cols, nslab, X, ldx, C, ldc, as_stream(stream));
 }
 
 int rsvd_spmm_csr_plan(int dtype, int idx64, int64_t nrows, int64_t nb, const void* col, const void* val,

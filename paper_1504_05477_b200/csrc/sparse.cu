@@ -247,6 +247,65 @@ int launch_spmm_plan(int64_t nb, const void* col, const void* val, const void* B
     return RSVD_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Slab tier of the hybrid product A X: the M most frequent columns that are
+// too sparse for the dense panel (C3: density 0.2 % - 3 %, ~21 % of the
+// nonzeros) keep their rows of the dense block X in SHARED MEMORY, so their
+// nonzeros cost a 100-byte shared-memory read instead of a 400-byte L2 gather.
+// The block width is cut into `nwc` column chunks of wb <= 32 floats so that
+// M x wb x 4 bytes fit one SM (C3: width 100 -> 4 chunks of 25, M = 2048,
+// 200 KB): CTA (g, wc) stages X[slab_cols, wc-th chunk] once and walks the
+// rows of row group g, warp per row, lane per output column; every lane of a
+// warp reads consecutive words of one slab row (conflict-free). The rows'
+// slab nonzeros come from their own CSR (slab row index instead of the column
+// index). C[r, chunk] += sum (fixed order: deterministic).
+__global__ void __launch_bounds__(1024, 1)
+k_spmm_slab(int64_t nrows, int64_t nb, int wb, int64_t rows_per_group, const int32_t* __restrict__ mptr,
+            const int32_t* __restrict__ midx, const float* __restrict__ mval, const int64_t* __restrict__ slab_cols,
+            int M, const float* __restrict__ X, int64_t ldx, float* __restrict__ C, int64_t ldc) {
+    extern __shared__ float slab[];  // [M][wb]
+    const int w0 = blockIdx.y * wb;
+    const int wn = (int)min((int64_t)wb, nb - w0);  // live columns of this chunk
+    for (int e = threadIdx.x; e < M * wb; e += blockDim.x) {
+        const int sidx = e / wb, j = e - sidx * wb;
+        slab[e] = j < wn ? X[slab_cols[sidx] * ldx + w0 + j] : 0.f;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_group;
+    const int64_t r1 = min(nrows, r0 + rows_per_group);
+    const bool live = lane < wn;
+    const float* sl = slab + (live ? lane : 0);
+    for (int64_t r = r0 + warp; r < r1; r += nw) {
+        const int lo = mptr[r], hi = mptr[r + 1];
+        if (lo == hi) continue;
+        float acc0 = 0.f, acc1 = 0.f;
+        for (int base = lo; base < hi; base += 32) {
+            const int e = base + lane;
+            int si = 0;
+            float v = 0.f;
+            if (e < hi) {
+                si = midx[e] * wb;
+                v = mval[e];
+            }
+            const int cnt = min(32, hi - base);
+            int i = 0;
+            for (; i + 2 <= cnt; i += 2) {
+                const int s0 = __shfl_sync(0xffffffffu, si, i), s1 = __shfl_sync(0xffffffffu, si, i + 1);
+                const float v0 = __shfl_sync(0xffffffffu, v, i), v1 = __shfl_sync(0xffffffffu, v, i + 1);
+                acc0 = fmaf(v0, sl[s0], acc0);
+                acc1 = fmaf(v1, sl[s1], acc1);
+            }
+            if (i < cnt) {
+                const int s0 = __shfl_sync(0xffffffffu, si, i);
+                const float v0 = __shfl_sync(0xffffffffu, v, i);
+                acc0 = fmaf(v0, sl[s0], acc0);
+            }
+        }
+        if (live) C[r * ldc + w0 + lane] += acc0 + acc1;
+    }
+}
+
 template <typename T, typename I>
 __global__ void k_csr_transpose_fill(int64_t nrows, int64_t nnz, const I* __restrict__ indptr,
                                      const I* __restrict__ col, const T* __restrict__ val,
@@ -310,6 +369,34 @@ int spmm_csr_plan(int dtype, int idx64, int64_t nb, const void* col, const void*
     if (idx64) RSVD_SPP(float, int64_t);
     RSVD_SPP(float, int32_t);
 #undef RSVD_SPP
+}
+
+int spmm_slab(int64_t nrows, int64_t nb, const int32_t* mptr, const int32_t* midx, const float* mval,
+              const int64_t* slab_cols, int64_t M, const float* X, int64_t ldx, float* C, int64_t ldc,
+              cudaStream_t st) {
+    if (nrows == 0 || nb == 0 || M == 0) return RSVD_OK;
+    // chunks of wb <= 32 columns whose M-row slab fits 200 KB of shared memory
+    const int64_t cap = 200 * 1024;
+    int64_t nwc = cdiv(nb, 32);
+    while (M * cdiv(nb, nwc) * 4 > cap) ++nwc;
+    const int wb = (int)cdiv(nb, nwc);
+    nwc = cdiv(nb, wb);
+    const size_t sm = (size_t)M * wb * sizeof(float);
+    static PerDevice<bool> attr_dev;
+    bool& attr = attr_dev.get();
+    if (!attr) {
+        RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_spmm_slab, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap));
+        attr = true;
+    }
+    // one CTA per SM: row groups x width chunks
+    int64_t groups = sm_count() / nwc;
+    if (groups < 1) groups = 1;
+    const int64_t rpg = cdiv(nrows, groups);
+    groups = cdiv(nrows, rpg);
+    dim3 grid((unsigned)groups, (unsigned)nwc);
+    k_spmm_slab<<<grid, 1024, sm, st>>>(nrows, nb, wb, rpg, mptr, midx, mval, slab_cols, (int)M, X, ldx, C, ldc);
+    RSVD_CHECK_LAUNCH();
+    return RSVD_OK;
 }
 
 template <typename T, typename I>

@@ -428,6 +428,16 @@ def spmm_csr_plan(plan, col, val, B, C, alpha=1.0, beta=0.0):
     return C
 
 
+def spmm_slab(slab, X, C):
+    """C += A_slab X (slab = dict(ptr, idx, val, cols): the slab tier of the hybrid CSR product)."""
+    assert X.dtype == C.dtype == torch.float32
+    nrows = slab["ptr"].numel() - 1
+    check(lib().rsvd_spmm_slab(nrows, X.shape[1], _ptr(slab["ptr"]), _ptr(slab["idx"]), _ptr(slab["val"]),
+                               _ptr(slab["cols"]), slab["cols"].numel(), _ptr(X), _ld(X), _ptr(C), _ld(C),
+                               _stream()), "spmm_slab")
+    return C
+
+
 def csr_transpose(indptr, col, val, nrows, ncols):
     """Device CSR of A^T (stable in row order). The stable column sort that
     orders the nonzeros is torch plumbing done once per operator."""

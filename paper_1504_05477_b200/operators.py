@@ -138,6 +138,13 @@ class CsrDeviceOp:
 
     HOT_DENSITY = float(os.environ.get("RSVD_SPMM_HOT_DENSITY", "0.03"))
     HOT_MAX = 2048
+    # Slab tier (A X only): the next SLAB_COLS most frequent columns keep their
+    # rows of X in shared memory (csrc/sparse.cu k_spmm_slab); 2048 columns x
+    # a 25-column chunk of the block fill one SM's 200 KB. A column is worth a
+    # slab row when every row group meets it several times: at least
+    # SLAB_MIN_COUNT nonzeros (RSVD_SPMM_SLAB_COLS=0 turns the tier off).
+    SLAB_COLS = int(os.environ.get("RSVD_SPMM_SLAB_COLS", "2048"))
+    SLAB_MIN_COUNT = 64
 
     def __init__(self, indptr, col, val, ncols, n_total=None, row_offset=0, hot_density=None):
         nrows = indptr.numel() - 1
@@ -156,10 +163,16 @@ class CsrDeviceOp:
             self.hot = self._split_hot(indptr, col, val, nrows, dens)
         if self.hot is not None:
             indptr, col, val = self.hot["cold"]
-        self.indptr, self.col, self.val = indptr, col, val
+        # A^T Y gathers over every non-hot nonzero; A X takes the slab columns out as well
         self.t_indptr, self.t_col, self.t_val = ops.csr_transpose(indptr, col, val, nrows, self.ncols)
-        self.plan = ops.SpmmPlan(indptr)
         self.t_plan = ops.SpmmPlan(self.t_indptr)
+        self.slab = None
+        if val.dtype == torch.float32 and self.SLAB_COLS > 0 and nrows >= 128 and val.numel() > 0:
+            self.slab = self._split_slab(indptr, col, val, nrows)
+        if self.slab is not None:
+            indptr, col, val = self.slab.pop("cold")
+        self.indptr, self.col, self.val = indptr, col, val
+        self.plan = ops.SpmmPlan(indptr)
 
     def prepare(self):
         """Per-factorization setup (nothing for CSR)."""
@@ -192,6 +205,35 @@ class CsrDeviceOp:
                 "cold": (cptr, col[cold].contiguous(), val[cold].contiguous()),
                 "hot_nnz": int(is_hot.sum())}
 
+    def _split_slab(self, indptr, col, val, nrows):
+        """Operator setup (torch plumbing, once): the most frequent remaining
+        columns as a CSR over slab row indices, and the CSR without them."""
+        counts = torch.bincount(col.to(torch.int64), minlength=self.ncols)
+        m = min(self.SLAB_COLS, self.ncols)
+        top = torch.topk(counts, m)
+        keep = top.values >= self.SLAB_MIN_COUNT
+        cols = top.indices[keep].sort().values
+        if cols.numel() == 0:
+            return None
+        pos = torch.full((self.ncols,), -1, dtype=torch.int64, device=col.device)
+        pos[cols] = torch.arange(cols.numel(), device=col.device)
+        ip = indptr.to(torch.int64)
+        rows = torch.repeat_interleave(torch.arange(nrows, device=col.device), ip[1:] - ip[:-1])
+        pcol = pos[col.to(torch.int64)]
+        in_slab = pcol >= 0
+
+        def ptr_of(sel):
+            c = torch.bincount(rows[sel], minlength=nrows)
+            p = torch.zeros(nrows + 1, dtype=torch.int32, device=col.device)
+            p[1:] = torch.cumsum(c, 0).to(torch.int32)
+            return p
+
+        cold = ~in_slab
+        cptr = ptr_of(cold).to(indptr.dtype)
+        return {"ptr": ptr_of(in_slab), "idx": pcol[in_slab].to(torch.int32).contiguous(),
+                "val": val[in_slab].contiguous(), "cols": cols.contiguous(), "nnz": int(in_slab.sum()),
+                "cold": (cptr, col[cold].contiguous(), val[cold].contiguous())}
+
     @property
     def is_sparse(self):
         return True
@@ -208,9 +250,13 @@ class CsrDeviceOp:
 
     def _apply32(self, X, out):
         if self.hot is None:
-            return ops.spmm_csr_plan(self.plan, self.col, self.val, X, out)
-        ops.gemm_nn(self.hot["panel"], self._x_hot(X), out)
-        return ops.spmm_csr_plan(self.plan, self.col, self.val, X, out, beta=1.0)
+            ops.spmm_csr_plan(self.plan, self.col, self.val, X, out)
+        else:
+            ops.gemm_nn(self.hot["panel"], self._x_hot(X), out)
+            ops.spmm_csr_plan(self.plan, self.col, self.val, X, out, beta=1.0)
+        if self.slab is not None:
+            ops.spmm_slab(self.slab, X, out)
+        return out
 
     def _apply_t32(self, Y, out):
         ops.spmm_csr_plan(self.t_plan, self.t_col, self.t_val, Y, out)

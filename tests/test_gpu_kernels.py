@@ -199,6 +199,53 @@ def test_chol_blk_matches_sweep_bitwise(ops, monkeypatch, p):
     assert list(np.nonzero(outs[0][1].cpu().numpy())[0]) == [5, 17, 40, p - 2]
 
 
+@pytest.mark.parametrize("nb", [8, 100, 300])
+def test_csr_slab_tier(ops, nb, monkeypatch):
+    """Slab tier of the hybrid CSR product (k_spmm_slab): 500 columns of 5 %
+    density stay below the dense-panel threshold used here and above the slab
+    threshold, so their rows of X are staged in shared memory; A X against the
+    dense FP64 product and against the operator without the tier, ragged and
+    empty rows included."""
+    from paper_1504_05477_b200.operators import CsrDeviceOp
+
+    rng = np.random.default_rng(nb + 11)
+    n, d = 3000, 5000
+    mask = rng.random((n, d)) < 0.004
+    mask[:, 200:700] |= rng.random((n, 500)) < 0.05
+    mask[:, 5] = True
+    mask[17] = False  # an empty row
+    mask[18, :] = False
+    mask[18, 300] = True  # a row with a single slab nonzero
+    A = np.zeros((n, d))
+    A[mask] = rng.lognormal(0, 1, int(mask.sum()))
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    indptr[1:] = np.cumsum(mask.sum(1))
+    rows, cols = np.nonzero(mask)
+    ip = torch.from_numpy(indptr).cuda().to(torch.int32)
+    cl = torch.from_numpy(cols).cuda().to(torch.int32)
+    vl = torch.from_numpy(A[rows, cols]).cuda().float()
+    op = CsrDeviceOp(ip, cl, vl, d, hot_density=0.2)
+    assert op.hot is not None and op.hot["H"] == 1
+    assert op.slab is not None and op.slab["cols"].numel() == 500
+    assert op.slab["nnz"] == int(mask[:, 200:700].sum())
+    monkeypatch.setattr(CsrDeviceOp, "SLAB_COLS", 0)
+    plain = CsrDeviceOp(ip, cl, vl, d, hot_density=0.2)
+    assert plain.slab is None
+    Xt = torch.from_numpy(rng.standard_normal((d, nb))).cuda().float()
+    A32 = A.astype(np.float32).astype(np.float64)
+    ref = A32 @ Xt.double().cpu().numpy()
+    outs = []
+    for o_ in (op, plain):
+        out = torch.full((n, nb), 7.0, device="cuda")
+        o_.apply(Xt, out)
+        outs.append(out.double().cpu().numpy())
+        assert np.max(np.abs(outs[-1] - ref)) < 2e-6 * np.abs(ref).max()
+    # deterministic: a second call is bitwise equal
+    out2 = torch.empty((n, nb), device="cuda")
+    op.apply(Xt, out2)
+    assert np.array_equal(out2.double().cpu().numpy(), outs[0])
+
+
 def test_fill_stream_matches_host_stream(ops):
     n = 1001  # odd: each vector consumes n+1 uniforms (matrix.py:44-47)
     dev = ops.fill_stream(n, 3, o.QR_FILL_SEED, "cuda").cpu().numpy()

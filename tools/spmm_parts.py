@@ -55,7 +55,9 @@ def main():
     for dens in dens_list:
         op = CsrDeviceOp(indptr, col, val, d, hot_density=dens)
         leg = {"H": op.hot["H"] if op.hot else 0,
-               "hot_nnz_frac": (op.hot["hot_nnz"] / val.numel()) if op.hot else 0.0}
+               "hot_nnz_frac": (op.hot["hot_nnz"] / val.numel()) if op.hot else 0.0,
+               "slab_cols": int(op.slab["cols"].numel()) if op.slab else 0,
+               "slab_nnz_frac": (op.slab["nnz"] / val.numel()) if op.slab else 0.0}
         leg["A.X_ms"] = timed(lambda: op.apply(X, oy))
         leg["A^T.Y_ms"] = timed(lambda: op.apply_t(Y, oc))
         if dens == dens_list[0]:
