@@ -157,6 +157,21 @@ int rsvd_spmm_csr_plan(int dtype, int idx64, int64_t nrows, int64_t nb, const vo
                        const int32_t *chunk_row, const int32_t *chunk_slot, int64_t nsplit,
                        const int32_t *split_row, const int64_t *split_beg, void *ws, int64_t ws_bytes,
                        void *stream);
+/* Nonzero-balanced FP32 product C = alpha A B + beta C (int32 indices, width
+ * nb <= 128, a multiple of 4; spmm_nt / spmm_t on a CSR, _kernels.pyx:74-113):
+ * work unit c = nonzeros [c chunk, (c + 1) chunk) with rowid[e] the row of
+ * nonzero e. A row that lies inside one unit is written straight to C; the
+ * first / last row of a unit that continues in a neighbouring unit goes to
+ * workspace slot head_slot[c] / tail_slot[c] (-1: none), the slots of one row
+ * being consecutive: split row s (split_row[s]) sums slots [split_beg[s],
+ * split_beg[s + 1]) in order. empty_rows: rows without a nonzero (C = beta C).
+ * ws: slots x nb floats. Deterministic, no atomics. */
+int rsvd_spmm_nnz_plan(int64_t nnz, int chunk, int64_t nb, const int32_t *col, const float *val,
+                       const int32_t *rowid, const float *B, int64_t ldb, double alpha, double beta,
+                       float *C, int64_t ldc, const int32_t *head_slot, const int32_t *tail_slot,
+                       int64_t nsplit, const int32_t *split_row, const int64_t *split_beg,
+                       int64_t nempty, const int32_t *empty_rows, void *ws, int64_t ws_bytes,
+                       void *stream);
 /* Slab tier of the hybrid CSR product (FP32): C += A_slab X, where A_slab holds
  * the nonzeros of `nslab` chosen columns (slab_cols[s] = the column of slab
  * row s) as a CSR over slab row indices (slab_ptr[nrows + 1], slab_idx,

@@ -40,6 +40,8 @@ _SIGS = {
     "rsvd_oz_gemm_planes": ([_int, _i64, _i64, _i64, _dbl, _vp, _int, _i64, _i64, _vp, _int, _vp, _i64, _dbl, _vp,
                              _i64, _vp, _i64, _vp, _vp], _int),
     "rsvd_spmm_csr": ([_int, _int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _i64, _vp], _int),
+    "rsvd_spmm_nnz_plan": ([_i64, _int, _i64, _vp, _vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _i64, _vp, _vp, _i64, _vp, _vp,
+                            _i64, _vp, _vp, _i64, _vp], _int),
     "rsvd_spmm_slab": ([_i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _vp], _int),
     "rsvd_spmm_csr_plan": ([_int, _int, _i64, _i64, _vp, _vp, _vp, _i64, _dbl, _dbl, _vp, _i64, _i64, _vp, _vp, _vp,
                             _vp, _i64, _vp, _vp, _vp, _i64, _vp], _int),

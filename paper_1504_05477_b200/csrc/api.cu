@@ -46,6 +46,10 @@ int fill_stream(int64_t n, int64_t nvec, uint64_t seed, double* out, cudaStream_
 int spmm_csr(int dtype, int idx64, int64_t nrows, int64_t ncols, int64_t nb, const void* indptr,
              const void* col, const void* val, const void* B, int64_t ldb, double alpha,
              double beta, void* C, int64_t ldc, cudaStream_t st);
+int spmm_nnz_plan(int64_t nnz, int chunk, int64_t nb, const int32_t* col, const float* val, const int32_t* rowid,
+                  const float* B, int64_t ldb, double alpha, double beta, float* C, int64_t ldc,
+                  const int32_t* head_slot, const int32_t* tail_slot, int64_t nsplit, const int32_t* srow,
+                  const int64_t* sbeg, int64_t nempty, const int32_t* empty_rows, float* ws, cudaStream_t st);
 int spmm_slab(int64_t nrows, int64_t nb, const int32_t* mptr, const int32_t* midx, const float* mval,
               const int64_t* slab_cols, int64_t M, const float* X, int64_t ldx, float* C, int64_t ldc,
               cudaStream_t st);
@@ -211,6 +215,19 @@ int rsvd_spmm_csr(int dtype, int idx64, int64_t nrows, int64_t ncols, int64_t nb
     RSVD_REQUIRE(nrows >= 0 && ncols >= 0 && nb >= 0 && ldb >= nb && ldc >= nb, "spmm: bad shape");
     return spmm_csr(dtype, idx64, nrows, ncols, nb, indptr, col, val, B, ldb, alpha, beta, C, ldc,
                     as_stream(stream));
+}
+
+int rsvd_spmm_nnz_plan(int64_t nnz, int chunk, int64_t nb, const int32_t* col, const float* val,
+                       const int32_t* rowid, const float* B, int64_t ldb, double alpha, double beta, float* C,
+                       int64_t ldc, const int32_t* head_slot, const int32_t* tail_slot, int64_t nsplit,
+                       const int32_t* split_row, const int64_t* split_beg, int64_t nempty,
+                       const int32_t* empty_rows, void* ws, int64_t ws_bytes, void* stream) {
+    RSVD_REQUIRE(nnz >= 0 && nb >= 0 && nsplit >= 0 && nempty >= 0, "spmm_nnz_plan: negative size");
+    RSVD_REQUIRE(ldb >= nb && ldc >= nb, "spmm_nnz_plan: leading dimension too small");
+    RSVD_REQUIRE(nsplit == 0 || (ws && split_row && split_beg), "spmm_nnz_plan: null pointer");
+    (void)ws_bytes;
+    return spmm_nnz_plan(nnz, chunk, nb, col, val, rowid, B, ldb, alpha, beta, C, ldc, head_slot, tail_slot, nsplit,
+                         split_row, split_beg, nempty, empty_rows, (float*)ws, as_stream(stream));
 }
 
 int rsvd_spmm_slab(int64_t nrows, int64_t nb, const int32_t* slab_ptr, const int32_t* slab_idx,

@@ -3,6 +3,9 @@
 // (no atomics). Warp per row: the warp loads 32 (col, val) pairs at a time,
 // broadcasts each with a shuffle, and every lane accumulates NPL contiguous
 // columns of the dense row B[col, :] (coalesced 32*NPL-wide reads).
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace rsvd {
@@ -175,6 +178,197 @@ k_spmm_plan(int64_t nchunks, int64_t nb, const I* __restrict__ col, const T* __r
     }
 }
 
+// FP32 / int32 / width <= 128 (a multiple of 4) fast path of the plan product:
+// persistent warps (chunks w, w + W, ...: no CTA launch churn, no CTA held by
+// its longest row), U row gathers in flight per lane with the batch padded to
+// a multiple of U by (column 0, value 0) entries instead of a remainder loop,
+// 32-bit column shuffles. ncu of k_spmm_plan on C3's cold CSR: 27.7
+// instructions per nonzero, 19 of 64 warps resident on average, 5.7-7 TB/s of
+// gathered rows against the 12-16 TB/s a bare gather loop reaches
+// (tools/l2_gather_probe.cu).
+template <int U>
+__global__ void __launch_bounds__(256, 3)
+k_spmm_gather_f32(int64_t nchunks, int nb, const int32_t* __restrict__ col, const float* __restrict__ val,
+                  const float* __restrict__ B, int64_t ldb, float alpha, float beta, float* __restrict__ C,
+                  int64_t ldc, const int64_t* __restrict__ clo, const int64_t* __restrict__ chi,
+                  const int32_t* __restrict__ crow, const int32_t* __restrict__ cslot, float* __restrict__ ws) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const bool on = 4 * lane < nb;
+    const float* Bl = B + 4 * lane;
+    for (int64_t ch = gw; ch < nchunks; ch += nwarps) {
+        const int64_t lo = clo[ch], hi = chi[ch];
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int64_t base = lo; base < hi; base += 32) {
+            const int64_t e = base + lane;
+            int c = 0;
+            float v = 0.f;
+            if (e < hi) {
+                c = col[e];
+                v = val[e];
+            }
+            const int cnt = (int)min((int64_t)32, hi - base);
+            for (int i = 0; i < cnt; i += U) {
+                int cu[U];
+                float vu[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    cu[u] = __shfl_sync(0xffffffffu, c, i + u);
+                    vu[u] = __shfl_sync(0xffffffffu, v, i + u);
+                }
+                float4 b4[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    b4[u] = on ? *reinterpret_cast<const float4*>(Bl + (int64_t)cu[u] * ldb)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    acc.x = fmaf(vu[u], b4[u].x, acc.x);
+                    acc.y = fmaf(vu[u], b4[u].y, acc.y);
+                    acc.z = fmaf(vu[u], b4[u].z, acc.z);
+                    acc.w = fmaf(vu[u], b4[u].w, acc.w);
+                }
+            }
+        }
+        if (!on) continue;
+        const int slot = cslot[ch];
+        if (slot >= 0) {
+            *reinterpret_cast<float4*>(ws + (int64_t)slot * nb + 4 * lane) = acc;
+        } else {
+            float* cp = C + (int64_t)crow[ch] * ldc + 4 * lane;
+            // same rounding as k_spmm_plan: alpha / beta applied in FP64
+            float4 r;
+            if (beta != 0.f) {
+                const float4 o = *reinterpret_cast<const float4*>(cp);
+                r.x = (float)((double)alpha * (double)acc.x + (double)beta * (double)o.x);
+                r.y = (float)((double)alpha * (double)acc.y + (double)beta * (double)o.y);
+                r.z = (float)((double)alpha * (double)acc.z + (double)beta * (double)o.z);
+                r.w = (float)((double)alpha * (double)acc.w + (double)beta * (double)o.w);
+            } else {
+                r.x = (float)((double)alpha * (double)acc.x);
+                r.y = (float)((double)alpha * (double)acc.y);
+                r.z = (float)((double)alpha * (double)acc.z);
+                r.w = (float)((double)alpha * (double)acc.w);
+            }
+            *reinterpret_cast<float4*>(cp) = r;
+        }
+    }
+}
+
+// Nonzero-balanced FP32 product (the default plan for FP32 / int32 / width <=
+// 128): a work unit is a fixed run of `chunk` consecutive nonzeros, whatever
+// rows they belong to. Measured on C3's cold CSR (tools/spmm_uniform_probe.py):
+// warp-per-row reaches 10.5 TB/s of gathered rows when every row has 54
+// nonzeros but 7.0 TB/s with C3's lognormal row lengths and the same columns
+// -- the short rows' fixed cost (pointer loads, a gather tail that cannot fill
+// the U loads in flight, the C row write) sets the pace, not the column
+// pattern. Here a warp walks its run 32 nonzeros at a time with U row gathers
+// in flight; at a row change it flushes the finished row: straight to C when
+// the row lies inside the run, to a workspace slot when it is the run's first
+// or last row and continues in a neighbouring run (head_slot / tail_slot from
+// the plan; a row's slots are consecutive and k_spmm_split_reduce adds them in
+// order: deterministic, no atomics). Rows without nonzeros are scaled by
+// k_spmm_empty_rows.
+template <int U>
+__global__ void __launch_bounds__(256, U >= 16 ? 2 : 3)
+k_spmm_nnz_f32(int64_t nnz, int chunk, int64_t nchunks, int nb, const int32_t* __restrict__ col,
+               const float* __restrict__ val, const int32_t* __restrict__ rowid, const float* __restrict__ B,
+               int64_t ldb, float alpha, float beta, float* __restrict__ C, int64_t ldc,
+               const int32_t* __restrict__ head_slot, const int32_t* __restrict__ tail_slot,
+               float* __restrict__ ws) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const bool on = 4 * lane < nb;
+    const float* Bl = B + 4 * lane;
+    for (int64_t ch = gw; ch < nchunks; ch += nwarps) {
+        const int64_t e0 = ch * chunk, e1 = min(nnz, e0 + (int64_t)chunk);
+        const int hs = head_slot[ch], ts = tail_slot[ch];
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        int cur = -1;
+        bool first = true;  // the row being accumulated is the run's first row
+        auto flush = [&](bool last) {
+            if (!on) return;
+            const int slot = first ? hs : (last ? ts : -1);
+            if (slot >= 0) {
+                *reinterpret_cast<float4*>(ws + (int64_t)slot * nb + 4 * lane) = acc;
+            } else {
+                float* cp = C + (int64_t)cur * ldc + 4 * lane;
+                float4 r;
+                if (beta != 0.f) {
+                    const float4 o = *reinterpret_cast<const float4*>(cp);
+                    r.x = (float)((double)alpha * (double)acc.x + (double)beta * (double)o.x);
+                    r.y = (float)((double)alpha * (double)acc.y + (double)beta * (double)o.y);
+                    r.z = (float)((double)alpha * (double)acc.z + (double)beta * (double)o.z);
+                    r.w = (float)((double)alpha * (double)acc.w + (double)beta * (double)o.w);
+                } else {
+                    r.x = (float)((double)alpha * (double)acc.x);
+                    r.y = (float)((double)alpha * (double)acc.y);
+                    r.z = (float)((double)alpha * (double)acc.z);
+                    r.w = (float)((double)alpha * (double)acc.w);
+                }
+                *reinterpret_cast<float4*>(cp) = r;
+            }
+        };
+        for (int64_t base = e0; base < e1; base += 32) {
+            const int64_t e = base + lane;
+            const int cnt = (int)min((int64_t)32, e1 - base);
+            int c = 0, r = 0;
+            float v = 0.f;
+            if (e < e1) {
+                c = col[e];
+                v = val[e];
+                r = rowid[e];
+            }
+            // padding entries (value 0, column 0) stay in the batch's last row
+            const int r_last = __shfl_sync(0xffffffffu, r, cnt - 1);  // every lane takes part in the shuffle
+            r = lane < cnt ? r : r_last;
+            for (int i = 0; i < cnt; i += U) {
+                int cu[U], ru[U];
+                float vu[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    cu[u] = __shfl_sync(0xffffffffu, c, i + u);
+                    vu[u] = __shfl_sync(0xffffffffu, v, i + u);
+                    ru[u] = __shfl_sync(0xffffffffu, r, i + u);
+                }
+                float4 b4[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    b4[u] = on ? *reinterpret_cast<const float4*>(Bl + (int64_t)cu[u] * ldb)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (ru[u] != cur) {  // warp-uniform
+                        if (cur >= 0) {
+                            flush(false);
+                            first = false;
+                        }
+                        cur = ru[u];
+                        acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                    acc.x = fmaf(vu[u], b4[u].x, acc.x);
+                    acc.y = fmaf(vu[u], b4[u].y, acc.y);
+                    acc.z = fmaf(vu[u], b4[u].z, acc.z);
+                    acc.w = fmaf(vu[u], b4[u].w, acc.w);
+                }
+            }
+        }
+        if (cur >= 0) flush(true);
+    }
+}
+
+// rows without a nonzero: C[r, :] = beta C[r, :]
+__global__ void k_spmm_empty_rows(int64_t nempty, int nb, const int32_t* __restrict__ rows, float beta,
+                                  float* __restrict__ C, int64_t ldc) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nempty * nb) return;
+    const int64_t i = e / nb, j = e % nb;
+    float* p = C + (int64_t)rows[i] * ldc + j;
+    *p = beta != 0.f ? beta * *p : 0.f;
+}
+
 template <typename T>
 __global__ void k_spmm_split_reduce(int64_t nsplit, int64_t nb, const int32_t* __restrict__ srow,
                                     const int64_t* __restrict__ sbeg, const T* __restrict__ ws, double alpha,
@@ -202,6 +396,32 @@ int launch_spmm_plan_panel(int64_t nb, const void* col, const void* val, const T
     const T* vp = (const T*)val;
     T* wp = (T*)ws;
     const bool vec = sizeof(T) == 4 && ldb % 4 == 0 && nb % 4 == 0 && ((uintptr_t)bp & 15) == 0;
+    if constexpr (sizeof(T) == 4 && sizeof(I) == 4) {
+        // persistent fast path (RSVD_SPMM_OLD=1: k_spmm_plan, for A/B measurement);
+        // C rows and workspace slots must take float4 stores
+        static const bool old_path = getenv("RSVD_SPMM_OLD") != nullptr;
+        static const int unroll = getenv("RSVD_SPMM_U") ? atoi(getenv("RSVD_SPMM_U")) : 8;
+        if (!old_path && vec && nb <= 128 && nchunks > 0 && ldc % 4 == 0 && ((uintptr_t)cc & 15) == 0 &&
+            ((uintptr_t)wp & 15) == 0) {
+            const int64_t want = cdiv(nchunks * 32, 256);
+            const unsigned g = (unsigned)std::min<int64_t>(want, (int64_t)sm_count() * 3);
+            if (unroll == 4)
+                k_spmm_gather_f32<4><<<g, 256, 0, st>>>(nchunks, (int)nb, (const int32_t*)cp, (const float*)vp,
+                                                        (const float*)bp, ldb, (float)alpha, (float)beta, (float*)cc,
+                                                        ldc, clo, chi, crow, cslot, (float*)wp);
+            else
+                k_spmm_gather_f32<8><<<g, 256, 0, st>>>(nchunks, (int)nb, (const int32_t*)cp, (const float*)vp,
+                                                        (const float*)bp, ldb, (float)alpha, (float)beta, (float*)cc,
+                                                        ldc, clo, chi, crow, cslot, (float*)wp);
+            RSVD_CHECK_LAUNCH();
+            if (nsplit > 0) {
+                k_spmm_split_reduce<T><<<(unsigned)cdiv(nsplit * 32, 256), 256, 0, st>>>(nsplit, nb, srow, sbeg, wp,
+                                                                                         alpha, beta, cc, ldc);
+                RSVD_CHECK_LAUNCH();
+            }
+            return RSVD_OK;
+        }
+    }
     if (nchunks > 0) {
         if (vec && nb <= 128)
             k_spmm_plan<T, I, 1, true><<<grid, 256, 0, st>>>(nchunks, nb, cp, vp, bp, ldb, alpha, beta, cc, ldc, clo,
@@ -396,6 +616,44 @@ int spmm_slab(int64_t nrows, int64_t nb, const int32_t* mptr, const int32_t* mid
     dim3 grid((unsigned)groups, (unsigned)nwc);
     k_spmm_slab<<<grid, 1024, sm, st>>>(nrows, nb, wb, rpg, mptr, midx, mval, slab_cols, (int)M, X, ldx, C, ldc);
     RSVD_CHECK_LAUNCH();
+    return RSVD_OK;
+}
+
+int spmm_nnz_plan(int64_t nnz, int chunk, int64_t nb, const int32_t* col, const float* val, const int32_t* rowid,
+                  const float* B, int64_t ldb, double alpha, double beta, float* C, int64_t ldc,
+                  const int32_t* head_slot, const int32_t* tail_slot, int64_t nsplit, const int32_t* srow,
+                  const int64_t* sbeg, int64_t nempty, const int32_t* empty_rows, float* ws, cudaStream_t st) {
+    if (nb == 0) return RSVD_OK;
+    RSVD_REQUIRE(nb <= 128 && nb % 4 == 0 && ldb % 4 == 0 && ldc % 4 == 0 && ((uintptr_t)B & 15) == 0 &&
+                     ((uintptr_t)C & 15) == 0 && ((uintptr_t)ws & 15) == 0,
+                 "spmm_nnz_plan: width <= 128, a multiple of 4, 16-byte aligned rows");
+    RSVD_REQUIRE(chunk >= 32 && chunk % 32 == 0, "spmm_nnz_plan: chunk must be a multiple of 32");
+    const int64_t nchunks = cdiv(nnz, chunk);
+    if (nchunks > 0) {
+        static const int ctas = getenv("RSVD_SPMM_CTAS") ? atoi(getenv("RSVD_SPMM_CTAS")) : 3;
+        const unsigned g = (unsigned)std::min<int64_t>(cdiv(nchunks * 32, 256), (int64_t)sm_count() * ctas);
+        static const int unroll = getenv("RSVD_SPMM_U") ? atoi(getenv("RSVD_SPMM_U")) : 8;
+        if (unroll == 4)
+            k_spmm_nnz_f32<4><<<g, 256, 0, st>>>(nnz, chunk, nchunks, (int)nb, col, val, rowid, B, ldb, (float)alpha,
+                                                 (float)beta, C, ldc, head_slot, tail_slot, ws);
+        else if (unroll == 16)
+            k_spmm_nnz_f32<16><<<g, 256, 0, st>>>(nnz, chunk, nchunks, (int)nb, col, val, rowid, B, ldb, (float)alpha,
+                                                  (float)beta, C, ldc, head_slot, tail_slot, ws);
+        else
+            k_spmm_nnz_f32<8><<<g, 256, 0, st>>>(nnz, chunk, nchunks, (int)nb, col, val, rowid, B, ldb, (float)alpha,
+                                                 (float)beta, C, ldc, head_slot, tail_slot, ws);
+        RSVD_CHECK_LAUNCH();
+    }
+    if (nsplit > 0) {
+        k_spmm_split_reduce<float><<<(unsigned)cdiv(nsplit * 32, 256), 256, 0, st>>>(nsplit, nb, srow, sbeg, ws, alpha,
+                                                                                     beta, C, ldc);
+        RSVD_CHECK_LAUNCH();
+    }
+    if (nempty > 0) {
+        k_spmm_empty_rows<<<(unsigned)cdiv(nempty * nb, 256), 256, 0, st>>>(nempty, (int)nb, empty_rows, (float)beta, C,
+                                                                            ldc);
+        RSVD_CHECK_LAUNCH();
+    }
     return RSVD_OK;
 }
 

@@ -428,6 +428,70 @@ def spmm_csr_plan(plan, col, val, B, C, alpha=1.0, beta=0.0):
     return C
 
 
+class SpmmNnzPlan:
+    """Nonzero-balanced plan of a CSR matrix for rsvd_spmm_nnz_plan (built
+    once per operator): work units of `chunk` consecutive nonzeros; a row cut
+    by a unit boundary gets one workspace slot per unit it touches (consecutive
+    slot numbers), summed in order afterwards."""
+
+    CHUNK = int(__import__("os").environ.get("RSVD_SPMM_CHUNK", "1024"))
+
+    def __init__(self, indptr, chunk=None):
+        chunk = int(chunk or self.CHUNK)
+        dev = indptr.device
+        ip = indptr.to(torch.int64)
+        n = ip.numel() - 1
+        nnz = int(ip[-1])  # host sync: plan construction is setup, not the hot loop
+        lens = ip[1:] - ip[:-1]
+        self.chunk, self.nnz, self.nrows = chunk, nnz, n
+        self.rowid = torch.repeat_interleave(torch.arange(n, device=dev, dtype=torch.int32), lens).contiguous()
+        nch = -(-nnz // chunk)
+        e0 = torch.arange(nch, device=dev, dtype=torch.int64) * chunk
+        e1 = torch.clamp(e0 + chunk, max=nnz)
+        if nch:
+            fr = self.rowid[e0].to(torch.int64)
+            lr = self.rowid[e1 - 1].to(torch.int64)
+            head = (ip[fr] < e0) | (ip[fr + 1] > e1)
+            tail = (lr != fr) & (ip[lr + 1] > e1)
+            flags = torch.stack([head, tail], 1).flatten()
+            ids = torch.cumsum(flags.to(torch.int64), 0) - 1
+            slot = torch.where(flags, ids, torch.full_like(ids, -1)).to(torch.int32).view(nch, 2)
+            self.head_slot = slot[:, 0].contiguous()
+            self.tail_slot = slot[:, 1].contiguous()
+            prow = torch.stack([fr, lr], 1).flatten()[flags]
+            self.nslots = int(prow.numel())
+            srow, counts = torch.unique_consecutive(prow, return_counts=True)
+            self.split_row = srow.to(torch.int32).contiguous()
+            self.split_beg = torch.zeros(srow.numel() + 1, dtype=torch.int64, device=dev)
+            self.split_beg[1:] = torch.cumsum(counts, 0)
+        else:
+            self.head_slot = self.tail_slot = torch.empty(0, dtype=torch.int32, device=dev)
+            self.split_row = torch.empty(0, dtype=torch.int32, device=dev)
+            self.split_beg = torch.zeros(1, dtype=torch.int64, device=dev)
+            self.nslots = 0
+        self.nsplit = int(self.split_row.numel())
+        self.empty_rows = torch.nonzero(lens == 0).flatten().to(torch.int32).contiguous()
+
+    @staticmethod
+    def eligible(col, val, B, C):
+        nb = B.shape[1]
+        return (val.dtype == torch.float32 and col.dtype == torch.int32 and B.dtype == C.dtype == torch.float32
+                and nb <= 128 and nb % 4 == 0 and _ld(B) % 4 == 0 and _ld(C) % 4 == 0
+                and B.data_ptr() % 16 == 0 and C.data_ptr() % 16 == 0)
+
+
+def spmm_nnz_plan(plan, col, val, B, C, alpha=1.0, beta=0.0):
+    """C = alpha A B + beta C through the nonzero-balanced kernel (rsvd_spmm_nnz_plan)."""
+    nb = B.shape[1]
+    ws = WS.get(max(16, plan.nslots * nb * 4), B.device) if plan.nslots else None
+    check(lib().rsvd_spmm_nnz_plan(plan.nnz, plan.chunk, nb, _ptr(col), _ptr(val), _ptr(plan.rowid), _ptr(B), _ld(B),
+                                   float(alpha), float(beta), _ptr(C), _ld(C), _ptr(plan.head_slot),
+                                   _ptr(plan.tail_slot), plan.nsplit, _ptr(plan.split_row), _ptr(plan.split_beg),
+                                   plan.empty_rows.numel(), _ptr(plan.empty_rows), _ptr(ws),
+                                   0 if ws is None else ws.numel(), _stream()), "spmm_nnz_plan")
+    return C
+
+
 def spmm_slab(slab, X, C):
     """C += A_slab X (slab = dict(ptr, idx, val, cols): the slab tier of the hybrid CSR product)."""
     assert X.dtype == C.dtype == torch.float32

@@ -21,6 +21,10 @@ from . import device as ops
 # Exact mode: Rayleigh-Ritz W = A^T Q with reduced digit levels
 # (RSVD_OZ_REDUCED_RR=0: full accuracy, for A/B measurement).
 OZ_REDUCED_RR = os.environ.get("RSVD_OZ_REDUCED_RR", "1") != "0"
+# FP32 CSR products on the nonzero-balanced plan (RSVD_SPMM_ROWPLAN=1: the
+# warp-per-row plan, for A/B measurement).
+NNZ_PLAN = os.environ.get("RSVD_SPMM_ROWPLAN", "0") != "1"
+NNZ_PLAN_T = os.environ.get("RSVD_SPMM_NNZ_T", "0") == "1"
 
 
 class DenseDeviceOp:
@@ -142,8 +146,12 @@ class CsrDeviceOp:
     # rows of X in shared memory (csrc/sparse.cu k_spmm_slab); 2048 columns x
     # a 25-column chunk of the block fill one SM's 200 KB. A column is worth a
     # slab row when every row group meets it several times: at least
-    # SLAB_MIN_COUNT nonzeros (RSVD_SPMM_SLAB_COLS=0 turns the tier off).
-    SLAB_COLS = int(os.environ.get("RSVD_SPMM_SLAB_COLS", "2048"))
+    # SLAB_MIN_COUNT nonzeros. OFF by default (RSVD_SPMM_SLAB_COLS=2048 turns it
+    # on): measured at C3 the tier takes 21 % of the nonzeros off the L2 gather
+    # (0.62 -> 0.47 ms) but its own pass costs 0.37 ms -- rows hold ~21 slab
+    # nonzeros each, so the per-row pointer / index / C read-modify-write
+    # latency, not shared-memory bandwidth, sets its pace (SpMM).
+    SLAB_COLS = int(os.environ.get("RSVD_SPMM_SLAB_COLS", "0"))
     SLAB_MIN_COUNT = 64
 
     def __init__(self, indptr, col, val, ncols, n_total=None, row_offset=0, hot_density=None):
@@ -173,6 +181,8 @@ class CsrDeviceOp:
             indptr, col, val = self.slab.pop("cold")
         self.indptr, self.col, self.val = indptr, col, val
         self.plan = ops.SpmmPlan(indptr)
+        # nonzero-balanced plans of the FP32 fast path, built on first use
+        self._nnz_plan = self._nnz_plan_t = None
 
     def prepare(self):
         """Per-factorization setup (nothing for CSR)."""
@@ -248,18 +258,39 @@ class CsrDeviceOp:
         ops.gather_rows(h["idx"], X, xh[: h["H"]])
         return xh
 
+    def _gather(self, trans, B, C, beta=0.0):
+        """The CSR part of a product: the nonzero-balanced kernel when the
+        block qualifies (FP32, int32 indices, width <= 128 and a multiple of
+        4, 16-byte rows), else warp-per-row chunks (RSVD_SPMM_ROWPLAN=1
+        forces those, for A/B measurement)."""
+        col, val = (self.t_col, self.t_val) if trans else (self.col, self.val)
+        # A^T Y stays on the row plan: the rows of A^T (columns of A) are mostly a
+        # handful of nonzeros, where a run of 256 nonzeros is a string of row
+        # flushes (measured at C3: 0.54 ms against 0.44 ms; A X 0.55 against 0.61)
+        if NNZ_PLAN and (not trans or NNZ_PLAN_T) and ops.SpmmNnzPlan.eligible(col, val, B, C):
+            if trans:
+                if self._nnz_plan_t is None:
+                    self._nnz_plan_t = ops.SpmmNnzPlan(self.t_indptr)
+                plan = self._nnz_plan_t
+            else:
+                if self._nnz_plan is None:
+                    self._nnz_plan = ops.SpmmNnzPlan(self.indptr)
+                plan = self._nnz_plan
+            return ops.spmm_nnz_plan(plan, col, val, B, C, beta=beta)
+        return ops.spmm_csr_plan(self.t_plan if trans else self.plan, col, val, B, C, beta=beta)
+
     def _apply32(self, X, out):
         if self.hot is None:
-            ops.spmm_csr_plan(self.plan, self.col, self.val, X, out)
+            self._gather(0, X, out)
         else:
             ops.gemm_nn(self.hot["panel"], self._x_hot(X), out)
-            ops.spmm_csr_plan(self.plan, self.col, self.val, X, out, beta=1.0)
+            self._gather(0, X, out, beta=1.0)
         if self.slab is not None:
             ops.spmm_slab(self.slab, X, out)
         return out
 
     def _apply_t32(self, Y, out):
-        ops.spmm_csr_plan(self.t_plan, self.t_col, self.t_val, Y, out)
+        self._gather(1, Y, out)
         if self.hot is not None:
             h = self.hot
             th = torch.empty((h["Hp"], Y.shape[1]), dtype=out.dtype, device=out.device)

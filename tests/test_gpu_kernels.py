@@ -199,6 +199,56 @@ def test_chol_blk_matches_sweep_bitwise(ops, monkeypatch, p):
     assert list(np.nonzero(outs[0][1].cpu().numpy())[0]) == [5, 17, 40, p - 2]
 
 
+@pytest.mark.parametrize("chunk", [32, 64, 256])
+@pytest.mark.parametrize("nb", [4, 100, 128])
+def test_spmm_nnz_plan_matches_dense_and_row_plan(ops, nb, chunk):
+    """Nonzero-balanced FP32 product (k_spmm_nnz_f32): runs of `chunk`
+    nonzeros cut rows anywhere -- rows spanning several runs, runs holding
+    many short rows, empty rows (first, middle, last), a run boundary exactly
+    on a row boundary -- against the dense FP64 product and, to FP32 rounding
+    of the split sums, the warp-per-row plan; alpha / beta applied; repeated
+    calls bitwise equal."""
+    rng = np.random.default_rng(100 * nb + chunk)
+    n, d = 700, 900
+    lens = rng.integers(0, 40, n)
+    lens[0] = 0
+    lens[5] = 3 * chunk + 7     # spans 4+ runs
+    lens[6] = 0
+    lens[7] = chunk             # a full run's worth
+    lens[n - 1] = 0
+    lens[100:140] = 1           # many rows inside one run
+    A = np.zeros((n, d))
+    for r in range(n):
+        cols = rng.choice(d, size=min(lens[r], d), replace=False)
+        A[r, cols] = rng.lognormal(0, 1, cols.size)
+    mask = A != 0
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    indptr[1:] = np.cumsum(mask.sum(1))
+    rows, cols = np.nonzero(mask)
+    ip = torch.from_numpy(indptr).cuda().to(torch.int32)
+    cl = torch.from_numpy(cols).cuda().to(torch.int32)
+    vl = torch.from_numpy(A[rows, cols]).cuda().float()
+    B = rng.standard_normal((d, nb))
+    C0 = rng.standard_normal((n, nb))
+    Bt = torch.from_numpy(B).cuda().float()
+    plan = ops.SpmmNnzPlan(ip, chunk=chunk)
+    assert plan.nsplit >= 1 and plan.empty_rows.numel() >= 3
+    assert ops.SpmmNnzPlan.eligible(cl, vl, Bt, torch.empty((n, nb), device="cuda"))
+    A32 = A.astype(np.float32).astype(np.float64)
+    for alpha, beta in ((1.0, 0.0), (0.5, 2.0)):
+        Ct = torch.from_numpy(C0).cuda().float()
+        ops.spmm_nnz_plan(plan, cl, vl, Bt, Ct, alpha=alpha, beta=beta)
+        ref = alpha * (A32 @ Bt.double().cpu().numpy()) + beta * torch.from_numpy(C0).float().double().numpy()
+        got = Ct.double().cpu().numpy()
+        assert np.max(np.abs(got - ref)) < 2e-6 * np.abs(ref).max()
+        C2 = torch.from_numpy(C0).cuda().float()
+        ops.spmm_nnz_plan(plan, cl, vl, Bt, C2, alpha=alpha, beta=beta)
+        assert torch.equal(Ct, C2)
+        Cr = torch.from_numpy(C0).cuda().float()
+        ops.spmm_csr_plan(ops.SpmmPlan(ip), cl, vl, Bt, Cr, alpha=alpha, beta=beta)
+        assert np.max(np.abs(got - Cr.double().cpu().numpy())) < 2e-6 * np.abs(ref).max()
+
+
 @pytest.mark.parametrize("nb", [8, 100, 300])
 def test_csr_slab_tier(ops, nb, monkeypatch):
     """Slab tier of the hybrid CSR product (k_spmm_slab): 500 columns of 5 %
@@ -224,6 +274,7 @@ def test_csr_slab_tier(ops, nb, monkeypatch):
     ip = torch.from_numpy(indptr).cuda().to(torch.int32)
     cl = torch.from_numpy(cols).cuda().to(torch.int32)
     vl = torch.from_numpy(A[rows, cols]).cuda().float()
+    monkeypatch.setattr(CsrDeviceOp, "SLAB_COLS", 2048)
     op = CsrDeviceOp(ip, cl, vl, d, hot_density=0.2)
     assert op.hot is not None and op.hot["H"] == 1
     assert op.slab is not None and op.slab["cols"].numel() == 500
