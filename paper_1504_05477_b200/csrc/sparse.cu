@@ -271,7 +271,7 @@ k_spmm_gather_f32(int64_t nchunks, int nb, const int32_t* __restrict__ col, cons
 // order: deterministic, no atomics). Rows without nonzeros are scaled by
 // k_spmm_empty_rows.
 template <int U>
-__global__ void __launch_bounds__(256, U >= 16 ? 2 : 4)
+__global__ void __launch_bounds__(256, U >= 16 ? 2 : 3)
 k_spmm_nnz_f32(int64_t nnz, int chunk, int64_t nchunks, int nb, const int32_t* __restrict__ col,
                const float* __restrict__ val, const int32_t* __restrict__ rowid, const float* __restrict__ B,
                int64_t ldb, float alpha, float beta, float* __restrict__ C, int64_t ldc,
@@ -325,31 +325,33 @@ k_spmm_nnz_f32(int64_t nnz, int chunk, int64_t nchunks, int nb, const int32_t* _
             const int r_last = __shfl_sync(0xffffffffu, r, cnt - 1);  // every lane takes part in the shuffle
             r = lane < cnt ? r : r_last;
             for (int i = 0; i < cnt; i += U) {
-                // only the U row loads are live across the gather latency: values and
-                // row ids are shuffled in when the rows arrive (64 registers, 4 CTAs/SM)
+                int cu[U], ru[U];
+                float vu[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    cu[u] = __shfl_sync(0xffffffffu, c, i + u);
+                    vu[u] = __shfl_sync(0xffffffffu, v, i + u);
+                    ru[u] = __shfl_sync(0xffffffffu, r, i + u);
+                }
                 float4 b4[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int cu = __shfl_sync(0xffffffffu, c, i + u);
-                    b4[u] = on ? *reinterpret_cast<const float4*>(Bl + (int64_t)cu * ldb)
+                for (int u = 0; u < U; ++u)
+                    b4[u] = on ? *reinterpret_cast<const float4*>(Bl + (int64_t)cu[u] * ldb)
                                : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const float vu = __shfl_sync(0xffffffffu, v, i + u);
-                    const int ru = __shfl_sync(0xffffffffu, r, i + u);
-                    if (ru != cur) {  // warp-uniform
+                    if (ru[u] != cur) {  // warp-uniform
                         if (cur >= 0) {
                             flush(false);
                             first = false;
                         }
-                        cur = ru;
+                        cur = ru[u];
                         acc = make_float4(0.f, 0.f, 0.f, 0.f);
                     }
-                    acc.x = fmaf(vu, b4[u].x, acc.x);
-                    acc.y = fmaf(vu, b4[u].y, acc.y);
-                    acc.z = fmaf(vu, b4[u].z, acc.z);
-                    acc.w = fmaf(vu, b4[u].w, acc.w);
+                    acc.x = fmaf(vu[u], b4[u].x, acc.x);
+                    acc.y = fmaf(vu[u], b4[u].y, acc.y);
+                    acc.z = fmaf(vu[u], b4[u].z, acc.z);
+                    acc.w = fmaf(vu[u], b4[u].w, acc.w);
                 }
             }
         }
@@ -628,7 +630,7 @@ int spmm_nnz_plan(int64_t nnz, int chunk, int64_t nb, const int32_t* col, const 
     RSVD_REQUIRE(chunk >= 32 && chunk % 32 == 0, "spmm_nnz_plan: chunk must be a multiple of 32");
     const int64_t nchunks = cdiv(nnz, chunk);
     if (nchunks > 0) {
-        static const int ctas = getenv("RSVD_SPMM_CTAS") ? atoi(getenv("RSVD_SPMM_CTAS")) : 4;
+        static const int ctas = getenv("RSVD_SPMM_CTAS") ? atoi(getenv("RSVD_SPMM_CTAS")) : 3;
         const unsigned g = (unsigned)std::min<int64_t>(cdiv(nchunks * 32, 256), (int64_t)sm_count() * ctas);
         static const int unroll = getenv("RSVD_SPMM_U") ? atoi(getenv("RSVD_SPMM_U")) : 8;
         if (unroll == 4)
