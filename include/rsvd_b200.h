@@ -108,6 +108,11 @@ int64_t rsvd_oz_planes_bytes(int64_t n, int64_t d);
 int rsvd_oz_num_planes(void);
 int rsvd_oz_prepare(int64_t n, int64_t d, const float *A, int64_t lda, int8_t *planes, int32_t *row_exp,
                     void *stream);
+/* rows [r0, r0 + nr) only (r0 a multiple of 32; A = base of the full matrix):
+ * lets the caller cut each row panel as its upload lands (the reference's
+ * DenseMatrix copy, matrix.py:73-85, pipelined with the first device pass). */
+int rsvd_oz_prepare_rows(int64_t n, int64_t d, int64_t r0, int64_t nr, const float *A, int64_t lda,
+                         int8_t *planes, int32_t *row_exp, void *stream);
 int64_t rsvd_oz_gemm_ws_bytes(int trans, int64_t n, int64_t d, int64_t p);
 int rsvd_oz_gemm(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t *planes,
                  const int32_t *row_exp, const double *B, int64_t ldb, double beta, double *C, int64_t ldc,

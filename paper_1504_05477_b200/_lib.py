@@ -30,6 +30,7 @@ _SIGS = {
     "rsvd_oz_planes_bytes": ([_i64, _i64], _i64),
     "rsvd_oz_num_planes": ([], _int),
     "rsvd_oz_prepare": ([_i64, _i64, _vp, _i64, _vp, _vp, _vp], _int),
+    "rsvd_oz_prepare_rows": ([_i64, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _vp], _int),
     "rsvd_oz_gemm_ws_bytes": ([_int, _i64, _i64, _i64], _i64),
     "rsvd_oz_gemm": ([_int, _i64, _i64, _i64, _dbl, _vp, _vp, _vp, _i64, _dbl, _vp, _i64, _vp, _i64, _vp, _vp],
                      _int),

@@ -120,6 +120,14 @@ int rsvd_oz_prepare(int64_t n, int64_t d, const float* A, int64_t lda, int8_t* p
     return oz_prepare(n, d, A, lda, planes, row_exp, as_stream(stream));
 }
 
+int rsvd_oz_prepare_rows(int64_t n, int64_t d, int64_t r0, int64_t nr, const float* A, int64_t lda, int8_t* planes,
+                         int32_t* row_exp, void* stream) {
+    RSVD_REQUIRE(n >= 0 && d >= 0, "oz_prepare_rows: negative dimension");
+    RSVD_REQUIRE(lda >= d, "oz_prepare_rows: leading dimension too small");
+    RSVD_REQUIRE(n == 0 || (A && planes && row_exp), "oz_prepare_rows: null pointer");
+    return oz_prepare_rows(n, d, r0, nr, A, lda, planes, row_exp, as_stream(stream));
+}
+
 int64_t rsvd_oz_gemm_ws_bytes(int trans, int64_t n, int64_t d, int64_t p) {
     if (n < 0 || d < 0 || p < 0) return 0;
     return oz_gemm_ws_bytes(trans, n, d, p);

@@ -58,6 +58,8 @@ int64_t oz_planes_bytes(int64_t n, int64_t d);
 int oz_num_planes();
 int oz_prepare(int64_t n, int64_t d, const float* A, int64_t lda, int8_t* planes, int32_t* row_exp,
                cudaStream_t st);
+int oz_prepare_rows(int64_t n, int64_t d, int64_t r0, int64_t nr, const float* A, int64_t lda, int8_t* planes,
+                    int32_t* row_exp, cudaStream_t st);
 int64_t oz_gemm_ws_bytes(int trans, int64_t n, int64_t d, int64_t p);
 int oz_gemm_planes(int trans, int64_t n, int64_t d, int64_t p, double alpha, const int8_t* planes, int nplanes,
                    int64_t rows_alloc, int64_t cols_alloc, const int32_t* exps, int col_scaled, const double* B,

@@ -468,10 +468,10 @@ __device__ __forceinline__ uint32_t oz_byte(unsigned long long M, int k) { retur
 // writes one contiguous 512-byte run per digit plane and block.
 __global__ void __launch_bounds__(256) k_oz_slice_a(int64_t n, int64_t d, const float* __restrict__ A, int64_t lda,
                                                     int64_t n_pad, int64_t d_pad, int8_t* __restrict__ planes,
-                                                    int32_t* __restrict__ row_exp) {
+                                                    int32_t* __restrict__ row_exp, int64_t row0) {
     __shared__ double s_scale[32];
     const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
-    const int64_t r0 = (int64_t)blockIdx.x * 32;
+    const int64_t r0 = row0 + (int64_t)blockIdx.x * 32;
     const bool vec = (lda % 4 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
     for (int rr = warp; rr < 32; rr += 8) {
         const int64_t r = r0 + rr;
@@ -777,7 +777,22 @@ int oz_prepare(int64_t n, int64_t d, const float* A, int64_t lda, int8_t* planes
                cudaStream_t st) {
     if (n == 0) return RSVD_OK;
     const int64_t n_pad = cdiv(n, 128) * 128, d_pad = cdiv(d, 128) * 128;
-    k_oz_slice_a<<<(unsigned)(n_pad / 32), 256, 0, st>>>(n, d, A, lda, n_pad, d_pad, planes, row_exp);
+    k_oz_slice_a<<<(unsigned)(n_pad / 32), 256, 0, st>>>(n, d, A, lda, n_pad, d_pad, planes, row_exp, 0);
+    RSVD_CHECK_LAUNCH();
+    return RSVD_OK;
+}
+
+// rows [r0, r0 + nr) of the n x d matrix A (r0 a multiple of 32): a row panel
+// can be cut as soon as it has arrived in HBM, while the next panel's upload
+// is still in flight; the panel that ends at row n also writes the zero
+// padding rows up to the next multiple of 128.
+int oz_prepare_rows(int64_t n, int64_t d, int64_t r0, int64_t nr, const float* A, int64_t lda, int8_t* planes,
+                    int32_t* row_exp, cudaStream_t st) {
+    RSVD_REQUIRE(r0 >= 0 && nr >= 0 && r0 + nr <= n && r0 % 32 == 0, "oz_prepare_rows: bad row range");
+    if (nr == 0) return RSVD_OK;
+    const int64_t n_pad = cdiv(n, 128) * 128, d_pad = cdiv(d, 128) * 128;
+    const int64_t end = r0 + nr == n ? n_pad : r0 + nr;
+    k_oz_slice_a<<<(unsigned)cdiv(end - r0, 32), 256, 0, st>>>(n, d, A, lda, n_pad, d_pad, planes, row_exp, r0);
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }

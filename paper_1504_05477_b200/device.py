@@ -165,6 +165,13 @@ class OzPlanes:
                                     _stream()), "oz_prepare")
         return self
 
+    def refresh_rows(self, A, r0, nr):
+        """Re-cut rows [r0, r0 + nr) only (r0 a multiple of 32): a row panel of
+        a matrix that is still being uploaded."""
+        check(lib().rsvd_oz_prepare_rows(self.n, self.d, int(r0), int(nr), _ptr(A), _ld(A), _ptr(self.planes),
+                                         _ptr(self.row_exp), _stream()), "oz_prepare_rows")
+        return self
+
 
 def oz_gemm(P, B, C, trans, alpha=1.0, beta=0.0, pred=None, reduced=False):
     """trans=0: C (n x p) = alpha A B + beta C; trans=1: C (d x p) = alpha A^T B

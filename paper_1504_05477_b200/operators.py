@@ -48,6 +48,9 @@ class DenseDeviceOp:
         self.device = A.device
         self.mu = None
         self.oz = None
+        # True: the caller cuts the digit planes itself (rsvd._run cuts each row
+        # panel as its upload lands), prepare() leaves them alone
+        self.external_planes = False
         if exact:
             if A.dtype != torch.float32:
                 raise ValueError("exact (Ozaki) products are for FP32 A; FP64 A uses FP64 products already")
@@ -72,7 +75,7 @@ class DenseDeviceOp:
 
     def prepare(self):
         """Per-factorization setup on the stream (exact mode: digit planes)."""
-        if self.oz is not None:
+        if self.oz is not None and not self.external_planes:
             self.oz.refresh(self.A)
 
     def apply(self, X, out):

@@ -492,14 +492,18 @@ class _PageableUploader:
             self.events = [None, None]
             self.pool = ThreadPoolExecutor(max_workers=self.THREADS)
 
-    def upload(self, dst, arr):
+    def upload(self, dst, arr, stream=None, on_chunk=None):
+        """``stream``: the stream the DMAs are issued on (default: the current
+        one); ``on_chunk(n_elements, event)`` is called after each chunk's DMA
+        has been enqueued, with the flat element count uploaded so far and the
+        event that marks its arrival."""
         self._setup()
         src = arr.reshape(-1)
         flat = dst.view(-1)
         esize = dst.element_size()
         npdt = np.float32 if dst.dtype == torch.float32 else np.float64
         per = self.CHUNK_BYTES // esize
-        stream = torch.cuda.current_stream(dst.device)
+        stream = stream or torch.cuda.current_stream(dst.device)
         for i, off in enumerate(range(0, src.size, per)):
             m = min(per, src.size - off)
             slot = i % 2
@@ -515,10 +519,13 @@ class _PageableUploader:
                     np.copyto(host[a:b], src[off + a: off + b], casting="unsafe")
 
             list(self.pool.map(cp, range(nt)))
-            flat[off: off + m].copy_(self.bufs[slot][: m * esize].view(dst.dtype), non_blocking=True)
+            with torch.cuda.stream(stream):
+                flat[off: off + m].copy_(self.bufs[slot][: m * esize].view(dst.dtype), non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(stream)
             self.events[slot] = ev
+            if on_chunk is not None:
+                on_chunk(off + m, ev)
         for ev in self.events:
             if ev is not None:
                 ev.synchronize()
@@ -527,9 +534,84 @@ class _PageableUploader:
 _UPLOADER = _PageableUploader()
 
 
-def _upload_into(buf, A):
+_COPY_STREAMS = {}
+# rows per panel of the pipelined upload (a multiple of 32)
+_PANEL_BYTES = 256 << 20
+
+
+def _upload_pipelined(buf, A, op):
+    """Exact mode, host input: the upload runs on a copy stream in row panels;
+    as each panel lands, the caller's stream adds its column sums (the
+    finiteness check) and cuts its digit planes (OzPlanes.refresh_rows), so
+    that only the last panel's share of that work (C2: ~1.5 ms in all) is left
+    when the upload ends. Returns the FP64 column sums (device)."""
+    dev = buf.device
+    main = torch.cuda.current_stream(dev)
+    cs = _COPY_STREAMS.get(dev)
+    if cs is None:
+        cs = _COPY_STREAMS[dev] = torch.cuda.Stream(device=dev)
+    start = torch.cuda.Event()
+    start.record(main)
+    cs.wait_event(start)  # earlier work on the caller's stream may still read buf
+    n, d = buf.shape
+    rows = max(32, (_PANEL_BYTES // max(1, d * buf.element_size())) // 32 * 32)
+    sums = torch.zeros(d, dtype=torch.float64, device=dev)
+    part = torch.empty(d, dtype=torch.float64, device=dev)
+    done = [0]
+
+    def rows_landed(r1, ev):
+        # rows [done, r1) are in HBM once ev has fired
+        r0 = done[0]
+        if r1 <= r0:
+            return
+        main.wait_event(ev)
+        ops.colreduce(buf[r0:r1], False, part)
+        sums.add_(part)
+        op.oz.refresh_rows(buf, r0, r1 - r0)
+        done[0] = r1
+
+    if isinstance(A, torch.Tensor):
+        src = A if A.is_contiguous() else A.contiguous()
+        for r0 in range(0, n, rows):
+            r1 = min(n, r0 + rows)
+            with torch.cuda.stream(cs):
+                buf[r0:r1].copy_(src[r0:r1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            rows_landed(r1, ev)
+    else:
+        def on_chunk(n_el, ev):
+            full = n_el // d  # complete rows uploaded so far
+            r1 = n if full >= n else full // rows * rows
+            rows_landed(r1, ev)
+
+        _UPLOADER.upload(buf, A, stream=cs, on_chunk=on_chunk)
+    return sums
+
+
+def _pipelined_ok(A, op, buf):
+    """Host input of the buffer's dtype, exact mode, big enough to be worth panels."""
+    if getattr(op, "oz", None) is None or not getattr(op, "external_planes", False):
+        return False
+    if buf.numel() * buf.element_size() < 2 * _PANEL_BYTES:
+        return False
+    if isinstance(A, torch.Tensor):
+        return (not A.is_cuda) and A.is_pinned() and A.dtype == buf.dtype
+    return isinstance(A, np.ndarray) and A.dtype == np.float32 and A.flags.c_contiguous
+
+
+def _upload_into(buf, A, op=None, defer_check=False):
     """Copy host / device A into the persistent buffer (DMA from pinned
-    memory), with the dense-input validation of make_operator."""
+    memory), with the dense-input validation of make_operator. With ``op`` in
+    exact mode and ``external_planes`` set, the digit planes of A are cut here
+    (pipelined with the upload when the input allows it). ``defer_check``:
+    return the column sums without the host-side finiteness check (the caller
+    checks after launching the factorization)."""
+    if op is not None and _pipelined_ok(A, op, buf):
+        sums = _upload_pipelined(buf, A, op)
+        if not defer_check and not bool(torch.isfinite(sums).all()):
+            raise ValueError("dense matrix entries must be finite")
+        return sums
     if isinstance(A, torch.Tensor):
         src = A if A.is_contiguous() else A.contiguous()
         if src.dtype == buf.dtype:
@@ -550,7 +632,9 @@ def _upload_into(buf, A):
     # only overflow with entries near 1e308)
     sums = torch.empty(buf.shape[1], dtype=torch.float64, device=buf.device)
     ops.colreduce(buf, False, sums)
-    if not bool(torch.isfinite(sums).all()):
+    if op is not None and getattr(op, "oz", None) is not None and getattr(op, "external_planes", False):
+        op.oz.refresh(buf)
+    if not defer_check and not bool(torch.isfinite(sums).all()):
         raise ValueError("dense matrix entries must be finite")
     return sums
 
@@ -574,6 +658,8 @@ def _run(A, cfg, expected, precision="auto", center=False, device=None, comm=Non
             if center:
                 buf.zero_()
             op = DenseDeviceOp(buf, center=center, exact=key[-1] == "exact")
+            # the planes are cut by _upload_into (per row panel, as the upload lands)
+            op.external_planes = op.oz is not None
             pi_host = gaussian(shape[1], cfg.p, SeededRng(cfg.seed)).data
             pi_dev = torch.from_numpy(np.array(pi_host, copy=True)).to(device=dev, dtype=op.dtype)
             entry = [buf, op, GraphedFactorization(op, cfg), pi_dev, 0]
@@ -581,13 +667,16 @@ def _run(A, cfg, expected, precision="auto", center=False, device=None, comm=Non
         buf, op, graphed, pi, calls = entry
         entry[4] = calls + 1
         with torch.cuda.device(dev):
-            sums = _upload_into(buf, A)
+            sums = _upload_into(buf, A, op=op, defer_check=True)
             if center:
                 op.set_column_sums(sums)
             t0 = time.perf_counter()
             # the first call of a shape runs eagerly; a repeated shape is
             # captured once and replayed from then on
             df = run_device(op, cfg, Pi=pi) if calls == 0 else graphed.run(pi)
+            # input validation (matrix.py:80-85) while the factorization runs
+            if not bool(torch.isfinite(sums).all()):
+                raise ValueError("dense matrix entries must be finite")
             return _finish(df, cfg, t0)
     n_total = row_offset = None
     if comm is not None and getattr(comm, "world", 1) > 1:
