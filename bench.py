@@ -608,7 +608,9 @@ def run_ours(args):
             planes = 5 * (-(-n_loc // 128) * 128) * (-(-d // 128) * 128)
             roofline["digit_plane_bytes_per_launch"] = planes
             roofline["digit_plane_gbs"] = planes / (avg_chain_ms * 1e-3) / 1e9
-            roofline["int8_tops"] = 20 * 2.0 * n_loc * d * 64 * (-(-cfg.p // 64)) / (avg_chain_ms * 1e-3) / 1e12
+            # MMA columns per digit pair: the N tile the kernel picks (32 / 56 / 64 per 64 columns)
+            ncols = 32 if cfg.p <= 32 else (56 if cfg.p <= 56 else 64 * (-(-cfg.p // 64)))
+            roofline["int8_tops"] = 20 * 2.0 * n_loc * d * ncols / (avg_chain_ms * 1e-3) / 1e12
             roofline["note"] = ("algorithmic bytes = FP32 A + FP64 blocks; the kernel streams A's int8 digit "
                                 "planes (digit_plane_gbs) and is co-limited by the int8 MMA issue (20 digit pairs)")
             px = _peaks_extra()

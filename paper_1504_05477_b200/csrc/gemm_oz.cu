@@ -79,7 +79,7 @@ struct OzCfg {
     static constexpr int ACC_COLS = LV * BN;
     static_assert(SMEM <= 227 * 1024, "stages do not fit shared memory");
     static_assert(ACC_COLS <= 512, "levels do not fit TMEM");
-    static_assert(STAGE % 1024 == 0, "stage must keep 1024-byte swizzle alignment");
+    static_assert(STAGE % 128 == 0, "stages must stay 128-byte aligned (TMA destinations; no swizzle is used)");
 };
 
 struct OzParams {
@@ -276,7 +276,10 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
                         for (int r0 = 0; r0 < SB * BN; r0 += 256) {
                             if (r0 >= rows) break;
-                            const int nn = (rows - r0) < 256 ? (rows - r0) : 256;
+                            // N is a multiple of 16 (M = 128): with BN = 56 an odd digit count
+                            // rounds up by 8 columns, which land past the last level's columns
+                            // (unused TMEM) and read 8 more rows of the B tile (the next digit)
+                            const int nn = (rows - r0) < 256 ? ((rows - r0 + 15) & ~15) : 256;
                             // B [half][j][c][16 B]: rows j BN + c, 8-row groups SBO 128 B, halves LBO
                             const uint64_t db = make_desc(bst + r0 * 16, SB * BN * 16, 128, kLayoutNone);
                             const uint32_t acc = (kb == 0 && i == 0) ? 0u : 1u;
@@ -297,8 +300,8 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
         // two epilogue warps per lane quarter, each drains half of the columns
         const int half = (warp - 2) / 4;
-        constexpr int HC = BN / 2;      // columns per epilogue thread
-        constexpr int NCH = HC / 16;    // 16-column chunks
+        constexpr int HC = BN / 2;             // columns per epilogue thread
+        constexpr int NCH = (HC + 15) / 16;    // 16-column chunks (the last one partly used when BN = 56)
         // per-column scale 2^(ea + fb - 16) as an exact power-of-two multiply
         // (ldexp's general path, 64 calls per thread, was a large part of a
         // ~20 us per-CTA epilogue), with ldexp kept for exponents outside the
@@ -373,20 +376,21 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             }
             // scale and store, 8 columns (64 bytes of the thread's row) at a time
 #pragma unroll
-            for (int c8 = 0; c8 < HC / 8; ++c8) {
+            for (int c8 = 0; c8 < (HC + 7) / 8; ++c8) {
                 const int c0 = half * HC + c8 * 8;
+                const int lim = HC - c8 * 8 < 8 ? HC - c8 * 8 : 8;  // columns of this thread's half in the chunk
                 const double* vv = &v[c8 / 2][(c8 % 2) * 8];
                 double sc[8];
 #pragma unroll
                 for (int t = 0; t < 8; ++t) {
                     const int64_t col = n0 + c0 + t;
-                    sc[t] = col < p.N ? scale_of(ea + p.fb[col] - 2 * OZ_DB) : 0.0;
+                    sc[t] = (col < p.N && t < lim) ? scale_of(ea + p.fb[col] - 2 * OZ_DB) : 0.0;
                 }
                 if (row < p.M && n0 + c0 < p.N) {
                     const int64_t base =
                         p.direct ? row * p.ldc + n0 + c0 : ((int64_t)z * p.M + row) * p.ldw + n0 + c0;
                     double* out = p.direct ? p.C + base : p.ws + base;
-                    const bool full8 = n0 + c0 + 8 <= p.N && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+                    const bool full8 = lim == 8 && n0 + c0 + 8 <= p.N && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
                     // all loads of the chunk before any store (C is read and written)
                     double cin[8];
                     const bool rmw = p.direct && p.beta != 0.0;
@@ -399,7 +403,7 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                         }
                     } else {
 #pragma unroll
-                        for (int t = 0; t < 8; ++t) cin[t] = (rmw && n0 + c0 + t < p.N) ? out[t] : 0.0;
+                        for (int t = 0; t < 8; ++t) cin[t] = (rmw && t < lim && n0 + c0 + t < p.N) ? out[t] : 0.0;
                     }
                     double res[8];
 #pragma unroll
@@ -415,7 +419,7 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                     } else {
 #pragma unroll
                         for (int t = 0; t < 8; ++t)
-                            if (n0 + c0 + t < p.N) out[t] = res[t];
+                            if (t < lim && n0 + c0 + t < p.N) out[t] = res[t];
                     }
                 }
             }
@@ -697,7 +701,11 @@ int oz_map_b(CUtensorMap* map, const int8_t* planes, int64_t Np, int64_t nkb, in
     return RSVD_OK;
 }
 
-int oz_bn(int64_t n) { return n <= 32 ? 32 : 64; }
+// N tile: 56 for widths 33..56 (C2's p = 50: 12.5 % fewer MMA columns than 64; RSVD_OZ_BN56=0 keeps 64)
+int oz_bn(int64_t n) {
+    static const bool bn56 = !(getenv("RSVD_OZ_BN56") && atoi(getenv("RSVD_OZ_BN56")) == 0);
+    return n <= 32 ? 32 : (n <= 56 && bn56 ? 56 : 64);
+}
 
 // split count: K per CTA <= OZ_MAX_K (exactness), then the smallest count
 // whose CTAs fill the SMs in waves >= 90% full (at most 64, >= 16 K steps
@@ -875,28 +883,25 @@ int oz_gemm_planes(int trans, int64_t n, int64_t d, int64_t p, double alpha, con
     }
     // persistent CTAs, one per SM, over the (split, tile) work units
     dim3 grid((unsigned)std::min<int64_t>(L.m_tiles * L.n_tiles * L.splits, sm_count()), 1, 1);
-    if (reduced) {
-        if (L.bn == 32)
-            rc = tr ? launch_oz<32, true, OZ_LV_R, OZ_LV_R>(tA, tB, prm, grid, st)
-                    : launch_oz<32, false, OZ_LV_R, OZ_LV_R>(tA, tB, prm, grid, st);
-        else
-            rc = tr ? launch_oz<64, true, OZ_LV_R, OZ_LV_R>(tA, tB, prm, grid, st)
-                    : launch_oz<64, false, OZ_LV_R, OZ_LV_R>(tA, tB, prm, grid, st);
-    } else if (nplanes == OZ_SA) {
-        if (L.bn == 32)
-            rc = tr ? launch_oz<32, true, OZ_SA, OZ_LV_A>(tA, tB, prm, grid, st)
-                    : launch_oz<32, false, OZ_SA, OZ_LV_A>(tA, tB, prm, grid, st);
-        else
-            rc = tr ? launch_oz<64, true, OZ_SA, OZ_LV_A>(tA, tB, prm, grid, st)
-                    : launch_oz<64, false, OZ_SA, OZ_LV_A>(tA, tB, prm, grid, st);
-    } else {
-        if (L.bn == 32)
-            rc = tr ? launch_oz<32, true, OZ_SQ, OZ_LV_Q>(tA, tB, prm, grid, st)
-                    : launch_oz<32, false, OZ_SQ, OZ_LV_Q>(tA, tB, prm, grid, st);
-        else
-            rc = tr ? launch_oz<64, true, OZ_SQ, OZ_LV_Q>(tA, tB, prm, grid, st)
-                    : launch_oz<64, false, OZ_SQ, OZ_LV_Q>(tA, tB, prm, grid, st);
-    }
+#define RSVD_OZ_LAUNCH(SA_, LV_)                                                                         \
+    do {                                                                                                 \
+        if (L.bn == 32)                                                                                  \
+            rc = tr ? launch_oz<32, true, SA_, LV_>(tA, tB, prm, grid, st)                               \
+                    : launch_oz<32, false, SA_, LV_>(tA, tB, prm, grid, st);                             \
+        else if (L.bn == 56)                                                                             \
+            rc = tr ? launch_oz<56, true, SA_, LV_>(tA, tB, prm, grid, st)                               \
+                    : launch_oz<56, false, SA_, LV_>(tA, tB, prm, grid, st);                             \
+        else                                                                                             \
+            rc = tr ? launch_oz<64, true, SA_, LV_>(tA, tB, prm, grid, st)                               \
+                    : launch_oz<64, false, SA_, LV_>(tA, tB, prm, grid, st);                             \
+    } while (0)
+    if (reduced)
+        RSVD_OZ_LAUNCH(OZ_LV_R, OZ_LV_R);
+    else if (nplanes == OZ_SA)
+        RSVD_OZ_LAUNCH(OZ_SA, OZ_LV_A);
+    else
+        RSVD_OZ_LAUNCH(OZ_SQ, OZ_LV_Q);
+#undef RSVD_OZ_LAUNCH
     if (rc) return rc;
     if (L.splits > 1) {
         const int64_t tot = Mop * p;
