@@ -87,3 +87,63 @@ def test_c1_regenerated_bitwise_and_reference_outputs():
     # the reference's sigma equals the true spectrum 1/i
     assert np.max(np.abs(g["sigma"] - 1.0 / np.arange(1, 21)) * np.arange(1, 21)) < 1e-13
     assert abs(o.spectral_error_exact(A, r.Z) - g["spectral_exact"][0]) < 1e-13
+
+
+def _ref_kernels():
+    """The reference's own compiled kernel module, built by oracle/build_ref.sh
+    from the sources under /root/reference into oracle/_ref (git-ignored; it
+    travels to the GPU box with the snapshot). None when it was never built."""
+    import importlib.util
+    import sysconfig
+
+    here = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref")
+    path = os.path.join(here, "_kernels" + sysconfig.get_config_var("EXT_SUFFIX"))
+    if not os.path.exists(path):
+        return None
+    spec = importlib.util.spec_from_file_location("_kernels", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_oracle_kernels_bitwise_against_compiled_reference(seed):
+    """oracle/kernels_oracle.c against the reference's compiled _kernels module
+    (backend.py:39-43 binds exactly these five functions) on fresh random
+    inputs, beyond the committed fixtures: Gaussian stream, mm, spmm_nt / spmm_t
+    and the Jacobi sweeps, all bitwise."""
+    ref = _ref_kernels()
+    if ref is None:
+        pytest.skip("oracle/_ref not built (no /root/reference on this machine)")
+    rng = np.random.default_rng(seed)
+    for count in (3, 64, 1001):
+        state = int(rng.integers(1, 2 ** 62))
+        a, sa = o.gauss_fill(count, state)
+        b, sb = ref.gauss_fill(count, state)
+        assert np.array_equal(a, np.asarray(b)) and int(sa) == int(sb)
+    m, k, n = 37, 29, 11
+    A = rng.standard_normal((m, k))
+    B = rng.standard_normal((k, n))
+    assert np.array_equal(o.mm_naive(A, B), np.asarray(ref.mm(A, B)))
+    rows, cols = 40, 31
+    dense = rng.standard_normal((rows, cols)) * (rng.random((rows, cols)) < 0.2)
+    dense[7] = 0.0  # an empty row
+    indptr = np.zeros(rows + 1, dtype=np.int64)
+    indptr[1:] = np.cumsum((dense != 0).sum(1))
+    r, c = np.nonzero(dense)
+    col = c.astype(np.int64)
+    val = dense[r, c].astype(np.float64)
+    X = rng.standard_normal((cols, 5))
+    Y = rng.standard_normal((rows, 5))
+    assert np.array_equal(o.spmm_nt(rows, indptr, col, val, X), np.asarray(ref.spmm_nt(rows, indptr, col, val, X)))
+    assert np.array_equal(o.spmm_t(rows, cols, indptr, col, val, Y),
+                          np.asarray(ref.spmm_t(rows, cols, indptr, col, val, Y)))
+    w = 24
+    S = rng.standard_normal((w, w))
+    S = 0.5 * (S + S.T)
+    M1, V1 = S.copy(), np.eye(w)
+    M2, V2 = S.copy(), np.eye(w)
+    r1 = o.jacobi_sweeps(M1, V1, 1e-14, 50)
+    r2 = ref.jacobi_sweeps(M2, V2, 1e-14, 50)
+    assert np.array_equal(M1, M2) and np.array_equal(V1, V2)
+    assert float(r1[0]) == float(r2[0]) and int(r1[1]) == int(r2[1]) and bool(r1[2]) == bool(r2[2])
