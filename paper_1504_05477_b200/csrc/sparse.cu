@@ -270,13 +270,16 @@ k_spmm_gather_f32(int64_t nchunks, int nb, const int32_t* __restrict__ col, cons
 // the plan; a row's slots are consecutive and k_spmm_split_reduce adds them in
 // order: deterministic, no atomics). Rows without nonzeros are scaled by
 // k_spmm_empty_rows.
+#ifndef RSVD_SPMM_NNZ_MINB
+#define RSVD_SPMM_NNZ_MINB 3
+#endif
 template <int U>
-__global__ void __launch_bounds__(256, U >= 16 ? 2 : 3)
+__global__ void __launch_bounds__(256, U >= 16 ? 2 : RSVD_SPMM_NNZ_MINB)
 k_spmm_nnz_f32(int64_t nnz, int chunk, int64_t nchunks, int nb, const int32_t* __restrict__ col,
                const float* __restrict__ val, const int32_t* __restrict__ rowid, const float* __restrict__ B,
                int64_t ldb, float alpha, float beta, float* __restrict__ C, int64_t ldc,
                const int32_t* __restrict__ head_slot, const int32_t* __restrict__ tail_slot,
-               float* __restrict__ ws) {
+               float* __restrict__ ws, int ablate) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -290,6 +293,7 @@ k_spmm_nnz_f32(int64_t nnz, int chunk, int64_t nchunks, int nb, const int32_t* _
         bool first = true;  // the row being accumulated is the run's first row
         auto flush = [&](bool last) {
             if (!on) return;
+            if ((ablate & 1) && acc.x != 1234.5f) return;  // profiling: no stores
             const int slot = first ? hs : (last ? ts : -1);
             if (slot >= 0) {
                 *reinterpret_cast<float4*>(ws + (int64_t)slot * nb + 4 * lane) = acc;
@@ -318,8 +322,8 @@ k_spmm_nnz_f32(int64_t nnz, int chunk, int64_t nchunks, int nb, const int32_t* _
             float v = 0.f;
             if (e < e1) {
                 c = col[e];
-                v = val[e];
-                r = rowid[e];
+                v = (ablate & 4) ? 1.f : val[e];
+                r = (ablate & 2) ? 0 : rowid[e];
             }
             // padding entries (value 0, column 0) stay in the batch's last row
             const int r_last = __shfl_sync(0xffffffffu, r, cnt - 1);  // every lane takes part in the shuffle
@@ -633,15 +637,16 @@ int spmm_nnz_plan(int64_t nnz, int chunk, int64_t nb, const int32_t* col, const 
         static const int ctas = getenv("RSVD_SPMM_CTAS") ? atoi(getenv("RSVD_SPMM_CTAS")) : 3;
         const unsigned g = (unsigned)std::min<int64_t>(cdiv(nchunks * 32, 256), (int64_t)sm_count() * ctas);
         static const int unroll = getenv("RSVD_SPMM_U") ? atoi(getenv("RSVD_SPMM_U")) : 8;
+        static const int abl = getenv("RSVD_SPMM_ABLATE") ? atoi(getenv("RSVD_SPMM_ABLATE")) : 0;
         if (unroll == 4)
             k_spmm_nnz_f32<4><<<g, 256, 0, st>>>(nnz, chunk, nchunks, (int)nb, col, val, rowid, B, ldb, (float)alpha,
-                                                 (float)beta, C, ldc, head_slot, tail_slot, ws);
+                                                 (float)beta, C, ldc, head_slot, tail_slot, ws, abl);
         else if (unroll == 16)
             k_spmm_nnz_f32<16><<<g, 256, 0, st>>>(nnz, chunk, nchunks, (int)nb, col, val, rowid, B, ldb, (float)alpha,
-                                                  (float)beta, C, ldc, head_slot, tail_slot, ws);
+                                                  (float)beta, C, ldc, head_slot, tail_slot, ws, abl);
         else
             k_spmm_nnz_f32<8><<<g, 256, 0, st>>>(nnz, chunk, nchunks, (int)nb, col, val, rowid, B, ldb, (float)alpha,
-                                                 (float)beta, C, ldc, head_slot, tail_slot, ws);
+                                                 (float)beta, C, ldc, head_slot, tail_slot, ws, abl);
         RSVD_CHECK_LAUNCH();
     }
     if (nsplit > 0) {

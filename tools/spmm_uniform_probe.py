@@ -36,8 +36,11 @@ out = torch.empty((n, b), device=dev)
 def run(label, indptr, col, val):
     plan = ops.SpmmPlan(indptr)
     ms = timed(lambda: ops.spmm_csr_plan(plan, col, val, X, out))
+    nplan = ops.SpmmNnzPlan(indptr)
+    ms2 = timed(lambda: ops.spmm_nnz_plan(nplan, col, val, X, out))
     nnz = val.numel()
-    print(f"{label}: nnz {nnz}, {ms:.3f} ms, {nnz * b * 4 / ms / 1e6:.0f} GB/s of gathered rows", flush=True)
+    print(f"{label}: nnz {nnz}, row plan {ms:.3f} ms ({nnz * b * 4 / ms / 1e6:.0f} GB/s of gathered rows), "
+          f"nnz plan {ms2:.3f} ms ({nnz * b * 4 / ms2 / 1e6:.0f} GB/s)", flush=True)
 
 
 # uniform columns, equal rows
