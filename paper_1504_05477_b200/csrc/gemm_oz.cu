@@ -53,12 +53,13 @@ constexpr int OZ_KS = 32;        // int8 K per MMA = bytes per smem tile row
 constexpr int OZ_DB = 8;         // bits per digit (signed base-256 digits in [-128, 127])
 constexpr int OZ_SA = 5;         // digit planes of an FP32 A (24-bit mantissas, 40 bits below the row scale)
 #ifndef RSVD_OZ_SQ
-#define RSVD_OZ_SQ 7
+#define RSVD_OZ_SQ 6
 #endif
-constexpr int OZ_SQ = RSVD_OZ_SQ;  // digit planes of an FP64 orthonormal basis (56 bits: every FP64 bit of
-                                 // entries down to 2^-3 of the column maximum)
+constexpr int OZ_SQ = RSVD_OZ_SQ;  // digit planes of an FP64 orthonormal basis: 6 = 48 bits below the column
+                                 // scale (7 = 56 bits measured the same C2 parity, 1.995e-6 vs 1.998e-6, for
+                                 // 14 % more plane bytes: C2 28.8 -> 28.4 ms with 6)
 constexpr int OZ_LV_A = 6;       // A products: kept levels i + j <= 5, 6 B digits (20 pairs)
-constexpr int OZ_LV_Q = 7;       // basis products: levels i + j <= 6, 7 B digits (448 TMEM columns at BN 64)
+constexpr int OZ_LV_Q = 7;       // basis products: levels i + j <= 6, 7 B digits, 27 digit pairs (448 TMEM columns at BN 64)
 constexpr int OZ_LV_R = 4;       // reduced A products (levels i + j <= 3, A digits 0..3, 10 pairs): ~1e-10
                                  // relative, for the Rayleigh-Ritz W = A^T Q (its error enters sigma^2
                                  // linearly, against the chain's 1e-15 amplified ~1e9 by the basis)
