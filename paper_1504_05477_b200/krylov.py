@@ -326,11 +326,12 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
     G = ws.G[:p, :p]
     T = ws.T[:p, :p]
     mask = ws.mask[:p]
-    if two_round and tau > 0.0 and ref2 is None:
-        ops.colreduce(V, True, ws.ref_orig[:p])  # original column norms^2
-        comm.allreduce(ws.ref_orig[:p])
     ops.gram(V, G)
     comm.allreduce(G)
+    if two_round and tau > 0.0 and ref2 is None:
+        # original column norms^2 = diag(V^T V): taken from the Gram instead of a
+        # separate pass over V (only round 2's 1e-12 test reads them)
+        ws.ref_orig[:p].copy_(torch.diagonal(G))
     # device-decided sections become CUDA-graph IF nodes under capture
     # (device.cond_section); they must not allocate, so their buffers are
     # made here. NCCL collectives stay out of conditional bodies (world 1 only).
@@ -389,10 +390,13 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
     # before it (residual <= 1e-6 of its norm, factor.py:111) is redrawn from
     # the next vectors of the same fill stream, as the reference's retry loop
     # does (factor.py:106-116); the repair steps run only if that happened.
-    ref_f = ws.ref_fin[:p]
-    ops.colreduce(out, True, ref_f)
-    comm.allreduce(ref_f)
+    # (without a prefix nothing happens between the norms and the Gram: the
+    # Gram's own diagonal is the reference, chol_deflate's default)
+    ref_f = None
     if has_prev:
+        ref_f = ws.ref_fin[:p]
+        ops.colreduce(out, True, ref_f)
+        comm.allreduce(ref_f)
         project_out(ops, comm, Qp, out, tmp_c, basis=basis)
     ops.gram(out, G)
     comm.allreduce(G)
