@@ -75,3 +75,39 @@ def test_exact_si_and_sketch(rk, variant, q):
     rng = np.random.default_rng(5)
     A = (rng.standard_normal((700, 300)) * (np.arange(1, 301) ** -0.7)).astype(np.float32)
     _check(rk, A, 10, variant, q, tol=1e-8)
+
+
+def test_exact_host_inputs_pipelined_upload(rk, monkeypatch):
+    """Public API, exact mode: a pinned host tensor and a pageable numpy array
+    go through the panel-pipelined upload (digit planes cut per row panel as it
+    lands, rsvd_oz_prepare_rows; panels forced small here, with a ragged last
+    panel), a CUDA tensor through the one-shot path: identical digit planes, so
+    the three results are bitwise equal. Non-finite input raises the
+    reference's ValueError on every path (matrix.py:80-85)."""
+    import torch
+
+    from paper_1504_05477_b200 import rsvd
+
+    monkeypatch.setattr(rsvd, "_PANEL_BYTES", 1 << 20)  # 1 MB panels: 7 panels + a ragged tail
+    rng = np.random.default_rng(77)
+    n, d = 6011, 300
+    A = (rng.standard_normal((n, 40)) @ rng.standard_normal((40, d)) / 6.0
+         + 1e-3 * rng.standard_normal((n, d))).astype(np.float32)
+    cfg = rk.RsvdConfig(k=8, variant="bk", q=4, seed=0)
+    outs = []
+    for src in (A, torch.from_numpy(A).pin_memory(), torch.from_numpy(A).cuda()):
+        for _ in range(2):  # second call of a shape replays the captured graph
+            r = rk.factorize(src, cfg)
+        outs.append((r.approx_singular_values.copy(), np.array(r.Z.data)))
+    for s, z in outs[1:]:
+        assert np.array_equal(s, outs[0][0]) and np.array_equal(z, outs[0][1])
+    ref = o.factorize(o.DenseOp(A.astype(np.float64)), 8, "bk", q=4, seed=0)
+    assert np.max(np.abs(outs[0][0] - ref.sigma)) <= 1e-9 * ref.sigma.max()
+    bad = A.copy()
+    bad[n - 3, 17] = np.nan
+    for src in (bad, torch.from_numpy(bad).pin_memory(), torch.from_numpy(bad).cuda()):
+        with pytest.raises(ValueError):
+            rk.factorize(src, cfg)
+    # and the cached graph still works afterwards
+    r = rk.factorize(A, cfg)
+    assert np.array_equal(r.approx_singular_values, outs[0][0])
