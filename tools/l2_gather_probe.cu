@@ -51,6 +51,111 @@ __global__ void __launch_bounds__(256) k_ldg(const float* __restrict__ T, int ld
     if (acc.x + acc.y + acc.z + acc.w == 1234.5f) sink[0] = 1.f;
 }
 
+// like k_ldg<8> but shaped like k_spmm_nnz_f32: each warp owns a contiguous run of
+// RUN indices, multiplies by a per-index value and shuffles a row id along
+template <int U, int RUN>
+__global__ void __launch_bounds__(256, 3) k_run(const float* __restrict__ T, int ld, int nb, const int* __restrict__ idx,
+                                                const float* __restrict__ val, int64_t n, float* sink) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool on = 4 * lane < nb;
+    const int64_t nruns = (n + RUN - 1) / RUN;
+    for (int64_t run = w; run < nruns; run += nw) {
+        const int64_t e0 = run * RUN, e1 = min(n, e0 + RUN);
+        for (int64_t base = e0; base < e1; base += 32) {
+            const int my = base + lane < e1 ? idx[base + lane] : 0;
+            const float mv = base + lane < e1 ? val[base + lane] : 0.f;
+            const int cnt = (int)min((int64_t)32, e1 - base);
+            for (int i = 0; i < cnt; i += U) {
+                int r[U];
+                float vv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    r[u] = __shfl_sync(0xffffffffu, my, i + u);
+                    vv[u] = __shfl_sync(0xffffffffu, mv, i + u);
+                }
+                float4 v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    v[u] = on ? *reinterpret_cast<const float4*>(T + (int64_t)r[u] * ld + 4 * lane) : make_float4(0, 0, 0, 0);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    acc.x = fmaf(vv[u], v[u].x, acc.x); acc.y = fmaf(vv[u], v[u].y, acc.y);
+                    acc.z = fmaf(vv[u], v[u].z, acc.z); acc.w = fmaf(vv[u], v[u].w, acc.w);
+                }
+            }
+        }
+    }
+    if (acc.x + acc.y + acc.z + acc.w == 1234.5f) sink[0] = 1.f;
+}
+
+// k_run + row ids: a finished row is flushed (MODE 1: the flush only counts; MODE 2: it stores the row)
+template <int U, int RUN, int MODE>
+__global__ void __launch_bounds__(256, 3) k_rows(const float* __restrict__ T, int ld, int nb, const int* __restrict__ idx,
+                                                 const float* __restrict__ val, const int* __restrict__ rowid, int64_t n,
+                                                 float* __restrict__ C, float* sink) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const bool on = 4 * lane < nb;
+    const int64_t nruns = (n + RUN - 1) / RUN;
+    float tot = 0.f;
+    for (int64_t run = w; run < nruns; run += nw) {
+        const int64_t e0 = run * RUN, e1 = min(n, e0 + RUN);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        int cur = -1;
+        for (int64_t base = e0; base < e1; base += 32) {
+            const bool in = base + lane < e1;
+            const int my = in ? idx[base + lane] : 0;
+            const float mv = in ? val[base + lane] : 0.f;
+            int rr = in ? rowid[base + lane] : 0;
+            const int cnt = (int)min((int64_t)32, e1 - base);
+            const int rl = __shfl_sync(0xffffffffu, rr, cnt - 1);
+            rr = lane < cnt ? rr : rl;
+            for (int i = 0; i < cnt; i += U) {
+                int r[U], ro[U];
+                float vv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    r[u] = __shfl_sync(0xffffffffu, my, i + u);
+                    vv[u] = __shfl_sync(0xffffffffu, mv, i + u);
+                    ro[u] = __shfl_sync(0xffffffffu, rr, i + u);
+                }
+                float4 v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    v[u] = on ? *reinterpret_cast<const float4*>(T + (int64_t)r[u] * ld + 4 * lane) : make_float4(0, 0, 0, 0);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (ro[u] != cur) {
+                        if (cur >= 0) {
+                            if (MODE == 2) {
+                                if (on) *reinterpret_cast<float4*>(C + (int64_t)cur * ld + 4 * lane) = acc;
+                            } else {
+                                tot += acc.x + acc.y + acc.z + acc.w;
+                            }
+                        }
+                        cur = ro[u];
+                        acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                    acc.x = fmaf(vv[u], v[u].x, acc.x); acc.y = fmaf(vv[u], v[u].y, acc.y);
+                    acc.z = fmaf(vv[u], v[u].z, acc.z); acc.w = fmaf(vv[u], v[u].w, acc.w);
+                }
+            }
+        }
+        if (cur >= 0) {
+            if (MODE == 2) {
+                if (on) *reinterpret_cast<float4*>(C + (int64_t)cur * ld + 4 * lane) = acc;
+            } else {
+                tot += acc.x + acc.y + acc.z + acc.w;
+            }
+        }
+    }
+    if (tot == 1234.5f) sink[0] = 1.f;
+}
+
 template <int S>
 __global__ void __launch_bounds__(256) k_bulk(const float* __restrict__ T, int ld, int nb, const int* __restrict__ idx,
                                               int64_t n, float* sink) {
@@ -148,7 +253,7 @@ int main(int argc, char** argv) {
         cudaError_t err = cudaGetLastError();
         if (err) printf("  error %s\n", cudaGetErrorString(err));
     };
-    for (int ctas : {4, 8}) {
+    for (int ctas : {2, 3, 4, 8}) {
         char nm[64];
         snprintf(nm, 64, "ldg U=2 ctas/sm=%d", ctas);
         run(nm, [&] { k_ldg<2><<<sms * ctas, 256>>>(T, ld, nb, idx, n, sink); });
@@ -157,6 +262,32 @@ int main(int argc, char** argv) {
         snprintf(nm, 64, "ldg U=8 ctas/sm=%d", ctas);
         run(nm, [&] { k_ldg<8><<<sms * ctas, 256>>>(T, ld, nb, idx, n, sink); });
     }
+    {
+        float* val;
+        cudaMalloc(&val, n * 4);
+        cudaMemset(val, 0, n * 4);
+        for (int ctas : {3, 4}) {
+            char nm[64];
+            snprintf(nm, 64, "run1024 U=8 ctas/sm=%d", ctas);
+            run(nm, [&] { k_run<8, 1024><<<sms * ctas, 256>>>(T, ld, nb, idx, val, n, sink); });
+            snprintf(nm, 64, "run32 U=8 ctas/sm=%d", ctas);
+            run(nm, [&] { k_run<8, 32><<<sms * ctas, 256>>>(T, ld, nb, idx, val, n, sink); });
+        }
+        int* rowid;
+        float* C;
+        cudaMalloc(&rowid, n * 4);
+        cudaMalloc(&C, (size_t)200000 * ld * 4);
+        int* hr = (int*)malloc(n * 4);
+        for (int64_t i = 0; i < n; ++i) hr[i] = (int)(i / 54);
+        cudaMemcpy(rowid, hr, n * 4, cudaMemcpyHostToDevice);
+        run("rows54 count U=8 ctas/sm=3", [&] { k_rows<8, 1024, 1><<<sms * 3, 256>>>(T, ld, nb, idx, val, rowid, n, C, sink); });
+        run("rows54 store U=8 ctas/sm=3", [&] { k_rows<8, 1024, 2><<<sms * 3, 256>>>(T, ld, nb, idx, val, rowid, n, C, sink); });
+        // lognormal-ish row lengths: alternate short (5) and long (103) rows, mean 54
+        { int64_t e = 0; int row = 0; while (e < n) { int len = (row & 1) ? 103 : 5; for (int k = 0; k < len && e < n; ++k) hr[e++] = row; ++row; } }
+        cudaMemcpy(rowid, hr, n * 4, cudaMemcpyHostToDevice);
+        run("rows5/103 store U=8 ctas/sm=3", [&] { k_rows<8, 1024, 2><<<sms * 3, 256>>>(T, ld, nb, idx, val, rowid, n, C, sink); });
+    }
+    if (argc > 2) return 0;
     {
         const int smb4 = 8 * 4 * nb * 4, smb8 = 8 * 8 * nb * 4, smb16 = 8 * 16 * nb * 4;
         cudaFuncSetAttribute(k_bulk<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb4);
