@@ -115,6 +115,28 @@ def test_oz_long_reduction_splits():
     assert err < TOL_DGEMM, err
 
 
+def test_oz_wide_reduction_and_extreme_digits():
+    """A X with d > 16384 (the NN reduction split for int32 exactness) on an
+    adversarial operand: every entry of A and X at the same magnitude and sign,
+    so that every digit product has the same sign and the int32 level sums run
+    as high as the scheme allows (7 pairs x 128^2 x 16384 < 2^31); plus the
+    random case."""
+    ops = _ops()
+    n, d, p = 300, 40000, 40
+    for kind in ("extreme", "random"):
+        if kind == "extreme":
+            A = torch.full((n, d), -0.99609375 * 0.5, device="cuda")  # u = -0.498...: digits near -127
+            X = torch.full((d, p), -(1.0 - 2.0 ** -40), device="cuda", dtype=torch.float64)
+        else:
+            A = _case(n, d, 31)
+            X = torch.randn((d, p), device="cuda", dtype=torch.float64)
+        P = ops.OzPlanes(A)
+        C = torch.empty((n, p), dtype=torch.float64, device="cuda")
+        ops.oz_gemm(P, X, C, trans=0)
+        torch.cuda.synchronize()
+        assert _normwise(C, A.double() @ X, A.double(), X) < TOL_DGEMM, kind
+
+
 def test_oz_zero_rows_and_columns():
     """All-zero rows of A and zero columns of B give exact zeros."""
     ops = _ops()
