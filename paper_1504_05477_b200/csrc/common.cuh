@@ -63,21 +63,21 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 // Sense-reversing grid barrier for cooperative launches (all CTAs resident).
 // bar[0] = arrival count (must start at 0), bar[1] = generation.
+// Grid-wide barrier of a cooperative launch (bar[0] zeroed before the launch):
+// ONE atomic per CTA on a counter that only grows -- arrival number `old`
+// belongs to generation old / nblocks, which ends when the counter reaches the
+// next multiple of nblocks -- and a spin on that counter. (The first version
+// reset the counter and bumped a separate generation word: two more dependent
+// L2 round trips per barrier by the last arriver, ~1 us of the ~7 us a column
+// of the grid tridiagonalisation takes.)
 __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned int* gen = bar + 1;
-        unsigned int g = *gen;
         __threadfence();
-        unsigned int arrived = atomicAdd(bar, 1u);
-        if (arrived == nblocks - 1) {
-            atomicExch(bar, 0u);
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (*gen == g) {
-                __nanosleep(32);
-            }
+        const unsigned int old = atomicAdd(bar, 1u);
+        const unsigned int target = (old / nblocks + 1u) * nblocks;
+        volatile unsigned int* cnt = bar;
+        while ((int)(*cnt - target) < 0) {
         }
         __threadfence();
     }
