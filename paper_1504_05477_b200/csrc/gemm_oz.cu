@@ -38,6 +38,7 @@
 // BN = 64) for the whole K range of the CTA; the epilogue reads them once.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -241,7 +242,7 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                             bulk_g2s(dst, p.b_planes + (kk / OZ_KS) * 2 * SB * p.Np * 16, SB * Cfg::B_TILE,
                                      &full[s]);
                         else  // 2 SB runs of BN x 16 B: one TMA box
-                            tma_load_3d(&tmB, &full[s], dst, (int)(n0 * 4), 0, (int)(kk / OZ_KS));
+                            tma_load_3d(&tmB, &full[s], dst, (int)(n0 * 2), 0, (int)(kk / OZ_KS));
                     }
                     if (++s == OZ_STAGES) { s = 0; ph ^= 1; }
                 }
@@ -302,7 +303,10 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         // two epilogue warps per lane quarter, each drains half of the columns
         const int half = (warp - 2) / 4;
         constexpr int HC = BN / 2;             // columns per epilogue thread
-        constexpr int NCH = (HC + 15) / 16;    // 16-column chunks (the last one partly used when BN = 56)
+        constexpr int PC = HC > 32 ? 32 : HC;  // columns per pass (64 FP64 values in registers at most)
+        constexpr int NPS = HC / PC;
+        static_assert(NPS * PC == HC, "passes must tile the thread's columns");
+        constexpr int NCH = (PC + 15) / 16;    // 16-column chunks per pass (the last one partly used when BN = 56)
         // per-column scale 2^(ea + fb - 16) as an exact power-of-two multiply
         // (ldexp's general path, 64 calls per thread, was a large part of a
         // ~20 us per-CTA epilogue), with ldexp kept for exponents outside the
@@ -336,91 +340,105 @@ k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             // 20 % of a chain product). All of the thread's columns are combined
             // before anything is stored, so that TMEM goes back to the MMA issuer
             // after ~2 us and the stores overlap the next unit's main loop.
-            double v[NCH][16];
-#pragma unroll
-            for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-                for (int t = 0; t < 16; ++t) v[ch][t] = 0.0;
+            // (BN = 128, the wide Rayleigh-Ritz product: two passes of 32 columns, TMEM
+            // handed back after the second pass's loads)
             if (nks > 0) {
                 mbar_wait(acc_full, aph);
                 aph ^= 1;
                 tc_fence_after();
                 if (first && warp == 2 && lane == 0) OZ_STAMP(2);
+            }
 #pragma unroll
-                for (int ch = 0; ch < NCH; ++ch) {
-                    const int c0 = half * HC + ch * 16;
+            for (int ps = 0; ps < NPS; ++ps) {
+                const int pb = half * HC + ps * PC;  // first column of the pass
+                double v[NCH][16];
 #pragma unroll
-                    for (int g = NG - 1; g >= 0; --g) {
-                        const int L0 = 3 * g;
-                        const int L1 = L0 + 3 < LV ? L0 + 3 : LV;
-                        int32_t a[3][16];
+                for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
-                        for (int L = 0; L < 3; ++L)
-                            if (L0 + L < L1)
-                                tmem_ld16_s32(tmem_base + lane_off + (uint32_t)((L0 + L) * BN + c0), a[L]);
-                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                        const double wg = pow2(-OZ_DB * (L1 - 1));
+                    for (int t = 0; t < 16; ++t) v[ch][t] = 0.0;
+                if (nks > 0) {
 #pragma unroll
-                        for (int t = 0; t < 16; ++t) {
-                            int64_t h = 0;
+                    for (int ch = 0; ch < NCH; ++ch) {
+                        const int c0 = pb + ch * 16;
+#pragma unroll
+                        for (int g = NG - 1; g >= 0; --g) {
+                            const int L0 = 3 * g;
+                            const int L1 = L0 + 3 < LV ? L0 + 3 : LV;
+                            int32_t a[3][16];
 #pragma unroll
                             for (int L = 0; L < 3; ++L)
-                                if (L0 + L < L1) h = h * (1 << OZ_DB) + a[L][t];
-                            v[ch][t] = fma((double)h, wg, v[ch][t]);
+                                if (L0 + L < L1)
+                                    tmem_ld16_s32(tmem_base + lane_off + (uint32_t)((L0 + L) * BN + c0), a[L]);
+                            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                            const double wg = pow2(-OZ_DB * (L1 - 1));
+#pragma unroll
+                            for (int t = 0; t < 16; ++t) {
+                                int64_t h = 0;
+#pragma unroll
+                                for (int L = 0; L < 3; ++L)
+                                    if (L0 + L < L1) h = h * (1 << OZ_DB) + a[L][t];
+                                v[ch][t] = fma((double)h, wg, v[ch][t]);
+                            }
                         }
                     }
-                }
-                // accumulators read: hand TMEM back
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(tmem_empty);
-            }
-            // scale and store, 8 columns (64 bytes of the thread's row) at a time
-#pragma unroll
-            for (int c8 = 0; c8 < (HC + 7) / 8; ++c8) {
-                const int c0 = half * HC + c8 * 8;
-                const int lim = HC - c8 * 8 < 8 ? HC - c8 * 8 : 8;  // columns of this thread's half in the chunk
-                const double* vv = &v[c8 / 2][(c8 % 2) * 8];
-                double sc[8];
-#pragma unroll
-                for (int t = 0; t < 8; ++t) {
-                    const int64_t col = n0 + c0 + t;
-                    sc[t] = (col < p.N && t < lim) ? scale_of(ea + p.fb[col] - 2 * OZ_DB) : 0.0;
-                }
-                if (row < p.M && n0 + c0 < p.N) {
-                    const int64_t base =
-                        p.direct ? row * p.ldc + n0 + c0 : ((int64_t)z * p.M + row) * p.ldw + n0 + c0;
-                    double* out = p.direct ? p.C + base : p.ws + base;
-                    const bool full8 = lim == 8 && n0 + c0 + 8 <= p.N && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-                    // all loads of the chunk before any store (C is read and written)
-                    double cin[8];
-                    const bool rmw = p.direct && p.beta != 0.0;
-                    if (rmw && full8) {
-#pragma unroll
-                        for (int t = 0; t < 8; t += 2) {
-                            const double2 c2 = *reinterpret_cast<const double2*>(out + t);
-                            cin[t] = c2.x;
-                            cin[t + 1] = c2.y;
-                        }
-                    } else {
-#pragma unroll
-                        for (int t = 0; t < 8; ++t) cin[t] = (rmw && t < lim && n0 + c0 + t < p.N) ? out[t] : 0.0;
+                    if (ps == NPS - 1) {
+                        // accumulators read: hand TMEM back
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(tmem_empty);
                     }
-                    double res[8];
+                }
+                // scale and store, 8 columns (64 bytes of the thread's row) at a time
+#pragma unroll
+                for (int c8 = 0; c8 < (PC + 7) / 8; ++c8) {
+                    const int c0 = pb + c8 * 8;
+                    const int left = HC - ps * PC - c8 * 8;
+                    const int lim = left < 8 ? left : 8;  // columns of this thread's half in the chunk
+                    const double* vv = &v[c8 / 2][(c8 % 2) * 8];
+                    double sc[8];
 #pragma unroll
                     for (int t = 0; t < 8; ++t) {
-                        const double val = sc[t] != 0.0 ? vv[t] * sc[t]
-                                                        : ldexp(vv[t], ea + p.fb[min(n0 + c0 + t, p.N - 1)] - 2 * OZ_DB);
-                        res[t] = p.direct ? (rmw ? p.alpha * val + p.beta * cin[t] : p.alpha * val) : val;
+                        const int64_t col = n0 + c0 + t;
+                        sc[t] = (col < p.N && t < lim) ? scale_of(ea + p.fb[col] - 2 * OZ_DB) : 0.0;
                     }
-                    if (full8) {
+                    if (row < p.M && n0 + c0 < p.N) {
+                        const int64_t base =
+                            p.direct ? row * p.ldc + n0 + c0 : ((int64_t)z * p.M + row) * p.ldw + n0 + c0;
+                        double* out = p.direct ? p.C + base : p.ws + base;
+                        const bool full8 =
+                            lim == 8 && n0 + c0 + 8 <= p.N && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+                        // all loads of the chunk before any store (C is read and written)
+                        double cin[8];
+                        const bool rmw = p.direct && p.beta != 0.0;
+                        if (rmw && full8) {
 #pragma unroll
-                        for (int t = 0; t < 8; t += 2)
-                            *reinterpret_cast<double2*>(out + t) = make_double2(res[t], res[t + 1]);
-                    } else {
+                            for (int t = 0; t < 8; t += 2) {
+                                const double2 c2 = *reinterpret_cast<const double2*>(out + t);
+                                cin[t] = c2.x;
+                                cin[t + 1] = c2.y;
+                            }
+                        } else {
 #pragma unroll
-                        for (int t = 0; t < 8; ++t)
-                            if (t < lim && n0 + c0 + t < p.N) out[t] = res[t];
+                            for (int t = 0; t < 8; ++t)
+                                cin[t] = (rmw && t < lim && n0 + c0 + t < p.N) ? out[t] : 0.0;
+                        }
+                        double res[8];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            const double val =
+                                sc[t] != 0.0 ? vv[t] * sc[t]
+                                             : ldexp(vv[t], ea + p.fb[min(n0 + c0 + t, p.N - 1)] - 2 * OZ_DB);
+                            res[t] = p.direct ? (rmw ? p.alpha * val + p.beta * cin[t] : p.alpha * val) : val;
+                        }
+                        if (full8) {
+#pragma unroll
+                            for (int t = 0; t < 8; t += 2)
+                                *reinterpret_cast<double2*>(out + t) = make_double2(res[t], res[t + 1]);
+                        } else {
+#pragma unroll
+                            for (int t = 0; t < 8; ++t)
+                                if (t < lim && n0 + c0 + t < p.N) out[t] = res[t];
+                        }
                     }
                 }
             }
@@ -691,11 +709,12 @@ int oz_map_a(CUtensorMap* map, const int8_t* planes, int64_t a_rows, int64_t d_p
 int oz_map_b(CUtensorMap* map, const int8_t* planes, int64_t Np, int64_t nkb, int bn, int sb) {
     EncodeTiledFn fn = encode_fn();
     RSVD_REQUIRE(fn != nullptr, "cuTensorMapEncodeTiled unavailable");
-    cuuint64_t dims[3] = {(cuuint64_t)(Np * 4), (cuuint64_t)(2 * sb), (cuuint64_t)nkb};
+    // u64 view (a 16-byte row piece = 2 elements): the box's inner extent stays <= 256 at BN = 128
+    cuuint64_t dims[3] = {(cuuint64_t)(Np * 2), (cuuint64_t)(2 * sb), (cuuint64_t)nkb};
     cuuint64_t strides[2] = {(cuuint64_t)(Np * 16), (cuuint64_t)(2 * sb * Np * 16)};
-    cuuint32_t box[3] = {(cuuint32_t)(bn * 4), (cuuint32_t)(2 * sb), 1};
+    cuuint32_t box[3] = {(cuuint32_t)(bn * 2), (cuuint32_t)(2 * sb), 1};
     cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<int8_t*>(planes), dims, strides, box, estr,
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<int8_t*>(planes), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     RSVD_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (Ozaki B planes) failed (%d)", (int)r);
@@ -703,8 +722,14 @@ int oz_map_b(CUtensorMap* map, const int8_t* planes, int64_t Np, int64_t nkb, in
 }
 
 // N tile: 56 for widths 33..56 (C2's p = 50: 12.5 % fewer MMA columns than 64; RSVD_OZ_BN56=0 keeps 64)
-int oz_bn(int64_t n) {
+// Wide reduced products (the Rayleigh-Ritz W = A^T Q, 4 levels): 128, so that an
+// A tile is streamed from L2 once per 128 output columns instead of once per 64
+// (C2: the 10 N tiles of width 600 re-read the planes 10 x, 20 GB of L2 -> SM
+// traffic in 2.26 ms; RSVD_OZ_BN128=0 keeps 64)
+int oz_bn(int64_t n, bool reduced = false) {
     static const bool bn56 = !(getenv("RSVD_OZ_BN56") && atoi(getenv("RSVD_OZ_BN56")) == 0);
+    static const bool bn128 = !(getenv("RSVD_OZ_BN128") && atoi(getenv("RSVD_OZ_BN128")) == 0);
+    if (reduced && n > 64 && bn128) return 128;
     return n <= 32 ? 32 : (n <= 56 && bn56 ? 56 : 64);
 }
 
@@ -739,9 +764,9 @@ struct OzLayout {
     int64_t planes_off, colmax_off, fb_off, part_off, total;
 };
 
-OzLayout oz_layout(bool trans, int64_t n, int64_t d, int64_t p) {
+OzLayout oz_layout(bool trans, int64_t n, int64_t d, int64_t p, bool reduced = false) {
     OzLayout L{};
-    L.bn = oz_bn(p);
+    L.bn = oz_bn(p, reduced);
     const int64_t Mop = trans ? d : n, Kop = trans ? n : d;
     L.Np = cdiv(p, L.bn) * L.bn;
     L.Kp = cdiv(Kop, 32) * 32;
@@ -807,7 +832,8 @@ int oz_prepare_rows(int64_t n, int64_t d, int64_t r0, int64_t nr, const float* A
 }
 
 int64_t oz_gemm_ws_bytes(int trans, int64_t n, int64_t d, int64_t p) {
-    return oz_layout(trans != 0, n, d, p).total;
+    // covers the reduced (wide N tile) layout of the same product too
+    return std::max(oz_layout(trans != 0, n, d, p, false).total, oz_layout(trans != 0, n, d, p, true).total);
 }
 
 // trans = 0: C (n x p) = alpha A X + beta C, X d x p.
@@ -827,7 +853,7 @@ int oz_gemm_planes(int trans, int64_t n, int64_t d, int64_t p, double alpha, con
     RSVD_REQUIRE(nplanes == OZ_SA || nplanes == OZ_SQ, "oz_gemm: %d digit planes not supported", nplanes);
     RSVD_REQUIRE(rows_alloc % 128 == 0 && cols_alloc % 128 == 0 && rows_alloc >= n && cols_alloc >= d,
                  "oz_gemm: plane geometry does not cover the product");
-    const OzLayout L = oz_layout(tr, n, d, p);
+    const OzLayout L = oz_layout(tr, n, d, p, reduced != 0);
     RSVD_REQUIRE(ws_bytes >= L.total, "oz_gemm: workspace too small (%lld < %lld)", (long long)ws_bytes,
                  (long long)L.total);
     RSVD_REQUIRE((reinterpret_cast<uintptr_t>(planes) & 15) == 0, "oz_gemm: digit planes must be 16-byte aligned");
@@ -896,7 +922,10 @@ int oz_gemm_planes(int trans, int64_t n, int64_t d, int64_t p, double alpha, con
             rc = tr ? launch_oz<64, true, SA_, LV_>(tA, tB, prm, grid, st)                               \
                     : launch_oz<64, false, SA_, LV_>(tA, tB, prm, grid, st);                             \
     } while (0)
-    if (reduced)
+    if (reduced && L.bn == 128)
+        rc = tr ? launch_oz<128, true, OZ_LV_R, OZ_LV_R>(tA, tB, prm, grid, st)
+                : launch_oz<128, false, OZ_LV_R, OZ_LV_R>(tA, tB, prm, grid, st);
+    else if (reduced)
         RSVD_OZ_LAUNCH(OZ_LV_R, OZ_LV_R);
     else if (nplanes == OZ_SA)
         RSVD_OZ_LAUNCH(OZ_SA, OZ_LV_A);

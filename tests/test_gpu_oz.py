@@ -183,10 +183,13 @@ def test_oz_basis_projections(jp):
     assert e_nn < TOL, e_nn
 
 
-def test_oz_reduced_levels():
-    """The Rayleigh-Ritz variant (digit levels i + j <= 3): ~1e-10 normwise."""
+@pytest.mark.parametrize("p", [64, 200, 600])
+def test_oz_reduced_levels(p):
+    """The Rayleigh-Ritz variant (digit levels i + j <= 3): ~1e-10 normwise;
+    widths above 64 run the 128-column N tile (two epilogue passes, u64 TMA
+    view of the B planes), 600 = C2's Krylov width with a ragged last tile."""
     ops = _ops()
-    n, d, p = 5000, 700, 64
+    n, d = 5000, 700
     A = _case(n, d, 21)
     A64 = A.double()
     Y = torch.randn((n, p), device="cuda", dtype=torch.float64)
