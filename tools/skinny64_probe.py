@@ -34,3 +34,11 @@ print(f"V T -> out: {timed(lambda: ops.gemm_nn(V, T, out)):.1f} us; "
       f"out += V T: {timed(lambda: ops.gemm_nn(V, T, out, alpha=-1.0, beta=1.0)):.1f} us; "
       f"Gram: {timed(lambda: ops.gram(V, G)):.1f} us; "
       f"chol p=50: {timed(lambda: ops.chol_deflate(G @ G.T + 50 * torch.eye(p, device='cuda', dtype=torch.float64), None, 1e-14, T.clone(), torch.empty(p, dtype=torch.int32, device='cuda'), torch.zeros(2, dtype=torch.int32, device='cuda'))):.1f} us (with torch setup)")
+
+# floor for these shapes: a strided copy of the same block (read 20 MB, write 20 MB)
+print(f"torch copy V -> out: {timed(lambda: out.copy_(V)):.1f} us; convert kernel: {timed(lambda: ops.convert(V, out)):.1f} us; "
+      f"colreduce: {timed(lambda: ops.colreduce(V, True)):.1f} us")
+Vc = torch.randn((n, p), device="cuda", dtype=torch.float64)
+oc = torch.empty((n, p), device="cuda", dtype=torch.float64)
+print(f"contiguous operands: V T {timed(lambda: ops.gemm_nn(Vc, T, oc)):.1f} us, Gram {timed(lambda: ops.gram(Vc, G)):.1f} us, "
+      f"copy {timed(lambda: oc.copy_(Vc)):.1f} us")
