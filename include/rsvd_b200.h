@@ -83,6 +83,29 @@ int rsvd_gauss_fill(int64_t count, uint64_t state, double *out, uint64_t *new_st
 int rsvd_gemm_nn(int dtype, int64_t m, int64_t n, int64_t k, double alpha, const void *A,
                  int64_t lda, const void *B, int64_t ldb, double beta, void *C, int64_t ldc,
                  const double *row_sub, int algo, const int32_t *pred, void *stream);
+/* Split planes of an FP32 block (K x N, row pitch ldb) as the B operand of the
+ * tcgen05 3xTF32 products: hi = TF32 truncation, lo = rna_tf32(x - hi), k-blocked
+ * K-major. rsvd_gemm_nn_f32_emit is rsvd_gemm_nn (FP32) that also writes the
+ * planes of its OUTPUT C from the epilogue (*emitted = 1; 0 when the shape took
+ * a non-tensor-core path and only C was written), so that a following
+ * rsvd_gemm_tn_f32_planes -- rsvd_gemm_tn with B given by its planes, B's row
+ * index being the reduction index -- needs no pass over B. Both replace mm
+ * (_kernels.pyx:56-71) inside _mgs's projections (factor.py:93-98).
+ * rsvd_gemm_tn_f32_planes_ok: 1 when that product's shape runs on the tensor
+ * cores (else use rsvd_gemm_tn). */
+int64_t rsvd_split_planes_bytes(int64_t K, int64_t N);
+int rsvd_split_planes(int64_t K, int64_t N, const float *B, int64_t ldb, float *planes,
+                      int64_t planes_bytes, const int32_t *pred, void *stream);
+int rsvd_gemm_nn_f32_emit(int64_t m, int64_t n, int64_t k, double alpha, const float *A, int64_t lda,
+                          const float *B, int64_t ldb, double beta, float *C, int64_t ldc,
+                          const double *row_sub, float *planes, int64_t planes_bytes,
+                          int32_t *emitted, const int32_t *pred, void *stream);
+int rsvd_gemm_tn_f32_planes(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha,
+                            const float *A, int64_t lda, const float *B_planes,
+                            int64_t planes_bytes, double beta, void *C, int64_t ldc,
+                            const double *mu, const double *colsum_b, void *ws, int64_t ws_bytes,
+                            const int32_t *pred, void *stream);
+int rsvd_gemm_tn_f32_planes_ok(int64_t m, int64_t n, int64_t k, const float *A, int64_t lda);
 int64_t rsvd_gemm_tn_ws_bytes(int dtype, int64_t m, int64_t n, int64_t k, int algo);
 int rsvd_gemm_tn(int dtype, int out_dtype, int64_t m, int64_t n, int64_t k, double alpha,
                  const void *A, int64_t lda, const void *B, int64_t ldb, double beta, void *C,

@@ -62,6 +62,13 @@ _SIGS = {
     "rsvd_canonicalize_signs": ([_int, _i64, _i64, _vp, _i64, _vp, _i64, _vp], _int),
     "rsvd_col_absargmax": ([_int, _i64, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _i64, _vp], _int),
     "rsvd_flip_by_sign": ([_int, _i64, _i64, _vp, _i64, _vp, _vp], _int),
+    "rsvd_split_planes_bytes": ([_i64, _i64], _i64),
+    "rsvd_split_planes": ([_i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp], _int),
+    "rsvd_gemm_nn_f32_emit": ([_i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64, _vp, _vp, _i64, _vp, _vp,
+                               _vp], _int),
+    "rsvd_gemm_tn_f32_planes": ([_int, _i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64, _vp, _vp, _vp,
+                                 _i64, _vp, _vp], _int),
+    "rsvd_gemm_tn_f32_planes_ok": ([_i64, _i64, _i64, _vp, _i64], _int),
     "rsvd_convert": ([_int, _int, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp], _int),
     "rsvd_gather_rows": ([_int, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp], _int),
     "rsvd_scatter_rows": ([_int, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp], _int),

@@ -167,6 +167,50 @@ int rsvd_oz_gemm_planes(int trans, int64_t n, int64_t d, int64_t p, double alpha
                           beta, C, ldc, ws, ws_bytes, pred, as_stream(stream));
 }
 
+int64_t rsvd_split_planes_bytes(int64_t K, int64_t N) { return (K < 0 || N < 0) ? 0 : split_planes_bytes(K, N); }
+
+int rsvd_split_planes(int64_t K, int64_t N, const float* B, int64_t ldb, float* planes, int64_t planes_bytes,
+                      const int32_t* pred, void* stream) {
+    RSVD_REQUIRE(K >= 0 && N >= 0 && ldb >= N, "split_planes: bad shape");
+    RSVD_REQUIRE(planes_bytes >= split_planes_bytes(K, N), "split_planes: plane buffer too small");
+    return split_planes(K, N, B, ldb, planes, pred, as_stream(stream));
+}
+
+int rsvd_gemm_nn_f32_emit(int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t lda, const float* B,
+                          int64_t ldb, double beta, float* C, int64_t ldc, const double* row_sub, float* planes,
+                          int64_t planes_bytes, int32_t* emitted, const int32_t* pred, void* stream) {
+    RSVD_REQUIRE(m >= 0 && n >= 0 && k >= 0, "gemm_nn_emit: negative dimension");
+    RSVD_REQUIRE(lda >= k && ldb >= n && ldc >= n, "gemm_nn_emit: leading dimension too small");
+    RSVD_REQUIRE(emitted != nullptr, "gemm_nn_emit: null pointer");
+    cudaStream_t st = as_stream(stream);
+    *emitted = 0;
+    // planes come out of the tcgen05 kernel's epilogue; any other path computes C only
+    if (planes != nullptr && !gemm_skinny_nn_supported(n, k) && gemm_tc_nn_supported(m, n, k, lda, ldb, ldc, A, B)) {
+        RSVD_REQUIRE(planes_bytes >= split_planes_bytes(m, n), "gemm_nn_emit: plane buffer too small");
+        *emitted = 1;
+        return gemm_nn_tc(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, row_sub, pred, st, planes);
+    }
+    return rsvd_gemm_nn(RSVD_F32, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, row_sub, RSVD_GEMM_AUTO, pred, stream);
+}
+
+int rsvd_gemm_tn_f32_planes(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, const float* A,
+                            int64_t lda, const float* B_planes, int64_t planes_bytes, double beta, void* C,
+                            int64_t ldc, const double* mu, const double* colsum_b, void* ws, int64_t ws_bytes,
+                            const int32_t* pred, void* stream) {
+    RSVD_REQUIRE(valid_dtype(out_dtype), "gemm_tn_planes: bad dtype");
+    RSVD_REQUIRE(m >= 0 && n >= 0 && k >= 0 && lda >= k && ldc >= n, "gemm_tn_planes: bad shape");
+    RSVD_REQUIRE((mu == nullptr) == (colsum_b == nullptr), "gemm_tn_planes: mu and colsum_b go together");
+    RSVD_REQUIRE(B_planes != nullptr && planes_bytes >= split_planes_bytes(m, n), "gemm_tn_planes: plane buffer");
+    RSVD_REQUIRE(gemm_tc_tn_supported(m, n, k, lda, n, A, B_planes),
+                 "gemm_tn_planes: shape/alignment not supported by the tcgen05 kernel");
+    return gemm_tn_tc(out_dtype, m, n, k, alpha, A, lda, nullptr, n, beta, C, ldc, mu, colsum_b, ws, ws_bytes, pred,
+                      as_stream(stream), B_planes);
+}
+
+int rsvd_gemm_tn_f32_planes_ok(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda) {
+    return (!gemm_skinny_tn_supported(n, k) && gemm_tc_tn_supported(m, n, k, lda, n, A, A)) ? 1 : 0;
+}
+
 int64_t rsvd_gemm_tn_ws_bytes(int dtype, int64_t m, int64_t n, int64_t k, int algo) {
     int64_t a = gemm_tn_simt_ws_bytes(m, n, k);
     if (dtype == RSVD_F64 && algo != RSVD_GEMM_SIMT) {

@@ -22,14 +22,17 @@ bool gemm_tc_nn_supported(int64_t m, int64_t n, int64_t k, int64_t lda, int64_t 
                           int64_t ldc, const void* A, const void* B);
 int gemm_nn_tc(int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t lda,
                const float* B, int64_t ldb, double beta, float* C, int64_t ldc,
-               const double* row_sub, const int32_t* pred, cudaStream_t st);
+               const double* row_sub, const int32_t* pred, cudaStream_t st, float* emit = nullptr);
+int64_t split_planes_bytes(int64_t K, int64_t N);
+int split_planes(int64_t K, int64_t N, const float* B, int64_t ldb, float* planes, const int32_t* pred,
+                 cudaStream_t st);
 bool gemm_tc_tn_supported(int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb,
                           const void* A, const void* B);
 int64_t gemm_tn_tc_ws_bytes(int64_t m, int64_t n, int64_t k);
 int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, const float* A,
                int64_t lda, const float* B, int64_t ldb, double beta, void* C, int64_t ldc,
                const double* mu, const double* cs, void* ws, int64_t ws_bytes, const int32_t* pred,
-               cudaStream_t st);
+               cudaStream_t st, const float* b_planes = nullptr);
 
 // FP64 tensor-core (mma.sync f64) kernels (gemm_dmma.cu).
 int gemm_nn_dmma(int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda,

@@ -77,6 +77,11 @@ struct TcParams {
     int sub_vec;            // direct, alpha = 1, beta = 0, row_sub, C rows 16-byte aligned, N % 4 == 0
     const int32_t* pred;
     int n_tiles;            // N tiles per M tile (blockIdx.x = m_tile * n_tiles + n_tile)
+    // direct epilogue only: also write C's hi / lo planes in the k-blocked split-B
+    // layout (k index = C's row), ready to be the B operand of a following TN
+    // product -- instead of a k_split_b pass over C (read C, write 2 planes)
+    float* emit;
+    int64_t emit_np;        // rows per emitted plane (C's columns rounded up to 32)
 };
 
 // Profiling ablations (tools/ablate_tc.py builds variants; 0 in the product):
@@ -157,6 +162,7 @@ __device__ __forceinline__ void drain_epilogue(const TcParams& p, uint32_t tmem_
                                              (float)((double)sum[i + 2] - rs[i + 2]),
                                              (float)((double)sum[i + 3] - rs[i + 3]));
                 *reinterpret_cast<float4*>(out + i) = v;
+                sum[i] = v.x; sum[i + 1] = v.y; sum[i + 2] = v.z; sum[i + 3] = v.w;
             }
         }
     } else if (row < p.M && (!p.direct || p.plain_vec)) {
@@ -194,6 +200,8 @@ __device__ __forceinline__ void drain_epilogue(const TcParams& p, uint32_t tmem_
                     res[t] = (float)r;
                 }
                 *reinterpret_cast<float4*>(crow) = make_float4(res[0], res[1], res[2], res[3]);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) sum[i + t] = res[t];
             } else if (p.direct) {
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
@@ -204,8 +212,27 @@ __device__ __forceinline__ void drain_epilogue(const TcParams& p, uint32_t tmem_
                         r *= p.alpha;
                         if (p.beta != 0.0) r += p.beta * (double)p.C[row * p.ldc + col];
                         p.C[row * p.ldc + col] = (float)r;
+                        sum[i + t] = (float)r;
                     }
                 }
+            }
+        }
+    }
+    // sum[] now holds the stored values of this lane's row. Emission: lanes of a
+    // warp are 32 consecutive rows of one 32-row k-block, so for a fixed column
+    // the warp writes one contiguous 128-byte run per plane (rows past M, up to
+    // the end of the last k-block, are written as zeros like k_split_b does)
+    if (p.direct && p.emit != nullptr && row < (p.M + 31) / 32 * 32) {
+        const int ncols = (int)min((int64_t)BN, p.N - n0);
+        float* blk = p.emit + (row / 32) * (2 * p.emit_np) * 32 + (row % 32);
+        const bool live = row < p.M;
+#pragma unroll
+        for (int i = 0; i < BN; ++i) {
+            if (i < ncols) {
+                const float x = live ? sum[i] : 0.f;
+                const float h = tf32_hi(x);
+                blk[(n0 + i) * 32] = h;
+                blk[(p.emit_np + n0 + i) * 32] = tf32_rna(x - h);
             }
         }
     }
@@ -909,9 +936,17 @@ bool gemm_tc_nn_supported(int64_t m, int64_t n, int64_t k, int64_t lda, int64_t 
     return m >= BM && k >= BK && n >= 1 && (lda % 4) == 0 && aligned16(A) && m < (1ll << 31) && k < (1ll << 31);
 }
 
+int64_t split_planes_bytes(int64_t K, int64_t N) { return 2 * (cdiv(K, BK) * BK) * (cdiv(N, 32) * 32) * 4; }
+
+int split_planes(int64_t K, int64_t N, const float* B, int64_t ldb, float* planes, const int32_t* pred,
+                 cudaStream_t st) {
+    if (K == 0 || N == 0) return RSVD_OK;
+    return split_b(B, K, N, ldb, cdiv(K, BK) * BK, cdiv(N, 32) * 32, planes, pred, st);
+}
+
 int gemm_nn_tc(int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t lda, const float* B,
                int64_t ldb, double beta, float* C, int64_t ldc, const double* row_sub, const int32_t* pred,
-               cudaStream_t st) {
+               cudaStream_t st, float* emit) {
     int bn = pick_bn(n);
     // planes padded to 32 rows only: a last N tile's hi box may run into the lo
     // plane (and its lo box past 2 Np, zero-filled) -- those rows feed output
@@ -934,6 +969,8 @@ int gemm_nn_tc(int64_t m, int64_t n, int64_t k, double alpha, const float* A, in
     p.c_vec = ldc % 4 == 0 && aligned16(C);
     p.sub_vec = alpha == 1.0 && beta == 0.0 && row_sub != nullptr && ldc % 4 == 0 && n % 4 == 0 && aligned16(C);
     p.pred = pred;
+    p.emit = emit;
+    p.emit_np = cdiv(n, 32) * 32;
     p.n_tiles = (int)cdiv(n, bn);
     // (a split-K variant for wave balance -- C2: 391 tiles = 2.64 waves -- was
     // measured no faster: 2 / 3 / 4 splits 0.452 / 0.443 / 0.454 ms vs 0.441)
@@ -955,7 +992,7 @@ int64_t gemm_tn_tc_ws_bytes(int64_t m, int64_t n, int64_t k) {
 
 int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, const float* A, int64_t lda,
                const float* B, int64_t ldb, double beta, void* C, int64_t ldc, const double* mu, const double* cs,
-               void* ws, int64_t ws_bytes, const int32_t* pred, cudaStream_t st) {
+               void* ws, int64_t ws_bytes, const int32_t* pred, cudaStream_t st, const float* b_planes) {
     // operand view: D[Mop x Nop] = A^T[Mop x Kop] B[Kop x Nop], Mop = k, Kop = m
     const int64_t Mop = k, Nop = n, Kop = m;
     int bn = pick_bn(Nop);
@@ -963,11 +1000,18 @@ int gemm_tn_tc(int out_dtype, int64_t m, int64_t n, int64_t k, double alpha, con
     RSVD_REQUIRE(ws_bytes >= S * Mop * cdiv(Nop, 4) * 4 * 4, "gemm_tn_tc: workspace too small");
     RSVD_REQUIRE(aligned16(ws), "gemm_tn_tc: workspace must be 16-byte aligned");
     const int64_t Kp = cdiv(Kop, BK) * BK, Np = cdiv(Nop, 32) * 32;  // see gemm_nn_tc
-    static thread_local PerDevice<Scratch> sc_dev;
-    float* bs = scratch_get(sc_dev.get(), (size_t)(2 * Kp * Np * 4), st);
-    RSVD_REQUIRE(bs != nullptr, "gemm_tn_tc: scratch allocation failed");
-    int rc = split_b(B, Kop, Nop, ldb, Kp, Np, bs, pred, st);
-    if (rc) return rc;
+    // B already split by the caller (planes emitted by the NN product that wrote B,
+    // or rsvd_split_planes): no pass over B here
+    const float* bs = b_planes;
+    int rc = RSVD_OK;
+    if (bs == nullptr) {
+        static thread_local PerDevice<Scratch> sc_dev;
+        float* sb = scratch_get(sc_dev.get(), (size_t)(2 * Kp * Np * 4), st);
+        RSVD_REQUIRE(sb != nullptr, "gemm_tn_tc: scratch allocation failed");
+        rc = split_b(B, Kop, Nop, ldb, Kp, Np, sb, pred, st);
+        if (rc) return rc;
+        bs = sb;
+    }
     CUtensorMap tA, tB;
     rc = make_map(&tA, A, k /*inner = columns of A*/, m, lda, BK, true);
     if (rc) return rc;

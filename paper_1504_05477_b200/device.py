@@ -120,19 +120,83 @@ class _Workspace:
 WS = _Workspace()
 
 
-def gemm_nn(A, B, C, alpha=1.0, beta=0.0, row_sub=None, algo=GEMM_AUTO, pred=None):
+class SplitPlanes:
+    """hi / lo split planes of an FP32 block as the B operand of the tcgen05
+    3xTF32 TN products (rsvd_split_planes layout), with the identity of the
+    block they currently describe. ``gemm_nn(..., emit=planes)`` fills them
+    from the product's epilogue; ``gemm_tn(..., b_planes=planes)`` uses them
+    when they describe its B (no k_split_b pass over B). One buffer per
+    (device, stream), grown on demand (SplitPlanes.get)."""
+
+    _cache = {}
+
+    def __init__(self, nbytes, device):
+        self.buf = torch.empty(int(nbytes), dtype=torch.uint8, device=device)
+        self.key = None
+
+    @classmethod
+    def get(cls, rows, cols, device):
+        dev = torch.device(device)
+        sp = torch.cuda.current_stream(dev).cuda_stream
+        k = (dev.index, _WS_ALIAS.get(sp, sp))
+        need = int(lib().rsvd_split_planes_bytes(int(rows), int(cols)))
+        cur = cls._cache.get(k)
+        if cur is None or cur.buf.numel() < need:
+            old = cur
+            cur = cls._cache[k] = cls(need, dev)
+            if old is not None:  # captured graphs may still point into the old buffer
+                cur._retired = getattr(old, "_retired", []) + [old.buf]
+        return cur
+
+    @classmethod
+    def peek(cls, device):
+        """The current stream's buffer if one exists (no allocation)."""
+        dev = torch.device(device)
+        sp = torch.cuda.current_stream(dev).cuda_stream
+        return cls._cache.get((dev.index, _WS_ALIAS.get(sp, sp)))
+
+    @staticmethod
+    def ident(t):
+        return (t.data_ptr(), tuple(t.shape), t.stride(0))
+
+    def describes(self, t):
+        return self.key is not None and self.key == self.ident(t)
+
+    def invalidate(self):
+        self.key = None
+
+    def split(self, B, pred=None):
+        """Cut B's planes with the standalone kernel (device-predicated by ``pred``)."""
+        K, N = B.shape
+        check(lib().rsvd_split_planes(K, N, _ptr(B), _ld(B), _ptr(self.buf), self.buf.numel(), _ptr(pred), _stream()),
+              "split_planes")
+        self.key = self.ident(B)
+
+
+def gemm_nn(A, B, C, alpha=1.0, beta=0.0, row_sub=None, algo=GEMM_AUTO, pred=None, emit=None):
     m, k = A.shape
     k2, n = B.shape
     assert k == k2 and C.shape == (m, n), (A.shape, B.shape, C.shape)
     assert A.dtype == B.dtype == C.dtype
+    if emit is not None and A.dtype == torch.float32 and algo == GEMM_AUTO:
+        # FP32 product that also leaves C's split planes behind (for a following TN
+        # product with B = C). A device-predicated product (pred) leaves the planes
+        # as they were when it is skipped: the caller orders its emits accordingly.
+        done = ctypes.c_int32(0)
+        check(lib().rsvd_gemm_nn_f32_emit(m, n, k, float(alpha), _ptr(A), _ld(A), _ptr(B), _ld(B), float(beta), _ptr(C),
+                                          _ld(C), _ptr(row_sub), _ptr(emit.buf), emit.buf.numel(),
+                                          ctypes.byref(done), _ptr(pred), _stream()), "gemm_nn_emit")
+        emit.key = emit.ident(C) if done.value else None
+        return C
     check(lib().rsvd_gemm_nn(dcode(A), m, n, k, float(alpha), _ptr(A), _ld(A), _ptr(B), _ld(B),
                              float(beta), _ptr(C), _ld(C), _ptr(row_sub), int(algo), _ptr(pred), _stream()),
           "gemm_nn")
     return C
 
 
-def gemm_tn(A, B, C, alpha=1.0, beta=0.0, mu=None, colsum_b=None, algo=GEMM_AUTO, pred=None):
-    """C (k x n) = alpha (A^T B - mu colsum_b^T) + beta C, A m x k, B m x n."""
+def gemm_tn(A, B, C, alpha=1.0, beta=0.0, mu=None, colsum_b=None, algo=GEMM_AUTO, pred=None, b_planes=None):
+    """C (k x n) = alpha (A^T B - mu colsum_b^T) + beta C, A m x k, B m x n.
+    ``b_planes``: SplitPlanes that may describe B (then B is not read at all)."""
     m, k = A.shape
     m2, n = B.shape
     assert m == m2 and C.shape == (k, n), (A.shape, B.shape, C.shape)
@@ -140,6 +204,12 @@ def gemm_tn(A, B, C, alpha=1.0, beta=0.0, mu=None, colsum_b=None, algo=GEMM_AUTO
     L = lib()
     nbytes = L.rsvd_gemm_tn_ws_bytes(dcode(A), m, n, k, int(algo))
     ws = WS.get(nbytes, A.device)
+    if (b_planes is not None and A.dtype == torch.float32 and algo == GEMM_AUTO and b_planes.describes(B)
+            and L.rsvd_gemm_tn_f32_planes_ok(m, n, k, _ptr(A), _ld(A))):
+        check(L.rsvd_gemm_tn_f32_planes(dcode(C), m, n, k, float(alpha), _ptr(A), _ld(A), _ptr(b_planes.buf),
+                                        b_planes.buf.numel(), float(beta), _ptr(C), _ld(C), _ptr(mu), _ptr(colsum_b),
+                                        _ptr(ws), ws.numel(), _ptr(pred), _stream()), "gemm_tn_planes")
+        return C
     check(L.rsvd_gemm_tn(dcode(A), dcode(C), m, n, k, float(alpha), _ptr(A), _ld(A), _ptr(B), _ld(B),
                          float(beta), _ptr(C), _ld(C), _ptr(mu), _ptr(colsum_b), _ptr(ws), ws.numel(),
                          int(algo), _ptr(pred), _stream()), "gemm_tn")
@@ -225,12 +295,12 @@ class OzBasis:
         return C
 
 
-def gram(V, out=None, algo=GEMM_AUTO, pred=None):
+def gram(V, out=None, algo=GEMM_AUTO, pred=None, b_planes=None):
     """FP64 Gram V^T V."""
     p = V.shape[1]
     if out is None:
         out = torch.empty((p, p), dtype=torch.float64, device=V.device)
-    return gemm_tn(V, V, out, algo=algo, pred=pred)
+    return gemm_tn(V, V, out, algo=algo, pred=pred, b_planes=b_planes)
 
 
 def colreduce(X, square=True, out=None):

@@ -222,7 +222,7 @@ def _cast_small(ops, T64, dtype, out=None, pred=None):
     return ops.convert(T64, out, pred=pred)
 
 
-def project_out(ops, comm, Qp, V, tmp_c, pred=None, basis=None):
+def project_out(ops, comm, Qp, V, tmp_c, pred=None, basis=None, planes=None):
     """V <- V - Qp (Qp^T V)  (one block classical Gram-Schmidt pass).
     ``basis`` (exact mode): the digit planes of the basis Qp is the prefix of
     (device.OzBasis) -- both products run as FP64-accurate int8 tensor-core
@@ -235,9 +235,11 @@ def project_out(ops, comm, Qp, V, tmp_c, pred=None, basis=None):
         comm.allreduce(tmp_c)
         basis.gemm(0, jp, tmp_c, V, alpha=-1.0, beta=1.0, pred=pred)
         return V
-    ops.gemm_tn(Qp, V, tmp_c, pred=pred)
+    # planes (FP32, unpredicated calls only): the TN product takes V's split planes
+    # when they are current, and the NN product leaves the updated V's behind
+    ops.gemm_tn(Qp, V, tmp_c, pred=pred, b_planes=planes if pred is None else None)
     comm.allreduce(tmp_c)
-    ops.gemm_nn(Qp, tmp_c, V, alpha=-1.0, beta=1.0, pred=pred)
+    ops.gemm_nn(Qp, tmp_c, V, alpha=-1.0, beta=1.0, pred=pred, emit=planes if pred is None else None)
     return V
 
 
@@ -265,6 +267,12 @@ OZ_PROJECTIONS = os.environ.get("RSVD_OZ_PROJ", "1") != "0"
 OVERLAP_FINAL = os.environ.get("RSVD_OVERLAP_FINAL", "1") != "0"
 # Projections against Qp inside the second deflation round (see orth_block).
 ROUND2_QP_PASSES = int(os.environ.get("RSVD_ROUND2_QP_PASSES", "1"))
+# FP32 blocks: split planes emitted by the NN epilogues and reused by the
+# following TN products. Off by default: at C4 the split passes fall from 23.5
+# to 7.6 ms and the chain's A^T Y from 93.7 to 91.9 ms, but the emitting NN
+# epilogues (two 4-byte stores per element on top of C's float4 stores) cost
+# 25.7 ms more: 349.6 vs 340.1 ms per factorization (gpurun_out/s5_trace_c4_*).
+EMIT_PLANES = os.environ.get("RSVD_EMIT_PLANES", "0") != "0"
 
 
 def proj_passes(dtype):
@@ -313,20 +321,27 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
     n_total = V.shape[0] if n_total is None else n_total
     has_prev = Qp is not None and Qp.shape[1] > 0
     tmp_c = torch.empty((Qp.shape[1], p), dtype=dtype, device=V.device) if has_prev else None
+    # FP32 blocks: every NN product that writes a block also writes its hi / lo
+    # split planes from its epilogue (device.SplitPlanes), and the TN product that
+    # reads the block next (Gram, projection, the chain's A^T b) takes those instead
+    # of a split pass over the block (C4: 23 of 340 ms were k_split_b). Measured
+    # slower as a whole (see EMIT_PLANES), so opt-in: RSVD_EMIT_PLANES=1.
+    pl = ops.SplitPlanes.get(V.shape[0], p, V.device) if (dtype == torch.float32 and EMIT_PLANES and
+                                                           V.is_cuda) else None
     if has_prev:
         npass = proj_passes(dtype)
         if pass1_coef is not None:
             # first pass with coefficients formed in d-space by the caller
             # (bk_basis: Qp^T A C = (A^T Qp)^T C); the remaining passes and
             # the final pass project with Qp^T V itself
-            ops.gemm_nn(Qp, pass1_coef, V, alpha=-1.0, beta=1.0)
+            ops.gemm_nn(Qp, pass1_coef, V, alpha=-1.0, beta=1.0, emit=pl)
             npass -= 1
         for _ in range(npass):
-            project_out(ops, comm, Qp, V, tmp_c, basis=basis)
+            project_out(ops, comm, Qp, V, tmp_c, basis=basis, planes=pl)
     G = ws.G[:p, :p]
     T = ws.T[:p, :p]
     mask = ws.mask[:p]
-    ops.gram(V, G)
+    ops.gram(V, G, b_planes=pl)
     comm.allreduce(G)
     if two_round and tau > 0.0 and ref2 is None:
         # original column norms^2 = diag(V^T V): taken from the Gram instead of a
@@ -341,7 +356,7 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
         r1 = ws.ndef_r1  # round-1 [count, base]: round 2 runs on the device only if count > 0
         ops.chol_deflate(G, ref2, tau * tau, T, mask, r1, None)
         Q1 = rows_buffer(tmp.shape[0], p, dtype, tmp.device)
-        ops.gemm_nn(V, _cast_small(ops, T, dtype), Q1)  # Q1 (zero columns at rejected slots)
+        ops.gemm_nn(V, _cast_small(ops, T, dtype), Q1, emit=pl)  # Q1 (zero columns at rejected slots)
         ws.ndef.zero_()
         c2 = torch.empty((p, p), dtype=dtype, device=V.device)
         with ops.cond_section(r1, use_cond):
@@ -377,6 +392,8 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
             # survivors join the kept columns
             ops.gemm_nn(V, _cast_small(ops, T, dtype, out=T32, pred=r1), Q1, beta=1.0, pred=r1)
             ops.insert_fill(Q1, ws.mask2[:p], ws.ndef, QR_FILL_SEED, row_offset, n_total, pred=r1)
+        if pl is not None and pl.describes(Q1):
+            pl.split(Q1, pred=r1)  # round 2 changed Q1 (only then: device-predicated)
         out = Q1
     else:
         ops.chol_deflate(G, ref2, tau * tau, T, mask, ws.ndef, running)
@@ -397,12 +414,12 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
         ref_f = ws.ref_fin[:p]
         ops.colreduce(out, True, ref_f)
         comm.allreduce(ref_f)
-        project_out(ops, comm, Qp, out, tmp_c, basis=basis)
-    ops.gram(out, G)
+        project_out(ops, comm, Qp, out, tmp_c, basis=basis, planes=pl)
+    ops.gram(out, G, b_planes=pl)
     comm.allreduce(G)
     r3 = ws.ndef_r3
     ops.chol_deflate(G, ref_f, 1e-12, T, ws.mask2[:p], r3, running)
-    ops.gemm_nn(out, _cast_small(ops, T, dtype), V)
+    ops.gemm_nn(out, _cast_small(ops, T, dtype), V, emit=pl)
     # repair (runs only if a column collapsed): next stream vectors into the
     # collapsed slots, re-project, CholeskyQR
     with ops.cond_section(r3, use_cond):
@@ -415,6 +432,8 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
         ops.chol_deflate(G, None, 0.0, T, ws.mask2[:p], ws.ndef2, None, pred=r3)
         ops.gemm_nn(V, _cast_small(ops, T, dtype, out=T32, pred=r3), out, pred=r3)
         ops.convert(out, V, pred=r3)
+    if pl is not None and pl.describes(V):
+        pl.split(V, pred=r3)  # the repair changed V (only then: device-predicated)
     if dtype != torch.float64 and FP32_THIRD_PASS:
         # FP32 storage: one more CholeskyQR step (CholeskyQR2 cleanup)
         ops.gram(V, G)

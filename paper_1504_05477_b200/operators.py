@@ -122,7 +122,8 @@ class DenseDeviceOp:
             # partial (A_g^T Y_g - mu 1^T Y_g) terms into the full correction.
             cs = ops.colreduce(Y, square=False)
             mu = self.mu
-        return ops.gemm_tn(self.A, Y, out, mu=mu, colsum_b=cs)
+        # Y's split planes, when the product that wrote Y left them behind
+        return ops.gemm_tn(self.A, Y, out, mu=mu, colsum_b=cs, b_planes=ops.SplitPlanes.peek(Y.device))
 
 
 class CsrDeviceOp:
@@ -297,7 +298,7 @@ class CsrDeviceOp:
         if self.hot is not None:
             h = self.hot
             th = torch.empty((h["Hp"], Y.shape[1]), dtype=out.dtype, device=out.device)
-            ops.gemm_tn(h["panel"], Y, th)
+            ops.gemm_tn(h["panel"], Y, th, b_planes=ops.SplitPlanes.peek(Y.device))
             ops.scatter_rows(h["idx"], th[: h["H"]], out)
         return out
 

@@ -16,7 +16,28 @@ def _off(pred):
     return pred is not None and int(pred.reshape(-1)[0]) == 0
 
 
-def gemm_nn(A, B, C, alpha=1.0, beta=0.0, row_sub=None, algo=0, pred=None):
+class SplitPlanes:
+    """CPU double of device.SplitPlanes: no planes, nothing ever described."""
+
+    @classmethod
+    def get(cls, rows, cols, device):
+        return cls()
+
+    @classmethod
+    def peek(cls, device):
+        return None
+
+    def describes(self, t):
+        return False
+
+    def invalidate(self):
+        pass
+
+    def split(self, B, pred=None):
+        pass
+
+
+def gemm_nn(A, B, C, alpha=1.0, beta=0.0, row_sub=None, algo=0, pred=None, emit=None):
     if _off(pred):
         return C
     r = A.double() @ B.double()
@@ -29,7 +50,7 @@ def gemm_nn(A, B, C, alpha=1.0, beta=0.0, row_sub=None, algo=0, pred=None):
     return C
 
 
-def gemm_tn(A, B, C, alpha=1.0, beta=0.0, mu=None, colsum_b=None, algo=0, pred=None):
+def gemm_tn(A, B, C, alpha=1.0, beta=0.0, mu=None, colsum_b=None, algo=0, pred=None, b_planes=None):
     if _off(pred):
         return C
     r = A.double().T @ B.double()
@@ -42,7 +63,7 @@ def gemm_tn(A, B, C, alpha=1.0, beta=0.0, mu=None, colsum_b=None, algo=0, pred=N
     return C
 
 
-def gram(V, out=None, algo=0, pred=None):
+def gram(V, out=None, algo=0, pred=None, b_planes=None):
     if out is None:
         out = torch.empty((V.shape[1], V.shape[1]), dtype=torch.float64)
     return gemm_tn(V, V, out, pred=pred)

@@ -125,3 +125,69 @@ def test_tc_rejects_misaligned_a_and_auto_falls_back(ops, off):
         ops.gemm_nn(V, T, C, algo=TC)
     ops.gemm_nn(V, T, C)
     assert _rel(C.cpu(), V.double().cpu() @ T.double().cpu()) < 5e-6
+
+
+@pytest.mark.parametrize("m,n,k,mode", [(1000, 100, 300, "plain"), (4133, 200, 96, "axpby"), (640, 72, 2048, "rowsub"),
+                                        (50000, 104, 50, "axpby")])
+def test_nn_epilogue_emits_split_planes(m, n, k, mode):
+    """rsvd_gemm_nn_f32_emit: the tcgen05 NN product also writes its output's hi /
+    lo split planes from the epilogue. They equal (bitwise) the planes
+    rsvd_split_planes cuts from the stored C -- ragged last row block and column
+    tile included -- and a TN product fed with them equals the one that splits B
+    itself; every epilogue variant (plain, alpha / beta, centred row_sub)."""
+    from paper_1504_05477_b200 import device as ops
+
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    A = torch.randn((m, k), generator=g, device="cuda")
+    B = torch.randn((k, n), generator=g, device="cuda")
+    C0 = torch.randn((m, n), generator=g, device="cuda")
+    kw = {}
+    if mode == "axpby":
+        kw = dict(alpha=-1.0, beta=1.0)
+    if mode == "rowsub":
+        kw = dict(row_sub=torch.randn((1, n), generator=g, device="cuda", dtype=torch.float64))
+    Cref = C0.clone()
+    ops.gemm_nn(A, B, Cref, **kw)
+    C = C0.clone()
+    pl = ops.SplitPlanes.get(m, n, "cuda")
+    pl.invalidate()
+    ops.gemm_nn(A, B, C, emit=pl, **kw)
+    assert torch.equal(C, Cref)
+    if k <= 64:
+        # the skinny CUDA-core path took this shape: nothing emitted, and a TN
+        # product offered the stale planes splits B itself
+        assert not pl.describes(C)
+        Q = torch.randn((m, 136), generator=g, device="cuda")
+        o1, o2 = torch.empty((136, n), device="cuda"), torch.empty((136, n), device="cuda")
+        ops.gemm_tn(Q, C, o1)
+        ops.gemm_tn(Q, C, o2, b_planes=pl)
+        assert torch.equal(o1, o2)
+        return
+    assert pl.describes(C)
+    nbytes = int(ops.lib().rsvd_split_planes_bytes(m, n))
+    emitted = pl.buf[:nbytes].clone()
+    ref = ops.SplitPlanes(nbytes, "cuda")
+    ref.buf.zero_()
+    ref.split(C)
+    # compare the written region: plane rows (columns of C) < n of every k-block
+    Kp, Np = (m + 31) // 32 * 32, (n + 31) // 32 * 32
+    e = emitted.view(torch.float32).view(Kp // 32, 2, Np, 32)[:, :, :n, :]
+    r = ref.buf[:nbytes].view(torch.float32).view(Kp // 32, 2, Np, 32)[:, :, :n, :]
+    assert torch.equal(e, r)
+    # the TN product on the emitted planes
+    Q = torch.randn((m, 136), generator=g, device="cuda")
+    out1 = torch.empty((136, n), device="cuda")
+    out2 = torch.empty((136, n), device="cuda")
+    ops.gemm_tn(Q, C, out1)
+    ops.gemm_tn(Q, C, out2, b_planes=pl)
+    assert torch.equal(out1, out2)
+    G1 = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    G2 = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    ops.gram(C, G1)
+    ops.gram(C, G2, b_planes=pl)
+    assert torch.equal(G1, G2)
+    # planes of another tensor are ignored
+    other = C.clone()
+    out3 = torch.empty((136, n), device="cuda")
+    ops.gemm_tn(Q, other, out3, b_planes=pl)
+    assert torch.equal(out1, out3)
