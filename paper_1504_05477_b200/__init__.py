@@ -13,6 +13,7 @@ from .experiment import ExperimentSpec, OracleSpectrum, oracle_spectrum, rows_to
 from .io import load_dense_csv, load_matrix_market, write_matrix_market  # f3
 from .metrics import ErrorReport, compute_error_report
 from .errors import ConvergenceError, ParseError
+from .factor import EigResult, qr_orthonormalize, symmetric_eig  # factor.py's hot-path entry points
 from .matrix import DenseMatrix, SeededRng, SparseMatrixCSR, as_dense_array, gaussian
 from .synth import SyntheticSpec, synth_matrix
 from .rsvd import (
@@ -44,6 +45,9 @@ __all__ = [
     "SyntheticSpec",
     "synth_matrix",
     "ConvergenceError",
+    "EigResult",
+    "qr_orthonormalize",
+    "symmetric_eig",
     "ParseError",
     "DenseMatrix",
     "SparseMatrixCSR",

@@ -1,0 +1,104 @@
+"""Host-facing entry points of the two small factorizations on the hot path
+(reference factor.py): ``qr_orthonormalize`` (factor.py:121-129, the public
+face of ``_mgs``, factor.py:79-118) and ``symmetric_eig`` (factor.py:132-166),
+with the reference's signatures, validation and error behaviour. Both run on
+the GPU through the same kernels the factorization uses -- the blocked
+BCGS2 + CholeskyQR orthonormalization with deflation and the seeded fill
+stream (krylov.orth_block), and the Jacobi kernel of the kernel contract
+(device.jacobi_sweeps); there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import device as ops
+from . import krylov
+from .errors import ConvergenceError
+from .matrix import DenseMatrix, as_dense_array
+
+# Columns per orthonormalization step: one p <= 64 register Cholesky per block.
+QR_BLOCK = 64
+
+
+@dataclass(frozen=True)
+class EigResult:
+    """factor.py:44-56 -- eigenvalues descending; column i pairs with value i."""
+
+    eigenvalues: np.ndarray
+    eigenvectors: DenseMatrix
+
+    def __post_init__(self):
+        vals = np.array(self.eigenvalues, dtype=np.float64, copy=True)
+        if vals.ndim != 1 or np.any(np.diff(vals) > 0):
+            raise ValueError("eigenvalues must be a descending 1-D array")
+        vals.setflags(write=False)
+        object.__setattr__(self, "eigenvalues", vals)
+
+
+def _device(device):
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1504_05477_b200 requires a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+
+
+def qr_orthonormalize(M, device=None):
+    """Orthonormal basis with M's column count spanning span(M); numerically
+    dependent columns (residual <= 1e-12 x the column's norm) are replaced from
+    the seeded fill stream, one stream per call like one ``_mgs`` call. Columns
+    are processed in blocks of QR_BLOCK, each against the finished prefix."""
+    arr = as_dense_array(M)
+    n, m = arr.shape
+    if n < m:
+        raise ValueError("qr_orthonormalize requires rows >= cols")
+    dev = _device(device)
+    with torch.cuda.device(dev):
+        K = krylov.rows_buffer(n, m, torch.float64, dev)
+        K.copy_(torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)))
+        pb = max(1, min(QR_BLOCK, m))
+        ws = krylov.Workspace(dev, pb)
+        comm = krylov.LocalComm()
+        tmp = krylov.rows_buffer(n, pb, torch.float64, dev)
+        running = torch.zeros(1, dtype=torch.int32, device=dev)
+        for j0 in range(0, m, pb):
+            pw = min(pb, m - j0)
+            cur = K[:, j0: j0 + pw]
+            ref2 = ws.ref2[:pw]
+            ops.colreduce(cur, True, ref2)
+            krylov.orth_block(ops, comm, cur, tmp[:, :pw], ws, Qp=K[:, :j0] if j0 else None, ref2=ref2,
+                              running=running, n_total=n, row_offset=0)
+        return DenseMatrix(K.cpu().numpy())
+
+
+def symmetric_eig(M, tol=None, max_sweeps=None, device=None):
+    """Eigendecomposition of a symmetric matrix by Jacobi rotations on the GPU;
+    sweeps until the off-diagonal Frobenius mass is below tol x ||M||_F (default
+    1e-14) or max_sweeps (default 50), then ConvergenceError with the mass
+    reached. Eigenvalues descending, ties in their prior column order."""
+    arr = as_dense_array(M)
+    n, m = arr.shape
+    if n != m:
+        raise ValueError("symmetric_eig requires a square matrix")
+    scale = float(np.max(np.abs(arr))) if arr.size else 0.0
+    asym = float(np.max(np.abs(arr - arr.T))) if arr.size else 0.0
+    if asym > 1e-10 * max(1.0, scale):
+        raise ValueError("matrix is not symmetric to tolerance; symmetrize as (M + M^T)/2 first")
+    tol = krylov.JACOBI_TOL if tol is None else tol
+    max_sweeps = krylov.JACOBI_MAX_SWEEPS if max_sweeps is None else max_sweeps
+    dev = _device(device)
+    with torch.cuda.device(dev):
+        W = torch.from_numpy(0.5 * (arr + arr.T)).to(device=dev, dtype=torch.float64)
+        V = torch.eye(n, dtype=torch.float64, device=dev)
+        info, off = ops.jacobi_sweeps(W, V, float(tol), int(max_sweeps))
+        info = info.cpu().numpy()
+        off = float(off.cpu()[0])
+        if not bool(info[0]):
+            raise ConvergenceError(f"Jacobi did not converge in {max_sweeps} sweeps (off-diagonal mass {off:.3e})",
+                                   residual=off)
+        vals = torch.diagonal(W).cpu().numpy().copy()
+        vecs = V.cpu().numpy()
+    order = np.argsort(-vals, kind="stable")
+    return EigResult(vals[order], DenseMatrix(np.ascontiguousarray(vecs[:, order])))

@@ -215,3 +215,100 @@ def test_k_above_rank_still_returns_basis(rk):
 def test_wall_time_recorded(rk):
     r = rk.factorize(_g(rk, 30, 20, 70), rk.RsvdConfig(k=3, variant="bk", q=1, seed=0))
     assert r.wall_time_ms > 0.0
+
+
+# ---- qr_orthonormalize (test_factor.py:19-53) -------------------------------
+
+
+def test_qr_identity_unchanged(rk):
+    assert np.array_equal(rk.qr_orthonormalize(np.eye(3)).data, np.eye(3))
+
+
+def test_qr_rank_deficient_hand_case(rk):
+    q = rk.qr_orthonormalize(np.array([[3.0, 0.0], [4.0, 0.0]])).data
+    assert np.allclose(q[:, 0], [0.6, 0.8], atol=1e-15)
+    assert abs(np.linalg.norm(q[:, 1]) - 1.0) < 1e-12  # replacement column
+    assert abs(q[:, 0] @ q[:, 1]) < 1e-12
+
+
+def test_qr_random_block_contract(rk):
+    m = _g(rk, 50, 8, 4)
+    q = rk.qr_orthonormalize(m).data
+    assert _orth_err(q) < 1e-12
+    assert np.linalg.norm(q @ (q.T @ m) - m) < 1e-10 * np.linalg.norm(m)
+    # same basis as the reference's column-by-column _mgs (positive diagonal R: no sign freedom)
+    assert np.max(np.abs(q - o.mgs(m))) < 1e-12
+
+
+def test_qr_always_full_width_even_for_duplicates(rk):
+    base = _g(rk, 30, 3, 5)
+    q = rk.qr_orthonormalize(np.hstack([base, base, base])).data
+    assert q.shape == (30, 9)
+    assert _orth_err(q) < 1e-12
+    ref = o.mgs(np.hstack([base, base, base]))
+    assert np.max(np.abs(q[:, :3] - ref[:, :3])) < 1e-12
+    # the six replaced columns come from the same seeded fill stream
+    assert np.max(np.abs(q - ref)) < 1e-9
+
+
+def test_qr_rows_less_than_cols_rejected(rk):
+    with pytest.raises(ValueError):
+        rk.qr_orthonormalize(np.ones((2, 3)))
+
+
+def test_qr_deterministic_including_replacement(rk):
+    m = np.array([[3.0, 0.0], [4.0, 0.0], [0.0, 0.0]])
+    assert np.array_equal(rk.qr_orthonormalize(m).data, rk.qr_orthonormalize(m).data)
+
+
+def test_qr_wider_than_one_block(rk):
+    m = _g(rk, 700, 150, 6).copy()  # three blocks of QR_BLOCK columns, the last ragged
+    m[:, 100] = m[:, 3] - 2.0 * m[:, 77]  # a dependent column in the second block
+    q = rk.qr_orthonormalize(m).data
+    assert _orth_err(q) < 1e-12
+    ref = o.mgs(m)
+    assert list(o.mgs.last_replaced) == [100]
+    assert np.max(np.abs(q - ref)) < 1e-9
+
+
+# ---- symmetric_eig (test_factor.py:55-100) ----------------------------------
+
+
+def test_eig_diagonal(rk):
+    res = rk.symmetric_eig(np.diag([2.0, 1.0]))
+    assert res.eigenvalues.tolist() == [2.0, 1.0]
+    assert np.array_equal(res.eigenvectors.data, np.eye(2))
+
+
+def test_eig_exchange_matrix(rk):
+    res = rk.symmetric_eig(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    assert np.allclose(res.eigenvalues, [1.0, -1.0], atol=1e-12)
+    v = res.eigenvectors.data
+    s = 1.0 / np.sqrt(2.0)
+    assert np.allclose(np.abs(v), [[s, s], [s, s]], atol=1e-12)
+    assert np.allclose(v.T @ v, np.eye(2), atol=1e-12)
+
+
+@pytest.mark.parametrize("n,seed", [(6, 17), (9, 18), (40, 23)])
+def test_eig_reconstruction_and_orthonormal_vectors(rk, n, seed):
+    base = _g(rk, n, n, seed)
+    m = 0.5 * (base + base.T)
+    res = rk.symmetric_eig(m)
+    v = res.eigenvectors.data
+    assert np.max(np.abs(v @ np.diag(res.eigenvalues) @ v.T - m)) < 1e-10
+    assert _orth_err(v) < 1e-10
+    assert np.max(np.abs(res.eigenvalues - np.linalg.eigvalsh(m)[::-1])) < 1e-10
+
+
+def test_eig_rejections(rk):
+    with pytest.raises(ValueError):
+        rk.symmetric_eig(np.ones((2, 3)))
+    with pytest.raises(ValueError):
+        rk.symmetric_eig(np.array([[0.0, 1.0], [0.0, 0.0]]))
+
+
+def test_eig_nonconvergence_carries_residual(rk):
+    base = _g(rk, 8, 8, 19)
+    with pytest.raises(rk.ConvergenceError) as err:
+        rk.symmetric_eig(0.5 * (base + base.T), tol=0.0, max_sweeps=1)
+    assert err.value.residual is not None and err.value.residual > 0
