@@ -14,7 +14,8 @@ from .io import load_dense_csv, load_matrix_market, write_matrix_market  # f3
 from .metrics import ErrorReport, compute_error_report
 from .errors import ConvergenceError, ParseError
 from .factor import EigResult, qr_orthonormalize, symmetric_eig  # factor.py's hot-path entry points
-from .matrix import DenseMatrix, SeededRng, SparseMatrixCSR, as_dense_array, gaussian
+from .matrix import (DenseMatrix, MatrixOperator, SeededRng, SparseMatrixCSR, as_dense_array, as_operator,
+                     frobenius_norm_sq, gaussian, matmul, spmm)
 from .synth import SyntheticSpec, synth_matrix
 from .rsvd import (
     PartialSvdResult,
@@ -53,6 +54,11 @@ __all__ = [
     "SparseMatrixCSR",
     "SeededRng",
     "as_dense_array",
+    "MatrixOperator",
+    "as_operator",
+    "matmul",
+    "spmm",
+    "frobenius_norm_sq",
     "gaussian",
     "PartialSvdResult",
     "RsvdConfig",

@@ -156,3 +156,116 @@ def gaussian(rows, cols, rng):
     if rows < 1 or cols < 1:
         raise ValueError("gaussian dimensions must be at least 1")
     return DenseMatrix(rng.normal_fill(rows * cols).reshape(rows, cols))
+
+
+class MatrixOperator:
+    """matrix.py:195-257 -- uniform apply / apply-transpose access over dense or
+    CSR storage, numpy in / numpy out like the reference's. The matrix is
+    uploaded once (FP64, on first use) and stays resident on the device; the
+    products run in librsvd_b200.so (FP64 tensor-core GEMMs / CSR kernels)."""
+
+    def __init__(self, matrix):
+        if isinstance(matrix, MatrixOperator):
+            matrix = matrix.matrix
+        if isinstance(matrix, (DenseMatrix, SparseMatrixCSR)):
+            self.matrix = matrix
+        else:
+            self.matrix = DenseMatrix(np.asarray(matrix))
+        self._dev = None
+
+    @property
+    def shape(self):
+        return self.matrix.shape
+
+    @property
+    def is_sparse(self):
+        return isinstance(self.matrix, SparseMatrixCSR)
+
+    @property
+    def nnz(self):
+        if self.is_sparse:
+            return self.matrix.nnz
+        return int(np.count_nonzero(self.matrix.data))
+
+    def device_operator(self):
+        """The device-resident operator behind this one (operators.py)."""
+        if self._dev is None:
+            from .rsvd import make_operator
+
+            self._dev = make_operator(self.matrix, precision="fp64")
+        return self._dev
+
+    def _product(self, block, inner, rows_out, transpose):
+        import torch
+
+        b = np.ascontiguousarray(np.asarray(block, dtype=np.float64))
+        if b.ndim == 1:
+            b = b.reshape(-1, 1)
+        if b.shape[0] != inner:
+            raise ValueError("inner dimensions do not match")
+        op = self.device_operator()
+        with torch.cuda.device(op.device):
+            x = torch.from_numpy(b).to(op.device)
+            out = torch.empty((rows_out, b.shape[1]), dtype=torch.float64, device=op.device)
+            if b.shape[1]:
+                (op.apply_t if transpose else op.apply)(x, out)
+            return out.cpu().numpy()
+
+    def apply(self, block):
+        """A @ block."""
+        return self._product(block, self.shape[1], self.shape[0], False)
+
+    def apply_transpose(self, block):
+        """A.T @ block."""
+        return self._product(block, self.shape[0], self.shape[1], True)
+
+    def densify(self):
+        if self.is_sparse:
+            return DenseMatrix(self.matrix.toarray())
+        return self.matrix
+
+    def frobenius_sq(self):
+        from .metrics import frobenius_sq
+
+        return frobenius_sq(self.device_operator())
+
+
+def as_operator(A):
+    """matrix.py:260-263."""
+    if isinstance(A, MatrixOperator):
+        return A
+    return MatrixOperator(A)
+
+
+def matmul(A, B):
+    """matrix.py:279-287 -- dense product A @ B (FP64 tensor-core GEMM;
+    fixed summation order: bitwise reproducible)."""
+    from . import backend
+
+    a = as_dense_array(A)
+    b = as_dense_array(B)
+    if a.shape[1] != b.shape[0]:
+        raise ValueError(f"matmul dimension mismatch: {a.shape} x {b.shape}")
+    return DenseMatrix(backend.mm(a, b))
+
+
+def spmm(A, B, transpose_A=False):
+    """matrix.py:290-304 -- sparse-dense product A @ B, or A.T @ B."""
+    from . import backend
+
+    if not isinstance(A, SparseMatrixCSR):
+        raise TypeError("spmm expects a SparseMatrixCSR left operand")
+    b = as_dense_array(B)
+    inner = A.rows if transpose_A else A.cols
+    if b.shape[0] != inner:
+        raise ValueError(f"spmm dimension mismatch: {A.shape}{'^T' if transpose_A else ''} x {b.shape}")
+    if transpose_A:
+        out = backend.spmm_t(A.rows, A.cols, A.row_ptr, A.col_idx, A.values, b)
+    else:
+        out = backend.spmm_nt(A.rows, A.row_ptr, A.col_idx, A.values, b)
+    return DenseMatrix(out)
+
+
+def frobenius_norm_sq(A):
+    """matrix.py:307-309 -- sum of squared entries."""
+    return as_operator(A).frobenius_sq()

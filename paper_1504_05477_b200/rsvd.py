@@ -45,7 +45,7 @@ import torch
 from . import device as ops
 from . import krylov
 from .errors import ConvergenceError
-from .matrix import DenseMatrix, SeededRng, SparseMatrixCSR, as_dense_array, gaussian
+from .matrix import DenseMatrix, MatrixOperator, SeededRng, SparseMatrixCSR, as_dense_array, gaussian
 from .operators import CsrDeviceOp, DenseDeviceOp
 
 __all__ = [
@@ -248,6 +248,8 @@ def make_operator(A, precision="auto", center=False, device=None, comm=None, n_t
     matrix.py:260-263). Dense host input is validated like DenseMatrix."""
     if isinstance(A, (DenseDeviceOp, CsrDeviceOp)):
         return A
+    if isinstance(A, MatrixOperator):  # the reference's as_operator(A) handle: its host matrix
+        A = A.matrix
     if isinstance(A, SparseMatrixCSR):
         if center:
             raise ValueError("implicit centering is supported for dense A only")
