@@ -11,9 +11,11 @@ no CPU fallback.
 from . import metrics  # noqa: F401  (GPU parity metrics)
 from .experiment import ExperimentSpec, OracleSpectrum, oracle_spectrum, rows_to_csv, run_experiment  # f4
 from .io import load_dense_csv, load_matrix_market, write_matrix_market  # f3
-from .metrics import ErrorReport, compute_error_report
+from .metrics import (ErrorReport, compute_error_report, error_function, frob_error_ratio, per_vector_errors,
+                      spectral_error_ratio)
 from .errors import ConvergenceError, ParseError
-from .factor import EigResult, qr_orthonormalize, symmetric_eig  # factor.py's hot-path entry points
+from .factor import (EigResult, SvdResult, dense_svd_reference, qr_orthonormalize,  # factor.py's entry points
+                     symmetric_eig)
 from .matrix import (DenseMatrix, MatrixOperator, SeededRng, SparseMatrixCSR, as_dense_array, as_operator,
                      frobenius_norm_sq, gaussian, matmul, spmm)
 from .synth import SyntheticSpec, synth_matrix
@@ -43,10 +45,16 @@ __all__ = [
     "write_matrix_market",
     "ErrorReport",
     "compute_error_report",
+    "error_function",
+    "frob_error_ratio",
+    "per_vector_errors",
+    "spectral_error_ratio",
     "SyntheticSpec",
     "synth_matrix",
     "ConvergenceError",
     "EigResult",
+    "SvdResult",
+    "dense_svd_reference",
     "qr_orthonormalize",
     "symmetric_eig",
     "ParseError",

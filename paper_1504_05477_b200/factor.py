@@ -102,3 +102,61 @@ def symmetric_eig(M, tol=None, max_sweeps=None, device=None):
         vecs = V.cpu().numpy()
     order = np.argsort(-vals, kind="stable")
     return EigResult(vals[order], DenseMatrix(np.ascontiguousarray(vecs[:, order])))
+
+
+ORACLE_DIM_LIMIT = 2000  # factor.py:36
+
+
+@dataclass(frozen=True)
+class SvdResult:
+    """factor.py:59-76 -- thin SVD factors: U (n x r), singular values
+    descending, V (d x r)."""
+
+    U: DenseMatrix
+    singular_values: np.ndarray
+    V: DenseMatrix
+
+    def __post_init__(self):
+        sv = np.array(self.singular_values, dtype=np.float64, copy=True)
+        if sv.ndim != 1 or np.any(sv < 0) or np.any(np.diff(sv) > 0):
+            raise ValueError("singular values must be nonnegative and descending")
+        sv.setflags(write=False)
+        object.__setattr__(self, "singular_values", sv)
+
+    @property
+    def rank(self):
+        return int(self.singular_values.shape[0])
+
+
+def dense_svd_reference(A, dim_limit=ORACLE_DIM_LIMIT, device=None):
+    """factor.py:169-214 -- the desk-scale oracle SVD through the smaller Gram
+    matrix and symmetric_eig, refused above the guard; directions below 1e-12 of
+    the largest singular value are dropped. Products and the eigensolve run on
+    the GPU (FP64)."""
+    from .matrix import as_operator, matmul
+
+    op = as_operator(A)
+    n, d = op.shape
+    if min(n, d) > dim_limit:
+        raise ValueError(f"reference SVD guard: min(n, d) = {min(n, d)} exceeds {dim_limit}; "
+                         "supply a cached oracle or reduce the problem size")
+    dense = op.densify().data
+    via_transpose = d > n
+    left = dense if via_transpose else np.ascontiguousarray(dense.T)
+    gram = matmul(left, np.ascontiguousarray(left.T)).data
+    eig = symmetric_eig(0.5 * (gram + gram.T), device=device)
+    small = eig.eigenvectors.data
+    sigma = np.sqrt(np.clip(eig.eigenvalues, 0.0, None))
+    keep = sigma >= 1e-12 * sigma[0] if (sigma.size and sigma[0] > 0.0) else np.zeros(sigma.shape, dtype=bool)
+    sigma = sigma[keep]
+    kept = np.ascontiguousarray(small[:, keep])
+    if sigma.size:
+        if via_transpose:
+            u = kept
+            v = matmul(np.ascontiguousarray(dense.T), u).data / sigma[None, :]
+        else:
+            v = kept
+            u = matmul(dense, v).data / sigma[None, :]
+    else:
+        u, v = np.zeros((n, 0)), np.zeros((d, 0))
+    return SvdResult(DenseMatrix(u), sigma, DenseMatrix(v))

@@ -151,22 +151,59 @@ def spectral_error(A, Z, seeds=RESTART_SEEDS, tol=SPECTRAL_TOL, max_iters=SPECTR
     return float(best.max())
 
 
-def spectral_error_ratio(A, Z, sigma_k1, **kw):
-    """metrics.py:102-122: numerator over sigma_{k+1}; 1.0 for exact rank."""
+def _sv(oracle):
+    """Oracle singular values: the reference passes its SvdResult
+    (``.singular_values``, factor.py:59-76); a plain descending array works too.
+    Values past the oracle's rank read as 0 (metrics.py:50-52)."""
+    return np.asarray(getattr(oracle, "singular_values", oracle), dtype=np.float64).reshape(-1)
+
+
+def _ncols(Z):
+    from .matrix import DenseMatrix
+
+    z = Z.data if isinstance(Z, DenseMatrix) else Z
+    return int(z.shape[1])
+
+
+def spectral_error_ratio(A, Z, oracle, **kw):
+    """metrics.py:102-122: ||A - Z Z^T A||_2 over sigma_{k+1}; 1.0 for exact
+    rank. ``oracle``: the reference's oracle object / its singular values, or
+    sigma_{k+1} itself as a scalar."""
+    op = _operator(A, kw.get("precision", "auto"))
+    check_orthonormal(Z, op.device)
+    sigma_k1 = float(oracle) if np.isscalar(oracle) else _sig(_sv(oracle), _ncols(Z))
     if sigma_k1 == 0.0:
         return 1.0
-    return spectral_error(A, Z, **kw) / sigma_k1
+    return spectral_error(op, Z, **kw) / sigma_k1
 
 
-def per_vector_errors(A, Z, sigma, precision="auto"):
-    """metrics.py:125-142: |sigma_i^2 - ||A^T z_i||^2| / sigma_{k+1}^2 with the
-    oracle singular values `sigma` (length >= k + 1)."""
-    cap = captured_variance(A, Z, precision)
+def per_vector_errors(A, Z, oracle, precision="auto"):
+    """metrics.py:125-142: |sigma_i^2 - ||A^T z_i||^2| / sigma_{k+1}^2 against
+    the oracle's singular values; absolute errors when sigma_{k+1} = 0."""
+    op = _operator(A, precision)
+    check_orthonormal(Z, op.device)
+    cap = captured_variance(op, Z, precision)
     k = cap.shape[0]
-    sigma = np.asarray(sigma, dtype=np.float64)
-    errs = np.abs(sigma[:k] ** 2 - cap)
-    denom = sigma[k] ** 2 if sigma.shape[0] > k else 0.0
+    sigma = _sv(oracle)
+    true_sq = np.array([_sig(sigma, i) ** 2 for i in range(k)])
+    errs = np.abs(true_sq - cap)
+    denom = _sig(sigma, k) ** 2
     return errs if denom == 0.0 else errs / denom
+
+
+def error_function(A, Z, l, oracle, precision="auto"):
+    """metrics.py:145-158: Frobenius shortfall of the rank-l prefix of Z against
+    the optimal one, sum_{i<=l} sigma_i^2 - ||Z_l^T A||_F^2."""
+    from .matrix import DenseMatrix
+
+    z = Z.data if isinstance(Z, DenseMatrix) else Z
+    if l > z.shape[1]:
+        raise ValueError("l exceeds the number of columns of Z")
+    if l == 0:
+        return 0.0
+    sigma = _sv(oracle)
+    captured = float(np.sum(captured_variance(A, z[:, :l], precision)))
+    return float(np.sum(np.array([_sig(sigma, i) ** 2 for i in range(l)]))) - captured
 
 
 # ---------------------------------------------------------------------------
@@ -221,7 +258,7 @@ def frob_error_ratio(A, Z, sigma, precision="auto"):
     op = _operator(A, precision)
     check_orthonormal(Z, op.device)
     z = _as_device_z(Z, op)
-    sigma = np.asarray(sigma, dtype=np.float64)
+    sigma = _sv(sigma)
     k = z.shape[1]
     fro_sq = frobenius_sq(op)
     captured = float(np.sum(captured_variance(op, z)))
@@ -261,7 +298,7 @@ def compute_error_report(A, Z, sigma, q=None, variant=None, seed=None, precision
     op = _operator(A, precision)
     check_orthonormal(Z, op.device)
     z = _as_device_z(Z, op)
-    sigma = np.asarray(sigma, dtype=np.float64)
+    sigma = _sv(sigma)
     k = z.shape[1]
     pv = per_vector_errors(op, z, sigma)
     fro_sq = frobenius_sq(op)
