@@ -18,8 +18,9 @@
 // accumulates KCHUNK = 4 k-blocks (K = 128); two accumulator sets alternate
 // and four dedicated warps drain each finished chunk into round-to-nearest
 // FP32 registers while the tensor core fills the other set.
-// Two kernels: k_tc_gemm_t (BN <= 64, the Krylov-chain widths) keeps A_hi and
-// A_lo in TMEM (.ts MMAs); k_tc_gemm (BN 96 / 128) keeps them in smem.
+// One kernel, k_tc_gemm_t, for every N tile: A_hi and A_lo live in TMEM (.ts
+// MMAs). (An earlier BN 96 / 128 kernel with A_lo in shared memory was smem-
+// bandwidth bound -- C4's A X 10.2 vs 8.3 ms -- and has been removed.)
 #include <cuda.h>
 
 #include <cmath>
@@ -33,10 +34,6 @@ namespace {
 
 constexpr int BM = 128;      // UMMA M
 constexpr int BK = 32;       // fp32 elements per 128-byte swizzle row
-constexpr int kConvWarps = 4;
-constexpr int kConvThreads = 32 * kConvWarps;
-constexpr int kDrainWarp0 = 2 + kConvWarps;      // first accumulator-drain warp
-constexpr int kThreads = 32 * (kDrainWarp0 + 4);
 constexpr int KCHUNK = 4;  // k-blocks accumulated in TMEM before a drain
 
 // kind::tf32 instruction descriptor: F32 accumulate, TF32 A/B.
@@ -108,7 +105,7 @@ __device__ long long g_tc_trace[2][8][kTraceKb];
     } while (0)
 #endif
 
-// Accumulator drain + epilogue, shared by both kernels. TMEM lane quarter
+// Accumulator drain + epilogue. TMEM lane quarter
 // q = warp % 4 holds tile rows 32q..32q+31; D0 | D1 (2 BN columns) of each
 // finished chunk are summed into round-to-nearest FP32 registers.
 template <int BN, bool MERGED = true>
@@ -238,7 +235,7 @@ __device__ __forceinline__ void drain_epilogue(const TcParams& p, uint32_t tmem_
     }
 }
 
-// ---- kernel 1 (BN <= 64): both A halves in TMEM ---------------------------
+// ---- the kernel: both A halves in TMEM -------------------------------------
 // Rings: A (smem, TMA, one 128 x 32 box per stage; freed by the converters as
 // soon as they have read it), B (smem, TMA, [B_hi | B_lo] K-major for
 // KPS = 2 k-blocks per slot; freed by the MMA commit) and T (TMEM columns
@@ -513,176 +510,6 @@ k_tc_gemm_t(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     }
 }
 
-// ---- kernel 2 (BN 96 / 128): A_hi / A_lo in smem ---------------------------
-// The accumulators need 4 BN = 384 / 512 TMEM columns, leaving no room for A.
-// Stage = [A | A_lo | B_hi | B_lo]; the converters write A_lo beside the raw
-// A (the tensor core truncates raw FP32 to TF32 itself, so raw A is A_hi).
-// Warps: 0 TMA producer, 1 MMA issuer (+TMEM alloc), 2..5 converters, 6..9
-// drain.
-template <int BN, bool A_MN>
-struct TcCfg {
-    static constexpr int A_BYTES = BM * BK * 4;         // 16 KB
-    static constexpr int B_BYTES = BN * BK * 4;
-    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-    static constexpr int ACC_COLS = 4 * BN;              // 2 sets x (D0 | D1)
-    static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
-    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-    static constexpr int TMEM_COLS = ACC_COLS <= 128 ? 128 : (ACC_COLS <= 256 ? 256 : 512);
-};
-
-template <int BN, bool A_MN>
-__global__ void __launch_bounds__(kThreads, 1)
-k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
-    if (pred_off(p.pred)) return;
-    using Cfg = TcCfg<BN, A_MN>;
-    constexpr int STAGES = Cfg::STAGES;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
-    uint64_t* full = bars;
-    uint64_t* conv = bars + STAGES;
-    uint64_t* empty = bars + 2 * STAGES;
-    uint64_t* acc_full = bars + 3 * STAGES;   // [2]
-    uint64_t* acc_empty = bars + 3 * STAGES + 2;  // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
-
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int64_t m0 = (int64_t)(blockIdx.x / p.n_tiles) * BM;
-    const int64_t n0 = (int64_t)(blockIdx.x % p.n_tiles) * BN;
-    const int64_t kbeg = (int64_t)blockIdx.z * p.k_per_split;
-    const int64_t kend = min(p.K, kbeg + p.k_per_split);
-    const int nkb = (int)((kend - kbeg + BK - 1) / BK);
-
-    auto a_stage = [&](int s) { return smem + s * Cfg::STAGE_BYTES; };
-    auto alo_stage = [&](int s) { return smem + s * Cfg::STAGE_BYTES + Cfg::A_BYTES; };
-    auto b_stage = [&](int s) { return smem + s * Cfg::STAGE_BYTES + 2 * Cfg::A_BYTES; };  // [B_hi | B_lo]
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&conv[s], kConvWarps);
-            mbar_init(&empty[s], 1);
-        }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&acc_full[i], 1);
-            mbar_init(&acc_empty[i], 4);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(Cfg::TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            // ---------------- TMA producer
-            int s = 0;
-            uint32_t ph = 0;
-            for (int kb = 0; kb < nkb; ++kb) {
-                mbar_wait(&empty[s], ph ^ 1);
-                const int kk = (int)(kbeg + (int64_t)kb * BK);
-                mbar_expect_tx(&full[s], Cfg::A_BYTES + 2 * Cfg::B_BYTES);
-                if (!A_MN) {
-                    tma_load_2d(&tmA, &full[s], a_stage(s), kk, (int)m0);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < BM / 32; ++i)
-                        tma_load_2d(&tmA, &full[s], a_stage(s) + i * 32 * BK * 4, (int)(m0 + 32 * i), kk);
-                }
-                // K-major split-B planes: one box of BN rows x 32 k each
-                tma_load_3d(&tmB, &full[s], b_stage(s), 0, (int)n0, kk / BK);
-                tma_load_3d(&tmB, &full[s], b_stage(s) + Cfg::B_BYTES, 0, (int)(p.Np + n0), kk / BK);
-                if (++s == STAGES) { s = 0; ph ^= 1; }
-            }
-        }
-    } else if (warp == 1) {
-        // ---------------- MMA issuer. B_hi and B_lo sit back to back (K-major,
-        // BN rows each), so A_hi [B_hi | B_lo] is one N = 2 BN MMA -> D0 | D1.
-        constexpr uint32_t idesc2 = make_idesc(BM, 2 * BN, A_MN ? 1 : 0, 0);
-        constexpr uint32_t idesc1 = make_idesc(BM, BN, A_MN ? 1 : 0, 0);
-        int s = 0;
-        uint32_t ph = 0;
-        int chunk = 0;
-        for (int kb = 0; kb < nkb; ++kb) {
-            const int set = chunk & 1;
-            const uint32_t d0 = tmem_base + set * 2 * BN;
-            if (kb % KCHUNK == 0) {
-                mbar_wait(&acc_empty[set], ((chunk >> 1) & 1) ^ 1);
-                tc_fence_after();
-            }
-            mbar_wait(&conv[s], ph);
-            tc_fence_after();
-            if (lane == 0) {
-                const uint32_t a_hi = smem_u32(a_stage(s)), a_lo = smem_u32(alo_stage(s));
-                const uint32_t b = smem_u32(b_stage(s));
-#pragma unroll
-                for (int ks = 0; ks < BK / 8; ++ks) {
-                    uint64_t da_hi, da_lo;
-                    if (!A_MN) {  // K-major: advance 32 bytes inside the 128B row
-                        da_hi = make_desc(a_hi + ks * 32, 16, 1024, kLayoutSW128);
-                        da_lo = make_desc(a_lo + ks * 32, 16, 1024, kLayoutSW128);
-                    } else {  // MN-major: advance 8 K rows
-                        da_hi = make_desc(a_hi + ks * 1024, 32 * BK * 4, 512, kLayoutSW128Base32);
-                        da_lo = make_desc(a_lo + ks * 1024, 32 * BK * 4, 512, kLayoutSW128Base32);
-                    }
-                    const uint64_t db = make_desc(b + ks * 32, 16, 1024, kLayoutSW128);
-                    const uint32_t acc = (kb % KCHUNK > 0 || ks > 0) ? 1u : 0u;
-                    if (RSVD_TC_ABLATE & 2) continue;
-                    tc_mma_tf32(d0, da_hi, db, idesc2, acc);  // D0 | D1 += A_hi [B_hi | B_lo]
-                    if (RSVD_TC_ABLATE & 8) continue;
-                    tc_mma_tf32(d0, da_lo, db, idesc1, 1u);   // D0 += A_lo B_hi
-                }
-                tc_commit(&empty[s]);
-                if (kb % KCHUNK == KCHUNK - 1 || kb == nkb - 1) tc_commit(&acc_full[set]);
-            }
-            __syncwarp();
-            if (kb % KCHUNK == KCHUNK - 1 || kb == nkb - 1) ++chunk;
-            if (++s == STAGES) { s = 0; ph ^= 1; }
-        }
-    } else if (warp < kDrainWarp0) {
-        // ---------------- converters: A_lo to the sibling buffer
-        const int ct = threadIdx.x - 64;
-        constexpr int PER = Cfg::A_BYTES / 16 / kConvThreads;
-        int s = 0;
-        uint32_t ph = 0;
-        for (int kb = 0; kb < nkb; ++kb) {
-            mbar_wait(&full[s], ph);
-            const float4* a = reinterpret_cast<const float4*>(a_stage(s));
-            float4* lo = reinterpret_cast<float4*>(alo_stage(s));
-            float4 xs[PER];
-#pragma unroll
-            for (int i = 0; i < PER; ++i) xs[i] = a[ct + i * kConvThreads];
-#pragma unroll
-            for (int i = 0; i < PER; ++i) {
-                const float4 x = xs[i];
-                lo[ct + i * kConvThreads] = make_float4(tf32_rna(x.x - tf32_hi(x.x)), tf32_rna(x.y - tf32_hi(x.y)),
-                                                        tf32_rna(x.z - tf32_hi(x.z)), tf32_rna(x.w - tf32_hi(x.w)));
-            }
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&conv[s]);
-            if (++s == STAGES) { s = 0; ph ^= 1; }
-        }
-    } else {
-        drain_epilogue<BN>(p, tmem_base, warp, lane, nkb, m0, n0, acc_full, acc_empty);
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS));
-    }
-}
-
 // Split the operand B (K x N, ld) into two K-major planes, hi then lo, each
 // Np x Kp (row n holds column n of B), zero padded so boxes past K or N read
 // zeros, stored k-blocked: for k-block kb, rows [0, Np) of hi then [Np, 2 Np)
@@ -836,24 +663,13 @@ template <int BN, bool A_MN>
 int launch_tc(const CUtensorMap& tA, const CUtensorMap& tB, const TcParams& p, dim3 grid, cudaStream_t st) {
     static PerDevice<bool> attr_dev;  // cudaFuncSetAttribute is per device
     bool& attr_set = attr_dev.get();
-    static const bool legacy = getenv("RSVD_TC_LEGACY") != nullptr;  // A/B comparison: smem-A kernel for BN >= 96
-    if (BN <= 64 || !legacy) {
-        using Cfg = TmCfg<BN, A_MN>;
-        if (!attr_set) {
-            RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_tc_gemm_t<BN, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 Cfg::SMEM));
-            attr_set = true;
-        }
-        k_tc_gemm_t<BN, A_MN><<<grid, kTThreads, Cfg::SMEM, st>>>(tA, tB, p);
-    } else {
-        using Cfg = TcCfg<BN, A_MN>;
-        if (!attr_set) {
-            RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_tc_gemm<BN, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 Cfg::SMEM));
-            attr_set = true;
-        }
-        k_tc_gemm<BN, A_MN><<<grid, kThreads, Cfg::SMEM, st>>>(tA, tB, p);
+    using Cfg = TmCfg<BN, A_MN>;
+    if (!attr_set) {
+        RSVD_CHECK_CUDA(cudaFuncSetAttribute(k_tc_gemm_t<BN, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Cfg::SMEM));
+        attr_set = true;
     }
+    k_tc_gemm_t<BN, A_MN><<<grid, kTThreads, Cfg::SMEM, st>>>(tA, tB, p);
     RSVD_CHECK_LAUNCH();
     return RSVD_OK;
 }

@@ -309,8 +309,7 @@ int gemm_nn_skinny(int64_t m, int64_t n, int64_t k, double alpha, const float* A
                    cudaStream_t st) {
     RSVD_REQUIRE(n <= 64, "gemm_nn_skinny: n = %lld > 64", (long long)n);
     if (m == 0 || n == 0) return RSVD_OK;
-    static const bool v1 = getenv("RSVD_SKINNY_NN_V1") != nullptr;  // A/B switch
-    if (v1 || k > 64) {  // v2 measured faster at k = 50, slower at k = 100 (47.9 vs 41.4 us)
+    if (k > 64) {  // k_skinny_nn2 measured faster at k = 50, slower at k = 100 (47.9 vs 41.4 us)
         k_skinny_nn<<<(unsigned)cdiv(m, kNnRows), kNnThreads, 0, st>>>(m, (int)n, (int)k, alpha, A, lda, B, ldb,
                                                                       beta, C, ldc, row_sub, pred);
         RSVD_CHECK_LAUNCH();

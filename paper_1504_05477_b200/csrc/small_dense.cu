@@ -819,8 +819,8 @@ k_chol_blk(int p, const double* __restrict__ G, int64_t ldg, const double* __res
     CHOL_T(3);
 }
 
-// p <= 64: thread t holds column t of the Schur complement / R in registers
-// (fully unrolled steps, so every index is static). Per column j: thread j
+// p <= 64: thread t holds column t of the Schur complement / R in registers.
+// Per column j: thread j
 // takes the pivot decision (rsqrt), the scaled row j goes through shared
 // memory, and each thread updates its own column (2 barriers of 64 threads
 // per step; entries below a column's diagonal are never read, so the update
@@ -830,103 +830,16 @@ k_chol_blk(int p, const double* __restrict__ G, int64_t ldg, const double* __res
 // without block barriers, k_chol_warp, is slower: LDS latency is not hidden.)
 constexpr int kRegP = 64;
 
-__global__ void __launch_bounds__(kRegP)
-k_chol_reg64(int p, const double* __restrict__ G, int64_t ldg, const double* __restrict__ ref2, double tau2,
-             double* __restrict__ T, int64_t ldt, int32_t* __restrict__ mask, int32_t* __restrict__ ndef,
-             int32_t* __restrict__ running, const int32_t* __restrict__ active, const int32_t* __restrict__ pred) {
-    if (pred && *pred == 0) return;
-    __shared__ double Rs[kRegP][kRegP + 1];  // R (upper) after the factorization, R(i, c) = Rs[i][c]
-    __shared__ double s_row[kRegP];          // scaled row j of the current step
-    __shared__ double s_piv[2];              // inv (0 if deficient), rjj
-    __shared__ double s_rinv[kRegP];         // 1 / R(j, j) (1 for deficient columns)
-    __shared__ int s_msk[kRegP];
-    __shared__ int s_def, s_count;
-    const int t = threadIdx.x;
-    const bool mine = t < p;
-    double r[kRegP];  // r[i] = element (i, t), i <= t
-#pragma unroll
-    for (int i = 0; i < kRegP; ++i) r[i] = (mine && i <= t) ? G[(int64_t)i * ldg + t] : 0.0;
-    const double myref = mine ? (ref2 ? ref2[t] : G[(int64_t)t * ldg + t]) : 0.0;
-    const int myinact = mine ? (active && active[t] == 0) : 1;
-    s_msk[t] = myinact && mine ? 2 : 0;
-    if (t == 0) s_count = 0;
-    __syncthreads();
-    CHOL_T(0);
-#pragma unroll
-    for (int j = 0; j < kRegP; ++j) {
-        if (j < p) {  // uniform
-            if (t == j) {
-                const double d = r[j];
-                const bool def = myinact || !(d > tau2 * myref) || !(d > 0.0);
-                const double inv = def ? 0.0 : rsqrt(d);
-                s_piv[0] = inv;
-                s_piv[1] = def ? 1.0 : d * inv;
-                s_rinv[j] = def ? 1.0 : inv;
-                s_def = def;
-                if (def && !myinact) {
-                    s_msk[j] = 1;
-                    ++s_count;
-                }
-            }
-            __syncthreads();
-            const double inv = s_piv[0];
-            if (t == j) r[j] = s_piv[1];
-            else if (t > j) r[j] *= inv;
-            s_row[t] = r[j];  // R(j, t) for t > j
-            const bool def = s_def;
-            __syncthreads();
-            if (!def) {
-                const double rj = r[j];
-#pragma unroll
-                for (int i = j + 1; i < kRegP; ++i) r[i] = fma(-s_row[i], rj, r[i]);
-            }
-        }
-    }
-    CHOL_T(1);
-#pragma unroll
-    for (int i = 0; i < kRegP; ++i) Rs[i][t] = (mine && i <= t) ? r[i] : 0.0;
-    __syncthreads();
-    // column t of T: R x = e_t, swept from the bottom (x_i = 0 for i > t)
-    double x[kRegP];
-#pragma unroll
-    for (int i = 0; i < kRegP; ++i) x[i] = (i == t) ? 1.0 : 0.0;
-#pragma unroll
-    for (int i = kRegP - 1; i >= 0; --i) {
-        if (i < p) {
-            const double xi = x[i] * s_rinv[i];
-            x[i] = xi;
-#pragma unroll
-            for (int k = 0; k < i; ++k) x[k] = fma(-Rs[k][i], xi, x[k]);
-        }
-    }
-    CHOL_T(2);
-    if (mine) {
-        const bool zc = s_msk[t] != 0;
-#pragma unroll
-        for (int a = 0; a < kRegP; ++a)
-            if (a < p) T[(int64_t)a * ldt + t] = (a > t || zc || s_msk[a]) ? 0.0 : x[a];
-        mask[t] = s_msk[t] == 1 ? 1 : 0;
-    }
-    if (t == 0) {
-        const int32_t base = running ? running[0] : 0;
-        ndef[0] = s_count;
-        ndef[1] = base;
-        if (running) running[0] = base + s_count;
-    }
-    CHOL_T(3);
-}
-
 #ifndef RSVD_CHOL_UNROLL
 #define RSVD_CHOL_UNROLL 1
 #endif
 constexpr int kChUnroll = RSVD_CHOL_UNROLL;
-// Compact form of k_chol_reg64 (same arithmetic, same order, bitwise equal
-// results): the steps are a real loop and every register index is static
-// because the register window rotates by one each step (r[0] is always the
-// current pivot row's entry). The fully unrolled kernel is 64 KB of
-// straight-line code, fetched cold from HBM on every call inside a
-// factorization (the chain's 2 GB stream evicts it from L2): 83 us cold vs
-// 34 us warm at p = 50. This one is ~3 KB.
+// The steps are a real loop and every register index is static because the
+// register window rotates by one each step (r[0] is always the current pivot
+// row's entry). (A fully unrolled variant, bitwise equal, was 64 KB of
+// straight-line code fetched cold from HBM on every call inside a
+// factorization -- the chain's 2 GB stream evicts it from L2: 83 us cold vs
+// 34 us warm at p = 50 -- and was removed; this one is ~3 KB.)
 __global__ void __launch_bounds__(kRegP)
 k_chol_reg64c(int p, const double* __restrict__ G, int64_t ldg, const double* __restrict__ ref2, double tau2,
               double* __restrict__ T, int64_t ldt, int32_t* __restrict__ mask, int32_t* __restrict__ ndef,
@@ -1143,9 +1056,7 @@ int chol_deflate(int64_t p, const double* G, int64_t ldg, const double* ref2, do
     if (p == 0) return RSVD_OK;
     static const bool force_sweep = getenv("RSVD_CHOL_SWEEP") != nullptr;  // A/B experiments
     if (p <= kRegP && !force_sweep) {
-        if (getenv("RSVD_CHOL_REG_UNROLLED") != nullptr)  // A/B: the fully unrolled kernel
-            k_chol_reg64<<<1, kRegP, 0, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active, pred);
-        else if (getenv("RSVD_CHOL_REG_ONE") == nullptr)  // default: two threads per column
+        if (getenv("RSVD_CHOL_REG_ONE") == nullptr)  // default: two threads per column
             k_chol_reg64h<<<1, 2 * kRegP, 0, st>>>((int)p, G, ldg, ref2, tau2, T, ldt, mask, ndef, running, active,
                                                    pred);
         else
