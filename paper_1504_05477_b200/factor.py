@@ -66,8 +66,10 @@ def qr_orthonormalize(M, device=None):
         for j0 in range(0, m, pb):
             pw = min(pb, m - j0)
             cur = K[:, j0: j0 + pw]
-            ref2 = ws.ref2[:pw]
-            ops.colreduce(cur, True, ref2)
+            ref2 = None
+            if j0:  # norms before the projection against the prefix (the first block's come from its Gram)
+                ref2 = ws.ref2[:pw]
+                ops.colreduce(cur, True, ref2)
             krylov.orth_block(ops, comm, cur, tmp[:, :pw], ws, Qp=K[:, :j0] if j0 else None, ref2=ref2,
                               running=running, n_total=n, row_offset=0)
         return DenseMatrix(K.cpu().numpy())

@@ -39,6 +39,13 @@ JACOBI_MAX_SWEEPS = 50  # factor.py:35
 # norm (the reference's is 1e-12 on exact CGS2 residuals, factor.py:41,105;
 # a Gram-based test cannot resolve below ~sqrt(eps)).
 TAU = {torch.float64: 1e-7, torch.float32: 3e-3}
+# Blocks without a prefix (the Gram's diagonal is the reference): round 1
+# rejects a column whose Cholesky pivot is below PIVOT_NOISE x its squared norm
+# -- the pivot carries ~p eps of that norm in rounding, more for an
+# ill-conditioned leading block, so a smaller one is noise, not a residual, and
+# goes to round 2's explicit test (raw power blocks of rank-deficient inputs: a
+# dependent column accepted on a garbage pivot left Q orthonormal only to 5e-6).
+PIVOT_NOISE = {torch.float64: 1e-12, torch.float32: 0.0}
 REF_RTOL = 1e-12  # factor.py:41 (_DEFICIENCY_RTOL)
 # Second-round threshold per work precision: the reference's own 1e-12 in
 # FP64; in FP32 the explicit residuals are resolved only down to ~1e-7, and a
@@ -347,6 +354,9 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
         # original column norms^2 = diag(V^T V): taken from the Gram instead of a
         # separate pass over V (only round 2's 1e-12 test reads them)
         ws.ref_orig[:p].copy_(torch.diagonal(G))
+    # round-1 threshold: without separate reference norms the Gram's diagonal is
+    # the reference and the pivot-noise floor applies (see PIVOT_NOISE)
+    tau2_r1 = tau * tau if ref2 is not None else max(tau * tau, PIVOT_NOISE[dtype])
     # device-decided sections become CUDA-graph IF nodes under capture
     # (device.cond_section); they must not allocate, so their buffers are
     # made here. NCCL collectives stay out of conditional bodies (world 1 only).
@@ -354,7 +364,7 @@ def orth_block(ops, comm, V, tmp, ws, Qp=None, ref2=None, running=None, n_total=
     T32 = torch.empty((p, p), dtype=dtype, device=V.device) if dtype != torch.float64 else None
     if two_round and tau > 0.0:
         r1 = ws.ndef_r1  # round-1 [count, base]: round 2 runs on the device only if count > 0
-        ops.chol_deflate(G, ref2, tau * tau, T, mask, r1, None)
+        ops.chol_deflate(G, ref2, tau2_r1, T, mask, r1, None)
         Q1 = rows_buffer(tmp.shape[0], p, dtype, tmp.device)
         ops.gemm_nn(V, _cast_small(ops, T, dtype), Q1, emit=pl)  # Q1 (zero columns at rejected slots)
         ws.ndef.zero_()
@@ -643,6 +653,14 @@ def si_basis(ops, comm, op, Pi, q, every, ws, n_total, row_offset):
     running = torch.zeros(1, dtype=torch.int32, device=dev)
     op.apply(Pi, b)
     orthonormal = False
+    if dt == torch.float32:
+        # FP32 blocks cannot carry raw powers the way the reference's FP64 blocks
+        # do (a block's small directions sink below 2^-24 of its large ones after
+        # a step or two: sigma errors of 50 % measured on low-rank inputs with
+        # reorthonormalize_every = 0): orthonormalize after every step. The span
+        # is the same in exact arithmetic; the exact / fp64 modes keep the
+        # reference's schedule.
+        every = 1
     for t in range(1, q + 1):
         op.apply_t(b, C)
         comm.allreduce(C)
@@ -691,9 +709,13 @@ def rayleigh_ritz(ops, comm, op, Q, k, n_total, row_offset, sign_fn=None, W=None
     evals, Uk, info = ops.syev_topk(M, k)
     off = torch.zeros(1, dtype=torch.float64, device=dev)
     n = Q.shape[0]
+    ws = Workspace(dev, k)
+    again = ws.ndef2[:1]
     if Q.dtype == torch.float64:
-        Z = torch.empty((n, k), dtype=torch.float64, device=dev)
+        Z = rows_buffer(n, k, torch.float64, dev)
         ops.gemm_nn(Q, Uk, Z)
+        Z0 = rows_buffer(n, k, torch.float64, dev)
+        ws.ndef.zero_()
     else:
         Uk32 = torch.empty((w, k), dtype=Q.dtype, device=dev)
         ops.convert(Uk, Uk32)
@@ -708,7 +730,6 @@ def rayleigh_ritz(ops, comm, op, Q, k, n_total, row_offset, sign_fn=None, W=None
         # Gram says otherwise (or a column had to be refilled). The check Gram
         # also gives the orthogonality error reported with the result (the
         # sign canonicalization below only negates columns).
-        ws = Workspace(dev, k)
         Z = rows_buffer(n, k, torch.float64, dev)
         G = ws.G
         ops.gram(Z0, G)
@@ -716,29 +737,37 @@ def rayleigh_ritz(ops, comm, op, Q, k, n_total, row_offset, sign_fn=None, W=None
         ops.chol_deflate(G, None, 0.0, ws.T, ws.mask, ws.ndef)
         ops.gemm_nn(Z0, ws.T, Z)
         ops.insert_fill(Z, ws.mask, ws.ndef, QR_FILL_SEED, row_offset, n_total, pred=ws.ndef)
-        G2 = torch.empty((k, k), dtype=torch.float64, device=dev)
-        ops.gram(Z, G2)
-        comm.allreduce(G2)
-        zerr = ops.ortho_error(G2)
-        again = ws.ndef2[:1]
-        torch.gt(zerr, Z_REORTH_TOL, out=ws.flag_bool)
-        again.copy_(ws.flag_bool)
-        again.add_(ws.ndef[:1])
-        with ops.cond_section(again, GRAPH_COND and isinstance(comm, LocalComm)):
-            ops.chol_deflate(G2, None, 0.0, ws.T, ws.mask2, ws.ndef_r3, pred=again)
-            ops.gemm_nn(Z, ws.T, Z0, pred=again)
-            ops.convert(Z0, Z, pred=again)
-            ops.gram(Z, G2, pred=again)
-            comm.allreduce(G2)
-            ops.ortho_error(G2, zerr)  # unchanged G2 (gram skipped) gives the same zerr
+    # The check Gram gives the orthogonality error reported with the result;
+    # one more CholeskyQR step runs (device-decided) only if it says so. FP64:
+    # Z = Q U_k is orthonormal to ~1e-15 whenever Q is; a basis the
+    # orthonormalization could only bring to ~1e-6 (raw power blocks of a
+    # rank-deficient A, reorthonormalize_every = 0) is repaired here instead of
+    # failing PartialSvdResult's check.
+    G2 = torch.empty((k, k), dtype=torch.float64, device=dev)
+    ops.gram(Z, G2)
+    comm.allreduce(G2)
+    zerr = ops.ortho_error(G2)
+    torch.gt(zerr, Z_REORTH_TOL, out=ws.flag_bool)
+    again.copy_(ws.flag_bool)
+    again.add_(ws.ndef[:1])
+    G3 = torch.empty((k, k), dtype=torch.float64, device=dev)
+    z2 = torch.empty_like(zerr)
+    with ops.cond_section(again, GRAPH_COND and isinstance(comm, LocalComm)):
+        ops.chol_deflate(G2, None, 0.0, ws.T, ws.mask2, ws.ndef_r3, pred=again)
+        ops.gemm_nn(Z, ws.T, Z0, pred=again)
+        ops.convert(Z0, Z, pred=again)
+        # the re-check goes through its own buffer: when the section runs as
+        # predicated kernels (row-sharded A: collectives stay unconditional) and
+        # the predicate is off, the allreduce must not touch the reduced G2
+        G3.zero_()
+        ops.gram(Z, G3, pred=again)
+        comm.allreduce(G3)
+        ops.ortho_error(G3, z2)
+        torch.gt(again, 0, out=ws.flag_bool)
+        torch.where(ws.flag_bool, z2, zerr, out=zerr)
     if sign_fn is None:
         ops.canonicalize_signs(Z)
     else:
         sign_fn(Z)
     sigma = ops.sqrt_clip(evals)
-    if Q.dtype == torch.float64:
-        G = torch.empty((k, k), dtype=torch.float64, device=dev)
-        ops.gram(Z, G)
-        comm.allreduce(G)
-        zerr = ops.ortho_error(G)
     return RitzResult(Z, sigma, info, off, zerr)

@@ -111,3 +111,39 @@ def test_exact_host_inputs_pipelined_upload(rk, monkeypatch):
     # and the cached graph still works afterwards
     r = rk.factorize(A, cfg)
     assert np.array_equal(r.approx_singular_values, outs[0][0])
+
+
+@pytest.mark.parametrize("seed", [91, 104, 355, 385, 391])
+def test_raw_power_blocks_of_rank_deficient_input(rk, seed):
+    """simultaneous iteration without re-orthonormalization
+    (reorthonormalize_every = 0, test_rsvd.py:123-128) on inputs of rank below
+    k: the raw power block has exactly dependent columns whose Gram pivots are
+    rounding noise. The result is a valid factorization (these cases raised
+    'Z must have orthonormal columns' before the pivot-noise floor of round 1
+    and the conditional re-orthonormalization of Z) and the singular values
+    above the rank match the oracle."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(20, 60))
+    d = int(rng.integers(10, 40))
+    k = int(min(n, d, rng.integers(5, 30)))
+    r = int(rng.integers(1, max(2, min(n, d) // 2 + 1)))
+    A = rng.standard_normal((n, r)) @ rng.standard_normal((r, d))
+    q = int(rng.integers(1, 6))
+    res = rk.factorize(A, rk.RsvdConfig(k=k, variant="si", q=q, seed=seed, reorthonormalize_every=0))
+    z = res.Z.data
+    assert np.max(np.abs(z.T @ z - np.eye(k))) < 1e-10
+    ref = o.factorize(o.DenseOp(A), k, "si", q=q, seed=seed, every=0)
+    m = min(r, k)
+    assert np.max(np.abs(res.approx_singular_values[:m] - ref.sigma[:m]) / ref.sigma[0]) < 1e-7
+    assert np.all(res.approx_singular_values[m:] < 1e-6 * ref.sigma[0])
+
+
+def test_fp32_mode_si_without_reorthonormalization(rk):
+    """precision='fp32' with reorthonormalize_every = 0: FP32 blocks cannot carry
+    raw powers (50 % sigma errors measured), so the mode orthonormalizes after
+    every step; same span, singular values within the fp32 tolerance."""
+    rng = np.random.default_rng(12)
+    A = (rng.standard_normal((1196, 60)) @ rng.standard_normal((60, 501))).astype(np.float32)
+    ref = o.factorize(o.DenseOp(A.astype(np.float64)), 38, "si", q=3, seed=5, every=0)
+    res = rk.factorize(A, rk.RsvdConfig(k=38, variant="si", q=3, seed=5, reorthonormalize_every=0), precision="fp32")
+    assert np.max(np.abs(res.approx_singular_values - ref.sigma) / ref.sigma[0]) < 1e-4

@@ -76,7 +76,7 @@ def _sharded(rk, A, cfg, world, exact):
                 Z = gather_rows(df.Z, comm)
                 torch.cuda.current_stream().synchronize()
                 out[rank] = (Z.cpu().numpy(), df.sigma.cpu().numpy(),
-                             None if df.deflated is None else int(df.deflated.sum()))
+                             None if df.deflated is None else int(df.deflated.sum()), float(df.zerr.cpu()[0]))
         except Exception as exc:  # noqa: BLE001 - re-raised in the test thread
             errs.append(exc)
             g.barrier.abort()
@@ -96,7 +96,8 @@ def _single(rk, A, cfg, exact):
     from paper_1504_05477_b200.operators import DenseDeviceOp
 
     df = rsvd.run_device(DenseDeviceOp(A, exact=exact), cfg)
-    return df.Z.cpu().numpy(), df.sigma.cpu().numpy(), None if df.deflated is None else int(df.deflated.sum())
+    return (df.Z.cpu().numpy(), df.sigma.cpu().numpy(), None if df.deflated is None else int(df.deflated.sum()),
+            float(df.zerr.cpu()[0]))
 
 
 @pytest.fixture(scope="module")
@@ -117,14 +118,15 @@ def test_virtual_shards_deficient_basis(rk, world, exact):
     if exact:
         A = A.float()
     cfg = rk.RsvdConfig(k=12, variant="bk", q=8, seed=0)
-    Z1, s1, d1 = _single(rk, A, cfg, exact)
+    Z1, s1, d1, _ = _single(rk, A, cfg, exact)
     assert d1 and d1 > 0  # the case exercises insert_fill
     # exact mode: every shard slices its rows of Y with its own column exponents,
     # so the 48-bit digit rounding of A^T Y differs from the unsharded run's
     # (base-256 digits: 2.1e-10 measured on this deficient basis; FP64 mode 1e-10)
     tol = 5e-10 if exact else 1e-10
-    for Z, s, d in _sharded(rk, A, cfg, world, exact):
+    for Z, s, d, zerr in _sharded(rk, A, cfg, world, exact):
         assert d == d1
+        assert zerr < 1e-12  # the reported ||Z^T Z - I|| is the reduced one on every shard
         assert np.max(np.abs(s - s1) / s1) < tol
         assert np.max(np.abs(Z - Z1)) < 1e-7
 
@@ -136,6 +138,8 @@ def test_virtual_shards_si_fp32(rk, world):
     A = torch.from_numpy(((u * np.arange(1, 201) ** -0.5) @ np.linalg.qr(rng.standard_normal((200, 200)))[0]).astype(
         np.float32)).cuda()
     cfg = rk.RsvdConfig(k=10, variant="si", q=4, seed=1)
-    Z1, s1, _ = _single(rk, A, cfg, False)
-    for Z, s, _ in _sharded(rk, A, cfg, world, False):
+    Z1, s1, _, _ = _single(rk, A, cfg, False)
+    for Z, s, _, zerr in _sharded(rk, A, cfg, world, False):
         assert np.max(np.abs(s - s1) / s1) < 1e-5
+        assert zerr < 1e-12
+        assert np.max(np.abs(Z.T @ Z - np.eye(10))) < 1e-12

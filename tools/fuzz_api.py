@@ -1,0 +1,109 @@
+"""Randomized sweep of the public API against the oracle: random shapes
+(ragged, tiny, wide, tall), variants, q, p, dtypes (float64 -> fp64 mode,
+float32 -> exact and fp32 modes), dense and CSR, centred or not. Prints one
+line per failing case and a summary; exits 1 on any failure. GPU only.
+
+    python tools/fuzz_api.py [cases] [seed]
+"""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+import numpy as np
+
+import paper_1504_05477_b200 as rk
+import rsvd_oracle as o
+
+cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+fails = 0
+t0 = time.time()
+for it in range(cases):
+    n = int(rng.choice([rng.integers(2, 40), rng.integers(40, 400), rng.integers(400, 3000)]))
+    d = int(rng.choice([rng.integers(2, 40), rng.integers(40, 400), rng.integers(400, 1500)]))
+    k = int(rng.integers(1, max(2, min(n, d, 40) + 1)))
+    k = min(k, n, d)
+    p = k if rng.random() < 0.7 else int(rng.integers(k, min(n, d, k + 9) + 1))
+    variant = str(rng.choice(["bk", "si", "sketch"]))
+    q = int(rng.integers(0, 6))
+    every = int(rng.integers(0, 3))
+    sparse = rng.random() < 0.25
+    kind = str(rng.choice(["gauss", "lowrank", "decay", "scaled"]))
+    if kind == "gauss":
+        A = rng.standard_normal((n, d))
+    elif kind == "lowrank":
+        r = int(rng.integers(1, max(2, min(n, d) // 2 + 1)))
+        A = rng.standard_normal((n, r)) @ rng.standard_normal((r, d))
+    elif kind == "decay":
+        m = min(n, d)
+        U, _ = np.linalg.qr(rng.standard_normal((n, m)))
+        V, _ = np.linalg.qr(rng.standard_normal((d, m)))
+        A = (U * (0.8 ** np.arange(m))) @ V.T
+    else:
+        A = rng.standard_normal((n, d)) * np.exp(2 * rng.standard_normal((1, d)))
+    mode = str(rng.choice(["fp64", "exact", "fp32"]))
+    if sparse:
+        A = A * (rng.random((n, d)) < 0.15)
+        if not A.any():
+            A[0, 0] = 1.0
+        mode = str(rng.choice(["fp64", "fp32"]))
+    if mode != "fp64":
+        A = A.astype(np.float32)
+    A64 = A.astype(np.float64)
+    signs = rng.choice([-1.0, 1.0], size=A64.shape)  # drawn for every case: a replay keeps the stream
+    only = os.environ.get("FUZZ_ONLY")
+    if only is not None and it != int(only):
+        continue
+    desc = f"case {it}: {n}x{d} k={k} p={p} {variant} q={q} every={every} {kind} sparse={sparse} mode={mode}"
+    try:
+        if p > n and variant == "bk":
+            continue
+        ref = o.factorize(o.DenseOp(A64), k, variant, q=q, p=p, seed=it, every=every)
+        cfg = rk.RsvdConfig(k=k, variant=variant, q=q, p=p, seed=it, reorthonormalize_every=every)
+        if sparse:
+            nz = np.nonzero(A)
+            Ain = rk.SparseMatrixCSR.from_coo(n, d, nz[0], nz[1], A64[nz])
+        else:
+            Ain = A
+        r = rk.factorize(Ain, cfg, precision=mode)
+        s, sr = r.approx_singular_values, ref.sigma
+        scale = max(float(sr.max()), 1e-300)
+        tol = {"fp64": 1e-9, "exact": 1e-8, "fp32": 2e-4}[mode]
+        raw_powers = variant == "si" and every != 1 and q > 0
+        if raw_powers and mode == "fp32":
+            # the fp32 mode re-orthonormalizes every step (krylov.si_basis), the
+            # reference's raw FP64 powers lose the directions below 1e-16 of the
+            # block: no parity to expect, only a valid factorization
+            tol = np.inf
+        else:
+            # the reference's own result moves with 1-ulp changes of its input
+            # (raw powers without re-orthonormalization; sigma = sqrt(lambda) of
+            # the Gram M for values near 1e-8 sigma_1): allow 20x that sensitivity
+            pert = A64 * (1.0 + 2.0 ** -52 * signs)
+            ref2 = o.factorize(o.DenseOp(pert), k, variant, q=q, p=p, seed=it, every=every)
+            tol = max(tol, 20.0 * float(np.max(np.abs(ref2.sigma - sr))) / scale)
+        err = float(np.max(np.abs(s - sr))) / scale
+        z = r.Z.data
+        orth = float(np.max(np.abs(z.T @ z - np.eye(z.shape[1]))))
+        bad = []
+        if not (err <= tol):
+            bad.append(f"sigma err {err:.3e} > {tol}")
+        if not (orth <= 1e-9):
+            bad.append(f"orth {orth:.3e}")
+        if r.q_used != ref.q_used:
+            bad.append(f"q_used {r.q_used} != {ref.q_used}")
+        if only is not None:
+            np.set_printoptions(precision=6, linewidth=200)
+            print("ours", s)
+            print("ref ", sr)
+            print("ref replaced", ref.replaced, "orth", orth, "tol", tol)
+        if bad:
+            fails += 1
+            print("FAIL", desc, "; ".join(bad), flush=True)
+    except Exception as exc:  # noqa: BLE001
+        fails += 1
+        print("EXC ", desc, repr(exc)[:300], flush=True)
+print(f"{cases} cases, {fails} failures, {time.time() - t0:.1f} s")
+sys.exit(1 if fails else 0)
