@@ -18,16 +18,25 @@ import rsvd_oracle as o
 
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+# "large": blocks up to 200 columns and Krylov widths up to ~800 (the blocked
+# Cholesky, the grid tridiagonalisation, multi-tile products); default: k <= 40
+LARGE = len(sys.argv) > 3 and sys.argv[3] == "large"
 fails = 0
 t0 = time.time()
 for it in range(cases):
     n = int(rng.choice([rng.integers(2, 40), rng.integers(40, 400), rng.integers(400, 3000)]))
     d = int(rng.choice([rng.integers(2, 40), rng.integers(40, 400), rng.integers(400, 1500)]))
-    k = int(rng.integers(1, max(2, min(n, d, 40) + 1)))
+    if LARGE:
+        n = int(rng.integers(1000, 12000))
+        d = int(rng.integers(300, 2500))
+    k = int(rng.integers(1, max(2, min(n, d, 200 if LARGE else 40) + 1)))
     k = min(k, n, d)
     p = k if rng.random() < 0.7 else int(rng.integers(k, min(n, d, k + 9) + 1))
     variant = str(rng.choice(["bk", "si", "sketch"]))
     q = int(rng.integers(0, 6))
+    if LARGE and variant == "bk":
+        q = min(q, max(0, 800 // max(k, 1) - 1))
+    center = (not LARGE) and rng.random() < 0.2
     every = int(rng.integers(0, 3))
     sparse = rng.random() < 0.25
     kind = str(rng.choice(["gauss", "lowrank", "decay", "scaled"]))
@@ -44,6 +53,9 @@ for it in range(cases):
     else:
         A = rng.standard_normal((n, d)) * np.exp(2 * rng.standard_normal((1, d)))
     mode = str(rng.choice(["fp64", "exact", "fp32"]))
+    if center:
+        A = A + rng.uniform(-3, 3, size=(1, d))
+    sparse = sparse and not center
     if sparse:
         A = A * (rng.random((n, d)) < 0.15)
         if not A.any():
@@ -56,7 +68,9 @@ for it in range(cases):
     only = os.environ.get("FUZZ_ONLY")
     if only is not None and it != int(only):
         continue
-    desc = f"case {it}: {n}x{d} k={k} p={p} {variant} q={q} every={every} {kind} sparse={sparse} mode={mode}"
+    desc = f"case {it}: {n}x{d} k={k} p={p} {variant} q={q} every={every} {kind} sparse={sparse} center={center} mode={mode}"
+    if center:
+        A64 = A64 - A64.mean(axis=0, keepdims=True)  # the oracle factorizes the explicitly centred matrix
     try:
         if p > n and variant == "bk":
             continue
@@ -67,7 +81,7 @@ for it in range(cases):
             Ain = rk.SparseMatrixCSR.from_coo(n, d, nz[0], nz[1], A64[nz])
         else:
             Ain = A
-        r = rk.factorize(Ain, cfg, precision=mode)
+        r = rk.factorize(Ain, cfg, precision=mode, center=center)
         s, sr = r.approx_singular_values, ref.sigma
         scale = max(float(sr.max()), 1e-300)
         tol = {"fp64": 1e-9, "exact": 1e-8, "fp32": 2e-4}[mode]
