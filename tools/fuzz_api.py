@@ -21,6 +21,11 @@ rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
 # "large": blocks up to 200 columns and Krylov widths up to ~800 (the blocked
 # Cholesky, the grid tridiagonalisation, multi-tile products); default: k <= 40
 LARGE = len(sys.argv) > 3 and sys.argv[3] == "large"
+# "strict": only the classes where parity with the reference is well posed -- no
+# raw powers (SI with reorthonormalize_every != 1), no fp32 mode on spectra that
+# decay below 2^-24 within a step or on single-vector blocks -- and any failure
+# there is a bug (tests/test_gpu_fuzz.py runs this)
+STRICT = len(sys.argv) > 3 and sys.argv[3] == "strict"
 fails = 0
 t0 = time.time()
 for it in range(cases):
@@ -68,6 +73,8 @@ for it in range(cases):
     only = os.environ.get("FUZZ_ONLY")
     if only is not None and it != int(only):
         continue
+    if STRICT and ((variant == "si" and every != 1 and q > 0) or (mode == "fp32" and (kind == "decay" or p < 4))):
+        continue
     desc = f"case {it}: {n}x{d} k={k} p={p} {variant} q={q} every={every} {kind} sparse={sparse} center={center} mode={mode}"
     if center:
         A64 = A64 - A64.mean(axis=0, keepdims=True)  # the oracle factorizes the explicitly centred matrix
@@ -98,6 +105,10 @@ for it in range(cases):
             pert = A64 * (1.0 + 2.0 ** -52 * signs)
             ref2 = o.factorize(o.DenseOp(pert), k, variant, q=q, p=p, seed=it, every=every)
             tol = max(tol, 20.0 * float(np.max(np.abs(ref2.sigma - sr))) / scale)
+        if kind == "lowrank" or center:
+            # values at the Gram route's floor (sigma = sqrt(lambda), ~1e-8 sigma_1 for
+            # lambda ~ 0) and the implicit centring's cancellation against a large mean
+            tol = max(tol, 5e-8)
         err = float(np.max(np.abs(s - sr))) / scale
         z = r.Z.data
         orth = float(np.max(np.abs(z.T @ z - np.eye(z.shape[1]))))
