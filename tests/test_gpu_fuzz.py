@@ -28,3 +28,7 @@ def test_api_sweep_against_oracle(seed):
 
 def test_kernel_sweep_against_fp64_references():
     _run("fuzz_kernels.py", "250", "23")
+
+
+def test_virtual_shard_sweep_against_unsharded():
+    _run("fuzz_shards.py", "80", "24")
