@@ -168,3 +168,45 @@ def test_frobenius(rk):
     assert abs(rk.frobenius_norm_sq(a) - want) / want < 1e-10
     sp = _random_csr(rk, 12, 9, 33)
     assert abs(rk.frobenius_norm_sq(rk.MatrixOperator(sp)) - float(np.sum(sp.toarray() ** 2))) < 1e-12
+
+
+# ---- synthetic inputs (test_synth.py) ----------------------------------------
+
+
+def test_synthetic_spec_contract(rk):
+    spec = rk.SyntheticSpec(n=8, d=6, spectrum=np.array([2.0, 1.0]), seed=3)
+    again = rk.SyntheticSpec.from_dict(spec.to_dict())
+    assert (again.n, again.d, again.seed) == (spec.n, spec.d, spec.seed)
+    assert np.array_equal(again.spectrum, spec.spectrum)
+    for bad in (np.array([1.0, 2.0]), np.array([1.0, -0.5]), np.array([])):  # ascending, negative, empty
+        with pytest.raises(ValueError):
+            rk.SyntheticSpec(n=4, d=4, spectrum=bad)
+    with pytest.raises(ValueError):  # longer than min(n, d)
+        rk.SyntheticSpec(n=3, d=5, spectrum=np.array([3.0, 2.0, 1.0, 0.5]))
+
+
+@pytest.mark.gpu
+def test_synth_matrix_cases(rk):
+    a = rk.synth_matrix(rk.SyntheticSpec(n=3, d=3, spectrum=np.array([3.0, 2.0, 1.0]), seed=1))
+    assert np.max(np.abs(rk.dense_svd_reference(a).singular_values - [3.0, 2.0, 1.0])) < 1e-10 * 3.0
+    z = rk.synth_matrix(rk.SyntheticSpec(n=4, d=3, spectrum=np.zeros(3), seed=2))
+    assert np.all(z.data == 0.0)
+    spec = rk.SyntheticSpec(n=10, d=8, spectrum=np.linspace(2.0, 0.5, 6), seed=5)
+    assert np.array_equal(rk.synth_matrix(spec).data, rk.synth_matrix(spec).data)
+    assert np.array_equal(rk.synth_matrix(spec).data, o.synth_matrix(10, 8, np.linspace(2.0, 0.5, 6), seed=5))
+
+
+@pytest.mark.gpu
+def test_synth_adversarial_flat_top_spectral_floor(rk):
+    # six equal top values at sqrt(10), tail of ones: every rank-5 projector
+    # leaves spectral residual exactly sqrt(10) (exact oracle on the residual)
+    spectrum = np.concatenate([np.full(6, np.sqrt(10.0)), np.ones(100)])
+    a = rk.synth_matrix(rk.SyntheticSpec(n=106, d=106, spectrum=spectrum, seed=7))
+    oracle = rk.dense_svd_reference(a)
+    assert abs(oracle.singular_values[5] ** 2 - 10.0) < 1e-8
+    rng = rk.SeededRng(8)
+    for _ in range(5):
+        z = rk.qr_orthonormalize(rk.gaussian(106, 5, rng)).data
+        resid = a.data - z @ (z.T @ a.data)
+        top = rk.dense_svd_reference(resid).singular_values[0]
+        assert abs(top / oracle.singular_values[5] - 1.0) < 1e-6
