@@ -10,7 +10,7 @@ no CPU fallback.
 
 from . import metrics  # noqa: F401  (GPU parity metrics)
 from .experiment import ExperimentSpec, OracleSpectrum, oracle_spectrum, rows_to_csv, run_experiment  # f4
-from .io import load_dense_csv, load_matrix_market, write_matrix_market  # f3
+from .io import load_dense_csv, load_matrix_market, write_dense_csv, write_matrix_market  # f3
 from .metrics import (ErrorReport, compute_error_report, error_function, frob_error_ratio, per_vector_errors,
                       spectral_error_ratio)
 from .errors import ConvergenceError, ParseError
@@ -43,6 +43,7 @@ __all__ = [
     "load_dense_csv",
     "load_matrix_market",
     "write_matrix_market",
+    "write_dense_csv",
     "ErrorReport",
     "compute_error_report",
     "error_function",

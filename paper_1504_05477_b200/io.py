@@ -124,6 +124,10 @@ def write_matrix_market(A, path):
     """Matrix Market coordinate real general, 1-based, 17 significant digits
     (matrix.py:435-455): sparse input writes its stored nonzeros, dense input
     every nonzero entry in row-major order."""
+    from .matrix import MatrixOperator
+
+    if isinstance(A, MatrixOperator):
+        A = A.matrix
     if isinstance(A, SparseMatrixCSR):
         rows, cols = A.shape
         r = np.repeat(np.arange(rows), np.diff(A.row_ptr))
@@ -138,3 +142,17 @@ def write_matrix_market(A, path):
         fh.write(f"{rows} {cols} {len(v)}\n")
         for i, j, x in zip(r.tolist(), c.tolist(), v.tolist()):
             fh.write(f"{i + 1} {j + 1} {x:.17g}\n")
+
+
+def write_dense_csv(A, path):
+    """matrix.py:458-463: one row per line, 17 significant digits (a sparse
+    input is densified first)."""
+    from .matrix import MatrixOperator
+
+    if isinstance(A, MatrixOperator):
+        A = A.matrix
+    arr = A.toarray() if isinstance(A, SparseMatrixCSR) else as_dense_array(A)
+    with open(path, "w", encoding="utf-8") as fh:
+        for row in arr:
+            fh.write(",".join(f"{x:.17g}" for x in row))
+            fh.write("\n")

@@ -64,3 +64,14 @@ def test_write_read_round_trip(tmp_path):
         io.write_matrix_market(A, str(p))
         back = io.load_matrix_market(str(p))
         assert np.array_equal(back.toarray(), dense)  # 17 significant digits round-trip FP64 exactly
+
+
+def test_dense_csv_write_read_round_trip(tmp_path):
+    rng = np.random.default_rng(4)
+    dense = rng.standard_normal((6, 4))
+    p = tmp_path / "rt.csv"
+    io.write_dense_csv(dense, str(p))
+    assert np.array_equal(io.load_dense_csv(str(p)).data, dense)
+    sp = SparseMatrixCSR.from_coo(3, 3, [0, 2], [1, 2], [1.5, -2.0])
+    io.write_dense_csv(sp, str(p))
+    assert np.array_equal(io.load_dense_csv(str(p)).data, sp.toarray())
