@@ -9,13 +9,14 @@ no CPU fallback.
 """
 
 from . import metrics  # noqa: F401  (GPU parity metrics)
+from .backend import active_backend  # backend.py:31-36
 from .experiment import ExperimentSpec, OracleSpectrum, oracle_spectrum, rows_to_csv, run_experiment  # f4
 from .io import load_dense_csv, load_matrix_market, write_dense_csv, write_matrix_market  # f3
-from .metrics import (ErrorReport, compute_error_report, error_function, frob_error_ratio, per_vector_errors,
+from .metrics import (AdditiveSpectralCheck, ErrorReport, additive_spectral_check, compute_error_report, error_function, frob_error_ratio, per_vector_errors,
                       spectral_error_ratio)
 from .errors import ConvergenceError, ParseError
 from .factor import (EigResult, SvdResult, dense_svd_reference, qr_orthonormalize,  # factor.py's entry points
-                     symmetric_eig)
+                     spectral_norm_est, spectral_norm_max_restarts, symmetric_eig)
 from .matrix import (DenseMatrix, MatrixOperator, SeededRng, SparseMatrixCSR, as_dense_array, as_operator,
                      frobenius_norm_sq, gaussian, matmul, spmm)
 from .synth import SyntheticSpec, synth_matrix
@@ -35,6 +36,7 @@ from .rsvd import (
 __version__ = "0.1.0"
 
 __all__ = [
+    "active_backend",
     "ExperimentSpec",
     "OracleSpectrum",
     "oracle_spectrum",
@@ -46,6 +48,8 @@ __all__ = [
     "write_dense_csv",
     "ErrorReport",
     "compute_error_report",
+    "AdditiveSpectralCheck",
+    "additive_spectral_check",
     "error_function",
     "frob_error_ratio",
     "per_vector_errors",
@@ -56,6 +60,8 @@ __all__ = [
     "EigResult",
     "SvdResult",
     "dense_svd_reference",
+    "spectral_norm_est",
+    "spectral_norm_max_restarts",
     "qr_orthonormalize",
     "symmetric_eig",
     "ParseError",

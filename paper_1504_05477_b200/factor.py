@@ -162,3 +162,35 @@ def dense_svd_reference(A, dim_limit=ORACLE_DIM_LIMIT, device=None):
     else:
         u, v = np.zeros((n, 0)), np.zeros((d, 0))
     return SvdResult(DenseMatrix(u), sigma, DenseMatrix(v))
+
+
+def spectral_norm_est(op, tol=1e-9, max_iters=10000, rng=None, device=None):
+    """factor.py:217-253 -- power-iteration estimate of the largest singular
+    value (a lower bound: the largest Rayleigh estimate seen from a Gaussian
+    start, stopped when successive estimates agree to ``tol`` relative). ``op``:
+    a matrix or the operator handle; the products run on the GPU."""
+    from .matrix import SeededRng, as_operator
+    from .metrics import _Plain, spectral_norm_batched
+
+    if tol <= 0:
+        raise ValueError("tol must be positive")
+    if rng is None:
+        rng = SeededRng(0)
+    mop = as_operator(op)
+    start = rng.normal_fill(mop.shape[1]).reshape(-1, 1)
+    dop = mop.device_operator()
+    with torch.cuda.device(dop.device):
+        best, _ = spectral_norm_batched(_Plain(dop), tol=tol, max_iters=max_iters, starts=start)
+    return float(best[0])
+
+
+def spectral_norm_max_restarts(op, tol=1e-9, max_iters=10000, seeds=(101, 202, 303)):
+    """factor.py:256-261 -- max of spectral_norm_est over independent seeded
+    starts (batched as columns of one block: one pass over A per iteration)."""
+    from .matrix import as_operator
+    from .metrics import _Plain, spectral_norm_batched
+
+    dop = as_operator(op).device_operator()
+    with torch.cuda.device(dop.device):
+        best, _ = spectral_norm_batched(_Plain(dop), seeds=tuple(seeds), tol=tol, max_iters=max_iters)
+    return float(best.max())

@@ -103,13 +103,33 @@ def _colnorms(x):
     return out.sqrt()
 
 
-def spectral_norm_batched(defl, seeds=RESTART_SEEDS, tol=SPECTRAL_TOL, max_iters=SPECTRAL_MAX_ITERS):
+class _Plain:
+    """x -> A x and its transpose: the estimator's operator interface over a
+    device operator without deflation (spectral_norm_est on A itself)."""
+
+    def __init__(self, op):
+        self.op = op
+        self.n, self.d = op.local_rows, op.shape[1]
+        self.dtype, self.device = op.dtype, op.device
+
+    def apply(self, x):
+        y = rows_buffer(self.n, x.shape[1], self.dtype, self.device)
+        return self.op.apply(x, y)
+
+    def apply_t(self, x):
+        out = rows_buffer(self.d, x.shape[1], self.dtype, self.device)
+        return self.op.apply_t(x, out)
+
+
+def spectral_norm_batched(defl, seeds=RESTART_SEEDS, tol=SPECTRAL_TOL, max_iters=SPECTRAL_MAX_ITERS, starts=None):
     """The reference's spectral_norm_est for each seed, batched as columns.
-    Returns (best per seed, iterations per seed)."""
+    Returns (best per seed, iterations per seed). ``starts``: d x m start
+    vectors instead of SeededRng(seed).normal_fill(d) per seed."""
     if tol <= 0:
         raise ValueError("tol must be positive")
-    d, m = defl.d, len(seeds)
-    V = np.stack([SeededRng(s).normal_fill(d) for s in seeds], axis=1)
+    d = defl.d
+    V = np.stack([SeededRng(s).normal_fill(d) for s in seeds], axis=1) if starts is None else np.asarray(starts)
+    m = V.shape[1]
     v = rows_buffer(d, m, defl.dtype, defl.device)
     v.copy_(torch.from_numpy(V).to(defl.device, defl.dtype))
     nv = _colnorms(v).cpu().numpy()
@@ -267,6 +287,41 @@ def frob_error_ratio(A, Z, sigma, precision="auto"):
     if np.sqrt(tail) < EXACT_RANK_RTOL * np.sqrt(fro_sq):
         return 1.0
     return float(np.sqrt(num_sq / tail))
+
+
+@dataclass(frozen=True)
+class AdditiveSpectralCheck:
+    """metrics.py:160-168 -- outcome of the additive Frobenius-to-spectral
+    transfer property."""
+
+    passed: bool
+    eta: float
+    spectral_sq: float
+    bound: float
+    slack: float
+
+
+def additive_spectral_check(A, B, k, oracle):
+    """metrics.py:171-200: ||A - B||_2^2 <= sigma_{k+1}^2 + eta (+ 1e-8 sigma_1^2)
+    with eta the Frobenius excess of B over the best rank-k error; B must have
+    numerical rank at most k (1e-7 relative). Both spectral norms come from the
+    desk-scale oracle SVD (computed on the GPU, factor.dense_svd_reference)."""
+    from .factor import dense_svd_reference
+    from .matrix import DenseMatrix, as_dense_array, as_operator
+
+    op = as_operator(A)
+    b = as_dense_array(as_operator(B).densify())
+    sv_b = dense_svd_reference(DenseMatrix(b)).singular_values
+    if len(sv_b) > k and sv_b[0] > 0 and sv_b[k] >= 1e-7 * sv_b[0]:
+        raise ValueError(f"B has numerical rank above {k}")
+    diff = op.densify().data - b
+    sigma = _sv(oracle)
+    eta = float(np.sum(diff ** 2)) - _tail_sq(sigma, k)
+    diff_sv = dense_svd_reference(DenseMatrix(diff)).singular_values
+    spectral_sq = float(diff_sv[0] ** 2) if len(diff_sv) else 0.0
+    bound = _sig(sigma, k) ** 2 + eta + 1e-8 * _sig(sigma, 0) ** 2
+    return AdditiveSpectralCheck(passed=spectral_sq <= bound, eta=eta, spectral_sq=spectral_sq, bound=bound,
+                                 slack=bound - spectral_sq)
 
 
 @dataclass(frozen=True)

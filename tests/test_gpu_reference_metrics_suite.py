@@ -163,3 +163,49 @@ def test_error_report(rk, random_case):
     assert abs(r1.frob_ratio - r2.frob_ratio) < 1e-9
     assert abs(r1.spectral_ratio - r2.spectral_ratio) < 1e-9
     assert abs(r1.per_vector_max - r2.per_vector_max) < 1e-9
+
+
+# ---- spectral_norm_est (test_factor.py:145-172) -------------------------------
+
+
+def test_spectral_norm_est(rk):
+    est = rk.spectral_norm_est(rk.as_operator(np.diag([3.0, 2.0, 1.0])), tol=1e-10, rng=rk.SeededRng(3))
+    assert abs(est - 3.0) < 1e-8
+    assert rk.spectral_norm_est(rk.as_operator(np.zeros((3, 3))), tol=1e-9, rng=rk.SeededRng(4)) == 0.0
+    a = rk.gaussian(30, 20, rk.SeededRng(25))
+    sigma1 = rk.dense_svd_reference(a).singular_values[0]
+    assert abs(rk.spectral_norm_max_restarts(rk.as_operator(a), tol=1e-10) - sigma1) / sigma1 < 1e-6
+    for seed in range(5):
+        b = rk.gaussian(25, 15, rk.SeededRng(40 + seed))
+        s1 = rk.dense_svd_reference(b).singular_values[0]
+        assert rk.spectral_norm_max_restarts(rk.as_operator(b), tol=1e-9) <= s1 * (1 + 1e-8)
+    with pytest.raises(ValueError):
+        rk.spectral_norm_est(rk.as_operator(np.eye(2)), tol=0.0)
+    # the same estimate as the reference algorithm run on the host (oracle restatement)
+    import rsvd_oracle as o
+
+    A = rk.gaussian(40, 30, rk.SeededRng(26)).data
+    want = o.spectral_norm_est(lambda x: A @ x, lambda y: A.T @ y, 30, tol=1e-9, max_iters=10000, seed=101)
+    got = rk.spectral_norm_est(A, tol=1e-9, rng=rk.SeededRng(101))
+    assert abs(got - want) / want < 1e-12
+
+
+# ---- additive spectral transfer (test_metrics.py:161-194) ---------------------
+
+
+def test_additive_spectral_check(rk, random_case):
+    a, oracle = random_case
+    k = 4
+    b = oracle.U.data[:, :k] @ np.diag(oracle.singular_values[:k]) @ oracle.V.data[:, :k].T
+    res = rk.additive_spectral_check(a, b, k, oracle)
+    assert res.passed and abs(res.eta) < 1e-9
+    assert abs(res.spectral_sq - oracle.singular_values[k] ** 2) < 1e-9
+    dense = rk.as_operator(a).densify().data
+    r = rk.sketch_and_solve(a, rk.RsvdConfig(k=4, variant="sketch", seed=12))
+    assert rk.additive_spectral_check(a, r.Z.data @ (r.Z.data.T @ dense), 4, oracle).passed
+    rng = rk.SeededRng(77)
+    for _ in range(20):
+        y = _rand_basis(rk, 4, rng)
+        assert rk.additive_spectral_check(a, y @ (y.T @ dense), 4, oracle).passed
+    with pytest.raises(ValueError):
+        rk.additive_spectral_check(a, dense, 4, oracle)
