@@ -193,7 +193,8 @@ def test_synth_matrix_cases(rk):
     assert np.all(z.data == 0.0)
     spec = rk.SyntheticSpec(n=10, d=8, spectrum=np.linspace(2.0, 0.5, 6), seed=5)
     assert np.array_equal(rk.synth_matrix(spec).data, rk.synth_matrix(spec).data)
-    assert np.array_equal(rk.synth_matrix(spec).data, o.synth_matrix(10, 8, np.linspace(2.0, 0.5, 6), seed=5))
+    want = o.synth_matrix(10, 8, np.linspace(2.0, 0.5, 6), seed=5)  # the reference's fixed-order triple loop
+    assert np.max(np.abs(rk.synth_matrix(spec).data - want)) < 1e-14
 
 
 @pytest.mark.gpu
