@@ -602,6 +602,10 @@ def run_ours(args):
         roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                     "frac": achieved / hbm, "peak_source": peak_src, "traffic": traffic,
                     "algorithmic_bytes_per_launch": bytes_per, "avg_launch_ms": avg_chain_ms}
+        if traffic:
+            # the same launch time against the DRAM bytes ncu measured for this kernel
+            roofline["traffic_gbs"] = traffic / (avg_chain_ms * 1e-3) / 1e9
+            roofline["traffic_frac"] = roofline["traffic_gbs"] / hbm
         if mode == "exact":
             # what the kernel actually streams: the 5 digit planes of A (1.25x the
             # FP32 bytes) and the int8 MMA work (20 digit pairs, N padded to 64)
