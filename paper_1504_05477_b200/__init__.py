@@ -8,7 +8,14 @@ errors.py for the exception types). Compute runs in librsvd_b200.so
 no CPU fallback.
 """
 
-from . import metrics  # noqa: F401  (GPU parity metrics, SURVEY 8(f) f1)
+import warnings as _warnings
+
+# The reference's containers hand out read-only arrays (DenseMatrix.data,
+# SparseMatrixCSR.values ...); this package only ever uploads them, so torch's
+# one-time "array is not writable" warning on torch.from_numpy is noise here.
+_warnings.filterwarnings("ignore", message="The given NumPy array is not writable", category=UserWarning)
+
+from . import metrics  # noqa: F401,E402  (GPU parity metrics, SURVEY 8(f) f1)
 from .backend import active_backend  # backend.py:31-36
 from .experiment import ExperimentSpec, OracleSpectrum, oracle_spectrum, rows_to_csv, run_experiment  # f4
 from .io import load_dense_csv, load_matrix_market, write_dense_csv, write_matrix_market  # f3
