@@ -269,7 +269,7 @@ struct TmCfg {
     static constexpr int ACC_COLS = (MERGE ? 4 : 2) * BN;  // 2 sets x (D0 | D1) or 2 sets x D0
     static constexpr int T_COLS = 2 * KPS * BK;         // [A_hi | A_lo] per slot
     static constexpr int T_STAGES = (512 - ACC_COLS) / T_COLS;
-    static constexpr int B_STAGES = BN >= 128 ? 2 : (BN >= 64 ? 3 : 4);
+    static constexpr int B_STAGES = BN >= 112 ? 2 : (BN >= 64 ? 3 : 4);
     static constexpr int SMEM_BUDGET = (BN >= 96 ? 216 : 200) * 1024;  // 224 KB measured no faster
     static constexpr int A_STAGES_RAW = (SMEM_BUDGET - B_STAGES * B_SLOT) / A_BYTES;
     static constexpr int A_STAGES = A_STAGES_RAW > 12 ? 12 : A_STAGES_RAW;
@@ -652,11 +652,17 @@ int make_map_b(CUtensorMap* map, const void* base, int64_t Kp, int64_t Np, int b
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 int pick_bn(int64_t n) {
-    // widest tile first; the kernel is instantiated for these widths
+    // the kernel is instantiated for these widths (UMMA N: multiples of 16 at M = 128)
     if (n <= 32) return 32;
     if (n <= 64) return 64;
     if (n <= 96) return 96;
-    return 128;
+    // several N tiles: the width that pads the fewest MMA columns (n = 200: 2 x 112 = 224
+    // instead of 2 x 128 = 256, 12.5 % fewer tensor-pipe cycles), wider on ties
+    static const bool bn112 = !(getenv("RSVD_TC_BN112") && atoi(getenv("RSVD_TC_BN112")) == 0);
+    int best = 128;
+    int64_t best_cols = cdiv(n, 128) * 128;
+    if (bn112 && cdiv(n, 112) * 112 < best_cols && cdiv(n, 112) == cdiv(n, 128)) best = 112;
+    return best;
 }
 
 template <int BN, bool A_MN>
@@ -681,6 +687,7 @@ int dispatch_bn(int bn, const CUtensorMap& tA, const CUtensorMap& tB, const TcPa
         case 32: return launch_tc<32, A_MN>(tA, tB, p, grid, st);
         case 64: return launch_tc<64, A_MN>(tA, tB, p, grid, st);
         case 96: return launch_tc<96, A_MN>(tA, tB, p, grid, st);
+        case 112: return launch_tc<112, A_MN>(tA, tB, p, grid, st);
         default: return launch_tc<128, A_MN>(tA, tB, p, grid, st);
     }
 }
