@@ -41,3 +41,18 @@ def test_clock_sampler_without_gpu_returns():
         pass
     s = c.summary()
     assert s["reasons"] == ["unsampled"] or s["samples"] >= 1
+
+
+def test_gpus_flag_must_match_world_size():
+    """bench.py --gpus N under a launcher whose WORLD_SIZE differs refuses to
+    run (a scaling point must not silently measure another rank count)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "4"], env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "--gpus 4 but WORLD_SIZE=2" in r.stderr
